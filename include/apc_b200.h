@@ -1,0 +1,172 @@
+/*
+ * apc_b200.h -- C-ABI of the B200-native APLICUR hot path (libapc_b200.so).
+ *
+ * Plain C types only (pointers, sizes, int status codes); no torch or CUDA
+ * types cross this boundary.  Every entry point returns 0 (APC_OK) or an
+ * APC_* status; codes 1..9 are aplicur::ErrorKind + 1
+ * (/root/reference/proj/include/aplicur/error.hpp:10-20) so a C++ shim can
+ * rethrow aplicur::Error(kind, msg, index) unchanged.
+ *
+ * Each entry point cites the reference interface it replaces.  The reference
+ * is header-only C++ (no FFI of its own); the "binding" a maintainer adds is
+ * include/aplicur_b200.hpp (same namespace/types as the reference) or a ctypes
+ * stub -- see INTEGRATION.md.
+ */
+#ifndef APC_B200_H
+#define APC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define APC_ABI_VERSION 1
+
+enum apc_status {
+  APC_OK = 0,
+  APC_INVALID_ARGUMENT = 1,    /* ErrorKind::invalid_argument */
+  APC_DIMENSION_MISMATCH = 2,  /* ErrorKind::dimension_mismatch */
+  APC_RANK_DEFICIENT = 3,      /* ErrorKind::rank_deficient */
+  APC_SINGULAR = 4,            /* ErrorKind::singular */
+  APC_NOT_POSITIVE = 5,        /* ErrorKind::not_positive */
+  APC_NO_CONVERGENCE = 6,      /* ErrorKind::no_convergence */
+  APC_NUMERICAL_BREAKDOWN = 7, /* ErrorKind::numerical_breakdown */
+  APC_NOT_APPLICABLE = 8,      /* ErrorKind::not_applicable */
+  APC_IO = 9,                  /* ErrorKind::io */
+  APC_CUDA_ERROR = 20,         /* CUDA runtime failure */
+  APC_NCCL_ERROR = 21,         /* NCCL failure */
+  APC_NO_DEVICE = 22           /* no CUDA device: there is no CPU fallback */
+};
+
+typedef struct apc_ctx apc_ctx;         /* one per GPU / rank: stream, scratch, comm */
+typedef struct apc_mat apc_mat;         /* device-resident A (dense col-major or CSR+CSR^T) */
+typedef struct apc_result apc_result;   /* SolveResult (solver.hpp:101-112) */
+typedef struct apc_problem apc_problem; /* host-side synthetic problem (BASELINE configs) */
+
+/* ---- library / context --------------------------------------------------- */
+int apc_abi_version(void);
+/* last error message of the calling thread (for calls without a ctx) */
+const char* apc_last_error(int64_t* index);
+int apc_device_count(int* count);
+/* nccl_unique_id: 128 bytes from apc_nccl_unique_id() on rank 0 (NULL if nranks==1) */
+int apc_ctx_create(int device, int nranks, int rank, const void* nccl_unique_id, apc_ctx** out);
+int apc_ctx_destroy(apc_ctx* ctx);
+int apc_nccl_unique_id(void* out128);
+void* apc_ctx_stream(apc_ctx* ctx);              /* cudaStream_t all library work runs on */
+uint64_t apc_ctx_launches(apc_ctx* ctx);         /* kernels launched by this library so far */
+int apc_ctx_sync(apc_ctx* ctx);
+
+/* ---- matrices (replaces aplicur::Matrix storage, matrix.hpp:35-268) ------ */
+/* Host buffers are borrowed for the call only.  Rows [r0, r1) are kept on the
+ * device (block-row shard); pass r0 = 0, r1 = m for the whole matrix. */
+int apc_mat_upload_dense(apc_ctx* ctx, int64_t m, int64_t n, const double* colmajor,
+                         int64_t r0, int64_t r1, apc_mat** out);
+/* CSC with int64 indices, rows strictly increasing per column (the reference
+ * layout, matrix.hpp:66-94).  Device keeps CSR(A) and CSR(A^T) with int32 indices. */
+int apc_mat_upload_csc(apc_ctx* ctx, int64_t m, int64_t n, const int64_t* colptr,
+                       const int64_t* rowidx, const double* val, int64_t r0, int64_t r1,
+                       apc_mat** out);
+int apc_mat_free(apc_mat* a);
+int apc_mat_info(const apc_mat* a, int64_t* m, int64_t* n, int64_t* nnz, int* sparse,
+                 int64_t* r0, int64_t* r1);
+
+/* ---- operator products (Matrix::matvec / matvec_transpose, matrix.hpp:151-195;
+ *      AugmentedOperator::matvec / matvec_transpose, matrix.hpp:377-392) ------
+ * augmented == 0: y = A x (len m) / y = A^T x (len n).
+ * augmented != 0: y = [A x; mu x] (len m+n) / y = A^T x[0:m] + mu x[m:m+n] (len n).
+ * *_dev take device pointers and run on the ctx stream (asynchronous);
+ * *_host copy host buffers in and out (synchronous).  Sharded matrices use
+ * local row blocks (the transpose product is then a partial sum). */
+int apc_op_apply_dev(apc_mat* a, double mu, int augmented, int transpose, const double* x_dev,
+                     double* y_dev);
+int apc_op_apply_host(apc_mat* a, double mu, int augmented, int transpose, const double* x,
+                      double* y);
+
+/* ---- row partitioning for multi-GPU -------------------- */
+/* bounds[0..nranks]: contiguous row blocks balanced by nnz when row_nnz is
+ * given (prefix-sum split), else by row count. Host-only. */
+int apc_partition_rows(int64_t m, const int64_t* row_nnz, int nranks, int64_t* bounds);
+
+/* ---- seeded randomness (rng.hpp:12-78), host-side, bit-identical -------- */
+/* kind: 0 next_u64 (uint64 out), 1 uniform, 2 gaussian, 3 below(bound) (uint64 out), 4 sign.
+ * stream < 0: Rng(seed); else Rng(seed, RngStream(stream), index). */
+int apc_rng_fill(uint64_t seed, int stream, uint64_t index, int kind, uint64_t bound,
+                 int64_t count, void* out);
+uint64_t apc_mix64(uint64_t x);
+
+/* ---- synthetic BASELINE inputs (host) ---------------------------------- */
+/* config 1..5 = BASELINE.json configs[0..4]; m, n = 0 -> the BASELINE shape;
+ * seed = 0 -> 20260415 + config.  Dense problems are column-major; sparse ones
+ * are CSC with int64 indices (the reference Matrix layout). */
+int apc_problem_generate(int config, int64_t m, int64_t n, uint64_t seed, apc_problem** out);
+int apc_problem_info(const apc_problem* p, int64_t* m, int64_t* n, int* sparse, int64_t* nnz);
+const double* apc_problem_dense(const apc_problem* p);
+int apc_problem_csc(const apc_problem* p, const int64_t** colptr, const int64_t** rowidx,
+                    const double** vals);
+const double* apc_problem_b(const apc_problem* p);
+int apc_problem_free(apc_problem* p);
+
+/* ---- solver (aplicur_solve / plain_lsqr_solve, solver.hpp:162-448) ------ */
+/* Mirrors SolverConfig (solver.hpp:29-45) field for field, plus sketch_kind. */
+typedef struct apc_solver_config {
+  int64_t block;               /* 0: max(1, llround(n / 50)) */
+  double eps_cur;              /* < 0: 30 * mu */
+  double eps_lsqr;             /* 1e-10 */
+  double nu_prec;              /* 10 */
+  double nu_lsqr;              /* 100 */
+  double mu;                   /* scale of the [A; mu I] block */
+  int32_t variant;             /* 0 svd, 1 svd_free */
+  int32_t core;                /* 0 qr, 1 lu (CoreFactorKind) */
+  int64_t sketch_xi;           /* 8 */
+  int64_t probe_count;         /* 10 */
+  int64_t lsqr_cap;            /* 0: 4 n per phase */
+  int64_t max_rank;            /* 0: min of target dimensions */
+  uint64_t seed;               /* 0 */
+  int64_t trace_sample_stride; /* accepted; the device loop records no true_relres samples */
+  int64_t outer_cap;           /* 100000 */
+  int32_t sketch_kind;         /* 0 sparse sign (reference), 1 Gaussian (BASELINE C1/C3/C4) */
+  int32_t reserved;
+} apc_solver_config;
+
+typedef struct apc_phase_report { /* PhaseReport, solver.hpp:74-88 */
+  int32_t phase;
+  int32_t reason;  /* StopReason: 0 none 1 gradient-tol 2 dynamic-rate 3 dynamic-diff 4 iteration-cap 5 exact-zero-rhs */
+  int64_t rank;
+  double rho, sigma_hat, mu;
+  int64_t lsqr_iters;
+  double t_augment_ms, t_factor_ms, t_precond_ms, t_lsqr_ms;
+  double relres_at_end;
+} apc_phase_report;
+
+typedef struct apc_trace_row { /* LsqrTraceRow, lsqr.hpp:38-47 */
+  int32_t phase;
+  int32_t pad;
+  int64_t iter;
+  double phibar, cvgrate, cvgdiff;
+  uint64_t matvecs;
+  double wall_ms, true_relres;
+} apc_trace_row;
+
+int apc_config_default(apc_solver_config* cfg);
+/* b: full right-hand side (length m, host).  plain != 0 runs plain_lsqr_solve. */
+int apc_solve(apc_mat* a, const double* b, const apc_solver_config* cfg, int plain,
+              apc_result** out);
+int apc_result_free(apc_result* r);
+/* status: SolveStatus 0 converged, 1 rank-exhausted, 2 breakdown */
+int apc_result_summary(const apc_result* r, int* status, double* final_rho, double* final_relres,
+                       uint64_t* sketch_applications, uint64_t* system_matvecs, int64_t* n_phases,
+                       int64_t* n_trace, int64_t* rank, int64_t* n_rho);
+int apc_result_x(const apc_result* r, double* x);
+int apc_result_indices(const apc_result* r, int64_t* row_indices, int64_t* col_indices);
+int apc_result_rho_history(const apc_result* r, double* rho);
+int apc_result_phases(const apc_result* r, apc_phase_report* phases);
+int apc_result_trace(const apc_result* r, apc_trace_row* rows);
+/* wall-clock split of the last solve: setup (sketch + CUR + builds) and LSQR, ms */
+int apc_result_timing(const apc_result* r, double* total_ms, double* lsqr_ms, double* setup_ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* APC_B200_H */

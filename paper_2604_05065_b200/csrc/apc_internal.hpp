@@ -1,0 +1,122 @@
+// Internal declarations shared by the host runtime (.cpp) and the sm_100a
+// kernels (.cu) of libapc_b200.  Not part of the public C-ABI (include/apc_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "apc_b200.h"
+
+namespace apc {
+
+using i64 = std::int64_t;
+using i32 = std::int32_t;
+
+// Error carrying an APC_* status (1..9 mirror aplicur::ErrorKind + 1,
+// /root/reference/proj/include/aplicur/error.hpp:10-20) and an index payload.
+struct Status : std::runtime_error {
+  int code;
+  i64 index;
+  Status(int c, const std::string& what, i64 idx = -1)
+      : std::runtime_error(what), code(c), index(idx) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& what, i64 idx = -1) {
+  throw Status(code, what, idx);
+}
+inline void require(bool cond, int code, const std::string& what, i64 idx = -1) {
+  if (!cond) fail(code, what, idx);
+}
+
+void cuda_check(cudaError_t e, const char* what);
+#define APC_CUDA(call) ::apc::cuda_check((call), #call)
+
+// ---------------------------------------------------------------------------
+// Device buffers
+// ---------------------------------------------------------------------------
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  i64 n = 0;
+  DBuf() = default;
+  explicit DBuf(i64 count) { alloc(count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(i64 count) {
+    release();
+    n = count;
+    if (count > 0) APC_CUDA(cudaMalloc(&p, sizeof(T) * static_cast<size_t>(count)));
+  }
+  // grow-only reallocation (contents discarded)
+  void ensure(i64 count) { if (count > n) alloc(count); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return sizeof(T) * static_cast<size_t>(n); }
+};
+
+// ---------------------------------------------------------------------------
+// Compressed sparse rows (int32 indices; values fp64)
+// ---------------------------------------------------------------------------
+struct Csr {
+  i64 rows = 0, cols = 0, nnz = 0;
+  DBuf<i32> ptr;  // rows+1
+  DBuf<i32> idx;  // nnz
+  DBuf<double> val;
+  // nnz-balanced work units for rows longer than a warp can take in one unit:
+  // unit u covers [ustart[u], uend[u]) of row urow[u]; rows split in several
+  // units write partial sums to upart[slot] which a fix-up pass adds in order.
+  i64 n_units = 0, n_parts = 0, max_row_nnz = 0;
+  DBuf<i32> urow, ustart, uend, uslot;  // per unit (uslot < 0: whole row)
+  DBuf<i32> rfirst, rcount;             // per row: first partial slot (-1: not split), count
+  DBuf<double> upart;                   // n_parts partial sums
+  double avg_row_nnz = 0.0;
+};
+
+}  // namespace apc
+
+// ---------------------------------------------------------------------------
+// Context (one per GPU / rank)
+// ---------------------------------------------------------------------------
+struct apc_ctx {
+  int device = 0;
+  int nranks = 1, rank = 0;
+  cudaStream_t stream = nullptr;
+  void* nccl = nullptr;  // ncclComm_t when nranks > 1
+  std::string err;
+  apc::i64 err_index = -1;
+  int num_sms = 148;
+  // scratch reused across calls
+  apc::DBuf<double> scratch_d;
+  apc::DBuf<unsigned int> counters;  // last-block counters (zeroed)
+  // kernel launch counter (launches issued by this library on this ctx)
+  std::uint64_t launches = 0;
+};
+
+// Matrix handle: dense column-major (ld = local rows) or sparse stored twice
+// as CSR(A) (for A*x) and CSR(A^T) (for A^T*x; the same arrays as the
+// reference's CSC, matrix.hpp:31-34).  Row sharding keeps rows [r0, r1).
+struct apc_mat {
+  apc_ctx* ctx = nullptr;
+  apc::i64 m = 0, n = 0;    // global shape
+  apc::i64 r0 = 0, r1 = 0;  // local row shard [r0, r1)
+  bool sparse = false;
+  apc::DBuf<double> dense;  // local rows, column-major, ld = r1 - r0
+  apc::Csr a;               // CSR of the local rows (mloc x n)
+  apc::Csr at;              // CSR of their transpose (n x mloc)
+  apc::i64 nnz_global = 0;
+  apc::i64 mloc() const { return r1 - r0; }
+};

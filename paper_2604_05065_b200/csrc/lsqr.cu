@@ -1,0 +1,670 @@
+// Device-resident LSQR phase: Golub-Kahan bidiagonalisation with the vector
+// updates and norms fused into the operator kernels, scalars and stop rules on
+// the GPU, and the whole iteration captured as a CUDA graph whose conditional
+// WHILE node re-runs the body until the device stop flag is raised.
+//
+// Reference: lsqr_solve (/root/reference/proj/include/aplicur/lsqr.hpp:84-207),
+// dynamic_stop_check (lsqr.hpp:65-72), right_preconditioned
+// (operators.hpp:75-90), preconditioner applies (preconditioner.hpp:62-124,
+// 279-339).
+//
+// Per iteration (plain / preconditioned):
+//   [P^{-1} v -> z : project, core, expand]            (preconditioned only)
+//   fwd   : u <- A z - alpha*u  (+ ||u_top||^2, fused in the SpMV/GEMV)
+//   tail  : u_tail <- mu z - alpha*u_tail (+ ||u_tail||^2)       (mu > 0)
+//   adj   : g <- A^T u (raw, local rows)         [+ NCCL allreduce(n+1)]
+//   epi   : beta; g/beta; plain: v <- g - beta v, ||v||^2, alpha, rotation
+//   [P^{-T} g : project, core, expand + v update + alpha, rotation]
+//   upd   : v/alpha; y += t1 w; w = v + t2 w; ||y||; stop tests
+// u and v are kept unnormalised between kernels and normalised on the fly
+// (u/beta, v/alpha rounds exactly like the reference's in-place division).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "dev_common.cuh"
+#include "lsqr.hpp"
+#include "ops.cuh"
+
+namespace apc {
+
+constexpr int kVecThreads = 256;
+
+struct LsqrPtrs {
+  LsqrState* st;
+  TraceRow* trace;
+  double* u;  // mloc (+ n tail)
+  double* v;  // n
+  double* w;
+  double* y;
+  double* z;  // P^{-1} v (or v itself when unpreconditioned)
+  double* g;  // n + 1 (A^T u raw | ||u_top||^2)
+  double* h;  // n (g / beta, input of P^{-T})
+  double* fwd_part;
+  double* tail_part;
+  double* epi_part;
+  double* upd_part;
+  unsigned* ctr;  // [0] fwd, [1] tail, [2] epi, [3] upd
+  long long mloc, n;
+  double mu;
+  int has_tail;
+  // transpose-unit fix-up (sparse A)
+  const double* upart;
+  const int* rfirst;
+  const int* rcount;
+};
+
+// ---------------------------------------------------------------------------
+// scalar recurrences (single thread of the last block)
+// ---------------------------------------------------------------------------
+__device__ void finalize_alpha(LsqrState* st, TraceRow* trace, double alpha, double beta) {
+  const double wall = (globaltimer_ns() - st->t0_ns) * 1e-6;
+  if (st->iter < 0) {  // phase initialisation (lsqr.hpp:113-135)
+    st->iter = 0;
+    st->beta = beta;
+    st->phibar = beta;
+    st->phibar0 = beta;
+    st->alpha = alpha;
+    st->rhobar = alpha;
+    st->opnorm2 = alpha * alpha;
+    st->t1 = 0.0;
+    st->t2 = 0.0;
+    trace[0] = TraceRow{beta, 0.0, 0.0, wall, 0, 0ull};
+    if (alpha == 0.0) {
+      st->done = 1;
+      st->reason = kReasonGradientTol;
+    }
+    return;
+  }
+  // continue the bidiagonalisation (lsqr.hpp:139-164)
+  st->alpha = alpha;
+  st->beta = beta;
+  st->opnorm2 += alpha * alpha + beta * beta;
+  const double rho = hypot(st->rhobar, beta);
+  const double c = st->rhobar / rho;
+  const double s = beta / rho;
+  const double theta = s * alpha;
+  st->rhobar = -c * alpha;
+  const double phi = c * st->phibar;
+  const double phibar_prev = st->phibar;
+  const double phibar = s * st->phibar;
+  st->phibar = phibar;
+  st->t1 = phi / rho;
+  st->t2 = -theta / rho;
+  st->cabs = fabs(c);
+  const long long j = st->iter + 1;
+  st->iter = j;
+  if (!isfinite(phibar) || !isfinite(alpha) || !isfinite(beta)) {  // lsqr.hpp:173-174
+    st->breakdown = 1;
+    st->done = 1;
+  }
+  const double cvgrate = (phibar > 0.0 && phibar_prev > 0.0) ? log(phibar_prev / phibar)
+                                                             : CUDART_INF;
+  const double cvgdiff = phibar_prev - phibar;
+  if (j == 1) st->cvgrate1 = cvgrate;
+  st->t_cvgrate = cvgrate;
+  st->t_cvgdiff = cvgdiff;
+  if (j < st->trace_cap)
+    trace[j] = TraceRow{phibar, cvgrate, cvgdiff, wall, j, 1ull + 2ull * static_cast<unsigned long long>(j)};
+}
+
+// stop tests after the y/w update (lsqr.hpp:183-203)
+__device__ void stop_tests(LsqrState* st, double ynorm) {
+  const long long j = st->iter;
+  if (j <= 0 || st->done) return;
+  st->ynorm = ynorm;
+  const double phibar = st->phibar;
+  const double grad = phibar * st->alpha * st->cabs;
+  const double sq = sqrt(st->opnorm2);
+  const bool grad_small = grad <= st->eps * sq * phibar;
+  const bool res_small = phibar <= st->eps * (sq * ynorm + st->phibar0);
+  if (grad_small || res_small || phibar == 0.0) {
+    st->done = 1;
+    st->reason = kReasonGradientTol;
+    return;
+  }
+  if (j >= 2 && st->nu > 0.0 && !isinf(st->nu)) {  // dynamic_stop_check (lsqr.hpp:65-72)
+    const double rate = st->t_cvgrate, diff = st->t_cvgdiff;
+    int dyn = kReasonNone;
+    if (st->sigma_floor > 0.0 && diff < st->sigma_floor) dyn = kReasonDynamicDiff;
+    else if (rate <= 0.0) dyn = kReasonDynamicRate;
+    else if (st->cvgrate1 / rate > st->nu) dyn = kReasonDynamicRate;
+    if (dyn != kReasonNone) {
+      st->done = 1;
+      st->reason = dyn;
+      return;
+    }
+  }
+  if (j >= st->cap) {
+    st->done = 1;
+    st->reason = kReasonIterationCap;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+struct LsqrFwdEpi {  // u <- (A z) - alpha * u/beta ; ||u_top||^2 -> g[n]
+  double* u;
+  const LsqrState* st;
+  double* part;
+  unsigned* ctr;
+  double* out_norm2;
+  double alpha, beta;
+  __device__ void begin() {
+    alpha = st->alpha;
+    beta = st->beta;
+  }
+  __device__ double row(long long r, double av) {
+    const double uo = u[r];
+    const double uh = beta > 0.0 ? uo / beta : uo;
+    const double t = av - alpha * uh;
+    u[r] = t;
+    return t * t;
+  }
+  __device__ void tile_done(unsigned tile, unsigned ntiles, double sq) {
+    __shared__ double sh[32];
+    if (threadIdx.x == 0) part[tile] = sq;
+    if (elect_last_block(ctr, ntiles)) {
+      double s = ordered_sum<256>(part, ntiles, sh);
+      if (threadIdx.x == 0) *out_norm2 = s;
+    }
+  }
+};
+
+// init: u <- rhs; ||rhs_top||^2 -> g[n] ; ||rhs_tail||^2 -> st->tail_norm2
+__global__ void __launch_bounds__(kVecThreads)
+lsqr_init_copy_kernel(LsqrPtrs P, const double* rhs, long long len, long long off, int tail) {
+  __shared__ double sh[32];
+  long long i = static_cast<long long>(blockIdx.x) * kVecThreads + threadIdx.x;
+  double sq = 0.0;
+  if (i < len) {
+    double t = rhs[off + i];
+    P.u[off + i] = t;
+    sq = t * t;
+  }
+  sq = block_sum<kVecThreads>(sq, sh);
+  double* part = tail ? P.tail_part : P.fwd_part;
+  if (threadIdx.x == 0) part[blockIdx.x] = sq;
+  if (elect_last_block(P.ctr + (tail ? 1 : 0), gridDim.x)) {
+    double s = ordered_sum<kVecThreads>(part, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      if (tail) P.st->tail_norm2 = s;
+      else P.g[P.n] = s;
+    }
+  }
+}
+
+// mu-tail rows of the augmented system: u_t <- mu z - alpha u_t/beta
+__global__ void __launch_bounds__(kVecThreads) lsqr_tail_kernel(LsqrPtrs P) {
+  __shared__ double sh[32];
+  if (P.st->done) return;
+  const double alpha = P.st->alpha, beta = P.st->beta;
+  long long j = static_cast<long long>(blockIdx.x) * kVecThreads + threadIdx.x;
+  double sq = 0.0;
+  if (j < P.n) {
+    double* ut = P.u + P.mloc;
+    const double uo = ut[j];
+    const double uh = beta > 0.0 ? uo / beta : uo;
+    const double t = P.mu * P.z[j] - alpha * uh;
+    ut[j] = t;
+    sq = t * t;
+  }
+  sq = block_sum<kVecThreads>(sq, sh);
+  if (threadIdx.x == 0) P.tail_part[blockIdx.x] = sq;
+  if (elect_last_block(P.ctr + 1, gridDim.x)) {
+    double s = ordered_sum<kVecThreads>(P.tail_part, gridDim.x, sh);
+    if (threadIdx.x == 0) P.st->tail_norm2 = s;
+  }
+}
+
+// beta from the (allreduced) ||u_top||^2 and the tail; g = A_mu^T u / beta.
+// precond == 0: v <- g - beta v, ||v||^2 -> alpha -> rotation (last block).
+// precond != 0: h <- g (input of P^{-T}).
+__global__ void __launch_bounds__(kVecThreads) lsqr_epi_kernel(LsqrPtrs P, int precond) {
+  __shared__ double sh[32];
+  LsqrState* st = P.st;
+  if (st->done) return;
+  const double beta = sqrt(P.g[P.n] + st->tail_norm2);
+  if (st->iter < 0 && beta == 0.0) {  // exact_zero_rhs (lsqr.hpp:113-118)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      P.trace[0] = TraceRow{0.0, 0.0, 0.0, (globaltimer_ns() - st->t0_ns) * 1e-6, 0, 0ull};
+      st->phibar = 0.0;
+      st->phibar0 = 0.0;
+      st->done = 1;
+      st->reason = kReasonExactZeroRhs;
+    }
+    return;
+  }
+  long long j = static_cast<long long>(blockIdx.x) * kVecThreads + threadIdx.x;
+  double sq = 0.0;
+  if (j < P.n) {
+    double raw = P.upart ? unit_row_value(P.g, P.upart, P.rfirst, P.rcount, j) : P.g[j];
+    if (P.has_tail) raw += P.mu * P.u[P.mloc + j];
+    const double gj = beta > 0.0 ? raw / beta : raw;
+    if (precond) {
+      P.h[j] = gj;
+    } else {
+      const double t = gj - beta * P.v[j];
+      P.v[j] = t;
+      sq = t * t;
+    }
+  }
+  if (precond) return;
+  sq = block_sum<kVecThreads>(sq, sh);
+  if (threadIdx.x == 0) P.epi_part[blockIdx.x] = sq;
+  if (elect_last_block(P.ctr + 2, gridDim.x)) {
+    double s = ordered_sum<kVecThreads>(P.epi_part, gridDim.x, sh);
+    if (threadIdx.x == 0) finalize_alpha(st, P.trace, sqrt(s), beta);
+  }
+}
+
+// v <- v/alpha ; y += t1 w ; w = v + t2 w ; ||y|| ; stop tests (lsqr.hpp:145-203)
+__global__ void __launch_bounds__(kVecThreads)
+lsqr_update_kernel(LsqrPtrs P, cudaGraphConditionalHandle cond, int use_cond) {
+  __shared__ double sh[32];
+  LsqrState* st = P.st;
+  if (st->done) {
+    if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const double alpha = st->alpha, t1 = st->t1, t2 = st->t2;
+  long long j = static_cast<long long>(blockIdx.x) * kVecThreads + threadIdx.x;
+  double sq = 0.0;
+  if (j < P.n) {
+    const double vo = P.v[j];
+    const double vh = alpha > 0.0 ? vo / alpha : vo;
+    P.v[j] = vh;
+    const double wo = P.w[j];
+    const double yn = P.y[j] + t1 * wo;
+    P.y[j] = yn;
+    P.w[j] = vh + t2 * wo;
+    sq = yn * yn;
+  }
+  sq = block_sum<kVecThreads>(sq, sh);
+  if (threadIdx.x == 0) P.upd_part[blockIdx.x] = sq;
+  if (elect_last_block(P.ctr + 3, gridDim.x)) {
+    double s = ordered_sum<kVecThreads>(P.upd_part, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      stop_tests(st, sqrt(s));
+      if (use_cond) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// preconditioner kernels:  out = x + B (K (B^T x))  or  x + R^T (G (R x))
+// ---------------------------------------------------------------------------
+// s = K t  (K l x l column-major); t may be split partials summed in order
+__global__ void pc_core_kernel(const double* __restrict__ K, long long l,
+                               const double* __restrict__ t, double* __restrict__ s,
+                               const int* done) {
+  if (done && *done) return;
+  long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= l) return;
+  double acc = 0.0;
+  for (long long k = 0; k < l; ++k) acc += K[k * l + i] * t[k];
+  s[i] = acc;
+}
+
+// expand: o_j = x_j + (B s)_j (explicit) or x_j + (R^T s)_j (implicit), then
+// mode 0: out[j] = o_j ; mode 1: v_j = o_j - beta v_j, ||v||^2 -> alpha (last block)
+__global__ void __launch_bounds__(kVecThreads)
+pc_expand_kernel(LsqrPtrs P, int kind, const double* __restrict__ B, long long l,
+                 const int* __restrict__ tptr, const int* __restrict__ tidx,
+                 const double* __restrict__ tval, const double* __restrict__ s,
+                 const double* __restrict__ x, double* __restrict__ out, int mode,
+                 const int* done) {
+  __shared__ double sh[32];
+  if (done && *done) return;
+  long long j = static_cast<long long>(blockIdx.x) * kVecThreads + threadIdx.x;
+  const long long n = P.n;
+  double beta = 0.0;
+  if (mode == 1) beta = sqrt(P.g[n] + P.st->tail_norm2);
+  double sq = 0.0;
+  if (j < n) {
+    double acc = 0.0;
+    if (kind == 1) {
+      for (long long t = 0; t < l; ++t) acc += B[t * n + j] * s[t];
+    } else {
+      for (int q = tptr[j]; q < tptr[j + 1]; ++q) acc += tval[q] * s[tidx[q]];
+    }
+    const double o = x[j] + acc;
+    if (mode == 0) {
+      out[j] = o;
+    } else {
+      const double t = o - beta * P.v[j];
+      P.v[j] = t;
+      sq = t * t;
+    }
+  }
+  if (mode == 0) return;
+  sq = block_sum<kVecThreads>(sq, sh);
+  if (threadIdx.x == 0) P.epi_part[blockIdx.x] = sq;
+  if (elect_last_block(P.ctr + 2, gridDim.x)) {
+    double ssum = ordered_sum<kVecThreads>(P.epi_part, gridDim.x, sh);
+    if (threadIdx.x == 0) finalize_alpha(P.st, P.trace, sqrt(ssum), beta);
+  }
+}
+
+namespace {
+__global__ void zero_kernel(double* p, long long n) {
+  long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = 0.0;
+}
+__global__ void stamp_t0_kernel(LsqrState* st) { st->t0_ns = globaltimer_ns(); }
+inline unsigned nb(long long n, int t = kVecThreads) {
+  return static_cast<unsigned>(std::max<long long>(1, (n + t - 1) / t));
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// workspace
+// ---------------------------------------------------------------------------
+struct LsqrWork {
+  apc_ctx* ctx = nullptr;
+  long long mloc = 0, n = 0, ulen = 0;
+  double mu = 0.0;
+  DBuf<double> u, v, w, z, g, h, t, s, fwd_part, tail_part, epi_part, upd_part, pc_part;
+  DBuf<unsigned> ctr, pc_ctr;
+  DBuf<LsqrState> st;
+  DBuf<TraceRow> trace;
+  LsqrState* hst = nullptr;  // pinned
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+
+LsqrWork* lsqr_work_create(apc_mat& a, double mu) {
+  auto* w = new LsqrWork();
+  w->ctx = a.ctx;
+  w->mloc = a.mloc();
+  w->n = a.n;
+  w->mu = mu;
+  w->ulen = a.mloc() + (mu > 0.0 ? a.n : 0);
+  const long long n = a.n;
+  w->u.alloc(std::max<long long>(1, w->ulen));
+  w->v.alloc(std::max<long long>(1, n));
+  w->w.alloc(std::max<long long>(1, n));
+  w->z.alloc(std::max<long long>(1, n));
+  w->g.alloc(n + 1);
+  w->h.alloc(std::max<long long>(1, n));
+  const long long ntiles = std::max<long long>(fwd_num_tiles(a), nb(w->mloc));
+  w->fwd_part.alloc(std::max<long long>(1, ntiles));
+  w->tail_part.alloc(nb(n));
+  w->epi_part.alloc(nb(n));
+  w->upd_part.alloc(nb(n));
+  w->ctr.alloc(8);
+  APC_CUDA(cudaMemsetAsync(w->ctr.p, 0, w->ctr.bytes(), a.ctx->stream));
+  w->st.alloc(1);
+  APC_CUDA(cudaMallocHost(&w->hst, sizeof(LsqrState) * 2));
+  APC_CUDA(cudaEventCreateWithFlags(&w->ev[0], cudaEventDisableTiming));
+  APC_CUDA(cudaEventCreateWithFlags(&w->ev[1], cudaEventDisableTiming));
+  // operator scratch sized up front (no allocation during graph capture)
+  if (!a.sparse) {
+    DenseFwdPlan fp = dense_fwd_plan(a);
+    DenseAdjPlan ap = dense_adj_plan(a);
+    ctx_scratch(a.ctx, std::max(fp.nsplit * a.mloc(), ap.msplit * a.n));
+    ctx_counters(a.ctx, std::max(fp.ntiles, ap.ngroups));
+  }
+  return w;
+}
+
+void lsqr_work_destroy(LsqrWork* w) {
+  if (!w) return;
+  if (w->hst) cudaFreeHost(w->hst);
+  for (auto& e : w->ev)
+    if (e) cudaEventDestroy(e);
+  delete w;
+}
+
+// ---------------------------------------------------------------------------
+// preconditioner application pieces (enqueue on the ctx stream)
+// ---------------------------------------------------------------------------
+namespace {
+
+void pc_project(LsqrWork* w, PrecondDev& p, const double* x, const int* done) {
+  apc_ctx* ctx = w->ctx;
+  if (p.kind == 1) {
+    DenseAdjPlan pl = dense_adj_plan(p.n, p.l, ctx->num_sms);
+    launch_dense_adj(ctx, p.B.p, p.n, p.l, x, w->t.p, done, pl.msplit > 1 ? w->pc_part.p : nullptr,
+                     pl.msplit > 1 ? w->pc_ctr.p : nullptr);
+  } else {
+    const long long rows = p.R.rows;
+    const unsigned nbk = static_cast<unsigned>((rows + kCsrFwdRowsPerBlock - 1) / kCsrFwdRowsPerBlock);
+    csr_fwd_kernel<32, FwdStore><<<nbk, kCsrFwdThreads, 0, ctx->stream>>>(
+        p.R.ptr.p, p.R.idx.p, p.R.val.p, rows, x, done, FwdStore{w->t.p});
+    ctx->launches++;
+  }
+}
+
+void pc_core(LsqrWork* w, PrecondDev& p, bool transpose, const int* done) {
+  pc_core_kernel<<<nb(p.l, 128), 128, 0, w->ctx->stream>>>(transpose ? p.Ka.p : p.Kf.p, p.l,
+                                                            w->t.p, w->s.p, done);
+  w->ctx->launches++;
+}
+
+void pc_expand(LsqrWork* w, const LsqrPtrs& P, PrecondDev& p, const double* x, double* out,
+               int mode, const int* done) {
+  pc_expand_kernel<<<nb(w->n), kVecThreads, 0, w->ctx->stream>>>(
+      P, p.kind, p.B.p, p.l, p.RT.ptr.p, p.RT.idx.p, p.RT.val.p, w->s.p, x, out, mode, done);
+  w->ctx->launches++;
+}
+
+void ensure_pc_buffers(LsqrWork* w, PrecondDev& p) {
+  w->t.ensure(std::max<long long>(1, p.l));
+  w->s.ensure(std::max<long long>(1, p.l));
+  if (p.kind == 1) {
+    DenseAdjPlan pl = dense_adj_plan(p.n, p.l, w->ctx->num_sms);
+    w->pc_part.ensure(std::max<long long>(1, pl.msplit * p.l));
+    if (w->pc_ctr.n < pl.ngroups) {
+      w->pc_ctr.alloc(pl.ngroups);
+      APC_CUDA(cudaMemsetAsync(w->pc_ctr.p, 0, w->pc_ctr.bytes(), w->ctx->stream));
+    }
+  }
+}
+
+// one LSQR iteration (all kernels no-op once st->done is raised)
+void enqueue_iteration(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P,
+                       cudaGraphConditionalHandle cond, int use_cond) {
+  apc_ctx* ctx = w->ctx;
+  cudaStream_t st = ctx->stream;
+  const int* done = &P.st->done;
+  const bool pre = p && p->kind != 0;
+  const double* z = P.v;
+  if (pre) {  // z = P^{-1} v
+    pc_project(w, *p, P.v, done);
+    pc_core(w, *p, false, done);
+    pc_expand(w, P, *p, P.v, P.z, 0, done);
+    z = P.z;
+  }
+  LsqrFwdEpi epi{P.u, P.st, P.fwd_part, P.ctr + 0, P.g + P.n, 0.0, 0.0};
+  if (w->mloc > 0) {
+    launch_fwd(a, z, done, epi, st);
+  } else {
+    // empty shard: publish ||u_top||^2 = 0 through the init-copy path
+    lsqr_init_copy_kernel<<<1, kVecThreads, 0, st>>>(P, P.u, 0, 0, 0);
+    ctx->launches++;
+  }
+  if (P.has_tail) {
+    LsqrPtrs Pz = P;
+    Pz.z = const_cast<double*>(z);
+    lsqr_tail_kernel<<<nb(w->n), kVecThreads, 0, st>>>(Pz);
+    ctx->launches++;
+  }
+  op_adj_raw(a, P.u, P.g, done);
+  comm_allreduce(ctx, P.g, w->n + 1);
+  lsqr_epi_kernel<<<nb(w->n), kVecThreads, 0, st>>>(P, pre ? 1 : 0);
+  ctx->launches++;
+  if (pre) {  // v = P^{-T} h - beta v ; alpha ; rotation
+    pc_project(w, *p, P.h, done);
+    pc_core(w, *p, true, done);
+    pc_expand(w, P, *p, P.h, nullptr, 1, done);
+  }
+  lsqr_update_kernel<<<nb(w->n), kVecThreads, 0, st>>>(P, cond, use_cond);
+  ctx->launches++;
+}
+
+}  // namespace
+
+void precond_apply(apc_ctx* ctx, PrecondDev& p, bool transpose, const double* x, double* out) {
+  if (p.kind == 0) {
+    APC_CUDA(cudaMemcpyAsync(out, x, sizeof(double) * p.n, cudaMemcpyDeviceToDevice, ctx->stream));
+    return;
+  }
+  LsqrWork tmp;
+  tmp.ctx = ctx;
+  tmp.n = p.n;
+  ensure_pc_buffers(&tmp, p);
+  LsqrPtrs P{};
+  P.n = p.n;
+  pc_project(&tmp, p, x, nullptr);
+  pc_core(&tmp, p, transpose, nullptr);
+  pc_expand(&tmp, P, p, x, out, 0, nullptr);
+  APC_CUDA(cudaStreamSynchronize(ctx->stream));
+  APC_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// one phase
+// ---------------------------------------------------------------------------
+void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const double* rhs_d,
+                const StopCfg& stop, int phase, double* y_d, PhaseOut& out) {
+  (void)phase;
+  apc_ctx* ctx = w->ctx;
+  cudaStream_t st = ctx->stream;
+  PrecondDev* p = const_cast<PrecondDev*>(pc);
+  const long long n = w->n;
+  require(mu == w->mu, APC_INVALID_ARGUMENT, "lsqr_phase: workspace built for another mu");
+  if (p && p->kind != 0) ensure_pc_buffers(w, *p);
+  const long long cap = stop.max_iters > 0 ? stop.max_iters : 4 * n;
+  w->trace.ensure(cap + 1);
+
+  LsqrState h{};
+  h.eps = stop.eps_lsqr;
+  h.nu = stop.nu_lsqr;
+  h.sigma_floor = stop.sigma_floor;
+  h.iter = -1;  // initialisation pending
+  h.cap = cap;
+  h.trace_cap = cap + 1;
+  h.reason = kReasonNone;
+  std::memcpy(&w->hst[0], &h, sizeof(h));
+  APC_CUDA(cudaMemcpyAsync(w->st.p, &w->hst[0], sizeof(LsqrState), cudaMemcpyHostToDevice, st));
+
+  LsqrPtrs P{};
+  P.st = w->st.p;
+  P.trace = w->trace.p;
+  P.u = w->u.p;
+  P.v = w->v.p;
+  P.w = w->w.p;
+  P.y = y_d;
+  P.z = w->z.p;
+  P.g = w->g.p;
+  P.h = w->h.p;
+  P.fwd_part = w->fwd_part.p;
+  P.tail_part = w->tail_part.p;
+  P.epi_part = w->epi_part.p;
+  P.upd_part = w->upd_part.p;
+  P.ctr = w->ctr.p;
+  P.mloc = w->mloc;
+  P.n = n;
+  P.mu = mu;
+  P.has_tail = mu > 0.0 ? 1 : 0;
+  if (a.sparse) {
+    P.upart = a.at.upart.p;
+    P.rfirst = a.at.rfirst.p;
+    P.rcount = a.at.rcount.p;
+  }
+
+  auto t_start = std::chrono::steady_clock::now();
+  // ---- initialisation: u = rhs, beta, v = P^{-T} A^T u / beta, alpha, w = v
+  stamp_t0_kernel<<<1, 1, 0, st>>>(w->st.p);
+  zero_kernel<<<nb(n), kVecThreads, 0, st>>>(w->v.p, n);
+  zero_kernel<<<nb(n), kVecThreads, 0, st>>>(w->w.p, n);
+  zero_kernel<<<nb(n), kVecThreads, 0, st>>>(y_d, n);
+  ctx->launches += 4;
+  lsqr_init_copy_kernel<<<nb(w->mloc), kVecThreads, 0, st>>>(P, rhs_d, w->mloc, 0, 0);
+  ctx->launches++;
+  if (P.has_tail) {
+    lsqr_init_copy_kernel<<<nb(n), kVecThreads, 0, st>>>(P, rhs_d, n, w->mloc, 1);
+    ctx->launches++;
+  }
+  const int* done = &w->st.p->done;
+  const bool pre = p && p->kind != 0;
+  op_adj_raw(a, P.u, P.g, done);
+  comm_allreduce(ctx, P.g, n + 1);
+  lsqr_epi_kernel<<<nb(n), kVecThreads, 0, st>>>(P, pre ? 1 : 0);
+  ctx->launches++;
+  if (pre) {
+    pc_project(w, *p, P.h, done);
+    pc_core(w, *p, true, done);
+    pc_expand(w, P, *p, P.h, nullptr, 1, done);
+  }
+  lsqr_update_kernel<<<nb(n), kVecThreads, 0, st>>>(P, cudaGraphConditionalHandle{}, 0);
+  ctx->launches++;
+  APC_CUDA(cudaGetLastError());
+
+  // ---- iterations: graph with a conditional WHILE node (single rank), or
+  // batches of captured iterations polled from the host (multi-rank: the
+  // NCCL call stays outside conditional bodies)
+  const bool use_while = ctx->nranks == 1;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  if (use_while) {
+    APC_CUDA(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle cond;
+    APC_CUDA(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    APC_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    APC_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+    enqueue_iteration(w, a, p, P, cond, 1);
+    APC_CUDA(cudaStreamEndCapture(st, &body));
+    APC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    // skip the loop entirely if initialisation already stopped
+    APC_CUDA(cudaMemcpyAsync(&w->hst[1], w->st.p, sizeof(LsqrState), cudaMemcpyDeviceToHost, st));
+    APC_CUDA(cudaStreamSynchronize(st));
+    if (!w->hst[1].done) APC_CUDA(cudaGraphLaunch(exec, st));
+  } else {
+    constexpr int kBatch = 8;
+    APC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < kBatch; ++k) enqueue_iteration(w, a, p, P, cudaGraphConditionalHandle{}, 0);
+    APC_CUDA(cudaStreamEndCapture(st, &graph));
+    APC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    for (long long launch = 0;; ++launch) {
+      const int slot = static_cast<int>(launch & 1);
+      APC_CUDA(cudaGraphLaunch(exec, st));
+      APC_CUDA(cudaMemcpyAsync(&w->hst[slot], w->st.p, sizeof(LsqrState), cudaMemcpyDeviceToHost, st));
+      APC_CUDA(cudaEventRecord(w->ev[slot], st));
+      if (launch >= 1) {
+        APC_CUDA(cudaEventSynchronize(w->ev[slot ^ 1]));
+        if (w->hst[slot ^ 1].done) break;
+      }
+    }
+  }
+  APC_CUDA(cudaMemcpyAsync(&w->hst[0], w->st.p, sizeof(LsqrState), cudaMemcpyDeviceToHost, st));
+  APC_CUDA(cudaStreamSynchronize(st));
+  APC_CUDA(cudaGetLastError());
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  out.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+
+  const LsqrState& f = w->hst[0];
+  out.breakdown = f.breakdown != 0;
+  out.iters = f.iter < 0 ? 0 : f.iter;
+  out.reason = f.reason;
+  const long long nrows = out.iters + 1;
+  out.rows.resize(static_cast<size_t>(nrows));
+  static_assert(sizeof(TraceRowH) == sizeof(TraceRow), "trace row layout");
+  APC_CUDA(cudaMemcpy(out.rows.data(), w->trace.p, sizeof(TraceRow) * nrows, cudaMemcpyDeviceToHost));
+  if (out.breakdown) fail(APC_NUMERICAL_BREAKDOWN, "lsqr_solve: non-finite recurrence");
+}
+
+}  // namespace apc

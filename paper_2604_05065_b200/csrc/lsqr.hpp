@@ -1,0 +1,68 @@
+// Host interface of the device LSQR phase (lsqr.cu) and the device-resident
+// right preconditioner.  Mirrors lsqr_solve / StopConfig / LsqrTraceRow
+// (/root/reference/proj/include/aplicur/lsqr.hpp:17-207) and the
+// Preconditioner apply contract (preconditioner.hpp:19-28).
+#pragma once
+
+#include <vector>
+
+#include "apc_internal.hpp"
+
+namespace apc {
+
+struct TraceRowH {  // LsqrTraceRow (lsqr.hpp:38-47); layout == dev TraceRow
+  double phibar, cvgrate, cvgdiff, wall_ms;
+  long long iter;
+  unsigned long long matvecs;
+};
+
+// Device form of a right preconditioner P^{-1} = I + B K B^T (explicit basis,
+// B dense n x l) or I + R^T G R (implicit basis, R sparse l x n).  Both the
+// SVD form (preconditioner.hpp:37-136; K = diag(sigma_hat/sigma_reg - 1),
+// symmetric) and the SVD-free form (preconditioner.hpp:250-349; K = sigma_hat
+// M^{-1} - I, transpose uses M^{-T}) reduce to this shape once the l x l
+// middle operators are formed per rebuild.
+struct PrecondDev {
+  int kind = 0;  // 0 identity, 1 explicit, 2 implicit
+  i64 n = 0, l = 0;
+  DBuf<double> B;       // explicit basis, n x l column-major
+  DBuf<double> Kf, Ka;  // l x l column-major middle operators (P^{-1} / P^{-T})
+  Csr R, RT;            // implicit basis rows (l x n) and their transpose (n x l)
+  double sigma_hat = 1.0;
+  double sigma_floor = 0.0;  // cvgdiff floor of the dynamic stop (solver.hpp:216-219)
+};
+
+struct StopCfg {  // StopConfig (lsqr.hpp:54-59)
+  double eps_lsqr = 1e-10;
+  double nu_lsqr = 0.0;  // <= 0 or inf: disabled
+  double sigma_floor = 0.0;
+  i64 max_iters = 0;
+};
+
+struct PhaseOut {
+  i64 iters = 0;
+  int reason = 0;
+  bool breakdown = false;
+  std::vector<TraceRowH> rows;
+  double ms = 0.0;
+};
+
+struct LsqrWork;  // device workspace, opaque
+LsqrWork* lsqr_work_create(apc_mat& a, double mu);
+void lsqr_work_destroy(LsqrWork* w);
+
+// One LSQR call from y = 0 on the right-preconditioned system A_mu P^{-1}
+// (operators.hpp:75-90) for rhs (device, local rows [+ n tail rows when
+// mu > 0]); y_d (device, n) receives the solution.  Throws Status on breakdown.
+void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* p, const double* rhs_d,
+                const StopCfg& stop, int phase, double* y_d, PhaseOut& out);
+
+// out = P^{-1} x (transpose: P^{-T} x); device pointers, ctx stream.
+void precond_apply(apc_ctx* ctx, PrecondDev& p, bool transpose, const double* x, double* out);
+
+// allreduce(sum) of a device fp64 buffer over the ctx communicator (no-op at 1 rank)
+void comm_allreduce(apc_ctx* ctx, double* buf, i64 count);
+void comm_init(apc_ctx* ctx, const void* uid);
+void comm_destroy(apc_ctx* ctx);
+
+}  // namespace apc

@@ -1,0 +1,415 @@
+// Operator kernels and matrix upload (see ops.cuh for the design notes).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "ops.cuh"
+
+namespace apc {
+
+// ---------------------------------------------------------------------------
+// Dense A^T u
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kDenseAdjThreads)
+dense_adj_kernel(const double* __restrict__ A, long long ld, long long mloc, long long n,
+                 const double* __restrict__ u, long long rows_per_split,
+                 double* __restrict__ part, unsigned* __restrict__ grp_ctr,
+                 double* __restrict__ out, const int* done) {
+  if (done && *done) return;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long cA = static_cast<long long>(blockIdx.x) * kDenseAdjCols + w;
+  const long long cB = cA + 8;
+  const long long rb = static_cast<long long>(blockIdx.y) * rows_per_split;
+  const long long re = rb + rows_per_split < mloc ? rb + rows_per_split : mloc;
+  const bool okA = cA < n, okB = cB < n;
+  const double* pa = A + (okA ? cA : 0) * ld;
+  const double* pb = A + (okB ? cB : 0) * ld;
+  double sa0 = 0.0, sa1 = 0.0, sb0 = 0.0, sb1 = 0.0;
+  long long r = rb + lane;
+  if (okA && okB) {
+    for (; r + 32 < re; r += 64) {
+      double u0 = __ldg(u + r), u1 = __ldg(u + r + 32);
+      sa0 += __ldg(pa + r) * u0;
+      sb0 += __ldg(pb + r) * u0;
+      sa1 += __ldg(pa + r + 32) * u1;
+      sb1 += __ldg(pb + r + 32) * u1;
+    }
+    for (; r < re; r += 32) {
+      double u0 = __ldg(u + r);
+      sa0 += __ldg(pa + r) * u0;
+      sb0 += __ldg(pb + r) * u0;
+    }
+  } else if (okA) {
+    for (; r < re; r += 32) sa0 += __ldg(pa + r) * __ldg(u + r);
+  }
+  double sa = warp_sum(sa0 + sa1), sb = warp_sum(sb0 + sb1);
+  const int msplit = gridDim.y;
+  if (msplit == 1) {
+    if (lane == 0) {
+      if (okA) out[cA] = sa;
+      if (okB) out[cB] = sb;
+    }
+    return;
+  }
+  if (lane == 0) {
+    if (okA) part[blockIdx.y * n + cA] = sa;
+    if (okB) part[blockIdx.y * n + cB] = sb;
+  }
+  if (!elect_last_block(grp_ctr + blockIdx.x, msplit)) return;
+  if (lane == 0) {
+    double ta = 0.0, tb = 0.0;
+    for (int s = 0; s < msplit; ++s) {
+      if (okA) ta += ((volatile double*)part)[s * n + cA];
+      if (okB) tb += ((volatile double*)part)[s * n + cB];
+    }
+    if (okA) out[cA] = ta;
+    if (okB) out[cB] = tb;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CSR over work units (transpose products)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kCsrUnitThreads)
+csr_units_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
+                 const double* __restrict__ val, const double* __restrict__ u, long long n_units,
+                 const int* __restrict__ urow, const int* __restrict__ ustart,
+                 const int* __restrict__ uend, const int* __restrict__ uslot,
+                 double* __restrict__ out, double* __restrict__ upart, const int* done) {
+  if (done && *done) return;
+  const long long unit = (static_cast<long long>(blockIdx.x) * kCsrUnitThreads + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (unit >= n_units) return;
+  const int b = __ldg(ustart + unit), e = __ldg(uend + unit);
+  double s0 = 0.0, s1 = 0.0;
+  int q = b + lane;
+  for (; q + 32 < e; q += 64) {
+    s0 += __ldg(val + q) * __ldg(u + __ldg(idx + q));
+    s1 += __ldg(val + q + 32) * __ldg(u + __ldg(idx + q + 32));
+  }
+  if (q < e) s0 += __ldg(val + q) * __ldg(u + __ldg(idx + q));
+  double s = warp_sum(s0 + s1);
+  if (lane == 0) {
+    const int slot = __ldg(uslot + unit);
+    if (slot < 0) out[__ldg(urow + unit)] = s;
+    else upart[slot] = s;
+  }
+  (void)ptr;
+}
+
+namespace {
+
+__global__ void unit_fixup_kernel(const double* out_raw, const double* upart, const int* rfirst,
+                                  const int* rcount, long long n, double mu, const double* tail,
+                                  double* y) {
+  long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double v = unit_row_value(out_raw, upart, rfirst, rcount, j);
+  if (tail) v += mu * tail[j];
+  y[j] = v;
+}
+
+__global__ void tail_fwd_kernel(const double* x, long long n, double mu, double* y) {
+  long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j < n) y[j] = mu * x[j];
+}
+
+__global__ void add_tail_kernel(const double* t, long long n, double mu, double* y) {
+  long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j < n) y[j] += mu * t[j];
+}
+
+// ---- CSC -> CSR(A) build (stable radix sort by row keeps columns ascending)
+__global__ void expand_cols_kernel(const int* colptr, long long ncols, int* colof) {
+  long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= ncols) return;
+  for (int k = colptr[j]; k < colptr[j + 1]; ++k) colof[k] = static_cast<int>(j);
+}
+__global__ void iota_kernel(int* p, long long n) {
+  long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) p[k] = static_cast<int>(k);
+}
+__global__ void gather_csr_kernel(const int* perm, const int* colof, const double* val,
+                                  long long nnz, int* oidx, double* oval) {
+  long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= nnz) return;
+  int p = perm[k];
+  oidx[k] = colof[p];
+  oval[k] = val[p];
+}
+__global__ void row_ptr_kernel(const int* sorted_rows, long long nnz, long long rows, int* ptr) {
+  // ptr[r] = first k with sorted_rows[k] >= r (lower bound), ptr[rows] = nnz
+  long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r > rows) return;
+  long long lo = 0, hi = nnz;
+  while (lo < hi) {
+    long long mid = (lo + hi) >> 1;
+    if (sorted_rows[mid] < r) lo = mid + 1;
+    else hi = mid;
+  }
+  ptr[r] = static_cast<int>(lo);
+}
+
+inline unsigned nblk(long long n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// plans
+// ---------------------------------------------------------------------------
+DenseFwdPlan dense_fwd_plan(const apc_mat& a) {
+  DenseFwdPlan p;
+  const long long mloc = a.mloc();
+  p.ntiles = (mloc + kDenseFwdTile - 1) / kDenseFwdTile;
+  if (p.ntiles < 1) p.ntiles = 1;
+  // aim for >= 6 CTAs per SM, but keep >= 64 columns per split
+  const long long want = 6LL * a.ctx->num_sms;
+  long long ns = (want + p.ntiles - 1) / p.ntiles;
+  long long maxs = std::max<long long>(1, a.n / 64);
+  ns = std::max<long long>(1, std::min(ns, maxs));
+  p.nsplit = std::min<long long>(ns, 65535);
+  p.cols_per_split = (a.n + p.nsplit - 1) / p.nsplit;
+  if (p.cols_per_split < 1) p.cols_per_split = 1;
+  p.nsplit = (a.n + p.cols_per_split - 1) / p.cols_per_split;
+  if (p.nsplit < 1) p.nsplit = 1;
+  return p;
+}
+
+DenseAdjPlan dense_adj_plan(const apc_mat& a) { return dense_adj_plan(a.mloc(), a.n, a.ctx->num_sms); }
+
+DenseAdjPlan dense_adj_plan(long long mloc, long long n, int num_sms) {
+  DenseAdjPlan p;
+  p.ngroups = (n + kDenseAdjCols - 1) / kDenseAdjCols;
+  if (p.ngroups < 1) p.ngroups = 1;
+  const long long want = 6LL * num_sms;
+  long long ms = (want + p.ngroups - 1) / p.ngroups;
+  long long maxs = std::max<long long>(1, mloc / 512);
+  ms = std::max<long long>(1, std::min(ms, maxs));
+  p.rows_per_split = (mloc + ms - 1) / ms;
+  p.rows_per_split = std::max<long long>(32, (p.rows_per_split + 31) / 32 * 32);
+  p.msplit = (mloc + p.rows_per_split - 1) / p.rows_per_split;
+  if (p.msplit < 1) p.msplit = 1;
+  return p;
+}
+
+int csr_group_size(double avg) {
+  if (avg <= 5.0) return 4;
+  if (avg <= 10.0) return 8;
+  if (avg <= 24.0) return 16;
+  return 32;
+}
+
+double* ctx_scratch(apc_ctx* ctx, long long count) {
+  ctx->scratch_d.ensure(count);
+  return ctx->scratch_d.p;
+}
+
+unsigned* ctx_counters(apc_ctx* ctx, long long count) {
+  if (count > ctx->counters.n) {
+    ctx->counters.alloc(count);
+    APC_CUDA(cudaMemsetAsync(ctx->counters.p, 0, ctx->counters.bytes(), ctx->stream));
+  }
+  return ctx->counters.p;
+}
+
+// ---------------------------------------------------------------------------
+// operator products
+// ---------------------------------------------------------------------------
+void op_fwd(apc_mat& a, double mu, bool augmented, const double* x, double* y) {
+  cudaStream_t st = a.ctx->stream;
+  if (a.mloc() > 0) launch_fwd(a, x, nullptr, FwdStore{y}, st);
+  if (augmented && a.n > 0) {
+    tail_fwd_kernel<<<nblk(a.n, 256), 256, 0, st>>>(x, a.n, mu, y + a.mloc());
+    a.ctx->launches++;
+  }
+  APC_CUDA(cudaGetLastError());
+}
+
+void op_adj_raw(apc_mat& a, const double* u, double* out, const int* done) {
+  cudaStream_t st = a.ctx->stream;
+  if (!a.sparse) {
+    if (a.mloc() == 0) {
+      APC_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * a.n, st));
+      return;
+    }
+    DenseAdjPlan p = dense_adj_plan(a);
+    double* part = p.msplit > 1 ? ctx_scratch(a.ctx, p.msplit * a.n) : nullptr;
+    unsigned* ctr = p.msplit > 1 ? ctx_counters(a.ctx, p.ngroups) : nullptr;
+    launch_dense_adj(a.ctx, a.dense.p, a.mloc(), a.n, u, out, done, part, ctr);
+    return;
+  }
+  const Csr& c = a.at;
+  if (c.n_units == 0) return;
+  unsigned nb = nblk(c.n_units * 32, kCsrUnitThreads);
+  csr_units_kernel<<<nb, kCsrUnitThreads, 0, st>>>(c.ptr.p, c.idx.p, c.val.p, u, c.n_units,
+                                                   c.urow.p, c.ustart.p, c.uend.p, c.uslot.p, out,
+                                                   c.upart.p, done);
+  a.ctx->launches++;
+}
+
+void launch_dense_adj(apc_ctx* ctx, const double* A, long long mloc, long long n, const double* u,
+                      double* out, const int* done, double* part, unsigned* ctr) {
+  DenseAdjPlan p = dense_adj_plan(mloc, n, ctx->num_sms);
+  dim3 grid(static_cast<unsigned>(p.ngroups), static_cast<unsigned>(p.msplit));
+  dense_adj_kernel<<<grid, kDenseAdjThreads, 0, ctx->stream>>>(A, mloc, mloc, n, u, p.rows_per_split,
+                                                               part, ctr, out, done);
+  ctx->launches++;
+}
+
+void op_adj(apc_mat& a, double mu, bool augmented, const double* u, double* y) {
+  cudaStream_t st = a.ctx->stream;
+  if (!a.sparse) {
+    op_adj_raw(a, u, y, nullptr);
+    if (augmented && a.n > 0) {
+      add_tail_kernel<<<nblk(a.n, 256), 256, 0, st>>>(u + a.mloc(), a.n, mu, y);
+      a.ctx->launches++;
+    }
+  } else {
+    double* raw = ctx_scratch(a.ctx, a.n);
+    op_adj_raw(a, u, raw, nullptr);
+    unit_fixup_kernel<<<nblk(a.n, 256), 256, 0, st>>>(raw, a.at.upart.p, a.at.rfirst.p,
+                                                      a.at.rcount.p, a.n, mu,
+                                                      augmented ? u + a.mloc() : nullptr, y);
+    a.ctx->launches++;
+  }
+  APC_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// work units for a CSR (host-built from the row lengths)
+// ---------------------------------------------------------------------------
+void build_units(apc_ctx* ctx, Csr& c, const std::vector<long long>& row_nnz) {
+  std::vector<int> urow, ustart, uend, uslot, rfirst(c.rows, -1), rcount(c.rows, 0);
+  urow.reserve(c.rows);
+  long long off = 0, nparts = 0, maxr = 0;
+  for (long long r = 0; r < c.rows; ++r) {
+    long long L = row_nnz[r];
+    maxr = std::max(maxr, L);
+    if (L <= kCsrUnitMax) {
+      urow.push_back(static_cast<int>(r));
+      ustart.push_back(static_cast<int>(off));
+      uend.push_back(static_cast<int>(off + L));
+      uslot.push_back(-1);
+    } else {
+      long long k = (L + kCsrUnitMax - 1) / kCsrUnitMax;
+      rfirst[r] = static_cast<int>(nparts);
+      rcount[r] = static_cast<int>(k);
+      for (long long q = 0; q < k; ++q) {
+        long long b = off + q * kCsrUnitMax, e = std::min(off + L, b + kCsrUnitMax);
+        urow.push_back(static_cast<int>(r));
+        ustart.push_back(static_cast<int>(b));
+        uend.push_back(static_cast<int>(e));
+        uslot.push_back(static_cast<int>(nparts + q));
+      }
+      nparts += k;
+    }
+    off += L;
+  }
+  c.n_units = static_cast<long long>(urow.size());
+  c.n_parts = nparts;
+  c.max_row_nnz = maxr;
+  c.avg_row_nnz = c.rows > 0 ? static_cast<double>(off) / static_cast<double>(c.rows) : 0.0;
+  auto up = [&](DBuf<int>& d, const std::vector<int>& h) {
+    d.alloc(static_cast<long long>(h.size()));
+    if (!h.empty())
+      APC_CUDA(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  };
+  up(c.urow, urow);
+  up(c.ustart, ustart);
+  up(c.uend, uend);
+  up(c.uslot, uslot);
+  up(c.rfirst, rfirst);
+  up(c.rcount, rcount);
+  c.upart.alloc(std::max<long long>(1, nparts));
+  APC_CUDA(cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
+}
+
+// ---------------------------------------------------------------------------
+// CSC (int64, reference layout) -> device CSR(A^T) (= CSC arrays, local rows
+// only) and CSR(A) via a stable radix sort by row.
+// ---------------------------------------------------------------------------
+void upload_csc(apc_mat& a, const long long* colptr, const long long* rowidx, const double* val) {
+  apc_ctx* ctx = a.ctx;
+  cudaStream_t st = ctx->stream;
+  const long long n = a.n, r0 = a.r0, r1 = a.r1, mloc = a.mloc();
+  // host: filter to local rows and narrow indices to int32 (pinned staging)
+  std::vector<int> tptr(n + 1);
+  long long cnt = 0;
+  for (long long j = 0; j < n; ++j) {
+    tptr[j] = static_cast<int>(cnt);
+    for (long long k = colptr[j]; k < colptr[j + 1]; ++k)
+      if (rowidx[k] >= r0 && rowidx[k] < r1) ++cnt;
+  }
+  tptr[n] = static_cast<int>(cnt);
+  require(cnt < (1LL << 31), APC_INVALID_ARGUMENT, "upload_csc: nnz exceeds int32 range");
+  const long long nnz = cnt;
+  int* hidx = nullptr;
+  double* hval = nullptr;
+  APC_CUDA(cudaMallocHost(&hidx, sizeof(int) * std::max<long long>(1, nnz)));
+  APC_CUDA(cudaMallocHost(&hval, sizeof(double) * std::max<long long>(1, nnz)));
+  std::vector<long long> tlen(n);
+  {
+    long long q = 0;
+    for (long long j = 0; j < n; ++j) {
+      for (long long k = colptr[j]; k < colptr[j + 1]; ++k) {
+        long long r = rowidx[k];
+        if (r >= r0 && r < r1) {
+          hidx[q] = static_cast<int>(r - r0);
+          hval[q] = val[k];
+          ++q;
+        }
+      }
+      tlen[j] = tptr[j + 1] - tptr[j];
+    }
+  }
+  Csr& t = a.at;
+  t.rows = n;
+  t.cols = mloc;
+  t.nnz = nnz;
+  t.ptr.alloc(n + 1);
+  t.idx.alloc(std::max<long long>(1, nnz));
+  t.val.alloc(std::max<long long>(1, nnz));
+  APC_CUDA(cudaMemcpyAsync(t.ptr.p, tptr.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice, st));
+  if (nnz > 0) {
+    APC_CUDA(cudaMemcpyAsync(t.idx.p, hidx, sizeof(int) * nnz, cudaMemcpyHostToDevice, st));
+    APC_CUDA(cudaMemcpyAsync(t.val.p, hval, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+  }
+  build_units(ctx, t, tlen);  // synchronizes the stream
+  cudaFreeHost(hidx);
+  cudaFreeHost(hval);
+
+  // CSR(A): sort entries by row (stable), keeping column order within rows
+  Csr& c = a.a;
+  c.rows = mloc;
+  c.cols = n;
+  c.nnz = nnz;
+  c.ptr.alloc(mloc + 1);
+  c.idx.alloc(std::max<long long>(1, nnz));
+  c.val.alloc(std::max<long long>(1, nnz));
+  if (nnz > 0) {
+    DBuf<int> colof(nnz), perm_in(nnz), perm_out(nnz), keys_out(nnz);
+    expand_cols_kernel<<<nblk(n, 256), 256, 0, st>>>(t.ptr.p, n, colof.p);
+    iota_kernel<<<nblk(nnz, 256), 256, 0, st>>>(perm_in.p, nnz);
+    int end_bit = 1;
+    while ((1LL << end_bit) < mloc + 1 && end_bit < 31) ++end_bit;
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, t.idx.p, keys_out.p, perm_in.p, perm_out.p,
+                                    static_cast<int>(nnz), 0, end_bit, st);
+    DBuf<char> tmp(static_cast<long long>(tmp_bytes));
+    APC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, t.idx.p, keys_out.p, perm_in.p,
+                                             perm_out.p, static_cast<int>(nnz), 0, end_bit, st));
+    gather_csr_kernel<<<nblk(nnz, 256), 256, 0, st>>>(perm_out.p, colof.p, t.val.p, nnz, c.idx.p,
+                                                      c.val.p);
+    row_ptr_kernel<<<nblk(mloc + 1, 256), 256, 0, st>>>(keys_out.p, nnz, mloc, c.ptr.p);
+    ctx->launches += 4;
+    APC_CUDA(cudaStreamSynchronize(st));
+  } else {
+    APC_CUDA(cudaMemsetAsync(c.ptr.p, 0, sizeof(int) * (mloc + 1), st));
+  }
+  c.avg_row_nnz = mloc > 0 ? static_cast<double>(nnz) / static_cast<double>(mloc) : 0.0;
+  APC_CUDA(cudaGetLastError());
+}
+
+}  // namespace apc

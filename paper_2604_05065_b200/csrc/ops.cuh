@@ -1,0 +1,238 @@
+// Operator kernels for A_mu*x and A_mu^T*u on sm_100a (fp64, HBM-bound).
+//
+// Reference semantics: Matrix::matvec / matvec_transpose
+// (/root/reference/proj/include/aplicur/matrix.hpp:151-195) and the
+// AugmentedOperator tail (matrix.hpp:377-392).  Summation order differs from
+// the reference's sequential loops (parallel, but fixed: reruns are
+// bit-identical); LSQR parity is judged at the x / iteration level, never on
+// CUR indices.
+//
+// Forward kernels take an epilogue functor so the LSQR vector update
+// (u <- A z - alpha*u, ||u||^2 partials, lsqr.hpp:139-145) is fused into the
+// pass that produces A z.  Transpose kernels only produce the raw A^T u; the
+// LSQR epilogue runs in a light n-length kernel after the (optional) NCCL
+// allreduce, which is where partial A_p^T u_p from row shards meet.
+#pragma once
+
+#include "apc_internal.hpp"
+#include "dev_common.cuh"
+#include "ops_host.hpp"
+
+namespace apc {
+
+constexpr int kDenseFwdThreads = 256;
+constexpr int kDenseFwdRowsPerThread = 2;
+constexpr int kDenseFwdTile = kDenseFwdThreads * kDenseFwdRowsPerThread;
+constexpr int kDenseAdjThreads = 256;
+constexpr int kDenseAdjCols = 16;  // 8 warps x 2 columns
+constexpr int kCsrFwdThreads = 256;
+constexpr int kCsrFwdRowsPerBlock = 256;
+constexpr int kCsrUnitThreads = 256;
+constexpr int kCsrUnitMax = 2048;  // max nnz per work unit of the transpose SpMV
+
+// ---------------------------------------------------------------------------
+// forward epilogue interface:
+//   __device__ void begin();                       // load scalars
+//   __device__ double row(i64 r, double v);        // consume (A x)_r, return ||.||^2 term
+//   __device__ void tile_done(unsigned tile, unsigned ntiles, double sum_sq);
+// ---------------------------------------------------------------------------
+struct FwdStore {  // y = A x
+  double* y;
+  __device__ void begin() {}
+  __device__ double row(long long r, double v) { y[r] = v; return 0.0; }
+  __device__ void tile_done(unsigned, unsigned, double) {}
+};
+
+// ---------------------------------------------------------------------------
+// Dense A x (column-major, ld = mloc), split over columns.
+// grid = (ntiles, nsplit); part: nsplit x mloc partials; tile_ctr: ntiles counters
+// ---------------------------------------------------------------------------
+template <class Epi>
+__global__ void __launch_bounds__(kDenseFwdThreads)
+dense_fwd_kernel(const double* __restrict__ A, long long ld, long long mloc, long long n,
+                 const double* __restrict__ x, long long cols_per_split,
+                 double* __restrict__ part, unsigned* __restrict__ tile_ctr, const int* done,
+                 Epi epi) {
+  __shared__ double red[32];
+  if (done && *done) return;
+  const int nsplit = gridDim.y;
+  const long long tile = blockIdx.x;
+  const long long r0 = tile * kDenseFwdTile + threadIdx.x;
+  const long long r1 = r0 + kDenseFwdThreads;
+  const long long c0 = blockIdx.y * cols_per_split;
+  const long long c1 = c0 + cols_per_split < n ? c0 + cols_per_split : n;
+  double acc0 = 0.0, acc1 = 0.0;
+  const bool ok0 = r0 < mloc, ok1 = r1 < mloc;
+  const double* a0 = A + r0;
+  const double* a1 = A + r1;
+  long long c = c0;
+  if (ok1) {
+    for (; c + 4 <= c1; c += 4) {
+      double x0 = __ldg(x + c), x1 = __ldg(x + c + 1), x2 = __ldg(x + c + 2), x3 = __ldg(x + c + 3);
+      double p0 = __ldg(a0 + c * ld), p1 = __ldg(a0 + (c + 1) * ld);
+      double p2 = __ldg(a0 + (c + 2) * ld), p3 = __ldg(a0 + (c + 3) * ld);
+      double q0 = __ldg(a1 + c * ld), q1 = __ldg(a1 + (c + 1) * ld);
+      double q2 = __ldg(a1 + (c + 2) * ld), q3 = __ldg(a1 + (c + 3) * ld);
+      acc0 += p0 * x0; acc1 += q0 * x0;
+      acc0 += p1 * x1; acc1 += q1 * x1;
+      acc0 += p2 * x2; acc1 += q2 * x2;
+      acc0 += p3 * x3; acc1 += q3 * x3;
+    }
+    for (; c < c1; ++c) {
+      double xc = __ldg(x + c);
+      acc0 += __ldg(a0 + c * ld) * xc;
+      acc1 += __ldg(a1 + c * ld) * xc;
+    }
+  } else if (ok0) {
+    for (; c < c1; ++c) acc0 += __ldg(a0 + c * ld) * __ldg(x + c);
+  }
+  if (nsplit > 1) {
+    if (ok0) part[blockIdx.y * mloc + r0] = acc0;
+    if (ok1) part[blockIdx.y * mloc + r1] = acc1;
+    if (!elect_last_block(tile_ctr + tile, nsplit)) return;
+    acc0 = 0.0;
+    acc1 = 0.0;
+    for (int s = 0; s < nsplit; ++s) {
+      if (ok0) acc0 += ((volatile double*)part)[s * mloc + r0];
+      if (ok1) acc1 += ((volatile double*)part)[s * mloc + r1];
+    }
+  }
+  epi.begin();
+  double sq = 0.0;
+  if (ok0) sq += epi.row(r0, acc0);
+  if (ok1) sq += epi.row(r1, acc1);
+  sq = block_sum<kDenseFwdThreads>(sq, red);
+  epi.tile_done(static_cast<unsigned>(tile), gridDim.x, sq);
+}
+
+// ---------------------------------------------------------------------------
+// Dense A^T u: CTA = 16 columns x one row split; warp-shuffle dot products.
+// grid = (ceil(n/16), msplit); part: msplit x n; grp_ctr: ceil(n/16) counters.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kDenseAdjThreads)
+dense_adj_kernel(const double* __restrict__ A, long long ld, long long mloc, long long n,
+                 const double* __restrict__ u, long long rows_per_split,
+                 double* __restrict__ part, unsigned* __restrict__ grp_ctr,
+                 double* __restrict__ out, const int* done);
+
+// ---------------------------------------------------------------------------
+// CSR A x: G lanes per row, fixed rows per block (deterministic tile slots).
+// ---------------------------------------------------------------------------
+template <int G, class Epi>
+__global__ void __launch_bounds__(kCsrFwdThreads)
+csr_fwd_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
+               const double* __restrict__ val, long long rows, const double* __restrict__ x,
+               const int* done, Epi epi) {
+  __shared__ double red[32];
+  if (done && *done) return;
+  constexpr int kGroups = kCsrFwdThreads / G;
+  const int g = threadIdx.x / G, lane = threadIdx.x % G;
+  const long long rbase = static_cast<long long>(blockIdx.x) * kCsrFwdRowsPerBlock;
+  epi.begin();
+  double sq = 0.0;
+  for (int k = 0; k < kCsrFwdRowsPerBlock; k += kGroups) {
+    const long long r = rbase + k + g;
+    double s = 0.0;
+    if (r < rows) {
+      const int b = __ldg(ptr + r), e = __ldg(ptr + r + 1);
+      for (int q = b + lane; q < e; q += G) s += __ldg(val + q) * __ldg(x + __ldg(idx + q));
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
+    if (lane == 0 && r < rows) sq += epi.row(r, s);
+  }
+  sq = block_sum<kCsrFwdThreads>(sq, red);
+  epi.tile_done(blockIdx.x, gridDim.x, sq);
+}
+
+// ---------------------------------------------------------------------------
+// CSR A^T u over nnz-balanced work units (one warp per unit).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kCsrUnitThreads)
+csr_units_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
+                 const double* __restrict__ val, const double* __restrict__ u, long long n_units,
+                 const int* __restrict__ urow, const int* __restrict__ ustart,
+                 const int* __restrict__ uend, const int* __restrict__ uslot,
+                 double* __restrict__ out, double* __restrict__ upart, const int* done);
+
+// value of row j of a unit-split SpMV (fix-up of split rows in slot order)
+__device__ __forceinline__ double unit_row_value(const double* out, const double* upart,
+                                                 const int* rfirst, const int* rcount,
+                                                 long long j) {
+  const int f = rfirst[j];
+  if (f < 0) return out[j];
+  const int cnt = rcount[j];
+  double s = 0.0;
+  for (int k = 0; k < cnt; ++k) s += upart[f + k];
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// host-side launch helpers (ops.cu)
+// ---------------------------------------------------------------------------
+struct DenseFwdPlan {
+  long long ntiles, nsplit, cols_per_split;
+};
+DenseFwdPlan dense_fwd_plan(const apc_mat& a);
+struct DenseAdjPlan {
+  long long ngroups, msplit, rows_per_split;
+};
+DenseAdjPlan dense_adj_plan(const apc_mat& a);
+DenseAdjPlan dense_adj_plan(long long mloc, long long n, int num_sms);
+// raw dense A^T u for an arbitrary column-major block (ld = mloc)
+void launch_dense_adj(apc_ctx* ctx, const double* A, long long mloc, long long n, const double* u,
+                      double* out, const int* done, double* part, unsigned* ctr);
+int csr_group_size(double avg_row_nnz);
+
+// scratch owned by the matrix-independent ctx
+double* ctx_scratch(apc_ctx* ctx, long long count);
+unsigned* ctx_counters(apc_ctx* ctx, long long count);
+
+// A x -> y (local rows), optional mu-tail: y[mloc + j] = mu * x[j]
+void op_fwd(apc_mat& a, double mu, bool augmented, const double* x, double* y);
+// A^T u -> y (local contribution), optional + mu * u[mloc + j]
+void op_adj(apc_mat& a, double mu, bool augmented, const double* u, double* y);
+// raw A^T u into out[0..n) (units fix-up is left to the caller for CSR)
+void op_adj_raw(apc_mat& a, const double* u, double* out, const int* done);
+
+// device CSR build from host CSC (matrix upload)
+void upload_csc(apc_mat& a, const long long* colptr, const long long* rowidx, const double* val);
+void build_units(apc_ctx* ctx, apc::Csr& c, const std::vector<long long>& row_nnz);
+
+template <class Epi>
+void launch_dense_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaStream_t st) {
+  DenseFwdPlan p = dense_fwd_plan(a);
+  double* part = p.nsplit > 1 ? ctx_scratch(a.ctx, p.nsplit * a.mloc()) : nullptr;
+  unsigned* ctr = p.nsplit > 1 ? ctx_counters(a.ctx, p.ntiles) : nullptr;
+  dim3 grid(static_cast<unsigned>(p.ntiles), static_cast<unsigned>(p.nsplit));
+  dense_fwd_kernel<Epi><<<grid, kDenseFwdThreads, 0, st>>>(a.dense.p, a.mloc(), a.mloc(), a.n, x,
+                                                             p.cols_per_split, part, ctr, done, epi);
+  a.ctx->launches++;
+}
+
+template <class Epi>
+void launch_csr_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaStream_t st) {
+  const long long rows = a.a.rows;
+  const unsigned nb = static_cast<unsigned>((rows + kCsrFwdRowsPerBlock - 1) / kCsrFwdRowsPerBlock);
+  if (nb == 0) return;
+  switch (csr_group_size(a.a.avg_row_nnz)) {
+    case 4: csr_fwd_kernel<4, Epi><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi); break;
+    case 8: csr_fwd_kernel<8, Epi><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi); break;
+    case 16: csr_fwd_kernel<16, Epi><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi); break;
+    default: csr_fwd_kernel<32, Epi><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi); break;
+  }
+  a.ctx->launches++;
+}
+
+template <class Epi>
+void launch_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaStream_t st) {
+  if (a.sparse) launch_csr_fwd(a, x, done, epi, st);
+  else launch_dense_fwd(a, x, done, epi, st);
+}
+
+inline unsigned fwd_num_tiles(const apc_mat& a) {
+  if (a.sparse) return static_cast<unsigned>((a.a.rows + kCsrFwdRowsPerBlock - 1) / kCsrFwdRowsPerBlock);
+  return static_cast<unsigned>(dense_fwd_plan(a).ntiles);
+}
+
+}  // namespace apc
