@@ -95,6 +95,31 @@ int apc_rng_fill(uint64_t seed, int stream, uint64_t index, int kind, uint64_t b
                  int64_t count, void* out);
 uint64_t apc_mix64(uint64_t x);
 
+/* ---- single-sketch incremental CUR (CurState, cur.hpp:200-371) ----------
+ * Exact-order device kernels: Y, E^row, the LUPP pivot order and rho are
+ * bit-identical to the reference.  sketch_kind 0 = SparseSignEmbedding
+ * (CurState::init, cur.hpp:209-226), 1 = GaussianEmbedding (sketch.hpp:173-197). */
+typedef struct apc_cur apc_cur;
+int apc_cur_create(apc_mat* a, int64_t block, uint64_t seed, int64_t xi, int64_t probe_count,
+                   int core_kind, int sketch_kind, apc_cur** out);
+int apc_cur_free(apc_cur* c);
+/* CurState::augment: added = 0 and exhausted = 1 when no admissible pivot remains */
+int apc_cur_augment(apc_cur* c, int64_t* added, int* exhausted);
+/* CurState::refresh: returns APC_SINGULAR on a numerically singular intersection */
+int apc_cur_refresh(apc_cur* c);
+int apc_cur_rollback_last_augment(apc_cur* c);
+int apc_cur_state(const apc_cur* c, int64_t* rank, double* rho, int64_t* sketch_rows, int64_t* n_rho);
+int apc_cur_indices(const apc_cur* c, int64_t* rows, int64_t* cols);
+int apc_cur_rho_history(const apc_cur* c, double* rho);
+/* sketch_matrix() / sketch_residual(): s x n column-major, host copies */
+int apc_cur_sketch(const apc_cur* c, double* y);
+int apc_cur_residual(const apc_cur* c, double* e);
+
+/* lu_partial_pivot (dense_factor.hpp:119-157) on a host column-major matrix,
+ * run on the device; order/mags sized min(rows, cols, max_pivots). */
+int apc_lupp(apc_ctx* ctx, const double* w, int64_t rows, int64_t cols, int64_t max_pivots,
+             int64_t* order, double* mags, int64_t* steps);
+
 /* ---- synthetic BASELINE inputs (host) ---------------------------------- */
 /* config 1..5 = BASELINE.json configs[0..4]; m, n = 0 -> the BASELINE shape;
  * seed = 0 -> 20260415 + config.  Dense problems are column-major; sparse ones

@@ -158,6 +158,17 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
         "apc_result_phases": (C.c_int, [vp, C.POINTER(_Phase)]),
         "apc_result_trace": (C.c_int, [vp, C.POINTER(_Trace)]),
         "apc_result_timing": (C.c_int, [vp, _dp, _dp, _dp]),
+        "apc_cur_create": (C.c_int, [vp, _i64, _u64, _i64, _i64, C.c_int, C.c_int, C.POINTER(vp)]),
+        "apc_cur_free": (C.c_int, [vp]),
+        "apc_cur_augment": (C.c_int, [vp, _i64p, C.POINTER(C.c_int)]),
+        "apc_cur_refresh": (C.c_int, [vp]),
+        "apc_cur_rollback_last_augment": (C.c_int, [vp]),
+        "apc_cur_state": (C.c_int, [vp, _i64p, _dp, _i64p, _i64p]),
+        "apc_cur_indices": (C.c_int, [vp, _i64p, _i64p]),
+        "apc_cur_rho_history": (C.c_int, [vp, _dp]),
+        "apc_cur_sketch": (C.c_int, [vp, _dp]),
+        "apc_cur_residual": (C.c_int, [vp, _dp]),
+        "apc_lupp": (C.c_int, [vp, _dp, _i64, _i64, _i64, _i64p, _dp, _i64p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -301,6 +312,85 @@ class DeviceMatrix:
             self.free()
         except Exception:
             pass
+
+
+class CurState:
+    """Device CurState (cur.hpp:200-371): single sketch, incremental augment /
+    refresh with exact-order kernels (bit-identical indices and rho)."""
+
+    def __init__(self, mat: DeviceMatrix, block: int, seed: int, xi: int = 8, probe_count: int = 10,
+                 core: CoreFactorKind = CoreFactorKind.qr, sketch: SketchKind = SketchKind.sparse_sign):
+        h = C.c_void_p()
+        _check(load_library().apc_cur_create(mat.h, block, seed, xi, probe_count, int(core), int(sketch),
+                                             C.byref(h)))
+        self.h, self.mat = h, mat
+
+    def augment(self):
+        added, ex = _i64(), C.c_int()
+        _check(load_library().apc_cur_augment(self.h, C.byref(added), C.byref(ex)))
+        return added.value, bool(ex.value)
+
+    def refresh(self) -> None:
+        _check(load_library().apc_cur_refresh(self.h))
+
+    def rollback_last_augment(self) -> None:
+        _check(load_library().apc_cur_rollback_last_augment(self.h))
+
+    def _state(self):
+        r, rho, s, nr = _i64(), C.c_double(), _i64(), _i64()
+        load_library().apc_cur_state(self.h, C.byref(r), C.byref(rho), C.byref(s), C.byref(nr))
+        return r.value, rho.value, s.value, nr.value
+
+    def rank(self) -> int:
+        return self._state()[0]
+
+    def rho(self) -> float:
+        return self._state()[1]
+
+    def indices(self):
+        r = self.rank()
+        rows, cols = np.zeros(r, np.int64), np.zeros(r, np.int64)
+        load_library().apc_cur_indices(self.h, _iptr(rows), _iptr(cols))
+        return rows, cols
+
+    def rho_history(self) -> np.ndarray:
+        out = np.zeros(self._state()[3])
+        load_library().apc_cur_rho_history(self.h, _dptr(out))
+        return out
+
+    def sketch_matrix(self) -> np.ndarray:
+        s = self._state()[2]
+        y = np.zeros(s * self.mat.n)
+        _check(load_library().apc_cur_sketch(self.h, _dptr(y)))
+        return y.reshape(self.mat.n, s).T
+
+    def sketch_residual(self) -> np.ndarray:
+        s = self._state()[2]
+        y = np.zeros(s * self.mat.n)
+        _check(load_library().apc_cur_residual(self.h, _dptr(y)))
+        return y.reshape(self.mat.n, s).T
+
+    def close(self):
+        if getattr(self, "h", None):
+            load_library().apc_cur_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def lu_partial_pivot(ctx: Context, W: np.ndarray, max_pivots: int = -1):
+    """Pivot order + magnitudes of partial-pivoting LU (dense_factor.hpp:119-157), on the GPU."""
+    rows, cols = W.shape
+    w = np.asfortranarray(W, dtype=np.float64).reshape(-1, order="F")
+    k = min(rows, cols) if max_pivots < 0 else min(rows, cols, max_pivots)
+    order, mags, ns = np.zeros(max(k, 1), np.int64), np.zeros(max(k, 1)), _i64()
+    _check(load_library().apc_lupp(ctx.h, _dptr(w), rows, cols, max_pivots, _iptr(order), _dptr(mags),
+                                   C.byref(ns)))
+    return order[: ns.value], mags[: ns.value]
 
 
 def partition_rows(m: int, nranks: int, row_nnz: Optional[np.ndarray] = None) -> np.ndarray:
@@ -480,5 +570,5 @@ __all__ = [
     "ApcError", "StopReason", "SolveStatus", "PrecondVariant", "CoreFactorKind", "SketchKind",
     "Context", "DeviceMatrix", "Problem", "SolverConfig", "SolveResult", "PhaseReport",
     "aplicur_solve", "plain_lsqr_solve", "solve", "load_library", "device_count",
-    "partition_rows", "rng_fill", "LIB_PATH", "HEADER_PATHS",
+    "partition_rows", "rng_fill", "LIB_PATH", "HEADER_PATHS", "CurState", "lu_partial_pivot",
 ]

@@ -4,6 +4,7 @@
 // device-facing calls fail with APC_NO_DEVICE.
 #include <algorithm>
 #include <cstring>
+#include <functional>
 #include <string>
 
 #include "apc_internal.hpp"
@@ -58,6 +59,9 @@ void need_device() {
 }
 
 }  // namespace
+
+int capi_guard(apc_ctx* ctx, const std::function<void()>& f) { return guard(ctx, f); }
+
 }  // namespace apc
 
 using namespace apc;

@@ -1,0 +1,983 @@
+// Exact-order CUR kernels + the DeviceCur state machine (see cur.hpp).
+//
+// "Exact order" means: every output element is produced by the same sequence
+// of IEEE operations as the reference's scalar loops (products and sums
+// rounded separately, -fmad=false, sums in the reference's index order).  The
+// parallelism comes from independent output elements, never from reordering a
+// sum.  This is what makes I, J and rho_history bit-identical to the CPU.
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <numeric>
+
+#include "cur.hpp"
+#include "dev_common.cuh"
+#include "ops.cuh"
+
+namespace apc {
+
+namespace {
+
+constexpr int kT = 256;
+inline unsigned nb(long long n, int t = kT) {
+  return static_cast<unsigned>(std::max<long long>(1, (n + t - 1) / t));
+}
+
+// A(i, j) of a CSR matrix (columns sorted within rows): binary search
+__device__ __forceinline__ double csr_at(const int* ptr, const int* idx, const double* val, long long i,
+                                         long long j) {
+  int lo = ptr[i], hi = ptr[i + 1];
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (idx[mid] < j) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < ptr[i + 1] && idx[lo] == j) ? val[lo] : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// sketch Y = S * A (sparse sign), sketch.hpp:77-162.  One warp per column of
+// A; Y(:, j) lives in shared memory; rows k in ascending order, each adding
+// +-scale*A(k, j) to its xi rows (distinct within k, so lanes never collide).
+// ---------------------------------------------------------------------------
+constexpr int kSketchWarps = 8;
+
+__global__ void __launch_bounds__(kSketchWarps * 32)
+sketch_ss_dense_kernel(const double* __restrict__ A, long long m, long long n, int s, int xi,
+                       const int* __restrict__ srow, const signed char* __restrict__ ssgn,
+                       double scale, double mu_scale, int aug, double* __restrict__ Y) {
+  extern __shared__ double ysh[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long j = static_cast<long long>(blockIdx.x) * kSketchWarps + w;
+  if (j >= n) return;
+  double* yc = ysh + static_cast<long long>(w) * s;
+  for (int i = lane; i < s; i += 32) yc[i] = 0.0;
+  __syncwarp();
+  const double* col = A + j * m;
+  for (long long k0 = 0; k0 < m; k0 += 32) {
+    const long long k = k0 + lane;
+    const double v = k < m ? col[k] : 0.0;
+    const int cnt = static_cast<int>(m - k0 < 32 ? m - k0 : 32);
+    for (int kk = 0; kk < cnt; ++kk) {
+      const double vk = __shfl_sync(0xffffffffu, v, kk);
+      if (vk != 0.0) {
+        const double sv = scale * vk;
+        if (lane < xi) {
+          const long long e = (k0 + kk) * xi + lane;
+          const double sg = static_cast<double>(ssgn[e]);
+          yc[srow[e]] += sv * sg;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (aug && lane < xi) {  // mu tail: column m + j of S (sketch.hpp:152-160)
+    const long long e = (m + j) * xi + lane;
+    yc[srow[e]] += mu_scale * static_cast<double>(ssgn[e]);
+  }
+  __syncwarp();
+  for (int i = lane; i < s; i += 32) Y[j * s + i] = yc[i];
+}
+
+// CSC input: the device CSR(A^T) rows are the reference CSC columns
+__global__ void __launch_bounds__(kSketchWarps * 32)
+sketch_ss_csc_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
+                     const double* __restrict__ cval, long long m, long long n, int s, int xi,
+                     const int* __restrict__ srow, const signed char* __restrict__ ssgn,
+                     double scale, double mu_scale, int aug, double* __restrict__ Y) {
+  extern __shared__ double ysh[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long j = static_cast<long long>(blockIdx.x) * kSketchWarps + w;
+  if (j >= n) return;
+  double* yc = ysh + static_cast<long long>(w) * s;
+  for (int i = lane; i < s; i += 32) yc[i] = 0.0;
+  __syncwarp();
+  const int b = cptr[j], e = cptr[j + 1];
+  for (int p0 = b; p0 < e; p0 += 32) {
+    const int p = p0 + lane;
+    const double v = p < e ? cval[p] : 0.0;
+    const int k = p < e ? ridx[p] : 0;
+    const int cnt = e - p0 < 32 ? e - p0 : 32;
+    for (int q = 0; q < cnt; ++q) {
+      const double vk = __shfl_sync(0xffffffffu, v, q);
+      const int kq = __shfl_sync(0xffffffffu, k, q);
+      const double sv = scale * vk;
+      if (lane < xi) {
+        const long long ee = static_cast<long long>(kq) * xi + lane;
+        yc[srow[ee]] += sv * static_cast<double>(ssgn[ee]);
+      }
+      __syncwarp();
+    }
+  }
+  if (aug && lane < xi) {
+    const long long ee = (m + j) * xi + lane;
+    yc[srow[ee]] += mu_scale * static_cast<double>(ssgn[ee]);
+  }
+  __syncwarp();
+  for (int i = lane; i < s; i += 32) Y[j * s + i] = yc[i];
+}
+
+// ---------------------------------------------------------------------------
+// Gaussian sketch Y = S A via matmul (sketch.hpp:189-192 -> matrix.hpp:351-361):
+// Y(i, j) = sum_k A(k, j) * S(i, k), k ascending.  Register-tiled FP64 GEMM
+// whose k loop runs in order with separate DMUL/DADD: the exact chain of the
+// reference, at GEMM data reuse.
+// ---------------------------------------------------------------------------
+constexpr int kGT = 64, kGK = 16;
+
+__global__ void __launch_bounds__(256)
+sketch_gauss_dense_kernel(const double* __restrict__ S, int s, const double* __restrict__ A, long long m,
+                          long long n, double* __restrict__ Y) {
+  __shared__ double Ss[kGK][kGT + 1];
+  __shared__ double As[kGK][kGT + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const long long i0 = static_cast<long long>(blockIdx.y) * kGT;
+  const long long j0 = static_cast<long long>(blockIdx.x) * kGT;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+  for (long long k0 = 0; k0 < m; k0 += kGK) {
+    for (int e = threadIdx.x; e < kGK * kGT; e += 256) {
+      const int kk = e / kGT, ii = e % kGT;
+      const long long k = k0 + kk;
+      Ss[kk][ii] = (k < m && i0 + ii < s) ? S[k * s + i0 + ii] : 0.0;
+    }
+    for (int e = threadIdx.x; e < kGK * kGT; e += 256) {
+      const int jj = e / kGK, kk = e % kGK;
+      const long long k = k0 + kk;
+      As[kk][jj] = (k < m && j0 + jj < n) ? A[(j0 + jj) * m + k] : 0.0;
+    }
+    __syncthreads();
+    const int kmax = static_cast<int>(m - k0 < kGK ? m - k0 : kGK);
+    for (int kk = 0; kk < kmax; ++kk) {
+      double sa[4], ab[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) sa[a] = Ss[kk][ty * 4 + a];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) ab[c] = As[kk][tx * 4 + c];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = __dadd_rn(acc[a][c], __dmul_rn(ab[c], sa[a]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const long long i = i0 + ty * 4 + a, j = j0 + tx * 4 + c;
+      if (i < s && j < n) Y[j * s + i] = acc[a][c];
+    }
+}
+
+// sparse A with a Gaussian S: per (i, j) chain over the stored rows of column j
+__global__ void sketch_gauss_csc_kernel(const double* __restrict__ S, int s, const int* __restrict__ cptr,
+                                        const int* __restrict__ ridx, const double* __restrict__ cval,
+                                        long long n, double* __restrict__ Y) {
+  const int lane = threadIdx.x & 31;
+  const long long j = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (j >= n) return;
+  for (int i = lane; i < s; i += 32) {
+    double acc = 0.0;
+    for (int p = cptr[j]; p < cptr[j + 1]; ++p) acc += cval[p] * S[static_cast<long long>(ridx[p]) * s + i];
+    Y[j * s + i] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// LUPP pivot order (dense_factor.hpp:119-157), right-looking and exact:
+// one launch per step k applies step k-1's elimination to every unpivoted row
+// (w(r,c) -= (w(r,k-1)/pval) * w(prow,c), skipped when pval or the factor is
+// 0), then elects step k's pivot = max |w(r,k)|, ties to the lowest row index.
+// ---------------------------------------------------------------------------
+struct LuppPivot {
+  double pval;
+  long long prow;
+};
+
+__device__ __forceinline__ bool better(double m1, long long i1, double m2, long long i2) {
+  return m1 > m2 || (m1 == m2 && i1 < i2);
+}
+
+__global__ void __launch_bounds__(kT)
+lupp_step_kernel(double* __restrict__ W, long long ld, long long rows, long long cols, int k,
+                 char* __restrict__ piv, long long* __restrict__ order, double* __restrict__ mags,
+                 LuppPivot* __restrict__ pv, double* __restrict__ pmag, long long* __restrict__ pidx,
+                 unsigned* __restrict__ ctr) {
+  __shared__ double sm[kT / 32];
+  __shared__ long long si[kT / 32];
+  const long long r = static_cast<long long>(blockIdx.x) * kT + threadIdx.x;
+  double best = -1.0;
+  long long bidx = LLONG_MAX;
+  if (r < rows && !piv[r]) {
+    if (k > 0) {
+      const double pval = pv->pval;
+      const long long prow = pv->prow;
+      if (pval != 0.0) {
+        const double f = W[(k - 1) * ld + r] / pval;
+        if (f != 0.0)
+          for (long long c = k; c < cols; ++c) W[c * ld + r] -= f * W[c * ld + prow];
+      }
+    }
+    best = fabs(W[static_cast<long long>(k) * ld + r]);
+    bidx = r;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double om = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (better(om, oi, best, bidx)) {
+      best = om;
+      bidx = oi;
+    }
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sm[w] = best;
+    si[w] = bidx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < kT / 32; ++q)
+      if (better(sm[q], si[q], best, bidx)) {
+        best = sm[q];
+        bidx = si[q];
+      }
+    pmag[blockIdx.x] = best;
+    pidx[blockIdx.x] = bidx;
+  }
+  if (!elect_last_block(ctr, gridDim.x)) return;
+  // final election over block partials (a total order: any tree gives the same winner)
+  best = -1.0;
+  bidx = LLONG_MAX;
+  for (long long q = threadIdx.x; q < gridDim.x; q += kT) {
+    const double om = ((volatile double*)pmag)[q];
+    const long long oi = ((volatile long long*)pidx)[q];
+    if (better(om, oi, best, bidx)) {
+      best = om;
+      bidx = oi;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double om = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (better(om, oi, best, bidx)) {
+      best = om;
+      bidx = oi;
+    }
+  }
+  __syncthreads();
+  if (lane == 0) {
+    sm[w] = best;
+    si[w] = bidx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < kT / 32; ++q)
+      if (better(sm[q], si[q], best, bidx)) {
+        best = sm[q];
+        bidx = si[q];
+      }
+    order[k] = bidx;
+    mags[k] = best;
+    piv[bidx] = 1;
+    pv->prow = bidx;
+    pv->pval = ((volatile double*)W)[static_cast<long long>(k) * ld + bidx];
+  }
+}
+
+// W (n x s column-major) = E^T with rows in J zeroed (cur.hpp:254-261)
+__global__ void transpose_zero_kernel(const double* __restrict__ E, long long s, long long n,
+                                      const int* __restrict__ colsel, double* __restrict__ W) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= s * n) return;
+  const long long c = idx / n, r = idx % n;
+  W[idx] = colsel[r] ? 0.0 : E[r * s + c];
+}
+
+// ---------------------------------------------------------------------------
+// refresh: H = U R (core solve per column, cur.hpp:119-144,175-181) and
+// E^row = Y - Y(:,J) H (cur.hpp:306-312)
+// ---------------------------------------------------------------------------
+__global__ void core_solve_cols_kernel(const double* __restrict__ R, double* __restrict__ H, long long l,
+                                       long long n, int kind, const double* __restrict__ hh,
+                                       const double* __restrict__ fa, const long long* __restrict__ perm) {
+  const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double* y = H + j;  // y[i] at H[i * n + j]
+  if (kind == 0) {
+    for (long long i = 0; i < l; ++i) y[i * n] = R[i * n + j];
+    for (long long t = 0; t < l; ++t) {  // y <- Q^T y (dense_factor.hpp:75-83)
+      const double* v = hh + t * l;
+      double d = 0.0;
+      for (long long i = t; i < l; ++i) d += v[i] * y[i * n];
+      d *= 2.0;
+      for (long long i = t; i < l; ++i) y[i * n] -= d * v[i];
+    }
+    for (long long i = l - 1; i >= 0; --i) {  // back substitution
+      double sacc = y[i * n];
+      for (long long q = i + 1; q < l; ++q) sacc -= fa[q * l + i] * y[q * n];
+      y[i * n] = sacc / fa[i * l + i];
+    }
+  } else {
+    for (long long i = 0; i < l; ++i) y[i * n] = R[perm[i] * n + j];
+    for (long long i = 1; i < l; ++i)
+      for (long long q = 0; q < i; ++q) y[i * n] -= fa[q * l + i] * y[q * n];
+    for (long long i = l - 1; i >= 0; --i) {
+      for (long long q = i + 1; q < l; ++q) y[i * n] -= fa[q * l + i] * y[q * n];
+      y[i * n] /= fa[i * l + i];
+    }
+  }
+}
+
+// lanes over sketch rows i, one warp per column j: E(i,j) = Y(i,j) - sum_t H(t,j) SC(i,t)
+__global__ void eres_kernel(const double* __restrict__ Y, const double* __restrict__ SC,
+                            const double* __restrict__ H, long long s, long long n, long long l,
+                            double* __restrict__ E) {
+  const long long j = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  for (long long i0 = 0; i0 < s; i0 += 32) {
+    const long long i = i0 + lane;
+    double acc = 0.0;
+    for (long long t = 0; t < l; ++t) {
+      const double h = H[t * n + j];
+      if (h == 0.0) continue;
+      if (i < s) acc += h * SC[t * s + i];
+    }
+    if (i < s) E[j * s + i] = Y[j * s + i] - acc;
+  }
+}
+
+// rho probes: out(i, p) = (E w_p)_i with the dense matvec chain (j ascending,
+// zero entries of w skipped), sketch.hpp:219-221 -> matrix.hpp:156-162
+__global__ void probe_kernel(const double* __restrict__ E, long long s, long long n,
+                             const double* __restrict__ W, double* __restrict__ out) {
+  const long long i = static_cast<long long>(blockIdx.x) * 32 + (threadIdx.x & 31);
+  const long long p = blockIdx.y;
+  if (i >= s) return;
+  const double* w = W + p * n;
+  double acc = 0.0;
+  for (long long j = 0; j < n; ++j) {
+    const double x = w[j];
+    if (x == 0.0) continue;
+    acc += x * E[j * s + i];
+  }
+  out[p * s + i] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// gathers
+// ---------------------------------------------------------------------------
+__global__ void gather_block_kernel(const double* A, long long m, const int* ptr, const int* idx,
+                                    const double* val, int sparse, const long long* I, const long long* J,
+                                    long long li, long long lj, double* out) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= li * lj) return;
+  const long long jj = e / li, ii = e % li;
+  out[e] = sparse ? csr_at(ptr, idx, val, I[ii], J[jj]) : A[J[jj] * m + I[ii]];
+}
+
+// rows I[q] of A -> R row-major (q in [0, cnt)), dense source
+__global__ void gather_rows_dense_kernel(const double* A, long long m, long long n, const long long* I,
+                                         long long cnt, double* R) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= cnt * n) return;
+  const long long q = e / n, c = e % n;
+  R[e] = A[c * m + I[q]];
+}
+
+__global__ void scatter_rows_csr_kernel(const int* ptr, const int* idx, const double* val, long long n,
+                                        const long long* I, long long cnt, double* R) {
+  const long long q = blockIdx.x;
+  if (q >= cnt) return;
+  const long long i = I[q];
+  for (int p = ptr[i] + threadIdx.x; p < ptr[i + 1]; p += blockDim.x) R[q * n + idx[p]] = val[p];
+}
+
+// SC = Y(:, J) (s x l column-major)
+__global__ void gather_sc_kernel(const double* Y, long long s, const long long* J, long long l, double* SC) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= s * l) return;
+  const long long t = e / s, i = e % s;
+  SC[e] = Y[J[t] * s + i];
+}
+
+// R(:, J+) from the row-major R (l x b, column-major)
+__global__ void gather_rcols_kernel(const double* R, long long n, long long l, const long long* Jp, long long b,
+                                    double* out) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= l * b) return;
+  const long long jj = e / l, i = e % l;
+  out[e] = R[i * n + Jp[jj]];
+}
+
+// ---------------------------------------------------------------------------
+// E^col = A(:, J+) - C (U R(:, J+)), rows I zeroed (cur.hpp:268-283)
+// ---------------------------------------------------------------------------
+constexpr int kEcolTile = 8;
+
+__global__ void ecol_dense_kernel(const double* __restrict__ A, long long m, const long long* __restrict__ J,
+                                  long long l, const long long* __restrict__ Jp, long long b,
+                                  const double* __restrict__ urj, const int* __restrict__ rowsel,
+                                  double* __restrict__ out) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long jj0 = static_cast<long long>(blockIdx.y) * kEcolTile;
+  if (i >= m) return;
+  double acc[kEcolTile];
+#pragma unroll
+  for (int q = 0; q < kEcolTile; ++q) acc[q] = 0.0;
+  for (long long t = 0; t < l; ++t) {
+    const double c = A[J[t] * m + i];
+#pragma unroll
+    for (int q = 0; q < kEcolTile; ++q) {
+      if (jj0 + q < b) {
+        const double x = urj[(jj0 + q) * l + t];
+        if (x != 0.0) acc[q] += x * c;
+      }
+    }
+  }
+  const bool zero = rowsel[i] != 0;
+#pragma unroll
+  for (int q = 0; q < kEcolTile; ++q) {
+    const long long jj = jj0 + q;
+    if (jj < b) out[jj * m + i] = zero ? 0.0 : A[Jp[jj] * m + i] - acc[q];
+  }
+}
+
+// sparse A: per row i, C(i, :) entries (t ascending) from crow lists
+__global__ void ecol_sparse_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                   const double* __restrict__ val, long long m, const int* __restrict__ cptr,
+                                   const int* __restrict__ ct, const double* __restrict__ cv, long long l,
+                                   const long long* __restrict__ Jp, long long b, const double* __restrict__ urj,
+                                   const int* __restrict__ rowsel, double* __restrict__ out) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const bool zero = rowsel[i] != 0;
+  for (long long jj = 0; jj < b; ++jj) {
+    double v = 0.0;
+    if (!zero) {
+      const double aval = csr_at(ptr, idx, val, i, Jp[jj]);
+      double acc = 0.0;
+      if (l > 0)
+        for (int e = cptr[i]; e < cptr[i + 1]; ++e) {
+          const double x = urj[jj * l + ct[e]];
+          if (x != 0.0) acc += x * cv[e];
+        }
+      v = l > 0 ? aval - acc : aval;
+    }
+    out[jj * m + i] = v;
+  }
+}
+
+// C row lists: entries of CSR(A) row i whose column is in J, as (t = position in J, value), t ascending
+__global__ void crow_count_kernel(const int* ptr, const int* idx, long long m, const int* colpos, int* cnt) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  int c = 0;
+  for (int p = ptr[i]; p < ptr[i + 1]; ++p) c += colpos[idx[p]] >= 0;
+  cnt[i] = c;
+}
+
+__global__ void crow_fill_kernel(const int* ptr, const int* idx, const double* val, long long m, const int* colpos,
+                                 const int* cptr, int* ct, double* cv) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  int q = cptr[i];
+  const int q0 = q;
+  for (int p = ptr[i]; p < ptr[i + 1]; ++p) {
+    const int t = colpos[idx[p]];
+    if (t < 0) continue;
+    // insertion by t (rows hold few entries)
+    int at = q;
+    while (at > q0 && ct[at - 1] > t) {
+      ct[at] = ct[at - 1];
+      cv[at] = cv[at - 1];
+      --at;
+    }
+    ct[at] = t;
+    cv[at] = val[p];
+    ++q;
+  }
+}
+
+__global__ void set_flags_kernel(int* flags, const long long* ids, long long cnt, int value) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < cnt) flags[ids[e]] = value;
+}
+
+__global__ void set_colpos_kernel(int* colpos, const long long* J, long long l) {
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < l) colpos[J[t]] = static_cast<int>(t);
+}
+
+template <class T>
+void upload(apc_ctx* ctx, DBuf<T>& d, const T* h, i64 n) {
+  d.ensure(std::max<i64>(1, n));
+  if (n > 0) APC_CUDA(cudaMemcpyAsync(d.p, h, sizeof(T) * n, cudaMemcpyHostToDevice, ctx->stream));
+}
+
+template <class T>
+std::vector<T> download(apc_ctx* ctx, const T* d, i64 n) {
+  std::vector<T> h(static_cast<size_t>(std::max<i64>(0, n)));
+  if (n > 0) APC_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(T) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  APC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return h;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// device LUPP driver
+// ---------------------------------------------------------------------------
+LuppOut device_lupp(apc_ctx* ctx, double* w, i64 rows, i64 cols, i64 max_pivots) {
+  LuppOut out;
+  i64 steps = std::min(rows, cols);
+  if (max_pivots >= 0) steps = std::min(steps, max_pivots);
+  if (steps <= 0) return out;
+  cudaStream_t st = ctx->stream;
+  const unsigned nbk = nb(rows);
+  DBuf<char> piv(rows);
+  DBuf<long long> order(steps), pidx(nbk);
+  DBuf<double> mags(steps), pmag(nbk);
+  DBuf<LuppPivot> pv(1);
+  DBuf<unsigned> ctr(1);
+  APC_CUDA(cudaMemsetAsync(piv.p, 0, rows, st));
+  APC_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned), st));
+  for (i64 k = 0; k < steps; ++k) {
+    lupp_step_kernel<<<nbk, kT, 0, st>>>(w, rows, rows, cols, static_cast<int>(k), piv.p, order.p, mags.p,
+                                         pv.p, pmag.p, pidx.p, ctr.p);
+  }
+  ctx->launches += static_cast<std::uint64_t>(steps);
+  APC_CUDA(cudaGetLastError());
+  auto o = download(ctx, order.p, steps);
+  out.order.assign(o.begin(), o.end());
+  out.mags = download(ctx, mags.p, steps);
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// DeviceCur
+// ---------------------------------------------------------------------------
+DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 probes, int core_kind,
+                     int sketch_kind, i64 max_rank)
+    : a_(a), ctx_(a.ctx), m_(a.m), n_(a.n), block_size_(block), probes_(probes), max_rank_(max_rank),
+      core_kind_(core_kind), rho_(std::numeric_limits<double>::infinity()),
+      probe_rng_(seed, Stream::probes) {
+  require(block >= 1, APC_INVALID_ARGUMENT, "CurState: block size must be >= 1");
+  require(block <= n_, APC_INVALID_ARGUMENT, "CurState: block size exceeds column count");
+  require(a.r0 == 0 && a.r1 == a.m, APC_NOT_APPLICABLE, "CurState: needs the full matrix on this rank");
+  s_ = static_cast<i64>(std::ceil(1.1 * static_cast<double>(block)));
+  const std::uint64_t emb_seed = splitmix(seed ^ 0x5ce7c3a1b2d4f688ULL);
+  cudaStream_t st = ctx_->stream;
+  Y_.alloc(std::max<i64>(1, s_ * n_));
+  E_.alloc(std::max<i64>(1, s_ * n_));
+  if (sketch_kind == 0) {
+    // SparseSignEmbedding ctor (sketch.hpp:20-50), host RNG, bit-identical
+    const i64 x = std::min(xi, s_);
+    std::vector<int> rows(static_cast<size_t>(m_ * x));
+    std::vector<signed char> sg(static_cast<size_t>(m_ * x));
+    HostRng rng(emb_seed);
+    std::vector<i64> pick(static_cast<size_t>(x));
+    for (i64 c = 0; c < m_; ++c) {
+      size_t cnt = 0;
+      for (i64 t = s_ - x; t < s_; ++t) {
+        const i64 r = static_cast<i64>(rng.below(static_cast<std::uint64_t>(t) + 1));
+        bool dup = false;
+        for (size_t q = 0; q < cnt; ++q)
+          if (pick[q] == r) {
+            dup = true;
+            break;
+          }
+        pick[cnt++] = dup ? t : r;
+      }
+      std::sort(pick.begin(), pick.begin() + static_cast<std::ptrdiff_t>(cnt));
+      for (size_t q = 0; q < cnt; ++q) {
+        rows[c * x + q] = static_cast<int>(pick[q]);
+        sg[c * x + q] = static_cast<signed char>(rng.sign() > 0 ? 1 : -1);
+      }
+    }
+    const double scale = 1.0 / std::sqrt(static_cast<double>(x));
+    DBuf<int> d_rows;
+    DBuf<signed char> d_sg;
+    upload(ctx_, d_rows, rows.data(), m_ * x);
+    upload(ctx_, d_sg, sg.data(), m_ * x);
+    const size_t smem = sizeof(double) * kSketchWarps * s_;
+    if (smem > 48 * 1024) {
+      APC_CUDA(cudaFuncSetAttribute(sketch_ss_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      APC_CUDA(cudaFuncSetAttribute(sketch_ss_csc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
+    const unsigned g = nb(n_, kSketchWarps);
+    if (!a.sparse)
+      sketch_ss_dense_kernel<<<g, kSketchWarps * 32, smem, st>>>(a.dense.p, m_, n_, (int)s_, (int)x, d_rows.p,
+                                                                d_sg.p, scale, 0.0, 0, Y_.p);
+    else
+      sketch_ss_csc_kernel<<<g, kSketchWarps * 32, smem, st>>>(a.at.ptr.p, a.at.idx.p, a.at.val.p, m_, n_, (int)s_,
+                                                              (int)x, d_rows.p, d_sg.p, scale, 0.0, 0, Y_.p);
+    ctx_->launches++;
+    APC_CUDA(cudaStreamSynchronize(st));
+  } else {
+    // GaussianEmbedding (sketch.hpp:173-182): entries scale * gaussian() in storage order
+    std::vector<double> S(static_cast<size_t>(s_ * m_));
+    HostRng rng(emb_seed);
+    const double scale = 1.0 / std::sqrt(static_cast<double>(s_));
+    for (auto& v : S) v = scale * rng.gaussian();
+    DBuf<double> d_S;
+    upload(ctx_, d_S, S.data(), s_ * m_);
+    if (!a.sparse) {
+      dim3 grid(static_cast<unsigned>((n_ + kGT - 1) / kGT), static_cast<unsigned>((s_ + kGT - 1) / kGT));
+      sketch_gauss_dense_kernel<<<grid, 256, 0, st>>>(d_S.p, (int)s_, a.dense.p, m_, n_, Y_.p);
+    } else {
+      sketch_gauss_csc_kernel<<<nb(n_ * 32), kT, 0, st>>>(d_S.p, (int)s_, a.at.ptr.p, a.at.idx.p, a.at.val.p, n_,
+                                                          Y_.p);
+    }
+    ctx_->launches++;
+    APC_CUDA(cudaStreamSynchronize(st));
+  }
+  APC_CUDA(cudaGetLastError());
+  APC_CUDA(cudaMemcpyAsync(E_.p, Y_.p, sizeof(double) * s_ * n_, cudaMemcpyDeviceToDevice, st));
+  // ztol = 1e-14 ||Y||_F (frob_norm: sequential over storage order, cur.hpp:224)
+  std::vector<double> yh = download(ctx_, Y_.p, s_ * n_);
+  double f2 = 0.0;
+  for (double v : yh) f2 += v * v;
+  ztol_ = 1e-14 * std::sqrt(f2);
+  rowsel_.alloc(std::max<i64>(1, m_));
+  colsel_.alloc(std::max<i64>(1, n_));
+  APC_CUDA(cudaMemsetAsync(rowsel_.p, 0, rowsel_.bytes(), st));
+  APC_CUDA(cudaMemsetAsync(colsel_.p, 0, colsel_.bytes(), st));
+}
+
+DeviceCur::~DeviceCur() = default;
+
+void DeviceCur::compute_rho() {
+  // spectral_norm_estimate (sketch.hpp:209-223): probes drawn on the host
+  const i64 r = probes_;
+  std::vector<double> w(static_cast<size_t>(r * n_));
+  for (i64 p = 0; p < r; ++p)
+    for (i64 j = 0; j < n_; ++j) w[p * n_ + j] = probe_rng_.gaussian();
+  DBuf<double> d_w, d_out(std::max<i64>(1, s_ * r));
+  upload(ctx_, d_w, w.data(), r * n_);
+  dim3 grid(static_cast<unsigned>((s_ + 31) / 32), static_cast<unsigned>(r));
+  probe_kernel<<<grid, 32, 0, ctx_->stream>>>(E_.p, s_, n_, d_w.p, d_out.p);
+  ctx_->launches++;
+  std::vector<double> ew = download(ctx_, d_out.p, s_ * r);
+  double best = 0.0;
+  for (i64 p = 0; p < r; ++p) {
+    double nrm2 = 0.0;
+    for (i64 i = 0; i < s_; ++i) nrm2 += ew[p * s_ + i] * ew[p * s_ + i];
+    best = std::max(best, std::sqrt(nrm2));
+  }
+  rho_ = 10.0 * std::sqrt(2.0 / 3.14159265358979323846) * best;
+  rho_hist_.push_back(rho_);
+}
+
+static std::vector<i64> admissible(const LuppOut& piv, i64 cap, double ztol) {  // cur.hpp:341-348
+  std::vector<i64> out;
+  for (size_t k = 0; k < piv.order.size() && static_cast<i64>(out.size()) < cap; ++k) {
+    if (piv.mags[k] <= ztol) break;
+    out.push_back(piv.order[k]);
+  }
+  return out;
+}
+
+AugmentResult DeviceCur::augment() {
+  cudaStream_t st = ctx_->stream;
+  i64 want = block_size_;
+  const i64 room = std::min(m_, n_) - rank();
+  require(room > 0, APC_INVALID_ARGUMENT, "CurState::augment: rank at capacity");
+  want = std::min(want, room);
+
+  // column pivots: LUPP over (E^row with J zeroed)^T  (n x s)
+  work_.ensure(std::max<i64>(1, s_ * n_));
+  transpose_zero_kernel<<<nb(s_ * n_), kT, 0, st>>>(E_.p, s_, n_, colsel_.p, work_.p);
+  ctx_->launches++;
+  LuppOut col_piv = device_lupp(ctx_, work_.p, n_, s_, want);
+  std::vector<i64> jplus = admissible(col_piv, want, ztol_);
+  if (jplus.empty()) {
+    if (rank() == 0) compute_rho();
+    return {0, true};
+  }
+  const i64 b = static_cast<i64>(jplus.size()), l = rank();
+  DBuf<long long> d_jp, d_J;
+  upload(ctx_, d_jp, reinterpret_cast<const long long*>(jplus.data()), b);
+  upload(ctx_, d_J, reinterpret_cast<const long long*>(J_.data()), l);
+
+  // urj = U R(:, J+) on the host (l x b)
+  Vec urj;
+  DBuf<double> d_urj;
+  if (l > 0) {
+    DBuf<double> d_rj(l * b);
+    gather_rcols_kernel<<<nb(l * b), kT, 0, st>>>(Rrm_.p, n_, l, d_jp.p, b, d_rj.p);
+    ctx_->launches++;
+    Vec rj = download(ctx_, d_rj.p, l * b);
+    urj = core_.solve_matrix(b, std::move(rj));
+    upload(ctx_, d_urj, urj.data(), l * b);
+  }
+  // E^col = A(:, J+) - C urj, rows I zeroed (m x b)
+  DBuf<double> ecol(std::max<i64>(1, m_ * b));
+  if (!a_.sparse) {
+    dim3 grid(nb(m_), static_cast<unsigned>((b + kEcolTile - 1) / kEcolTile));
+    ecol_dense_kernel<<<grid, kT, 0, st>>>(a_.dense.p, m_, d_J.p, l, d_jp.p, b, d_urj.p, rowsel_.p, ecol.p);
+    ctx_->launches++;
+  } else {
+    DBuf<int> colpos(n_), ccnt(m_ + 1), cptr(m_ + 1);
+    APC_CUDA(cudaMemsetAsync(colpos.p, 0xff, colpos.bytes(), st));
+    if (l > 0) set_colpos_kernel<<<nb(l), kT, 0, st>>>(colpos.p, d_J.p, l);
+    crow_count_kernel<<<nb(m_), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, m_, colpos.p, ccnt.p);
+    APC_CUDA(cudaMemsetAsync(ccnt.p + m_, 0, sizeof(int), st));
+    size_t tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, ccnt.p, cptr.p, static_cast<int>(m_ + 1), st);
+    DBuf<char> tbuf(static_cast<i64>(tmp));
+    APC_CUDA(cub::DeviceScan::ExclusiveSum(tbuf.p, tmp, ccnt.p, cptr.p, static_cast<int>(m_ + 1), st));
+    int total = 0;
+    APC_CUDA(cudaMemcpyAsync(&total, cptr.p + m_, sizeof(int), cudaMemcpyDeviceToHost, st));
+    APC_CUDA(cudaStreamSynchronize(st));
+    DBuf<int> ct(std::max(1, total));
+    DBuf<double> cv(std::max(1, total));
+    crow_fill_kernel<<<nb(m_), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p, m_, colpos.p, cptr.p, ct.p, cv.p);
+    ecol_sparse_kernel<<<nb(m_), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p, m_, cptr.p, ct.p, cv.p, l,
+                                              d_jp.p, b, d_urj.p, rowsel_.p, ecol.p);
+    ctx_->launches += 4;
+    APC_CUDA(cudaStreamSynchronize(st));
+  }
+  APC_CUDA(cudaGetLastError());
+  LuppOut row_piv = device_lupp(ctx_, ecol.p, m_, b, b);
+  std::vector<i64> iplus = admissible(row_piv, b, ztol_);
+  if (iplus.empty()) return {0, true};
+  const bool exhausted = static_cast<i64>(iplus.size()) < want;
+  jplus.resize(iplus.size());
+  I_.insert(I_.end(), iplus.begin(), iplus.end());
+  J_.insert(J_.end(), jplus.begin(), jplus.end());
+  last_added_ = static_cast<i64>(iplus.size());
+  DBuf<long long> d_ip;
+  upload(ctx_, d_ip, reinterpret_cast<const long long*>(iplus.data()), last_added_);
+  upload(ctx_, d_jp, reinterpret_cast<const long long*>(jplus.data()), last_added_);
+  set_flags_kernel<<<nb(last_added_), kT, 0, st>>>(rowsel_.p, d_ip.p, last_added_, 1);
+  set_flags_kernel<<<nb(last_added_), kT, 0, st>>>(colsel_.p, d_jp.p, last_added_, 1);
+  ctx_->launches += 2;
+  APC_CUDA(cudaStreamSynchronize(st));
+  return {last_added_, exhausted};
+}
+
+void DeviceCur::rollback_last_augment() {
+  require(last_added_ > 0 && last_added_ <= rank(), APC_INVALID_ARGUMENT,
+          "CurState::rollback_last_augment: nothing to roll back");
+  cudaStream_t st = ctx_->stream;
+  std::vector<i64> di(I_.end() - last_added_, I_.end()), dj(J_.end() - last_added_, J_.end());
+  DBuf<long long> d_i, d_j;
+  upload(ctx_, d_i, reinterpret_cast<const long long*>(di.data()), last_added_);
+  upload(ctx_, d_j, reinterpret_cast<const long long*>(dj.data()), last_added_);
+  set_flags_kernel<<<nb(last_added_), kT, 0, st>>>(rowsel_.p, d_i.p, last_added_, 0);
+  set_flags_kernel<<<nb(last_added_), kT, 0, st>>>(colsel_.p, d_j.p, last_added_, 0);
+  ctx_->launches += 2;
+  APC_CUDA(cudaStreamSynchronize(st));
+  I_.resize(I_.size() - last_added_);
+  J_.resize(J_.size() - last_added_);
+  last_added_ = 0;
+}
+
+void DeviceCur::refresh() {
+  require(rank() > 0, APC_INVALID_ARGUMENT, "CurState::refresh: empty index sets");
+  cudaStream_t st = ctx_->stream;
+  const i64 l = rank();
+  DBuf<long long> d_I, d_J;
+  upload(ctx_, d_I, reinterpret_cast<const long long*>(I_.data()), l);
+  upload(ctx_, d_J, reinterpret_cast<const long long*>(J_.data()), l);
+  // intersection block A(I, J) -> host factor
+  DBuf<double> d_blk(l * l);
+  gather_block_kernel<<<nb(l * l), kT, 0, st>>>(a_.dense.p, m_, a_.a.ptr.p, a_.a.idx.p, a_.a.val.p,
+                                                a_.sparse ? 1 : 0, d_I.p, d_J.p, l, l, d_blk.p);
+  ctx_->launches++;
+  block_ = download(ctx_, d_blk.p, l * l);
+  core_ = CoreFactorH::build(l, block_, core_kind_);  // throws singular
+  // R = A(I, :) row-major (all rows re-gathered: I may have changed after a rollback)
+  Rrm_.ensure(l * n_);
+  if (!a_.sparse) {
+    gather_rows_dense_kernel<<<nb(l * n_), kT, 0, st>>>(a_.dense.p, m_, n_, d_I.p, l, Rrm_.p);
+  } else {
+    APC_CUDA(cudaMemsetAsync(Rrm_.p, 0, sizeof(double) * l * n_, st));
+    scatter_rows_csr_kernel<<<static_cast<unsigned>(l), 128, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p, n_,
+                                                                     d_I.p, l, Rrm_.p);
+  }
+  ctx_->launches++;
+  // H = U R (core solve per column)
+  upload_core();
+  H_.ensure(l * n_);
+  core_solve_cols_kernel<<<nb(n_, 128), 128, 0, st>>>(Rrm_.p, H_.p, l, n_, core_kind_, core_h_.p, core_a_.p,
+                                                      core_perm_.p);
+  // E^row = Y - Y(:, J) H
+  DBuf<double> d_sc(s_ * l);
+  gather_sc_kernel<<<nb(s_ * l), kT, 0, st>>>(Y_.p, s_, d_J.p, l, d_sc.p);
+  eres_kernel<<<nb(n_ * 32), kT, 0, st>>>(Y_.p, d_sc.p, H_.p, s_, n_, l, E_.p);
+  ctx_->launches += 3;
+  APC_CUDA(cudaGetLastError());
+  compute_rho();
+}
+
+void DeviceCur::upload_core() {
+  const i64 l = core_.l;
+  if (core_.kind == 0) {
+    upload(ctx_, core_h_, core_.qr.hh.data(), l * l);
+    upload(ctx_, core_a_, core_.qr.a.data(), l * l);
+  } else {
+    upload(ctx_, core_a_, core_.lu.data(), l * l);
+    upload(ctx_, core_perm_, reinterpret_cast<const long long*>(core_.perm.data()), l);
+  }
+}
+
+Vec DeviceCur::r_dense_rows(i64 first, i64 count) const {
+  return download(ctx_, Rrm_.p + first * n_, count * n_);
+}
+
+Vec DeviceCur::c_dense() const {
+  require(!a_.sparse, APC_INVALID_ARGUMENT, "c_dense: dense A only");
+  const i64 l = rank();
+  Vec out(static_cast<size_t>(m_ * l));
+  for (i64 t = 0; t < l; ++t)
+    APC_CUDA(cudaMemcpyAsync(out.data() + t * m_, a_.dense.p + J_[t] * m_, sizeof(double) * m_,
+                             cudaMemcpyDeviceToHost, ctx_->stream));
+  APC_CUDA(cudaStreamSynchronize(ctx_->stream));
+  return out;
+}
+
+namespace {
+// rows `which` of a device CSR as a host CSC-like triple (columns = which order)
+void csr_rows_to_host(apc_ctx* ctx, const Csr& c, const std::vector<i64>& which, std::vector<i64>& ptr,
+                      std::vector<i64>& idx, Vec& val) {
+  ptr.assign(1, 0);
+  idx.clear();
+  val.clear();
+  std::vector<int> hp(2), hi;
+  std::vector<double> hv;
+  for (i64 r : which) {
+    APC_CUDA(cudaMemcpy(hp.data(), c.ptr.p + r, sizeof(int) * 2, cudaMemcpyDeviceToHost));
+    const int len = hp[1] - hp[0];
+    hi.resize(len);
+    hv.resize(len);
+    if (len > 0) {
+      APC_CUDA(cudaMemcpy(hi.data(), c.idx.p + hp[0], sizeof(int) * len, cudaMemcpyDeviceToHost));
+      APC_CUDA(cudaMemcpy(hv.data(), c.val.p + hp[0], sizeof(double) * len, cudaMemcpyDeviceToHost));
+    }
+    for (int q = 0; q < len; ++q) {
+      idx.push_back(hi[q]);
+      val.push_back(hv[q]);
+    }
+    ptr.push_back(static_cast<i64>(idx.size()));
+  }
+}
+}  // namespace
+
+void DeviceCur::c_csc(std::vector<i64>& ptr, std::vector<i64>& idx, Vec& val) const {
+  csr_rows_to_host(ctx_, a_.at, J_, ptr, idx, val);  // CSR(A^T) row j == column j of A
+}
+
+void DeviceCur::rt_csc(std::vector<i64>& ptr, std::vector<i64>& idx, Vec& val) const {
+  csr_rows_to_host(ctx_, a_.a, I_, ptr, idx, val);  // row i of A == column of R^T
+}
+
+}  // namespace apc
+
+// ---------------------------------------------------------------------------
+// C-ABI: CurState stepping and the LUPP pivot order
+// ---------------------------------------------------------------------------
+struct apc_cur {
+  apc::DeviceCur* cur;
+  apc_ctx* ctx;
+};
+
+namespace apc {
+int capi_guard(apc_ctx* ctx, const std::function<void()>& f);
+}
+
+extern "C" {
+
+int apc_cur_create(apc_mat* a, int64_t block, uint64_t seed, int64_t xi, int64_t probe_count, int core_kind,
+                   int sketch_kind, apc_cur** out) {
+  *out = nullptr;
+  return apc::capi_guard(a->ctx, [&] {
+    auto* c = new apc_cur{nullptr, a->ctx};
+    try {
+      c->cur = new apc::DeviceCur(*a, block, seed, xi, probe_count, core_kind, sketch_kind, 0);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int apc_cur_free(apc_cur* c) {
+  if (c) {
+    delete c->cur;
+    delete c;
+  }
+  return APC_OK;
+}
+
+int apc_cur_augment(apc_cur* c, int64_t* added, int* exhausted) {
+  return apc::capi_guard(c->ctx, [&] {
+    apc::AugmentResult r = c->cur->augment();
+    *added = r.added;
+    *exhausted = r.exhausted ? 1 : 0;
+  });
+}
+
+int apc_cur_refresh(apc_cur* c) { return apc::capi_guard(c->ctx, [&] { c->cur->refresh(); }); }
+
+int apc_cur_rollback_last_augment(apc_cur* c) {
+  return apc::capi_guard(c->ctx, [&] { c->cur->rollback_last_augment(); });
+}
+
+int apc_cur_state(const apc_cur* c, int64_t* rank, double* rho, int64_t* sketch_rows, int64_t* n_rho) {
+  if (rank) *rank = c->cur->rank();
+  if (rho) *rho = c->cur->rho();
+  if (sketch_rows) *sketch_rows = c->cur->sketch_rows();
+  if (n_rho) *n_rho = static_cast<int64_t>(c->cur->rho_history().size());
+  return APC_OK;
+}
+
+int apc_cur_indices(const apc_cur* c, int64_t* rows, int64_t* cols) {
+  std::copy(c->cur->rows().begin(), c->cur->rows().end(), rows);
+  std::copy(c->cur->cols().begin(), c->cur->cols().end(), cols);
+  return APC_OK;
+}
+
+int apc_cur_rho_history(const apc_cur* c, double* rho) {
+  std::copy(c->cur->rho_history().begin(), c->cur->rho_history().end(), rho);
+  return APC_OK;
+}
+
+int apc_cur_sketch(const apc_cur* c, double* y) {
+  return apc::capi_guard(c->ctx, [&] {
+    const apc::i64 cnt = c->cur->sketch_rows() * c->cur->n();
+    APC_CUDA(cudaMemcpy(y, c->cur->y_dev(), sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+  });
+}
+
+int apc_cur_residual(const apc_cur* c, double* e) {
+  return apc::capi_guard(c->ctx, [&] {
+    const apc::i64 cnt = c->cur->sketch_rows() * c->cur->n();
+    APC_CUDA(cudaMemcpy(e, c->cur->eres_dev(), sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+  });
+}
+
+int apc_lupp(apc_ctx* ctx, const double* w, int64_t rows, int64_t cols, int64_t max_pivots, int64_t* order,
+             double* mags, int64_t* steps) {
+  return apc::capi_guard(ctx, [&] {
+    apc::DBuf<double> d(std::max<apc::i64>(1, rows * cols));
+    if (rows * cols > 0)
+      APC_CUDA(cudaMemcpy(d.p, w, sizeof(double) * rows * cols, cudaMemcpyHostToDevice));
+    apc::LuppOut o = apc::device_lupp(ctx, d.p, rows, cols, max_pivots);
+    *steps = static_cast<int64_t>(o.order.size());
+    std::copy(o.order.begin(), o.order.end(), order);
+    std::copy(o.mags.begin(), o.mags.end(), mags);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// Device-side incremental CUR (the single-sketch IterativeCUR state,
+// /root/reference/proj/include/aplicur/cur.hpp:200-371).
+//
+// Everything that decides indices runs in exact-order kernels (per-element
+// summation chains in the reference's order, no FMA): the sketch Y = S A,
+// E^row = Y - Y(:,J) U R, E^col = A(:,J+) - C U R(:,J+), the LUPP pivot order
+// and the rho probes.  Only the l x l intersection factor (CoreFactor) and the
+// small U R(:,J+) solve run on the host with the restated reference routines
+// (host_dense.hpp), so I, J and rho_history are bit-identical to the reference.
+#pragma once
+
+#include <vector>
+
+#include "apc_internal.hpp"
+#include "host_dense.hpp"
+#include "host_rng.hpp"
+
+namespace apc {
+
+struct LuppOut {
+  std::vector<i64> order;
+  std::vector<double> mags;
+};
+
+// Pivot order of partial-pivoting elimination on a column-major rows x cols
+// device matrix (destroyed), lu_partial_pivot semantics (dense_factor.hpp:119-157).
+LuppOut device_lupp(apc_ctx* ctx, double* w, i64 rows, i64 cols, i64 max_pivots);
+
+struct AugmentResult {
+  i64 added = 0;
+  bool exhausted = false;
+};
+
+class DeviceCur {
+ public:
+  // target = A (the svd variant, or svd-free with mu == 0)
+  DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 probes, int core_kind,
+            int sketch_kind, i64 max_rank);
+  ~DeviceCur();
+
+  i64 rank() const { return static_cast<i64>(I_.size()); }
+  const std::vector<i64>& rows() const { return I_; }
+  const std::vector<i64>& cols() const { return J_; }
+  double rho() const { return rho_; }
+  const std::vector<double>& rho_history() const { return rho_hist_; }
+  i64 last_added() const { return last_added_; }
+  i64 sketch_rows() const { return s_; }
+  i64 n() const { return n_; }
+  const CoreFactorH& core() const { return core_; }
+  const Vec& intersection() const { return block_; }  // l x l column-major
+  std::uint64_t sketch_applications() const { return 1; }
+
+  AugmentResult augment();   // cur.hpp:248-294
+  void refresh();            // cur.hpp:298-315 (throws Status(APC_SINGULAR) on a singular core)
+  void rollback_last_augment();
+
+  // host copies used by the preconditioner builders
+  Vec r_dense_rows(i64 first, i64 count) const;  // rows I[first..first+count) of A, row-major count x n
+  Vec c_dense() const;                           // dense m x l, column-major (dense A only)
+  // sparse C / R on the host (CSC of C = A(:,J), CSC of R^T = A(I,:)^T)
+  void c_csc(std::vector<i64>& ptr, std::vector<i64>& idx, Vec& val) const;
+  void rt_csc(std::vector<i64>& ptr, std::vector<i64>& idx, Vec& val) const;
+
+  // device views for tests / builders
+  const double* y_dev() const { return Y_.p; }
+  const double* eres_dev() const { return E_.p; }
+  const double* r_rowmajor_dev() const { return Rrm_.p; }
+
+ private:
+  void compute_rho();
+  void upload_core();
+
+  apc_mat& a_;
+  apc_ctx* ctx_;
+  i64 m_, n_, s_, block_size_, probes_, max_rank_;
+  int core_kind_;
+  double ztol_ = 0.0;
+  double rho_;
+  i64 last_added_ = 0;
+  std::vector<i64> I_, J_;
+  std::vector<double> rho_hist_;
+  HostRng probe_rng_;
+  CoreFactorH core_;
+  Vec block_;
+  DBuf<double> Y_, E_;        // s x n column-major
+  DBuf<double> Rrm_;          // R = A(I,:) row-major, capacity max_rank x n
+  DBuf<double> H_;            // U R row-major l x n
+  DBuf<double> core_a_, core_h_;  // factor payload (l x l)
+  DBuf<long long> core_perm_;
+  DBuf<double> work_;         // generic scratch
+  DBuf<int> rowsel_, colsel_;  // flags (rows in I, cols in J)
+};
+
+}  // namespace apc

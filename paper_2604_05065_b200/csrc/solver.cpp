@@ -1,11 +1,237 @@
-// aplicur_solve outer loop (placeholder until the CUR path lands).
+// aplicur_solve on the device: the adaptive outer loop of
+// /root/reference/proj/include/aplicur/solver.hpp:162-392 (Alg. 5.3) driving
+// the device CUR state (cur.cu), the per-rebuild preconditioner construction
+// (precond.cpp) and device-resident warm-started LSQR phases (lsqr.cu).
+#include <chrono>
+#include <cmath>
+#include <limits>
+#include <memory>
+
+#include "cur.hpp"
+#include "precond.hpp"
 #include "solver.hpp"
+#include "vec.hpp"
 
 namespace apc {
 
-apc_result* aplicur_solve(apc_mat& a, const double* b, const apc_solver_config& cfg) {
-  (void)a; (void)b; (void)cfg;
-  fail(APC_NOT_APPLICABLE, "aplicur_solve: CUR path not built yet");
+double host_norm(const double* v, i64 n);
+
+namespace {
+
+using clock_t_ = std::chrono::steady_clock;
+double ms_since(clock_t_::time_point t0) {
+  return std::chrono::duration<double, std::milli>(clock_t_::now() - t0).count();
+}
+
+// reprecondition_check (solver.hpp:68-72)
+bool reprecondition_check(double d_cur, double rho, double eps_cur, double nu_prec) {
+  if (rho <= eps_cur) return true;
+  if (std::isinf(d_cur)) return true;
+  return d_cur / (rho - eps_cur) >= nu_prec;
+}
+
+bool is_solver_error(const Status& s) { return s.code >= 1 && s.code <= 9; }
+
+}  // namespace
+
+apc_result* aplicur_solve(apc_mat& a, const double* b, const apc_solver_config& cfg_in) {
+  auto t_start = clock_t_::now();
+  const i64 n = a.n, m = a.m;
+  apc_solver_config cfg = resolve_config(cfg_in, n);
+  require(cfg.block <= n, APC_INVALID_ARGUMENT, "aplicur_solve: block > cols");
+  const double mu = cfg.mu;
+  apc_ctx* ctx = a.ctx;
+  cudaStream_t st = ctx->stream;
+  const double bnorm = host_norm(b, m);
+  require(std::isfinite(bnorm), APC_INVALID_ARGUMENT, "aplicur_solve: non-finite right-hand side");
+  require(!(cfg.variant == 1 && mu > 0.0), APC_NOT_APPLICABLE,
+          "aplicur_solve: svd-free with mu > 0 (augmented CUR target) is not built on the device yet");
+
+  DeviceCur cur(a, cfg.block, cfg.seed, cfg.sketch_xi, cfg.probe_count, cfg.core, cfg.sketch_kind,
+                cfg.max_rank);
+  i64 max_rank = std::min(m, n);
+  if (cfg.max_rank > 0) max_rank = std::min(max_rank, cfg.max_rank);
+  const double density = (m * n == 0) ? 0.0 : static_cast<double>(a.nnz_global) / static_cast<double>(m * n);
+  const bool implicit_mode = a.sparse && density < 0.10;
+
+  QrAcc qr_acc;
+  Vec t_r_implicit;
+  auto* res = new apc_result();
+  std::unique_ptr<apc_result> guard(res);
+  res->n = n;
+  const i64 mloc = a.mloc();
+  const i64 ulen = mloc + (mu > 0.0 ? n : 0);
+  DBuf<double> d_x(std::max<i64>(1, n)), d_y(std::max<i64>(1, n)), d_dx(std::max<i64>(1, n));
+  DBuf<double> d_b(std::max<i64>(1, mloc)), d_rhs(std::max<i64>(1, ulen));
+  APC_CUDA(cudaMemsetAsync(d_x.p, 0, d_x.bytes(), st));
+  if (mloc > 0) APC_CUDA(cudaMemcpyAsync(d_b.p, b + a.r0, sizeof(double) * mloc, cudaMemcpyHostToDevice, st));
+  VecWork vw(a, mu);
+  LsqrWork* work = lsqr_work_create(a, mu);
+  std::unique_ptr<LsqrWork, void (*)(LsqrWork*)> work_guard(work, lsqr_work_destroy);
+
+  double d_cur = std::numeric_limits<double>::infinity();
+  int phase = 0;
+  bool done = false;
+  std::uint64_t matvecs = 0;
+
+  auto run_phase = [&](PrecondDev& P, bool final_phase, double rho_at_build, apc_phase_report& rep,
+                       const PrecondInfo& info) {
+    auto t0 = clock_t_::now();
+    residual(a, vw, d_x.p, d_b.p, d_rhs.p);  // rhs = b_aug - A_mu x (solver.hpp:207-210)
+    matvecs += 1;
+    StopCfg stop;
+    stop.eps_lsqr = cfg.eps_lsqr;
+    stop.nu_lsqr = final_phase ? std::numeric_limits<double>::infinity() : cfg.nu_lsqr;
+    stop.max_iters = cfg.lsqr_cap > 0 ? cfg.lsqr_cap : 4 * n;
+    stop.sigma_floor = info.sigma_floor;
+    PhaseOut po;
+    lsqr_phase(work, a, mu, &P, d_rhs.p, stop, phase, d_y.p, po);
+    matvecs += po.iters > 0 ? 1 + 2 * static_cast<std::uint64_t>(po.iters) : (po.reason == 5 ? 0 : 1);
+    precond_apply(ctx, P, false, d_y.p, d_dx.p);  // x += P^{-1} y (solver.hpp:238-240)
+    axpy(ctx, d_x.p, d_dx.p, n);
+    for (const auto& row : po.rows)
+      res->trace.push_back(apc_trace_row{phase, 0, row.iter, row.phibar, row.cvgrate, row.cvgdiff, row.matvecs,
+                                         row.wall_ms, std::numeric_limits<double>::quiet_NaN()});
+    res->last_reason = po.reason;
+    rep.phase = phase;
+    rep.mu = mu;
+    rep.rho = rho_at_build;
+    rep.sigma_hat = info.sigma_hat;
+    rep.rank = P.kind == 0 ? 0 : P.l;
+    rep.lsqr_iters = po.iters;
+    rep.reason = po.reason;
+    rep.t_lsqr_ms = ms_since(t0);
+    res->lsqr_ms += po.ms;
+    rep.relres_at_end = bnorm > 0.0 ? std::sqrt(residual(a, vw, d_x.p, d_b.p, nullptr)) / bnorm : 0.0;
+  };
+
+  for (i64 outer = 0; outer < cfg.outer_cap && !done; ++outer) {
+    apc_phase_report rep{};
+    bool final_phase = false;
+    auto t_aug0 = clock_t_::now();
+    bool grew = false;
+    if (cur.rank() < max_rank) {
+      AugmentResult out = cur.augment();
+      if (out.added > 0) {
+        try {
+          cur.refresh();
+          grew = true;
+        } catch (const Status& e) {
+          if (e.code != APC_SINGULAR) throw;
+          cur.rollback_last_augment();
+          res->status = 1;
+          final_phase = true;
+          done = true;
+        }
+      } else {
+        res->status = 1;
+        final_phase = true;
+        done = true;
+      }
+    } else {
+      if (cur.rho() > cfg.eps_cur) res->status = 1;
+      final_phase = true;
+      done = true;
+    }
+    rep.t_augment_ms = ms_since(t_aug0);
+
+    auto t_fac0 = clock_t_::now();
+    if (grew) {
+      const i64 l = cur.rank();
+      if (implicit_mode) {
+        // T_R with T_R^T T_R = R R^T (the reference maintains it with
+        // CholGramAccumulator; the from-scratch gram_factor is the same factor)
+        std::vector<i64> rp, ri;
+        Vec rv;
+        cur.rt_csc(rp, ri, rv);
+        t_r_implicit = gram_factor_sparse(n, l, rp, ri, rv);
+      } else {
+        const i64 added = cur.last_added();
+        Vec newblock = cur.r_dense_rows(l - added, added);  // row-major added x n == column-major n x added
+        try {
+          qr_acc.append(n, added, std::move(newblock));
+        } catch (const Status& e) {
+          if (!is_solver_error(e)) throw;
+          qr_acc.clear();
+          qr_acc.append(n, l, cur.r_dense_rows(0, l));  // full refactorisation
+        }
+      }
+      if (cur.rank() >= max_rank) {
+        final_phase = true;
+        done = true;
+        if (cur.rho() > cfg.eps_cur) res->status = 1;
+      }
+    }
+    rep.t_factor_ms = ms_since(t_fac0);
+
+    const double rho = cur.rho();
+    if (rho <= cfg.eps_cur) {
+      final_phase = true;
+      done = true;
+      res->status = 0;
+    }
+    const bool trigger = final_phase || reprecondition_check(d_cur, rho, cfg.eps_cur, cfg.nu_prec);
+    if (trigger && cur.rank() > 0) {
+      if (!res->phases.empty() && res->phases.back().rank == cur.rank()) break;  // duplicate rank
+      ++phase;
+      auto t_pre0 = clock_t_::now();
+      PrecondDev P;
+      PrecondInfo info;
+      try {
+        BuildInputs in;
+        in.ctx = ctx;
+        in.variant = cfg.variant;
+        in.implicit = implicit_mode;
+        in.m = m;
+        in.n = n;
+        in.l = cur.rank();
+        in.mu = mu;
+        in.target_level = rho;
+        in.core = &cur.core();
+        in.block = &cur.intersection();
+        in.t_r = implicit_mode ? &t_r_implicit : &qr_acc.t;
+        in.q_r = &qr_acc.q;
+        in.c_sparse = a.sparse;
+        if (a.sparse) cur.c_csc(in.c_ptr, in.c_idx, in.c_val);
+        else in.c_dense = cur.c_dense();
+        if (implicit_mode) cur.rt_csc(in.r_ptr, in.r_idx, in.r_val);
+        build_precond(in, P, info);
+      } catch (const Status& e) {
+        if (!is_solver_error(e)) throw;
+        res->status = 2;
+        --phase;
+        break;
+      }
+      rep.t_precond_ms = ms_since(t_pre0);
+      run_phase(P, final_phase, rho, rep, info);
+      if (std::isfinite(rho)) d_cur = rho - cfg.eps_cur;
+      res->phases.push_back(rep);
+    }
+  }
+
+  if (res->phases.empty()) {  // identity-preconditioned phase (solver.hpp:376-383)
+    ++phase;
+    apc_phase_report rep{};
+    PrecondDev ident;
+    ident.n = n;
+    PrecondInfo info;
+    run_phase(ident, true, cur.rho(), rep, info);
+    res->phases.push_back(rep);
+  }
+
+  res->x.resize(static_cast<size_t>(n));
+  APC_CUDA(cudaMemcpy(res->x.data(), d_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  res->final_rho = cur.rho();
+  res->final_relres = bnorm > 0.0 ? std::sqrt(residual(a, vw, d_x.p, d_b.p, nullptr)) / bnorm : 0.0;
+  res->sketch_applications = cur.sketch_applications();
+  res->system_matvecs = matvecs;
+  res->rows.assign(cur.rows().begin(), cur.rows().end());
+  res->cols.assign(cur.cols().begin(), cur.cols().end());
+  res->rho_history = cur.rho_history();
+  res->total_ms = ms_since(t_start);
+  res->setup_ms = res->total_ms - res->lsqr_ms;
+  guard.release();
+  return res;
 }
 
 }  // namespace apc

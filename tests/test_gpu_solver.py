@@ -1,0 +1,65 @@
+"""End-to-end aplicur_solve on the device against the reference solver
+(solver.hpp:162-392): CUR indices and rho history bit-identical, phase
+structure and iteration counts within 5%, x within 1e-6 relative."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _solve_both(apc, ref, ctx, p, **cfg):
+    A = apc.DeviceMatrix.from_problem(ctx, p)
+    g = apc.aplicur_solve(A, p.b, apc.SolverConfig(**cfg))
+    r = ref.solve(ref.Problem.from_apc(p), p.b, dict(cfg, trace_sample_stride=0))
+    return g, r
+
+
+CASES = [
+    # cfg, m, n, solver knobs
+    (1, 400, 50, dict(mu=0.0, eps_lsqr=1e-8, block=5, seed=1)),
+    (1, 4000, 500, dict(mu=0.0, eps_lsqr=1e-8, block=20, seed=1, max_rank=100)),
+    (2, 20000, 2000, dict(mu=1e-6, eps_lsqr=1e-8, block=20, seed=1, max_rank=60)),
+    (2, 4000, 400, dict(mu=1e-3, eps_lsqr=1e-10, block=8, seed=3, max_rank=40)),
+    (3, 3000, 300, dict(mu=1e-4, eps_lsqr=1e-8, block=10, seed=1, max_rank=60)),
+    (1, 400, 50, dict(mu=0.0, eps_lsqr=1e-8, block=5, seed=1, variant=1)),
+    (2, 4000, 400, dict(mu=0.0, eps_lsqr=1e-10, block=8, seed=3, max_rank=40, variant=1)),
+    (1, 600, 60, dict(mu=0.0, eps_lsqr=1e-8, block=6, seed=2, core=1)),
+]
+
+
+@pytest.mark.parametrize("cfg,m,n,knobs", CASES)
+def test_aplicur_solve_matches_reference(apc, ref, ctx, cfg, m, n, knobs):
+    p = apc.Problem(cfg, m, n)
+    g, r = _solve_both(apc, ref, ctx, p, **knobs)
+    # CUR indices and rho history: bit-exact
+    assert np.array_equal(g.row_indices, r.row_indices)
+    assert np.array_equal(g.col_indices, r.col_indices)
+    assert np.array_equal(g.rho_history.view(np.uint64), r.rho_history.view(np.uint64))
+    assert g.sketch_applications == r.sketch_applications == 1
+    assert int(g.status) == r.status
+    # phase structure: same rebuild ranks; iteration counts within 5%
+    assert [ph.rank for ph in g.phases] == list(r.phase_rank)
+    it_g, it_r = g.lsqr_iters, int(r.phase_iters.sum())
+    assert abs(it_g - it_r) <= max(3, 0.05 * it_r), (it_g, it_r, [ph.lsqr_iters for ph in g.phases], r.phase_iters)
+    # solution
+    rel = np.linalg.norm(g.x - r.x) / max(np.linalg.norm(r.x), 1e-300)
+    assert rel <= 1e-6 or abs(g.final_relres - r.final_relres) <= 1e-9 * r.final_relres, (rel, g.final_relres, r.final_relres)
+
+
+def test_zero_matrix_single_identity_phase(apc, ctx):
+    A = apc.DeviceMatrix.dense(ctx, np.zeros(20 * 6), 20, 6)
+    b = np.random.default_rng(2).standard_normal(20)
+    g = apc.aplicur_solve(A, b, apc.SolverConfig(block=2))
+    assert len(g.phases) == 1 and g.phases[0].rank == 0
+    assert np.all(g.x == 0.0)
+
+
+def test_bit_identical_reruns(apc, ctx):
+    p = apc.Problem(2, 4000, 400)
+    A = apc.DeviceMatrix.from_problem(ctx, p)
+    cfg = apc.SolverConfig(mu=1e-3, eps_lsqr=1e-10, block=8, seed=3, max_rank=40)
+    g1 = apc.aplicur_solve(A, p.b, cfg)
+    g2 = apc.aplicur_solve(A, p.b, cfg)
+    assert np.array_equal(g1.x, g2.x)
+    assert np.array_equal(g1.trace["phibar"], g2.trace["phibar"])
+    assert np.array_equal(g1.row_indices, g2.row_indices)
