@@ -1,0 +1,110 @@
+"""ORACLE / TEST INFRASTRUCTURE ONLY -- generates tests/golden/ fixtures by
+running the unmodified reference (oracle/_ref, built from /root/reference) on
+the seeded BASELINE inputs.  Run here (where /root/reference exists):
+
+    python oracle/make_golden.py small      # seconds: CPU-test fixtures
+    python oracle/make_golden.py c1 c2      # full BASELINE C1 / C2 solves (C2 ~ 10 min)
+
+The fixtures are small .npz files (indices, rho history, phase iterations,
+x, residuals, trace heads) so tests on the GPU box never need /root/reference.
+"""
+from __future__ import annotations
+
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import paper_2604_05065_b200 as apc  # noqa: E402  (host-side generator only)
+from oracle import ref  # noqa: E402
+
+GOLD = ROOT / "tests" / "golden"
+
+# the solver settings each config is run with
+BASELINE_SOLVER = {
+    1: dict(mu=0.0, block=20, eps_lsqr=1e-8, seed=1),
+    2: dict(mu=1e-6, block=50, eps_lsqr=1e-8, max_rank=200, seed=1),
+    3: dict(mu=1e-4, block=100, eps_lsqr=1e-8, eps_cur=3e-3, max_rank=1000, seed=1),
+    4: dict(mu=0.0, block=250, eps_lsqr=1e-10, max_rank=250, seed=1),
+    5: dict(mu=1e-8, block=250, eps_lsqr=1e-8, eps_cur=3e-7, max_rank=500, seed=1),
+}
+
+
+def _save(name: str, **arrays):
+    GOLD.mkdir(parents=True, exist_ok=True)
+    np.savez_compressed(GOLD / f"{name}.npz", **arrays)
+    print("wrote", GOLD / f"{name}.npz", flush=True)
+
+
+def solve_fixture(name, cfgid, m, n, knobs, plain=False):
+    p = apc.Problem(cfgid, m, n)
+    rp = ref.Problem.from_apc(p)
+    t0 = time.time()
+    r = ref.solve(rp, p.b, dict(knobs, trace_sample_stride=0), plain=plain)
+    wall = time.time() - t0
+    _save(name, x=r.x, status=r.status, final_rho=r.final_rho, final_relres=r.final_relres,
+          system_matvecs=r.system_matvecs, row_indices=r.row_indices, col_indices=r.col_indices,
+          rho_history=r.rho_history, phase_rank=r.phase_rank, phase_iters=r.phase_iters,
+          phase_reason=r.phase_reason, phase_rho=r.phase_rho, phase_relres=r.phase_relres,
+          phase_t_lsqr_ms=r.phase_t_lsqr_ms, phase_t_total_ms=r.phase_t_total_ms,
+          trace_phibar_head=r.trace_phibar[:64], wall_s=wall,
+          meta=json.dumps(dict(config=cfgid, m=m, n=n, knobs=knobs, plain=plain)))
+    return r, wall
+
+
+def small():
+    # reference known answers used by the CPU suite (port pinning) and GPU tests
+    rng = np.random.default_rng(20260415)
+    # RNG streams
+    _save("rng", u64=ref.rng(20260416, 0, 256, stream=3, index=9), gauss=ref.rng(20260416, 2, 256, stream=2),
+          below=ref.rng(7, 3, 256, bound=1000003), mix=np.array([ref.mix64(x) for x in (0, 1, 12345)], np.uint64))
+    # sparse-sign embedding and sketches
+    rows, signs, scale = ref.sparse_sign(11, 300, 8, ref.mix64(1 ^ 0x5CE7C3A1B2D4F688))
+    A = rng.standard_normal((300, 40))
+    A[rng.random(A.shape) < 0.5] = 0.0
+    Y = ref.sketch_sparse_sign(ref.Problem.from_numpy(A), 11, 8, ref.mix64(1 ^ 0x5CE7C3A1B2D4F688))
+    Ys = ref.sketch_sparse_sign(ref.Problem.from_numpy(A, sparse=True), 11, 8, 99)
+    Ya = ref.sketch_sparse_sign(ref.Problem.from_numpy(A), 11, 8, 5, mu=0.25, augmented=True)
+    _save("sketch", rows=rows, signs=signs, scale=scale, A=A, Y=Y, Ys=Ys, Ya=Ya)
+    # LUPP known answers (ties, zero columns, random)
+    cases = {}
+    for k, W in enumerate([rng.standard_normal((50, 12)), np.ones((6, 4)), np.zeros((5, 3)),
+                           np.where(rng.random((40, 9)) < 0.4, 0.0, rng.standard_normal((40, 9)))]):
+        o, mg = ref.lupp(W, -1)
+        cases[f"W{k}"], cases[f"o{k}"], cases[f"m{k}"] = W, o, mg
+    _save("lupp", **cases)
+    # matvec known answers (dense, CSC, augmented)
+    x = rng.standard_normal(40)
+    u = rng.standard_normal(340)
+    rp, rs = ref.Problem.from_numpy(A), ref.Problem.from_numpy(A, sparse=True)
+    _save("matvec", A=A, x=x, u=u, y=ref.matvec(rp, x), ys=ref.matvec(rs, x), g=ref.matvec(rp, u[:300], transpose=True),
+          gs=ref.matvec(rs, u[:300], transpose=True), ya=ref.matvec(rp, x, 0.3, True),
+          ga=ref.matvec(rs, u, 0.3, True, True))
+    # LSQR and full solves on small BASELINE-shaped inputs
+    solve_fixture("plain_c2_small", 2, 3000, 300, dict(mu=1e-3, eps_lsqr=1e-10, lsqr_cap=300), plain=True)
+    solve_fixture("solve_c1_small", 1, 400, 50, dict(mu=0.0, eps_lsqr=1e-8, block=5, seed=1))
+    solve_fixture("solve_c2_small", 2, 4000, 400, dict(mu=1e-3, eps_lsqr=1e-10, block=8, seed=3, max_rank=40))
+    cur = ref.cur_steps(ref.Problem.from_apc(apc.Problem(2, 3000, 300)), 7, 7, 6)
+    _save("cur_c2_small", I=cur["I"], J=cur["J"], rho=cur["rho"], added=cur["added"])
+
+
+def main(argv):
+    if not ref.available():
+        ref.build()
+    for what in argv or ["small"]:
+        if what == "small":
+            small()
+        elif what.startswith("c") and what[1:].isdigit():
+            k = int(what[1:])
+            r, wall = solve_fixture(f"baseline_c{k}", k, 0, 0, BASELINE_SOLVER[k])
+            print(f"C{k}: wall {wall:.1f}s status {r.status} rank {len(r.row_indices)} iters {r.phase_iters} "
+                  f"relres {r.final_relres}", flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

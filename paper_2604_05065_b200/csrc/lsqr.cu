@@ -611,6 +611,8 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   const bool use_while = ctx->nranks == 1;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  const std::uint64_t launches_before_capture = ctx->launches;
+  std::uint64_t per_iter = 0;
   if (use_while) {
     APC_CUDA(cudaGraphCreate(&graph, 0));
     cudaGraphConditionalHandle cond;
@@ -626,6 +628,7 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
     APC_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeThreadLocal));
     enqueue_iteration(w, a, p, P, cond, 1);
+    per_iter = ctx->launches - launches_before_capture;
     APC_CUDA(cudaStreamEndCapture(st, &body));
     APC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     // skip the loop entirely if initialisation already stopped
@@ -636,6 +639,7 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
     constexpr int kBatch = 8;
     APC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     for (int k = 0; k < kBatch; ++k) enqueue_iteration(w, a, p, P, cudaGraphConditionalHandle{}, 0);
+    per_iter = (ctx->launches - launches_before_capture) / kBatch;
     APC_CUDA(cudaStreamEndCapture(st, &graph));
     APC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     for (long long launch = 0;; ++launch) {
@@ -659,6 +663,8 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   const LsqrState& f = w->hst[0];
   out.breakdown = f.breakdown != 0;
   out.iters = f.iter < 0 ? 0 : f.iter;
+  // count executed (graph-replayed) kernels, not captured ones
+  ctx->launches = launches_before_capture + per_iter * static_cast<std::uint64_t>(out.iters);
   out.reason = f.reason;
   const long long nrows = out.iters + 1;
   out.rows.resize(static_cast<size_t>(nrows));

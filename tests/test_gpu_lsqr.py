@@ -78,7 +78,9 @@ def test_plain_lsqr_ill_conditioned_configs(apc, ref, ctx, cfg, m, n, mu, eps, c
     assert g.phases[0].reason == r.phase_reason[0]
     assert abs(it_g - it_r) <= max(2, 0.05 * it_r), (it_g, it_r)
     np.testing.assert_allclose(g.trace["phibar"][:5], r.trace_phibar[:5], rtol=1e-9)
-    assert abs(g.final_relres - r.final_relres) <= 1e-3 * r.final_relres
+    # converged phases reach the same residual level; capped ones are path-dependent
+    tol = 1e-6 if r.phase_reason[0] == apc.StopReason.gradient_tol else 1e-2
+    assert abs(g.final_relres - r.final_relres) <= tol * r.final_relres
 
 
 def test_counts_and_cap(apc, ref, ctx):
