@@ -17,6 +17,7 @@ import ctypes as C
 import dataclasses
 import enum
 import os
+import weakref
 from pathlib import Path
 from typing import Optional
 
@@ -213,6 +214,7 @@ class Context:
         _check(lib.apc_ctx_create(device, nranks, rank, uid, C.byref(h)))
         self.h = h
         self.device, self.nranks, self.rank = device, nranks, rank
+        self._children = weakref.WeakSet()  # device objects freed before the ctx
 
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -233,6 +235,8 @@ class Context:
 
     def close(self) -> None:
         if getattr(self, "h", None):
+            for c in list(self._children):
+                c.close()
             load_library().apc_ctx_destroy(self.h)
             self.h = None
 
@@ -249,6 +253,7 @@ class DeviceMatrix:
     def __init__(self, ctx: Context, h, m: int, n: int, sparse: bool, r0: int, r1: int, keep=None):
         self.ctx, self.h, self.m, self.n, self.sparse, self.r0, self.r1 = ctx, h, m, n, sparse, r0, r1
         self._keep = keep
+        ctx._children.add(self)
 
     @classmethod
     def dense(cls, ctx: Context, a_colmajor: np.ndarray, m: int, n: int, r0: int = 0,
@@ -304,8 +309,11 @@ class DeviceMatrix:
 
     def free(self) -> None:
         if getattr(self, "h", None):
-            load_library().apc_mat_free(self.h)
+            if getattr(self.ctx, "h", None):  # a closed ctx already freed it
+                load_library().apc_mat_free(self.h)
             self.h = None
+
+    close = free
 
     def __del__(self):
         try:
@@ -324,6 +332,7 @@ class CurState:
         _check(load_library().apc_cur_create(mat.h, block, seed, xi, probe_count, int(core), int(sketch),
                                              C.byref(h)))
         self.h, self.mat = h, mat
+        mat.ctx._children.add(self)
 
     def augment(self):
         added, ex = _i64(), C.c_int()
@@ -372,7 +381,8 @@ class CurState:
 
     def close(self):
         if getattr(self, "h", None):
-            load_library().apc_cur_free(self.h)
+            if getattr(self.mat.ctx, "h", None):
+                load_library().apc_cur_free(self.h)
             self.h = None
 
     def __del__(self):

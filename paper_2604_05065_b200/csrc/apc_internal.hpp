@@ -36,6 +36,22 @@ inline void require(bool cond, int code, const std::string& what, i64 idx = -1) 
 void cuda_check(cudaError_t e, const char* what);
 #define APC_CUDA(call) ::apc::cuda_check((call), #call)
 
+// Caching device allocator (per device, size-class free lists): the CUR and
+// LSQR setup paths allocate many short-lived buffers; cudaMalloc/cudaFree
+// (which synchronises the device) would dominate their wall time.
+void* pool_alloc(size_t bytes);
+void pool_free(void* p, size_t bytes);
+void pool_trim();  // return every cached block to the driver
+
+// Blocking copy ordered on the library stream (the ctx stream is created
+// non-blocking, so plain cudaMemcpy on the legacy stream would not order
+// against its kernels).
+inline void copy_sync(cudaStream_t st, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  if (bytes == 0) return;
+  APC_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, st));
+  APC_CUDA(cudaStreamSynchronize(st));
+}
+
 // ---------------------------------------------------------------------------
 // Device buffers
 // ---------------------------------------------------------------------------
@@ -55,13 +71,13 @@ struct DBuf {
   ~DBuf() { release(); }
   void alloc(i64 count) {
     release();
+    if (count > 0) p = static_cast<T*>(pool_alloc(sizeof(T) * static_cast<size_t>(count)));
     n = count;
-    if (count > 0) APC_CUDA(cudaMalloc(&p, sizeof(T) * static_cast<size_t>(count)));
   }
   // grow-only reallocation (contents discarded)
   void ensure(i64 count) { if (count > n) alloc(count); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) pool_free(p, sizeof(T) * static_cast<size_t>(n));
     p = nullptr;
     n = 0;
   }

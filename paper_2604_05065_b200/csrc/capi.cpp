@@ -5,7 +5,10 @@
 #include <algorithm>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "apc_internal.hpp"
 #include "host_rng.hpp"
@@ -22,6 +25,59 @@ void cuda_check(cudaError_t e, const char* what) {
     cudaGetLastError();
     fail(APC_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
   }
+}
+
+// ---- caching device allocator ---------------------------------------------
+namespace {
+std::mutex g_pool_mu;
+std::map<std::pair<int, size_t>, std::vector<void*>> g_pool;  // (device, class) -> blocks
+
+size_t size_class(size_t bytes) {
+  if (bytes <= 512) return 512;
+  if (bytes >= (size_t{256} << 20)) return (bytes + 0xFFFFF) & ~size_t{0xFFFFF};  // 1 MB granules
+  size_t c = 512;
+  while (c < bytes) c <<= 1;
+  return c;
+}
+}  // namespace
+
+void* pool_alloc(size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const size_t c = size_class(bytes);
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto it = g_pool.find({dev, c});
+    if (it != g_pool.end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, c);
+  if (e != cudaSuccess) {  // give cached blocks back and retry once
+    cudaGetLastError();
+    pool_trim();
+    APC_CUDA(cudaMalloc(&p, c));
+  }
+  return p;
+}
+
+void pool_free(void* p, size_t bytes) {
+  if (!p) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  g_pool[{dev, size_class(bytes)}].push_back(p);
+}
+
+void pool_trim() {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  cudaDeviceSynchronize();
+  for (auto& kv : g_pool)
+    for (void* p : kv.second) cudaFree(p);
+  g_pool.clear();
 }
 
 namespace {
@@ -121,6 +177,7 @@ int apc_ctx_destroy(apc_ctx* ctx) {
     ctx->counters.release();
     cudaStreamDestroy(ctx->stream);
     delete ctx;
+    pool_trim();
   });
 }
 

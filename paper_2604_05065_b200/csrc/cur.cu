@@ -364,10 +364,19 @@ __global__ void probe_kernel(const double* __restrict__ E, long long s, long lon
   if (i >= s) return;
   const double* w = W + p * n;
   double acc = 0.0;
-  for (long long j = 0; j < n; ++j) {
-    const double x = w[j];
-    if (x == 0.0) continue;
-    acc += x * E[j * s + i];
+  // loads hoisted 16 at a time; the add chain keeps the reference's j order
+  constexpr int U = 16;
+  for (long long j0 = 0; j0 < n; j0 += U) {
+    double xs[U], es[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const long long j = j0 + q;
+      xs[q] = j < n ? w[j] : 0.0;
+      es[q] = j < n ? E[j * s + i] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q)
+      if (xs[q] != 0.0) acc += xs[q] * es[q];
   }
   out[p * s + i] = acc;
 }
@@ -856,13 +865,13 @@ void csr_rows_to_host(apc_ctx* ctx, const Csr& c, const std::vector<i64>& which,
   std::vector<int> hp(2), hi;
   std::vector<double> hv;
   for (i64 r : which) {
-    APC_CUDA(cudaMemcpy(hp.data(), c.ptr.p + r, sizeof(int) * 2, cudaMemcpyDeviceToHost));
+    copy_sync(ctx->stream, hp.data(), c.ptr.p + r, sizeof(int) * 2, cudaMemcpyDeviceToHost);
     const int len = hp[1] - hp[0];
     hi.resize(len);
     hv.resize(len);
     if (len > 0) {
-      APC_CUDA(cudaMemcpy(hi.data(), c.idx.p + hp[0], sizeof(int) * len, cudaMemcpyDeviceToHost));
-      APC_CUDA(cudaMemcpy(hv.data(), c.val.p + hp[0], sizeof(double) * len, cudaMemcpyDeviceToHost));
+      APC_CUDA(cudaMemcpyAsync(hi.data(), c.idx.p + hp[0], sizeof(int) * len, cudaMemcpyDeviceToHost, ctx->stream));
+      copy_sync(ctx->stream, hv.data(), c.val.p + hp[0], sizeof(double) * len, cudaMemcpyDeviceToHost);
     }
     for (int q = 0; q < len; ++q) {
       idx.push_back(hi[q]);
@@ -956,14 +965,14 @@ int apc_cur_rho_history(const apc_cur* c, double* rho) {
 int apc_cur_sketch(const apc_cur* c, double* y) {
   return apc::capi_guard(c->ctx, [&] {
     const apc::i64 cnt = c->cur->sketch_rows() * c->cur->n();
-    APC_CUDA(cudaMemcpy(y, c->cur->y_dev(), sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+    apc::copy_sync(c->ctx->stream, y, c->cur->y_dev(), sizeof(double) * cnt, cudaMemcpyDeviceToHost);
   });
 }
 
 int apc_cur_residual(const apc_cur* c, double* e) {
   return apc::capi_guard(c->ctx, [&] {
     const apc::i64 cnt = c->cur->sketch_rows() * c->cur->n();
-    APC_CUDA(cudaMemcpy(e, c->cur->eres_dev(), sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+    apc::copy_sync(c->ctx->stream, e, c->cur->eres_dev(), sizeof(double) * cnt, cudaMemcpyDeviceToHost);
   });
 }
 
@@ -972,7 +981,7 @@ int apc_lupp(apc_ctx* ctx, const double* w, int64_t rows, int64_t cols, int64_t 
   return apc::capi_guard(ctx, [&] {
     apc::DBuf<double> d(std::max<apc::i64>(1, rows * cols));
     if (rows * cols > 0)
-      APC_CUDA(cudaMemcpy(d.p, w, sizeof(double) * rows * cols, cudaMemcpyHostToDevice));
+      apc::copy_sync(ctx->stream, d.p, w, sizeof(double) * rows * cols, cudaMemcpyHostToDevice);
     apc::LuppOut o = apc::device_lupp(ctx, d.p, rows, cols, max_pivots);
     *steps = static_cast<int64_t>(o.order.size());
     std::copy(o.order.begin(), o.order.end(), order);

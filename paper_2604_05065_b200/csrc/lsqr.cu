@@ -23,7 +23,9 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "dev_common.cuh"
 #include "lsqr.hpp"
@@ -298,16 +300,48 @@ lsqr_update_kernel(LsqrPtrs P, cudaGraphConditionalHandle cond, int use_cond) {
 // ---------------------------------------------------------------------------
 // preconditioner kernels:  out = x + B (K (B^T x))  or  x + R^T (G (R x))
 // ---------------------------------------------------------------------------
-// s = K t  (K l x l column-major); t may be split partials summed in order
-__global__ void pc_core_kernel(const double* __restrict__ K, long long l,
+// s = K t with K stored row-major (KT[i * l + k] = K(i, k)): one warp per row,
+// lanes stride k (coalesced), fixed shuffle tree
+__global__ void pc_core_kernel(const double* __restrict__ KT, long long l,
                                const double* __restrict__ t, double* __restrict__ s,
                                const int* done) {
   if (done && *done) return;
-  long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (i >= l) return;
+  const double* row = KT + i * l;
   double acc = 0.0;
-  for (long long k = 0; k < l; ++k) acc += K[k * l + i] * t[k];
-  s[i] = acc;
+  for (long long k = lane; k < l; k += 32) acc += row[k] * t[k];
+  acc = warp_sum(acc);
+  if (lane == 0) s[i] = acc;
+}
+
+// implicit basis, one CTA: t = R x (warp per row of R), then s = K t
+constexpr int kSmallThreads = 1024;
+__global__ void __launch_bounds__(kSmallThreads)
+pc_small_kernel(const int* __restrict__ rptr, const int* __restrict__ ridx, const double* __restrict__ rval,
+                const double* __restrict__ KT, long long l, const double* __restrict__ x,
+                double* __restrict__ t, double* __restrict__ s, const int* done) {
+  extern __shared__ double tsh[];
+  if (done && *done) return;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kW = kSmallThreads / 32;
+  for (long long i = w; i < l; i += kW) {
+    double acc = 0.0;
+    for (int q = rptr[i] + lane; q < rptr[i + 1]; q += 32) acc += rval[q] * x[ridx[q]];
+    acc = warp_sum(acc);
+    if (lane == 0) tsh[i] = acc;
+  }
+  __syncthreads();
+  for (long long i = w; i < l; i += kW) {
+    const double* row = KT + i * l;
+    double acc = 0.0;
+    for (long long k = lane; k < l; k += 32) acc += row[k] * tsh[k];
+    acc = warp_sum(acc);
+    if (lane == 0) s[i] = acc;
+  }
+  if (t && threadIdx.x < l)
+    for (long long i = threadIdx.x; i < l; i += kSmallThreads) t[i] = tsh[i];
 }
 
 // expand: o_j = x_j + (B s)_j (explicit) or x_j + (R^T s)_j (implicit), then
@@ -424,25 +458,21 @@ void lsqr_work_destroy(LsqrWork* w) {
 // ---------------------------------------------------------------------------
 namespace {
 
-void pc_project(LsqrWork* w, PrecondDev& p, const double* x, const int* done) {
+// s = K (B^T x)  (explicit)  or  s = G (R x)  (implicit, one fused CTA)
+void pc_project_core(LsqrWork* w, PrecondDev& p, const double* x, bool transpose, const int* done) {
   apc_ctx* ctx = w->ctx;
+  const double* KT = transpose ? p.Ka.p : p.Kf.p;
   if (p.kind == 1) {
     DenseAdjPlan pl = dense_adj_plan(p.n, p.l, ctx->num_sms);
     launch_dense_adj(ctx, p.B.p, p.n, p.l, x, w->t.p, done, pl.msplit > 1 ? w->pc_part.p : nullptr,
                      pl.msplit > 1 ? w->pc_ctr.p : nullptr);
+    pc_core_kernel<<<nb(p.l * 32), kVecThreads, 0, ctx->stream>>>(KT, p.l, w->t.p, w->s.p, done);
+    ctx->launches++;
   } else {
-    const long long rows = p.R.rows;
-    const unsigned nbk = static_cast<unsigned>((rows + kCsrFwdRowsPerBlock - 1) / kCsrFwdRowsPerBlock);
-    csr_fwd_kernel<32, FwdStore><<<nbk, kCsrFwdThreads, 0, ctx->stream>>>(
-        p.R.ptr.p, p.R.idx.p, p.R.val.p, rows, x, done, FwdStore{w->t.p});
+    pc_small_kernel<<<1, kSmallThreads, sizeof(double) * p.l, ctx->stream>>>(
+        p.R.ptr.p, p.R.idx.p, p.R.val.p, KT, p.l, x, nullptr, w->s.p, done);
     ctx->launches++;
   }
-}
-
-void pc_core(LsqrWork* w, PrecondDev& p, bool transpose, const int* done) {
-  pc_core_kernel<<<nb(p.l, 128), 128, 0, w->ctx->stream>>>(transpose ? p.Ka.p : p.Kf.p, p.l,
-                                                            w->t.p, w->s.p, done);
-  w->ctx->launches++;
 }
 
 void pc_expand(LsqrWork* w, const LsqrPtrs& P, PrecondDev& p, const double* x, double* out,
@@ -474,8 +504,7 @@ void enqueue_iteration(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P
   const bool pre = p && p->kind != 0;
   const double* z = P.v;
   if (pre) {  // z = P^{-1} v
-    pc_project(w, *p, P.v, done);
-    pc_core(w, *p, false, done);
+    pc_project_core(w, *p, P.v, false, done);
     pc_expand(w, P, *p, P.v, P.z, 0, done);
     z = P.z;
   }
@@ -498,8 +527,7 @@ void enqueue_iteration(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P
   lsqr_epi_kernel<<<nb(w->n), kVecThreads, 0, st>>>(P, pre ? 1 : 0);
   ctx->launches++;
   if (pre) {  // v = P^{-T} h - beta v ; alpha ; rotation
-    pc_project(w, *p, P.h, done);
-    pc_core(w, *p, true, done);
+    pc_project_core(w, *p, P.h, true, done);
     pc_expand(w, P, *p, P.h, nullptr, 1, done);
   }
   lsqr_update_kernel<<<nb(w->n), kVecThreads, 0, st>>>(P, cond, use_cond);
@@ -519,8 +547,7 @@ void precond_apply(apc_ctx* ctx, PrecondDev& p, bool transpose, const double* x,
   ensure_pc_buffers(&tmp, p);
   LsqrPtrs P{};
   P.n = p.n;
-  pc_project(&tmp, p, x, nullptr);
-  pc_core(&tmp, p, transpose, nullptr);
+  pc_project_core(&tmp, p, x, transpose, nullptr);
   pc_expand(&tmp, P, p, x, out, 0, nullptr);
   APC_CUDA(cudaStreamSynchronize(ctx->stream));
   APC_CUDA(cudaGetLastError());
@@ -597,8 +624,7 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   lsqr_epi_kernel<<<nb(n), kVecThreads, 0, st>>>(P, pre ? 1 : 0);
   ctx->launches++;
   if (pre) {
-    pc_project(w, *p, P.h, done);
-    pc_core(w, *p, true, done);
+    pc_project_core(w, *p, P.h, true, done);
     pc_expand(w, P, *p, P.h, nullptr, 1, done);
   }
   lsqr_update_kernel<<<nb(n), kVecThreads, 0, st>>>(P, cudaGraphConditionalHandle{}, 0);
@@ -608,7 +634,12 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   // ---- iterations: graph with a conditional WHILE node (single rank), or
   // batches of captured iterations polled from the host (multi-rank: the
   // NCCL call stays outside conditional bodies)
-  const bool use_while = ctx->nranks == 1;
+  // APC_LSQR_MODE: "while" (default, 1 rank) | "batch" (graph of 8 iterations,
+  // host-polled; used for multi-rank) | "eager" (no graph; for kernel profiling)
+  const char* mode_env = std::getenv("APC_LSQR_MODE");
+  const std::string mode = mode_env ? mode_env : "";
+  const bool eager = mode == "eager";
+  const bool use_while = ctx->nranks == 1 && mode != "batch" && !eager;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   const std::uint64_t launches_before_capture = ctx->launches;
@@ -635,6 +666,14 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
     APC_CUDA(cudaMemcpyAsync(&w->hst[1], w->st.p, sizeof(LsqrState), cudaMemcpyDeviceToHost, st));
     APC_CUDA(cudaStreamSynchronize(st));
     if (!w->hst[1].done) APC_CUDA(cudaGraphLaunch(exec, st));
+  } else if (eager) {
+    for (;;) {
+      for (int k = 0; k < 8; ++k) enqueue_iteration(w, a, p, P, cudaGraphConditionalHandle{}, 0);
+      APC_CUDA(cudaMemcpyAsync(&w->hst[1], w->st.p, sizeof(LsqrState), cudaMemcpyDeviceToHost, st));
+      APC_CUDA(cudaStreamSynchronize(st));
+      if (w->hst[1].done) break;
+    }
+    per_iter = 0;  // eager launches were counted as issued
   } else {
     constexpr int kBatch = 8;
     APC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -664,12 +703,12 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   out.breakdown = f.breakdown != 0;
   out.iters = f.iter < 0 ? 0 : f.iter;
   // count executed (graph-replayed) kernels, not captured ones
-  ctx->launches = launches_before_capture + per_iter * static_cast<std::uint64_t>(out.iters);
+  if (!eager) ctx->launches = launches_before_capture + per_iter * static_cast<std::uint64_t>(out.iters);
   out.reason = f.reason;
   const long long nrows = out.iters + 1;
   out.rows.resize(static_cast<size_t>(nrows));
   static_assert(sizeof(TraceRowH) == sizeof(TraceRow), "trace row layout");
-  APC_CUDA(cudaMemcpy(out.rows.data(), w->trace.p, sizeof(TraceRow) * nrows, cudaMemcpyDeviceToHost));
+  copy_sync(st, out.rows.data(), w->trace.p, sizeof(TraceRow) * nrows, cudaMemcpyDeviceToHost);
   if (out.breakdown) fail(APC_NUMERICAL_BREAKDOWN, "lsqr_solve: non-finite recurrence");
 }
 

@@ -26,7 +26,7 @@ struct PrecondDev {
   int kind = 0;  // 0 identity, 1 explicit, 2 implicit
   i64 n = 0, l = 0;
   DBuf<double> B;       // explicit basis, n x l column-major
-  DBuf<double> Kf, Ka;  // l x l column-major middle operators (P^{-1} / P^{-T})
+  DBuf<double> Kf, Ka;  // l x l middle operators (P^{-1} / P^{-T}), stored row-major
   Csr R, RT;            // implicit basis rows (l x n) and their transpose (n x l)
   double sigma_hat = 1.0;
   double sigma_floor = 0.0;  // cvgdiff floor of the dynamic stop (solver.hpp:216-219)

@@ -245,16 +245,17 @@ void build_precond(const BuildInputs& in, PrecondDev& p, PrecondInfo& info) {
         Kf[j * l + i] = info.sigma_hat * Minv[j * l + i] - (i == j ? 1.0 : 0.0);
         Ka[j * l + i] = info.sigma_hat * Minv[i * l + j] - (i == j ? 1.0 : 0.0);
       }
+    // the device keeps the middle operators row-major (warp per output row)
     if (!in.implicit) {
       p.kind = 1;
       upload_vec(ctx, p.B, *in.q_r);
-      upload_vec(ctx, p.Kf, Kf);
-      upload_vec(ctx, p.Ka, Ka);
+      upload_vec(ctx, p.Kf, transpose(l, l, Kf));
+      upload_vec(ctx, p.Ka, transpose(l, l, Ka));
     } else {
       p.kind = 2;
       upload_r(ctx, n, l, in.r_ptr, in.r_idx, in.r_val, p);
-      upload_vec(ctx, p.Kf, conjugate_by_tinv(l, *in.t_r, Kf));
-      upload_vec(ctx, p.Ka, conjugate_by_tinv(l, *in.t_r, Ka));
+      upload_vec(ctx, p.Kf, transpose(l, l, conjugate_by_tinv(l, *in.t_r, Kf)));
+      upload_vec(ctx, p.Ka, transpose(l, l, conjugate_by_tinv(l, *in.t_r, Ka)));
     }
   }
   p.sigma_hat = info.sigma_hat;

@@ -220,7 +220,7 @@ apc_result* aplicur_solve(apc_mat& a, const double* b, const apc_solver_config& 
   }
 
   res->x.resize(static_cast<size_t>(n));
-  APC_CUDA(cudaMemcpy(res->x.data(), d_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  copy_sync(st, res->x.data(), d_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost);
   res->final_rho = cur.rho();
   res->final_relres = bnorm > 0.0 ? std::sqrt(residual(a, vw, d_x.p, d_b.p, nullptr)) / bnorm : 0.0;
   res->sketch_applications = cur.sketch_applications();

@@ -65,7 +65,7 @@ apc_result* plain_solve(apc_mat& a, const double* b, const apc_solver_config& cf
   auto* r = new apc_result();
   r->n = n;
   r->x.resize(static_cast<size_t>(n));
-  APC_CUDA(cudaMemcpy(r->x.data(), d_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  copy_sync(st, r->x.data(), d_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost);
   VecWork vw(a, mu);
   const double rr = bnorm > 0.0 ? std::sqrt(residual(a, vw, d_x.p, d_b.p, nullptr)) / bnorm : 0.0;
   for (const auto& row : po.rows)
