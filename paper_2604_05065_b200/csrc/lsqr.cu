@@ -29,6 +29,7 @@
 
 #include "dev_common.cuh"
 #include "lsqr.hpp"
+#include "lsqr_persistent.hpp"
 #include "ops.cuh"
 
 namespace apc {
@@ -402,7 +403,7 @@ struct LsqrWork {
   apc_ctx* ctx = nullptr;
   long long mloc = 0, n = 0, ulen = 0;
   double mu = 0.0;
-  DBuf<double> u, v, w, z, g, h, t, s, fwd_part, tail_part, epi_part, upd_part, pc_part;
+  DBuf<double> u, v, w, z, g, h, t, s, fwd_part, tail_part, epi_part, upd_part, pc_part, pers_part;
   DBuf<unsigned> ctr, pc_ctr;
   DBuf<LsqrState> st;
   DBuf<TraceRow> trace;
@@ -639,12 +640,22 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   const char* mode_env = std::getenv("APC_LSQR_MODE");
   const std::string mode = mode_env ? mode_env : "";
   const bool eager = mode == "eager";
-  const bool use_while = ctx->nranks == 1 && mode != "batch" && !eager;
+  const bool persistent = (mode.empty() || mode == "persistent") && persistent_eligible(a, p, ctx);
+  const bool use_while = !persistent && ctx->nranks == 1 && mode != "batch" && !eager;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   const std::uint64_t launches_before_capture = ctx->launches;
   std::uint64_t per_iter = 0;
-  if (use_while) {
+  if (persistent) {
+    // one cooperative launch runs every iteration (L2-resident sparse systems)
+    if (p && p->kind == 2) w->s.ensure(std::max<long long>(1, p->l));
+    w->pers_part.ensure(4LL * persistent_max_grid(ctx));
+    const char* bps = std::getenv("APC_PERSISTENT_BLOCKS_PER_SM");
+    PersistentBuffers pb{w->u.p, w->v.p, w->w.p, y_d, w->z.p, w->h.p, w->s.p, w->pers_part.p,
+                         w->st.p, w->trace.p, bps ? std::atoi(bps) : 0};
+    lsqr_persistent_run(a, mu, p, pb);
+    per_iter = 0;
+  } else if (use_while) {
     APC_CUDA(cudaGraphCreate(&graph, 0));
     cudaGraphConditionalHandle cond;
     APC_CUDA(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
@@ -703,7 +714,8 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   out.breakdown = f.breakdown != 0;
   out.iters = f.iter < 0 ? 0 : f.iter;
   // count executed (graph-replayed) kernels, not captured ones
-  if (!eager) ctx->launches = launches_before_capture + per_iter * static_cast<std::uint64_t>(out.iters);
+  if (!eager && !persistent)
+    ctx->launches = launches_before_capture + per_iter * static_cast<std::uint64_t>(out.iters);
   out.reason = f.reason;
   const long long nrows = out.iters + 1;
   out.rows.resize(static_cast<size_t>(nrows));
