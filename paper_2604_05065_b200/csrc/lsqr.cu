@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -317,6 +318,20 @@ __global__ void pc_core_kernel(const double* __restrict__ KT, long long l,
   if (lane == 0) s[i] = acc;
 }
 
+// t = R x: one warp per (short) row of R, spread over many CTAs
+__global__ void pc_rproj_kernel(const int* __restrict__ rptr, const int* __restrict__ ridx,
+                                const double* __restrict__ rval, long long l, const double* __restrict__ x,
+                                double* __restrict__ t, const int* done) {
+  if (done && *done) return;
+  const long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= l) return;
+  double acc = 0.0;
+  for (int q = rptr[i] + lane; q < rptr[i + 1]; q += 32) acc += rval[q] * x[ridx[q]];
+  acc = warp_sum(acc);
+  if (lane == 0) t[i] = acc;
+}
+
 // implicit basis, one CTA: t = R x (warp per row of R), then s = K t
 constexpr int kSmallThreads = 1024;
 __global__ void __launch_bounds__(kSmallThreads)
@@ -470,9 +485,11 @@ void pc_project_core(LsqrWork* w, PrecondDev& p, const double* x, bool transpose
     pc_core_kernel<<<nb(p.l * 32), kVecThreads, 0, ctx->stream>>>(KT, p.l, w->t.p, w->s.p, done);
     ctx->launches++;
   } else {
-    pc_small_kernel<<<1, kSmallThreads, sizeof(double) * p.l, ctx->stream>>>(
-        p.R.ptr.p, p.R.idx.p, p.R.val.p, KT, p.l, x, nullptr, w->s.p, done);
-    ctx->launches++;
+    // two wide launches beat one latency-bound CTA (pc_small_kernel) by ~3x
+    pc_rproj_kernel<<<nb(p.l * 32, 128), 128, 0, ctx->stream>>>(p.R.ptr.p, p.R.idx.p, p.R.val.p, p.l, x,
+                                                                w->t.p, done);
+    pc_core_kernel<<<nb(p.l * 32, 128), 128, 0, ctx->stream>>>(KT, p.l, w->t.p, w->s.p, done);
+    ctx->launches += 2;
   }
 }
 
@@ -648,13 +665,37 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   std::uint64_t per_iter = 0;
   if (persistent) {
     // one cooperative launch runs every iteration (L2-resident sparse systems)
-    if (p && p->kind == 2) w->s.ensure(std::max<long long>(1, p->l));
+    if (p && p->kind == 2) {
+      w->s.ensure(std::max<long long>(1, p->l));
+      w->t.ensure(std::max<long long>(1, p->l));
+    }
     w->pers_part.ensure(4LL * persistent_max_grid(ctx));
     const char* bps = std::getenv("APC_PERSISTENT_BLOCKS_PER_SM");
-    PersistentBuffers pb{w->u.p, w->v.p, w->w.p, y_d, w->z.p, w->h.p, w->s.p, w->pers_part.p,
-                         w->st.p, w->trace.p, bps ? std::atoi(bps) : 0};
+    const bool prof = std::getenv("APC_PERSISTENT_PROF") != nullptr;
+    DBuf<unsigned long long> d_prof(prof ? 64 * 8 : 0);
+    if (prof) APC_CUDA(cudaMemsetAsync(d_prof.p, 0, d_prof.bytes(), st));
+    PersistentBuffers pb{w->u.p, w->v.p, w->w.p, y_d, w->z.p, w->h.p, w->s.p, w->t.p, w->pers_part.p,
+                         w->st.p, w->trace.p, bps ? std::atoi(bps) : 0, prof ? d_prof.p : nullptr};
     lsqr_persistent_run(a, mu, p, pb);
     per_iter = 0;
+    if (prof) {
+      std::vector<unsigned long long> h(64 * 8);
+      copy_sync(st, h.data(), d_prof.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+      double acc[8] = {0};
+      int cnt = 0;
+      for (int it = 2; it < 63; ++it) {
+        if (h[(it + 1) * 8] == 0) break;
+        for (int k = 0; k < 8; ++k) {
+          unsigned long long a0 = h[it * 8 + k], a1 = k < 7 ? h[it * 8 + k + 1] : h[(it + 1) * 8];
+          if (a0 && a1) acc[k] += (a1 - a0) * 1e-3;
+        }
+        ++cnt;
+      }
+      if (cnt)
+        std::fprintf(stderr, "persistent stage us/iter (%d its): S1 %.2f S2 %.2f S3 %.2f S4 %.2f S5 %.2f S6 %.2f S7 %.2f S8 %.2f\n",
+                     cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt,
+                     acc[6] / cnt, acc[7] / cnt);
+    }
   } else if (use_while) {
     APC_CUDA(cudaGraphCreate(&graph, 0));
     cudaGraphConditionalHandle cond;

@@ -30,6 +30,9 @@ namespace cg = cooperative_groups;
 
 namespace apc {
 
+#define STAMP(k) \
+  if (P.prof && blockIdx.x == 0 && threadIdx.x == 0 && j < 64) P.prof[j * 8 + (k)] = globaltimer_ns()
+
 namespace {
 
 constexpr int kPT = 256;  // threads per CTA
@@ -54,8 +57,9 @@ struct PArgs {
   const double *Gf, *Ga;  // row-major l x l
   long long l;
   // vectors
-  double *u, *v, *w, *y, *z, *h, *s;
+  double *u, *v, *w, *y, *z, *h, *s, *t;
   double* part;  // gridDim.x x 4
+  unsigned long long* prof;  // optional stage timestamps (first 64 iterations)
   LsqrState* st;
   TraceRow* trace;
 };
@@ -67,21 +71,23 @@ __device__ __forceinline__ double grid_sum(const double* part, int slot, int nbl
   return block_sum<kPT>(v, sh);
 }
 
-// CTA-local: s = K (M x) for the l x n sparse M (R) and row-major K
-__device__ void small_project(const int* mptr, const int* midx, const double* mval, const double* KT,
-                              long long l, const double* x, double* tsh, double* s_out) {
-  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (long long i = wi; i < l; i += kNW) {
+// s = K (M x) for the l x n sparse M (R) and row-major K, spread over the
+// whole grid (one warp per row in each half, a barrier between them): the
+// rows are short, so the stage is latency-bound and wants many warps.
+__device__ void grid_project(cg::grid_group& grid, const int* mptr, const int* midx, const double* mval,
+                             const double* KT, long long l, const double* x, double* t, double* s_out,
+                             long long gwarp, long long nwarps, int lane) {
+  for (long long i = gwarp; i < l; i += nwarps) {
     double acc = 0.0;
     for (int q = mptr[i] + lane; q < mptr[i + 1]; q += 32) acc += mval[q] * x[midx[q]];
     acc = warp_sum(acc);
-    if (lane == 0) tsh[i] = acc;
+    if (lane == 0) t[i] = acc;
   }
-  __syncthreads();
-  for (long long i = wi; i < l; i += kNW) {
+  grid.sync();
+  for (long long i = gwarp; i < l; i += nwarps) {
     const double* row = KT + i * l;
     double acc = 0.0;
-    for (long long k = lane; k < l; k += 32) acc += row[k] * tsh[k];
+    for (long long k = lane; k < l; k += 32) acc += row[k] * t[k];
     acc = warp_sum(acc);
     if (lane == 0) s_out[i] = acc;
   }
@@ -111,15 +117,18 @@ __global__ void __launch_bounds__(kPT) lsqr_persistent_kernel(PArgs P) {
 
   for (;;) {
     // ---- S1/S2: z = v + R^T Gf R v
+    STAMP(0);
     if (P.pre) {
-      if (blockIdx.x == 0) small_project(P.rptr, P.ridx, P.rval, P.Gf, P.l, P.v, tsh, P.s);
+      grid_project(grid, P.rptr, P.ridx, P.rval, P.Gf, P.l, P.v, P.t, P.s, gwarp, nwarps, lane);
       grid.sync();
+      STAMP(1);
       for (long long c = gtid; c < P.n; c += gsize) {
         double acc = 0.0;
         for (int q = P.rtptr[c]; q < P.rtptr[c + 1]; ++q) acc += P.rtval[q] * P.s[P.rtidx[q]];
         P.z[c] = P.v[c] + acc;
       }
       grid.sync();
+      STAMP(2);
     }
     // ---- S3: u <- A z - alpha u/beta ; tail rows
     {
@@ -159,6 +168,7 @@ __global__ void __launch_bounds__(kPT) lsqr_persistent_kernel(PArgs P) {
       }
     }
     grid.sync();
+    STAMP(3);
     // ---- S4: beta ; h = (A^T u + mu u_t) / beta  [plain: v = h - beta v, ||v||^2]
     const double bnew = sqrt(grid_sum(P.part, 0, nb, red) + grid_sum(P.part, 1, nb, red));
     {
@@ -185,10 +195,12 @@ __global__ void __launch_bounds__(kPT) lsqr_persistent_kernel(PArgs P) {
       }
     }
     grid.sync();
+    STAMP(4);
     if (P.pre) {
       // ---- S5/S6: v = h + R^T Ga R h - beta v ; ||v||^2
-      if (blockIdx.x == 0) small_project(P.rptr, P.ridx, P.rval, P.Ga, P.l, P.h, tsh, P.s);
+      grid_project(grid, P.rptr, P.ridx, P.rval, P.Ga, P.l, P.h, P.t, P.s, gwarp, nwarps, lane);
       grid.sync();
+      STAMP(5);
       double sq = 0.0;
       for (long long c = gtid; c < P.n; c += gsize) {
         double acc = 0.0;
@@ -200,6 +212,7 @@ __global__ void __launch_bounds__(kPT) lsqr_persistent_kernel(PArgs P) {
       sq = block_sum<kPT>(sq, red);
       if (threadIdx.x == 0) P.part[blockIdx.x * 4 + 2] = sq;
       grid.sync();
+      STAMP(6);
     }
     // ---- S7: alpha ; rotation (lsqr.hpp:145-171) ; vector updates ; ||y||^2
     const double anew = sqrt(grid_sum(P.part, 2, nb, red));
@@ -236,6 +249,7 @@ __global__ void __launch_bounds__(kPT) lsqr_persistent_kernel(PArgs P) {
       if (threadIdx.x == 0) P.part[blockIdx.x * 4 + 3] = sq;
     }
     grid.sync();
+    STAMP(7);
     // ---- S8: stop tests (identical decision in every CTA)
     const double ynorm = sqrt(grid_sum(P.part, 3, nb, red));
     int reason = kReasonNone;
@@ -323,6 +337,8 @@ void lsqr_persistent_run(apc_mat& a, double mu, const PrecondDev* p, const Persi
   P.z = b.z;
   P.h = b.h;
   P.s = b.s;
+  P.t = b.t;
+  P.prof = b.prof;
   P.st = b.st;
   P.trace = b.trace;
   const int G = csr_group_size_p(a.a.avg_row_nnz);

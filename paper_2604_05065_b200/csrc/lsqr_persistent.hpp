@@ -7,10 +7,11 @@
 namespace apc {
 
 struct PersistentBuffers {
-  double *u, *v, *w, *y, *z, *h, *s, *part;
+  double *u, *v, *w, *y, *z, *h, *s, *t, *part;
   LsqrState* st;
   TraceRow* trace;
   int blocks_per_sm;
+  unsigned long long* prof;  // optional: 64 x 8 stage timestamps
 };
 
 // sparse A, one rank, no split transpose rows, identity or implicit basis
