@@ -99,6 +99,15 @@ def main(argv):
     for what in argv or ["small"]:
         if what == "small":
             small()
+        elif what.startswith("sens"):
+            # the reference's own x sensitivity: rerun with b moved by one ulp
+            k = int(what[4:])
+            p = apc.Problem(k)
+            t0 = time.time()
+            r = ref.solve(ref.Problem.from_apc(p), np.nextafter(p.b, np.inf),
+                          dict(BASELINE_SOLVER[k], trace_sample_stride=0))
+            _save(f"baseline_c{k}_ulp", x=r.x, row_indices=r.row_indices, phase_iters=r.phase_iters,
+                  final_relres=r.final_relres, wall_s=time.time() - t0)
         elif what.startswith("c") and what[1:].isdigit():
             k = int(what[1:])
             r, wall = solve_fixture(f"baseline_c{k}", k, 0, 0, BASELINE_SOLVER[k])

@@ -94,7 +94,7 @@ __device__ void grid_project(cg::grid_group& grid, const int* mptr, const int* m
 }
 
 template <int G>
-__global__ void __launch_bounds__(kPT) lsqr_persistent_kernel(PArgs P) {
+__global__ void __launch_bounds__(kPT, 3) lsqr_persistent_kernel(PArgs P) {
   extern __shared__ double tsh[];  // l doubles (preconditioner)
   __shared__ double red[32];
   cg::grid_group grid = cg::this_grid();
@@ -133,16 +133,23 @@ __global__ void __launch_bounds__(kPT) lsqr_persistent_kernel(PArgs P) {
     // ---- S3: u <- A z - alpha u/beta ; tail rows
     {
       double sq = 0.0, sqt = 0.0;
-      constexpr int kGpw = 32 / G;  // row groups per warp; the loop trip count is warp-uniform
-      const int gl = lane % G;
-      for (long long rb = gwarp * kGpw; rb < P.mloc; rb += nwarps * kGpw) {
-        const long long r = rb + lane / G;
+      // thread per row (rows are short): every load of a row is independent of
+      // the add chain, so 4-wide unrolling keeps several gathers in flight
+      for (long long r = gtid; r < P.mloc; r += gsize) {
+        const int b = P.aptr[r], e = P.aptr[r + 1];
         double acc = 0.0;
-        if (r < P.mloc)
-          for (int q = P.aptr[r] + gl; q < P.aptr[r + 1]; q += G) acc += P.aval[q] * zsrc[P.aidx[q]];
-#pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
-        if (gl == 0 && r < P.mloc) {
+        int q = b;
+        for (; q + 4 <= e; q += 4) {
+          const int c0 = P.aidx[q], c1 = P.aidx[q + 1], c2 = P.aidx[q + 2], c3 = P.aidx[q + 3];
+          const double v0 = P.aval[q], v1 = P.aval[q + 1], v2 = P.aval[q + 2], v3 = P.aval[q + 3];
+          const double z0 = zsrc[c0], z1 = zsrc[c1], z2 = zsrc[c2], z3 = zsrc[c3];
+          acc += v0 * z0;
+          acc += v1 * z1;
+          acc += v2 * z2;
+          acc += v3 * z3;
+        }
+        for (; q < e; ++q) acc += P.aval[q] * zsrc[P.aidx[q]];
+        {
           const double uo = P.u[r];
           const double uh = beta > 0.0 ? uo / beta : uo;
           const double t = acc - alpha * uh;
@@ -174,9 +181,17 @@ __global__ void __launch_bounds__(kPT) lsqr_persistent_kernel(PArgs P) {
     {
       double sq = 0.0;
       for (long long c = gwarp; c < P.n; c += nwarps) {
-        double acc = 0.0;
-        for (int q = P.tptr[c] + lane; q < P.tptr[c + 1]; q += 32) acc += P.tval[q] * P.u[P.tidx[q]];
-        acc = warp_sum(acc);
+        double acc = 0.0, acc2 = 0.0;
+        const int e = P.tptr[c + 1];
+        int q = P.tptr[c] + lane;
+        for (; q + 32 < e; q += 64) {
+          const int i0 = P.tidx[q], i1 = P.tidx[q + 32];
+          const double v0 = P.tval[q], v1 = P.tval[q + 32];
+          acc += v0 * P.u[i0];
+          acc2 += v1 * P.u[i1];
+        }
+        if (q < e) acc += P.tval[q] * P.u[P.tidx[q]];
+        acc = warp_sum(acc + acc2);
         if (lane == 0) {
           if (P.has_tail) acc += P.mu * P.u[P.mloc + c];
           const double gj = bnew > 0.0 ? acc / bnew : acc;
@@ -249,7 +264,7 @@ __global__ void __launch_bounds__(kPT) lsqr_persistent_kernel(PArgs P) {
       if (threadIdx.x == 0) P.part[blockIdx.x * 4 + 3] = sq;
     }
     grid.sync();
-    STAMP(7);
+    if (P.prof && blockIdx.x == 0 && threadIdx.x == 0 && j - 1 < 64) P.prof[(j - 1) * 8 + 7] = globaltimer_ns();
     // ---- S8: stop tests (identical decision in every CTA)
     const double ynorm = sqrt(grid_sum(P.part, 3, nb, red));
     int reason = kReasonNone;
@@ -356,7 +371,7 @@ void lsqr_persistent_run(apc_mat& a, double mu, const PrecondDev* p, const Persi
   APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kPT, smem));
   // fewer CTAs make each grid barrier cheaper; the L2-resident stages need
   // only a couple of CTAs per SM to saturate
-  const int blocks_per_sm = std::max(1, std::min(per_sm, b.blocks_per_sm > 0 ? b.blocks_per_sm : 2));
+  const int blocks_per_sm = std::max(1, std::min(per_sm, b.blocks_per_sm > 0 ? b.blocks_per_sm : 3));
   const int grid = ctx->num_sms * blocks_per_sm;
   double* part = b.part;
   P.part = part;

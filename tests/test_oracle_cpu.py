@@ -1,0 +1,113 @@
+"""Oracle pinning (CPU, no GPU): the plain-Python restatement (oracle/port.py)
+reproduces the reference's golden vectors bit for bit (tests/golden/, generated
+by the unmodified reference via oracle/make_golden.py), and the compiled
+reference (oracle/_ref) agrees with the same fixtures where it is present."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import port
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def _g(name):
+    return np.load(GOLD / f"{name}.npz")
+
+
+def _bits(a):
+    return np.asarray(a, dtype=np.float64).view(np.uint64)
+
+
+def test_rng_golden():
+    g = _g("rng")
+    r = port.Rng(20260416, stream=3, index=9)
+    assert [r.next_u64() for _ in range(256)] == [int(x) for x in g["u64"]]
+    r = port.Rng(20260416, stream=2)
+    assert np.array_equal(_bits([r.gaussian() for _ in range(256)]), _bits(g["gauss"]))
+    r = port.Rng(7)
+    assert [r.below(1000003) for _ in range(256)] == [int(x) for x in g["below"]]
+    assert [port.mix64(x) for x in (0, 1, 12345)] == [int(x) for x in g["mix"]]
+
+
+def test_sparse_sign_and_sketch_golden():
+    g = _g("sketch")
+    rows, signs, scale = port.sparse_sign(11, 300, 8, port.mix64(1 ^ 0x5CE7C3A1B2D4F688))
+    assert np.array_equal(rows, g["rows"]) and np.array_equal(signs, g["signs"]) and scale == float(g["scale"])
+    Y = port.sketch_dense(g["A"], 11, rows, signs, scale)
+    assert np.array_equal(_bits(Y), _bits(g["Y"]))
+    # CSC input walks the same nonzeros in the same order -> same bits
+    r2, s2, sc2 = port.sparse_sign(11, 300, 8, 99)
+    assert np.array_equal(_bits(port.sketch_dense(g["A"], 11, r2, s2, sc2)), _bits(g["Ys"]))
+    r3, s3, sc3 = port.sparse_sign(11, 340, 8, 5)
+    assert np.array_equal(_bits(port.sketch_augmented_dense(g["A"], 0.25, 11, r3, s3, sc3)), _bits(g["Ya"]))
+
+
+def test_lupp_golden():
+    g = _g("lupp")
+    for k in range(4):
+        o, mg = port.lu_partial_pivot(g[f"W{k}"])
+        assert np.array_equal(o, g[f"o{k}"])
+        assert np.array_equal(_bits(mg), _bits(g[f"m{k}"]))
+
+
+def test_matvec_golden():
+    g = _g("matvec")
+    A, x, u = g["A"], g["x"], g["u"]
+    assert np.array_equal(_bits(port.matvec_dense(A, x)), _bits(g["y"]))
+    assert np.array_equal(_bits(port.matvec_t_dense(A, u[:300])), _bits(g["g"]))
+    cp = [0]
+    ri, va = [], []
+    for j in range(A.shape[1]):
+        nz = np.nonzero(A[:, j])[0]
+        ri += nz.tolist()
+        va += A[nz, j].tolist()
+        cp.append(len(ri))
+    assert np.array_equal(_bits(port.matvec_csc(300, cp, ri, va, x)), _bits(g["ys"]))
+    assert np.array_equal(_bits(port.matvec_t_csc(cp, ri, va, u[:300])), _bits(g["gs"]))
+
+
+def test_plain_lsqr_golden(apc):
+    g = _g("plain_c2_small")
+    p = apc.Problem(2, 3000, 300)
+    y, trace, reason = port.plain_lsqr_csc(p.m, p.n, p.colptr.tolist(), p.rowidx.tolist(), p.vals.tolist(),
+                                           p.b.tolist(), 1e-3, 1e-10, 300)
+    assert reason == int(g["phase_reason"][0])
+    assert len(trace) - 1 == int(g["phase_iters"][0])
+    assert np.array_equal(_bits(trace[:64]), _bits(g["trace_phibar_head"][: len(trace[:64])]))
+    assert np.array_equal(_bits(y), _bits(g["x"]))
+
+
+def test_reference_library_matches_golden(ref):
+    g = _g("lupp")
+    o, mg = ref.lupp(g["W0"])
+    assert np.array_equal(o, g["o0"]) and np.array_equal(_bits(mg), _bits(g["m0"]))
+    gm = _g("matvec")
+    rp = ref.Problem.from_numpy(gm["A"])
+    assert np.array_equal(_bits(ref.matvec(rp, gm["x"])), _bits(gm["y"]))
+
+
+def test_reference_self_sensitivity_justifies_x_tolerance(apc, ref):
+    """Evidence for the x-parity tolerance on ill-conditioned BASELINE shapes:
+    the unmodified reference moves x by far more than 1e-6 when b changes by a
+    single ulp (same CUR indices), so no reordered-sum implementation can meet
+    a flat 1e-6 there; the GPU tests bound x by 10x this self-sensitivity."""
+    p = apc.Problem(1, 400, 50)
+    knobs = dict(mu=0.0, eps_lsqr=1e-8, block=5, seed=1, variant=1, trace_sample_stride=0)
+    r1 = ref.solve(ref.Problem.from_apc(p), p.b, knobs)
+    r2 = ref.solve(ref.Problem.from_apc(p), np.nextafter(p.b, np.inf), knobs)
+    assert np.array_equal(r1.row_indices, r2.row_indices)
+    sens = np.linalg.norm(r2.x - r1.x) / np.linalg.norm(r1.x)
+    assert sens > 1e-4
+
+
+@pytest.mark.parametrize("name", ["solve_c1_small", "solve_c2_small", "baseline_c1"])
+def test_golden_solve_fixtures_well_formed(name):
+    f = GOLD / f"{name}.npz"
+    if not f.exists():
+        pytest.skip(f"{name} not generated")
+    g = np.load(f)
+    assert len(g["row_indices"]) == len(g["col_indices"]) > 0
+    assert len(set(g["row_indices"].tolist())) == len(g["row_indices"])
+    assert np.all(np.diff(g["rho_history"]) <= 1e-9 * g["rho_history"][0] + np.abs(np.diff(g["rho_history"])))
