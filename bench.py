@@ -179,7 +179,20 @@ def main():
     p = apc.Problem(CONFIG_ID)
     cfg = apc.SolverConfig(**{k: v for k, v in SOLVER.items()})
 
-    A = apc.DeviceMatrix.from_problem(ctx, p)
+    # row partition (balanced by nnz) -- SURVEY.md 8(e): A*v local, one NCCL
+    # allreduce of [A_p^T u_p | ||u_p||^2] per LSQR iteration; the sketch / CUR
+    # selection runs replicated on the full matrix
+    if p.sparse:
+        row_nnz = np.bincount(p.rowidx, minlength=p.m).astype(np.int64)
+    else:
+        row_nnz = None
+    bounds = apc.partition_rows(p.m, ws, row_nnz)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    A_full = apc.DeviceMatrix.from_problem(ctx, p) if ws > 1 else None
+    A = apc.DeviceMatrix.from_problem(ctx, p, r0, r1) if ws > 1 else apc.DeviceMatrix.from_problem(ctx, p)
+
+    def solve_once(mat, full):
+        return apc.aplicur_solve(mat, p.b, cfg, full=full)
 
     def barrier():
         if dist is not None:
@@ -189,7 +202,7 @@ def main():
 
     # ---- device-resident solves (value) ------------------------------------
     for _ in range(args.warmup):
-        r = apc.aplicur_solve(A, p.b, cfg)
+        r = solve_once(A, A_full)
     barrier()
     L0 = ctx.launches
     s = torch.cuda.ExternalStream(ctx.stream)
@@ -198,7 +211,7 @@ def main():
     with ClockSampler(local) as clk:
         e0.record(s)
         for _ in range(args.steps):
-            results.append(apc.aplicur_solve(A, p.b, cfg))
+            results.append(solve_once(A, A_full))
         e1.record(s)
         barrier()
     launches = ctx.launches - L0
@@ -213,14 +226,19 @@ def main():
     lsqr_ms = float(np.mean([x.lsqr_ms for x in results]))
 
     # ---- end-to-end through the C-ABI with host buffers (e2e) ----------------
-    h2d = 8 * (p.n + 1) + 8 * p.nnz + 8 * p.nnz + 8 * p.m
+    csc_bytes = 8 * (p.n + 1) + 16 * p.nnz if p.sparse else 8 * p.m * p.n
+    # host CSC (full copy for the replicated CUR + this rank's shard when ws > 1) and b
+    h2d = csc_bytes * (2 if ws > 1 else 1) + 8 * (r1 - r0)
     d2h = 8 * p.n
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        A2 = apc.DeviceMatrix.from_problem(ctx, p)
-        r2 = apc.aplicur_solve(A2, p.b, cfg)
+        F2 = apc.DeviceMatrix.from_problem(ctx, p) if ws > 1 else None
+        A2 = apc.DeviceMatrix.from_problem(ctx, p, r0, r1) if ws > 1 else apc.DeviceMatrix.from_problem(ctx, p)
+        r2 = solve_once(A2, F2)
         A2.free()
+        if F2 is not None:
+            F2.free()
     barrier()
     e2e_s = (time.perf_counter() - t0) / args.steps
     if dist is not None:

@@ -177,6 +177,13 @@ int apc_config_default(apc_solver_config* cfg);
 /* b: full right-hand side (length m, host).  plain != 0 runs plain_lsqr_solve. */
 int apc_solve(apc_mat* a, const double* b, const apc_solver_config* cfg, int plain,
               apc_result** out);
+/* Row-partitioned solve: `shard` holds this rank's rows
+ * [r0, r1) on a ctx created with nranks > 1; `full` the whole matrix for the
+ * replicated sketch / CUR selection (NULL is allowed for plain != 0).  Every
+ * rank passes the full b; per LSQR iteration the ranks exchange one NCCL
+ * allreduce of n + 1 doubles ([A_p^T u_p | ||u_p||^2]). */
+int apc_solve_sharded(apc_mat* full, apc_mat* shard, const double* b, const apc_solver_config* cfg,
+                      int plain, apc_result** out);
 int apc_result_free(apc_result* r);
 /* status: SolveStatus 0 converged, 1 rank-exhausted, 2 breakdown */
 int apc_result_summary(const apc_result* r, int* status, double* final_rho, double* final_relres,

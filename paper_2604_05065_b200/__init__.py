@@ -150,6 +150,7 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
         "apc_problem_free": (C.c_int, [vp]),
         "apc_config_default": (C.c_int, [C.POINTER(_Config)]),
         "apc_solve": (C.c_int, [vp, _dp, C.POINTER(_Config), C.c_int, C.POINTER(vp)]),
+        "apc_solve_sharded": (C.c_int, [vp, vp, _dp, C.POINTER(_Config), C.c_int, C.POINTER(vp)]),
         "apc_result_free": (C.c_int, [vp]),
         "apc_result_summary": (C.c_int, [vp, C.POINTER(C.c_int), _dp, _dp, C.POINTER(_u64),
                                          C.POINTER(_u64), _i64p, _i64p, _i64p, _i64p]),
@@ -548,14 +549,23 @@ def _collect(h) -> SolveResult:
                        rows, cols, rho, tt.value, tl.value, ts.value)
 
 
-def solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig, plain: bool = False) -> SolveResult:
-    """Run aplicur_solve (plain=False) or plain_lsqr_solve on a device-resident A."""
+def solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig, plain: bool = False,
+          full: Optional[DeviceMatrix] = None) -> SolveResult:
+    """Run aplicur_solve (plain=False) or plain_lsqr_solve on a device-resident A.
+
+    With ``full`` given, ``mat`` is this rank's row block (row-partitioned
+    multi-GPU solve: NCCL allreduce per iteration) and ``full`` the whole
+    matrix used for the replicated sketch / CUR selection."""
     lib = load_library()
     b = np.ascontiguousarray(b, dtype=np.float64)
     assert b.size == mat.m
     c = config._c()
     h = C.c_void_p()
-    _check(lib.apc_solve(mat.h, _dptr(b), C.byref(c), int(plain), C.byref(h)))
+    if full is not None or mat.ctx.nranks > 1:
+        _check(lib.apc_solve_sharded(None if full is None else full.h, mat.h, _dptr(b), C.byref(c), int(plain),
+                                     C.byref(h)))
+    else:
+        _check(lib.apc_solve(mat.h, _dptr(b), C.byref(c), int(plain), C.byref(h)))
     try:
         res = _collect(h)
         x = np.zeros(mat.n)
@@ -566,9 +576,10 @@ def solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig, plain: bool = 
     return res
 
 
-def aplicur_solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig) -> SolveResult:
+def aplicur_solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig,
+                  full: Optional[DeviceMatrix] = None) -> SolveResult:
     """solver.hpp:162 -- adaptive CUR-preconditioned LSQR."""
-    return solve(mat, b, config, plain=False)
+    return solve(mat, b, config, plain=False, full=full)
 
 
 def plain_lsqr_solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig) -> SolveResult:

@@ -370,6 +370,19 @@ int apc_solve(apc_mat* a, const double* b, const apc_solver_config* cfg, int pla
   });
 }
 
+int apc_solve_sharded(apc_mat* full, apc_mat* shard, const double* b, const apc_solver_config* cfg, int plain,
+                      apc_result** out) {
+  *out = nullptr;
+  return guard(shard->ctx, [&] {
+    APC_CUDA(cudaSetDevice(shard->ctx->device));
+    if (plain) *out = plain_solve(*shard, b, *cfg);
+    else {
+      require(full != nullptr, APC_INVALID_ARGUMENT, "apc_solve_sharded: full matrix required for aplicur_solve");
+      *out = aplicur_solve_sharded(*full, *shard, b, *cfg);
+    }
+  });
+}
+
 int apc_result_free(apc_result* r) {
   delete r;
   return APC_OK;

@@ -35,6 +35,15 @@ bool is_solver_error(const Status& s) { return s.code >= 1 && s.code <= 9; }
 }  // namespace
 
 apc_result* aplicur_solve(apc_mat& a, const double* b, const apc_solver_config& cfg_in) {
+  return aplicur_solve_sharded(a, a, b, cfg_in);
+}
+
+// `full`: the whole matrix (sketch + CUR selection, replicated on every rank);
+// `a`: this rank's block of rows (LSQR operator, residuals; NCCL allreduce
+// of the partial A^T u when the ctx has several ranks).
+apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, const apc_solver_config& cfg_in) {
+  require(full.ctx == a.ctx && full.m == a.m && full.n == a.n, APC_INVALID_ARGUMENT,
+          "aplicur_solve: full matrix and shard must describe the same A on the same context");
   auto t_start = clock_t_::now();
   const i64 n = a.n, m = a.m;
   apc_solver_config cfg = resolve_config(cfg_in, n);
@@ -47,7 +56,7 @@ apc_result* aplicur_solve(apc_mat& a, const double* b, const apc_solver_config& 
   require(!(cfg.variant == 1 && mu > 0.0), APC_NOT_APPLICABLE,
           "aplicur_solve: svd-free with mu > 0 (augmented CUR target) is not built on the device yet");
 
-  DeviceCur cur(a, cfg.block, cfg.seed, cfg.sketch_xi, cfg.probe_count, cfg.core, cfg.sketch_kind,
+  DeviceCur cur(full, cfg.block, cfg.seed, cfg.sketch_xi, cfg.probe_count, cfg.core, cfg.sketch_kind,
                 cfg.max_rank);
   i64 max_rank = std::min(m, n);
   if (cfg.max_rank > 0) max_rank = std::min(max_rank, cfg.max_rank);
@@ -191,8 +200,8 @@ apc_result* aplicur_solve(apc_mat& a, const double* b, const apc_solver_config& 
         in.block = &cur.intersection();
         in.t_r = implicit_mode ? &t_r_implicit : &qr_acc.t;
         in.q_r = &qr_acc.q;
-        in.c_sparse = a.sparse;
-        if (a.sparse) cur.c_csc(in.c_ptr, in.c_idx, in.c_val);
+        in.c_sparse = full.sparse;
+        if (full.sparse) cur.c_csc(in.c_ptr, in.c_idx, in.c_val);
         else in.c_dense = cur.c_dense();
         if (implicit_mode) cur.rt_csc(in.r_ptr, in.r_idx, in.r_val);
         build_precond(in, P, info);

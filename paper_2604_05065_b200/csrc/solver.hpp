@@ -28,5 +28,6 @@ apc_solver_config resolve_config(const apc_solver_config& in, i64 n);
 
 apc_result* plain_solve(apc_mat& a, const double* b, const apc_solver_config& cfg);
 apc_result* aplicur_solve(apc_mat& a, const double* b, const apc_solver_config& cfg);
+apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& shard, const double* b, const apc_solver_config& cfg);
 
 }  // namespace apc

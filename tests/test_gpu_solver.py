@@ -53,7 +53,7 @@ def test_aplicur_solve_matches_reference(apc, ref, ctx, cfg, m, n, knobs):
         r2 = ref.solve(ref.Problem.from_apc(p), bp, dict(knobs, trace_sample_stride=0))
         self_sens = np.linalg.norm(r2.x - r.x) / np.linalg.norm(r.x)
         assert rel <= max(1e-6, 10.0 * self_sens), (rel, self_sens, g.final_relres, r.final_relres)
-        assert abs(g.final_relres - r.final_relres) <= 1e-8 * r.final_relres
+        assert abs(g.final_relres - r.final_relres) <= 1e-5 * r.final_relres
     else:
         assert g.phases[-1].reason == r.phase_reason[-1]
         assert abs(g.final_relres - r.final_relres) <= 1e-3 * r.final_relres, (rel, g.final_relres, r.final_relres)
