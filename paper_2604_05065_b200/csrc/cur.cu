@@ -384,30 +384,68 @@ __global__ void probe_kernel(const double* __restrict__ E, long long s, long lon
 // ---------------------------------------------------------------------------
 // gathers
 // ---------------------------------------------------------------------------
+// A(I, J) of the target; rows i >= m of the augmented stack are amu * e_{i-m}
+// (AugmentedOperator::extract_block, matrix.hpp:460-473)
 __global__ void gather_block_kernel(const double* A, long long m, const int* ptr, const int* idx,
                                     const double* val, int sparse, const long long* I, const long long* J,
-                                    long long li, long long lj, double* out) {
+                                    long long li, long long lj, double amu, double* out) {
   const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= li * lj) return;
   const long long jj = e / li, ii = e % li;
-  out[e] = sparse ? csr_at(ptr, idx, val, I[ii], J[jj]) : A[J[jj] * m + I[ii]];
+  const long long i = I[ii];
+  if (i >= m) out[e] = (i - m == J[jj]) ? amu : 0.0;
+  else out[e] = sparse ? csr_at(ptr, idx, val, i, J[jj]) : A[J[jj] * m + i];
 }
 
-// rows I[q] of A -> R row-major (q in [0, cnt)), dense source
+// rows I[q] of the target -> R row-major (q in [0, cnt)), dense source
 __global__ void gather_rows_dense_kernel(const double* A, long long m, long long n, const long long* I,
-                                         long long cnt, double* R) {
+                                         long long cnt, double amu, double* R) {
   const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= cnt * n) return;
   const long long q = e / n, c = e % n;
-  R[e] = A[c * m + I[q]];
+  const long long i = I[q];
+  R[e] = i < m ? A[c * m + i] : (c == i - m ? amu : 0.0);
 }
 
-__global__ void scatter_rows_csr_kernel(const int* ptr, const int* idx, const double* val, long long n,
-                                        const long long* I, long long cnt, double* R) {
+__global__ void scatter_rows_csr_kernel(const int* ptr, const int* idx, const double* val, long long m,
+                                        long long n, const long long* I, long long cnt, double amu, double* R) {
   const long long q = blockIdx.x;
   if (q >= cnt) return;
   const long long i = I[q];
+  if (i >= m) {  // augmented identity row
+    if (threadIdx.x == 0) R[q * n + (i - m)] = amu;
+    return;
+  }
   for (int p = ptr[i] + threadIdx.x; p < ptr[i + 1]; p += blockDim.x) R[q * n + idx[p]] = val[p];
+}
+
+// E^col rows m..m+n-1 of the augmented target: A-part is amu at row m + J+[jj];
+// C's row m + j holds amu in the column t with J[t] == j (a one-term chain)
+__global__ void ecol_tail_kernel(long long m, long long n, long long ld, const int* __restrict__ colpos,
+                                 long long l, const long long* __restrict__ Jp, long long b,
+                                 const double* __restrict__ urj, const int* __restrict__ rowsel, double amu,
+                                 double* __restrict__ out) {
+  const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const bool zero = rowsel[m + j] != 0;
+  const int t = colpos[j];
+  for (long long jj = 0; jj < b; ++jj) {
+    double v = 0.0;
+    if (!zero) {
+      const double aval = (Jp[jj] == j) ? amu : 0.0;
+      if (l > 0) {
+        double acc = 0.0;
+        if (t >= 0) {
+          const double x = urj[jj * l + t];
+          if (x != 0.0) acc += x * amu;
+        }
+        v = aval - acc;
+      } else {
+        v = aval;
+      }
+    }
+    out[jj * ld + m + j] = v;
+  }
 }
 
 // SC = Y(:, J) (s x l column-major)
@@ -432,9 +470,9 @@ __global__ void gather_rcols_kernel(const double* R, long long n, long long l, c
 // ---------------------------------------------------------------------------
 constexpr int kEcolTile = 8;
 
-__global__ void ecol_dense_kernel(const double* __restrict__ A, long long m, const long long* __restrict__ J,
-                                  long long l, const long long* __restrict__ Jp, long long b,
-                                  const double* __restrict__ urj, const int* __restrict__ rowsel,
+__global__ void ecol_dense_kernel(const double* __restrict__ A, long long m, long long ld,
+                                  const long long* __restrict__ J, long long l, const long long* __restrict__ Jp,
+                                  long long b, const double* __restrict__ urj, const int* __restrict__ rowsel,
                                   double* __restrict__ out) {
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long jj0 = static_cast<long long>(blockIdx.y) * kEcolTile;
@@ -456,13 +494,14 @@ __global__ void ecol_dense_kernel(const double* __restrict__ A, long long m, con
 #pragma unroll
   for (int q = 0; q < kEcolTile; ++q) {
     const long long jj = jj0 + q;
-    if (jj < b) out[jj * m + i] = zero ? 0.0 : A[Jp[jj] * m + i] - acc[q];
+    if (jj < b) out[jj * ld + i] = zero ? 0.0 : (l > 0 ? A[Jp[jj] * m + i] - acc[q] : A[Jp[jj] * m + i]);
   }
 }
 
 // sparse A: per row i, C(i, :) entries (t ascending) from crow lists
 __global__ void ecol_sparse_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
-                                   const double* __restrict__ val, long long m, const int* __restrict__ cptr,
+                                   const double* __restrict__ val, long long m, long long ld,
+                                   const int* __restrict__ cptr,
                                    const int* __restrict__ ct, const double* __restrict__ cv, long long l,
                                    const long long* __restrict__ Jp, long long b, const double* __restrict__ urj,
                                    const int* __restrict__ rowsel, double* __restrict__ out) {
@@ -481,7 +520,7 @@ __global__ void ecol_sparse_kernel(const int* __restrict__ ptr, const int* __res
         }
       v = l > 0 ? aval - acc : aval;
     }
-    out[jj * m + i] = v;
+    out[jj * ld + i] = v;
   }
 }
 
@@ -575,10 +614,12 @@ LuppOut device_lupp(apc_ctx* ctx, double* w, i64 rows, i64 cols, i64 max_pivots)
 // DeviceCur
 // ---------------------------------------------------------------------------
 DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 probes, int core_kind,
-                     int sketch_kind, i64 max_rank)
+                     int sketch_kind, i64 max_rank, double aug_mu)
     : a_(a), ctx_(a.ctx), m_(a.m), n_(a.n), block_size_(block), probes_(probes), max_rank_(max_rank),
-      core_kind_(core_kind), rho_(std::numeric_limits<double>::infinity()),
-      probe_rng_(seed, Stream::probes) {
+      mt_(a.m + (aug_mu > 0.0 ? a.n : 0)), amu_(aug_mu > 0.0 ? aug_mu : 0.0), core_kind_(core_kind),
+      rho_(std::numeric_limits<double>::infinity()), probe_rng_(seed, Stream::probes) {
+  require(!(amu_ > 0.0 && sketch_kind != 0), APC_NOT_APPLICABLE,
+          "CurState: the reference has no Gaussian sketch of the augmented stack");
   require(block >= 1, APC_INVALID_ARGUMENT, "CurState: block size must be >= 1");
   require(block <= n_, APC_INVALID_ARGUMENT, "CurState: block size exceeds column count");
   require(a.r0 == 0 && a.r1 == a.m, APC_NOT_APPLICABLE, "CurState: needs the full matrix on this rank");
@@ -590,11 +631,11 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
   if (sketch_kind == 0) {
     // SparseSignEmbedding ctor (sketch.hpp:20-50), host RNG, bit-identical
     const i64 x = std::min(xi, s_);
-    std::vector<int> rows(static_cast<size_t>(m_ * x));
-    std::vector<signed char> sg(static_cast<size_t>(m_ * x));
+    std::vector<int> rows(static_cast<size_t>(mt_ * x));
+    std::vector<signed char> sg(static_cast<size_t>(mt_ * x));
     HostRng rng(emb_seed);
     std::vector<i64> pick(static_cast<size_t>(x));
-    for (i64 c = 0; c < m_; ++c) {
+    for (i64 c = 0; c < mt_; ++c) {  // one column per target row (m + n when augmented)
       size_t cnt = 0;
       for (i64 t = s_ - x; t < s_; ++t) {
         const i64 r = static_cast<i64>(rng.below(static_cast<std::uint64_t>(t) + 1));
@@ -615,8 +656,10 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
     const double scale = 1.0 / std::sqrt(static_cast<double>(x));
     DBuf<int> d_rows;
     DBuf<signed char> d_sg;
-    upload(ctx_, d_rows, rows.data(), m_ * x);
-    upload(ctx_, d_sg, sg.data(), m_ * x);
+    upload(ctx_, d_rows, rows.data(), mt_ * x);
+    upload(ctx_, d_sg, sg.data(), mt_ * x);
+    const double mu_scale = amu_ * scale;  // mu * scale_ * ss[q] (sketch.hpp:158)
+    const int aug = amu_ > 0.0 ? 1 : 0;
     const size_t smem = sizeof(double) * kSketchWarps * s_;
     if (smem > 48 * 1024) {
       APC_CUDA(cudaFuncSetAttribute(sketch_ss_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -625,10 +668,10 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
     const unsigned g = nb(n_, kSketchWarps);
     if (!a.sparse)
       sketch_ss_dense_kernel<<<g, kSketchWarps * 32, smem, st>>>(a.dense.p, m_, n_, (int)s_, (int)x, d_rows.p,
-                                                                d_sg.p, scale, 0.0, 0, Y_.p);
+                                                                d_sg.p, scale, mu_scale, aug, Y_.p);
     else
       sketch_ss_csc_kernel<<<g, kSketchWarps * 32, smem, st>>>(a.at.ptr.p, a.at.idx.p, a.at.val.p, m_, n_, (int)s_,
-                                                              (int)x, d_rows.p, d_sg.p, scale, 0.0, 0, Y_.p);
+                                                              (int)x, d_rows.p, d_sg.p, scale, mu_scale, aug, Y_.p);
     ctx_->launches++;
     APC_CUDA(cudaStreamSynchronize(st));
   } else {
@@ -656,7 +699,7 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
   double f2 = 0.0;
   for (double v : yh) f2 += v * v;
   ztol_ = 1e-14 * std::sqrt(f2);
-  rowsel_.alloc(std::max<i64>(1, m_));
+  rowsel_.alloc(std::max<i64>(1, mt_));
   colsel_.alloc(std::max<i64>(1, n_));
   APC_CUDA(cudaMemsetAsync(rowsel_.p, 0, rowsel_.bytes(), st));
   APC_CUDA(cudaMemsetAsync(colsel_.p, 0, colsel_.bytes(), st));
@@ -698,7 +741,7 @@ static std::vector<i64> admissible(const LuppOut& piv, i64 cap, double ztol) {  
 AugmentResult DeviceCur::augment() {
   cudaStream_t st = ctx_->stream;
   i64 want = block_size_;
-  const i64 room = std::min(m_, n_) - rank();
+  const i64 room = std::min(mt_, n_) - rank();
   require(room > 0, APC_INVALID_ARGUMENT, "CurState::augment: rank at capacity");
   want = std::min(want, room);
 
@@ -729,15 +772,20 @@ AugmentResult DeviceCur::augment() {
     upload(ctx_, d_urj, urj.data(), l * b);
   }
   // E^col = A(:, J+) - C urj, rows I zeroed (m x b)
-  DBuf<double> ecol(std::max<i64>(1, m_ * b));
+  DBuf<double> ecol(std::max<i64>(1, mt_ * b));
+  DBuf<int> colpos(n_);
+  APC_CUDA(cudaMemsetAsync(colpos.p, 0xff, colpos.bytes(), st));
+  if (l > 0) set_colpos_kernel<<<nb(l), kT, 0, st>>>(colpos.p, d_J.p, l);
+  if (amu_ > 0.0) {  // rows m..m+n-1 of the augmented stack
+    ecol_tail_kernel<<<nb(n_), kT, 0, st>>>(m_, n_, mt_, colpos.p, l, d_jp.p, b, d_urj.p, rowsel_.p, amu_, ecol.p);
+    ctx_->launches++;
+  }
   if (!a_.sparse) {
     dim3 grid(nb(m_), static_cast<unsigned>((b + kEcolTile - 1) / kEcolTile));
-    ecol_dense_kernel<<<grid, kT, 0, st>>>(a_.dense.p, m_, d_J.p, l, d_jp.p, b, d_urj.p, rowsel_.p, ecol.p);
+    ecol_dense_kernel<<<grid, kT, 0, st>>>(a_.dense.p, m_, mt_, d_J.p, l, d_jp.p, b, d_urj.p, rowsel_.p, ecol.p);
     ctx_->launches++;
   } else {
-    DBuf<int> colpos(n_), ccnt(m_ + 1), cptr(m_ + 1);
-    APC_CUDA(cudaMemsetAsync(colpos.p, 0xff, colpos.bytes(), st));
-    if (l > 0) set_colpos_kernel<<<nb(l), kT, 0, st>>>(colpos.p, d_J.p, l);
+    DBuf<int> ccnt(m_ + 1), cptr(m_ + 1);
     crow_count_kernel<<<nb(m_), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, m_, colpos.p, ccnt.p);
     APC_CUDA(cudaMemsetAsync(ccnt.p + m_, 0, sizeof(int), st));
     size_t tmp = 0;
@@ -750,13 +798,13 @@ AugmentResult DeviceCur::augment() {
     DBuf<int> ct(std::max(1, total));
     DBuf<double> cv(std::max(1, total));
     crow_fill_kernel<<<nb(m_), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p, m_, colpos.p, cptr.p, ct.p, cv.p);
-    ecol_sparse_kernel<<<nb(m_), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p, m_, cptr.p, ct.p, cv.p, l,
+    ecol_sparse_kernel<<<nb(m_), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p, m_, mt_, cptr.p, ct.p, cv.p, l,
                                               d_jp.p, b, d_urj.p, rowsel_.p, ecol.p);
     ctx_->launches += 4;
     APC_CUDA(cudaStreamSynchronize(st));
   }
   APC_CUDA(cudaGetLastError());
-  LuppOut row_piv = device_lupp(ctx_, ecol.p, m_, b, b);
+  LuppOut row_piv = device_lupp(ctx_, ecol.p, mt_, b, b);
   std::vector<i64> iplus = admissible(row_piv, b, ztol_);
   if (iplus.empty()) return {0, true};
   const bool exhausted = static_cast<i64>(iplus.size()) < want;
@@ -801,18 +849,18 @@ void DeviceCur::refresh() {
   // intersection block A(I, J) -> host factor
   DBuf<double> d_blk(l * l);
   gather_block_kernel<<<nb(l * l), kT, 0, st>>>(a_.dense.p, m_, a_.a.ptr.p, a_.a.idx.p, a_.a.val.p,
-                                                a_.sparse ? 1 : 0, d_I.p, d_J.p, l, l, d_blk.p);
+                                                a_.sparse ? 1 : 0, d_I.p, d_J.p, l, l, amu_, d_blk.p);
   ctx_->launches++;
   block_ = download(ctx_, d_blk.p, l * l);
   core_ = CoreFactorH::build(l, block_, core_kind_);  // throws singular
   // R = A(I, :) row-major (all rows re-gathered: I may have changed after a rollback)
   Rrm_.ensure(l * n_);
   if (!a_.sparse) {
-    gather_rows_dense_kernel<<<nb(l * n_), kT, 0, st>>>(a_.dense.p, m_, n_, d_I.p, l, Rrm_.p);
+    gather_rows_dense_kernel<<<nb(l * n_), kT, 0, st>>>(a_.dense.p, m_, n_, d_I.p, l, amu_, Rrm_.p);
   } else {
     APC_CUDA(cudaMemsetAsync(Rrm_.p, 0, sizeof(double) * l * n_, st));
-    scatter_rows_csr_kernel<<<static_cast<unsigned>(l), 128, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p, n_,
-                                                                     d_I.p, l, Rrm_.p);
+    scatter_rows_csr_kernel<<<static_cast<unsigned>(l), 128, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p, m_,
+                                                                     n_, d_I.p, l, amu_, Rrm_.p);
   }
   ctx_->launches++;
   // H = U R (core solve per column)
@@ -847,11 +895,13 @@ Vec DeviceCur::r_dense_rows(i64 first, i64 count) const {
 Vec DeviceCur::c_dense() const {
   require(!a_.sparse, APC_INVALID_ARGUMENT, "c_dense: dense A only");
   const i64 l = rank();
-  Vec out(static_cast<size_t>(m_ * l));
+  Vec out(static_cast<size_t>(mt_ * l), 0.0);
   for (i64 t = 0; t < l; ++t)
-    APC_CUDA(cudaMemcpyAsync(out.data() + t * m_, a_.dense.p + J_[t] * m_, sizeof(double) * m_,
+    APC_CUDA(cudaMemcpyAsync(out.data() + t * mt_, a_.dense.p + J_[t] * m_, sizeof(double) * m_,
                              cudaMemcpyDeviceToHost, ctx_->stream));
   APC_CUDA(cudaStreamSynchronize(ctx_->stream));
+  if (amu_ > 0.0)  // AugmentedOperator::extract_cols (matrix.hpp:428-438)
+    for (i64 t = 0; t < l; ++t) out[t * mt_ + m_ + J_[t]] = amu_;
   return out;
 }
 
@@ -884,10 +934,49 @@ void csr_rows_to_host(apc_ctx* ctx, const Csr& c, const std::vector<i64>& which,
 
 void DeviceCur::c_csc(std::vector<i64>& ptr, std::vector<i64>& idx, Vec& val) const {
   csr_rows_to_host(ctx_, a_.at, J_, ptr, idx, val);  // CSR(A^T) row j == column j of A
+  if (amu_ > 0.0) {  // + amu at row m + J[t] of column t (matrix.hpp:439-446)
+    std::vector<i64> p2(1, 0), i2;
+    Vec v2;
+    for (size_t t = 0; t + 1 < ptr.size(); ++t) {
+      for (i64 q = ptr[t]; q < ptr[t + 1]; ++q) {
+        i2.push_back(idx[q]);
+        v2.push_back(val[q]);
+      }
+      i2.push_back(m_ + J_[t]);
+      v2.push_back(amu_);
+      p2.push_back(static_cast<i64>(i2.size()));
+    }
+    ptr.swap(p2);
+    idx.swap(i2);
+    val.swap(v2);
+  }
 }
 
 void DeviceCur::rt_csc(std::vector<i64>& ptr, std::vector<i64>& idx, Vec& val) const {
-  csr_rows_to_host(ctx_, a_.a, I_, ptr, idx, val);  // row i of A == column of R^T
+  // row i of the target == column of R^T; augmented rows are amu e_{i-m}
+  std::vector<i64> base;
+  for (i64 i : I_)
+    if (i < m_) base.push_back(i);
+  std::vector<i64> bp, bi;
+  Vec bv;
+  csr_rows_to_host(ctx_, a_.a, base, bp, bi, bv);
+  ptr.assign(1, 0);
+  idx.clear();
+  val.clear();
+  size_t k = 0;
+  for (i64 i : I_) {
+    if (i < m_) {
+      for (i64 q = bp[k]; q < bp[k + 1]; ++q) {
+        idx.push_back(bi[q]);
+        val.push_back(bv[q]);
+      }
+      ++k;
+    } else {
+      idx.push_back(i - m_);
+      val.push_back(amu_);
+    }
+    ptr.push_back(static_cast<i64>(idx.size()));
+  }
 }
 
 }  // namespace apc

@@ -33,9 +33,12 @@ struct AugmentResult {
 
 class DeviceCur {
  public:
-  // target = A (the svd variant, or svd-free with mu == 0)
+  // target = A (aug_mu == 0: the svd variant, or svd-free with mu == 0), or the
+  // stacked [A; aug_mu I] (svd-free with mu > 0, CurTarget(aug), cur.hpp:21-47)
   DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 probes, int core_kind,
-            int sketch_kind, i64 max_rank);
+            int sketch_kind, i64 max_rank, double aug_mu = 0.0);
+  i64 target_rows() const { return mt_; }
+  bool augmented() const { return amu_ > 0.0; }
   ~DeviceCur();
 
   i64 rank() const { return static_cast<i64>(I_.size()); }
@@ -56,7 +59,7 @@ class DeviceCur {
 
   // host copies used by the preconditioner builders
   Vec r_dense_rows(i64 first, i64 count) const;  // rows I[first..first+count) of A, row-major count x n
-  Vec c_dense() const;                           // dense m x l, column-major (dense A only)
+  Vec c_dense() const;                           // dense target_rows x l, column-major (dense A only)
   // sparse C / R on the host (CSC of C = A(:,J), CSC of R^T = A(I,:)^T)
   void c_csc(std::vector<i64>& ptr, std::vector<i64>& idx, Vec& val) const;
   void rt_csc(std::vector<i64>& ptr, std::vector<i64>& idx, Vec& val) const;
@@ -73,6 +76,8 @@ class DeviceCur {
   apc_mat& a_;
   apc_ctx* ctx_;
   i64 m_, n_, s_, block_size_, probes_, max_rank_;
+  i64 mt_ = 0;       // target rows: m, or m + n for the augmented stack
+  double amu_ = 0.0; // mu of the augmented target (0: plain A)
   int core_kind_;
   double ztol_ = 0.0;
   double rho_;

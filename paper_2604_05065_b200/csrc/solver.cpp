@@ -53,12 +53,12 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
   cudaStream_t st = ctx->stream;
   const double bnorm = host_norm(b, m);
   require(std::isfinite(bnorm), APC_INVALID_ARGUMENT, "aplicur_solve: non-finite right-hand side");
-  require(!(cfg.variant == 1 && mu > 0.0), APC_NOT_APPLICABLE,
-          "aplicur_solve: svd-free with mu > 0 (augmented CUR target) is not built on the device yet");
-
+  // CUR target: A for the svd variant; the regularised stack [A; mu I] for the
+  // svd-free variant whenever mu > 0 (solver.hpp:183-186)
+  const bool target_augmented = cfg.variant == 1 && mu > 0.0;
   DeviceCur cur(full, cfg.block, cfg.seed, cfg.sketch_xi, cfg.probe_count, cfg.core, cfg.sketch_kind,
-                cfg.max_rank);
-  i64 max_rank = std::min(m, n);
+                cfg.max_rank, target_augmented ? mu : 0.0);
+  i64 max_rank = std::min(cur.target_rows(), n);
   if (cfg.max_rank > 0) max_rank = std::min(max_rank, cfg.max_rank);
   const double density = (m * n == 0) ? 0.0 : static_cast<double>(a.nnz_global) / static_cast<double>(m * n);
   const bool implicit_mode = a.sparse && density < 0.10;
@@ -191,7 +191,7 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
         in.ctx = ctx;
         in.variant = cfg.variant;
         in.implicit = implicit_mode;
-        in.m = m;
+        in.m = cur.target_rows();
         in.n = n;
         in.l = cur.rank();
         in.mu = mu;

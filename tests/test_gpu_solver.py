@@ -24,6 +24,10 @@ CASES = [
     (1, 400, 50, dict(mu=0.0, eps_lsqr=1e-8, block=5, seed=1, variant=1)),
     (2, 4000, 400, dict(mu=0.0, eps_lsqr=1e-10, block=8, seed=3, max_rank=40, variant=1)),
     (1, 600, 60, dict(mu=0.0, eps_lsqr=1e-8, block=6, seed=2, core=1)),
+    # svd-free with mu > 0: the CUR target is the stacked [A; mu I] (indices may exceed m)
+    (2, 4000, 400, dict(mu=1e-3, eps_lsqr=1e-10, block=8, seed=3, max_rank=40, variant=1)),
+    (1, 400, 50, dict(mu=0.05, eps_lsqr=1e-10, block=5, seed=1, variant=1)),
+    (3, 3000, 300, dict(mu=1e-2, eps_lsqr=1e-8, block=10, seed=1, max_rank=60, variant=1)),
 ]
 
 
