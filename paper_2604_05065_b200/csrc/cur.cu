@@ -88,15 +88,16 @@ __global__ void __launch_bounds__(kSketchWarps * 32)
 sketch_ss_csc_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
                      const double* __restrict__ cval, long long m, long long n, int s, int xi,
                      const int* __restrict__ srow, const signed char* __restrict__ ssgn,
-                     double scale, double mu_scale, int aug, double* __restrict__ Y) {
+                     double scale, double mu_scale, int aug, int heavy, double* __restrict__ Y) {
   extern __shared__ double ysh[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long j = static_cast<long long>(blockIdx.x) * kSketchWarps + w;
   if (j >= n) return;
   double* yc = ysh + static_cast<long long>(w) * s;
+  const int b = cptr[j], e = cptr[j + 1];
+  if (e - b > heavy) return;  // long columns: sketch_ss_heavy_kernel
   for (int i = lane; i < s; i += 32) yc[i] = 0.0;
   __syncwarp();
-  const int b = cptr[j], e = cptr[j + 1];
   for (int p0 = b; p0 < e; p0 += 32) {
     const int p = p0 + lane;
     const double v = p < e ? cval[p] : 0.0;
@@ -119,6 +120,47 @@ sketch_ss_csc_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
   }
   __syncwarp();
   for (int i = lane; i < s; i += 32) Y[j * s + i] = yc[i];
+}
+
+// Long CSC columns (C5's Zipf head: up to 7.2M nonzeros): parallel over the
+// sketch rows instead.  Lane i of slab w owns output row 32w + i and walks the
+// column's nonzeros in ascending row order, adding +-scale*A(k, j) whenever
+// row i is one of S(:, k)'s xi rows -- the same per-element chain as the
+// reference, so Y stays bit-identical.
+__global__ void __launch_bounds__(256)
+sketch_ss_heavy_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
+                       const double* __restrict__ cval, const int* __restrict__ heavy_cols, int nheavy,
+                       long long m, int s, int xi, const int* __restrict__ srow,
+                       const signed char* __restrict__ ssgn, double scale, double mu_scale, int aug,
+                       double* __restrict__ Y) {
+  const int nslab = (s + 31) / 32;
+  const long long wid = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= static_cast<long long>(nheavy) * nslab) return;
+  const long long j = heavy_cols[wid / nslab];
+  const int i = static_cast<int>(wid % nslab) * 32 + lane;
+  const int b = cptr[j], e = cptr[j + 1];
+  double acc = 0.0;
+  for (int p0 = b; p0 < e; p0 += 32) {
+    const int p = p0 + lane;
+    const double v = p < e ? cval[p] : 0.0;
+    const int k = p < e ? ridx[p] : 0;
+    const int cnt = e - p0 < 32 ? e - p0 : 32;
+    for (int q = 0; q < cnt; ++q) {
+      const double vk = __shfl_sync(0xffffffffu, v, q);
+      const long long kq = __shfl_sync(0xffffffffu, k, q);
+      const double sv = scale * vk;
+      const int* rr = srow + kq * xi;
+      for (int t = 0; t < xi; ++t)
+        if (rr[t] == i) acc += sv * static_cast<double>(ssgn[kq * xi + t]);
+    }
+  }
+  if (aug) {
+    const int* rr = srow + (m + j) * xi;
+    for (int t = 0; t < xi; ++t)
+      if (rr[t] == i) acc += mu_scale * static_cast<double>(ssgn[(m + j) * xi + t]);
+  }
+  if (i < s) Y[j * s + i] = acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -669,9 +711,28 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
     if (!a.sparse)
       sketch_ss_dense_kernel<<<g, kSketchWarps * 32, smem, st>>>(a.dense.p, m_, n_, (int)s_, (int)x, d_rows.p,
                                                                 d_sg.p, scale, mu_scale, aug, Y_.p);
-    else
+    else {
+      // columns longer than kHeavy go to the row-parallel kernel
+      constexpr int kHeavy = 8192;
+      std::vector<int> cp(static_cast<size_t>(n_ + 1));
+      copy_sync(st, cp.data(), a.at.ptr.p, sizeof(int) * (n_ + 1), cudaMemcpyDeviceToHost);
+      std::vector<int> heavy;
+      for (i64 j = 0; j < n_; ++j)
+        if (cp[j + 1] - cp[j] > kHeavy) heavy.push_back(static_cast<int>(j));
       sketch_ss_csc_kernel<<<g, kSketchWarps * 32, smem, st>>>(a.at.ptr.p, a.at.idx.p, a.at.val.p, m_, n_, (int)s_,
-                                                              (int)x, d_rows.p, d_sg.p, scale, mu_scale, aug, Y_.p);
+                                                              (int)x, d_rows.p, d_sg.p, scale, mu_scale, aug,
+                                                              kHeavy, Y_.p);
+      if (!heavy.empty()) {
+        DBuf<int> d_heavy;
+        upload(ctx_, d_heavy, heavy.data(), static_cast<i64>(heavy.size()));
+        const long long warps = static_cast<long long>(heavy.size()) * ((s_ + 31) / 32);
+        sketch_ss_heavy_kernel<<<nb(warps * 32), 256, 0, st>>>(a.at.ptr.p, a.at.idx.p, a.at.val.p, d_heavy.p,
+                                                             static_cast<int>(heavy.size()), m_, (int)s_, (int)x,
+                                                             d_rows.p, d_sg.p, scale, mu_scale, aug, Y_.p);
+        ctx_->launches++;
+        APC_CUDA(cudaStreamSynchronize(st));
+      }
+    }
     ctx_->launches++;
     APC_CUDA(cudaStreamSynchronize(st));
   } else {

@@ -35,7 +35,7 @@ namespace apc {
 
 namespace {
 
-constexpr int kPT = 256;  // threads per CTA
+constexpr int kPT = 1024;  // threads per CTA: one fat CTA per SM keeps grid barriers cheap
 constexpr int kNW = kPT / 32;
 
 struct PArgs {
@@ -94,7 +94,7 @@ __device__ void grid_project(cg::grid_group& grid, const int* mptr, const int* m
 }
 
 template <int G>
-__global__ void __launch_bounds__(kPT, 3) lsqr_persistent_kernel(PArgs P) {
+__global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
   extern __shared__ double tsh[];  // l doubles (preconditioner)
   __shared__ double red[32];
   cg::grid_group grid = cg::this_grid();

@@ -83,13 +83,19 @@ csr_units_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
   const int lane = threadIdx.x & 31;
   if (unit >= n_units) return;
   const int b = __ldg(ustart + unit), e = __ldg(uend + unit);
-  double s0 = 0.0, s1 = 0.0;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   int q = b + lane;
-  for (; q + 32 < e; q += 64) {
-    s0 += __ldg(val + q) * __ldg(u + __ldg(idx + q));
-    s1 += __ldg(val + q + 32) * __ldg(u + __ldg(idx + q + 32));
+  // CSR(A^T) streamed with evict-first loads so the gathered u stays in L2
+  for (; q + 96 < e; q += 128) {
+    const int i0 = __ldcs(idx + q), i1 = __ldcs(idx + q + 32), i2 = __ldcs(idx + q + 64), i3 = __ldcs(idx + q + 96);
+    s0 += __ldcs(val + q) * __ldg(u + i0);
+    s1 += __ldcs(val + q + 32) * __ldg(u + i1);
+    s2 += __ldcs(val + q + 64) * __ldg(u + i2);
+    s3 += __ldcs(val + q + 96) * __ldg(u + i3);
   }
-  if (q < e) s0 += __ldg(val + q) * __ldg(u + __ldg(idx + q));
+  for (; q < e; q += 32) s0 += __ldcs(val + q) * __ldg(u + __ldcs(idx + q));
+  s0 += s2;
+  s1 += s3;
   double s = warp_sum(s0 + s1);
   if (lane == 0) {
     const int slot = __ldg(uslot + unit);

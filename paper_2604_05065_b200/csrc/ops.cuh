@@ -118,7 +118,7 @@ dense_adj_kernel(const double* __restrict__ A, long long ld, long long mloc, lon
 // ---------------------------------------------------------------------------
 // CSR A x: G lanes per row, fixed rows per block (deterministic tile slots).
 // ---------------------------------------------------------------------------
-template <int G, class Epi>
+template <int G, class Epi, int U = 1>
 __global__ void __launch_bounds__(kCsrFwdThreads)
 csr_fwd_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
                const double* __restrict__ val, long long rows, const double* __restrict__ x,
@@ -126,20 +126,42 @@ csr_fwd_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
   __shared__ double red[32];
   if (done && *done) return;
   constexpr int kGroups = kCsrFwdThreads / G;
+  // U rows in flight per lane group: more memory-level parallelism for the
+  // HBM-streaming case; U = 1 keeps small (L2-resident) matrices spread wide
   const int g = threadIdx.x / G, lane = threadIdx.x % G;
   const long long rbase = static_cast<long long>(blockIdx.x) * kCsrFwdRowsPerBlock;
   epi.begin();
   double sq = 0.0;
-  for (int k = 0; k < kCsrFwdRowsPerBlock; k += kGroups) {
-    const long long r = rbase + k + g;
-    double s = 0.0;
-    if (r < rows) {
-      const int b = __ldg(ptr + r), e = __ldg(ptr + r + 1);
-      for (int q = b + lane; q < e; q += G) s += __ldg(val + q) * __ldg(x + __ldg(idx + q));
+  for (int k = 0; k < kCsrFwdRowsPerBlock; k += kGroups * U) {
+    long long r[U];
+    int b[U], len[U];
+    int maxlen = 0;
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu) {
+      r[uu] = rbase + k + uu * kGroups + g;
+      b[uu] = 0;
+      len[uu] = 0;
+      if (k + uu * kGroups < kCsrFwdRowsPerBlock && r[uu] < rows) {
+        b[uu] = __ldg(ptr + r[uu]);
+        len[uu] = __ldg(ptr + r[uu] + 1) - b[uu];
+      }
+      maxlen = max(maxlen, len[uu]);
+    }
+    double s[U];
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu) s[uu] = 0.0;
+    // CSR arrays are streamed once (evict-first); x stays cached for the gathers
+    for (int q = lane; q < maxlen; q += G) {
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu)
+        if (q < len[uu]) s[uu] += __ldcs(val + b[uu] + q) * __ldg(x + __ldcs(idx + b[uu] + q));
     }
 #pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
-    if (lane == 0 && r < rows) sq += epi.row(r, s);
+    for (int uu = 0; uu < U; ++uu) {
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) s[uu] += __shfl_xor_sync(0xffffffffu, s[uu], o, G);
+      if (lane == 0 && k + uu * kGroups < kCsrFwdRowsPerBlock && r[uu] < rows) sq += epi.row(r[uu], s[uu]);
+    }
   }
   sq = block_sum<kCsrFwdThreads>(sq, red);
   epi.tile_done(blockIdx.x, gridDim.x, sq);
@@ -215,12 +237,22 @@ void launch_csr_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaS
   const long long rows = a.a.rows;
   const unsigned nb = static_cast<unsigned>((rows + kCsrFwdRowsPerBlock - 1) / kCsrFwdRowsPerBlock);
   if (nb == 0) return;
+  const bool big = rows >= (1LL << 21);
+#define APC_FWD_CASE(GG)                                                                                      \
+  case GG:                                                                                                    \
+    if (big) csr_fwd_kernel<GG, Epi, 4><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi); \
+    else csr_fwd_kernel<GG, Epi, 1><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi);     \
+    break;
   switch (csr_group_size(a.a.avg_row_nnz)) {
-    case 4: csr_fwd_kernel<4, Epi><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi); break;
-    case 8: csr_fwd_kernel<8, Epi><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi); break;
-    case 16: csr_fwd_kernel<16, Epi><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi); break;
-    default: csr_fwd_kernel<32, Epi><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi); break;
+    APC_FWD_CASE(4)
+    APC_FWD_CASE(8)
+    APC_FWD_CASE(16)
+    default:
+      if (big) csr_fwd_kernel<32, Epi, 4><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi);
+      else csr_fwd_kernel<32, Epi, 1><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi);
+      break;
   }
+#undef APC_FWD_CASE
   a.ctx->launches++;
 }
 
