@@ -162,6 +162,7 @@ typedef struct apc_phase_report { /* PhaseReport, solver.hpp:74-88 */
   int64_t lsqr_iters;
   double t_augment_ms, t_factor_ms, t_precond_ms, t_lsqr_ms;
   double relres_at_end;
+  double t_lsqr_device_ms; /* device time of the iteration loop (CUDA events on the library stream) */
 } apc_phase_report;
 
 typedef struct apc_trace_row { /* LsqrTraceRow, lsqr.hpp:38-47 */

@@ -98,7 +98,7 @@ class _Phase(C.Structure):
         ("phase", C.c_int32), ("reason", C.c_int32), ("rank", _i64), ("rho", C.c_double),
         ("sigma_hat", C.c_double), ("mu", C.c_double), ("lsqr_iters", _i64),
         ("t_augment_ms", C.c_double), ("t_factor_ms", C.c_double), ("t_precond_ms", C.c_double),
-        ("t_lsqr_ms", C.c_double), ("relres_at_end", C.c_double),
+        ("t_lsqr_ms", C.c_double), ("relres_at_end", C.c_double), ("t_lsqr_device_ms", C.c_double),
     ]
 
 
@@ -498,6 +498,7 @@ class PhaseReport:
     t_precond_ms: float
     t_lsqr_ms: float
     relres_at_end: float
+    t_lsqr_device_ms: float = 0.0
 
 
 @dataclasses.dataclass
@@ -543,7 +544,8 @@ def _collect(h) -> SolveResult:
     lib.apc_result_timing(h, C.byref(tt), C.byref(tl), C.byref(ts))
     tr = np.ctypeslib.as_array(trace)[: ntr.value].copy()
     ph = [PhaseReport(p.phase, p.rank, p.rho, p.sigma_hat, p.mu, p.lsqr_iters, StopReason(p.reason),
-                      p.t_augment_ms, p.t_factor_ms, p.t_precond_ms, p.t_lsqr_ms, p.relres_at_end)
+                      p.t_augment_ms, p.t_factor_ms, p.t_precond_ms, p.t_lsqr_ms, p.relres_at_end,
+                      p.t_lsqr_device_ms)
           for p in phases[: nph.value]]
     return SolveResult(None, ph, tr, SolveStatus(st.value), frho.value, frel.value, sk.value, smv.value,
                        rows, cols, rho, tt.value, tl.value, ts.value)

@@ -72,7 +72,8 @@ def build(verbose: bool = False) -> Path:
     newest = max(Path(o).stat().st_mtime for o in objs)
     if not LIB.exists() or LIB.stat().st_mtime < newest:
         tmp = LIB.with_suffix(".so.tmp")
-        _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, *_nccl_link_args(), "-lpthread"])
+        _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, *_nccl_link_args(), "-L/usr/local/cuda/lib64",
+              "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-lpthread"])
         shutil.move(str(tmp), str(LIB))
     return LIB
 

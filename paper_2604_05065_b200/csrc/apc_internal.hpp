@@ -112,6 +112,7 @@ struct apc_ctx {
   int nranks = 1, rank = 0;
   cudaStream_t stream = nullptr;
   void* nccl = nullptr;  // ncclComm_t when nranks > 1
+  void* blas = nullptr;  // cublasHandle_t (created lazily, bound to `stream`)
   std::string err;
   apc::i64 err_index = -1;
   int num_sms = 148;

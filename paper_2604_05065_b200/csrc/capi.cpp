@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "apc_internal.hpp"
+#include "blas.hpp"
 #include "host_rng.hpp"
 #include "lsqr.hpp"
 #include "ops_host.hpp"
@@ -173,6 +174,7 @@ int apc_ctx_destroy(apc_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     comm_destroy(ctx);
+    blas_destroy(ctx);
     ctx->scratch_d.release();
     ctx->counters.release();
     cudaStreamDestroy(ctx->stream);

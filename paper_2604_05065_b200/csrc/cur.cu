@@ -14,6 +14,7 @@
 #include <functional>
 #include <numeric>
 
+#include "blas.hpp"
 #include "cur.hpp"
 #include "dev_common.cuh"
 #include "ops.cuh"
@@ -597,6 +598,26 @@ __global__ void crow_fill_kernel(const int* ptr, const int* idx, const double* v
   }
 }
 
+// C = A(:, J) dense (m x l column-major) from a dense A
+__global__ void gather_cols_kernel(const double* A, long long m, const long long* J, long long l, double* C) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= m * l) return;
+  const long long t = e / m, i = e % m;
+  C[e] = A[J[t] * m + i];
+}
+
+// rows [r0, r0 + rb) of C = A(:, J) densified from CSR(A) (rb x l, zero-filled by caller)
+__global__ void densify_rows_kernel(const int* ptr, const int* idx, const double* val, long long r0, long long rb,
+                                    const int* colpos, double* D) {
+  const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= rb) return;
+  const long long i = r0 + q;
+  for (int p = ptr[i]; p < ptr[i + 1]; ++p) {
+    const int t = colpos[idx[p]];
+    if (t >= 0) D[static_cast<long long>(t) * rb + q] = val[p];
+  }
+}
+
 __global__ void set_flags_kernel(int* flags, const long long* ids, long long cnt, int value) {
   const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e < cnt) flags[ids[e]] = value;
@@ -947,6 +968,42 @@ void DeviceCur::upload_core() {
     upload(ctx_, core_a_, core_.lu.data(), l * l);
     upload(ctx_, core_perm_, reinterpret_cast<const long long*>(core_.perm.data()), l);
   }
+}
+
+// G = C^T C of the target's selected columns (l x l, full), on the device:
+// gather + DSYRK for dense A, row blocks densified + DSYRK accumulated in
+// fixed order for sparse A; + amu^2 I for the augmented stack.
+Vec DeviceCur::c_gram() const {
+  const i64 l = rank();
+  cudaStream_t st = ctx_->stream;
+  DBuf<long long> d_J;
+  upload(ctx_, d_J, reinterpret_cast<const long long*>(J_.data()), l);
+  DBuf<double> G(l * l);
+  if (!a_.sparse) {
+    DBuf<double> C(m_ * l);
+    gather_cols_kernel<<<nb(m_ * l), kT, 0, st>>>(a_.dense.p, m_, d_J.p, l, C.p);
+    ctx_->launches++;
+    dsyrk_t(ctx_, l, m_, 1.0, C.p, m_, 0.0, G.p, l);
+  } else {
+    DBuf<int> colpos(n_);
+    APC_CUDA(cudaMemsetAsync(colpos.p, 0xff, colpos.bytes(), st));
+    set_colpos_kernel<<<nb(l), kT, 0, st>>>(colpos.p, d_J.p, l);
+    const i64 rb = std::min<i64>(m_, std::max<i64>(1, (1LL << 28) / std::max<i64>(1, l)));  // <= 2 GB blocks
+    DBuf<double> D(rb * l);
+    for (i64 r0 = 0; r0 < m_; r0 += rb) {
+      const i64 cnt = std::min(rb, m_ - r0);
+      APC_CUDA(cudaMemsetAsync(D.p, 0, sizeof(double) * cnt * l, st));
+      densify_rows_kernel<<<nb(cnt), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p, r0, cnt, colpos.p, D.p);
+      dsyrk_t(ctx_, l, cnt, 1.0, D.p, cnt, r0 == 0 ? 0.0 : 1.0, G.p, l);
+      ctx_->launches++;
+    }
+  }
+  Vec g = download(ctx_, G.p, l * l);
+  for (i64 j = 0; j < l; ++j)
+    for (i64 i = j + 1; i < l; ++i) g[j * l + i] = g[i * l + j];  // mirror the upper triangle
+  if (amu_ > 0.0)
+    for (i64 t = 0; t < l; ++t) g[t * l + t] += amu_ * amu_;
+  return g;
 }
 
 Vec DeviceCur::r_dense_rows(i64 first, i64 count) const {

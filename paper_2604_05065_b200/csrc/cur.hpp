@@ -60,6 +60,8 @@ class DeviceCur {
   // host copies used by the preconditioner builders
   Vec r_dense_rows(i64 first, i64 count) const;  // rows I[first..first+count) of A, row-major count x n
   Vec c_dense() const;                           // dense target_rows x l, column-major (dense A only)
+  Vec c_gram() const;                            // C^T C (l x l), computed on the device
+  const double* r_rows_dev(i64 first) const { return Rrm_.p + first * n_; }  // row-major rows of R
   // sparse C / R on the host (CSC of C = A(:,J), CSC of R^T = A(I,:)^T)
   void c_csc(std::vector<i64>& ptr, std::vector<i64>& idx, Vec& val) const;
   void rt_csc(std::vector<i64>& ptr, std::vector<i64>& idx, Vec& val) const;

@@ -44,7 +44,8 @@ struct PhaseOut {
   int reason = 0;
   bool breakdown = false;
   std::vector<TraceRowH> rows;
-  double ms = 0.0;
+  double ms = 0.0;         // host wall time of the phase (init + loop + readback)
+  double device_ms = 0.0;  // CUDA-event time of the iteration loop on the library stream
 };
 
 struct LsqrWork;  // device workspace, opaque

@@ -1,13 +1,16 @@
 // Preconditioner construction per rebuild (preconditioner.hpp:138-396,
 // 424-592) and its upload as the device form I + B K B^T / I + R^T G R that
-// the LSQR loop applies (lsqr.cu).  The l x l algebra (Gram factors, core
-// spectrum, middle operators) runs on the host with the restated reference
-// routines; it is not index-affecting, so only the x / iteration
-// parity bar applies to it.
+// the LSQR loop applies (lsqr.cu).  The tall products (C^T C, Q^T c, Q p,
+// Q_R V_M) run on the device through cuBLAS; the l x l algebra (Cholesky of
+// the Gram matrix, core spectrum, middle operators) runs on the host with the
+// restated reference routines.  None of it is index-affecting:
+// only the x / iteration parity bar applies.
 #include <cmath>
 
+#include "blas.hpp"
 #include "cur.hpp"
 #include "precond.hpp"
+#include "svd.hpp"
 
 namespace apc {
 
@@ -43,25 +46,16 @@ Vec densify_csc(i64 m, i64 k, const std::vector<i64>& cp, const std::vector<i64>
   return d;
 }
 
-// QrAccumulator::factor_checked (preconditioner.hpp:486-505)
-QT factor_checked(i64 m, i64 k, Vec e, double scale) {
-  Householder f = householder(m, k, std::move(e));
-  for (i64 j = 0; j < k; ++j)
-    if (std::fabs(f.a[j * m + j]) <= 1e-12 * scale)
-      fail(APC_RANK_DEFICIENT, "QrAccumulator: dependent block", j);
-  QT r;
-  r.m = m;
-  r.k = k;
-  r.q = thin_q(f);
-  r.t = upper_of(f);
-  normalise_signs(m, k, r.q, r.t);
-  return r;
-}
-
 void upload_vec(apc_ctx* ctx, DBuf<double>& d, const Vec& h) {
   d.alloc(std::max<i64>(1, static_cast<i64>(h.size())));
   if (!h.empty())
     APC_CUDA(cudaMemcpyAsync(d.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, ctx->stream));
+}
+
+Vec download_vec(apc_ctx* ctx, const double* d, i64 n) {
+  Vec h(static_cast<size_t>(n));
+  copy_sync(ctx->stream, h.data(), d, sizeof(double) * n, cudaMemcpyDeviceToHost);
+  return h;
 }
 
 // host CSC (columns = rows of R) -> device CSR(R) (l x n) and CSR(R^T) (n x l)
@@ -71,7 +65,6 @@ void upload_r(apc_ctx* ctx, i64 n, i64 l, const std::vector<i64>& cp, const std:
   std::vector<int> rptr(l + 1), ridx(nnz);
   for (i64 i = 0; i <= l; ++i) rptr[i] = static_cast<int>(cp[i]);
   for (i64 q = 0; q < nnz; ++q) ridx[q] = static_cast<int>(ri[q]);
-  // transpose: row j of R^T lists (i, R(i, j)) for i ascending
   std::vector<int> tptr(n + 1, 0), tidx(nnz);
   Vec tval(nnz);
   for (i64 q = 0; q < nnz; ++q) tptr[ri[q] + 1]++;
@@ -85,7 +78,8 @@ void upload_r(apc_ctx* ctx, i64 n, i64 l, const std::vector<i64>& cp, const std:
     }
   auto up_i = [&](DBuf<int>& d, const std::vector<int>& h) {
     d.alloc(std::max<i64>(1, static_cast<i64>(h.size())));
-    APC_CUDA(cudaMemcpyAsync(d.p, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice, ctx->stream));
+    if (!h.empty())
+      APC_CUDA(cudaMemcpyAsync(d.p, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice, ctx->stream));
   };
   p.R.rows = l;
   p.R.cols = n;
@@ -104,7 +98,6 @@ void upload_r(apc_ctx* ctx, i64 n, i64 l, const std::vector<i64>& cp, const std:
 
 // G = T^{-1} K T^{-T} for an implicit basis Q = R^T T^{-1} (l x l, T upper)
 Vec conjugate_by_tinv(i64 l, const Vec& t, const Vec& K) {
-  // X = T^{-1} K  (column by column), then G = X T^{-T} = (T^{-1} X^T)^T
   Vec X = K;
   for (i64 j = 0; j < l; ++j) tri_solve(l, t.data(), X.data() + j * l, false);
   Vec Xt = transpose(l, l, X);
@@ -112,55 +105,95 @@ Vec conjugate_by_tinv(i64 l, const Vec& t, const Vec& K) {
   return transpose(l, l, Xt);
 }
 
+// mirror an upper-filled square matrix into a full symmetric one
+void symmetrize_upper(i64 n, Vec& g) {
+  for (i64 j = 0; j < n; ++j)
+    for (i64 i = j + 1; i < n; ++i) g[j * n + i] = g[i * n + j];
+}
+
+// upper R with R^T R = e^T e for a device block (CholeskyQR, e <- e R^{-1})
+Vec cholqr_step(apc_ctx* ctx, i64 m, i64 b, double* e) {
+  DBuf<double> G(b * b);
+  dsyrk_t(ctx, b, m, 1.0, e, m, 0.0, G.p, b);
+  Vec g = download_vec(ctx, G.p, b * b);
+  symmetrize_upper(b, g);
+  Vec r;
+  try {
+    r = chol_upper(b, g, "QrAccumulator: dependent block");
+  } catch (const Status& s) {
+    fail(APC_RANK_DEFICIENT, "QrAccumulator: dependent block", s.index);
+  }
+  DBuf<double> R(b * b);
+  upload_vec(ctx, R, r);
+  dtrsm_right_upper(ctx, m, b, R.p, b, e, m);
+  APC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return r;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
-void QrAcc::append(i64 m, i64 b, Vec c) {  // preconditioner.hpp:435-476
+void DevQrAcc::append(i64 m, i64 b, const double* c) {  // preconditioner.hpp:435-476
   require(b >= 1, APC_INVALID_ARGUMENT, "QrAccumulator: empty block");
+  cudaStream_t st = ctx->stream;
+  // incoming column scale (max column norm of the new block)
+  Vec ch = download_vec(ctx, c, m * b);
   double scale = 0.0;
-  for (i64 j = 0; j < b; ++j) scale = std::max(scale, col_norm(m, c.data() + j * m));
-  if (k == 0) {
-    QT qr = factor_checked(m, b, std::move(c), scale);
-    rows = m;
-    k = b;
-    q = std::move(qr.q);
-    t = std::move(qr.t);
-    return;
+  for (i64 j = 0; j < b; ++j) scale = std::max(scale, col_norm(m, ch.data() + j * m));
+  if (k > 0) require(m == rows, APC_DIMENSION_MISMATCH, "QrAccumulator: row count mismatch");
+  DBuf<double> e(m * b);
+  APC_CUDA(cudaMemcpyAsync(e.p, c, sizeof(double) * m * b, cudaMemcpyDeviceToDevice, st));
+  Vec p1(static_cast<size_t>(k * b), 0.0), p2(static_cast<size_t>(k * b), 0.0);
+  if (k > 0) {  // two projection passes: e = c - Q Q^T c, then once more
+    DBuf<double> P(k * b);
+    dgemm(ctx, true, false, k, b, m, 1.0, q.p, m, e.p, m, 0.0, P.p, k);
+    dgemm(ctx, false, false, m, b, k, -1.0, q.p, m, P.p, k, 1.0, e.p, m);
+    p1 = download_vec(ctx, P.p, k * b);
+    dgemm(ctx, true, false, k, b, m, 1.0, q.p, m, e.p, m, 0.0, P.p, k);
+    dgemm(ctx, false, false, m, b, k, -1.0, q.p, m, P.p, k, 1.0, e.p, m);
+    p2 = download_vec(ctx, P.p, k * b);
   }
-  require(m == rows, APC_DIMENSION_MISMATCH, "QrAccumulator: row count mismatch");
-  const Vec qt = transpose(m, k, q);
-  Vec p1 = matmul(k, m, b, qt, c);
-  Vec qp = matmul(m, k, b, q, p1);
-  Vec e = c;
-  for (size_t s = 0; s < e.size(); ++s) e[s] -= qp[s];
-  Vec p2 = matmul(k, m, b, qt, e);
-  Vec qp2 = matmul(m, k, b, q, p2);
-  for (size_t s = 0; s < e.size(); ++s) e[s] -= qp2[s];
-  QT qr = factor_checked(m, b, std::move(e), scale);
-  const i64 n0 = k, nt = k + b;
-  Vec qn(static_cast<size_t>(m * nt));
-  std::copy(q.begin(), q.end(), qn.begin());
-  std::copy(qr.q.begin(), qr.q.end(), qn.begin() + m * n0);
+  // factor the block: Householder on the host when small, CholeskyQR2 on the device otherwise
+  Vec rb;
+  if (static_cast<double>(m) * b * b <= 2e8) {
+    Vec eh = download_vec(ctx, e.p, m * b);
+    Householder f = householder(m, b, std::move(eh));
+    for (i64 j = 0; j < b; ++j)
+      if (std::fabs(f.a[j * m + j]) <= 1e-12 * scale) fail(APC_RANK_DEFICIENT, "QrAccumulator: dependent block", j);
+    Vec qe = thin_q(f);
+    rb = upper_of(f);
+    normalise_signs(m, b, qe, rb);
+    APC_CUDA(cudaMemcpyAsync(e.p, qe.data(), sizeof(double) * m * b, cudaMemcpyHostToDevice, st));
+    APC_CUDA(cudaStreamSynchronize(st));
+  } else {
+    Vec r1 = cholqr_step(ctx, m, b, e.p);
+    Vec r2 = cholqr_step(ctx, m, b, e.p);
+    rb = matmul(b, b, b, r2, r1);
+    for (i64 j = 0; j < b; ++j)
+      if (std::fabs(rb[j * b + j]) <= 1e-12 * scale) fail(APC_RANK_DEFICIENT, "QrAccumulator: dependent block", j);
+  }
+  // Q <- [Q, q_e]
+  if (k + b > cap) {
+    const i64 ncap = std::max(2 * cap, k + b);
+    DBuf<double> nq(m * ncap);
+    if (k > 0) APC_CUDA(cudaMemcpyAsync(nq.p, q.p, sizeof(double) * m * k, cudaMemcpyDeviceToDevice, st));
+    q = std::move(nq);
+    cap = ncap;
+  }
+  APC_CUDA(cudaMemcpyAsync(q.p + m * k, e.p, sizeof(double) * m * b, cudaMemcpyDeviceToDevice, st));
+  // T <- [[T, p1 + p2], [0, R_e]]
+  const i64 nt = k + b;
   Vec tn(static_cast<size_t>(nt * nt), 0.0);
-  for (i64 j = 0; j < n0; ++j)
-    for (i64 i = 0; i <= j; ++i) tn[j * nt + i] = t[j * n0 + i];
+  for (i64 j = 0; j < k; ++j)
+    for (i64 i = 0; i <= j; ++i) tn[j * nt + i] = t[j * k + i];
   for (i64 j = 0; j < b; ++j)
-    for (i64 i = 0; i < n0; ++i) tn[(n0 + j) * nt + i] = p1[j * n0 + i] + p2[j * n0 + i];
+    for (i64 i = 0; i < k; ++i) tn[(k + j) * nt + i] = p1[j * k + i] + p2[j * k + i];
   for (i64 j = 0; j < b; ++j)
-    for (i64 i = 0; i <= j; ++i) tn[(n0 + j) * nt + n0 + i] = qr.t[j * b + i];
-  q = std::move(qn);
+    for (i64 i = 0; i <= j; ++i) tn[(k + j) * nt + k + i] = rb[j * b + i];
   t = std::move(tn);
+  rows = m;
   k = nt;
-}
-
-// gram_factor (preconditioner.hpp:143-150): Cholesky of C^T C, QR fallback
-Vec gram_factor_dense(i64 m, i64 k, const Vec& c) {
-  try {
-    return chol_gram_dense(m, k, c.data());
-  } catch (const Status& s) {
-    if (s.code != APC_NOT_POSITIVE) throw;
-    return thin_qr(m, k, c).t;
-  }
+  APC_CUDA(cudaStreamSynchronize(st));
 }
 
 Vec gram_factor_sparse(i64 m, i64 k, const std::vector<i64>& cp, const std::vector<i64>& ri, const Vec& va) {
@@ -180,15 +213,26 @@ void build_precond(const BuildInputs& in, PrecondDev& p, PrecondInfo& info) {
   p = PrecondDev();
   p.n = n;
   p.l = l;
-  // T_C = gram_factor(C)
-  Vec t_c = in.c_sparse ? gram_factor_sparse(in.m, l, in.c_ptr, in.c_idx, in.c_val)
-                        : gram_factor_dense(in.m, l, in.c_dense);
-  Vec K;
+  // T_C = gram_factor(C): Cholesky of the device Gram, QR fallback (preconditioner.hpp:143-150)
+  Vec t_c;
+  try {
+    t_c = chol_upper(l, in.gram, "chol_gram: non-positive pivot");
+  } catch (const Status& s) {
+    if (s.code != APC_NOT_POSITIVE) throw;
+    t_c = thin_qr(in.m, l, in.c_dense()).t;
+  }
   if (in.variant == 0) {
     // SVD form: M = T_C U T_R^T, small_svd(M) (preconditioner.hpp:158-192)
     Vec ut = in.core->solve_matrix(l, transpose(l, l, *in.t_r));
     Vec mm = matmul(l, l, l, t_c, ut);
-    SvdH s = small_svd(l, l, mm);
+    require(l <= 4096, APC_INVALID_ARGUMENT, "small_svd: dimension exceeds the small-problem cap");
+    SvdH s;
+    if (l > 256) {  // parallel-order Jacobi on the device; serial cyclic on the host for small cores
+      s.m = s.n = l;
+      device_jacobi_svd(ctx, l, mm, s.sigma, s.v);
+    } else {
+      s = small_svd(l, l, mm);
+    }
     info.sigma_cur = s.sigma;
     info.sigma_reg.resize(l);
     for (i64 i = 0; i < l; ++i) info.sigma_reg[i] = std::sqrt(s.sigma[i] * s.sigma[i] + in.mu * in.mu);
@@ -197,25 +241,26 @@ void build_precond(const BuildInputs& in, PrecondDev& p, PrecondInfo& info) {
     Vec d(l);
     for (i64 i = 0; i < l; ++i) d[i] = info.sigma_hat / info.sigma_reg[i] - 1.0;
     if (!in.implicit) {
-      // V = Q_R V_M (explicit, n x l), K = diag(d)
+      // V = Q_R V_M (explicit, n x l, on the device), K = diag(d)
       p.kind = 1;
-      upload_vec(ctx, p.B, matmul(n, l, l, *in.q_r, s.v));
-      K.assign(static_cast<size_t>(l * l), 0.0);
+      DBuf<double> vm;
+      upload_vec(ctx, vm, s.v);
+      p.B.alloc(n * l);
+      dgemm(ctx, false, false, n, l, l, 1.0, in.q_dev, n, vm.p, l, 0.0, p.B.p, n);
+      Vec K(static_cast<size_t>(l * l), 0.0);
       for (i64 i = 0; i < l; ++i) K[i * l + i] = d[i];
       upload_vec(ctx, p.Kf, K);
       upload_vec(ctx, p.Ka, K);
+      APC_CUDA(cudaStreamSynchronize(ctx->stream));
     } else {
-      // V = R^T T_R^{-1} V_M: G = W diag(d) W^T with W = T_R^{-1} V_M
+      // V = R^T T_R^{-1} V_M: G = W diag(d) W^T with W = T_R^{-1} V_M (symmetric)
       p.kind = 2;
       Vec W = s.v;
       for (i64 j = 0; j < l; ++j) tri_solve(l, in.t_r->data(), W.data() + j * l, false);
-      Vec G(static_cast<size_t>(l * l), 0.0);
-      for (i64 j = 0; j < l; ++j)
-        for (i64 i = 0; i < l; ++i) {
-          double acc = 0.0;
-          for (i64 t = 0; t < l; ++t) acc += W[t * l + i] * d[t] * W[t * l + j];
-          G[j * l + i] = acc;
-        }
+      Vec WD = W;
+      for (i64 t = 0; t < l; ++t)
+        for (i64 i = 0; i < l; ++i) WD[t * l + i] *= d[t];
+      Vec G = matmul(l, l, l, WD, transpose(l, l, W));
       upload_r(ctx, n, l, in.r_ptr, in.r_idx, in.r_val, p);
       upload_vec(ctx, p.Kf, G);
       upload_vec(ctx, p.Ka, G);
@@ -248,7 +293,8 @@ void build_precond(const BuildInputs& in, PrecondDev& p, PrecondInfo& info) {
     // the device keeps the middle operators row-major (warp per output row)
     if (!in.implicit) {
       p.kind = 1;
-      upload_vec(ctx, p.B, *in.q_r);
+      p.B.alloc(n * l);
+      APC_CUDA(cudaMemcpyAsync(p.B.p, in.q_dev, sizeof(double) * n * l, cudaMemcpyDeviceToDevice, ctx->stream));
       upload_vec(ctx, p.Kf, transpose(l, l, Kf));
       upload_vec(ctx, p.Ka, transpose(l, l, Ka));
     } else {

@@ -1,6 +1,7 @@
 // Preconditioner construction (precond.cpp).
 #pragma once
 
+#include <functional>
 #include <vector>
 
 #include "host_dense.hpp"
@@ -9,32 +10,34 @@
 namespace apc {
 
 // QrAccumulator (preconditioner.hpp:424-509): growing thin QR of R^T with one
-// re-orthogonalisation pass per appended block.
-struct QrAcc {
-  i64 rows = 0, k = 0;
-  Vec q, t;  // rows x k, k x k
-  void append(i64 m, i64 b, Vec newcols);
-  void clear() { rows = k = 0; q.clear(); t.clear(); }
+// re-orthogonalisation pass per appended block.  Q lives on the device (the
+// projections are cuBLAS GEMMs); the block factorisation is Householder on the
+// host for small blocks and CholeskyQR2 on the device for tall ones.  T is
+// small and stays on the host.
+struct DevQrAcc {
+  apc_ctx* ctx = nullptr;
+  i64 rows = 0, k = 0, cap = 0;
+  DBuf<double> q;  // rows x cap, column-major (first k columns valid)
+  Vec t;           // k x k upper
+  // append the b columns of the device block c (rows x b, column-major)
+  void append(i64 m, i64 b, const double* c);
+  void clear() { rows = k = 0; t.clear(); }
 };
 
-Vec gram_factor_dense(i64 m, i64 k, const Vec& c);
 Vec gram_factor_sparse(i64 m, i64 k, const std::vector<i64>& cp, const std::vector<i64>& ri, const Vec& va);
 
 struct BuildInputs {
   apc_ctx* ctx = nullptr;
   int variant = 0;  // 0 svd, 1 svd_free
   bool implicit = false;
-  i64 m = 0, n = 0, l = 0;
+  i64 m = 0, n = 0, l = 0;  // m: target rows (C's rows)
   double mu = 0.0, target_level = 0.0;
   const CoreFactorH* core = nullptr;
   const Vec* block = nullptr;  // intersection A(I, J), l x l
   const Vec* t_r = nullptr;    // T_R (l x l upper)
-  const Vec* q_r = nullptr;    // explicit Q_R (n x l)
-  // C = A(:, J)
-  bool c_sparse = false;
-  Vec c_dense;
-  std::vector<i64> c_ptr, c_idx;
-  Vec c_val;
+  const double* q_dev = nullptr;  // explicit Q_R on the device (n x l, ld = n)
+  Vec gram;                       // C^T C (l x l), from the device
+  std::function<Vec()> c_dense;   // C densified on the host (QR fallback only)
   // R = A(I, :) as CSC of R^T (implicit)
   std::vector<i64> r_ptr, r_idx;
   Vec r_val;

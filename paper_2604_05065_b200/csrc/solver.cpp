@@ -63,7 +63,8 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
   const double density = (m * n == 0) ? 0.0 : static_cast<double>(a.nnz_global) / static_cast<double>(m * n);
   const bool implicit_mode = a.sparse && density < 0.10;
 
-  QrAcc qr_acc;
+  DevQrAcc qr_acc;
+  qr_acc.ctx = ctx;
   Vec t_r_implicit;
   auto* res = new apc_result();
   std::unique_ptr<apc_result> guard(res);
@@ -110,6 +111,7 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
     rep.lsqr_iters = po.iters;
     rep.reason = po.reason;
     rep.t_lsqr_ms = ms_since(t0);
+    rep.t_lsqr_device_ms = po.device_ms;
     res->lsqr_ms += po.ms;
     rep.relres_at_end = bnorm > 0.0 ? std::sqrt(residual(a, vw, d_x.p, d_b.p, nullptr)) / bnorm : 0.0;
   };
@@ -156,13 +158,13 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
         t_r_implicit = gram_factor_sparse(n, l, rp, ri, rv);
       } else {
         const i64 added = cur.last_added();
-        Vec newblock = cur.r_dense_rows(l - added, added);  // row-major added x n == column-major n x added
+        // rows of R are stored row-major on the device: added x n == column-major n x added
         try {
-          qr_acc.append(n, added, std::move(newblock));
+          qr_acc.append(n, added, cur.r_rows_dev(l - added));
         } catch (const Status& e) {
           if (!is_solver_error(e)) throw;
           qr_acc.clear();
-          qr_acc.append(n, l, cur.r_dense_rows(0, l));  // full refactorisation
+          qr_acc.append(n, l, cur.r_rows_dev(0));  // full refactorisation
         }
       }
       if (cur.rank() >= max_rank) {
@@ -199,10 +201,19 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
         in.core = &cur.core();
         in.block = &cur.intersection();
         in.t_r = implicit_mode ? &t_r_implicit : &qr_acc.t;
-        in.q_r = &qr_acc.q;
-        in.c_sparse = full.sparse;
-        if (full.sparse) cur.c_csc(in.c_ptr, in.c_idx, in.c_val);
-        else in.c_dense = cur.c_dense();
+        in.q_dev = qr_acc.q.p;
+        in.gram = cur.c_gram();
+        in.c_dense = [&cur, &full]() -> Vec {  // only for the QR fallback of gram_factor
+          if (!full.sparse) return cur.c_dense();
+          std::vector<i64> cp, ci;
+          Vec cv;
+          cur.c_csc(cp, ci, cv);
+          const i64 mt = cur.target_rows(), l = cur.rank();
+          Vec d(static_cast<size_t>(mt * l), 0.0);
+          for (i64 j = 0; j < l; ++j)
+            for (i64 q = cp[j]; q < cp[j + 1]; ++q) d[j * mt + ci[q]] = cv[q];
+          return d;
+        };
         if (implicit_mode) cur.rt_csc(in.r_ptr, in.r_idx, in.r_val);
         build_precond(in, P, info);
       } catch (const Status& e) {

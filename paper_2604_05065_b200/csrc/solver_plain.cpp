@@ -78,6 +78,7 @@ apc_result* plain_solve(apc_mat& a, const double* b, const apc_solver_config& cf
   rep.mu = mu;
   rep.lsqr_iters = po.iters;
   rep.t_lsqr_ms = po.ms;
+  rep.t_lsqr_device_ms = po.device_ms;
   rep.relres_at_end = rr;
   r->phases.push_back(rep);
   r->last_reason = po.reason;
