@@ -170,52 +170,82 @@ sketch_ss_heavy_kernel(const int* __restrict__ cptr, const int* __restrict__ rid
 // whose k loop runs in order with separate DMUL/DADD: the exact chain of the
 // reference, at GEMM data reuse.
 // ---------------------------------------------------------------------------
-constexpr int kGT = 64, kGK = 16;
+// Tile 96 (sketch rows) x 64 (columns of A), k in chunks of 16, double-buffered
+// shared memory with a register prefetch of the next chunk; each thread owns a
+// 6 x 4 block strided by 16 so shared reads are conflict-free or broadcast.
+constexpr int kGI = 96, kGJ = 64, kGK = 16, kGA = kGI / 16, kGC = kGJ / 16;
 
 __global__ void __launch_bounds__(256)
 sketch_gauss_dense_kernel(const double* __restrict__ S, int s, const double* __restrict__ A, long long m,
                           long long n, double* __restrict__ Y) {
-  __shared__ double Ss[kGK][kGT + 1];
-  __shared__ double As[kGK][kGT + 1];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const long long i0 = static_cast<long long>(blockIdx.y) * kGT;
-  const long long j0 = static_cast<long long>(blockIdx.x) * kGT;
-  double acc[4][4];
+  __shared__ double Ss[2][kGK][kGI];
+  __shared__ double As[2][kGK][kGJ];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const long long i0 = static_cast<long long>(blockIdx.y) * kGI;
+  const long long j0 = static_cast<long long>(blockIdx.x) * kGJ;
+  constexpr int kSL = kGK * kGI / 256, kAL = kGK * kGJ / 256;  // loads per thread per chunk
+  double rs[kSL], ra[kAL];
+  auto fetch = [&](long long k0) {
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+    for (int r = 0; r < kSL; ++r) {
+      const int e = tid + 256 * r, kk = e / kGI, ii = e % kGI;
+      const long long k = k0 + kk;
+      rs[r] = (k < m && i0 + ii < s) ? S[k * s + i0 + ii] : 0.0;
+    }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+    for (int r = 0; r < kAL; ++r) {
+      const int e = tid + 256 * r, jj = e / kGK, kk = e % kGK;
+      const long long k = k0 + kk;
+      ra[r] = (k < m && j0 + jj < n) ? A[(j0 + jj) * m + k] : 0.0;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int r = 0; r < kSL; ++r) {
+      const int e = tid + 256 * r;
+      Ss[buf][e / kGI][e % kGI] = rs[r];
+    }
+#pragma unroll
+    for (int r = 0; r < kAL; ++r) {
+      const int e = tid + 256 * r;
+      As[buf][e % kGK][e / kGK] = ra[r];
+    }
+  };
+  double acc[kGA][kGC];
+#pragma unroll
+  for (int a = 0; a < kGA; ++a)
+#pragma unroll
+    for (int c = 0; c < kGC; ++c) acc[a][c] = 0.0;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  int buf = 0;
   for (long long k0 = 0; k0 < m; k0 += kGK) {
-    for (int e = threadIdx.x; e < kGK * kGT; e += 256) {
-      const int kk = e / kGT, ii = e % kGT;
-      const long long k = k0 + kk;
-      Ss[kk][ii] = (k < m && i0 + ii < s) ? S[k * s + i0 + ii] : 0.0;
+    const bool more = k0 + kGK < m;
+    if (more) fetch(k0 + kGK);  // global loads in flight during the chunk's arithmetic
+#pragma unroll 4
+    for (int kk = 0; kk < kGK; ++kk) {
+      double sa[kGA], ab[kGC];
+#pragma unroll
+      for (int a = 0; a < kGA; ++a) sa[a] = Ss[buf][kk][ty + 16 * a];
+#pragma unroll
+      for (int c = 0; c < kGC; ++c) ab[c] = As[buf][kk][tx + 16 * c];
+#pragma unroll
+      for (int a = 0; a < kGA; ++a)
+#pragma unroll
+        for (int c = 0; c < kGC; ++c) acc[a][c] = __dadd_rn(acc[a][c], __dmul_rn(ab[c], sa[a]));
     }
-    for (int e = threadIdx.x; e < kGK * kGT; e += 256) {
-      const int jj = e / kGK, kk = e % kGK;
-      const long long k = k0 + kk;
-      As[kk][jj] = (k < m && j0 + jj < n) ? A[(j0 + jj) * m + k] : 0.0;
+    if (more) {
+      stash(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
     }
-    __syncthreads();
-    const int kmax = static_cast<int>(m - k0 < kGK ? m - k0 : kGK);
-    for (int kk = 0; kk < kmax; ++kk) {
-      double sa[4], ab[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) sa[a] = Ss[kk][ty * 4 + a];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) ab[c] = As[kk][tx * 4 + c];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][c] = __dadd_rn(acc[a][c], __dmul_rn(ab[c], sa[a]));
-    }
-    __syncthreads();
   }
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < kGA; ++a)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const long long i = i0 + ty * 4 + a, j = j0 + tx * 4 + c;
+    for (int c = 0; c < kGC; ++c) {
+      const long long i = i0 + ty + 16 * a, j = j0 + tx + 16 * c;
       if (i < s && j < n) Y[j * s + i] = acc[a][c];
     }
 }
@@ -765,7 +795,7 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
     DBuf<double> d_S;
     upload(ctx_, d_S, S.data(), s_ * m_);
     if (!a.sparse) {
-      dim3 grid(static_cast<unsigned>((n_ + kGT - 1) / kGT), static_cast<unsigned>((s_ + kGT - 1) / kGT));
+      dim3 grid(static_cast<unsigned>((n_ + kGJ - 1) / kGJ), static_cast<unsigned>((s_ + kGI - 1) / kGI));
       sketch_gauss_dense_kernel<<<grid, 256, 0, st>>>(d_S.p, (int)s_, a.dense.p, m_, n_, Y_.p);
     } else {
       sketch_gauss_csc_kernel<<<nb(n_ * 32), kT, 0, st>>>(d_S.p, (int)s_, a.at.ptr.p, a.at.idx.p, a.at.val.p, n_,

@@ -21,6 +21,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "dev_common.cuh"
 #include "lsqr.hpp"
@@ -48,6 +49,7 @@ struct PArgs {
   double mu;
   int has_tail;
   int group;  // lanes per row of the forward SpMV (4/8/16/32)
+  int zsmem;  // 1: z staged per CTA in shared memory (n small)
   // preconditioner (implicit) or identity
   int pre;
   const int *rptr, *ridx;
@@ -113,7 +115,10 @@ __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
   long long j = st->iter;
   const unsigned long long t0 = st->t0_ns;
   if (st->done) return;
-  const double* zsrc = P.pre ? P.z : P.v;
+  // small n: every CTA builds its own copy of z in shared memory (the forward
+  // SpMV then gathers from smem instead of L2, and the z stage needs no grid
+  // barrier); otherwise z goes through global memory
+  const double* zsrc = P.zsmem ? tsh : (P.pre ? P.z : P.v);
 
   for (;;) {
     // ---- S1/S2: z = v + R^T Gf R v
@@ -122,6 +127,17 @@ __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
       grid_project(grid, P.rptr, P.ridx, P.rval, P.Gf, P.l, P.v, P.t, P.s, gwarp, nwarps, lane);
       grid.sync();
       STAMP(1);
+    }
+    if (P.zsmem) {
+      for (long long c = threadIdx.x; c < P.n; c += kPT) {
+        double acc = 0.0;
+        if (P.pre)
+          for (int q = P.rtptr[c]; q < P.rtptr[c + 1]; ++q) acc += P.rtval[q] * P.s[P.rtidx[q]];
+        tsh[c] = P.pre ? P.v[c] + acc : P.v[c];
+      }
+      __syncthreads();
+      STAMP(2);
+    } else if (P.pre) {
       for (long long c = gtid; c < P.n; c += gsize) {
         double acc = 0.0;
         for (int q = P.rtptr[c]; q < P.rtptr[c + 1]; ++q) acc += P.rtval[q] * P.s[P.rtidx[q]];
@@ -365,7 +381,8 @@ void lsqr_persistent_run(apc_mat& a, double mu, const PrecondDev* p, const Persi
     default: kfn = reinterpret_cast<void*>(lsqr_persistent_kernel<32>); break;
   }
   P.group = G;
-  const size_t smem = sizeof(double) * static_cast<size_t>(std::max<long long>(1, P.l));
+  P.zsmem = (P.n * 8 <= 200 * 1024 && !std::getenv("APC_PERSISTENT_NO_ZSMEM")) ? 1 : 0;
+  const size_t smem = sizeof(double) * static_cast<size_t>(std::max<long long>(1, P.zsmem ? P.n : 1));
   if (smem > 48 * 1024) APC_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kPT, smem));
