@@ -47,6 +47,46 @@ __device__ __forceinline__ double csr_at(const int* ptr, const int* idx, const d
 // ---------------------------------------------------------------------------
 constexpr int kSketchWarps = 8;
 
+// Stage the S columns of a 32-row chunk (rows k0..k0+cnt-1 of A) in the warp's
+// shared slice: one coalesced load round instead of a dependent load per row.
+__device__ __forceinline__ void stage_s(const int* __restrict__ srow, const signed char* __restrict__ ssgn,
+                                        long long k0, int cnt, int xi, int lane, int* rs, signed char* sg) {
+  const int tot = cnt * xi;
+  const long long base = k0 * xi;
+  for (int e = lane; e < tot; e += 32) {
+    rs[e] = srow[base + e];
+    sg[e] = ssgn[base + e];
+  }
+  __syncwarp();
+}
+
+// same for a gathered list of rows (CSC column chunk): entry q is row kq
+__device__ __forceinline__ void stage_s_rows(const int* __restrict__ srow, const signed char* __restrict__ ssgn,
+                                             long long kq, bool valid, int xi, int lane, int* rs, signed char* sg) {
+  if (valid)
+    for (int t = 0; t < xi; ++t) {
+      rs[lane * xi + t] = srow[kq * xi + t];
+      sg[lane * xi + t] = ssgn[kq * xi + t];
+    }
+  __syncwarp();
+}
+
+struct SketchSmem {  // per-warp slices of the dynamic shared memory
+  double* y;
+  int* rs;
+  signed char* sg;
+};
+
+__device__ __forceinline__ SketchSmem sketch_smem(double* base, int s, int xi, int w) {
+  SketchSmem m;
+  m.y = base + static_cast<long long>(w) * s;
+  int* ri = reinterpret_cast<int*>(base + static_cast<long long>(kSketchWarps) * s);
+  m.rs = ri + w * 32 * xi;
+  signed char* sb = reinterpret_cast<signed char*>(ri + kSketchWarps * 32 * xi);
+  m.sg = sb + w * 32 * xi;
+  return m;
+}
+
 __global__ void __launch_bounds__(kSketchWarps * 32)
 sketch_ss_dense_kernel(const double* __restrict__ A, long long m, long long n, int s, int xi,
                        const int* __restrict__ srow, const signed char* __restrict__ ssgn,
@@ -55,7 +95,8 @@ sketch_ss_dense_kernel(const double* __restrict__ A, long long m, long long n, i
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long j = static_cast<long long>(blockIdx.x) * kSketchWarps + w;
   if (j >= n) return;
-  double* yc = ysh + static_cast<long long>(w) * s;
+  SketchSmem sm = sketch_smem(ysh, s, xi, w);
+  double* yc = sm.y;
   for (int i = lane; i < s; i += 32) yc[i] = 0.0;
   __syncwarp();
   const double* col = A + j * m;
@@ -63,15 +104,12 @@ sketch_ss_dense_kernel(const double* __restrict__ A, long long m, long long n, i
     const long long k = k0 + lane;
     const double v = k < m ? col[k] : 0.0;
     const int cnt = static_cast<int>(m - k0 < 32 ? m - k0 : 32);
+    stage_s(srow, ssgn, k0, cnt, xi, lane, sm.rs, sm.sg);
     for (int kk = 0; kk < cnt; ++kk) {
       const double vk = __shfl_sync(0xffffffffu, v, kk);
       if (vk != 0.0) {
         const double sv = scale * vk;
-        if (lane < xi) {
-          const long long e = (k0 + kk) * xi + lane;
-          const double sg = static_cast<double>(ssgn[e]);
-          yc[srow[e]] += sv * sg;
-        }
+        if (lane < xi) yc[sm.rs[kk * xi + lane]] += sv * static_cast<double>(sm.sg[kk * xi + lane]);
       }
       __syncwarp();
     }
@@ -94,7 +132,8 @@ sketch_ss_csc_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long j = static_cast<long long>(blockIdx.x) * kSketchWarps + w;
   if (j >= n) return;
-  double* yc = ysh + static_cast<long long>(w) * s;
+  SketchSmem sm = sketch_smem(ysh, s, xi, w);
+  double* yc = sm.y;
   const int b = cptr[j], e = cptr[j + 1];
   if (e - b > heavy) return;  // long columns: sketch_ss_heavy_kernel
   for (int i = lane; i < s; i += 32) yc[i] = 0.0;
@@ -104,14 +143,11 @@ sketch_ss_csc_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
     const double v = p < e ? cval[p] : 0.0;
     const int k = p < e ? ridx[p] : 0;
     const int cnt = e - p0 < 32 ? e - p0 : 32;
+    stage_s_rows(srow, ssgn, k, p < e, xi, lane, sm.rs, sm.sg);
     for (int q = 0; q < cnt; ++q) {
       const double vk = __shfl_sync(0xffffffffu, v, q);
-      const int kq = __shfl_sync(0xffffffffu, k, q);
       const double sv = scale * vk;
-      if (lane < xi) {
-        const long long ee = static_cast<long long>(kq) * xi + lane;
-        yc[srow[ee]] += sv * static_cast<double>(ssgn[ee]);
-      }
+      if (lane < xi) yc[sm.rs[q * xi + lane]] += sv * static_cast<double>(sm.sg[q * xi + lane]);
       __syncwarp();
     }
   }
@@ -127,17 +163,22 @@ sketch_ss_csc_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
 // sketch rows instead.  Lane i of slab w owns output row 32w + i and walks the
 // column's nonzeros in ascending row order, adding +-scale*A(k, j) whenever
 // row i is one of S(:, k)'s xi rows -- the same per-element chain as the
-// reference, so Y stays bit-identical.
+// reference, so Y stays bit-identical.  The S columns of each 32-entry chunk
+// are staged in shared memory first (one load round per chunk).
 __global__ void __launch_bounds__(256)
 sketch_ss_heavy_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
                        const double* __restrict__ cval, const int* __restrict__ heavy_cols, int nheavy,
                        long long m, int s, int xi, const int* __restrict__ srow,
                        const signed char* __restrict__ ssgn, double scale, double mu_scale, int aug,
                        double* __restrict__ Y) {
+  extern __shared__ int hs[];  // 8 warps x 32 x xi rows, then signs
   const int nslab = (s + 31) / 32;
+  const int w = threadIdx.x >> 5;
   const long long wid = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (wid >= static_cast<long long>(nheavy) * nslab) return;
+  int* rs = hs + w * 32 * xi;
+  signed char* sg = reinterpret_cast<signed char*>(hs + 8 * 32 * xi) + w * 32 * xi;
   const long long j = heavy_cols[wid / nslab];
   const int i = static_cast<int>(wid % nslab) * 32 + lane;
   const int b = cptr[j], e = cptr[j + 1];
@@ -147,14 +188,14 @@ sketch_ss_heavy_kernel(const int* __restrict__ cptr, const int* __restrict__ rid
     const double v = p < e ? cval[p] : 0.0;
     const int k = p < e ? ridx[p] : 0;
     const int cnt = e - p0 < 32 ? e - p0 : 32;
+    stage_s_rows(srow, ssgn, k, p < e, xi, lane, rs, sg);
     for (int q = 0; q < cnt; ++q) {
       const double vk = __shfl_sync(0xffffffffu, v, q);
-      const long long kq = __shfl_sync(0xffffffffu, k, q);
       const double sv = scale * vk;
-      const int* rr = srow + kq * xi;
       for (int t = 0; t < xi; ++t)
-        if (rr[t] == i) acc += sv * static_cast<double>(ssgn[kq * xi + t]);
+        if (rs[q * xi + t] == i) acc += sv * static_cast<double>(sg[q * xi + t]);
     }
+    __syncwarp();
   }
   if (aug) {
     const int* rr = srow + (m + j) * xi;
@@ -628,6 +669,52 @@ __global__ void crow_fill_kernel(const int* ptr, const int* idx, const double* v
   }
 }
 
+// Exact-order Gram of a dense column block: G(i, j) = sum_r C(r, i) C(r, j) with
+// r ascending and separate mul/add, i.e. chol_gram's loop (dense_factor.hpp:
+// 199-209) element by element; 64 x 64 output tiles (upper-triangle tiles only).
+__global__ void __launch_bounds__(256)
+gram_exact_kernel(const double* __restrict__ C, long long m, long long l, double* __restrict__ G) {
+  constexpr int T = 64, K = 16;
+  __shared__ double Ci[K][T + 1];
+  __shared__ double Cj[K][T + 1];
+  const long long i0 = static_cast<long long>(blockIdx.y) * T, j0 = static_cast<long long>(blockIdx.x) * T;
+  if (i0 > j0 + T - 1) return;  // strictly-lower tile
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+  for (long long k0 = 0; k0 < m; k0 += K) {
+    for (int e = threadIdx.x; e < K * T; e += 256) {
+      const int cc = e / K, kk = e % K;
+      const long long r = k0 + kk;
+      Ci[kk][cc] = (r < m && i0 + cc < l) ? C[(i0 + cc) * m + r] : 0.0;
+      Cj[kk][cc] = (r < m && j0 + cc < l) ? C[(j0 + cc) * m + r] : 0.0;
+    }
+    __syncthreads();
+    for (int kk = 0; kk < K; ++kk) {
+      double a4[4], b4[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) a4[a] = Ci[kk][ty + 16 * a];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) b4[c] = Cj[kk][tx + 16 * c];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = __dadd_rn(acc[a][c], __dmul_rn(a4[a], b4[c]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const long long i = i0 + ty + 16 * a, j = j0 + tx + 16 * c;
+      if (i <= j && j < l) G[j * l + i] = acc[a][c];
+    }
+}
+
 // C = A(:, J) dense (m x l column-major) from a dense A
 __global__ void gather_cols_kernel(const double* A, long long m, const long long* J, long long l, double* C) {
   const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -753,7 +840,7 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
     upload(ctx_, d_sg, sg.data(), mt_ * x);
     const double mu_scale = amu_ * scale;  // mu * scale_ * ss[q] (sketch.hpp:158)
     const int aug = amu_ > 0.0 ? 1 : 0;
-    const size_t smem = sizeof(double) * kSketchWarps * s_;
+    const size_t smem = sizeof(double) * kSketchWarps * s_ + (sizeof(int) + 1) * kSketchWarps * 32 * x;
     if (smem > 48 * 1024) {
       APC_CUDA(cudaFuncSetAttribute(sketch_ss_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       APC_CUDA(cudaFuncSetAttribute(sketch_ss_csc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -777,7 +864,10 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
         DBuf<int> d_heavy;
         upload(ctx_, d_heavy, heavy.data(), static_cast<i64>(heavy.size()));
         const long long warps = static_cast<long long>(heavy.size()) * ((s_ + 31) / 32);
-        sketch_ss_heavy_kernel<<<nb(warps * 32), 256, 0, st>>>(a.at.ptr.p, a.at.idx.p, a.at.val.p, d_heavy.p,
+        const size_t hsm = (sizeof(int) + 1) * 8 * 32 * x;
+        if (hsm > 48 * 1024)
+          APC_CUDA(cudaFuncSetAttribute(sketch_ss_heavy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+        sketch_ss_heavy_kernel<<<nb(warps * 32), 256, hsm, st>>>(a.at.ptr.p, a.at.idx.p, a.at.val.p, d_heavy.p,
                                                              static_cast<int>(heavy.size()), m_, (int)s_, (int)x,
                                                              d_rows.p, d_sg.p, scale, mu_scale, aug, Y_.p);
         ctx_->launches++;
@@ -1012,8 +1102,10 @@ Vec DeviceCur::c_gram() const {
   if (!a_.sparse) {
     DBuf<double> C(m_ * l);
     gather_cols_kernel<<<nb(m_ * l), kT, 0, st>>>(a_.dense.p, m_, d_J.p, l, C.p);
-    ctx_->launches++;
-    dsyrk_t(ctx_, l, m_, 1.0, C.p, m_, 0.0, G.p, l);
+    // exact chol_gram order: T_C then equals the reference's factor bit for bit
+    dim3 grid(static_cast<unsigned>((l + 63) / 64), static_cast<unsigned>((l + 63) / 64));
+    gram_exact_kernel<<<grid, 256, 0, st>>>(C.p, m_, l, G.p);
+    ctx_->launches += 2;
   } else {
     DBuf<int> colpos(n_);
     APC_CUDA(cudaMemsetAsync(colpos.p, 0xff, colpos.bytes(), st));

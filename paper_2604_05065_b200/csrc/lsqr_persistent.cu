@@ -381,7 +381,9 @@ void lsqr_persistent_run(apc_mat& a, double mu, const PrecondDev* p, const Persi
     default: kfn = reinterpret_cast<void*>(lsqr_persistent_kernel<32>); break;
   }
   P.group = G;
-  P.zsmem = (P.n * 8 <= 200 * 1024 && !std::getenv("APC_PERSISTENT_NO_ZSMEM")) ? 1 : 0;
+  // measured on C2: the per-CTA z build costs more (latency-bound RT walk) than
+  // the L2 gathers it saves, so shared-memory z is opt-in only
+  P.zsmem = (P.n * 8 <= 200 * 1024 && std::getenv("APC_PERSISTENT_ZSMEM")) ? 1 : 0;
   const size_t smem = sizeof(double) * static_cast<size_t>(std::max<long long>(1, P.zsmem ? P.n : 1));
   if (smem > 48 * 1024) APC_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
