@@ -111,6 +111,9 @@ int apc_cur_rollback_last_augment(apc_cur* c);
 int apc_cur_state(const apc_cur* c, int64_t* rank, double* rho, int64_t* sketch_rows, int64_t* n_rho);
 int apc_cur_indices(const apc_cur* c, int64_t* rows, int64_t* cols);
 int apc_cur_rho_history(const apc_cur* c, double* rho);
+/* time of the one-time sketch: host embedding generation (seeded RNG) and the
+ * device sketch kernels (CUDA events on the library stream), ms */
+int apc_cur_timing(const apc_cur* c, double* embedding_host_ms, double* sketch_device_ms);
 /* sketch_matrix() / sketch_residual(): s x n column-major, host copies */
 int apc_cur_sketch(const apc_cur* c, double* y);
 int apc_cur_residual(const apc_cur* c, double* e);

@@ -168,6 +168,7 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
         "apc_cur_state": (C.c_int, [vp, _i64p, _dp, _i64p, _i64p]),
         "apc_cur_indices": (C.c_int, [vp, _i64p, _i64p]),
         "apc_cur_rho_history": (C.c_int, [vp, _dp]),
+        "apc_cur_timing": (C.c_int, [vp, _dp, _dp]),
         "apc_cur_sketch": (C.c_int, [vp, _dp]),
         "apc_cur_residual": (C.c_int, [vp, _dp]),
         "apc_lupp": (C.c_int, [vp, _dp, _i64, _i64, _i64, _i64p, _dp, _i64p]),
@@ -362,6 +363,12 @@ class CurState:
         rows, cols = np.zeros(r, np.int64), np.zeros(r, np.int64)
         load_library().apc_cur_indices(self.h, _iptr(rows), _iptr(cols))
         return rows, cols
+
+    def sketch_timing(self):
+        """(host embedding generation ms, device sketch kernel ms)."""
+        e, k = C.c_double(), C.c_double()
+        load_library().apc_cur_timing(self.h, C.byref(e), C.byref(k))
+        return e.value, k.value
 
     def rho_history(self) -> np.ndarray:
         out = np.zeros(self._state()[3])

@@ -8,6 +8,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -808,6 +809,10 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
   cudaStream_t st = ctx_->stream;
   Y_.alloc(std::max<i64>(1, s_ * n_));
   E_.alloc(std::max<i64>(1, s_ * n_));
+  cudaEvent_t ev0, ev1;
+  APC_CUDA(cudaEventCreate(&ev0));
+  APC_CUDA(cudaEventCreate(&ev1));
+  const auto th0 = std::chrono::steady_clock::now();
   if (sketch_kind == 0) {
     // SparseSignEmbedding ctor (sketch.hpp:20-50), host RNG, bit-identical
     const i64 x = std::min(xi, s_);
@@ -834,10 +839,12 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
       }
     }
     const double scale = 1.0 / std::sqrt(static_cast<double>(x));
+    embed_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
     DBuf<int> d_rows;
     DBuf<signed char> d_sg;
     upload(ctx_, d_rows, rows.data(), mt_ * x);
     upload(ctx_, d_sg, sg.data(), mt_ * x);
+    APC_CUDA(cudaEventRecord(ev0, st));
     const double mu_scale = amu_ * scale;  // mu * scale_ * ss[q] (sketch.hpp:158)
     const int aug = amu_ > 0.0 ? 1 : 0;
     const size_t smem = sizeof(double) * kSketchWarps * s_ + (sizeof(int) + 1) * kSketchWarps * 32 * x;
@@ -871,10 +878,10 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
                                                              static_cast<int>(heavy.size()), m_, (int)s_, (int)x,
                                                              d_rows.p, d_sg.p, scale, mu_scale, aug, Y_.p);
         ctx_->launches++;
-        APC_CUDA(cudaStreamSynchronize(st));
       }
     }
     ctx_->launches++;
+    APC_CUDA(cudaEventRecord(ev1, st));
     APC_CUDA(cudaStreamSynchronize(st));
   } else {
     // GaussianEmbedding (sketch.hpp:173-182): entries scale * gaussian() in storage order
@@ -882,8 +889,10 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
     HostRng rng(emb_seed);
     const double scale = 1.0 / std::sqrt(static_cast<double>(s_));
     for (auto& v : S) v = scale * rng.gaussian();
+    embed_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
     DBuf<double> d_S;
     upload(ctx_, d_S, S.data(), s_ * m_);
+    APC_CUDA(cudaEventRecord(ev0, st));
     if (!a.sparse) {
       dim3 grid(static_cast<unsigned>((n_ + kGJ - 1) / kGJ), static_cast<unsigned>((s_ + kGI - 1) / kGI));
       sketch_gauss_dense_kernel<<<grid, 256, 0, st>>>(d_S.p, (int)s_, a.dense.p, m_, n_, Y_.p);
@@ -892,7 +901,15 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
                                                           Y_.p);
     }
     ctx_->launches++;
+    APC_CUDA(cudaEventRecord(ev1, st));
     APC_CUDA(cudaStreamSynchronize(st));
+  }
+  {
+    float ms = 0.f;
+    APC_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    sketch_ms_ = ms;
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
   }
   APC_CUDA(cudaGetLastError());
   APC_CUDA(cudaMemcpyAsync(E_.p, Y_.p, sizeof(double) * s_ * n_, cudaMemcpyDeviceToDevice, st));
@@ -1283,6 +1300,12 @@ int apc_cur_state(const apc_cur* c, int64_t* rank, double* rho, int64_t* sketch_
 int apc_cur_indices(const apc_cur* c, int64_t* rows, int64_t* cols) {
   std::copy(c->cur->rows().begin(), c->cur->rows().end(), rows);
   std::copy(c->cur->cols().begin(), c->cur->cols().end(), cols);
+  return APC_OK;
+}
+
+int apc_cur_timing(const apc_cur* c, double* embedding_host_ms, double* sketch_device_ms) {
+  if (embedding_host_ms) *embedding_host_ms = c->cur->embedding_ms();
+  if (sketch_device_ms) *sketch_device_ms = c->cur->sketch_ms();
   return APC_OK;
 }
 

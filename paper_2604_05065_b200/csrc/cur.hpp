@@ -38,6 +38,8 @@ class DeviceCur {
   DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 probes, int core_kind,
             int sketch_kind, i64 max_rank, double aug_mu = 0.0);
   i64 target_rows() const { return mt_; }
+  double embedding_ms() const { return embed_ms_; }
+  double sketch_ms() const { return sketch_ms_; }
   bool augmented() const { return amu_ > 0.0; }
   ~DeviceCur();
 
@@ -80,6 +82,7 @@ class DeviceCur {
   i64 m_, n_, s_, block_size_, probes_, max_rank_;
   i64 mt_ = 0;       // target rows: m, or m + n for the augmented stack
   double amu_ = 0.0; // mu of the augmented target (0: plain A)
+  double embed_ms_ = 0.0, sketch_ms_ = 0.0;
   int core_kind_;
   double ztol_ = 0.0;
   double rho_;

@@ -87,12 +87,15 @@ def main():
             ctx.sync()
             dt = time.time() - t0
             s = int(np.ceil(1.1 * block))
+            emb_ms, dev_ms = cur.sketch_timing()
             if kind == apc.SketchKind.gaussian:
-                sk["gaussian"] = dict(s=s, seconds=dt, flops=2.0 * s * p.m * p.n,
-                                      TFLOPs=2.0 * s * p.m * p.n / dt / 1e12)
+                sk["gaussian"] = dict(s=s, seconds=dt, embedding_host_ms=emb_ms, kernel_ms=dev_ms,
+                                      flops=2.0 * s * p.m * p.n,
+                                      kernel_TFLOPs=2.0 * s * p.m * p.n / (dev_ms / 1e3) / 1e12)
             else:
-                sk["sparse_sign"] = dict(s=s, seconds=dt,
-                                         bytes=(8 * p.m * p.n if not p.sparse else 12 * p.nnz))
+                byts = 8 * p.m * p.n if not p.sparse else 12 * p.nnz
+                sk["sparse_sign"] = dict(s=s, seconds=dt, embedding_host_ms=emb_ms, kernel_ms=dev_ms, bytes=byts,
+                                         kernel_GBps=byts / (dev_ms / 1e3) / 1e9)
             if kind == apc.SketchKind.sparse_sign:
                 steps = []
                 for st in range(args.steps):
