@@ -5,6 +5,7 @@
 // rounded separately, -fmad=false, sums in the reference's index order).  The
 // parallelism comes from independent output elements, never from reordering a
 // sum.  This is what makes I, J and rho_history bit-identical to the CPU.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -204,6 +205,79 @@ sketch_ss_heavy_kernel(const int* __restrict__ cptr, const int* __restrict__ rid
       if (rr[t] == i) acc += mu_scale * static_cast<double>(ssgn[(m + j) * xi + t]);
   }
   if (i < s) Y[j * s + i] = acc;
+}
+
+// Inverted-index sketch for long columns.  The reference's chain for output
+// (i, j) is: for the stored rows k of column j in ascending order, whenever
+// row i is one of S(:, k)'s xi rows, add (scale * A(k, j)) * sign.  Emitting
+// one (key = slot(j) * s + i, value = entry * xi + t) pair per (entry, t) and
+// stable-sorting by key gathers each chain contiguously, still in ascending
+// entry order; one thread per (j, i) then walks its chain.  The critical path
+// is the chain length (~ nnz(j) * xi / s), not nnz(j).
+__global__ void heavy_pairs_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
+                                   const int* __restrict__ bcols, const long long* __restrict__ boff, int nb,
+                                   long long total, int s, int xi, const int* __restrict__ srow,
+                                   unsigned* __restrict__ keys, unsigned* __restrict__ vals) {
+  const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;  // batch entry
+  if (q >= total) return;
+  int lo = 0, hi = nb;  // slot: last b with boff[b] <= q
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (boff[mid] <= q) lo = mid;
+    else hi = mid;
+  }
+  const long long p = cptr[bcols[lo]] + (q - boff[lo]);
+  const long long k = ridx[p];
+  for (int t = 0; t < xi; ++t) {
+    keys[q * xi + t] = static_cast<unsigned>(lo) * static_cast<unsigned>(s) + static_cast<unsigned>(srow[k * xi + t]);
+    vals[q * xi + t] = static_cast<unsigned>(p * xi + t);
+  }
+}
+
+__global__ void heavy_walk_kernel(const unsigned* __restrict__ keys, const unsigned* __restrict__ vals,
+                                  long long npairs, const int* __restrict__ bcols, int nb, int s, int xi,
+                                  const int* __restrict__ ridx, const double* __restrict__ cval,
+                                  const signed char* __restrict__ ssgn, const int* __restrict__ srow,
+                                  double scale, double mu_scale, int aug, long long m, double* __restrict__ Y) {
+  const long long key = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (key >= static_cast<long long>(nb) * s) return;
+  // segment [lower_bound(key), lower_bound(key + 1)) of the sorted keys
+  auto lower = [&](unsigned kk) {
+    long long lo = 0, hi = npairs;
+    while (lo < hi) {
+      const long long mid = (lo + hi) >> 1;
+      if (keys[mid] < kk) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  };
+  const long long b = lower(static_cast<unsigned>(key)), e = lower(static_cast<unsigned>(key + 1));
+  const int i = static_cast<int>(key % s);
+  const long long j = bcols[key / s];
+  double acc = 0.0;
+  long long q = b;
+  for (; q + 4 <= e; q += 4) {  // loads ahead of the (ordered) add chain
+    double sv[4], sg[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned ev = vals[q + u];
+      const long long p = ev / xi;
+      sv[u] = scale * cval[p];
+      sg[u] = static_cast<double>(ssgn[static_cast<long long>(ridx[p]) * xi + ev % xi]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc += sv[u] * sg[u];
+  }
+  for (; q < e; ++q) {
+    const unsigned ev = vals[q];
+    const long long p = ev / xi;
+    acc += (scale * cval[p]) * static_cast<double>(ssgn[static_cast<long long>(ridx[p]) * xi + ev % xi]);
+  }
+  if (aug) {
+    for (int t = 0; t < xi; ++t)
+      if (srow[(m + j) * xi + t] == i) acc += mu_scale * static_cast<double>(ssgn[(m + j) * xi + t]);
+  }
+  Y[j * s + i] = acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -868,16 +942,46 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
                                                               (int)x, d_rows.p, d_sg.p, scale, mu_scale, aug,
                                                               kHeavy, Y_.p);
       if (!heavy.empty()) {
-        DBuf<int> d_heavy;
-        upload(ctx_, d_heavy, heavy.data(), static_cast<i64>(heavy.size()));
-        const long long warps = static_cast<long long>(heavy.size()) * ((s_ + 31) / 32);
-        const size_t hsm = (sizeof(int) + 1) * 8 * 32 * x;
-        if (hsm > 48 * 1024)
-          APC_CUDA(cudaFuncSetAttribute(sketch_ss_heavy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
-        sketch_ss_heavy_kernel<<<nb(warps * 32), 256, hsm, st>>>(a.at.ptr.p, a.at.idx.p, a.at.val.p, d_heavy.p,
-                                                             static_cast<int>(heavy.size()), m_, (int)s_, (int)x,
-                                                             d_rows.p, d_sg.p, scale, mu_scale, aug, Y_.p);
-        ctx_->launches++;
+        // inverted-index pass over the long columns, in batches of <= 2^28 pairs
+        require(static_cast<double>(a.at.nnz) * x < 4.0e9, APC_INVALID_ARGUMENT,
+                "sketch: nnz * xi exceeds the 32-bit pair encoding");
+        constexpr long long kMaxPairs = 1LL << 28;
+        size_t h0 = 0;
+        while (h0 < heavy.size()) {
+          std::vector<int> bcols;
+          std::vector<long long> boff;
+          long long tot = 0;
+          while (h0 < heavy.size()) {
+            const long long len = cp[heavy[h0] + 1] - cp[heavy[h0]];
+            if (!bcols.empty() && (tot + len) * x > kMaxPairs) break;
+            bcols.push_back(heavy[h0]);
+            boff.push_back(tot);
+            tot += len;
+            ++h0;
+          }
+          const long long npairs = tot * x;
+          const int nbc = static_cast<int>(bcols.size());
+          DBuf<int> d_bcols;
+          DBuf<long long> d_boff;
+          upload(ctx_, d_bcols, bcols.data(), nbc);
+          upload(ctx_, d_boff, boff.data(), nbc);
+          DBuf<unsigned> kin(npairs), kout(npairs), vin(npairs), vout(npairs);
+          heavy_pairs_kernel<<<nb(tot), kT, 0, st>>>(a.at.ptr.p, a.at.idx.p, d_bcols.p, d_boff.p, nbc, tot,
+                                                     (int)s_, (int)x, d_rows.p, kin.p, vin.p);
+          int end_bit = 1;
+          while ((1LL << end_bit) < static_cast<long long>(nbc) * s_ && end_bit < 32) ++end_bit;
+          size_t tmp_bytes = 0;
+          cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kin.p, kout.p, vin.p, vout.p,
+                                          static_cast<std::int64_t>(npairs), 0, end_bit, st);
+          DBuf<char> tmp(static_cast<i64>(tmp_bytes));
+          APC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, kin.p, kout.p, vin.p, vout.p,
+                                                   static_cast<std::int64_t>(npairs), 0, end_bit, st));
+          heavy_walk_kernel<<<nb(static_cast<long long>(nbc) * s_), kT, 0, st>>>(
+              kout.p, vout.p, npairs, d_bcols.p, nbc, (int)s_, (int)x, a.at.idx.p, a.at.val.p, d_sg.p, d_rows.p,
+              scale, mu_scale, aug, m_, Y_.p);
+          ctx_->launches += 3;
+          APC_CUDA(cudaStreamSynchronize(st));
+        }
       }
     }
     ctx_->launches++;

@@ -128,10 +128,18 @@ __global__ void add_tail_kernel(const double* t, long long n, double mu, double*
 }
 
 // ---- CSC -> CSR(A) build (stable radix sort by row keeps columns ascending)
-__global__ void expand_cols_kernel(const int* colptr, long long ncols, int* colof) {
-  long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= ncols) return;
-  for (int k = colptr[j]; k < colptr[j + 1]; ++k) colof[k] = static_cast<int>(j);
+// colof[k] = column of entry k (thread per entry, binary search in colptr:
+// balanced even when a few columns hold most entries, as C5's Zipf head does)
+__global__ void expand_cols_kernel(const int* colptr, long long ncols, long long nnz, int* colof) {
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= nnz) return;
+  long long lo = 0, hi = ncols;  // last j with colptr[j] <= k
+  while (hi - lo > 1) {
+    const long long mid = (lo + hi) >> 1;
+    if (colptr[mid] <= k) lo = mid;
+    else hi = mid;
+  }
+  colof[k] = static_cast<int>(lo);
 }
 __global__ void iota_kernel(int* p, long long n) {
   long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -396,7 +404,7 @@ void upload_csc(apc_mat& a, const long long* colptr, const long long* rowidx, co
   c.val.alloc(std::max<long long>(1, nnz));
   if (nnz > 0) {
     DBuf<int> colof(nnz), perm_in(nnz), perm_out(nnz), keys_out(nnz);
-    expand_cols_kernel<<<nblk(n, 256), 256, 0, st>>>(t.ptr.p, n, colof.p);
+    expand_cols_kernel<<<nblk(nnz, 256), 256, 0, st>>>(t.ptr.p, n, nnz, colof.p);
     iota_kernel<<<nblk(nnz, 256), 256, 0, st>>>(perm_in.p, nnz);
     int end_bit = 1;
     while ((1LL << end_bit) < mloc + 1 && end_bit < 31) ++end_bit;
