@@ -892,12 +892,21 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
     const i64 x = std::min(xi, s_);
     std::vector<int> rows(static_cast<size_t>(mt_ * x));
     std::vector<signed char> sg(static_cast<size_t>(mt_ * x));
-    HostRng rng(emb_seed);
-    std::vector<i64> pick(static_cast<size_t>(x));
-    for (i64 c = 0; c < mt_; ++c) {  // one column per target row (m + n when augmented)
+    // Every column consumes exactly 2*xi draws (xi for Floyd's below(t+1),
+    // xi for the signs) unless below() rejects a draw (probability < s/2^64):
+    // draw the raw stream sequentially, build the columns in parallel, and
+    // fall back to the sequential construction if any draw would be rejected.
+    auto build_column = [&](i64 c, auto&& next_draw) {
+      i64 pickbuf[64];
+      std::vector<i64> big;
+      i64* pick = pickbuf;
+      if (x > 64) {
+        big.resize(static_cast<size_t>(x));
+        pick = big.data();
+      }
       size_t cnt = 0;
       for (i64 t = s_ - x; t < s_; ++t) {
-        const i64 r = static_cast<i64>(rng.below(static_cast<std::uint64_t>(t) + 1));
+        const i64 r = static_cast<i64>(next_draw(static_cast<std::uint64_t>(t) + 1));
         bool dup = false;
         for (size_t q = 0; q < cnt; ++q)
           if (pick[q] == r) {
@@ -906,10 +915,35 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
           }
         pick[cnt++] = dup ? t : r;
       }
-      std::sort(pick.begin(), pick.begin() + static_cast<std::ptrdiff_t>(cnt));
-      for (size_t q = 0; q < cnt; ++q) {
-        rows[c * x + q] = static_cast<int>(pick[q]);
-        sg[c * x + q] = static_cast<signed char>(rng.sign() > 0 ? 1 : -1);
+      std::sort(pick, pick + cnt);
+      for (size_t q = 0; q < cnt; ++q) rows[c * x + q] = static_cast<int>(pick[q]);
+      return cnt;
+    };
+    HostRng rng(emb_seed);
+    bool ok = x <= 64;
+    if (ok) {
+      std::vector<std::uint64_t> raw(static_cast<size_t>(mt_ * 2 * x));
+      for (auto& d : raw) d = rng.bits();
+      std::vector<char> bad(static_cast<size_t>(std::max<i64>(1, mt_)), 0);
+      host_parallel_for(mt_, [&](i64 b, i64 e) {
+        for (i64 c = b; c < e; ++c) {
+          const std::uint64_t* d = raw.data() + c * 2 * x;
+          i64 k = 0;
+          build_column(c, [&](std::uint64_t nn) {
+            const std::uint64_t v = d[k++];
+            if (!HostRng::below_accepts(v, nn)) bad[c] = 1;
+            return v % nn;
+          });
+          for (i64 q = 0; q < x; ++q) sg[c * x + q] = static_cast<signed char>((d[x + q] & 1ULL) ? 1 : -1);
+        }
+      });
+      for (char f : bad) ok = ok && !f;
+    }
+    if (!ok) {  // sequential reference construction (sketch.hpp:31-49)
+      HostRng seq(emb_seed);
+      for (i64 c = 0; c < mt_; ++c) {
+        const size_t cnt = build_column(c, [&](std::uint64_t nn) { return seq.below(nn); });
+        for (size_t q = 0; q < cnt; ++q) sg[c * x + q] = static_cast<signed char>(seq.sign() > 0 ? 1 : -1);
       }
     }
     const double scale = 1.0 / std::sqrt(static_cast<double>(x));
@@ -992,7 +1026,7 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
     std::vector<double> S(static_cast<size_t>(s_ * m_));
     HostRng rng(emb_seed);
     const double scale = 1.0 / std::sqrt(static_cast<double>(s_));
-    for (auto& v : S) v = scale * rng.gaussian();
+    fill_gaussians(rng, S.data(), s_ * m_, scale, true);  // scale * gaussian() in storage order
     embed_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
     DBuf<double> d_S;
     upload(ctx_, d_S, S.data(), s_ * m_);
@@ -1035,7 +1069,7 @@ void DeviceCur::compute_rho() {
   const i64 r = probes_;
   std::vector<double> w(static_cast<size_t>(r * n_));
   for (i64 p = 0; p < r; ++p)
-    for (i64 j = 0; j < n_; ++j) w[p * n_ + j] = probe_rng_.gaussian();
+    fill_gaussians(probe_rng_, w.data() + p * n_, n_);
   DBuf<double> d_w, d_out(std::max<i64>(1, s_ * r));
   upload(ctx_, d_w, w.data(), r * n_);
   dim3 grid(static_cast<unsigned>((s_ + 31) / 32), static_cast<unsigned>(r));

@@ -6,9 +6,12 @@
 // are generated here and uploaded.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <random>
+#include <thread>
+#include <vector>
 
 #include "apc_internal.hpp"
 
@@ -48,8 +51,53 @@ class HostRng {
   }
   double sign() { return (eng_() & 1ULL) ? 1.0 : -1.0; }
 
+  // the same distributions as pure functions of the raw 64-bit draws, so a
+  // stream consumed in a fixed pattern can be generated sequentially (fast)
+  // and transformed in parallel with identical results
+  static double uniform_of(std::uint64_t d) { return static_cast<double>(d >> 11) * 0x1.0p-53; }
+  static double gaussian_of(std::uint64_t d1, std::uint64_t d2) {
+    const double a = 1.0 - uniform_of(d1);
+    const double b = uniform_of(d2);
+    return std::sqrt(-2.0 * std::log(a)) * std::cos(6.283185307179586476925286766559 * b);
+  }
+  // below(n) when the first draw is accepted (rejection probability < n / 2^64)
+  static bool below_accepts(std::uint64_t d, std::uint64_t n) {
+    return d < ~std::uint64_t{0} - (~std::uint64_t{0} % n);
+  }
+
  private:
   std::mt19937_64 eng_;
 };
+
+// run f(begin, end) over [0, n) on the host's cores
+template <class F>
+void host_parallel_for(i64 n, F f) {
+  unsigned hc = std::thread::hardware_concurrency();
+  const i64 nt = std::max<i64>(1, std::min<i64>(hc ? hc : 1, 32));
+  if (n < 4096 || nt == 1) {
+    f(i64{0}, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const i64 chunk = (n + nt - 1) / nt;
+  for (i64 t = 0; t < nt; ++t) {
+    const i64 b = t * chunk, e = std::min(n, b + chunk);
+    if (b >= e) break;
+    th.emplace_back([=] { f(b, e); });
+  }
+  for (auto& x : th) x.join();
+}
+
+// n Gaussians of the stream (each consumes exactly two draws), transformed in parallel
+inline void fill_gaussians(HostRng& rng, double* out, i64 n, double scale = 1.0, bool scaled = false) {
+  std::vector<std::uint64_t> raw(static_cast<size_t>(2 * n));
+  for (auto& d : raw) d = rng.bits();
+  host_parallel_for(n, [&](i64 b, i64 e) {
+    for (i64 i = b; i < e; ++i) {
+      const double g = HostRng::gaussian_of(raw[2 * i], raw[2 * i + 1]);
+      out[i] = scaled ? scale * g : g;
+    }
+  });
+}
 
 }  // namespace apc
