@@ -227,7 +227,7 @@ void build_precond(const BuildInputs& in, PrecondDev& p, PrecondInfo& info) {
     Vec mm = matmul(l, l, l, t_c, ut);
     require(l <= 4096, APC_INVALID_ARGUMENT, "small_svd: dimension exceeds the small-problem cap");
     SvdH s;
-    if (l > 256) {  // parallel-order Jacobi on the device; serial cyclic on the host for small cores
+    if (l > 96) {  // parallel-order Jacobi on the device; serial cyclic on the host for small cores
       s.m = s.n = l;
       device_jacobi_svd(ctx, l, mm, s.sigma, s.v);
     } else {
