@@ -102,6 +102,17 @@ struct Csr {
   double avg_row_nnz = 0.0;
 };
 
+// SELL-32 copy of a CSR (built on demand for L2-resident systems): rows in
+// chunks of 32, entry k of the chunk's lane-th row at off[chunk] + 32 k + lane,
+// so a warp walking 32 rows thread-per-row reads idx/val fully coalesced while
+// every row is still summed sequentially in column order.
+struct Sell {
+  i64 rows = 0, chunks = 0, slots = 0;
+  DBuf<i32> off;  // chunks + 1 (entries)
+  DBuf<i32> idx;  // slots (padding never read)
+  DBuf<double> val;
+};
+
 }  // namespace apc
 
 // ---------------------------------------------------------------------------
@@ -134,6 +145,7 @@ struct apc_mat {
   apc::DBuf<double> dense;  // local rows, column-major, ld = r1 - r0
   apc::Csr a;               // CSR of the local rows (mloc x n)
   apc::Csr at;              // CSR of their transpose (n x mloc)
+  apc::Sell sell;           // SELL-32 copy of `a` (persistent LSQR, built lazily)
   apc::i64 nnz_global = 0;
   apc::i64 mloc() const { return r1 - r0; }
 };

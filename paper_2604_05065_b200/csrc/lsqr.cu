@@ -680,27 +680,29 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
     const bool prof = std::getenv("APC_PERSISTENT_PROF") != nullptr;
     DBuf<unsigned long long> d_prof(prof ? 64 * 8 : 0);
     if (prof) APC_CUDA(cudaMemsetAsync(d_prof.p, 0, d_prof.bytes(), st));
-    PersistentBuffers pb{w->u.p, w->v.p, w->w.p, y_d, w->z.p, w->h.p, w->s.p, w->t.p, w->pers_part.p,
+    PersistentBuffers pb{w->u.p, w->v.p, w->g.p, w->w.p, y_d, w->z.p, w->h.p, w->s.p, w->t.p, w->pers_part.p,
                          w->st.p, w->trace.p, bps ? std::atoi(bps) : 0, prof ? d_prof.p : nullptr};
     lsqr_persistent_run(a, mu, p, pb);
     per_iter = 0;
     if (prof) {
       std::vector<unsigned long long> h(64 * 8);
       copy_sync(st, h.data(), d_prof.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
-      double acc[8] = {0};
+      // stamps: 0 top, 1 B1, 2 z staged, 3 B2, 4 B3, 5 B4, 6 end of S7
+      double acc[7] = {0};
       int cnt = 0;
       for (int it = 2; it < 63; ++it) {
         if (h[(it + 1) * 8] == 0) break;
-        for (int k = 0; k < 8; ++k) {
-          unsigned long long a0 = h[it * 8 + k], a1 = k < 7 ? h[it * 8 + k + 1] : h[(it + 1) * 8];
+        for (int k = 0; k < 7; ++k) {
+          unsigned long long a0 = h[it * 8 + k], a1 = k < 6 ? h[it * 8 + k + 1] : h[(it + 1) * 8];
           if (a0 && a1) acc[k] += (a1 - a0) * 1e-3;
         }
         ++cnt;
       }
       if (cnt)
-        std::fprintf(stderr, "persistent stage us/iter (%d its): S1 %.2f S2 %.2f S3 %.2f S4 %.2f S5 %.2f S6 %.2f S7 %.2f S8 %.2f\n",
+        std::fprintf(stderr, "persistent stage us/iter (%d its): S12+B1 %.2f stop+zcopy %.2f S3+B2 %.2f S4+B3 %.2f "
+                     "S56+B4 %.2f S7 %.2f loop %.2f\n",
                      cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt,
-                     acc[6] / cnt, acc[7] / cnt);
+                     acc[6] / cnt);
     }
   } else if (use_while) {
     APC_CUDA(cudaGraphCreate(&graph, 0));

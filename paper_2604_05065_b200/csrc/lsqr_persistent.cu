@@ -6,22 +6,29 @@
 // reduces the same block partials in the same fixed order, so all copies stay
 // bit-identical and no scalar ever round-trips through a broadcast.
 //
-// Stages per iteration (implicit preconditioner P^{-1} = I + R^T G R):
-//   S1  CTA 0: t = R v, s = Gf t                                   | sync
-//   S2  z = v + R^T s                                              | sync
-//   S3  u <- A z - alpha u/beta_old ; u_tail <- mu z - alpha u_t/beta_old ;
-//       ||u||^2 block partials                                     | sync
-//   S4  beta ; h = (A^T u + mu u_t)/beta  (warp per row of A^T)    | sync
-//   S5  CTA 0: t = R h, s = Ga t                                   | sync
-//   S6  v = h + R^T s - beta v ; ||v||^2 partials                  | sync
-//   S7  alpha, rotation ; v /= alpha ; y += t1 w ; w = v + t2 w ;
-//       ||y||^2 partials                                           | sync
-//   S8  ||y|| ; stop tests (lsqr.hpp:183-203) ; trace row
-// Unpreconditioned phases skip S1, S2, S5 and fuse S6 into S4.
+// Stages per iteration (implicit preconditioner P^{-1} = I + R^T G R, R the
+// l selected rows of A):
+//   S12 t = R v, d_q = RT_q * (Gf t)_i, z = v + sum d      (per CTA)  | B1
+//       stop tests of the previous iteration (its ||y|| partials are
+//       complete only now; nothing persistent was written since)
+//   S3  z -> shared memory ; u <- A z - alpha u/beta_old (SELL-32, thread
+//       per row) ; u_tail <- mu z - alpha u_t/beta_old ; ||u||^2 partials| B2
+//   S4  beta ; h = (A^T u + mu u_t)/beta  (warp per row of A^T)         | B3
+//   S56 t = R h ; v_raw = h + R^T Ga t - beta v ; ||v_raw||^2  (per CTA)| B4
+//   S7  alpha, rotation ; v = v_raw/alpha ; y += t1 w ; w = v + t2 w ;
+//       ||y||^2 partials  (no barrier: the next S12 reads v_raw/alpha,
+//       bit-identical to v, and every other read of v is the owner's own)
+// "Per CTA" stages: each CTA owns a contiguous column range, recomputes the
+// (short) l-vector t itself and only the (G t)_i its columns need, which
+// saves the two grid barriers a grid-wide projection would cost.  Large R
+// falls back to the grid-wide projection (two extra barriers per use).
+// Unpreconditioned phases skip S12/S56; S4 then writes v_raw directly.
 #include <cooperative_groups.h>
+#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "dev_common.cuh"
 #include "lsqr.hpp"
@@ -38,6 +45,7 @@ namespace {
 
 constexpr int kPT = 1024;  // threads per CTA: one fat CTA per SM keeps grid barriers cheap
 constexpr int kNW = kPT / 32;
+constexpr long long kSmemBudget = 200 * 1024;  // dynamic shared memory the kernel may use
 
 struct PArgs {
   // A: CSR rows (mloc) and CSR of A^T (n rows, no split rows)
@@ -45,13 +53,18 @@ struct PArgs {
   const double* aval;
   const int *tptr, *tidx;
   const double* tval;
+  // SELL-32 copy of A (null: thread-per-row CSR walk)
+  const int *soff, *sidx;
+  const double* sval;
+  long long nchunks;
   long long mloc, n;
   double mu;
   int has_tail;
-  int group;  // lanes per row of the forward SpMV (4/8/16/32)
-  int zsmem;  // 1: z staged per CTA in shared memory (n small)
+  int zsmem;  // 1: every CTA stages z in shared memory for the forward gathers
   // preconditioner (implicit) or identity
   int pre;
+  int fused;          // 1: per-CTA projection (small R), 0: grid-wide
+  long long cchunk;   // columns owned per CTA
   const int *rptr, *ridx;
   const double* rval;
   const int *rtptr, *rtidx;
@@ -59,7 +72,7 @@ struct PArgs {
   const double *Gf, *Ga;  // row-major l x l
   long long l;
   // vectors
-  double *u, *v, *w, *y, *z, *h, *s, *t;
+  double *u, *v, *vr, *w, *y, *z, *h, *s, *t;
   double* part;  // gridDim.x x 4
   unsigned long long* prof;  // optional stage timestamps (first 64 iterations)
   LsqrState* st;
@@ -73,15 +86,14 @@ __device__ __forceinline__ double grid_sum(const double* part, int slot, int nbl
   return block_sum<kPT>(v, sh);
 }
 
-// s = K (M x) for the l x n sparse M (R) and row-major K, spread over the
-// whole grid (one warp per row in each half, a barrier between them): the
-// rows are short, so the stage is latency-bound and wants many warps.
+// t = M (x / xdiv), s = K t for the l x n sparse M (R) and row-major K, spread
+// over the whole grid (one warp per row in each half, a barrier between them).
 __device__ void grid_project(cg::grid_group& grid, const int* mptr, const int* midx, const double* mval,
-                             const double* KT, long long l, const double* x, double* t, double* s_out,
-                             long long gwarp, long long nwarps, int lane) {
+                             const double* KT, long long l, const double* x, double xdiv, double* t,
+                             double* s_out, long long gwarp, long long nwarps, int lane) {
   for (long long i = gwarp; i < l; i += nwarps) {
     double acc = 0.0;
-    for (int q = mptr[i] + lane; q < mptr[i + 1]; q += 32) acc += mval[q] * x[midx[q]];
+    for (int q = mptr[i] + lane; q < mptr[i + 1]; q += 32) acc += mval[q] * (x[midx[q]] / xdiv);
     acc = warp_sum(acc);
     if (lane == 0) t[i] = acc;
   }
@@ -95,16 +107,42 @@ __device__ void grid_project(cg::grid_group& grid, const int* mptr, const int* m
   }
 }
 
-template <int G>
+// Per-CTA projection for the columns [c0, c1) this CTA owns:
+//   tsh = R (x / xdiv)                 (all l rows, thread per row, in order)
+//   dsh[q - RT_ptr[c0]] = RT_val[q] * (K tsh)_{RT_idx[q]}   for q of the range
+__device__ void cta_project(const PArgs& P, const double* x, double xdiv, const double* K, double* tsh,
+                            double* dsh, long long c0, long long c1, int warp, int lane) {
+  for (long long i = threadIdx.x; i < P.l; i += kPT) {
+    const int b = __ldg(P.rptr + i), e = __ldg(P.rptr + i + 1);
+    double acc = 0.0;
+    for (int q = b; q < e; ++q) acc += __ldg(P.rval + q) * (x[__ldg(P.ridx + q)] / xdiv);
+    tsh[i] = acc;
+  }
+  __syncthreads();
+  const int qb0 = __ldg(P.rtptr + c0), qb1 = __ldg(P.rtptr + c1);
+  for (int q = qb0 + warp; q < qb1; q += kNW) {
+    const double* row = K + static_cast<long long>(__ldg(P.rtidx + q)) * P.l;
+    double acc = 0.0;
+    for (long long k = lane; k < P.l; k += 32) acc += __ldg(row + k) * tsh[k];
+    acc = warp_sum(acc);
+    if (lane == 0) dsh[q - qb0] = __ldg(P.rtval + q) * acc;
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
-  extern __shared__ double tsh[];  // l doubles (preconditioner)
+  extern __shared__ double dyn[];  // z copy (S3) / t + d (S12, S56): disjoint in time
   __shared__ double red[32];
   cg::grid_group grid = cg::this_grid();
   const long long gtid = static_cast<long long>(blockIdx.x) * kPT + threadIdx.x;
   const long long gsize = static_cast<long long>(gridDim.x) * kPT;
   const long long gwarp = gtid >> 5, nwarps = gsize >> 5;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nb = gridDim.x;
+  // owned columns of the n-length stages
+  const long long cb = static_cast<long long>(blockIdx.x) * P.cchunk;
+  const long long c0 = cb < P.n ? cb : P.n;
+  const long long c1 = c0 + P.cchunk < P.n ? c0 + P.cchunk : P.n;
   LsqrState* st = P.st;
   // replicated scalar recurrence (initialised by the phase-init kernels)
   double alpha = st->alpha, beta = st->beta, rhobar = st->rhobar, phibar = st->phibar;
@@ -115,59 +153,150 @@ __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
   long long j = st->iter;
   const unsigned long long t0 = st->t0_ns;
   if (st->done) return;
-  // small n: every CTA builds its own copy of z in shared memory (the forward
-  // SpMV then gathers from smem instead of L2, and the z stage needs no grid
-  // barrier); otherwise z goes through global memory
-  const double* zsrc = P.zsmem ? tsh : (P.pre ? P.z : P.v);
+  // quantities of the last completed iteration, tested after the next B1
+  bool pending = false, nonfinite = false;
+  double cc = 0.0, cvgrate = 0.0, cvgdiff = 0.0;
+  // v of the next S12 = vsrc / vdiv (first iteration: the initialised v)
+  const double* vsrc = P.v;
+  double vdiv = 1.0;
+  double* tsh = dyn;
+  double* dsh = dyn + P.l;
 
   for (;;) {
-    // ---- S1/S2: z = v + R^T Gf R v
+    // ---- S12: z = v + R^T Gf R v
     STAMP(0);
     if (P.pre) {
-      grid_project(grid, P.rptr, P.ridx, P.rval, P.Gf, P.l, P.v, P.t, P.s, gwarp, nwarps, lane);
-      grid.sync();
-      STAMP(1);
-    }
-    if (P.zsmem) {
-      for (long long c = threadIdx.x; c < P.n; c += kPT) {
-        double acc = 0.0;
-        if (P.pre)
+      if (P.fused) {
+        cta_project(P, vsrc, vdiv, P.Gf, tsh, dsh, c0, c1, warp, lane);
+        const int qb0 = __ldg(P.rtptr + c0);
+        for (long long c = c0 + threadIdx.x; c < c1; c += kPT) {
+          double acc = 0.0;
+          for (int q = __ldg(P.rtptr + c); q < __ldg(P.rtptr + c + 1); ++q) acc += dsh[q - qb0];
+          P.z[c] = P.v[c] + acc;
+        }
+      } else {
+        grid_project(grid, P.rptr, P.ridx, P.rval, P.Gf, P.l, vsrc, vdiv, P.t, P.s, gwarp, nwarps, lane);
+        grid.sync();
+        for (long long c = c0 + threadIdx.x; c < c1; c += kPT) {
+          double acc = 0.0;
           for (int q = P.rtptr[c]; q < P.rtptr[c + 1]; ++q) acc += P.rtval[q] * P.s[P.rtidx[q]];
-        tsh[c] = P.pre ? P.v[c] + acc : P.v[c];
+          P.z[c] = P.v[c] + acc;
+        }
       }
-      __syncthreads();
-      STAMP(2);
-    } else if (P.pre) {
-      for (long long c = gtid; c < P.n; c += gsize) {
-        double acc = 0.0;
-        for (int q = P.rtptr[c]; q < P.rtptr[c + 1]; ++q) acc += P.rtval[q] * P.s[P.rtidx[q]];
-        P.z[c] = P.v[c] + acc;
+    }
+    grid.sync();  // B1
+    STAMP(1);
+    if (pending) {
+      // ---- stop tests of iteration j (lsqr.hpp:183-203), identical in every CTA
+      const double ynorm = sqrt(grid_sum(P.part, 3, nb, red));
+      int reason = kReasonNone;
+      bool stop = false;
+      if (nonfinite) {
+        stop = true;
+      } else {
+        const double grad = phibar * alpha * fabs(cc);
+        const double sqn = sqrt(opnorm2);
+        if (grad <= eps * sqn * phibar || phibar <= eps * (sqn * ynorm + phibar0) || phibar == 0.0) {
+          stop = true;
+          reason = kReasonGradientTol;
+        } else if (j >= 2 && nu > 0.0 && !isinf(nu)) {
+          if (floor_ > 0.0 && cvgdiff < floor_) reason = kReasonDynamicDiff;
+          else if (cvgrate <= 0.0) reason = kReasonDynamicRate;
+          else if (cvgrate1 / cvgrate > nu) reason = kReasonDynamicRate;
+          stop = reason != kReasonNone;
+        }
+        if (!stop && j >= cap) {
+          stop = true;
+          reason = kReasonIterationCap;
+        }
       }
-      grid.sync();
-      STAMP(2);
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (j < tcap)
+          P.trace[j] = TraceRow{phibar, cvgrate, cvgdiff, (globaltimer_ns() - t0) * 1e-6, j,
+                                1ull + 2ull * static_cast<unsigned long long>(j)};
+        if (stop) {
+          st->alpha = alpha;
+          st->beta = beta;
+          st->rhobar = rhobar;
+          st->phibar = phibar;
+          st->opnorm2 = opnorm2;
+          st->cvgrate1 = cvgrate1;
+          st->ynorm = ynorm;
+          st->iter = j;
+          st->done = 1;
+          st->reason = reason;
+          st->breakdown = nonfinite ? 1 : 0;
+        }
+      }
+      if (stop) return;
     }
     // ---- S3: u <- A z - alpha u/beta ; tail rows
+    const double* zg = P.pre ? P.z : P.v;
+    const double* zs = zg;
+    if (P.zsmem) {
+      const long long h2 = P.n >> 1;
+      const double2* src = reinterpret_cast<const double2*>(zg);
+      double2* dst = reinterpret_cast<double2*>(dyn);
+      for (long long i = threadIdx.x; i < h2; i += kPT) dst[i] = src[i];
+      if ((P.n & 1) && threadIdx.x == 0) dyn[P.n - 1] = zg[P.n - 1];
+      __syncthreads();
+      zs = dyn;
+    }
+    STAMP(2);
     {
       double sq = 0.0, sqt = 0.0;
-      // thread per row (rows are short): every load of a row is independent of
-      // the add chain, so 4-wide unrolling keeps several gathers in flight
-      for (long long r = gtid; r < P.mloc; r += gsize) {
-        const int b = P.aptr[r], e = P.aptr[r + 1];
-        double acc = 0.0;
-        int q = b;
-        for (; q + 4 <= e; q += 4) {
-          const int c0 = P.aidx[q], c1 = P.aidx[q + 1], c2 = P.aidx[q + 2], c3 = P.aidx[q + 3];
-          const double v0 = P.aval[q], v1 = P.aval[q + 1], v2 = P.aval[q + 2], v3 = P.aval[q + 3];
-          const double z0 = zsrc[c0], z1 = zsrc[c1], z2 = zsrc[c2], z3 = zsrc[c3];
-          acc += v0 * z0;
-          acc += v1 * z1;
-          acc += v2 * z2;
-          acc += v3 * z3;
+      const double rb = beta;
+      if (P.sidx) {
+        // SELL-32: warp = 32 consecutive rows, lane = row; idx/val coalesced
+        for (long long ch = gwarp; ch < P.nchunks; ch += nwarps) {
+          const long long r = ch * 32 + lane;
+          const bool ok = r < P.mloc;
+          const int len = ok ? __ldg(P.aptr + r + 1) - __ldg(P.aptr + r) : 0;
+          const long long off = __ldg(P.soff + ch) + lane;
+          const int* ip = P.sidx + off;
+          const double* vp = P.sval + off;
+          double acc = 0.0;
+          int k = 0;
+          for (; k + 4 <= len; k += 4) {
+            const int i0 = __ldg(ip + 32 * k), i1 = __ldg(ip + 32 * (k + 1));
+            const int i2 = __ldg(ip + 32 * (k + 2)), i3 = __ldg(ip + 32 * (k + 3));
+            const double a0 = __ldg(vp + 32 * k), a1 = __ldg(vp + 32 * (k + 1));
+            const double a2 = __ldg(vp + 32 * (k + 2)), a3 = __ldg(vp + 32 * (k + 3));
+            const double z0 = zs[i0], z1 = zs[i1], z2 = zs[i2], z3 = zs[i3];
+            acc += a0 * z0;
+            acc += a1 * z1;
+            acc += a2 * z2;
+            acc += a3 * z3;
+          }
+          for (; k < len; ++k) acc += __ldg(vp + 32 * k) * zs[__ldg(ip + 32 * k)];
+          if (ok) {
+            const double uo = P.u[r];
+            const double uh = rb > 0.0 ? uo / rb : uo;
+            const double t = acc - alpha * uh;
+            P.u[r] = t;
+            sq += t * t;
+          }
         }
-        for (; q < e; ++q) acc += P.aval[q] * zsrc[P.aidx[q]];
-        {
+      } else {
+        // thread per row (rows are short): 4-wide unrolling keeps gathers in flight
+        for (long long r = gtid; r < P.mloc; r += gsize) {
+          const int b = __ldg(P.aptr + r), e = __ldg(P.aptr + r + 1);
+          double acc = 0.0;
+          int q = b;
+          for (; q + 4 <= e; q += 4) {
+            const int i0 = __ldg(P.aidx + q), i1 = __ldg(P.aidx + q + 1);
+            const int i2 = __ldg(P.aidx + q + 2), i3 = __ldg(P.aidx + q + 3);
+            const double a0 = __ldg(P.aval + q), a1 = __ldg(P.aval + q + 1);
+            const double a2 = __ldg(P.aval + q + 2), a3 = __ldg(P.aval + q + 3);
+            const double z0 = zs[i0], z1 = zs[i1], z2 = zs[i2], z3 = zs[i3];
+            acc += a0 * z0;
+            acc += a1 * z1;
+            acc += a2 * z2;
+            acc += a3 * z3;
+          }
+          for (; q < e; ++q) acc += __ldg(P.aval + q) * zs[__ldg(P.aidx + q)];
           const double uo = P.u[r];
-          const double uh = beta > 0.0 ? uo / beta : uo;
+          const double uh = rb > 0.0 ? uo / rb : uo;
           const double t = acc - alpha * uh;
           P.u[r] = t;
           sq += t * t;
@@ -177,8 +306,8 @@ __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
         double* ut = P.u + P.mloc;
         for (long long c = gtid; c < P.n; c += gsize) {
           const double uo = ut[c];
-          const double uh = beta > 0.0 ? uo / beta : uo;
-          const double t = P.mu * zsrc[c] - alpha * uh;
+          const double uh = rb > 0.0 ? uo / rb : uo;
+          const double t = P.mu * zs[c] - alpha * uh;
           ut[c] = t;
           sqt += t * t;
         }
@@ -190,24 +319,28 @@ __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
         P.part[blockIdx.x * 4 + 1] = sqt;
       }
     }
-    grid.sync();
+    grid.sync();  // B2
     STAMP(3);
-    // ---- S4: beta ; h = (A^T u + mu u_t) / beta  [plain: v = h - beta v, ||v||^2]
+    // ---- S4: beta ; h = (A^T u + mu u_t) / beta  [plain: v_raw = h - beta v, ||v_raw||^2]
     const double bnew = sqrt(grid_sum(P.part, 0, nb, red) + grid_sum(P.part, 1, nb, red));
     {
       double sq = 0.0;
       for (long long c = gwarp; c < P.n; c += nwarps) {
-        double acc = 0.0, acc2 = 0.0;
-        const int e = P.tptr[c + 1];
-        int q = P.tptr[c] + lane;
-        for (; q + 32 < e; q += 64) {
-          const int i0 = P.tidx[q], i1 = P.tidx[q + 32];
-          const double v0 = P.tval[q], v1 = P.tval[q + 32];
-          acc += v0 * P.u[i0];
-          acc2 += v1 * P.u[i1];
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        const int e = __ldg(P.tptr + c + 1);
+        int q = __ldg(P.tptr + c) + lane;
+        for (; q + 96 < e; q += 128) {
+          const int i0 = __ldg(P.tidx + q), i1 = __ldg(P.tidx + q + 32);
+          const int i2 = __ldg(P.tidx + q + 64), i3 = __ldg(P.tidx + q + 96);
+          const double v0 = __ldg(P.tval + q), v1 = __ldg(P.tval + q + 32);
+          const double v2 = __ldg(P.tval + q + 64), v3 = __ldg(P.tval + q + 96);
+          a0 += v0 * P.u[i0];
+          a1 += v1 * P.u[i1];
+          a2 += v2 * P.u[i2];
+          a3 += v3 * P.u[i3];
         }
-        if (q < e) acc += P.tval[q] * P.u[P.tidx[q]];
-        acc = warp_sum(acc + acc2);
+        for (; q < e; q += 32) a0 += __ldg(P.tval + q) * P.u[__ldg(P.tidx + q)];
+        double acc = warp_sum((a0 + a1) + (a2 + a3));
         if (lane == 0) {
           if (P.has_tail) acc += P.mu * P.u[P.mloc + c];
           const double gj = bnew > 0.0 ? acc / bnew : acc;
@@ -215,7 +348,7 @@ __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
             P.h[c] = gj;
           } else {
             const double t = gj - bnew * P.v[c];
-            P.v[c] = t;
+            P.vr[c] = t;
             sq += t * t;
           }
         }
@@ -225,105 +358,133 @@ __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
         if (threadIdx.x == 0) P.part[blockIdx.x * 4 + 2] = sq;
       }
     }
-    grid.sync();
+    grid.sync();  // B3
     STAMP(4);
     if (P.pre) {
-      // ---- S5/S6: v = h + R^T Ga R h - beta v ; ||v||^2
-      grid_project(grid, P.rptr, P.ridx, P.rval, P.Ga, P.l, P.h, P.t, P.s, gwarp, nwarps, lane);
-      grid.sync();
-      STAMP(5);
+      // ---- S56: v_raw = h + R^T Ga R h - beta v ; ||v_raw||^2
       double sq = 0.0;
-      for (long long c = gtid; c < P.n; c += gsize) {
-        double acc = 0.0;
-        for (int q = P.rtptr[c]; q < P.rtptr[c + 1]; ++q) acc += P.rtval[q] * P.s[P.rtidx[q]];
-        const double t = (P.h[c] + acc) - bnew * P.v[c];
-        P.v[c] = t;
-        sq += t * t;
+      if (P.fused) {
+        cta_project(P, P.h, 1.0, P.Ga, tsh, dsh, c0, c1, warp, lane);
+        const int qb0 = __ldg(P.rtptr + c0);
+        for (long long c = c0 + threadIdx.x; c < c1; c += kPT) {
+          double acc = 0.0;
+          for (int q = __ldg(P.rtptr + c); q < __ldg(P.rtptr + c + 1); ++q) acc += dsh[q - qb0];
+          const double t = (P.h[c] + acc) - bnew * P.v[c];
+          P.vr[c] = t;
+          sq += t * t;
+        }
+      } else {
+        grid_project(grid, P.rptr, P.ridx, P.rval, P.Ga, P.l, P.h, 1.0, P.t, P.s, gwarp, nwarps, lane);
+        grid.sync();
+        for (long long c = c0 + threadIdx.x; c < c1; c += kPT) {
+          double acc = 0.0;
+          for (int q = P.rtptr[c]; q < P.rtptr[c + 1]; ++q) acc += P.rtval[q] * P.s[P.rtidx[q]];
+          const double t = (P.h[c] + acc) - bnew * P.v[c];
+          P.vr[c] = t;
+          sq += t * t;
+        }
       }
       sq = block_sum<kPT>(sq, red);
       if (threadIdx.x == 0) P.part[blockIdx.x * 4 + 2] = sq;
-      grid.sync();
-      STAMP(6);
+      grid.sync();  // B4
     }
-    // ---- S7: alpha ; rotation (lsqr.hpp:145-171) ; vector updates ; ||y||^2
+    STAMP(5);
+    // ---- S7: alpha ; rotation (lsqr.hpp:145-171) ; owner-column updates ; ||y||^2
     const double anew = sqrt(grid_sum(P.part, 2, nb, red));
     beta = bnew;
     alpha = anew;
     opnorm2 += alpha * alpha + beta * beta;
     const double rho = hypot(rhobar, beta);
-    const double c = rhobar / rho;
+    cc = rhobar / rho;
     const double s = beta / rho;
     const double theta = s * alpha;
-    rhobar = -c * alpha;
-    const double phi = c * phibar;
+    rhobar = -cc * alpha;
+    const double phi = cc * phibar;
     const double phibar_prev = phibar;
     phibar = s * phibar;
     const double t1 = phi / rho, t2 = -theta / rho;
     ++j;
-    const bool nonfinite = !isfinite(phibar) || !isfinite(alpha) || !isfinite(beta);
-    const double cvgrate = (phibar > 0.0 && phibar_prev > 0.0) ? log(phibar_prev / phibar) : CUDART_INF;
-    const double cvgdiff = phibar_prev - phibar;
+    nonfinite = !isfinite(phibar) || !isfinite(alpha) || !isfinite(beta);
+    cvgrate = (phibar > 0.0 && phibar_prev > 0.0) ? log(phibar_prev / phibar) : CUDART_INF;
+    cvgdiff = phibar_prev - phibar;
     if (j == 1) cvgrate1 = cvgrate;
+    vdiv = alpha > 0.0 ? alpha : 1.0;
+    vsrc = P.vr;
     {
       double sq = 0.0;
-      for (long long cc = gtid; cc < P.n; cc += gsize) {
-        const double vo = P.v[cc];
-        const double vh = alpha > 0.0 ? vo / alpha : vo;
-        P.v[cc] = vh;
-        const double wo = P.w[cc];
-        const double yn = P.y[cc] + t1 * wo;
-        P.y[cc] = yn;
-        P.w[cc] = vh + t2 * wo;
+      for (long long c = c0 + threadIdx.x; c < c1; c += kPT) {
+        const double vh = P.vr[c] / vdiv;
+        P.v[c] = vh;
+        const double wo = P.w[c];
+        const double yn = P.y[c] + t1 * wo;
+        P.y[c] = yn;
+        P.w[c] = vh + t2 * wo;
         sq += yn * yn;
       }
       sq = block_sum<kPT>(sq, red);
       if (threadIdx.x == 0) P.part[blockIdx.x * 4 + 3] = sq;
     }
-    grid.sync();
-    if (P.prof && blockIdx.x == 0 && threadIdx.x == 0 && j - 1 < 64) P.prof[(j - 1) * 8 + 7] = globaltimer_ns();
-    // ---- S8: stop tests (identical decision in every CTA)
-    const double ynorm = sqrt(grid_sum(P.part, 3, nb, red));
-    int reason = kReasonNone;
-    bool stop = false;
-    if (nonfinite) {
-      stop = true;
-    } else {
-      const double grad = phibar * alpha * fabs(c);
-      const double sqn = sqrt(opnorm2);
-      if (grad <= eps * sqn * phibar || phibar <= eps * (sqn * ynorm + phibar0) || phibar == 0.0) {
-        stop = true;
-        reason = kReasonGradientTol;
-      } else if (j >= 2 && nu > 0.0 && !isinf(nu)) {
-        if (floor_ > 0.0 && cvgdiff < floor_) reason = kReasonDynamicDiff;
-        else if (cvgrate <= 0.0) reason = kReasonDynamicRate;
-        else if (cvgrate1 / cvgrate > nu) reason = kReasonDynamicRate;
-        stop = reason != kReasonNone;
-      }
-      if (!stop && j >= cap) {
-        stop = true;
-        reason = kReasonIterationCap;
-      }
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      if (j < tcap)
-        P.trace[j] = TraceRow{phibar, cvgrate, cvgdiff, (globaltimer_ns() - t0) * 1e-6, j,
-                              1ull + 2ull * static_cast<unsigned long long>(j)};
-      if (stop) {
-        st->alpha = alpha;
-        st->beta = beta;
-        st->rhobar = rhobar;
-        st->phibar = phibar;
-        st->opnorm2 = opnorm2;
-        st->cvgrate1 = cvgrate1;
-        st->ynorm = ynorm;
-        st->iter = j;
-        st->done = 1;
-        st->reason = reason;
-        st->breakdown = nonfinite ? 1 : 0;
-      }
-    }
-    if (stop) return;
+    pending = true;
+    if (P.prof && blockIdx.x == 0 && threadIdx.x == 0 && j - 1 < 64) P.prof[(j - 1) * 8 + 6] = globaltimer_ns();
   }
+}
+
+// ---- SELL-32 build from the CSR (once per matrix)
+__global__ void sell_width_kernel(const int* __restrict__ ptr, long long rows, long long chunks,
+                                  int* __restrict__ width) {
+  const long long ch = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (ch > chunks) return;
+  if (ch == chunks) {
+    width[ch] = 0;
+    return;
+  }
+  int w = 0;
+  const long long rend = ch * 32 + 32 < rows ? ch * 32 + 32 : rows;
+  for (long long r = ch * 32; r < rend; ++r) w = max(w, ptr[r + 1] - ptr[r]);
+  width[ch] = 32 * w;
+}
+
+__global__ void sell_fill_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                 const double* __restrict__ val, long long rows, const int* __restrict__ off,
+                                 int* __restrict__ sidx, double* __restrict__ sval) {
+  const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const long long base = off[r >> 5] + (r & 31);
+  const int b = ptr[r], e = ptr[r + 1];
+  for (int q = b; q < e; ++q) {
+    sidx[base + 32LL * (q - b)] = idx[q];
+    sval[base + 32LL * (q - b)] = val[q];
+  }
+}
+
+void build_sell(apc_mat& a) {
+  apc_ctx* ctx = a.ctx;
+  cudaStream_t st = ctx->stream;
+  Sell& s = a.sell;
+  const long long rows = a.a.rows;
+  s.rows = rows;
+  s.chunks = (rows + 31) / 32;
+  s.off.alloc(s.chunks + 1);
+  DBuf<int> width(s.chunks + 1);
+  sell_width_kernel<<<static_cast<unsigned>((s.chunks + 1 + 255) / 256), 256, 0, st>>>(a.a.ptr.p, rows, s.chunks,
+                                                                                         width.p);
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, width.p, s.off.p, static_cast<int>(s.chunks + 1), st);
+  DBuf<unsigned char> tbuf(static_cast<long long>(std::max<size_t>(tmp, 1)));
+  APC_CUDA(cub::DeviceScan::ExclusiveSum(tbuf.p, tmp, width.p, s.off.p, static_cast<int>(s.chunks + 1), st));
+  int slots = 0;
+  copy_sync(st, &slots, s.off.p + s.chunks, sizeof(int), cudaMemcpyDeviceToHost);
+  s.slots = slots;
+  s.idx.alloc(std::max(1, slots));
+  s.val.alloc(std::max(1, slots));
+  APC_CUDA(cudaMemsetAsync(s.idx.p, 0, s.idx.bytes(), st));
+  APC_CUDA(cudaMemsetAsync(s.val.p, 0, s.val.bytes(), st));
+  if (rows > 0)
+    sell_fill_kernel<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p,
+                                                                               rows, s.off.p, s.idx.p, s.val.p);
+  APC_CUDA(cudaGetLastError());
+  ctx->launches += rows > 0 ? 3 : 2;
+  APC_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace
@@ -350,6 +511,24 @@ void lsqr_persistent_run(apc_mat& a, double mu, const PrecondDev* p, const Persi
   P.mu = mu;
   P.has_tail = mu > 0.0 ? 1 : 0;
   P.pre = (p && p->kind == 2) ? 1 : 0;
+  // the SELL copy pays for itself when the CSR is L2-resident (the gathers,
+  // not HBM, bound the forward product); APC_PERSISTENT_SELL=0 disables it
+  const char* sell_env = std::getenv("APC_PERSISTENT_SELL");
+  const bool want_sell = (sell_env ? std::atoi(sell_env) != 0 : true) && a.a.nnz * 12 <= (96LL << 20) &&
+                         a.a.nnz * 3 / 2 + 32 * 64 < (1LL << 31);
+  if (want_sell) {
+    if (a.sell.rows != a.a.rows || !a.sell.off.p) build_sell(a);
+    P.soff = a.sell.off.p;
+    P.sidx = a.sell.idx.p;
+    P.sval = a.sell.val.p;
+    P.nchunks = a.sell.chunks;
+  }
+  int per_sm = 0;
+  APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lsqr_persistent_kernel, kPT, 0));
+  const int blocks_per_sm = std::max(1, std::min(per_sm, b.blocks_per_sm > 0 ? b.blocks_per_sm : 3));
+  const int grid = ctx->num_sms * blocks_per_sm;
+  P.cchunk = std::max<long long>(1, (a.n + grid - 1) / grid);
+  long long smem_doubles = 1;
   if (P.pre) {
     P.rptr = p->R.ptr.p;
     P.ridx = p->R.idx.p;
@@ -360,9 +539,30 @@ void lsqr_persistent_run(apc_mat& a, double mu, const PrecondDev* p, const Persi
     P.Gf = p->Kf.p;
     P.Ga = p->Ka.p;
     P.l = p->l;
+    // per-CTA projection when R is small: every CTA re-walks nnz(R) and reads
+    // one K row per R^T entry of its columns
+    const char* fe = std::getenv("APC_PERSISTENT_FUSED");
+    const bool want_fused = (fe ? std::atoi(fe) != 0 : true) && p->R.nnz <= 32768 && p->R.nnz * p->l <= (8LL << 20);
+    if (want_fused) {
+      std::vector<int> hp(static_cast<size_t>(a.n + 1));
+      copy_sync(ctx->stream, hp.data(), p->RT.ptr.p, sizeof(int) * hp.size(), cudaMemcpyDeviceToHost);
+      long long qmax = 0;
+      for (long long c0 = 0; c0 < a.n; c0 += P.cchunk)
+        qmax = std::max<long long>(qmax, hp[std::min<long long>(a.n, c0 + P.cchunk)] - hp[c0]);
+      if ((P.l + qmax) * 8 <= kSmemBudget) {
+        P.fused = 1;
+        smem_doubles = std::max(smem_doubles, P.l + qmax);
+      }
+    }
+  }
+  const char* ze = std::getenv("APC_PERSISTENT_ZSMEM");
+  if ((ze ? std::atoi(ze) != 0 : true) && P.n * 8 <= kSmemBudget) {
+    P.zsmem = 1;
+    smem_doubles = std::max(smem_doubles, P.n);
   }
   P.u = b.u;
   P.v = b.v;
+  P.vr = b.vr;
   P.w = b.w;
   P.y = b.y;
   P.z = b.z;
@@ -372,28 +572,12 @@ void lsqr_persistent_run(apc_mat& a, double mu, const PrecondDev* p, const Persi
   P.prof = b.prof;
   P.st = b.st;
   P.trace = b.trace;
-  const int G = csr_group_size_p(a.a.avg_row_nnz);
-  void* kfn = nullptr;
-  switch (G) {
-    case 4: kfn = reinterpret_cast<void*>(lsqr_persistent_kernel<4>); break;
-    case 8: kfn = reinterpret_cast<void*>(lsqr_persistent_kernel<8>); break;
-    case 16: kfn = reinterpret_cast<void*>(lsqr_persistent_kernel<16>); break;
-    default: kfn = reinterpret_cast<void*>(lsqr_persistent_kernel<32>); break;
-  }
-  P.group = G;
-  // measured on C2: the per-CTA z build costs more (latency-bound RT walk) than
-  // the L2 gathers it saves, so shared-memory z is opt-in only
-  P.zsmem = (P.n * 8 <= 200 * 1024 && std::getenv("APC_PERSISTENT_ZSMEM")) ? 1 : 0;
-  const size_t smem = sizeof(double) * static_cast<size_t>(std::max<long long>(1, P.zsmem ? P.n : 1));
-  if (smem > 48 * 1024) APC_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
+  void* kfn = reinterpret_cast<void*>(lsqr_persistent_kernel);
+  const size_t smem = sizeof(double) * static_cast<size_t>(smem_doubles);
+  APC_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kPT, smem));
-  // fewer CTAs make each grid barrier cheaper; the L2-resident stages need
-  // only a couple of CTAs per SM to saturate
-  const int blocks_per_sm = std::max(1, std::min(per_sm, b.blocks_per_sm > 0 ? b.blocks_per_sm : 3));
-  const int grid = ctx->num_sms * blocks_per_sm;
-  double* part = b.part;
-  P.part = part;
+  require(per_sm >= blocks_per_sm, APC_CUDA_ERROR, "persistent LSQR: grid does not fit co-resident");
+  P.part = b.part;
   void* args[] = {&P};
   APC_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kPT), args, smem, ctx->stream));
   ctx->launches++;

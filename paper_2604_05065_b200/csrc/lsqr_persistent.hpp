@@ -7,11 +7,11 @@
 namespace apc {
 
 struct PersistentBuffers {
-  double *u, *v, *w, *y, *z, *h, *s, *t, *part;
+  double *u, *v, *vr, *w, *y, *z, *h, *s, *t, *part;  // vr: raw v (n)
   LsqrState* st;
   TraceRow* trace;
   int blocks_per_sm;
-  unsigned long long* prof;  // optional: 64 x 8 stage timestamps
+  unsigned long long* prof;  // optional: 64 x 8 stage timestamps (7 used)
 };
 
 // sparse A, one rank, no split transpose rows, identity or implicit basis
