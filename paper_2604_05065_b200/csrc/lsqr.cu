@@ -678,31 +678,56 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
     w->pers_part.ensure(4LL * persistent_max_grid(ctx));
     const char* bps = std::getenv("APC_PERSISTENT_BLOCKS_PER_SM");
     const bool prof = std::getenv("APC_PERSISTENT_PROF") != nullptr;
-    DBuf<unsigned long long> d_prof(prof ? 64 * 8 : 0);
+    DBuf<unsigned long long> d_prof(prof ? 64 * 16 + 16LL * persistent_max_grid(ctx) : 0);
     if (prof) APC_CUDA(cudaMemsetAsync(d_prof.p, 0, d_prof.bytes(), st));
     PersistentBuffers pb{w->u.p, w->v.p, w->g.p, w->w.p, y_d, w->z.p, w->h.p, w->s.p, w->t.p, w->pers_part.p,
                          w->st.p, w->trace.p, bps ? std::atoi(bps) : 0, prof ? d_prof.p : nullptr};
     lsqr_persistent_run(a, mu, p, pb);
     per_iter = 0;
     if (prof) {
-      std::vector<unsigned long long> h(64 * 8);
+      std::vector<unsigned long long> h(static_cast<size_t>(d_prof.n));
       copy_sync(st, h.data(), d_prof.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
-      // stamps: 0 top, 1 B1, 2 z staged, 3 B2, 4 B3, 5 B4, 6 end of S7
-      double acc[7] = {0};
+      // 16 stamps per iteration (lsqr_persistent.cu STAMP(k)); interval k runs
+      // from stamp k to the next recorded one
+      static const char* names[16] = {"S12proj", "S12z", "B1", "zcopy", "-", "S3loop", "S3red", "B2",
+                                      "beta+stop", "S4loop", "B3", "S56proj", "S56v", "B4", "S7", "-"};
+      double acc[16] = {0};
       int cnt = 0;
       for (int it = 2; it < 63; ++it) {
-        if (h[(it + 1) * 8] == 0) break;
-        for (int k = 0; k < 7; ++k) {
-          unsigned long long a0 = h[it * 8 + k], a1 = k < 6 ? h[it * 8 + k + 1] : h[(it + 1) * 8];
-          if (a0 && a1) acc[k] += (a1 - a0) * 1e-3;
+        if (h[(it + 1) * 16] == 0) break;
+        for (int k = 0; k < 16; ++k) {
+          const unsigned long long a0 = h[it * 16 + k];
+          if (!a0) continue;
+          unsigned long long a1 = 0;
+          for (int q = k + 1; q < 16 && !a1; ++q) a1 = h[it * 16 + q];
+          if (!a1) a1 = h[(it + 1) * 16];
+          acc[k] += (a1 - a0) * 1e-3;
         }
         ++cnt;
       }
-      if (cnt)
-        std::fprintf(stderr, "persistent stage us/iter (%d its): S12+B1 %.2f stop+zcopy %.2f S3+B2 %.2f S4+B3 %.2f "
-                     "S56+B4 %.2f S7 %.2f loop %.2f\n",
-                     cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt,
-                     acc[6] / cnt);
+      if (cnt) {
+        std::fprintf(stderr, "persistent stage us/iter (%d its):", cnt);
+        double tot = 0.0;
+        for (int k = 0; k < 16; ++k)
+          if (acc[k] > 0.0) {
+            std::fprintf(stderr, " %s %.2f", names[k], acc[k] / cnt);
+            tot += acc[k] / cnt;
+          }
+        std::fprintf(stderr, " | total %.2f\n", tot);
+        // per-CTA interval sums (iterations 2..63): min / median / max over CTAs
+        std::fprintf(stderr, "per-CTA us/iter min/med/max:");
+        for (int k = 1; k < 16; ++k) {
+          std::vector<double> v;
+          for (int b = 0; b < persistent_max_grid(ctx); ++b) {
+            const unsigned long long x = h[64 * 16 + b * 16 + k];
+            if (x) v.push_back(x * 1e-3 / 62.0);
+          }
+          if (v.empty()) continue;
+          std::sort(v.begin(), v.end());
+          std::fprintf(stderr, " [%s %.1f/%.1f/%.1f]", names[k - 1], v.front(), v[v.size() / 2], v.back());
+        }
+        std::fprintf(stderr, "\n");
+      }
     }
   } else if (use_while) {
     APC_CUDA(cudaGraphCreate(&graph, 0));

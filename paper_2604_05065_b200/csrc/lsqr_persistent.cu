@@ -38,14 +38,23 @@ namespace cg = cooperative_groups;
 
 namespace apc {
 
-#define STAMP(k) \
-  if (P.prof && blockIdx.x == 0 && threadIdx.x == 0 && j < 64) P.prof[j * 8 + (k)] = globaltimer_ns()
+#define STAMP(k)                                                                                 \
+  if (P.prof && threadIdx.x == 0 && j < 64) {                                                      \
+    const unsigned long long now_ = globaltimer_ns();                                              \
+    if (blockIdx.x == 0) P.prof[j * 16 + (k)] = now_;                                              \
+    if (j >= 2) P.prof[64 * 16 + blockIdx.x * 16 + (k)] += now_ - prev_stamp;                      \
+    prev_stamp = now_;                                                                             \
+  }
 
 namespace {
 
-constexpr int kPT = 1024;  // threads per CTA: one fat CTA per SM keeps grid barriers cheap
-constexpr int kNW = kPT / 32;
-constexpr long long kSmemBudget = 200 * 1024;  // dynamic shared memory the kernel may use
+// threads per CTA (template PT): one fat CTA per SM keeps grid barriers cheap;
+// 1024 threads cap registers at 64, 512 allow 128 (no spills, fewer warps)
+#ifndef APC_SELL_U
+#define APC_SELL_U 8
+#endif
+constexpr int kSellU = APC_SELL_U;  // SELL entries per predicated load block
+constexpr long long kSmemBudget = 200 * 1024;  // dynamic shared memory (z / projection scratch)
 
 struct PArgs {
   // A: CSR rows (mloc) and CSR of A^T (n rows, no split rows)
@@ -71,19 +80,102 @@ struct PArgs {
   const double* rtval;
   const double *Gf, *Ga;  // row-major l x l
   long long l;
+  int rnnz;        // nnz(R) (fused: products staged per CTA)
+  long long qmax;  // max R^T entries over the CTAs' column ranges (fused)
+  int regs;  // 1: phase-constant projection operands held in registers (small R, l <= 256)
   // vectors
   double *u, *v, *vr, *w, *y, *z, *h, *s, *t;
-  double* part;  // gridDim.x x 4
+  double* part;  // 4 slots x kPartStride
   unsigned long long* prof;  // optional stage timestamps (first 64 iterations)
   LsqrState* st;
   TraceRow* trace;
 };
 
-__device__ __forceinline__ double grid_sum(const double* part, int slot, int nblocks, double* sh) {
-  // every CTA sums the same per-CTA partials in the same order
-  double v = 0.0;
-  for (int b = threadIdx.x; b < nblocks; b += kPT) v += part[b * 4 + slot];
-  return block_sum<kPT>(v, sh);
+// sum_{k < len} val[s k] * (x[idx[s k]] / xdiv), added strictly in k order; U
+// entries per block are loaded under predicates so one block costs one memory
+// round trip (a plain loop would pay one per entry)
+template <int U, bool kDiv>
+__device__ __forceinline__ double seq_dot(const int* idx, const double* val, int s, int len, const double* x,
+                                          double xdiv = 1.0) {
+  double acc = 0.0;
+  for (int k0 = 0; k0 < len; k0 += U) {
+    int i[U];
+    double a[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = k0 + u < len;
+      i[u] = ok ? __ldg(idx + s * (k0 + u)) : 0;
+      a[u] = ok ? __ldg(val + s * (k0 + u)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = (k0 + u < len) ? x[i[u]] : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k0 + u < len) acc += a[u] * (kDiv ? xv[u] / xdiv : xv[u]);
+  }
+  return acc;
+}
+
+// Grid sums of per-CTA partials (layout part[slot * kPartStride + cta]): warp
+// 0 of every CTA sums each requested slot in the same fixed order (lane
+// stripes, then butterfly) and shares the results through shared memory --
+// one reader per SM keeps the few hot partial lines from being hammered.
+constexpr int kPartStride = 2048;
+template <int NS>
+__device__ __forceinline__ void grid_sums(const double* part, const int (&slots)[NS], int nblocks, double* out_sh,
+                                          double (&out)[NS]) {
+  if (threadIdx.x < 32) {
+    double v[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) v[k] = 0.0;
+    for (int b0 = 0; b0 < nblocks; b0 += 256) {  // all loads of a block in flight at once
+      double x[NS][8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int b = b0 + threadIdx.x + 32 * u;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) x[k][u] = b < nblocks ? part[slots[k] * kPartStride + b] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+          if (b0 + threadIdx.x + 32 * u < nblocks) v[k] += x[k][u];
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const double t = warp_sum(v[k]);
+      if (threadIdx.x == 0) out_sh[k] = t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NS; ++k) out[k] = out_sh[k];
+}
+
+// CTA partial sums of up to two values -> part[blockIdx.x * 4 + slot] (fixed
+// order: lanes by butterfly, warps in index order).  One block barrier; the
+// caller's next grid barrier orders the reuse of `red`.
+template <int PT>
+__device__ __forceinline__ void cta_partial(double a, double b, double* red, double* part, int slot_a,
+                                            int slot_b) {
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[w] = a;
+    red[32 + w] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sa = 0.0, sb = 0.0;
+    for (int k = 0; k < PT / 32; ++k) {
+      sa += red[k];
+      sb += red[32 + k];
+    }
+    part[slot_a * kPartStride + blockIdx.x] = sa;
+    if (slot_b >= 0) part[slot_b * kPartStride + blockIdx.x] = sb;
+  }
 }
 
 // t = M (x / xdiv), s = K t for the l x n sparse M (R) and row-major K, spread
@@ -108,34 +200,146 @@ __device__ void grid_project(cg::grid_group& grid, const int* mptr, const int* m
 }
 
 // Per-CTA projection for the columns [c0, c1) this CTA owns:
-//   tsh = R (x / xdiv)                 (all l rows, thread per row, in order)
+//   psh[q] = R_val[q] * (x[R_idx[q]] / xdiv)   every entry of R (entry-parallel)
+//   tsh[i] = sum_q psh[q] over row i, in order  (= (R x)_i)
 //   dsh[q - RT_ptr[c0]] = RT_val[q] * (K tsh)_{RT_idx[q]}   for q of the range
+// The K rows are fetched before t exists, so the stage costs about two memory
+// round trips (R entries -> x gathers) instead of one per dependent load.
+template <int PT>
 __device__ void cta_project(const PArgs& P, const double* x, double xdiv, const double* K, double* tsh,
-                            double* dsh, long long c0, long long c1, int warp, int lane) {
-  for (long long i = threadIdx.x; i < P.l; i += kPT) {
+                            double* dsh, double* psh, long long c0, long long c1, int warp, int lane) {
+  const int nr = P.rnnz;
+  for (int q0 = threadIdx.x; q0 < nr; q0 += 4 * PT) {
+    int i[4];
+    double a[4], xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + u * PT;
+      i[u] = q < nr ? __ldg(P.ridx + q) : 0;
+      a[u] = q < nr ? __ldg(P.rval + q) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xv[u] = q0 + u * PT < nr ? x[i[u]] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (q0 + u * PT < nr) psh[q0 + u * PT] = a[u] * (xv[u] / xdiv);
+  }
+  const int qb0 = __ldg(P.rtptr + c0), qb1 = __ldg(P.rtptr + c1);
+  const int qa = qb0 + warp;
+  const bool small = P.l <= 256;
+  double g[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) g[u] = 0.0;
+  if (small && qa < qb1) {
+    const double* row = K + static_cast<long long>(__ldg(P.rtidx + qa)) * P.l;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (lane + 32 * u < P.l) g[u] = __ldg(row + lane + 32 * u);
+  }
+  __syncthreads();
+  for (long long i = threadIdx.x; i < P.l; i += PT) {
     const int b = __ldg(P.rptr + i), e = __ldg(P.rptr + i + 1);
     double acc = 0.0;
-    for (int q = b; q < e; ++q) acc += __ldg(P.rval + q) * (x[__ldg(P.ridx + q)] / xdiv);
+    for (int q = b; q < e; ++q) acc += psh[q];
     tsh[i] = acc;
   }
   __syncthreads();
-  const int qb0 = __ldg(P.rtptr + c0), qb1 = __ldg(P.rtptr + c1);
-  for (int q = qb0 + warp; q < qb1; q += kNW) {
-    const double* row = K + static_cast<long long>(__ldg(P.rtidx + q)) * P.l;
+  for (int q = qa; q < qb1; q += PT / 32) {
     double acc = 0.0;
-    for (long long k = lane; k < P.l; k += 32) acc += __ldg(row + k) * tsh[k];
+    if (small && q == qa) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (lane + 32 * u < P.l) acc += g[u] * tsh[lane + 32 * u];
+    } else {
+      const double* row = K + static_cast<long long>(__ldg(P.rtidx + q)) * P.l;
+      for (long long k = lane; k < P.l; k += 32) acc += __ldg(row + k) * tsh[k];
+    }
     acc = warp_sum(acc);
     if (lane == 0) dsh[q - qb0] = __ldg(P.rtval + q) * acc;
   }
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
-  extern __shared__ double dyn[];  // z copy (S3) / t + d (S12, S56): disjoint in time
-  __shared__ double red[32];
+// The phase-constant operands of the per-CTA projection held in registers
+// (small R, l <= 256): R entries (4 per thread), the thread's row bounds of R,
+// this warp's first R^T entry and its rows of Gf / Ga.
+struct ProjRegs {
+  int ri[4];
+  double rv[4];
+  int rb, re;
+  int qb0, qb1, qa;
+  long long gi;  // K row of this warp's first R^T entry (-1: none)
+};
+
+template <int PT>
+__device__ __forceinline__ void proj_regs_load(const PArgs& P, ProjRegs& R, long long c0, long long c1, int warp) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int q = threadIdx.x + u * PT;
+    R.ri[u] = q < P.rnnz ? __ldg(P.ridx + q) : 0;
+    R.rv[u] = q < P.rnnz ? __ldg(P.rval + q) : 0.0;
+  }
+  R.rb = threadIdx.x < P.l ? __ldg(P.rptr + threadIdx.x) : 0;
+  R.re = threadIdx.x < P.l ? __ldg(P.rptr + threadIdx.x + 1) : 0;
+  R.qb0 = __ldg(P.rtptr + c0);
+  R.qb1 = __ldg(P.rtptr + c1);
+  R.qa = R.qb0 + warp;
+  R.gi = R.qa < R.qb1 ? static_cast<long long>(__ldg(P.rtidx + R.qa)) * P.l : -1;
+}
+
+// cta_project with the operands of ProjRegs: one memory round trip (the x
+// gathers) plus three block barriers.  Same arithmetic and order as cta_project.
+template <int PT, bool kFwd>
+__device__ __forceinline__ void cta_project_reg(const PArgs& P, const ProjRegs& R, const double* x, double xdiv,
+                                                double* tsh, double* dsh, double* psh, int lane) {
+  const int nr = P.rnnz;
+  double xv[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) xv[u] = threadIdx.x + u * PT < nr ? x[R.ri[u]] : 0.0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    if (threadIdx.x + u * PT < nr) psh[threadIdx.x + u * PT] = R.rv[u] * (xv[u] / xdiv);
+  for (int q = threadIdx.x + 4 * PT; q < nr; q += PT)  // beyond the register-held entries
+    psh[q] = __ldg(P.rval + q) * (x[__ldg(P.ridx + q)] / xdiv);
+  const double* K = kFwd ? P.Gf : P.Ga;
+  double g[8];  // this warp's first K row, fetched before t exists
+#pragma unroll
+  for (int u = 0; u < 8; ++u) g[u] = (R.gi >= 0 && lane + 32 * u < P.l) ? __ldg(K + R.gi + lane + 32 * u) : 0.0;
+  __syncthreads();
+  if (threadIdx.x < P.l) {
+    double acc = 0.0;
+    for (int q = R.rb; q < R.re; ++q) acc += psh[q];
+    tsh[threadIdx.x] = acc;
+  }
+  __syncthreads();
+  for (int q = R.qa; q < R.qb1; q += PT / 32) {
+    double acc = 0.0;
+    if (q == R.qa) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (lane + 32 * u < P.l) acc += g[u] * tsh[lane + 32 * u];
+    } else {
+      const double* row = K + static_cast<long long>(__ldg(P.rtidx + q)) * P.l;
+      for (long long k = lane; k < P.l; k += 32) acc += __ldg(row + k) * tsh[k];
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) dsh[q - R.qb0] = __ldg(P.rtval + q) * acc;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+template <int PT, bool kRegs>
+__global__ void __launch_bounds__(PT, 1) lsqr_persistent_kernel(PArgs P) {
+  extern __shared__ double dyn[];  // z copy (S3) / t, d, products (S12, S56): disjoint in time
+  __shared__ double red[64];
+  __shared__ double gsh[4];
   cg::grid_group grid = cg::this_grid();
-  const long long gtid = static_cast<long long>(blockIdx.x) * kPT + threadIdx.x;
-  const long long gsize = static_cast<long long>(gridDim.x) * kPT;
+  const long long gtid = static_cast<long long>(blockIdx.x) * PT + threadIdx.x;
+  const long long gsize = static_cast<long long>(gridDim.x) * PT;
   const long long gwarp = gtid >> 5, nwarps = gsize >> 5;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nb = gridDim.x;
@@ -153,7 +357,7 @@ __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
   long long j = st->iter;
   const unsigned long long t0 = st->t0_ns;
   if (st->done) return;
-  // quantities of the last completed iteration, tested after the next B1
+  // quantities of the last completed iteration, tested after the next B2
   bool pending = false, nonfinite = false;
   double cc = 0.0, cvgrate = 0.0, cvgdiff = 0.0;
   // v of the next S12 = vsrc / vdiv (first iteration: the initialised v)
@@ -161,15 +365,31 @@ __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
   double vdiv = 1.0;
   double* tsh = dyn;
   double* dsh = dyn + P.l;
+  double* psh = dsh + P.qmax;
+  unsigned long long prev_stamp = 0;
+  ProjRegs R;
+  constexpr bool regs = kRegs;
+  if (regs && P.fused) proj_regs_load<PT>(P, R, c0, c1, warp);
+  // z staging by one bulk (TMA) copy per iteration, completion on an mbarrier
+  __shared__ __align__(8) unsigned long long zbar;
+  unsigned zphase = 0;
+  const bool ztma = P.zsmem && ((P.n * 8) % 16 == 0);
+  if (ztma && threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&zbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
 
   for (;;) {
     // ---- S12: z = v + R^T Gf R v
     STAMP(0);
     if (P.pre) {
       if (P.fused) {
-        cta_project(P, vsrc, vdiv, P.Gf, tsh, dsh, c0, c1, warp, lane);
+        if (regs) cta_project_reg<PT, true>(P, R, vsrc, vdiv, tsh, dsh, psh, lane);
+        else cta_project<PT>(P, vsrc, vdiv, P.Gf, tsh, dsh, psh, c0, c1, warp, lane);
+        STAMP(1);
         const int qb0 = __ldg(P.rtptr + c0);
-        for (long long c = c0 + threadIdx.x; c < c1; c += kPT) {
+        for (long long c = c0 + threadIdx.x; c < c1; c += PT) {
           double acc = 0.0;
           for (int q = __ldg(P.rtptr + c); q < __ldg(P.rtptr + c + 1); ++q) acc += dsh[q - qb0];
           P.z[c] = P.v[c] + acc;
@@ -177,18 +397,110 @@ __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
       } else {
         grid_project(grid, P.rptr, P.ridx, P.rval, P.Gf, P.l, vsrc, vdiv, P.t, P.s, gwarp, nwarps, lane);
         grid.sync();
-        for (long long c = c0 + threadIdx.x; c < c1; c += kPT) {
+        for (long long c = c0 + threadIdx.x; c < c1; c += PT) {
           double acc = 0.0;
           for (int q = P.rtptr[c]; q < P.rtptr[c + 1]; ++q) acc += P.rtval[q] * P.s[P.rtidx[q]];
           P.z[c] = P.v[c] + acc;
         }
       }
     }
+    STAMP(2);
     grid.sync();  // B1
-    STAMP(1);
+    STAMP(3);
+    // ---- S3: u <- A z - alpha u/beta ; tail rows
+    const double* zg = P.pre ? P.z : P.v;
+    const double* zs = zg;
+    if (ztma) {
+      // B1 ordered every generic access to dyn and the z stores of all CTAs
+      // before this point; the proxy fence hands them to the async proxy
+      if (threadIdx.x == 0) {
+        const unsigned bytes = static_cast<unsigned>(P.n * 8);
+        asm volatile("fence.proxy.async;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&zbar)), "r"(bytes)
+                     : "memory");
+        for (unsigned off = 0; off < bytes; off += 32768) {
+          const unsigned len = bytes - off < 32768 ? bytes - off : 32768;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(reinterpret_cast<char*>(dyn) + off)),
+              "l"(reinterpret_cast<const char*>(zg) + off), "r"(len), "r"(smem_u32(&zbar))
+              : "memory");
+        }
+      }
+      asm volatile(
+          "{\n .reg .pred p;\n ZWAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra ZWAIT_%=;\n}" ::"r"(
+              smem_u32(&zbar)),
+          "r"(zphase)
+          : "memory");
+      zphase ^= 1u;
+      zs = dyn;
+    } else if (P.zsmem) {
+      const long long h2 = P.n >> 1;
+      const double2* src = reinterpret_cast<const double2*>(zg);
+      double2* dst = reinterpret_cast<double2*>(dyn);
+#pragma unroll 4
+      for (long long i = threadIdx.x; i < h2; i += PT) dst[i] = src[i];
+      if ((P.n & 1) && threadIdx.x == 0) dyn[P.n - 1] = zg[P.n - 1];
+      __syncthreads();
+      zs = dyn;
+    }
+    STAMP(5);
+    {
+      double sq = 0.0, sqt = 0.0;
+      const double rb = beta;
+      if (P.sidx) {
+        // SELL-32: warp = 32 consecutive rows, lane = row; idx/val coalesced
+        for (long long ch = gwarp; ch < P.nchunks; ch += nwarps) {
+          const long long r = ch * 32 + lane;
+          const bool ok = r < P.mloc;
+          const int len = ok ? __ldg(P.aptr + r + 1) - __ldg(P.aptr + r) : 0;
+          const double uo = ok ? P.u[r] : 0.0;
+          const long long off = __ldg(P.soff + ch) + lane;
+          const double acc = seq_dot<kSellU, false>(P.sidx + off, P.sval + off, 32, len, zs);
+          if (ok) {
+            const double uh = rb > 0.0 ? uo / rb : uo;
+            const double t = acc - alpha * uh;
+            P.u[r] = t;
+            sq += t * t;
+          }
+        }
+      } else {
+        // thread per row (rows are short)
+        for (long long r = gtid; r < P.mloc; r += gsize) {
+          const int b = __ldg(P.aptr + r), e = __ldg(P.aptr + r + 1);
+          const double uo = P.u[r];
+          const double acc = seq_dot<8, false>(P.aidx + b, P.aval + b, 1, e - b, zs);
+          const double uh = rb > 0.0 ? uo / rb : uo;
+          const double t = acc - alpha * uh;
+          P.u[r] = t;
+          sq += t * t;
+        }
+      }
+      if (P.has_tail) {
+        double* ut = P.u + P.mloc;
+        for (long long c = gtid; c < P.n; c += gsize) {
+          const double uo = ut[c];
+          const double uh = rb > 0.0 ? uo / rb : uo;
+          const double t = P.mu * zs[c] - alpha * uh;
+          ut[c] = t;
+          sqt += t * t;
+        }
+      }
+      STAMP(6);
+      cta_partial<PT>(sq, sqt, red, P.part, 0, 1);
+    }
+    STAMP(7);
+    grid.sync();  // B2
+    STAMP(8);
+    // beta of this iteration and ||y|| of the previous one in one pass
+    double sums[3];
+    grid_sums<3>(P.part, {0, 1, 3}, nb, gsh, sums);
+    const double s3 = pending ? sums[2] : 0.0;
+    const double bnew = sqrt(sums[0] + sums[1]);
     if (pending) {
-      // ---- stop tests of iteration j (lsqr.hpp:183-203), identical in every CTA
-      const double ynorm = sqrt(grid_sum(P.part, 3, nb, red));
+      // ---- stop tests of iteration j (lsqr.hpp:183-203), identical in every
+      // CTA; the S12/S3 work done since only touched z and u (scratch)
+      const double ynorm = sqrt(s3);
       int reason = kReasonNone;
       bool stop = false;
       if (nonfinite) {
@@ -230,143 +542,75 @@ __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
       }
       if (stop) return;
     }
-    // ---- S3: u <- A z - alpha u/beta ; tail rows
-    const double* zg = P.pre ? P.z : P.v;
-    const double* zs = zg;
-    if (P.zsmem) {
-      const long long h2 = P.n >> 1;
-      const double2* src = reinterpret_cast<const double2*>(zg);
-      double2* dst = reinterpret_cast<double2*>(dyn);
-      for (long long i = threadIdx.x; i < h2; i += kPT) dst[i] = src[i];
-      if ((P.n & 1) && threadIdx.x == 0) dyn[P.n - 1] = zg[P.n - 1];
-      __syncthreads();
-      zs = dyn;
-    }
-    STAMP(2);
-    {
-      double sq = 0.0, sqt = 0.0;
-      const double rb = beta;
-      if (P.sidx) {
-        // SELL-32: warp = 32 consecutive rows, lane = row; idx/val coalesced
-        for (long long ch = gwarp; ch < P.nchunks; ch += nwarps) {
-          const long long r = ch * 32 + lane;
-          const bool ok = r < P.mloc;
-          const int len = ok ? __ldg(P.aptr + r + 1) - __ldg(P.aptr + r) : 0;
-          const long long off = __ldg(P.soff + ch) + lane;
-          const int* ip = P.sidx + off;
-          const double* vp = P.sval + off;
-          double acc = 0.0;
-          int k = 0;
-          for (; k + 4 <= len; k += 4) {
-            const int i0 = __ldg(ip + 32 * k), i1 = __ldg(ip + 32 * (k + 1));
-            const int i2 = __ldg(ip + 32 * (k + 2)), i3 = __ldg(ip + 32 * (k + 3));
-            const double a0 = __ldg(vp + 32 * k), a1 = __ldg(vp + 32 * (k + 1));
-            const double a2 = __ldg(vp + 32 * (k + 2)), a3 = __ldg(vp + 32 * (k + 3));
-            const double z0 = zs[i0], z1 = zs[i1], z2 = zs[i2], z3 = zs[i3];
-            acc += a0 * z0;
-            acc += a1 * z1;
-            acc += a2 * z2;
-            acc += a3 * z3;
-          }
-          for (; k < len; ++k) acc += __ldg(vp + 32 * k) * zs[__ldg(ip + 32 * k)];
-          if (ok) {
-            const double uo = P.u[r];
-            const double uh = rb > 0.0 ? uo / rb : uo;
-            const double t = acc - alpha * uh;
-            P.u[r] = t;
-            sq += t * t;
-          }
-        }
-      } else {
-        // thread per row (rows are short): 4-wide unrolling keeps gathers in flight
-        for (long long r = gtid; r < P.mloc; r += gsize) {
-          const int b = __ldg(P.aptr + r), e = __ldg(P.aptr + r + 1);
-          double acc = 0.0;
-          int q = b;
-          for (; q + 4 <= e; q += 4) {
-            const int i0 = __ldg(P.aidx + q), i1 = __ldg(P.aidx + q + 1);
-            const int i2 = __ldg(P.aidx + q + 2), i3 = __ldg(P.aidx + q + 3);
-            const double a0 = __ldg(P.aval + q), a1 = __ldg(P.aval + q + 1);
-            const double a2 = __ldg(P.aval + q + 2), a3 = __ldg(P.aval + q + 3);
-            const double z0 = zs[i0], z1 = zs[i1], z2 = zs[i2], z3 = zs[i3];
-            acc += a0 * z0;
-            acc += a1 * z1;
-            acc += a2 * z2;
-            acc += a3 * z3;
-          }
-          for (; q < e; ++q) acc += __ldg(P.aval + q) * zs[__ldg(P.aidx + q)];
-          const double uo = P.u[r];
-          const double uh = rb > 0.0 ? uo / rb : uo;
-          const double t = acc - alpha * uh;
-          P.u[r] = t;
-          sq += t * t;
-        }
-      }
-      if (P.has_tail) {
-        double* ut = P.u + P.mloc;
-        for (long long c = gtid; c < P.n; c += gsize) {
-          const double uo = ut[c];
-          const double uh = rb > 0.0 ? uo / rb : uo;
-          const double t = P.mu * zs[c] - alpha * uh;
-          ut[c] = t;
-          sqt += t * t;
-        }
-      }
-      sq = block_sum<kPT>(sq, red);
-      sqt = block_sum<kPT>(sqt, red);
-      if (threadIdx.x == 0) {
-        P.part[blockIdx.x * 4 + 0] = sq;
-        P.part[blockIdx.x * 4 + 1] = sqt;
-      }
-    }
-    grid.sync();  // B2
-    STAMP(3);
-    // ---- S4: beta ; h = (A^T u + mu u_t) / beta  [plain: v_raw = h - beta v, ||v_raw||^2]
-    const double bnew = sqrt(grid_sum(P.part, 0, nb, red) + grid_sum(P.part, 1, nb, red));
+    STAMP(9);
+    // ---- S4: h = (A^T u + mu u_t) / beta  [plain: v_raw = h - beta v, ||v_raw||^2]
     {
       double sq = 0.0;
-      for (long long c = gwarp; c < P.n; c += nwarps) {
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        const int e = __ldg(P.tptr + c + 1);
-        int q = __ldg(P.tptr + c) + lane;
-        for (; q + 96 < e; q += 128) {
-          const int i0 = __ldg(P.tidx + q), i1 = __ldg(P.tidx + q + 32);
-          const int i2 = __ldg(P.tidx + q + 64), i3 = __ldg(P.tidx + q + 96);
-          const double v0 = __ldg(P.tval + q), v1 = __ldg(P.tval + q + 32);
-          const double v2 = __ldg(P.tval + q + 64), v3 = __ldg(P.tval + q + 96);
-          a0 += v0 * P.u[i0];
-          a1 += v1 * P.u[i1];
-          a2 += v2 * P.u[i2];
-          a3 += v3 * P.u[i3];
+      auto finish = [&](long long c, double acc) {
+        if (P.has_tail) acc += P.mu * P.u[P.mloc + c];
+        const double gj = bnew > 0.0 ? acc / bnew : acc;
+        if (P.pre) {
+          P.h[c] = gj;
+        } else {
+          const double t = gj - bnew * P.v[c];
+          P.vr[c] = t;
+          sq += t * t;
         }
-        for (; q < e; q += 32) a0 += __ldg(P.tval + q) * P.u[__ldg(P.tidx + q)];
-        double acc = warp_sum((a0 + a1) + (a2 + a3));
-        if (lane == 0) {
-          if (P.has_tail) acc += P.mu * P.u[P.mloc + c];
-          const double gj = bnew > 0.0 ? acc / bnew : acc;
-          if (P.pre) {
-            P.h[c] = gj;
-          } else {
-            const double t = gj - bnew * P.v[c];
-            P.vr[c] = t;
-            sq += t * t;
+      };
+      // two rows of A^T per warp pass, 4 predicated entries per lane and row:
+      // up to 8 independent gathers in flight per lane
+      for (long long c = gwarp; c < P.n; c += 2 * nwarps) {
+        const long long c2 = c + nwarps;
+        const bool has2 = c2 < P.n;
+        const int b1 = __ldg(P.tptr + c), n1 = __ldg(P.tptr + c + 1) - b1;
+        const int b2 = has2 ? __ldg(P.tptr + c2) : 0, n2 = has2 ? __ldg(P.tptr + c2 + 1) - b2 : 0;
+        const int nmax = max(n1, n2);
+        double acc1 = 0.0, acc2 = 0.0;
+        for (int k0 = lane; k0 < nmax; k0 += 128) {
+          int i1[4], i2[4];
+          double v1[4], v2[4], g1[4], g2[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int q = k0 + 32 * u;
+            i1[u] = q < n1 ? __ldg(P.tidx + b1 + q) : 0;
+            v1[u] = q < n1 ? __ldg(P.tval + b1 + q) : 0.0;
+            i2[u] = q < n2 ? __ldg(P.tidx + b2 + q) : 0;
+            v2[u] = q < n2 ? __ldg(P.tval + b2 + q) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int q = k0 + 32 * u;
+            g1[u] = q < n1 ? P.u[i1[u]] : 0.0;
+            g2[u] = q < n2 ? P.u[i2[u]] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int q = k0 + 32 * u;
+            if (q < n1) acc1 += v1[u] * g1[u];
+            if (q < n2) acc2 += v2[u] * g2[u];
           }
         }
+        acc1 = warp_sum(acc1);
+        acc2 = warp_sum(acc2);
+        if (lane == 0) {
+          finish(c, acc1);
+          if (has2) finish(c2, acc2);
+        }
       }
-      if (!P.pre) {
-        sq = block_sum<kPT>(sq, red);
-        if (threadIdx.x == 0) P.part[blockIdx.x * 4 + 2] = sq;
-      }
+      if (!P.pre) cta_partial<PT>(sq, 0.0, red, P.part, 2, -1);
     }
+    STAMP(10);
     grid.sync();  // B3
-    STAMP(4);
+    STAMP(11);
     if (P.pre) {
       // ---- S56: v_raw = h + R^T Ga R h - beta v ; ||v_raw||^2
       double sq = 0.0;
       if (P.fused) {
-        cta_project(P, P.h, 1.0, P.Ga, tsh, dsh, c0, c1, warp, lane);
+        if (regs) cta_project_reg<PT, false>(P, R, P.h, 1.0, tsh, dsh, psh, lane);
+        else cta_project<PT>(P, P.h, 1.0, P.Ga, tsh, dsh, psh, c0, c1, warp, lane);
+        STAMP(12);
         const int qb0 = __ldg(P.rtptr + c0);
-        for (long long c = c0 + threadIdx.x; c < c1; c += kPT) {
+        for (long long c = c0 + threadIdx.x; c < c1; c += PT) {
           double acc = 0.0;
           for (int q = __ldg(P.rtptr + c); q < __ldg(P.rtptr + c + 1); ++q) acc += dsh[q - qb0];
           const double t = (P.h[c] + acc) - bnew * P.v[c];
@@ -376,7 +620,7 @@ __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
       } else {
         grid_project(grid, P.rptr, P.ridx, P.rval, P.Ga, P.l, P.h, 1.0, P.t, P.s, gwarp, nwarps, lane);
         grid.sync();
-        for (long long c = c0 + threadIdx.x; c < c1; c += kPT) {
+        for (long long c = c0 + threadIdx.x; c < c1; c += PT) {
           double acc = 0.0;
           for (int q = P.rtptr[c]; q < P.rtptr[c + 1]; ++q) acc += P.rtval[q] * P.s[P.rtidx[q]];
           const double t = (P.h[c] + acc) - bnew * P.v[c];
@@ -384,13 +628,23 @@ __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
           sq += t * t;
         }
       }
-      sq = block_sum<kPT>(sq, red);
-      if (threadIdx.x == 0) P.part[blockIdx.x * 4 + 2] = sq;
+      cta_partial<PT>(sq, 0.0, red, P.part, 2, -1);
+      STAMP(13);
       grid.sync();  // B4
     }
-    STAMP(5);
+    STAMP(14);
     // ---- S7: alpha ; rotation (lsqr.hpp:145-171) ; owner-column updates ; ||y||^2
-    const double anew = sqrt(grid_sum(P.part, 2, nb, red));
+    // (the owner's first column is fetched before the alpha reduction)
+    const long long cf = c0 + threadIdx.x;
+    double vo = 0.0, wo = 0.0, yo = 0.0;
+    if (cf < c1) {
+      vo = P.vr[cf];
+      wo = P.w[cf];
+      yo = P.y[cf];
+    }
+    double sa[1];
+    grid_sums<1>(P.part, {2}, nb, gsh + 3, sa);
+    const double anew = sqrt(sa[0]);
     beta = bnew;
     alpha = anew;
     opnorm2 += alpha * alpha + beta * beta;
@@ -412,20 +666,23 @@ __global__ void __launch_bounds__(kPT, 1) lsqr_persistent_kernel(PArgs P) {
     vsrc = P.vr;
     {
       double sq = 0.0;
-      for (long long c = c0 + threadIdx.x; c < c1; c += kPT) {
-        const double vh = P.vr[c] / vdiv;
+      for (long long c = cf; c < c1; c += PT) {
+        if (c != cf) {
+          vo = P.vr[c];
+          wo = P.w[c];
+          yo = P.y[c];
+        }
+        const double vh = vo / vdiv;
         P.v[c] = vh;
-        const double wo = P.w[c];
-        const double yn = P.y[c] + t1 * wo;
+        const double yn = yo + t1 * wo;
         P.y[c] = yn;
         P.w[c] = vh + t2 * wo;
         sq += yn * yn;
       }
-      sq = block_sum<kPT>(sq, red);
-      if (threadIdx.x == 0) P.part[blockIdx.x * 4 + 3] = sq;
+      cta_partial<PT>(sq, 0.0, red, P.part, 3, -1);
     }
     pending = true;
-    if (P.prof && blockIdx.x == 0 && threadIdx.x == 0 && j - 1 < 64) P.prof[(j - 1) * 8 + 6] = globaltimer_ns();
+    if (P.prof && blockIdx.x == 0 && threadIdx.x == 0 && j - 1 < 64) P.prof[(j - 1) * 16 + 15] = globaltimer_ns();
   }
 }
 
@@ -523,8 +780,12 @@ void lsqr_persistent_run(apc_mat& a, double mu, const PrecondDev* p, const Persi
     P.sval = a.sell.val.p;
     P.nchunks = a.sell.chunks;
   }
+  const char* pte = std::getenv("APC_PERSISTENT_PT");
+  const int pt = (pte && std::atoi(pte) == 1024) ? 1024 : 512;
+  void* kfn = pt == 512 ? reinterpret_cast<void*>(lsqr_persistent_kernel<512, false>)
+                        : reinterpret_cast<void*>(lsqr_persistent_kernel<1024, false>);
   int per_sm = 0;
-  APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lsqr_persistent_kernel, kPT, 0));
+  APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, pt, 0));
   const int blocks_per_sm = std::max(1, std::min(per_sm, b.blocks_per_sm > 0 ? b.blocks_per_sm : 3));
   const int grid = ctx->num_sms * blocks_per_sm;
   P.cchunk = std::max<long long>(1, (a.n + grid - 1) / grid);
@@ -549,9 +810,11 @@ void lsqr_persistent_run(apc_mat& a, double mu, const PrecondDev* p, const Persi
       long long qmax = 0;
       for (long long c0 = 0; c0 < a.n; c0 += P.cchunk)
         qmax = std::max<long long>(qmax, hp[std::min<long long>(a.n, c0 + P.cchunk)] - hp[c0]);
-      if ((P.l + qmax) * 8 <= kSmemBudget) {
+      if ((P.l + qmax + p->R.nnz) * 8 <= kSmemBudget) {
         P.fused = 1;
-        smem_doubles = std::max(smem_doubles, P.l + qmax);
+        P.rnnz = static_cast<int>(p->R.nnz);
+        P.qmax = qmax;
+        smem_doubles = std::max(smem_doubles, P.l + qmax + p->R.nnz);
       }
     }
   }
@@ -572,17 +835,22 @@ void lsqr_persistent_run(apc_mat& a, double mu, const PrecondDev* p, const Persi
   P.prof = b.prof;
   P.st = b.st;
   P.trace = b.trace;
-  void* kfn = reinterpret_cast<void*>(lsqr_persistent_kernel);
+  const char* re = std::getenv("APC_PERSISTENT_REGS");
+  P.regs = ((re ? std::atoi(re) != 0 : false) && P.fused && P.rnnz <= 4 * pt && P.l <= pt && P.l <= 256) ? 1 : 0;
+  if (P.regs)
+    kfn = pt == 512 ? reinterpret_cast<void*>(lsqr_persistent_kernel<512, true>)
+                    : reinterpret_cast<void*>(lsqr_persistent_kernel<1024, true>);
   const size_t smem = sizeof(double) * static_cast<size_t>(smem_doubles);
   APC_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kPT, smem));
+  APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, pt, smem));
   require(per_sm >= blocks_per_sm, APC_CUDA_ERROR, "persistent LSQR: grid does not fit co-resident");
   P.part = b.part;
+  require(grid <= kPartStride, APC_CUDA_ERROR, "persistent LSQR: grid larger than the partial stride");
   void* args[] = {&P};
-  APC_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kPT), args, smem, ctx->stream));
+  APC_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(pt), args, smem, ctx->stream));
   ctx->launches++;
 }
 
-int persistent_max_grid(apc_ctx* ctx) { return ctx->num_sms * 8; }
+int persistent_max_grid(apc_ctx* ctx) { return std::max(ctx->num_sms * 8, kPartStride); }
 
 }  // namespace apc
