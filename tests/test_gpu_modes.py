@@ -53,3 +53,65 @@ def test_row_shard_operator_products(apc, ref, ctx, problem):
     full_u[r0:r1] = u
     np.testing.assert_allclose(S.apply(u, transpose=True), A.apply(full_u, transpose=True), rtol=1e-11,
                                atol=1e-13)
+
+
+# Persistent-kernel code paths (lsqr_persistent.cu), each against the CUDA-graph
+# path on the same system: per-CTA vs grid-wide preconditioner projection,
+# shared-memory z by TMA bulk copy vs by plain loads vs gathers from L2, odd n
+# (no 16-byte bulk copy), SELL-32 vs CSR forward walk, 512 vs 1024 threads.
+PERSISTENT_VARIANTS = [
+    {},
+    {"APC_PERSISTENT_FUSED": "0"},
+    {"APC_PERSISTENT_ZSMEM": "0"},
+    {"APC_PERSISTENT_SELL": "0"},
+    {"APC_PERSISTENT_PT": "1024"},
+    {"APC_PERSISTENT_REGS": "1"},
+    {"APC_PERSISTENT_FUSED": "0", "APC_PERSISTENT_ZSMEM": "0", "APC_PERSISTENT_SELL": "0"},
+]
+
+
+@pytest.mark.parametrize("n", [400, 401])
+@pytest.mark.parametrize("env", PERSISTENT_VARIANTS, ids=lambda e: ",".join(f"{k[15:]}={v}" for k, v in e.items()) or "default")
+def test_persistent_variants_agree_with_graph(apc, ctx, env, n):
+    p = apc.Problem(2, 4000, n)
+    A = apc.DeviceMatrix.from_problem(ctx, p)
+    os.environ["APC_LSQR_MODE"] = "while"
+    try:
+        base = apc.aplicur_solve(A, p.b, apc.SolverConfig(**KNOBS))
+    finally:
+        del os.environ["APC_LSQR_MODE"]
+    for k, v in env.items():
+        os.environ[k] = v
+    try:
+        other = apc.aplicur_solve(A, p.b, apc.SolverConfig(**KNOBS))
+        rerun = apc.aplicur_solve(A, p.b, apc.SolverConfig(**KNOBS))
+    finally:
+        for k in env:
+            del os.environ[k]
+    assert np.array_equal(base.row_indices, other.row_indices)
+    assert abs(base.lsqr_iters - other.lsqr_iters) <= max(3, 0.05 * base.lsqr_iters)
+    assert abs(base.final_relres - other.final_relres) <= 1e-3 * base.final_relres
+    # the persistent kernel is deterministic: a rerun is bit-identical
+    assert np.array_equal(other.x, rerun.x)
+    assert other.lsqr_iters == rerun.lsqr_iters
+
+
+@pytest.mark.parametrize("mu", [0.0, 1e-2])
+def test_persistent_plain_lsqr_matches_graph(apc, ctx, mu):
+    # unpreconditioned phases (S12/S56 skipped, S4 writes v_raw directly) on a
+    # well-conditioned sparse system, where the two paths agree to rounding
+    rng = np.random.default_rng(11)
+    m, n, k = 3000, 301, 8
+    rows = np.concatenate([np.sort(rng.choice(m, k, replace=False)) for _ in range(n)])
+    colptr = np.arange(0, (n + 1) * k, k)
+    A = apc.DeviceMatrix.csc(ctx, m, n, colptr, rows, rng.standard_normal(n * k))
+    b = rng.standard_normal(m)
+    cfg = apc.SolverConfig(mu=mu, eps_lsqr=1e-12, lsqr_cap=400)
+    os.environ["APC_LSQR_MODE"] = "while"
+    try:
+        g = apc.plain_lsqr_solve(A, b, cfg)
+    finally:
+        del os.environ["APC_LSQR_MODE"]
+    q = apc.plain_lsqr_solve(A, b, cfg)
+    assert q.lsqr_iters == g.lsqr_iters
+    np.testing.assert_allclose(q.x, g.x, rtol=1e-9, atol=1e-12 * np.abs(g.x).max())
