@@ -118,7 +118,9 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # APC_LIB_PATH: an alternative build of the same library (kernel-variant
+    # experiments, scripts/build_variant.py); the default is the in-tree build
+    p = Path(path) if path else Path(os.environ.get("APC_LIB_PATH", LIB_PATH))
     if not p.exists():
         raise ApcError(20, f"CUDA library missing: {p} (run __graft_entry__.build())")
     lib = C.CDLL(str(p), mode=C.RTLD_GLOBAL)
