@@ -55,7 +55,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -232,13 +232,18 @@ def main():
     d2h = 8 * p.n
     barrier()
     t0 = time.perf_counter()
+    e2e_parts = []
     for _ in range(args.steps):
+        ta = time.perf_counter()
         F2 = apc.DeviceMatrix.from_problem(ctx, p) if ws > 1 else None
         A2 = apc.DeviceMatrix.from_problem(ctx, p, r0, r1) if ws > 1 else apc.DeviceMatrix.from_problem(ctx, p)
+        tb = time.perf_counter()
         r2 = solve_once(A2, F2)
+        tc = time.perf_counter()
         A2.free()
         if F2 is not None:
             F2.free()
+        e2e_parts.append((tb - ta, tc - tb, time.perf_counter() - tc, r2.setup_ms / 1e3, r2.lsqr_ms / 1e3))
     barrier()
     e2e_s = (time.perf_counter() - t0) / args.steps
     if dist is not None:
@@ -306,7 +311,12 @@ def main():
         "lsqr_iters": iters, "lsqr_iter_per_s": iters / (lsqr_ms / 1e3) if lsqr_ms > 0 else None,
         "final_relres": r.final_relres, "rank": int(len(r.row_indices)), "phases": len(r.phases),
         "setup_ms": float(np.mean([x.setup_ms for x in results])), "lsqr_ms": lsqr_ms,
-        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "upload_s": float(np.mean([x[0] for x in e2e_parts])),
+                "solve_wall_s": float(np.mean([x[1] for x in e2e_parts])),
+                "free_s": float(np.mean([x[2] for x in e2e_parts])),
+                "solve_setup_s": float(np.mean([x[3] for x in e2e_parts])),
+                "solve_lsqr_s": float(np.mean([x[4] for x in e2e_parts]))},
         "gpu_launches": int(launches),
         "roofline": roofline,
         "clocks": clk.summary(),

@@ -132,7 +132,27 @@ struct apc_ctx {
   apc::DBuf<unsigned int> counters;  // last-block counters (zeroed)
   // kernel launch counter (launches issued by this library on this ctx)
   std::uint64_t launches = 0;
+  // grow-only pinned host staging buffers (cudaMallocHost takes driver locks
+  // and costs milliseconds; uploads and solves reuse these): 0/1 CSC upload
+  // index/value staging, 2 LSQR state readback
+  struct Pinned {
+    void* p = nullptr;
+    size_t n = 0;
+  } pinned[4];
 };
+
+// pinned host buffer `slot` of at least `bytes` (contents not preserved on growth)
+inline void* ctx_pinned(apc_ctx* c, int slot, size_t bytes) {
+  apc_ctx::Pinned& b = c->pinned[slot];
+  if (b.n < bytes) {
+    if (b.p) cudaFreeHost(b.p);
+    b.p = nullptr;
+    b.n = 0;
+    APC_CUDA(cudaMallocHost(&b.p, bytes));
+    b.n = bytes;
+  }
+  return b.p;
+}
 
 // Matrix handle: dense column-major (ld = local rows) or sparse stored twice
 // as CSR(A) (for A*x) and CSR(A^T) (for A^T*x; the same arrays as the

@@ -175,6 +175,8 @@ int apc_ctx_destroy(apc_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     comm_destroy(ctx);
     blas_destroy(ctx);
+    for (auto& b : ctx->pinned)
+      if (b.p) cudaFreeHost(b.p);
     ctx->scratch_d.release();
     ctx->counters.release();
     cudaStreamDestroy(ctx->stream);

@@ -449,7 +449,7 @@ LsqrWork* lsqr_work_create(apc_mat& a, double mu) {
   w->ctr.alloc(8);
   APC_CUDA(cudaMemsetAsync(w->ctr.p, 0, w->ctr.bytes(), a.ctx->stream));
   w->st.alloc(1);
-  APC_CUDA(cudaMallocHost(&w->hst, sizeof(LsqrState) * 2));
+  w->hst = static_cast<LsqrState*>(ctx_pinned(a.ctx, 2, sizeof(LsqrState) * 2));
   APC_CUDA(cudaEventCreateWithFlags(&w->ev[0], cudaEventDisableTiming));
   APC_CUDA(cudaEventCreateWithFlags(&w->ev[1], cudaEventDisableTiming));
   APC_CUDA(cudaEventCreate(&w->tev[0]));
@@ -466,7 +466,6 @@ LsqrWork* lsqr_work_create(apc_mat& a, double mu) {
 
 void lsqr_work_destroy(LsqrWork* w) {
   if (!w) return;
-  if (w->hst) cudaFreeHost(w->hst);
   for (auto& e : w->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : w->tev)

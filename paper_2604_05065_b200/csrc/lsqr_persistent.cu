@@ -28,6 +28,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "dev_common.cuh"
@@ -744,6 +747,26 @@ void build_sell(apc_mat& a) {
   APC_CUDA(cudaStreamSynchronize(st));
 }
 
+// occupancy of a kernel variant at a dynamic shared-memory size, with the
+// opt-in attribute set; cached (the driver calls take locks that a concurrent
+// NVML poller also takes, and would otherwise run at every LSQR phase)
+int occupancy(void* kfn, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, void*, int, size_t>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  int dev = 0;
+  APC_CUDA(cudaGetDevice(&dev));
+  const auto key = std::make_tuple(dev, kfn, threads, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (smem > 48 * 1024)
+    APC_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, threads, smem));
+  cache[key] = per_sm;
+  return per_sm;
+}
+
 }  // namespace
 
 bool persistent_eligible(const apc_mat& a, const PrecondDev* p, const apc_ctx* ctx) {
@@ -785,7 +808,7 @@ void lsqr_persistent_run(apc_mat& a, double mu, const PrecondDev* p, const Persi
   void* kfn = pt == 512 ? reinterpret_cast<void*>(lsqr_persistent_kernel<512, false>)
                         : reinterpret_cast<void*>(lsqr_persistent_kernel<1024, false>);
   int per_sm = 0;
-  APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, pt, 0));
+  per_sm = occupancy(kfn, pt, 0);
   const int blocks_per_sm = std::max(1, std::min(per_sm, b.blocks_per_sm > 0 ? b.blocks_per_sm : 3));
   const int grid = ctx->num_sms * blocks_per_sm;
   P.cchunk = std::max<long long>(1, (a.n + grid - 1) / grid);
@@ -841,8 +864,7 @@ void lsqr_persistent_run(apc_mat& a, double mu, const PrecondDev* p, const Persi
     kfn = pt == 512 ? reinterpret_cast<void*>(lsqr_persistent_kernel<512, true>)
                     : reinterpret_cast<void*>(lsqr_persistent_kernel<1024, true>);
   const size_t smem = sizeof(double) * static_cast<size_t>(smem_doubles);
-  APC_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, pt, smem));
+  per_sm = occupancy(kfn, pt, smem);
   require(per_sm >= blocks_per_sm, APC_CUDA_ERROR, "persistent LSQR: grid does not fit co-resident");
   P.part = b.part;
   require(grid <= kPartStride, APC_CUDA_ERROR, "persistent LSQR: grid larger than the partial stride");

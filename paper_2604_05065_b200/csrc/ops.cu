@@ -361,8 +361,8 @@ void upload_csc(apc_mat& a, const long long* colptr, const long long* rowidx, co
   const long long nnz = cnt;
   int* hidx = nullptr;
   double* hval = nullptr;
-  APC_CUDA(cudaMallocHost(&hidx, sizeof(int) * std::max<long long>(1, nnz)));
-  APC_CUDA(cudaMallocHost(&hval, sizeof(double) * std::max<long long>(1, nnz)));
+  hidx = static_cast<int*>(ctx_pinned(ctx, 0, sizeof(int) * std::max<long long>(1, nnz)));
+  hval = static_cast<double*>(ctx_pinned(ctx, 1, sizeof(double) * std::max<long long>(1, nnz)));
   std::vector<long long> tlen(n);
   {
     long long q = 0;
@@ -390,9 +390,7 @@ void upload_csc(apc_mat& a, const long long* colptr, const long long* rowidx, co
     APC_CUDA(cudaMemcpyAsync(t.idx.p, hidx, sizeof(int) * nnz, cudaMemcpyHostToDevice, st));
     APC_CUDA(cudaMemcpyAsync(t.val.p, hval, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
   }
-  build_units(ctx, t, tlen);  // synchronizes the stream
-  cudaFreeHost(hidx);
-  cudaFreeHost(hval);
+  build_units(ctx, t, tlen);  // synchronizes the stream (the staging buffers are free again)
 
   // CSR(A): sort entries by row (stable), keeping column order within rows
   Csr& c = a.a;
