@@ -94,6 +94,24 @@ struct PArgs {
   TraceRow* trace;
 };
 
+// Cache policy of the A^T u loads (A/B knobs): u gathers are random with no
+// L1 reuse; the CSR(A^T) streams are read once per iteration.
+#ifndef APC_GATHER_CG
+#define APC_GATHER_CG 1
+#endif
+#ifndef APC_STREAM_CS
+#define APC_STREAM_CS 0
+#endif
+__device__ __forceinline__ double ld_gather(const double* p) {
+  if constexpr (APC_GATHER_CG) return __ldcg(p);
+  else return *p;
+}
+template <class T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+  if constexpr (APC_STREAM_CS) return __ldcs(p);
+  else return __ldg(p);
+}
+
 // sum_{k < len} val[s k] * (x[idx[s k]] / xdiv), added strictly in k order; U
 // entries per block are loaded under predicates so one block costs one memory
 // round trip (a plain loop would pay one per entry)
@@ -575,16 +593,16 @@ __global__ void __launch_bounds__(PT, 1) lsqr_persistent_kernel(PArgs P) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int q = k0 + 32 * u;
-            i1[u] = q < n1 ? __ldg(P.tidx + b1 + q) : 0;
-            v1[u] = q < n1 ? __ldg(P.tval + b1 + q) : 0.0;
-            i2[u] = q < n2 ? __ldg(P.tidx + b2 + q) : 0;
-            v2[u] = q < n2 ? __ldg(P.tval + b2 + q) : 0.0;
+            i1[u] = q < n1 ? ld_stream(P.tidx + b1 + q) : 0;
+            v1[u] = q < n1 ? ld_stream(P.tval + b1 + q) : 0.0;
+            i2[u] = q < n2 ? ld_stream(P.tidx + b2 + q) : 0;
+            v2[u] = q < n2 ? ld_stream(P.tval + b2 + q) : 0.0;
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int q = k0 + 32 * u;
-            g1[u] = q < n1 ? P.u[i1[u]] : 0.0;
-            g2[u] = q < n2 ? P.u[i2[u]] : 0.0;
+            g1[u] = q < n1 ? ld_gather(P.u + i1[u]) : 0.0;
+            g2[u] = q < n2 ? ld_gather(P.u + i2[u]) : 0.0;
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
