@@ -98,6 +98,8 @@ struct Csr {
   i64 n_units = 0, n_parts = 0, max_row_nnz = 0;
   DBuf<i32> urow, ustart, uend, uslot;  // per unit (uslot < 0: whole row)
   DBuf<i32> rfirst, rcount;             // per row: first partial slot (-1: not split), count
+  i64 n_split = 0;
+  DBuf<i32> srows;                      // the split rows (summed into the output by op_adj_raw)
   DBuf<double> upart;                   // n_parts partial sums
   double avg_row_nnz = 0.0;
 };

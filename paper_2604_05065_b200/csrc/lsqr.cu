@@ -55,10 +55,6 @@ struct LsqrPtrs {
   long long mloc, n;
   double mu;
   int has_tail;
-  // transpose-unit fix-up (sparse A)
-  const double* upart;
-  const int* rfirst;
-  const int* rcount;
 };
 
 // ---------------------------------------------------------------------------
@@ -162,8 +158,8 @@ struct LsqrFwdEpi {  // u <- (A z) - alpha * u/beta ; ||u_top||^2 -> g[n]
     alpha = st->alpha;
     beta = st->beta;
   }
-  __device__ double row(long long r, double av) {
-    const double uo = u[r];
+  __device__ double load(long long r) { return u[r]; }
+  __device__ double row(long long r, double av, double uo) {
     const double uh = beta > 0.0 ? uo / beta : uo;
     const double t = av - alpha * uh;
     u[r] = t;
@@ -246,7 +242,7 @@ __global__ void __launch_bounds__(kVecThreads) lsqr_epi_kernel(LsqrPtrs P, int p
   long long j = static_cast<long long>(blockIdx.x) * kVecThreads + threadIdx.x;
   double sq = 0.0;
   if (j < P.n) {
-    double raw = P.upart ? unit_row_value(P.g, P.upart, P.rfirst, P.rcount, j) : P.g[j];
+    double raw = P.g[j];  // split rows of A^T were summed by op_adj_raw
     if (P.has_tail) raw += P.mu * P.u[P.mloc + j];
     const double gj = beta > 0.0 ? raw / beta : raw;
     if (precond) {
@@ -620,11 +616,6 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   P.n = n;
   P.mu = mu;
   P.has_tail = mu > 0.0 ? 1 : 0;
-  if (a.sparse) {
-    P.upart = a.at.upart.p;
-    P.rfirst = a.at.rfirst.p;
-    P.rcount = a.at.rcount.p;
-  }
 
   auto t_start = std::chrono::steady_clock::now();
   // ---- initialisation: u = rhs, beta, v = P^{-T} A^T u / beta, alpha, w = v

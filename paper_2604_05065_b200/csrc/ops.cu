@@ -4,6 +4,9 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "ops.cuh"
 
@@ -107,12 +110,10 @@ csr_units_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
 
 namespace {
 
-__global__ void unit_fixup_kernel(const double* out_raw, const double* upart, const int* rfirst,
-                                  const int* rcount, long long n, double mu, const double* tail,
-                                  double* y) {
+__global__ void unit_fixup_kernel(const double* out_raw, long long n, double mu, const double* tail, double* y) {
   long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= n) return;
-  double v = unit_row_value(out_raw, upart, rfirst, rcount, j);
+  double v = out_raw[j];
   if (tail) v += mu * tail[j];
   y[j] = v;
 }
@@ -168,7 +169,37 @@ __global__ void row_ptr_kernel(const int* sorted_rows, long long nnz, long long 
 
 inline unsigned nblk(long long n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
+// sum of the partials of every split row (rows longer than one work unit),
+// block per split row, fixed order: written to out[row] so every consumer of
+// op_adj_raw (LSQR epilogue, NCCL allreduce, op_adj) reads plain values
+__global__ void __launch_bounds__(256)
+split_fixup_kernel(const int* __restrict__ srows, const int* __restrict__ rfirst, const int* __restrict__ rcount,
+                   const double* __restrict__ upart, double* __restrict__ out, const int* done) {
+  __shared__ double red[32];
+  if (done && *done) return;
+  const int j = srows[blockIdx.x];
+  const int f = rfirst[j], cnt = rcount[j];
+  double s = 0.0;
+  for (int k = threadIdx.x; k < cnt; k += 256) s += upart[f + k];
+  s = block_sum<256>(s, red);
+  if (threadIdx.x == 0) out[j] = s;
+}
+
 }  // namespace
+
+unsigned fwd_gs_grid(apc_ctx* ctx, const void* kfn) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, unsigned> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_pair(ctx->device, kfn);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int per_sm = 0;
+  APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kCsrFwdThreads, 0));
+  const unsigned g = static_cast<unsigned>(ctx->num_sms * std::max(1, per_sm));
+  cache[key] = g;
+  return g;
+}
 
 // ---------------------------------------------------------------------------
 // plans
@@ -261,6 +292,11 @@ void op_adj_raw(apc_mat& a, const double* u, double* out, const int* done) {
                                                    c.urow.p, c.ustart.p, c.uend.p, c.uslot.p, out,
                                                    c.upart.p, done);
   a.ctx->launches++;
+  if (c.n_split > 0) {
+    split_fixup_kernel<<<static_cast<unsigned>(c.n_split), 256, 0, st>>>(c.srows.p, c.rfirst.p, c.rcount.p, c.upart.p,
+                                                                         out, done);
+    a.ctx->launches++;
+  }
 }
 
 void launch_dense_adj(apc_ctx* ctx, const double* A, long long mloc, long long n, const double* u,
@@ -283,9 +319,7 @@ void op_adj(apc_mat& a, double mu, bool augmented, const double* u, double* y) {
   } else {
     double* raw = ctx_scratch(a.ctx, a.n);
     op_adj_raw(a, u, raw, nullptr);
-    unit_fixup_kernel<<<nblk(a.n, 256), 256, 0, st>>>(raw, a.at.upart.p, a.at.rfirst.p,
-                                                      a.at.rcount.p, a.n, mu,
-                                                      augmented ? u + a.mloc() : nullptr, y);
+    unit_fixup_kernel<<<nblk(a.n, 256), 256, 0, st>>>(raw, a.n, mu, augmented ? u + a.mloc() : nullptr, y);
     a.ctx->launches++;
   }
   APC_CUDA(cudaGetLastError());
@@ -323,6 +357,10 @@ void build_units(apc_ctx* ctx, Csr& c, const std::vector<long long>& row_nnz) {
   }
   c.n_units = static_cast<long long>(urow.size());
   c.n_parts = nparts;
+  std::vector<int> srows;
+  for (long long r = 0; r < c.rows; ++r)
+    if (rfirst[r] >= 0) srows.push_back(static_cast<int>(r));
+  c.n_split = static_cast<long long>(srows.size());
   c.max_row_nnz = maxr;
   c.avg_row_nnz = c.rows > 0 ? static_cast<double>(off) / static_cast<double>(c.rows) : 0.0;
   auto up = [&](DBuf<int>& d, const std::vector<int>& h) {
@@ -336,6 +374,7 @@ void build_units(apc_ctx* ctx, Csr& c, const std::vector<long long>& row_nnz) {
   up(c.uslot, uslot);
   up(c.rfirst, rfirst);
   up(c.rcount, rcount);
+  up(c.srows, srows);
   c.upart.alloc(std::max<long long>(1, nparts));
   APC_CUDA(cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
 }

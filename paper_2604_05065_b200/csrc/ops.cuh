@@ -14,6 +14,8 @@
 // allreduce, which is where partial A_p^T u_p from row shards meet.
 #pragma once
 
+#include <algorithm>
+
 #include "apc_internal.hpp"
 #include "dev_common.cuh"
 #include "ops_host.hpp"
@@ -33,13 +35,15 @@ constexpr int kCsrUnitMax = 2048;  // max nnz per work unit of the transpose SpM
 // ---------------------------------------------------------------------------
 // forward epilogue interface:
 //   __device__ void begin();                       // load scalars
-//   __device__ double row(i64 r, double v);        // consume (A x)_r, return ||.||^2 term
+//   __device__ double load(i64 r);                 // epilogue input of row r (issued early)
+//   __device__ double row(i64 r, double v, double pre); // consume (A x)_r, return ||.||^2 term
 //   __device__ void tile_done(unsigned tile, unsigned ntiles, double sum_sq);
 // ---------------------------------------------------------------------------
 struct FwdStore {  // y = A x
   double* y;
   __device__ void begin() {}
-  __device__ double row(long long r, double v) { y[r] = v; return 0.0; }
+  __device__ double load(long long) { return 0.0; }
+  __device__ double row(long long r, double v, double) { y[r] = v; return 0.0; }
   __device__ void tile_done(unsigned, unsigned, double) {}
 };
 
@@ -63,6 +67,8 @@ dense_fwd_kernel(const double* __restrict__ A, long long ld, long long mloc, lon
   const long long c1 = c0 + cols_per_split < n ? c0 + cols_per_split : n;
   double acc0 = 0.0, acc1 = 0.0;
   const bool ok0 = r0 < mloc, ok1 = r1 < mloc;
+  // epilogue inputs fetched up front (the split that finishes last uses them)
+  const double pre0 = ok0 ? epi.load(r0) : 0.0, pre1 = ok1 ? epi.load(r1) : 0.0;
   const double* a0 = A + r0;
   const double* a1 = A + r1;
   long long c = c0;
@@ -99,8 +105,8 @@ dense_fwd_kernel(const double* __restrict__ A, long long ld, long long mloc, lon
   }
   epi.begin();
   double sq = 0.0;
-  if (ok0) sq += epi.row(r0, acc0);
-  if (ok1) sq += epi.row(r1, acc1);
+  if (ok0) sq += epi.row(r0, acc0, pre0);
+  if (ok1) sq += epi.row(r1, acc1, pre1);
   sq = block_sum<kDenseFwdThreads>(sq, red);
   epi.tile_done(static_cast<unsigned>(tile), gridDim.x, sq);
 }
@@ -116,34 +122,34 @@ dense_adj_kernel(const double* __restrict__ A, long long ld, long long mloc, lon
                  double* __restrict__ out, const int* done);
 
 // ---------------------------------------------------------------------------
-// CSR A x: G lanes per row, fixed rows per block (deterministic tile slots).
+// CSR A x: G lanes per row, fixed rows per tile (deterministic tile slots).
 // ---------------------------------------------------------------------------
-template <int G, class Epi, int U = 1>
-__global__ void __launch_bounds__(kCsrFwdThreads)
-csr_fwd_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
-               const double* __restrict__ val, long long rows, const double* __restrict__ x,
-               const int* done, Epi epi) {
-  __shared__ double red[32];
-  if (done && *done) return;
+// one tile of rows; returns this thread's share of the epilogue's ||.||^2
+template <int G, class Epi, int U>
+__device__ __forceinline__ double csr_fwd_tile(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                               const double* __restrict__ val, long long rows,
+                                               const double* __restrict__ x, unsigned tile, Epi& epi) {
   constexpr int kGroups = kCsrFwdThreads / G;
   // U rows in flight per lane group: more memory-level parallelism for the
   // HBM-streaming case; U = 1 keeps small (L2-resident) matrices spread wide
   const int g = threadIdx.x / G, lane = threadIdx.x % G;
-  const long long rbase = static_cast<long long>(blockIdx.x) * kCsrFwdRowsPerBlock;
-  epi.begin();
+  const long long rbase = static_cast<long long>(tile) * kCsrFwdRowsPerBlock;
   double sq = 0.0;
   for (int k = 0; k < kCsrFwdRowsPerBlock; k += kGroups * U) {
     long long r[U];
     int b[U], len[U];
+    double pre[U];  // epilogue inputs, fetched with the row pointers (off the critical path)
     int maxlen = 0;
 #pragma unroll
     for (int uu = 0; uu < U; ++uu) {
       r[uu] = rbase + k + uu * kGroups + g;
       b[uu] = 0;
       len[uu] = 0;
+      pre[uu] = 0.0;
       if (k + uu * kGroups < kCsrFwdRowsPerBlock && r[uu] < rows) {
         b[uu] = __ldg(ptr + r[uu]);
         len[uu] = __ldg(ptr + r[uu] + 1) - b[uu];
+        if (lane == 0) pre[uu] = epi.load(r[uu]);
       }
       maxlen = max(maxlen, len[uu]);
     }
@@ -160,9 +166,40 @@ csr_fwd_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
     for (int uu = 0; uu < U; ++uu) {
 #pragma unroll
       for (int o = G / 2; o > 0; o >>= 1) s[uu] += __shfl_xor_sync(0xffffffffu, s[uu], o, G);
-      if (lane == 0 && k + uu * kGroups < kCsrFwdRowsPerBlock && r[uu] < rows) sq += epi.row(r[uu], s[uu]);
+      if (lane == 0 && k + uu * kGroups < kCsrFwdRowsPerBlock && r[uu] < rows) sq += epi.row(r[uu], s[uu], pre[uu]);
     }
   }
+  return sq;
+}
+
+template <int G, class Epi, int U = 1>
+__global__ void __launch_bounds__(kCsrFwdThreads)
+csr_fwd_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
+               const double* __restrict__ val, long long rows, const double* __restrict__ x,
+               const int* done, Epi epi) {
+  __shared__ double red[32];
+  if (done && *done) return;
+  epi.begin();
+  double sq = csr_fwd_tile<G, Epi, U>(ptr, idx, val, rows, x, blockIdx.x, epi);
+  sq = block_sum<kCsrFwdThreads>(sq, red);
+  epi.tile_done(blockIdx.x, gridDim.x, sq);
+}
+
+// Large CSR: exactly the co-resident CTAs walk the tiles grid-stride and the
+// epilogue sees one slot per CTA -- a per-tile epilogue would make ~10^4-10^5
+// CTAs serialise on the last-block counter (C5: +0.39 ms per product).
+#ifndef APC_FWD_GS_MINB
+#define APC_FWD_GS_MINB 4
+#endif
+template <int G, class Epi, int U>
+__global__ void __launch_bounds__(kCsrFwdThreads, APC_FWD_GS_MINB)
+csr_fwd_gs_kernel(const int* __restrict__ ptr, const int* __restrict__ idx, const double* __restrict__ val,
+                  long long rows, const double* __restrict__ x, unsigned ntiles, const int* done, Epi epi) {
+  __shared__ double red[32];
+  if (done && *done) return;
+  epi.begin();
+  double sq = 0.0;
+  for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) sq += csr_fwd_tile<G, Epi, U>(ptr, idx, val, rows, x, t, epi);
   sq = block_sum<kCsrFwdThreads>(sq, red);
   epi.tile_done(blockIdx.x, gridDim.x, sq);
 }
@@ -176,18 +213,6 @@ csr_units_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
                  const int* __restrict__ urow, const int* __restrict__ ustart,
                  const int* __restrict__ uend, const int* __restrict__ uslot,
                  double* __restrict__ out, double* __restrict__ upart, const int* done);
-
-// value of row j of a unit-split SpMV (fix-up of split rows in slot order)
-__device__ __forceinline__ double unit_row_value(const double* out, const double* upart,
-                                                 const int* rfirst, const int* rcount,
-                                                 long long j) {
-  const int f = rfirst[j];
-  if (f < 0) return out[j];
-  const int cnt = rcount[j];
-  double s = 0.0;
-  for (int k = 0; k < cnt; ++k) s += upart[f + k];
-  return s;
-}
 
 // ---------------------------------------------------------------------------
 // host-side launch helpers (ops.cu)
@@ -232,6 +257,9 @@ void launch_dense_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cud
   a.ctx->launches++;
 }
 
+// co-resident CTAs of a grid-stride forward kernel (cached occupancy)
+unsigned fwd_gs_grid(apc_ctx* ctx, const void* kfn);
+
 template <class Epi>
 void launch_csr_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaStream_t st) {
   const long long rows = a.a.rows;
@@ -240,17 +268,21 @@ void launch_csr_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaS
   const bool big = rows >= (1LL << 21);
 #define APC_FWD_CASE(GG)                                                                                      \
   case GG:                                                                                                    \
-    if (big) csr_fwd_kernel<GG, Epi, 4><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi); \
-    else csr_fwd_kernel<GG, Epi, 1><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi);     \
+    if (big) {                                                                                                \
+      const unsigned grid = std::min<unsigned>(nb, fwd_gs_grid(a.ctx, reinterpret_cast<const void*>(         \
+                                                       csr_fwd_gs_kernel<GG, Epi, 4>)));                      \
+      csr_fwd_gs_kernel<GG, Epi, 4><<<grid, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, \
+                                                                     nb, done, epi);                          \
+    } else {                                                                                                  \
+      csr_fwd_kernel<GG, Epi, 1><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, \
+                                                                epi);                                         \
+    }                                                                                                         \
     break;
   switch (csr_group_size(a.a.avg_row_nnz)) {
     APC_FWD_CASE(4)
     APC_FWD_CASE(8)
     APC_FWD_CASE(16)
-    default:
-      if (big) csr_fwd_kernel<32, Epi, 4><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi);
-      else csr_fwd_kernel<32, Epi, 1><<<nb, kCsrFwdThreads, 0, st>>>(a.a.ptr.p, a.a.idx.p, a.a.val.p, rows, x, done, epi);
-      break;
+    APC_FWD_CASE(32)
   }
 #undef APC_FWD_CASE
   a.ctx->launches++;

@@ -3,7 +3,7 @@
 usage: python scripts/build_variant.py NAME -DAPC_S4_ROWS=4 [...]
 writes _variants/libapc_NAME.so (git-ignored, travels with gpurun); select it
 with APC_LIB_PATH=<that path>.  Only sources mentioning a defined macro are
-recompiled."""
+recompiled (every .cu file when a macro appears in a header)."""
 import shutil
 import subprocess
 import sys
@@ -21,7 +21,8 @@ objs = []
 for src in sorted(B.CSRC.glob("*.cu")) + sorted(B.CSRC.glob("*.cpp")):
     obj = B.OBJ_DIR / (src.name + ".o")
     macros = [d[2:].split("=")[0] for d in defs if d.startswith("-D")]
-    if src.suffix == ".cu" and any(mc in src.read_text() for mc in macros):
+    in_header = any(mc in h.read_text() for mc in macros for h in list(B.CSRC.glob("*.cuh")) + list(B.CSRC.glob("*.hpp")))
+    if src.suffix == ".cu" and (in_header or any(mc in src.read_text() for mc in macros)):
         obj = obj_dir / (src.name + ".o")
         B._run([B.NVCC, *B.CU_FLAGS, *defs, f"-I{B.INC}", f"-I{B.CSRC}", "-c", str(src), "-o", str(obj)])
     objs.append(str(obj))
