@@ -115,3 +115,32 @@ def test_persistent_plain_lsqr_matches_graph(apc, ctx, mu):
     q = apc.plain_lsqr_solve(A, b, cfg)
     assert q.lsqr_iters == g.lsqr_iters
     np.testing.assert_allclose(q.x, g.x, rtol=1e-9, atol=1e-12 * np.abs(g.x).max())
+
+
+def test_split_transpose_rows_all_modes(apc, ctx):
+    # C5-shaped (Zipf columns): the heaviest columns exceed one 2048-entry work
+    # unit, so A^T u goes through split rows (partials + op_adj_raw's fix-up);
+    # every LSQR mode must see the same operator
+    p = apc.Problem(5, 60000, 3000)
+    assert np.diff(p.colptr).max() > 2048
+    A = apc.DeviceMatrix.from_problem(ctx, p)
+    knobs = dict(mu=1e-8, eps_lsqr=1e-8, block=25, seed=1, max_rank=50, trace_sample_stride=0, lsqr_cap=300)
+    res = {}
+    for mode in ["while", "batch", "eager"]:
+        os.environ["APC_LSQR_MODE"] = mode
+        try:
+            res[mode] = apc.aplicur_solve(A, p.b, apc.SolverConfig(**knobs))
+        finally:
+            del os.environ["APC_LSQR_MODE"]
+    base = res["while"]
+    for mode, r in res.items():
+        assert np.array_equal(r.row_indices, base.row_indices), mode
+        assert abs(r.lsqr_iters - base.lsqr_iters) <= max(3, 0.05 * base.lsqr_iters), mode
+        assert abs(r.final_relres - base.final_relres) <= 1e-6 * base.final_relres, mode
+    # the operator itself against a host product
+    u = np.random.default_rng(3).standard_normal(p.m)
+    ref = np.zeros(p.n)
+    for j in range(p.n):
+        s, e = p.colptr[j], p.colptr[j + 1]
+        ref[j] = np.dot(p.vals[s:e], u[p.rowidx[s:e]])
+    np.testing.assert_allclose(A.apply(u, transpose=True), ref, rtol=1e-11, atol=1e-12 * np.abs(ref).max())
