@@ -138,18 +138,20 @@ __device__ __forceinline__ double csr_fwd_tile(const int* __restrict__ ptr, cons
   for (int k = 0; k < kCsrFwdRowsPerBlock; k += kGroups * U) {
     long long r[U];
     int b[U], len[U];
-    double pre[U];  // epilogue inputs, fetched with the row pointers (off the critical path)
+    // the epilogue of row uu runs on lane uu of the group (U <= G): its
+    // input is fetched with the row pointers, off the critical path
+    static_assert(U <= G, "one epilogue lane per row");
+    double pre = 0.0;
     int maxlen = 0;
 #pragma unroll
     for (int uu = 0; uu < U; ++uu) {
       r[uu] = rbase + k + uu * kGroups + g;
       b[uu] = 0;
       len[uu] = 0;
-      pre[uu] = 0.0;
       if (k + uu * kGroups < kCsrFwdRowsPerBlock && r[uu] < rows) {
         b[uu] = __ldg(ptr + r[uu]);
         len[uu] = __ldg(ptr + r[uu] + 1) - b[uu];
-        if (lane == 0) pre[uu] = epi.load(r[uu]);
+        if (lane == uu) pre = epi.load(r[uu]);
       }
       maxlen = max(maxlen, len[uu]);
     }
@@ -162,11 +164,12 @@ __device__ __forceinline__ double csr_fwd_tile(const int* __restrict__ ptr, cons
       for (int uu = 0; uu < U; ++uu)
         if (q < len[uu]) s[uu] += __ldcs(val + b[uu] + q) * __ldg(x + __ldcs(idx + b[uu] + q));
     }
+    // butterfly: every lane of the group ends with the bit-identical row sum
 #pragma unroll
     for (int uu = 0; uu < U; ++uu) {
 #pragma unroll
       for (int o = G / 2; o > 0; o >>= 1) s[uu] += __shfl_xor_sync(0xffffffffu, s[uu], o, G);
-      if (lane == 0 && k + uu * kGroups < kCsrFwdRowsPerBlock && r[uu] < rows) sq += epi.row(r[uu], s[uu], pre[uu]);
+      if (lane == uu && k + uu * kGroups < kCsrFwdRowsPerBlock && r[uu] < rows) sq += epi.row(r[uu], s[uu], pre);
     }
   }
   return sq;
