@@ -201,6 +201,30 @@ int apc_result_trace(const apc_result* r, apc_trace_row* rows);
 /* wall-clock split of the last solve: setup (sketch + CUR + builds) and LSQR, ms */
 int apc_result_timing(const apc_result* r, double* total_ms, double* lsqr_ms, double* setup_ms);
 
+/* ---- formats around the path (host only, no GPU needed) ----------------- */
+/* Matrix Market, matrix_market.hpp:18-46 (write: coordinate for CSC, array for
+ * dense column-major; %.17g values, bit-exact on read-back) and :48-116 (read:
+ * general real/integer coordinate or array; entries sorted by (col,row),
+ * duplicates -> APC_INVALID_ARGUMENT, explicit zeros dropped, malformed ->
+ * APC_IO).  The read result is a host apc_problem (b = zeros(m)); use
+ * apc_problem_info / _csc / _dense and apc_mat_upload_* as for generated inputs. */
+int apc_mm_write_csc(const char* path, int64_t m, int64_t n, const int64_t* colptr, const int64_t* rowidx,
+                     const double* vals);
+int apc_mm_write_dense(const char* path, int64_t m, int64_t n, const double* a_colmajor);
+int apc_mm_read(const char* path, apc_problem** out);
+/* trace CSV, report_io.hpp:28-47: "phase,iter,phibar,relres,matvecs,wall_ms,reason",
+ * reason on the last row of each phase (that phase's report, else trace_reason);
+ * written to path.tmp then renamed (report_io.hpp:112-122) */
+int apc_trace_csv_write(const char* path, const apc_trace_row* rows, int64_t n_rows, const apc_phase_report* phases,
+                        int64_t n_phases, int32_t trace_reason);
+/* solve report JSON, report_io.hpp:49-110 (config, status, residuals, counters,
+ * trace path, CUR indices + rho history, phase reports); non-finite -> null */
+int apc_report_json_write(const char* path, const apc_solver_config* cfg, int32_t status, double final_relres,
+                          double final_rho, uint64_t sketch_applications, uint64_t system_matvecs,
+                          const char* trace_path, const int64_t* row_indices, const int64_t* col_indices,
+                          int64_t rank, const double* rho_history, int64_t n_rho, const apc_phase_report* phases,
+                          int64_t n_phases);
+
 #ifdef __cplusplus
 }
 #endif

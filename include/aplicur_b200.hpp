@@ -249,7 +249,7 @@ struct SolveResult {  // solver.hpp:101-112
 };
 
 namespace b200 {
-inline SolveResult run(const ProblemInstance& p, const SolverConfig& c, int plain) {
+inline apc_solver_config to_c(const SolverConfig& c) {
   apc_solver_config k;
   apc_config_default(&k);
   k.block = c.block;
@@ -268,6 +268,11 @@ inline SolveResult run(const ProblemInstance& p, const SolverConfig& c, int plai
   k.trace_sample_stride = c.trace_sample_stride;
   k.outer_cap = c.outer_cap;
   k.sketch_kind = c.gaussian_sketch ? 1 : 0;
+  return k;
+}
+
+inline SolveResult run(const ProblemInstance& p, const SolverConfig& c, int plain) {
+  apc_solver_config k = to_c(c);
   if (static_cast<Index>(p.b.size()) != p.a.rows())
     throw Error(ErrorKind::dimension_mismatch, "aplicur_solve: rhs length mismatch");
   apc_result* r = nullptr;
@@ -331,6 +336,85 @@ inline SolveResult aplicur_solve(const ProblemInstance& problem, const SolverCon
 /// solver.hpp:396 -- unpreconditioned LSQR baseline on the GPU
 inline SolveResult plain_lsqr_solve(const ProblemInstance& problem, const SolverConfig& config) {
   return b200::run(problem, config, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Formats around the path (host only): Matrix Market (matrix_market.hpp:18-116),
+// trace CSV and solve report JSON (report_io.hpp:28-122), same names.
+// ---------------------------------------------------------------------------
+inline void write_matrix_market(const Matrix& a, const std::string& path) {
+  if (a.is_sparse())
+    b200::check(apc_mm_write_csc(path.c_str(), a.rows(), a.cols(), a.col_ptr().data(), a.row_idx().data(),
+                                 a.values().data()));
+  else
+    b200::check(apc_mm_write_dense(path.c_str(), a.rows(), a.cols(), a.dense_data().data()));
+}
+
+inline Matrix read_matrix_market(const std::string& path) {
+  apc_problem* h = nullptr;
+  b200::check(apc_mm_read(path.c_str(), &h));
+  std::unique_ptr<apc_problem, int (*)(apc_problem*)> guard(h, apc_problem_free);
+  std::int64_t m = 0, n = 0, nnz = 0;
+  int sparse = 0;
+  apc_problem_info(h, &m, &n, &sparse, &nnz);
+  if (!sparse) {
+    const double* d = apc_problem_dense(h);
+    return Matrix::dense(m, n, std::vector<double>(d, d + m * n));
+  }
+  const std::int64_t *cp = nullptr, *ri = nullptr;
+  const double* va = nullptr;
+  b200::check(apc_problem_csc(h, &cp, &ri, &va));
+  std::vector<Triplet> t;
+  t.reserve(static_cast<size_t>(nnz));
+  for (Index j = 0; j < n; ++j)
+    for (Index k = cp[j]; k < cp[j + 1]; ++k) t.push_back({ri[k], j, va[k]});
+  return Matrix::sparse(m, n, std::move(t));
+}
+
+namespace b200 {
+inline std::vector<apc_phase_report> to_c(std::span<const PhaseReport> phases) {
+  std::vector<apc_phase_report> out;
+  for (const auto& p : phases) {
+    apc_phase_report q{};
+    q.phase = p.phase;
+    q.reason = static_cast<std::int32_t>(p.reason);
+    q.rank = p.rank;
+    q.rho = p.rho;
+    q.sigma_hat = p.sigma_hat;
+    q.mu = p.mu;
+    q.lsqr_iters = p.lsqr_iters;
+    q.t_augment_ms = p.t_augment_ms;
+    q.t_factor_ms = p.t_factor_ms;
+    q.t_precond_ms = p.t_precond_ms;
+    q.t_lsqr_ms = p.t_lsqr_ms;
+    q.relres_at_end = p.relres_at_end;
+    out.push_back(q);
+  }
+  return out;
+}
+}  // namespace b200
+
+/// report_io.hpp:28-47 (written to path.tmp, then renamed)
+inline void trace_to_csv(const LsqrTrace& trace, const std::string& path, std::span<const PhaseReport> phases = {}) {
+  std::vector<apc_trace_row> rows;
+  for (const auto& r : trace.rows)
+    rows.push_back({r.phase, 0, r.iter, r.phibar, r.cvgrate, r.cvgdiff, r.matvecs, r.wall_ms, r.true_relres});
+  const auto ph = b200::to_c(phases);
+  b200::check(apc_trace_csv_write(path.c_str(), rows.data(), static_cast<std::int64_t>(rows.size()), ph.data(),
+                                  static_cast<std::int64_t>(ph.size()), static_cast<std::int32_t>(trace.reason)));
+}
+
+/// report_io.hpp:94-122: solve report JSON, atomic write
+inline void write_solve_report(const SolverConfig& config, const SolveResult& r, const std::string& trace_path,
+                               const std::string& path) {
+  const apc_solver_config k = b200::to_c(config);
+  const auto ph = b200::to_c(r.phases);
+  b200::check(apc_report_json_write(path.c_str(), &k, static_cast<std::int32_t>(r.status), r.final_relres, r.final_rho,
+                                    r.sketch_applications, r.system_matvecs, trace_path.c_str(),
+                                    r.row_indices.data(), r.col_indices.data(),
+                                    static_cast<std::int64_t>(r.row_indices.size()), r.rho_history.data(),
+                                    static_cast<std::int64_t>(r.rho_history.size()), ph.data(),
+                                    static_cast<std::int64_t>(ph.size())));
 }
 
 }  // namespace aplicur

@@ -85,6 +85,8 @@ def lib() -> C.CDLL:
         L.ref_cur_steps.argtypes = [P, _i64, _u64, _i64, _i64, _i32, _i32, _i64, _dp, _i64p, _i64p,
                                     _i64p, _dp, _i64p, _dp]
         L.ref_time_op_pair.argtypes = [P, _i64, _dp]
+        L.ref_mm_write.argtypes = [P, C.c_char_p]
+        L.ref_mm_read.argtypes = [C.c_char_p, _i64p, _i64p, C.POINTER(_i32), _i64p, _i64p, _i64p, _dp, _dp]
         _lib = L
     return _lib
 
@@ -280,3 +282,29 @@ def time_op_pair(p: Problem, iters: int) -> float:
     out = C.c_double()
     _chk(lib().ref_time_op_pair(C.byref(p.c), iters, C.byref(out)))
     return out.value
+
+
+def mm_write(p: "Problem", path) -> None:
+    """Reference write_matrix_market (matrix_market.hpp:18-46)."""
+    _chk(lib().ref_mm_write(C.byref(p.c), str(path).encode()))
+
+
+def mm_read(path) -> dict:
+    """Reference read_matrix_market (matrix_market.hpp:48-116): CSC or dense arrays."""
+    m, n, nz, sp = _i64(), _i64(), _i64(), _i32()
+    _chk(lib().ref_mm_read(str(path).encode(), C.byref(m), C.byref(n), C.byref(sp), C.byref(nz), None, None, None,
+                           None))
+    out = dict(m=m.value, n=n.value, sparse=bool(sp.value))
+    if sp.value:
+        cp = np.zeros(n.value + 1, dtype=np.int64)
+        ri = np.zeros(nz.value, dtype=np.int64)
+        va = np.zeros(nz.value)
+        _chk(lib().ref_mm_read(str(path).encode(), C.byref(m), C.byref(n), C.byref(sp), C.byref(nz),
+                               cp.ctypes.data_as(_i64p), ri.ctypes.data_as(_i64p), va.ctypes.data_as(_dp), None))
+        out.update(colptr=cp, rowidx=ri, vals=va)
+    else:
+        d = np.zeros(m.value * n.value)
+        _chk(lib().ref_mm_read(str(path).encode(), C.byref(m), C.byref(n), C.byref(sp), C.byref(nz), None, None, None,
+                               d.ctypes.data_as(_dp)))
+        out.update(dense=d)
+    return out

@@ -39,6 +39,7 @@
 #include "aplicur/dense_factor.hpp"
 #include "aplicur/lsqr.hpp"
 #include "aplicur/matrix.hpp"
+#include "aplicur/matrix_market.hpp"
 #include "aplicur/operators.hpp"
 #include "aplicur/preconditioner.hpp"
 #include "aplicur/problems.hpp"
@@ -426,6 +427,30 @@ int ref_time_op_pair(const RefProblem* p, std::int64_t iters, double* sec_per_pa
     }
     *sec_per_pair = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() /
                     static_cast<double>(iters);
+  });
+}
+
+// ---- Matrix Market (matrix_market.hpp:18-116) --------------------------------
+int ref_mm_write(const RefProblem* p, const char* path) {
+  return guarded([&] { write_matrix_market(make_matrix(p), std::string(path)); });
+}
+
+// two calls: sizes first (array pointers null), then the arrays (CSC or dense)
+int ref_mm_read(const char* path, std::int64_t* m, std::int64_t* n, std::int32_t* sparse, std::int64_t* nnz,
+                std::int64_t* colptr, std::int64_t* rowidx, double* vals, double* dense) {
+  return guarded([&] {
+    Matrix a = read_matrix_market(std::string(path));
+    *m = a.rows();
+    *n = a.cols();
+    *sparse = a.is_sparse() ? 1 : 0;
+    *nnz = a.nnz();
+    if (a.is_sparse()) {
+      if (colptr) std::copy(a.col_ptr().begin(), a.col_ptr().end(), colptr);
+      if (rowidx) std::copy(a.row_idx().begin(), a.row_idx().end(), rowidx);
+      if (vals) std::copy(a.values().begin(), a.values().end(), vals);
+    } else if (dense) {
+      std::copy(a.dense_data().begin(), a.dense_data().end(), dense);
+    }
   });
 }
 

@@ -174,6 +174,13 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
         "apc_cur_sketch": (C.c_int, [vp, _dp]),
         "apc_cur_residual": (C.c_int, [vp, _dp]),
         "apc_lupp": (C.c_int, [vp, _dp, _i64, _i64, _i64, _i64p, _dp, _i64p]),
+        "apc_mm_write_csc": (C.c_int, [C.c_char_p, _i64, _i64, _i64p, _i64p, _dp]),
+        "apc_mm_write_dense": (C.c_int, [C.c_char_p, _i64, _i64, _dp]),
+        "apc_mm_read": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+        "apc_trace_csv_write": (C.c_int, [C.c_char_p, C.POINTER(_Trace), _i64, C.POINTER(_Phase), _i64, C.c_int32]),
+        "apc_report_json_write": (C.c_int, [C.c_char_p, C.POINTER(_Config), C.c_int32, C.c_double, C.c_double,
+                                            _u64, _u64, C.c_char_p, _i64p, _i64p, _i64, _dp, _i64,
+                                            C.POINTER(_Phase), _i64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -432,10 +439,13 @@ def rng_fill(seed: int, kind: int, count: int, stream: int = -1, index: int = 0,
 class Problem:
     """Host copy of a generated BASELINE input (same bytes for oracle and GPU)."""
 
-    def __init__(self, config: int, m: int = 0, n: int = 0, seed: int = 0):
+    def __init__(self, config: int, m: int = 0, n: int = 0, seed: int = 0, _handle=None):
         lib = load_library()
-        h = C.c_void_p()
-        _check(lib.apc_problem_generate(config, m, n, seed, C.byref(h)))
+        if _handle is None:
+            h = C.c_void_p()
+            _check(lib.apc_problem_generate(config, m, n, seed, C.byref(h)))
+        else:
+            h = _handle
         mm, nn, nz, sp = _i64(), _i64(), _i64(), C.c_int()
         lib.apc_problem_info(h, C.byref(mm), C.byref(nn), C.byref(sp), C.byref(nz))
         self.config, self.m, self.n, self.sparse, self.nnz = config, mm.value, nn.value, bool(sp.value), nz.value
@@ -526,10 +536,38 @@ class SolveResult:
     total_ms: float = 0.0
     lsqr_ms: float = 0.0
     setup_ms: float = 0.0
+    _raw_phases: object = None  # ctypes apc_phase_report array (for the report writers)
 
     @property
     def lsqr_iters(self) -> int:
         return int(sum(p.lsqr_iters for p in self.phases))
+
+    def _phase_array(self):
+        if self._raw_phases is not None:
+            return self._raw_phases
+        arr = (_Phase * max(1, len(self.phases)))()
+        for k, p in enumerate(self.phases):
+            arr[k] = _Phase(p.phase, int(p.reason), p.rank, p.rho, p.sigma_hat, p.mu, p.lsqr_iters, p.t_augment_ms,
+                            p.t_factor_ms, p.t_precond_ms, p.t_lsqr_ms, p.relres_at_end, p.t_lsqr_device_ms)
+        return arr
+
+    def write_trace_csv(self, path) -> None:
+        """report_io.hpp:28-47 -- one row per LSQR iteration, reason on each phase's last row."""
+        rows = np.ascontiguousarray(self.trace)
+        reason = int(self.phases[-1].reason) if self.phases else 0
+        _check(load_library().apc_trace_csv_write(str(path).encode(), rows.ctypes.data_as(C.POINTER(_Trace)),
+                                                  len(rows), self._phase_array(), len(self.phases), reason))
+
+    def write_report_json(self, path, config: "SolverConfig", trace_path: str = "") -> None:
+        """report_io.hpp:94-110 -- solve report (config, status, CUR indices, phases), atomic write."""
+        c = config._c()
+        ri = np.ascontiguousarray(self.row_indices, dtype=np.int64)
+        ci = np.ascontiguousarray(self.col_indices, dtype=np.int64)
+        rho = np.ascontiguousarray(self.rho_history, dtype=np.float64)
+        _check(load_library().apc_report_json_write(
+            str(path).encode(), C.byref(c), int(self.status), self.final_relres, self.final_rho,
+            self.sketch_applications, self.system_matvecs, str(trace_path).encode(), _iptr(ri), _iptr(ci), len(ri),
+            _dptr(rho), len(rho), self._phase_array(), len(self.phases)))
 
 
 def _collect(h) -> SolveResult:
@@ -557,7 +595,7 @@ def _collect(h) -> SolveResult:
                       p.t_lsqr_device_ms)
           for p in phases[: nph.value]]
     return SolveResult(None, ph, tr, SolveStatus(st.value), frho.value, frel.value, sk.value, smv.value,
-                       rows, cols, rho, tt.value, tl.value, ts.value)
+                       rows, cols, rho, tt.value, tl.value, ts.value, phases)
 
 
 def solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig, plain: bool = False,
@@ -598,9 +636,40 @@ def plain_lsqr_solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig) -> 
     return solve(mat, b, config, plain=True)
 
 
+def read_matrix_market(path) -> Problem:
+    """matrix_market.hpp:48-116 -- a host Problem (b = zeros(m)) from a Matrix Market file."""
+    h = C.c_void_p()
+    _check(load_library().apc_mm_read(str(path).encode(), C.byref(h)))
+    return Problem(0, _handle=h)
+
+
+def write_matrix_market(path, a) -> None:
+    """matrix_market.hpp:18-46 -- coordinate (a sparse Problem, or (m, n, colptr, rowidx, vals))
+    or array (a dense Problem, or a 2-D numpy array) with %.17g values."""
+    lib = load_library()
+    if isinstance(a, Problem):
+        if a.sparse:
+            cp, ri, va = (np.ascontiguousarray(x) for x in (a.colptr, a.rowidx, a.vals))
+            _check(lib.apc_mm_write_csc(str(path).encode(), a.m, a.n, _iptr(cp), _iptr(ri), _dptr(va)))
+        else:
+            d = np.ascontiguousarray(a.dense, dtype=np.float64)
+            _check(lib.apc_mm_write_dense(str(path).encode(), a.m, a.n, _dptr(d)))
+    elif isinstance(a, tuple):
+        m, n, cp, ri, va = a
+        cp = np.ascontiguousarray(cp, dtype=np.int64)
+        ri = np.ascontiguousarray(ri, dtype=np.int64)
+        va = np.ascontiguousarray(va, dtype=np.float64)
+        _check(lib.apc_mm_write_csc(str(path).encode(), m, n, _iptr(cp), _iptr(ri), _dptr(va)))
+    else:
+        A = np.asarray(a, dtype=np.float64)
+        d = np.ascontiguousarray(A.T).reshape(-1)  # column-major
+        _check(lib.apc_mm_write_dense(str(path).encode(), A.shape[0], A.shape[1], _dptr(d)))
+
+
 __all__ = [
     "ApcError", "StopReason", "SolveStatus", "PrecondVariant", "CoreFactorKind", "SketchKind",
     "Context", "DeviceMatrix", "Problem", "SolverConfig", "SolveResult", "PhaseReport",
     "aplicur_solve", "plain_lsqr_solve", "solve", "load_library", "device_count",
     "partition_rows", "rng_fill", "LIB_PATH", "HEADER_PATHS", "CurState", "lu_partial_pivot",
+    "read_matrix_market", "write_matrix_market",
 ]

@@ -21,14 +21,7 @@
 #include "host_dense.hpp"
 #include "host_rng.hpp"
 
-struct apc_problem {
-  apc::i64 m = 0, n = 0;
-  bool sparse = false;
-  std::vector<double> dense;                 // column-major
-  std::vector<std::int64_t> colptr, rowidx;  // CSC (reference layout)
-  std::vector<double> vals;
-  std::vector<double> b;
-};
+#include "problem.hpp"
 
 namespace apc {
 
