@@ -52,6 +52,20 @@ inline void copy_sync(cudaStream_t st, void* dst, const void* src, size_t bytes,
   APC_CUDA(cudaStreamSynchronize(st));
 }
 
+// Host wall-time breakdown of the solve setup (APC_SETUP_PROF=1): named
+// buckets, accumulated per thread, printed by the solver at the end.
+struct SetupProf {
+  static bool on();
+  static void add(const char* name, double ms);
+  static void dump_and_reset(const char* title);
+};
+struct ProfScope {
+  const char* name;
+  double t0;
+  explicit ProfScope(const char* n);
+  ~ProfScope();
+};
+
 // ---------------------------------------------------------------------------
 // Device buffers
 // ---------------------------------------------------------------------------

@@ -9,6 +9,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <memory>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -545,29 +546,58 @@ __global__ void eres_kernel(const double* __restrict__ Y, const double* __restri
 }
 
 // rho probes: out(i, p) = (E w_p)_i with the dense matvec chain (j ascending,
-// zero entries of w skipped), sketch.hpp:219-221 -> matrix.hpp:156-162
-__global__ void probe_kernel(const double* __restrict__ E, long long s, long long n,
-                             const double* __restrict__ W, double* __restrict__ out) {
-  const long long i = static_cast<long long>(blockIdx.x) * 32 + (threadIdx.x & 31);
+// zero entries of w skipped), sketch.hpp:219-221 -> matrix.hpp:156-162.
+// Each output is one sequential chain of n DMUL+DADD (the reference order).
+// The FP64 pipe, not memory, bounds such chains (measured: ~18 cycles per
+// step for one warp on an SM, ~35-70 with 18 warps sharing it), so the
+// chains are spread one warp per SM: CTA = (probe p, 32 consecutive rows i),
+// and the E rows / probe entries of the next kProbeStages-1 column chunks are
+// in flight as cp.async copies into shared memory while the current chunk runs.
+constexpr int kProbeJ = 32;       // columns per stage
+constexpr int kProbeStages = 4;   // cp.async pipeline depth
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__global__ void __launch_bounds__(32)
+probe_kernel(const double* __restrict__ E, long long s, long long n, const double* __restrict__ W,
+             double* __restrict__ out) {
+  __shared__ double et[kProbeStages][kProbeJ][32];
+  __shared__ double wt[kProbeStages][kProbeJ];
+  const int lane = threadIdx.x;
   const long long p = blockIdx.y;
-  if (i >= s) return;
+  const long long i = static_cast<long long>(blockIdx.x) * 32 + lane;
+  const bool act = i < s;
   const double* w = W + p * n;
-  double acc = 0.0;
-  // loads hoisted 16 at a time; the add chain keeps the reference's j order
-  constexpr int U = 16;
-  for (long long j0 = 0; j0 < n; j0 += U) {
-    double xs[U], es[U];
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      const long long j = j0 + q;
-      xs[q] = j < n ? w[j] : 0.0;
-      es[q] = j < n ? E[j * s + i] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < U; ++q)
-      if (xs[q] != 0.0) acc += xs[q] * es[q];
+  const long long nchunk = (n + kProbeJ - 1) / kProbeJ;
+  auto issue = [&](long long c) {
+    const int st = static_cast<int>(c % kProbeStages);
+    const long long j0 = c * kProbeJ;
+    for (int jj = 0; jj < kProbeJ; ++jj)
+      if (act && j0 + jj < n) cp_async8(&et[st][jj][lane], E + (j0 + jj) * s + i);
+    if (j0 + lane < n) cp_async8(&wt[st][lane], w + j0 + lane);
+  };
+  for (int c = 0; c < kProbeStages - 1; ++c) {
+    if (c < nchunk) issue(c);
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  out[p * s + i] = acc;
+  double acc = 0.0;
+  for (long long c = 0; c < nchunk; ++c) {
+    if (c + kProbeStages - 1 < nchunk) issue(c + kProbeStages - 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(kProbeStages - 1) : "memory");
+    __syncwarp();
+    const int st = static_cast<int>(c % kProbeStages);
+    const int jn = static_cast<int>(n - c * kProbeJ < kProbeJ ? n - c * kProbeJ : kProbeJ);
+    if (act)
+      for (int jj = 0; jj < jn; ++jj) {
+        const double wv = wt[st][jj];
+        if (wv != 0.0) acc += wv * et[st][jj][lane];
+      }
+    __syncwarp();
+  }
+  if (act) out[p * s + i] = acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -936,7 +966,7 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
           });
           for (i64 q = 0; q < x; ++q) sg[c * x + q] = static_cast<signed char>((d[x + q] & 1ULL) ? 1 : -1);
         }
-      });
+      }, 16 * x);
       for (char f : bad) ok = ok && !f;
     }
     if (!ok) {  // sequential reference construction (sketch.hpp:31-49)
@@ -1064,18 +1094,31 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
 
 DeviceCur::~DeviceCur() = default;
 
+std::vector<double> DeviceCur::draw_probes() {
+  // probe p = the p-th block of n consecutive Gaussians of the probe stream
+  std::vector<double> w(static_cast<size_t>(probes_ * n_));
+  fill_gaussians(probe_rng_, w.data(), probes_ * n_);
+  return w;
+}
+
 void DeviceCur::compute_rho() {
   // spectral_norm_estimate (sketch.hpp:209-223): probes drawn on the host
   const i64 r = probes_;
-  std::vector<double> w(static_cast<size_t>(r * n_));
-  for (i64 p = 0; p < r; ++p)
-    fill_gaussians(probe_rng_, w.data() + p * n_, n_);
+  std::unique_ptr<ProfScope> ps(new ProfScope("rho.gauss"));
+  std::vector<double> w = next_probes_.valid() ? next_probes_.get() : draw_probes();
+  static const bool sync_probes = std::getenv("APC_SYNC_PROBES") != nullptr;
+  if (!sync_probes) next_probes_ = std::async(std::launch::async, [this] { return draw_probes(); });
+  ps.reset(new ProfScope("rho.upload"));
   DBuf<double> d_w, d_out(std::max<i64>(1, s_ * r));
   upload(ctx_, d_w, w.data(), r * n_);
+  APC_CUDA(cudaStreamSynchronize(ctx_->stream));
+  ps.reset(new ProfScope("rho.kernel"));
+  // one warp per CTA: (32 rows of E) x (one probe), spread over the SMs
   dim3 grid(static_cast<unsigned>((s_ + 31) / 32), static_cast<unsigned>(r));
   probe_kernel<<<grid, 32, 0, ctx_->stream>>>(E_.p, s_, n_, d_w.p, d_out.p);
   ctx_->launches++;
   std::vector<double> ew = download(ctx_, d_out.p, s_ * r);
+  ps.reset();
   double best = 0.0;
   for (i64 p = 0; p < r; ++p) {
     double nrm2 = 0.0;
@@ -1106,7 +1149,9 @@ AugmentResult DeviceCur::augment() {
   work_.ensure(std::max<i64>(1, s_ * n_));
   transpose_zero_kernel<<<nb(s_ * n_), kT, 0, st>>>(E_.p, s_, n_, colsel_.p, work_.p);
   ctx_->launches++;
+  std::unique_ptr<ProfScope> ps(new ProfScope("aug.col_lupp"));
   LuppOut col_piv = device_lupp(ctx_, work_.p, n_, s_, want);
+  ps.reset(new ProfScope("aug.ecol"));
   std::vector<i64> jplus = admissible(col_piv, want, ztol_);
   if (jplus.empty()) {
     if (rank() == 0) compute_rho();
@@ -1161,7 +1206,9 @@ AugmentResult DeviceCur::augment() {
     APC_CUDA(cudaStreamSynchronize(st));
   }
   APC_CUDA(cudaGetLastError());
+  ps.reset(new ProfScope("aug.row_lupp"));
   LuppOut row_piv = device_lupp(ctx_, ecol.p, mt_, b, b);
+  ps.reset();
   std::vector<i64> iplus = admissible(row_piv, b, ztol_);
   if (iplus.empty()) return {0, true};
   const bool exhausted = static_cast<i64>(iplus.size()) < want;
@@ -1208,8 +1255,10 @@ void DeviceCur::refresh() {
   gather_block_kernel<<<nb(l * l), kT, 0, st>>>(a_.dense.p, m_, a_.a.ptr.p, a_.a.idx.p, a_.a.val.p,
                                                 a_.sparse ? 1 : 0, d_I.p, d_J.p, l, l, amu_, d_blk.p);
   ctx_->launches++;
+  std::unique_ptr<ProfScope> ps(new ProfScope("ref.core_build"));
   block_ = download(ctx_, d_blk.p, l * l);
   core_ = CoreFactorH::build(l, block_, core_kind_);  // throws singular
+  ps.reset(new ProfScope("ref.rows_H_eres"));
   // R = A(I, :) row-major (all rows re-gathered: I may have changed after a rollback)
   Rrm_.ensure(l * n_);
   if (!a_.sparse) {
@@ -1231,6 +1280,8 @@ void DeviceCur::refresh() {
   eres_kernel<<<nb(n_ * 32), kT, 0, st>>>(Y_.p, d_sc.p, H_.p, s_, n_, l, E_.p);
   ctx_->launches += 3;
   APC_CUDA(cudaGetLastError());
+  APC_CUDA(cudaStreamSynchronize(st));
+  ps.reset(new ProfScope("ref.rho"));
   compute_rho();
 }
 

@@ -9,6 +9,7 @@
 // (host_dense.hpp), so I, J and rho_history are bit-identical to the reference.
 #pragma once
 
+#include <future>
 #include <vector>
 
 #include "apc_internal.hpp"
@@ -75,6 +76,7 @@ class DeviceCur {
 
  private:
   void compute_rho();
+  std::vector<double> draw_probes();  // the next probes_ x n Gaussians of probe_rng_
   void upload_core();
 
   apc_mat& a_;
@@ -90,6 +92,9 @@ class DeviceCur {
   std::vector<i64> I_, J_;
   std::vector<double> rho_hist_;
   HostRng probe_rng_;
+  // the probe set of the next compute_rho, drawn on a host thread while the
+  // device works (the stream is consumed strictly in order, one set at a time)
+  std::future<std::vector<double>> next_probes_;
   CoreFactorH core_;
   Vec block_;
   DBuf<double> Y_, E_;        // s x n column-major

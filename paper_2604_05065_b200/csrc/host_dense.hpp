@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "apc_internal.hpp"
+#include "host_rng.hpp"
 
 namespace apc {
 
@@ -189,17 +190,28 @@ inline void tri_solve(i64 k, const double* t, double* x, bool transpose) {
 
 // column-major C = A (m x k) * B (k x n), per-column sequential chains that
 // skip zero B entries (matmul -> Matrix::matvec, matrix.hpp:151-162,351-361)
-inline Vec matmul(i64 m, i64 k, i64 n, const Vec& a, const Vec& b) {
-  Vec c(static_cast<size_t>(m * n), 0.0);
-  for (i64 j = 0; j < n; ++j) {
-    double* cc = c.data() + j * m;
-    for (i64 t = 0; t < k; ++t) {
-      const double x = b[j * k + t];
-      if (x == 0.0) continue;
-      const double* ac = a.data() + t * m;
-      for (i64 i = 0; i < m; ++i) cc[i] += x * ac[i];
+// (columns are independent, so they run on the host's cores: same bits)
+struct MatmulCols {  // named functor: see the note at host_parallel_for
+  i64 m, k;
+  const double* a;
+  const double* b;
+  double* c;
+  void operator()(i64 j0, i64 j1) const {
+    for (i64 j = j0; j < j1; ++j) {
+      double* cc = c + j * m;
+      for (i64 t = 0; t < k; ++t) {
+        const double x = b[j * k + t];
+        if (x == 0.0) continue;
+        const double* ac = a + t * m;
+        for (i64 i = 0; i < m; ++i) cc[i] += x * ac[i];
+      }
     }
   }
+};
+
+inline Vec matmul(i64 m, i64 k, i64 n, const Vec& a, const Vec& b) {
+  Vec c(static_cast<size_t>(m * n), 0.0);
+  host_parallel_for(n, MatmulCols{m, k, a.data(), b.data(), c.data()}, m * k);
   return c;
 }
 
@@ -451,12 +463,24 @@ struct CoreFactorH {
     }
   }
 
+  // columns are independent: parallel over the host's cores, same bits
+  struct SolveCols {  // named functor: see the note at host_parallel_for
+    const CoreFactorH* f;
+    double* b;
+    bool transpose;
+    void operator()(i64 j0, i64 j1) const {
+      for (i64 j = j0; j < j1; ++j) {
+        if (transpose) f->solve_transpose(b + j * f->l);
+        else f->solve(b + j * f->l);
+      }
+    }
+  };
   Vec solve_matrix(i64 ncols, Vec b) const {
-    for (i64 j = 0; j < ncols; ++j) solve(b.data() + j * l);
+    host_parallel_for(ncols, SolveCols{this, b.data(), false}, 3 * l * l);
     return b;
   }
   Vec solve_matrix_transpose(i64 ncols, Vec b) const {
-    for (i64 j = 0; j < ncols; ++j) solve_transpose(b.data() + j * l);
+    host_parallel_for(ncols, SolveCols{this, b.data(), true}, 3 * l * l);
     return b;
   }
 };

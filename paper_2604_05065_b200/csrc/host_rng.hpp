@@ -7,8 +7,10 @@
 #pragma once
 
 #include <algorithm>
+#include <exception>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <random>
 #include <thread>
 #include <vector>
@@ -69,35 +71,68 @@ class HostRng {
   std::mt19937_64 eng_;
 };
 
-// run f(begin, end) over [0, n) on the host's cores
+// run f(begin, end) over [0, n) on the host's cores when the total work
+// (n * unit_cost, in rough flop units) is worth the thread start-up;
+// exceptions thrown by f are rethrown on the calling thread.
+// NOTE: this header is compiled both by nvcc (.cu) and g++ (.cpp).  Closure
+// types of capturing lambdas are not guaranteed to have the same layout
+// under both front ends, and the inline instantiations are merged by the
+// linker -- so callers in shared headers pass named functors, and the worker
+// below is a named struct, never a lambda.
 template <class F>
-void host_parallel_for(i64 n, F f) {
+struct HostRangeWorker {
+  const F* f;
+  i64 b, e;
+  std::exception_ptr* err;
+  void operator()() const {
+    try {
+      (*f)(b, e);
+    } catch (...) {
+      *err = std::current_exception();
+    }
+  }
+};
+
+template <class F>
+void host_parallel_for(i64 n, const F& f, i64 unit_cost = 1) {
   unsigned hc = std::thread::hardware_concurrency();
-  const i64 nt = std::max<i64>(1, std::min<i64>(hc ? hc : 1, 32));
-  if (n < 4096 || nt == 1) {
+  const i64 nt = std::max<i64>(1, std::min<i64>({static_cast<i64>(hc ? hc : 1), 32, n}));
+  static const bool serial = std::getenv("APC_HOST_SERIAL") != nullptr;
+  if (serial || n * unit_cost < 1000000 || n < 2 || nt == 1) {
     f(i64{0}, n);
     return;
   }
   std::vector<std::thread> th;
+  std::vector<std::exception_ptr> err(static_cast<size_t>(nt));
   const i64 chunk = (n + nt - 1) / nt;
   for (i64 t = 0; t < nt; ++t) {
     const i64 b = t * chunk, e = std::min(n, b + chunk);
     if (b >= e) break;
-    th.emplace_back([=] { f(b, e); });
+    th.emplace_back(HostRangeWorker<F>{&f, b, e, &err[static_cast<size_t>(t)]});
   }
   for (auto& x : th) x.join();
+  for (auto& x : err)
+    if (x) std::rethrow_exception(x);
 }
 
 // n Gaussians of the stream (each consumes exactly two draws), transformed in parallel
-inline void fill_gaussians(HostRng& rng, double* out, i64 n, double scale = 1.0, bool scaled = false) {
-  std::vector<std::uint64_t> raw(static_cast<size_t>(2 * n));
-  for (auto& d : raw) d = rng.bits();
-  host_parallel_for(n, [&](i64 b, i64 e) {
+struct GaussFromRaw {
+  const std::uint64_t* raw;
+  double* out;
+  double scale;
+  bool scaled;
+  void operator()(i64 b, i64 e) const {
     for (i64 i = b; i < e; ++i) {
       const double g = HostRng::gaussian_of(raw[2 * i], raw[2 * i + 1]);
       out[i] = scaled ? scale * g : g;
     }
-  });
+  }
+};
+
+inline void fill_gaussians(HostRng& rng, double* out, i64 n, double scale = 1.0, bool scaled = false) {
+  std::vector<std::uint64_t> raw(static_cast<size_t>(2 * n));
+  for (auto& d : raw) d = rng.bits();
+  host_parallel_for(n, GaussFromRaw{raw.data(), out, scale, scaled}, 64);
 }
 
 }  // namespace apc

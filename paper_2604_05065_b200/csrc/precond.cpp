@@ -6,6 +6,7 @@
 // restated reference routines.  None of it is index-affecting:
 // only the x / iteration parity bar applies.
 #include <cmath>
+#include <memory>
 
 #include "blas.hpp"
 #include "cur.hpp"
@@ -215,6 +216,7 @@ void build_precond(const BuildInputs& in, PrecondDev& p, PrecondInfo& info) {
   p.l = l;
   // T_C = gram_factor(C): Cholesky of the device Gram, QR fallback (preconditioner.hpp:143-150)
   Vec t_c;
+  std::unique_ptr<ProfScope> ps(new ProfScope("pre.chol"));
   try {
     t_c = chol_upper(l, in.gram, "chol_gram: non-positive pivot");
   } catch (const Status& s) {
@@ -223,8 +225,10 @@ void build_precond(const BuildInputs& in, PrecondDev& p, PrecondInfo& info) {
   }
   if (in.variant == 0) {
     // SVD form: M = T_C U T_R^T, small_svd(M) (preconditioner.hpp:158-192)
+    ps.reset(new ProfScope("pre.core_matmul"));
     Vec ut = in.core->solve_matrix(l, transpose(l, l, *in.t_r));
     Vec mm = matmul(l, l, l, t_c, ut);
+    ps.reset(new ProfScope("pre.svd"));
     require(l <= 4096, APC_INVALID_ARGUMENT, "small_svd: dimension exceeds the small-problem cap");
     SvdH s;
     if (l > 96) {  // parallel-order Jacobi on the device; serial cyclic on the host for small cores
@@ -233,6 +237,7 @@ void build_precond(const BuildInputs& in, PrecondDev& p, PrecondInfo& info) {
     } else {
       s = small_svd(l, l, mm);
     }
+    ps.reset(new ProfScope("pre.G"));
     info.sigma_cur = s.sigma;
     info.sigma_reg.resize(l);
     for (i64 i = 0; i < l; ++i) info.sigma_reg[i] = std::sqrt(s.sigma[i] * s.sigma[i] + in.mu * in.mu);

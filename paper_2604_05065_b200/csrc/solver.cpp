@@ -4,8 +4,13 @@
 // (precond.cpp) and device-resident warm-started LSQR phases (lsqr.cu).
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <limits>
 #include <memory>
+#include <utility>
+#include <vector>
 
 #include "cur.hpp"
 #include "precond.hpp"
@@ -56,8 +61,10 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
   // CUR target: A for the svd variant; the regularised stack [A; mu I] for the
   // svd-free variant whenever mu > 0 (solver.hpp:183-186)
   const bool target_augmented = cfg.variant == 1 && mu > 0.0;
+  std::unique_ptr<ProfScope> ps_init(new ProfScope("cur_init"));
   DeviceCur cur(full, cfg.block, cfg.seed, cfg.sketch_xi, cfg.probe_count, cfg.core, cfg.sketch_kind,
                 cfg.max_rank, target_augmented ? mu : 0.0);
+  ps_init.reset();
   i64 max_rank = std::min(cur.target_rows(), n);
   if (cfg.max_rank > 0) max_rank = std::min(max_rank, cfg.max_rank);
   const double density = (m * n == 0) ? 0.0 : static_cast<double>(a.nnz_global) / static_cast<double>(m * n);
@@ -66,6 +73,7 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
   DevQrAcc qr_acc;
   qr_acc.ctx = ctx;
   Vec t_r_implicit;
+  bool t_r_stale = false;
   auto* res = new apc_result();
   std::unique_ptr<apc_result> guard(res);
   res->n = n;
@@ -87,7 +95,9 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
   auto run_phase = [&](PrecondDev& P, bool final_phase, double rho_at_build, apc_phase_report& rep,
                        const PrecondInfo& info) {
     auto t0 = clock_t_::now();
+    std::unique_ptr<ProfScope> ps_res(new ProfScope("residual"));
     residual(a, vw, d_x.p, d_b.p, d_rhs.p);  // rhs = b_aug - A_mu x (solver.hpp:207-210)
+    ps_res.reset();
     matvecs += 1;
     StopCfg stop;
     stop.eps_lsqr = cfg.eps_lsqr;
@@ -122,9 +132,14 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
     auto t_aug0 = clock_t_::now();
     bool grew = false;
     if (cur.rank() < max_rank) {
-      AugmentResult out = cur.augment();
+      AugmentResult out;
+      {
+        ProfScope ps("augment");
+        out = cur.augment();
+      }
       if (out.added > 0) {
         try {
+          ProfScope ps("refresh");
           cur.refresh();
           grew = true;
         } catch (const Status& e) {
@@ -147,15 +162,14 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
     rep.t_augment_ms = ms_since(t_aug0);
 
     auto t_fac0 = clock_t_::now();
+    std::unique_ptr<ProfScope> ps_fac(new ProfScope("factor"));
     if (grew) {
       const i64 l = cur.rank();
       if (implicit_mode) {
         // T_R with T_R^T T_R = R R^T (the reference maintains it with
-        // CholGramAccumulator; the from-scratch gram_factor is the same factor)
-        std::vector<i64> rp, ri;
-        Vec rv;
-        cur.rt_csc(rp, ri, rv);
-        t_r_implicit = gram_factor_sparse(n, l, rp, ri, rv);
+        // CholGramAccumulator; the from-scratch gram_factor is the same
+        // factor), computed when a preconditioner is next built
+        t_r_stale = true;
       } else {
         const i64 added = cur.last_added();
         // rows of R are stored row-major on the device: added x n == column-major n x added
@@ -173,6 +187,7 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
         if (cur.rho() > cfg.eps_cur) res->status = 1;
       }
     }
+    ps_fac.reset();
     rep.t_factor_ms = ms_since(t_fac0);
 
     const double rho = cur.rho();
@@ -184,6 +199,16 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
     const bool trigger = final_phase || reprecondition_check(d_cur, rho, cfg.eps_cur, cfg.nu_prec);
     if (trigger && cur.rank() > 0) {
       if (!res->phases.empty() && res->phases.back().rank == cur.rank()) break;  // duplicate rank
+      if (implicit_mode && t_r_stale) {
+        ProfScope ps("factor");
+        auto t_f0 = clock_t_::now();
+        std::vector<i64> rp, ri;
+        Vec rv;
+        cur.rt_csc(rp, ri, rv);
+        t_r_implicit = gram_factor_sparse(n, cur.rank(), rp, ri, rv);
+        t_r_stale = false;
+        rep.t_factor_ms += ms_since(t_f0);
+      }
       ++phase;
       auto t_pre0 = clock_t_::now();
       PrecondDev P;
@@ -214,6 +239,7 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
             for (i64 q = cp[j]; q < cp[j + 1]; ++q) d[j * mt + ci[q]] = cv[q];
           return d;
         };
+        ProfScope ps("precond");
         if (implicit_mode) cur.rt_csc(in.r_ptr, in.r_idx, in.r_val);
         build_precond(in, P, info);
       } catch (const Status& e) {
@@ -250,6 +276,8 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
   res->rho_history = cur.rho_history();
   res->total_ms = ms_since(t_start);
   res->setup_ms = res->total_ms - res->lsqr_ms;
+  SetupProf::add("lsqr_phases(total)", res->lsqr_ms);
+  SetupProf::dump_and_reset("aplicur_solve setup profile");
   guard.release();
   return res;
 }
