@@ -94,6 +94,10 @@ int apc_partition_rows(int64_t m, const int64_t* row_nnz, int nranks, int64_t* b
 int apc_rng_fill(uint64_t seed, int stream, uint64_t index, int kind, uint64_t bound,
                  int64_t count, void* out);
 uint64_t apc_mix64(uint64_t x);
+/* the same stream generated on the device: kind-0 draws (next_u64) of
+ * Rng(seed) (stream < 0) or Rng(seed, stream, index), count of them into the
+ * host buffer out.  Used by the sketch embedding; exposed for tests. */
+int apc_rng_fill_device(apc_ctx* ctx, uint64_t seed, int stream, uint64_t index, int64_t count, uint64_t* out);
 
 /* ---- single-sketch incremental CUR (CurState, cur.hpp:200-371) ----------
  * Exact-order device kernels: Y, E^row, the LUPP pivot order and rho are

@@ -144,6 +144,7 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
         "apc_partition_rows": (C.c_int, [_i64, _i64p, C.c_int, _i64p]),
         "apc_rng_fill": (C.c_int, [_u64, C.c_int, _u64, C.c_int, _u64, _i64, vp]),
         "apc_mix64": (_u64, [_u64]),
+        "apc_rng_fill_device": (C.c_int, [vp, _u64, C.c_int, _u64, _i64, C.POINTER(_u64)]),
         "apc_problem_generate": (C.c_int, [C.c_int, _i64, _i64, _u64, C.POINTER(vp)]),
         "apc_problem_info": (C.c_int, [vp, _i64p, _i64p, C.POINTER(C.c_int), _i64p]),
         "apc_problem_dense": (vp, [vp]),

@@ -13,6 +13,7 @@
 #include "apc_internal.hpp"
 #include "blas.hpp"
 #include "host_rng.hpp"
+#include "rng_dev.hpp"
 #include "lsqr.hpp"
 #include "ops_host.hpp"
 #include "solver.hpp"
@@ -339,6 +340,19 @@ int apc_rng_fill(uint64_t seed, int stream, uint64_t index, int kind, uint64_t b
 }
 
 uint64_t apc_mix64(uint64_t x) { return splitmix(x); }
+
+int apc_rng_fill_device(apc_ctx* ctx, uint64_t seed, int stream, uint64_t index, int64_t count, uint64_t* out) {
+  return guard(ctx, [&] {
+    require(ctx && (out || count == 0) && count >= 0, APC_INVALID_ARGUMENT, "apc_rng_fill_device: bad arguments");
+    require(mt64_device_ok(), APC_CUDA_ERROR, "apc_rng_fill_device: engine replica does not match the host library");
+    // HostRng's engine seed (host_rng.hpp): splitmix(seed) or the stream derivation
+    const std::uint64_t es = stream < 0 ? splitmix(seed)
+                                        : splitmix(splitmix(seed ^ (0x51ed2701a3c5e1bdULL * static_cast<std::uint64_t>(stream))) + index);
+    DBuf<std::uint64_t> d(std::max<int64_t>(1, count));
+    mt64_stream_device(ctx, es, count, d.p);
+    copy_sync(ctx->stream, out, d.p, sizeof(std::uint64_t) * count, cudaMemcpyDeviceToHost);
+  });
+}
 
 int apc_problem_generate(int config, int64_t m, int64_t n, uint64_t seed, apc_problem** out) {
   *out = nullptr;

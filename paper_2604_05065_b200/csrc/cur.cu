@@ -19,6 +19,7 @@
 
 #include "blas.hpp"
 #include "cur.hpp"
+#include "rng_dev.hpp"
 #include "dev_common.cuh"
 #include "ops.cuh"
 
@@ -545,6 +546,43 @@ __global__ void eres_kernel(const double* __restrict__ Y, const double* __restri
   }
 }
 
+// SparseSignEmbedding columns (sketch.hpp:31-49) from the raw draws of the
+// embedding stream: column c consumes draws [2 x c, 2 x c + 2 x) -- x for
+// Floyd's below(t + 1) picks, x for the signs -- exactly as the sequential
+// construction does whenever below() accepts every draw; a rejected draw
+// (probability < s / 2^64 per draw) raises *bad and the host redoes the
+// embedding sequentially.
+__global__ void ss_columns_kernel(const std::uint64_t* __restrict__ raw, long long ncols, int s, int x,
+                                  int* __restrict__ rows, signed char* __restrict__ sg, int* __restrict__ bad) {
+  const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  const std::uint64_t* d = raw + c * 2 * x;
+  int pick[64];
+  int cnt = 0;
+  for (int t = s - x; t < s; ++t) {
+    const std::uint64_t nn = static_cast<std::uint64_t>(t) + 1;
+    const std::uint64_t v = d[cnt];
+    if (!(v < ~0ULL - (~0ULL % nn))) atomicExch(bad, 1);
+    const int r = static_cast<int>(v % nn);
+    bool dup = false;
+    for (int q = 0; q < cnt; ++q) dup = dup || pick[q] == r;
+    pick[cnt++] = dup ? t : r;
+  }
+  for (int q = 1; q < cnt; ++q) {  // insertion sort (distinct values)
+    const int key = pick[q];
+    int p = q - 1;
+    while (p >= 0 && pick[p] > key) {
+      pick[p + 1] = pick[p];
+      --p;
+    }
+    pick[p + 1] = key;
+  }
+  for (int q = 0; q < x; ++q) {
+    rows[c * x + q] = pick[q];
+    sg[c * x + q] = static_cast<signed char>((d[x + q] & 1ULL) ? 1 : -1);
+  }
+}
+
 // rho probes: out(i, p) = (E w_p)_i with the dense matvec chain (j ascending,
 // zero entries of w skipped), sketch.hpp:219-221 -> matrix.hpp:156-162.
 // Each output is one sequential chain of n DMUL+DADD (the reference order).
@@ -951,7 +989,26 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
     };
     HostRng rng(emb_seed);
     bool ok = x <= 64;
-    if (ok) {
+    // device path: the raw stream and the columns are produced on the GPU
+    DBuf<int> d_rows;
+    DBuf<signed char> d_sg;
+    bool on_device = false;
+    if (ok && mt64_device_ok() && !std::getenv("APC_HOST_EMBEDDING")) {
+      DBuf<std::uint64_t> raw(mt_ * 2 * x);
+      DBuf<int> bad(1);
+      APC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+      mt64_stream_device(ctx_, splitmix(emb_seed), mt_ * 2 * x, raw.p);
+      d_rows.alloc(mt_ * x);
+      d_sg.alloc(mt_ * x);
+      ss_columns_kernel<<<nb(mt_), kT, 0, st>>>(raw.p, mt_, static_cast<int>(s_), static_cast<int>(x), d_rows.p,
+                                               d_sg.p, bad.p);
+      ctx_->launches++;
+      int hb = 0;
+      copy_sync(st, &hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost);
+      on_device = hb == 0;
+      ok = on_device;  // a rejected draw: redo sequentially below
+    }
+    if (ok && !on_device) {
       std::vector<std::uint64_t> raw(static_cast<size_t>(mt_ * 2 * x));
       for (auto& d : raw) d = rng.bits();
       std::vector<char> bad(static_cast<size_t>(std::max<i64>(1, mt_)), 0);
@@ -978,10 +1035,10 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
     }
     const double scale = 1.0 / std::sqrt(static_cast<double>(x));
     embed_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
-    DBuf<int> d_rows;
-    DBuf<signed char> d_sg;
-    upload(ctx_, d_rows, rows.data(), mt_ * x);
-    upload(ctx_, d_sg, sg.data(), mt_ * x);
+    if (!on_device) {
+      upload(ctx_, d_rows, rows.data(), mt_ * x);
+      upload(ctx_, d_sg, sg.data(), mt_ * x);
+    }
     APC_CUDA(cudaEventRecord(ev0, st));
     const double mu_scale = amu_ * scale;  // mu * scale_ * ss[q] (sketch.hpp:158)
     const int aug = amu_ > 0.0 ? 1 : 0;
@@ -1090,6 +1147,8 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
   colsel_.alloc(std::max<i64>(1, n_));
   APC_CUDA(cudaMemsetAsync(rowsel_.p, 0, rowsel_.bytes(), st));
   APC_CUDA(cudaMemsetAsync(colsel_.p, 0, colsel_.bytes(), st));
+  SetupProf::add("init.embed", embed_ms_);
+  SetupProf::add("init.sketch_kernel", sketch_ms_);
 }
 
 DeviceCur::~DeviceCur() = default;

@@ -102,3 +102,18 @@ def test_block_equal_to_columns_selects_all(apc, ctx):
     assert added == 4
     cur.refresh()
     assert sorted(cur.indices()[1]) == [0, 1, 2, 3]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed,stream,index,count", [(7, -1, 0, 5000), (20260417, 1, 0, 313), (3, 2, 9, 1)])
+def test_device_rng_stream_matches_host(apc, ctx, seed, stream, index, count):
+    # the embedding's raw std::mt19937_64 stream generated on the device (rng_dev.cu)
+    import ctypes as C
+
+    lib = apc.load_library()
+    host = np.zeros(count, dtype=np.uint64)
+    lib.apc_rng_fill(seed, stream, index, 0, 0, count, host.ctypes.data_as(C.c_void_p))
+    dev = np.zeros(count, dtype=np.uint64)
+    assert lib.apc_rng_fill_device(ctx.h, seed, stream, index, count,
+                                   dev.ctypes.data_as(C.POINTER(C.c_uint64))) == 0
+    assert np.array_equal(host, dev)
