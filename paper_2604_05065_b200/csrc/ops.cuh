@@ -23,7 +23,10 @@
 namespace apc {
 
 constexpr int kDenseFwdThreads = 256;
-constexpr int kDenseFwdRowsPerThread = 2;
+#ifndef APC_DENSE_FWD_R
+#define APC_DENSE_FWD_R 8
+#endif
+constexpr int kDenseFwdRowsPerThread = APC_DENSE_FWD_R;
 constexpr int kDenseFwdTile = kDenseFwdThreads * kDenseFwdRowsPerThread;
 constexpr int kDenseAdjThreads = 256;
 constexpr int kDenseAdjCols = 16;  // 8 warps x 2 columns
@@ -57,56 +60,73 @@ dense_fwd_kernel(const double* __restrict__ A, long long ld, long long mloc, lon
                  const double* __restrict__ x, long long cols_per_split,
                  double* __restrict__ part, unsigned* __restrict__ tile_ctr, const int* done,
                  Epi epi) {
+  constexpr int R = kDenseFwdRowsPerThread;
   __shared__ double red[32];
   if (done && *done) return;
   const int nsplit = gridDim.y;
   const long long tile = blockIdx.x;
-  const long long r0 = tile * kDenseFwdTile + threadIdx.x;
-  const long long r1 = r0 + kDenseFwdThreads;
   const long long c0 = blockIdx.y * cols_per_split;
   const long long c1 = c0 + cols_per_split < n ? c0 + cols_per_split : n;
-  double acc0 = 0.0, acc1 = 0.0;
-  const bool ok0 = r0 < mloc, ok1 = r1 < mloc;
-  // epilogue inputs fetched up front (the split that finishes last uses them)
-  const double pre0 = ok0 ? epi.load(r0) : 0.0, pre1 = ok1 ? epi.load(r1) : 0.0;
-  const double* a0 = A + r0;
-  const double* a1 = A + r1;
+  // R rows per thread, kDenseFwdThreads apart: per column the CTA reads one
+  // contiguous R x 2 KB segment
+  long long r[R];
+  bool ok[R];
+  double acc[R], pre[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    r[k] = tile * kDenseFwdTile + threadIdx.x + k * kDenseFwdThreads;
+    ok[k] = r[k] < mloc;
+    acc[k] = 0.0;
+    // epilogue inputs fetched up front (the split that finishes last uses them)
+    pre[k] = ok[k] ? epi.load(r[k]) : 0.0;
+  }
+  const double* ab = A + tile * kDenseFwdTile + threadIdx.x;
   long long c = c0;
-  if (ok1) {
+  if (ok[R - 1]) {
     for (; c + 4 <= c1; c += 4) {
-      double x0 = __ldg(x + c), x1 = __ldg(x + c + 1), x2 = __ldg(x + c + 2), x3 = __ldg(x + c + 3);
-      double p0 = __ldg(a0 + c * ld), p1 = __ldg(a0 + (c + 1) * ld);
-      double p2 = __ldg(a0 + (c + 2) * ld), p3 = __ldg(a0 + (c + 3) * ld);
-      double q0 = __ldg(a1 + c * ld), q1 = __ldg(a1 + (c + 1) * ld);
-      double q2 = __ldg(a1 + (c + 2) * ld), q3 = __ldg(a1 + (c + 3) * ld);
-      acc0 += p0 * x0; acc1 += q0 * x0;
-      acc0 += p1 * x1; acc1 += q1 * x1;
-      acc0 += p2 * x2; acc1 += q2 * x2;
-      acc0 += p3 * x3; acc1 += q3 * x3;
+      double xv[4], av[4][R];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) xv[u] = __ldg(x + c + u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < R; ++k) av[u][k] = __ldg(ab + (c + u) * ld + k * kDenseFwdThreads);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < R; ++k) acc[k] += av[u][k] * xv[u];
     }
     for (; c < c1; ++c) {
-      double xc = __ldg(x + c);
-      acc0 += __ldg(a0 + c * ld) * xc;
-      acc1 += __ldg(a1 + c * ld) * xc;
+      const double xc = __ldg(x + c);
+#pragma unroll
+      for (int k = 0; k < R; ++k) acc[k] += __ldg(ab + c * ld + k * kDenseFwdThreads) * xc;
     }
-  } else if (ok0) {
-    for (; c < c1; ++c) acc0 += __ldg(a0 + c * ld) * __ldg(x + c);
+  } else {
+    for (; c < c1; ++c) {
+      const double xc = __ldg(x + c);
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        if (ok[k]) acc[k] += __ldg(ab + c * ld + k * kDenseFwdThreads) * xc;
+    }
   }
   if (nsplit > 1) {
-    if (ok0) part[blockIdx.y * mloc + r0] = acc0;
-    if (ok1) part[blockIdx.y * mloc + r1] = acc1;
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (ok[k]) part[blockIdx.y * mloc + r[k]] = acc[k];
     if (!elect_last_block(tile_ctr + tile, nsplit)) return;
-    acc0 = 0.0;
-    acc1 = 0.0;
-    for (int s = 0; s < nsplit; ++s) {
-      if (ok0) acc0 += ((volatile double*)part)[s * mloc + r0];
-      if (ok1) acc1 += ((volatile double*)part)[s * mloc + r1];
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] = 0.0;
+    for (int sp = 0; sp < nsplit; ++sp) {
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        if (ok[k]) acc[k] += ((volatile double*)part)[sp * mloc + r[k]];
     }
   }
   epi.begin();
   double sq = 0.0;
-  if (ok0) sq += epi.row(r0, acc0, pre0);
-  if (ok1) sq += epi.row(r1, acc1, pre1);
+#pragma unroll
+  for (int k = 0; k < R; ++k)
+    if (ok[k]) sq += epi.row(r[k], acc[k], pre[k]);
   sq = block_sum<kDenseFwdThreads>(sq, red);
   epi.tile_done(static_cast<unsigned>(tile), gridDim.x, sq);
 }
