@@ -55,7 +55,7 @@ struct FwdStore {  // y = A x
 // grid = (ntiles, nsplit); part: nsplit x mloc partials; tile_ctr: ntiles counters
 // ---------------------------------------------------------------------------
 template <class Epi>
-__global__ void __launch_bounds__(kDenseFwdThreads)
+__global__ void __launch_bounds__(kDenseFwdThreads, 4)
 dense_fwd_kernel(const double* __restrict__ A, long long ld, long long mloc, long long n,
                  const double* __restrict__ x, long long cols_per_split,
                  double* __restrict__ part, unsigned* __restrict__ tile_ctr, const int* done,
@@ -71,14 +71,12 @@ dense_fwd_kernel(const double* __restrict__ A, long long ld, long long mloc, lon
   // contiguous R x 2 KB segment
   long long r[R];
   bool ok[R];
-  double acc[R], pre[R];
+  double acc[R];
 #pragma unroll
   for (int k = 0; k < R; ++k) {
     r[k] = tile * kDenseFwdTile + threadIdx.x + k * kDenseFwdThreads;
     ok[k] = r[k] < mloc;
     acc[k] = 0.0;
-    // epilogue inputs fetched up front (the split that finishes last uses them)
-    pre[k] = ok[k] ? epi.load(r[k]) : 0.0;
   }
   const double* ab = A + tile * kDenseFwdTile + threadIdx.x;
   long long c = c0;
@@ -109,18 +107,27 @@ dense_fwd_kernel(const double* __restrict__ A, long long ld, long long mloc, lon
         if (ok[k]) acc[k] += __ldg(ab + c * ld + k * kDenseFwdThreads) * xc;
     }
   }
+  double pre[R];  // epilogue inputs (loaded only by the CTA that finishes the tile; in flight
+                 // while the split partials are summed)
   if (nsplit > 1) {
 #pragma unroll
     for (int k = 0; k < R; ++k)
       if (ok[k]) part[blockIdx.y * mloc + r[k]] = acc[k];
     if (!elect_last_block(tile_ctr + tile, nsplit)) return;
 #pragma unroll
-    for (int k = 0; k < R; ++k) acc[k] = 0.0;
+    for (int k = 0; k < R; ++k) {
+      pre[k] = ok[k] ? epi.load(r[k]) : 0.0;
+      acc[k] = 0.0;
+    }
     for (int sp = 0; sp < nsplit; ++sp) {
 #pragma unroll
       for (int k = 0; k < R; ++k)
         if (ok[k]) acc[k] += ((volatile double*)part)[sp * mloc + r[k]];
     }
+  }
+  else {
+#pragma unroll
+    for (int k = 0; k < R; ++k) pre[k] = ok[k] ? epi.load(r[k]) : 0.0;
   }
   epi.begin();
   double sq = 0.0;
