@@ -527,6 +527,159 @@ __global__ void core_solve_cols_kernel(const double* __restrict__ R, double* __r
   }
 }
 
+// Same product, warp per column: y = R(:, j) lives in registers, lane k
+// holding rows [k KP, (k + 1) KP).  Every reduction keeps the reference's
+// sequential order by walking the lanes in order (a running value handed on
+// with one shuffle per lane, each lane adding its rows in order); the
+// elementwise updates (y -= d v) are lane-parallel.  The chains are bound by
+// FP64 latency (~9-18 cycles per step) instead of one memory round trip per
+// step as in the thread-per-column kernel above.  fat: the factor transposed
+// (row-major), so a lane's run of one row is contiguous.
+template <int KP>
+__global__ void __launch_bounds__(128)
+core_solve_warp_kernel(const double* __restrict__ R, double* __restrict__ H, int l, long long n, int kind,
+                       const double* __restrict__ hh, const double* __restrict__ fat,
+                       const long long* __restrict__ perm) {
+  const long long j = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  const int base = lane * KP;
+  double y[KP];
+#pragma unroll
+  for (int e = 0; e < KP; ++e) {
+    const int i = base + e;
+    y[e] = i < l ? R[(kind == 0 ? static_cast<long long>(i) : perm[i]) * n + j] : 0.0;
+  }
+  const int lastlane = (l - 1) / KP;
+  if (kind == 0) {
+    for (int t = 0; t < l; ++t) {  // y <- Q^T y (dense_factor.hpp:75-83)
+      const double* v = hh + static_cast<long long>(t) * l;
+      double vr[KP];
+#pragma unroll
+      for (int e = 0; e < KP; ++e) {
+        const int i = base + e;
+        vr[e] = (i >= t && i < l) ? __ldg(v + i) : 0.0;
+      }
+      // d = sum_{i >= t} v_i y_i in index order: lanes t/KP .. lastlane in turn
+      double d = 0.0;
+      for (int k = t / KP; k <= lastlane; ++k) {
+        if (lane == k) {
+#pragma unroll
+          for (int e = 0; e < KP; ++e) {
+            const int i = base + e;
+            if (i >= t && i < l) d += vr[e] * y[e];
+          }
+        }
+        d = __shfl_sync(0xffffffffu, d, k);
+      }
+      d *= 2.0;
+#pragma unroll
+      for (int e = 0; e < KP; ++e) {
+        const int i = base + e;
+        if (i >= t && i < l) y[e] -= d * vr[e];
+      }
+    }
+    for (int i = l - 1; i >= 0; --i) {  // back substitution, q = i+1 .. l-1 ascending
+      const int li = i / KP, ei = i % KP;
+      const double* row = fat + static_cast<long long>(i) * l;  // row i of the factor
+      double fr[KP];
+#pragma unroll
+      for (int e = 0; e < KP; ++e) {
+        const int q = base + e;
+        fr[e] = (q > i && q < l) ? __ldg(row + q) : 0.0;
+      }
+      double sacc = 0.0;
+#pragma unroll
+      for (int e = 0; e < KP; ++e)
+        if (e == ei) sacc = y[e];
+      sacc = __shfl_sync(0xffffffffu, sacc, li);
+      for (int k = li; k <= lastlane; ++k) {
+        if (lane == k) {
+#pragma unroll
+          for (int e = 0; e < KP; ++e) {
+            const int q = base + e;
+            if (q > i && q < l) sacc -= fr[e] * y[e];
+          }
+        }
+        sacc = __shfl_sync(0xffffffffu, sacc, k);
+      }
+      if (lane == li) {
+        const double dv = __ldg(row + i);
+#pragma unroll
+        for (int e = 0; e < KP; ++e)
+          if (e == ei) y[e] = sacc / dv;
+      }
+    }
+  } else {
+    for (int i = 1; i < l; ++i) {  // forward: y_i -= L(i, q) y_q, q = 0 .. i-1 ascending
+      const int li = i / KP, ei = i % KP;
+      const double* row = fat + static_cast<long long>(i) * l;
+      double fr[KP];
+#pragma unroll
+      for (int e = 0; e < KP; ++e) {
+        const int q = base + e;
+        fr[e] = q < i ? __ldg(row + q) : 0.0;
+      }
+      double r = 0.0;
+#pragma unroll
+      for (int e = 0; e < KP; ++e)
+        if (e == ei) r = y[e];
+      r = __shfl_sync(0xffffffffu, r, li);
+      for (int k = 0; k <= li; ++k) {
+        if (lane == k) {
+#pragma unroll
+          for (int e = 0; e < KP; ++e) {
+            const int q = base + e;
+            if (q < i) r -= fr[e] * y[e];
+          }
+        }
+        r = __shfl_sync(0xffffffffu, r, k);
+      }
+      if (lane == li) {
+#pragma unroll
+        for (int e = 0; e < KP; ++e)
+          if (e == ei) y[e] = r;
+      }
+    }
+    for (int i = l - 1; i >= 0; --i) {  // back: y_i -= U(i, q) y_q, q ascending; y_i /= U(i, i)
+      const int li = i / KP, ei = i % KP;
+      const double* row = fat + static_cast<long long>(i) * l;
+      double fr[KP];
+#pragma unroll
+      for (int e = 0; e < KP; ++e) {
+        const int q = base + e;
+        fr[e] = (q > i && q < l) ? __ldg(row + q) : 0.0;
+      }
+      double r = 0.0;
+#pragma unroll
+      for (int e = 0; e < KP; ++e)
+        if (e == ei) r = y[e];
+      r = __shfl_sync(0xffffffffu, r, li);
+      for (int k = li; k <= lastlane; ++k) {
+        if (lane == k) {
+#pragma unroll
+          for (int e = 0; e < KP; ++e) {
+            const int q = base + e;
+            if (q > i && q < l) r -= fr[e] * y[e];
+          }
+        }
+        r = __shfl_sync(0xffffffffu, r, k);
+      }
+      if (lane == li) {
+        const double dv = __ldg(row + i);
+#pragma unroll
+        for (int e = 0; e < KP; ++e)
+          if (e == ei) y[e] = r / dv;
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < KP; ++e) {
+    const int i = base + e;
+    if (i < l) H[static_cast<long long>(i) * n + j] = y[e];
+  }
+}
+
 // lanes over sketch rows i, one warp per column j: E(i,j) = Y(i,j) - sum_t H(t,j) SC(i,t)
 __global__ void eres_kernel(const double* __restrict__ Y, const double* __restrict__ SC,
                             const double* __restrict__ H, long long s, long long n, long long l,
@@ -1331,8 +1484,24 @@ void DeviceCur::refresh() {
   // H = U R (core solve per column)
   upload_core();
   H_.ensure(l * n_);
-  core_solve_cols_kernel<<<nb(n_, 128), 128, 0, st>>>(Rrm_.p, H_.p, l, n_, core_kind_, core_h_.p, core_a_.p,
-                                                      core_perm_.p);
+  // warp per column wins when there are few columns (latency-bound chains,
+  // C1: n = 500); with many columns the FP64 pipe is the limit and a thread
+  // per column issues 32x fewer predicated instructions (C2/C3: n >= 10^4)
+  if (l <= 1024 && n_ <= 4096 && !std::getenv("APC_CORE_SOLVE_THREAD")) {
+    const unsigned g = static_cast<unsigned>((n_ * 32 + 127) / 128);
+    const int li = static_cast<int>(l);
+    if (l <= 128)
+      core_solve_warp_kernel<4><<<g, 128, 0, st>>>(Rrm_.p, H_.p, li, n_, core_kind_, core_h_.p, core_at_.p, core_perm_.p);
+    else if (l <= 256)
+      core_solve_warp_kernel<8><<<g, 128, 0, st>>>(Rrm_.p, H_.p, li, n_, core_kind_, core_h_.p, core_at_.p, core_perm_.p);
+    else if (l <= 512)
+      core_solve_warp_kernel<16><<<g, 128, 0, st>>>(Rrm_.p, H_.p, li, n_, core_kind_, core_h_.p, core_at_.p, core_perm_.p);
+    else
+      core_solve_warp_kernel<32><<<g, 128, 0, st>>>(Rrm_.p, H_.p, li, n_, core_kind_, core_h_.p, core_at_.p, core_perm_.p);
+  } else {
+    core_solve_cols_kernel<<<nb(n_, 128), 128, 0, st>>>(Rrm_.p, H_.p, l, n_, core_kind_, core_h_.p, core_a_.p,
+                                                        core_perm_.p);
+  }
   // E^row = Y - Y(:, J) H
   DBuf<double> d_sc(s_ * l);
   gather_sc_kernel<<<nb(s_ * l), kT, 0, st>>>(Y_.p, s_, d_J.p, l, d_sc.p);
@@ -1349,10 +1518,13 @@ void DeviceCur::upload_core() {
   if (core_.kind == 0) {
     upload(ctx_, core_h_, core_.qr.hh.data(), l * l);
     upload(ctx_, core_a_, core_.qr.a.data(), l * l);
+    core_at_host_ = transpose(l, l, core_.qr.a);
   } else {
     upload(ctx_, core_a_, core_.lu.data(), l * l);
     upload(ctx_, core_perm_, reinterpret_cast<const long long*>(core_.perm.data()), l);
+    core_at_host_ = transpose(l, l, core_.lu);
   }
+  upload(ctx_, core_at_, core_at_host_.data(), l * l);
 }
 
 // G = C^T C of the target's selected columns (l x l, full), on the device:

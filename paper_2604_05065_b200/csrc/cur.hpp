@@ -101,6 +101,8 @@ class DeviceCur {
   DBuf<double> Rrm_;          // R = A(I,:) row-major, capacity max_rank x n
   DBuf<double> H_;            // U R row-major l x n
   DBuf<double> core_a_, core_h_;  // factor payload (l x l)
+  DBuf<double> core_at_;          // the factor transposed (row-major), for the warp-per-column solve
+  Vec core_at_host_;              // its host staging copy (alive until the async upload completes)
   DBuf<long long> core_perm_;
   DBuf<double> work_;         // generic scratch
   DBuf<int> rowsel_, colsel_;  // flags (rows in I, cols in J)

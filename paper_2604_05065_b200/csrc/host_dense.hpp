@@ -29,6 +29,21 @@ struct Householder {
   Vec a, hh;
 };
 
+struct HhTrailing {  // columns j+1+[b, e) <- (I - 2 v v^T) columns (named functor: see host_parallel_for)
+  double* a;
+  const double* v;
+  i64 m, j;
+  void operator()(i64 b, i64 e) const {
+    for (i64 jj = j + 1 + b; jj < j + 1 + e; ++jj) {
+      double* c = a + jj * m;
+      double d = 0.0;
+      for (i64 i = j; i < m; ++i) d += v[i] * c[i];
+      d *= 2.0;
+      for (i64 i = j; i < m; ++i) c[i] -= d * v[i];
+    }
+  }
+};
+
 inline Householder householder(i64 m, i64 k, Vec buf) {
   Householder f;
   f.m = m;
@@ -52,13 +67,8 @@ inline Householder householder(i64 m, i64 k, Vec buf) {
     for (i64 i = j; i < m; ++i) v[i] /= vn;
     col[j] = alpha;
     for (i64 i = j + 1; i < m; ++i) col[i] = 0.0;
-    for (i64 jj = j + 1; jj < k; ++jj) {
-      double* c = f.a.data() + jj * m;
-      double d = 0.0;
-      for (i64 i = j; i < m; ++i) d += v[i] * c[i];
-      d *= 2.0;
-      for (i64 i = j; i < m; ++i) c[i] -= d * v[i];
-    }
+    // trailing columns are independent: same per-column chain on any core
+    host_parallel_for(k - j - 1, HhTrailing{f.a.data(), v, m, j}, m - j);
   }
   return f;
 }
@@ -364,6 +374,19 @@ inline SvdH small_svd(i64 m, i64 n, const Vec& mat) {
 // ---------------------------------------------------------------------------
 // CoreFactor: factor of the l x l intersection block A(I, J) (cur.hpp:53-197)
 // ---------------------------------------------------------------------------
+struct LuTrailing {  // rows k+1+[b, e) of the LU elimination step k (independent rows)
+  double* lu;
+  i64 l, k;
+  double piv;
+  void operator()(i64 b, i64 e) const {
+    for (i64 i = k + 1 + b; i < k + 1 + e; ++i) {
+      const double fac = lu[k * l + i] / piv;
+      lu[k * l + i] = fac;
+      for (i64 j = k + 1; j < l; ++j) lu[j * l + i] -= fac * lu[j * l + k];
+    }
+  }
+};
+
 struct CoreFactorH {
   i64 l = 0;
   int kind = 0;  // 0 Householder QR, 1 LU with partial pivoting
@@ -410,11 +433,7 @@ struct CoreFactorH {
       dmax = std::max(dmax, std::fabs(piv));
       dmin = std::min(dmin, std::fabs(piv));
       if (piv == 0.0) fail(APC_SINGULAR, "CoreFactor: intersection block numerically singular");
-      for (i64 i = k + 1; i < l; ++i) {
-        const double fac = f.lu[k * l + i] / piv;
-        f.lu[k * l + i] = fac;
-        for (i64 j = k + 1; j < l; ++j) f.lu[j * l + i] -= fac * f.lu[j * l + k];
-      }
+      host_parallel_for(l - k - 1, LuTrailing{f.lu.data(), l, k, piv}, l - k);
     }
     if (!(dmin > 1e-14 * dmax))
       fail(APC_SINGULAR, "CoreFactor: intersection block numerically singular");

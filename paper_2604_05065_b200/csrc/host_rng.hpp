@@ -71,48 +71,30 @@ class HostRng {
   std::mt19937_64 eng_;
 };
 
-// run f(begin, end) over [0, n) on the host's cores when the total work
-// (n * unit_cost, in rough flop units) is worth the thread start-up;
-// exceptions thrown by f are rethrown on the calling thread.
+// run f(begin, end) over [0, n) on the host's cores (a persistent worker pool,
+// host_pool.cpp) when the total work (n * unit_cost, rough flop units) is
+// worth it; exceptions thrown by f are rethrown on the calling thread.
 // NOTE: this header is compiled both by nvcc (.cu) and g++ (.cpp).  Closure
 // types of capturing lambdas are not guaranteed to have the same layout
-// under both front ends, and the inline instantiations are merged by the
-// linker -- so callers in shared headers pass named functors, and the worker
-// below is a named struct, never a lambda.
+// under both front ends while inline instantiations are merged by the
+// linker, so callers in shared headers pass named functors, never lambdas.
+int host_pool_workers();
+void host_pool_run(i64 n, int nt, void (*fn)(void*, i64, i64), void* ctx);
+
 template <class F>
-struct HostRangeWorker {
-  const F* f;
-  i64 b, e;
-  std::exception_ptr* err;
-  void operator()() const {
-    try {
-      (*f)(b, e);
-    } catch (...) {
-      *err = std::current_exception();
-    }
-  }
-};
+void host_range_invoke(void* ctx, i64 b, i64 e) {
+  (*static_cast<const F*>(ctx))(b, e);
+}
 
 template <class F>
 void host_parallel_for(i64 n, const F& f, i64 unit_cost = 1) {
-  unsigned hc = std::thread::hardware_concurrency();
-  const i64 nt = std::max<i64>(1, std::min<i64>({static_cast<i64>(hc ? hc : 1), 32, n}));
   static const bool serial = std::getenv("APC_HOST_SERIAL") != nullptr;
-  if (serial || n * unit_cost < 1000000 || n < 2 || nt == 1) {
+  const i64 nt = std::min<i64>(host_pool_workers() + 1, n);
+  if (serial || n * unit_cost < 30000 || nt < 2) {
     f(i64{0}, n);
     return;
   }
-  std::vector<std::thread> th;
-  std::vector<std::exception_ptr> err(static_cast<size_t>(nt));
-  const i64 chunk = (n + nt - 1) / nt;
-  for (i64 t = 0; t < nt; ++t) {
-    const i64 b = t * chunk, e = std::min(n, b + chunk);
-    if (b >= e) break;
-    th.emplace_back(HostRangeWorker<F>{&f, b, e, &err[static_cast<size_t>(t)]});
-  }
-  for (auto& x : th) x.join();
-  for (auto& x : err)
-    if (x) std::rethrow_exception(x);
+  host_pool_run(n, static_cast<int>(nt), &host_range_invoke<F>, const_cast<void*>(static_cast<const void*>(&f)));
 }
 
 // n Gaussians of the stream (each consumes exactly two draws), transformed in parallel

@@ -1,4 +1,4 @@
-"""Short capped solve of a BASELINE config (profiling driver): prof_cfg.py CONFIG CAP"""
+"""Short capped solve of a BASELINE config (profiling driver): prof_cfg.py CONFIG CAP [REPS]"""
 import sys
 from pathlib import Path
 
@@ -16,7 +16,9 @@ cfgid, cap = int(sys.argv[1]), int(sys.argv[2])
 ctx = apc.Context(0)
 p = apc.Problem(cfgid)
 A = apc.DeviceMatrix.from_problem(ctx, p)
-r = apc.aplicur_solve(A, p.b, apc.SolverConfig(lsqr_cap=cap, trace_sample_stride=0, **SOLVER[cfgid]))
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2  # the last solve is reported (the first pays one-time init)
+for _ in range(reps):
+    r = apc.aplicur_solve(A, p.b, apc.SolverConfig(lsqr_cap=cap, trace_sample_stride=0, **SOLVER[cfgid]))
 print("setup_ms", r.setup_ms, "lsqr_ms", r.lsqr_ms, "iters", r.lsqr_iters,
       [(ph.rank, ph.lsqr_iters, round(ph.t_lsqr_device_ms, 1),
         round(ph.t_lsqr_device_ms * 1e3 / max(1, ph.lsqr_iters), 1)) for ph in r.phases], flush=True)
