@@ -121,6 +121,42 @@ def run_reference(args):
     print(json.dumps(out))
 
 
+def hbm_operator_pair(apc, ctx, cfg_id, reps=20):
+    """Live A*v + A^T*u timing on an HBM-bound BASELINE config (CUDA events on the
+    library stream), against SURVEY 8(d)'s algorithmic bytes."""
+    import torch
+
+    p = apc.Problem(cfg_id)
+    A = apc.DeviceMatrix.from_problem(ctx, p)
+    dev = torch.device("cuda", ctx.device)
+    x = torch.randn(p.n, dtype=torch.float64, device=dev)
+    y = torch.empty(p.m, dtype=torch.float64, device=dev)
+    g = torch.empty(p.n, dtype=torch.float64, device=dev)
+    s = torch.cuda.ExternalStream(ctx.stream)
+    for _ in range(3):
+        A.apply_dev(x.data_ptr(), y.data_ptr())
+        A.apply_dev(y.data_ptr(), g.data_ptr(), transpose=True)
+    ctx.sync()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record(s)
+    for _ in range(reps):
+        A.apply_dev(x.data_ptr(), y.data_ptr())
+    ev[1].record(s)
+    for _ in range(reps):
+        A.apply_dev(y.data_ptr(), g.data_ptr(), transpose=True)
+    ev[2].record(s)
+    ctx.sync()
+    tf = ev[0].elapsed_time(ev[1]) / reps * 1e-3
+    ta = ev[1].elapsed_time(ev[2]) / reps * 1e-3
+    if p.sparse:
+        byts = 24 * p.nnz + 4 * (p.m + 1) + 4 * (p.n + 1) + 16 * (p.m + p.n)
+    else:
+        byts = 16 * p.m * p.n + 16 * (p.m + p.n)
+    A.free()
+    del p
+    return {"fwd_us": tf * 1e6, "adj_us": ta * 1e6, "bytes": byts, "GBps": byts / (tf + ta) / 1e9}
+
+
 def cpu_time_to_tol(ref, rp, p, sample_iters=1200):
     """Reference aplicur_solve with lsqr_cap = sample_iters (identical sketch, CUR
     indices and preconditioners as the full run) -> measured setup + measured
@@ -156,6 +192,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-sample-iters", type=int, default=1200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-hbm-pairs", action="store_true",
+                    help="skip the live C3/C5 operator-pair measurement (HBM-bound configs) in the roofline")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -298,6 +336,19 @@ def main():
                 "note": "C2's CSR pair (52.4 MB) is L2-resident on B200 (126 MB L2): the loop is latency-bound, not "
                         "HBM-bound; the HBM-bound operator numbers (C3/C4/C5) are in profiles/r1_summary.md",
                 "peak_source": "MEASURED_PEAKS.json" if "fallback" not in peaks else "fallback"}
+
+    if rank == 0 and ws == 1 and not args.no_hbm_pairs:
+        # the C2 loop is L2-resident; the HBM roofline of the same operator
+        # kernels is measured live on the HBM-bound configs
+        pairs = {}
+        for cid, name in ((3, "C3 dense 100000x10000"), (5, "C5 sparse 8e6x4e5 nnz 1.28e8")):
+            try:
+                d = hbm_operator_pair(apc, ctx, cid)
+                d["frac"] = d["GBps"] / hbm
+                pairs[name] = d
+            except Exception as e:  # reported, never required
+                pairs[name] = {"unavailable": str(e)}
+        roofline["hbm_operator_pairs"] = pairs
 
     out = {
         "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,
