@@ -324,8 +324,15 @@ def main():
     per_launch_bytes = bytes_pair * loop_iters / max(loop_launches, 1)
     loop_achieved = bytes_pair * loop_iters / (loop_ms / 1e3) / 1e9 if loop_ms > 0 else 0.0
     hbm = peaks.get("hbm_gbs", 6650.0)
+    # DRAM bytes per iteration of lsqr_persistent_kernel from one `ncu --set full`
+    # capture (profiles/r1_ncu_persistent_c2.txt: 52.06 MB read + 0.73 MB written
+    # over a 300-iteration launch), scaled to this run's average launch
+    dram_per_iter = (52058368 + 733952) / 300.0
     roofline = {"bound": "hbm", "achieved": loop_achieved, "peak": hbm, "unit": "GB/s",
-                "frac": loop_achieved / hbm, "traffic": None,
+                "frac": loop_achieved / hbm,
+                "traffic": dram_per_iter * loop_iters / max(loop_launches, 1),
+                "traffic_note": "ncu DRAM bytes per launch (per-iteration figure x iterations per launch): far "
+                                "below the algorithmic bytes because A, A^T and every vector stay in L2",
                 "kernel": "lsqr_persistent_kernel (whole LSQR phase: A*z + A^T*u + preconditioner + updates)",
                 "algorithmic_bytes_per_launch": per_launch_bytes,
                 "algorithmic_bytes_per_iteration": bytes_pair, "iterations": loop_iters,
