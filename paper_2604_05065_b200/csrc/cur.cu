@@ -139,7 +139,7 @@ sketch_ss_csc_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
   SketchSmem sm = sketch_smem(ysh, s, xi, w);
   double* yc = sm.y;
   const int b = cptr[j], e = cptr[j + 1];
-  if (e - b > heavy) return;  // long columns: sketch_ss_heavy_kernel
+  if (e - b > heavy) return;  // long columns: the inverted-index kernels below
   for (int i = lane; i < s; i += 32) yc[i] = 0.0;
   __syncwarp();
   for (int p0 = b; p0 < e; p0 += 32) {
@@ -161,52 +161,6 @@ sketch_ss_csc_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
   }
   __syncwarp();
   for (int i = lane; i < s; i += 32) Y[j * s + i] = yc[i];
-}
-
-// Long CSC columns (C5's Zipf head: up to 7.2M nonzeros): parallel over the
-// sketch rows instead.  Lane i of slab w owns output row 32w + i and walks the
-// column's nonzeros in ascending row order, adding +-scale*A(k, j) whenever
-// row i is one of S(:, k)'s xi rows -- the same per-element chain as the
-// reference, so Y stays bit-identical.  The S columns of each 32-entry chunk
-// are staged in shared memory first (one load round per chunk).
-__global__ void __launch_bounds__(256)
-sketch_ss_heavy_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
-                       const double* __restrict__ cval, const int* __restrict__ heavy_cols, int nheavy,
-                       long long m, int s, int xi, const int* __restrict__ srow,
-                       const signed char* __restrict__ ssgn, double scale, double mu_scale, int aug,
-                       double* __restrict__ Y) {
-  extern __shared__ int hs[];  // 8 warps x 32 x xi rows, then signs
-  const int nslab = (s + 31) / 32;
-  const int w = threadIdx.x >> 5;
-  const long long wid = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (wid >= static_cast<long long>(nheavy) * nslab) return;
-  int* rs = hs + w * 32 * xi;
-  signed char* sg = reinterpret_cast<signed char*>(hs + 8 * 32 * xi) + w * 32 * xi;
-  const long long j = heavy_cols[wid / nslab];
-  const int i = static_cast<int>(wid % nslab) * 32 + lane;
-  const int b = cptr[j], e = cptr[j + 1];
-  double acc = 0.0;
-  for (int p0 = b; p0 < e; p0 += 32) {
-    const int p = p0 + lane;
-    const double v = p < e ? cval[p] : 0.0;
-    const int k = p < e ? ridx[p] : 0;
-    const int cnt = e - p0 < 32 ? e - p0 : 32;
-    stage_s_rows(srow, ssgn, k, p < e, xi, lane, rs, sg);
-    for (int q = 0; q < cnt; ++q) {
-      const double vk = __shfl_sync(0xffffffffu, v, q);
-      const double sv = scale * vk;
-      for (int t = 0; t < xi; ++t)
-        if (rs[q * xi + t] == i) acc += sv * static_cast<double>(sg[q * xi + t]);
-    }
-    __syncwarp();
-  }
-  if (aug) {
-    const int* rr = srow + (m + j) * xi;
-    for (int t = 0; t < xi; ++t)
-      if (rr[t] == i) acc += mu_scale * static_cast<double>(ssgn[(m + j) * xi + t]);
-  }
-  if (i < s) Y[j * s + i] = acc;
 }
 
 // Inverted-index sketch for long columns.  The reference's chain for output
