@@ -175,6 +175,41 @@ struct LsqrFwdEpi {  // u <- (A z) - alpha * u/beta ; ||u_top||^2 -> g[n]
   }
 };
 
+// Explicit basis (dense B, n x l column-major): out = x + B s through the dense
+// forward kernel (8 rows per thread, split over the l columns) instead of a
+// thread-per-row chain over l.  mode 0: out_j = x_j + (B s)_j ; mode 1:
+// v_j = (x_j + (B s)_j) - beta v_j, ||v||^2 -> alpha and the rotation (last block).
+struct PcExpandEpi {
+  LsqrPtrs P;
+  const double* x;
+  double* out;
+  int mode;
+  double beta;
+  __device__ void begin() {
+    if (mode == 1) beta = sqrt(P.g[P.n] + P.st->tail_norm2);
+  }
+  __device__ double load(long long j) { return mode == 1 ? P.v[j] : 0.0; }
+  __device__ double row(long long j, double acc, double vj) {
+    const double o = x[j] + acc;
+    if (mode == 0) {
+      out[j] = o;
+      return 0.0;
+    }
+    const double t = o - beta * vj;
+    P.v[j] = t;
+    return t * t;
+  }
+  __device__ void tile_done(unsigned tile, unsigned ntiles, double sq) {
+    if (mode == 0) return;
+    __shared__ double sh[32];
+    if (threadIdx.x == 0) P.epi_part[tile] = sq;
+    if (elect_last_block(P.ctr + 2, ntiles)) {
+      const double s = ordered_sum<256>(P.epi_part, ntiles, sh);
+      if (threadIdx.x == 0) finalize_alpha(P.st, P.trace, sqrt(s), beta);
+    }
+  }
+};
+
 // init: u <- rhs; ||rhs_top||^2 -> g[n] ; ||rhs_tail||^2 -> st->tail_norm2
 __global__ void __launch_bounds__(kVecThreads)
 lsqr_init_copy_kernel(LsqrPtrs P, const double* rhs, long long len, long long off, int tail) {
@@ -414,8 +449,8 @@ struct LsqrWork {
   apc_ctx* ctx = nullptr;
   long long mloc = 0, n = 0, ulen = 0;
   double mu = 0.0;
-  DBuf<double> u, v, w, z, g, h, t, s, fwd_part, tail_part, epi_part, upd_part, pc_part, pers_part;
-  DBuf<unsigned> ctr, pc_ctr;
+  DBuf<double> u, v, w, z, g, h, t, s, fwd_part, tail_part, epi_part, upd_part, pc_part, pers_part, pcf_part;
+  DBuf<unsigned> ctr, pc_ctr, pcf_ctr;
   DBuf<LsqrState> st;
   DBuf<TraceRow> trace;
   LsqrState* hst = nullptr;  // pinned
@@ -495,6 +530,15 @@ void pc_project_core(LsqrWork* w, PrecondDev& p, const double* x, bool transpose
 
 void pc_expand(LsqrWork* w, const LsqrPtrs& P, PrecondDev& p, const double* x, double* out,
                int mode, const int* done) {
+  if (p.kind == 1 && !std::getenv("APC_PC_EXPAND_ROWS")) {
+    const DenseFwdPlan pl = dense_fwd_plan(p.n, p.l, w->ctx->num_sms);
+    dim3 grid(static_cast<unsigned>(pl.ntiles), static_cast<unsigned>(pl.nsplit));
+    dense_fwd_kernel<PcExpandEpi><<<grid, kDenseFwdThreads, 0, w->ctx->stream>>>(
+        p.B.p, p.n, p.n, p.l, w->s.p, pl.cols_per_split, pl.nsplit > 1 ? w->pcf_part.p : nullptr,
+        pl.nsplit > 1 ? w->pcf_ctr.p : nullptr, done, PcExpandEpi{P, x, out, mode, 0.0});
+    w->ctx->launches++;
+    return;
+  }
   pc_expand_kernel<<<nb(w->n), kVecThreads, 0, w->ctx->stream>>>(
       P, p.kind, p.B.p, p.l, p.RT.ptr.p, p.RT.idx.p, p.RT.val.p, w->s.p, x, out, mode, done);
   w->ctx->launches++;
@@ -509,6 +553,12 @@ void ensure_pc_buffers(LsqrWork* w, PrecondDev& p) {
     if (w->pc_ctr.n < pl.ngroups) {
       w->pc_ctr.alloc(pl.ngroups);
       APC_CUDA(cudaMemsetAsync(w->pc_ctr.p, 0, w->pc_ctr.bytes(), w->ctx->stream));
+    }
+    const DenseFwdPlan fp = dense_fwd_plan(p.n, p.l, w->ctx->num_sms);
+    w->pcf_part.ensure(std::max<long long>(1, fp.nsplit * p.n));
+    if (w->pcf_ctr.n < fp.ntiles) {
+      w->pcf_ctr.alloc(fp.ntiles);
+      APC_CUDA(cudaMemsetAsync(w->pcf_ctr.p, 0, w->pcf_ctr.bytes(), w->ctx->stream));
     }
   }
 }

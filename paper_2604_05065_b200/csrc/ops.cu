@@ -204,20 +204,21 @@ unsigned fwd_gs_grid(apc_ctx* ctx, const void* kfn) {
 // ---------------------------------------------------------------------------
 // plans
 // ---------------------------------------------------------------------------
-DenseFwdPlan dense_fwd_plan(const apc_mat& a) {
+DenseFwdPlan dense_fwd_plan(const apc_mat& a) { return dense_fwd_plan(a.mloc(), a.n, a.ctx->num_sms); }
+
+DenseFwdPlan dense_fwd_plan(long long mloc, long long ncols, int num_sms) {
   DenseFwdPlan p;
-  const long long mloc = a.mloc();
   p.ntiles = (mloc + kDenseFwdTile - 1) / kDenseFwdTile;
   if (p.ntiles < 1) p.ntiles = 1;
   // aim for >= 6 CTAs per SM, but keep >= 64 columns per split
-  const long long want = 6LL * a.ctx->num_sms;
+  const long long want = 6LL * num_sms;
   long long ns = (want + p.ntiles - 1) / p.ntiles;
-  long long maxs = std::max<long long>(1, a.n / 64);
+  long long maxs = std::max<long long>(1, ncols / 64);
   ns = std::max<long long>(1, std::min(ns, maxs));
   p.nsplit = std::min<long long>(ns, 65535);
-  p.cols_per_split = (a.n + p.nsplit - 1) / p.nsplit;
+  p.cols_per_split = (ncols + p.nsplit - 1) / p.nsplit;
   if (p.cols_per_split < 1) p.cols_per_split = 1;
-  p.nsplit = (a.n + p.cols_per_split - 1) / p.cols_per_split;
+  p.nsplit = (ncols + p.cols_per_split - 1) / p.cols_per_split;
   if (p.nsplit < 1) p.nsplit = 1;
   return p;
 }

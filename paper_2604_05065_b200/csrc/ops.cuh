@@ -251,6 +251,7 @@ struct DenseFwdPlan {
   long long ntiles, nsplit, cols_per_split;
 };
 DenseFwdPlan dense_fwd_plan(const apc_mat& a);
+DenseFwdPlan dense_fwd_plan(long long mloc, long long ncols, int num_sms);
 struct DenseAdjPlan {
   long long ngroups, msplit, rows_per_split;
 };
