@@ -32,6 +32,10 @@ struct Status : std::runtime_error {
 inline void require(bool cond, int code, const std::string& what, i64 idx = -1) {
   if (!cond) fail(code, what, idx);
 }
+// literal messages: no std::string is built unless the check fails
+inline void require(bool cond, int code, const char* what, i64 idx = -1) {
+  if (!cond) fail(code, what, idx);
+}
 
 void cuda_check(cudaError_t e, const char* what);
 #define APC_CUDA(call) ::apc::cuda_check((call), #call)

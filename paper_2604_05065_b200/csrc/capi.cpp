@@ -231,12 +231,14 @@ int apc_mat_upload_csc(apc_ctx* ctx, int64_t m, int64_t n, const int64_t* colptr
     require(m >= 0 && n >= 0, APC_INVALID_ARGUMENT, "negative matrix shape");
     require(0 <= r0 && r0 <= r1 && r1 <= m, APC_INVALID_ARGUMENT, "apc_mat_upload_csc: bad row range");
     require(colptr[0] == 0, APC_INVALID_ARGUMENT, "apc_mat_upload_csc: colptr[0] != 0");
+    // validation (messages built only on failure: a std::string per entry
+    // would cost more than the whole upload)
     for (i64 j = 0; j < n; ++j) {
-      require(colptr[j + 1] >= colptr[j], APC_INVALID_ARGUMENT, "apc_mat_upload_csc: colptr not monotone", j);
+      if (colptr[j + 1] < colptr[j]) fail(APC_INVALID_ARGUMENT, "apc_mat_upload_csc: colptr not monotone", j);
       for (i64 k = colptr[j]; k < colptr[j + 1]; ++k) {
-        require(rowidx[k] >= 0 && rowidx[k] < m, APC_INVALID_ARGUMENT, "Matrix::sparse: entry out of range", k);
-        require(k == colptr[j] || rowidx[k] > rowidx[k - 1], APC_INVALID_ARGUMENT,
-                "Matrix::sparse: rows must be strictly increasing per column", k);
+        if (rowidx[k] < 0 || rowidx[k] >= m) fail(APC_INVALID_ARGUMENT, "Matrix::sparse: entry out of range", k);
+        if (k != colptr[j] && rowidx[k] <= rowidx[k - 1])
+          fail(APC_INVALID_ARGUMENT, "Matrix::sparse: rows must be strictly increasing per column", k);
       }
     }
     APC_CUDA(cudaSetDevice(ctx->device));

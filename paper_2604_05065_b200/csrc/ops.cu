@@ -5,9 +5,11 @@
 #include <algorithm>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <utility>
 
+#include "host_rng.hpp"
 #include "ops.cuh"
 
 namespace apc {
@@ -384,27 +386,51 @@ void build_units(apc_ctx* ctx, Csr& c, const std::vector<long long>& row_nnz) {
 // CSC (int64, reference layout) -> device CSR(A^T) (= CSC arrays, local rows
 // only) and CSR(A) via a stable radix sort by row.
 // ---------------------------------------------------------------------------
+struct StageCsc {  // narrow row indices to int32 and copy values into pinned staging
+  const long long* rowidx;
+  const double* val;
+  int* hidx;
+  double* hval;
+  void operator()(long long b, long long e) const {
+    for (long long k = b; k < e; ++k) {
+      hidx[k] = static_cast<int>(rowidx[k]);
+      hval[k] = val[k];
+    }
+  }
+};
+
 void upload_csc(apc_mat& a, const long long* colptr, const long long* rowidx, const double* val) {
   apc_ctx* ctx = a.ctx;
   cudaStream_t st = ctx->stream;
   const long long n = a.n, r0 = a.r0, r1 = a.r1, mloc = a.mloc();
   // host: filter to local rows and narrow indices to int32 (pinned staging)
+  std::unique_ptr<ProfScope> ps(new ProfScope("upload.host"));
   std::vector<int> tptr(n + 1);
-  long long cnt = 0;
-  for (long long j = 0; j < n; ++j) {
-    tptr[j] = static_cast<int>(cnt);
-    for (long long k = colptr[j]; k < colptr[j + 1]; ++k)
-      if (rowidx[k] >= r0 && rowidx[k] < r1) ++cnt;
-  }
-  tptr[n] = static_cast<int>(cnt);
-  require(cnt < (1LL << 31), APC_INVALID_ARGUMENT, "upload_csc: nnz exceeds int32 range");
-  const long long nnz = cnt;
+  std::vector<long long> tlen(n);
   int* hidx = nullptr;
   double* hval = nullptr;
-  hidx = static_cast<int*>(ctx_pinned(ctx, 0, sizeof(int) * std::max<long long>(1, nnz)));
-  hval = static_cast<double*>(ctx_pinned(ctx, 1, sizeof(double) * std::max<long long>(1, nnz)));
-  std::vector<long long> tlen(n);
-  {
+  long long nnz = 0;
+  if (r0 == 0 && r1 == a.m) {
+    // whole matrix: no filtering; narrow and stage on the host cores
+    nnz = n > 0 ? colptr[n] - colptr[0] : 0;
+    require(nnz < (1LL << 31), APC_INVALID_ARGUMENT, "upload_csc: nnz exceeds int32 range");
+    for (long long j = 0; j <= n; ++j) tptr[j] = static_cast<int>(colptr[j] - colptr[0]);
+    for (long long j = 0; j < n; ++j) tlen[j] = tptr[j + 1] - tptr[j];
+    hidx = static_cast<int*>(ctx_pinned(ctx, 0, sizeof(int) * std::max<long long>(1, nnz)));
+    hval = static_cast<double*>(ctx_pinned(ctx, 1, sizeof(double) * std::max<long long>(1, nnz)));
+    host_parallel_for(nnz, StageCsc{rowidx + colptr[0], val + colptr[0], hidx, hval}, 4);
+  } else {
+    long long cnt = 0;
+    for (long long j = 0; j < n; ++j) {
+      tptr[j] = static_cast<int>(cnt);
+      for (long long k = colptr[j]; k < colptr[j + 1]; ++k)
+        if (rowidx[k] >= r0 && rowidx[k] < r1) ++cnt;
+    }
+    tptr[n] = static_cast<int>(cnt);
+    require(cnt < (1LL << 31), APC_INVALID_ARGUMENT, "upload_csc: nnz exceeds int32 range");
+    nnz = cnt;
+    hidx = static_cast<int*>(ctx_pinned(ctx, 0, sizeof(int) * std::max<long long>(1, nnz)));
+    hval = static_cast<double*>(ctx_pinned(ctx, 1, sizeof(double) * std::max<long long>(1, nnz)));
     long long q = 0;
     for (long long j = 0; j < n; ++j) {
       for (long long k = colptr[j]; k < colptr[j + 1]; ++k) {
@@ -418,6 +444,7 @@ void upload_csc(apc_mat& a, const long long* colptr, const long long* rowidx, co
       tlen[j] = tptr[j + 1] - tptr[j];
     }
   }
+  ps.reset(new ProfScope("upload.csc_units"));
   Csr& t = a.at;
   t.rows = n;
   t.cols = mloc;
@@ -432,6 +459,7 @@ void upload_csc(apc_mat& a, const long long* colptr, const long long* rowidx, co
   }
   build_units(ctx, t, tlen);  // synchronizes the stream (the staging buffers are free again)
 
+  ps.reset(new ProfScope("upload.csr_build"));
   // CSR(A): sort entries by row (stable), keeping column order within rows
   Csr& c = a.a;
   c.rows = mloc;
