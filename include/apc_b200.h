@@ -155,7 +155,7 @@ typedef struct apc_solver_config {
   int64_t lsqr_cap;            /* 0: 4 n per phase */
   int64_t max_rank;            /* 0: min of target dimensions */
   uint64_t seed;               /* 0 */
-  int64_t trace_sample_stride; /* accepted; the device loop records no true_relres samples */
+  int64_t trace_sample_stride; /* 1; true-residual sample every k-th iteration, 0 off (bench: 0) */
   int64_t outer_cap;           /* 100000 */
   int32_t sketch_kind;         /* 0 sparse sign (reference), 1 Gaussian (BASELINE C1/C3/C4) */
   int32_t reserved;
@@ -192,6 +192,35 @@ int apc_solve(apc_mat* a, const double* b, const apc_solver_config* cfg, int pla
  * allreduce of n + 1 doubles ([A_p^T u_p | ||u_p||^2]). */
 int apc_solve_sharded(apc_mat* full, apc_mat* shard, const double* b, const apc_solver_config* cfg,
                       int plain, apc_result** out);
+/* SolveHooks (solver.hpp:114-120): diagnostic observers, called on the host
+ * thread of the solve.  on_rebuild runs after each preconditioner build and
+ * before its LSQR phase (solver.hpp:367) with a view of the CUR state and the
+ * preconditioner (pointers valid during the call only); on_phase_end runs at
+ * the end of every phase with x so far (solver.hpp:261), copied to the host. */
+typedef struct apc_rebuild_info {
+  int32_t phase;
+  int32_t variant;          /* 0 svd, 1 svd-free */
+  int64_t rank;             /* l = |I| = |J| */
+  const int64_t* rows;      /* I */
+  const int64_t* cols;      /* J */
+  double rho;               /* CUR error estimate the preconditioner was built at */
+  double sigma_hat;         /* Preconditioner::target_level() */
+  double sigma_floor;       /* smallest_cur_sigma() (svd) / target_level() (svd-free) */
+  const double* sigma_cur;  /* svd variant: CUR singular values (n_sigma), else NULL */
+  const double* sigma_reg;  /* svd variant: regularized_spectrum() (n_sigma), else NULL */
+  int64_t n_sigma;
+} apc_rebuild_info;
+typedef void (*apc_rebuild_fn)(void* user, const apc_rebuild_info* info);
+typedef void (*apc_phase_end_fn)(void* user, int32_t phase, const double* x, int64_t n);
+typedef struct apc_hooks {
+  void* user;
+  apc_rebuild_fn on_rebuild;     /* may be NULL */
+  apc_phase_end_fn on_phase_end; /* may be NULL */
+} apc_hooks;
+/* aplicur_solve(problem, cfg, &hooks) (solver.hpp:162-163).  full: NULL for a
+ * single-rank solve, else as in apc_solve_sharded.  hooks may be NULL. */
+int apc_solve_hooked(apc_mat* full, apc_mat* a, const double* b, const apc_solver_config* cfg,
+                     const apc_hooks* hooks, apc_result** out);
 int apc_result_free(apc_result* r);
 /* status: SolveStatus 0 converged, 1 rank-exhausted, 2 breakdown */
 int apc_result_summary(const apc_result* r, int* status, double* final_rho, double* final_relres,
@@ -201,6 +230,9 @@ int apc_result_x(const apc_result* r, double* x);
 int apc_result_indices(const apc_result* r, int64_t* row_indices, int64_t* col_indices);
 int apc_result_rho_history(const apc_result* r, double* rho);
 int apc_result_phases(const apc_result* r, apc_phase_report* phases);
+/* PhaseReport::precond_spectrum of phase k (solver.hpp:87,258-260; svd
+ * variant only, else empty): *n receives its length, out (may be NULL) the values */
+int apc_result_phase_spectrum(const apc_result* r, int64_t k, double* out, int64_t* n);
 int apc_result_trace(const apc_result* r, apc_trace_row* rows);
 /* wall-clock split of the last solve: setup (sketch + CUR + builds) and LSQR, ms */
 int apc_result_timing(const apc_result* r, double* total_ms, double* lsqr_ms, double* setup_ms);
@@ -227,7 +259,8 @@ int apc_report_json_write(const char* path, const apc_solver_config* cfg, int32_
                           double final_rho, uint64_t sketch_applications, uint64_t system_matvecs,
                           const char* trace_path, const int64_t* row_indices, const int64_t* col_indices,
                           int64_t rank, const double* rho_history, int64_t n_rho, const apc_phase_report* phases,
-                          int64_t n_phases);
+                          int64_t n_phases, const double* const* spectra, const int64_t* n_spectra);
+/* spectra / n_spectra: per phase precond_spectrum (both may be NULL: none) */
 
 #ifdef __cplusplus
 }

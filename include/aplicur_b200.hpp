@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <exception>
 #include <functional>
 #include <limits>
 #include <memory>
@@ -271,12 +272,13 @@ inline apc_solver_config to_c(const SolverConfig& c) {
   return k;
 }
 
-inline SolveResult run(const ProblemInstance& p, const SolverConfig& c, int plain) {
+inline SolveResult run(const ProblemInstance& p, const SolverConfig& c, int plain, const apc_hooks* hooks = nullptr) {
   apc_solver_config k = to_c(c);
   if (static_cast<Index>(p.b.size()) != p.a.rows())
     throw Error(ErrorKind::dimension_mismatch, "aplicur_solve: rhs length mismatch");
   apc_result* r = nullptr;
-  check(apc_solve(p.a.device(), p.b.data(), &k, plain, &r));
+  if (hooks) check(apc_solve_hooked(nullptr, p.a.device(), p.b.data(), &k, hooks, &r));
+  else check(apc_solve(p.a.device(), p.b.data(), &k, plain, &r));
   std::unique_ptr<apc_result, int (*)(apc_result*)> guard(r, apc_result_free);
   int status = 0;
   std::int64_t nph = 0, ntr = 0, rank = 0, nrho = 0;
@@ -293,8 +295,13 @@ inline SolveResult run(const ProblemInstance& p, const SolverConfig& c, int plai
   apc_result_rho_history(r, out.rho_history.data());
   std::vector<apc_phase_report> ph(static_cast<size_t>(nph));
   apc_result_phases(r, ph.data());
-  for (const auto& q : ph) {
+  for (size_t k = 0; k < ph.size(); ++k) {
+    const apc_phase_report& q = ph[k];
     PhaseReport rep;
+    std::int64_t ns = 0;
+    apc_result_phase_spectrum(r, static_cast<std::int64_t>(k), nullptr, &ns);
+    rep.precond_spectrum.resize(static_cast<size_t>(ns));
+    apc_result_phase_spectrum(r, static_cast<std::int64_t>(k), rep.precond_spectrum.data(), &ns);
     rep.phase = q.phase;
     rep.rank = q.rank;
     rep.rho = q.rho;
@@ -318,19 +325,75 @@ inline SolveResult run(const ProblemInstance& p, const SolverConfig& c, int plai
 }
 }  // namespace b200
 
-/// Diagnostic observers (solver.hpp:115-120).  The device solve does not
-/// stream intermediate states back to the host, so non-empty hooks are
-/// rejected with ErrorKind::not_applicable rather than silently ignored.
+/// Views handed to SolveHooks::on_rebuild.  The CUR state and the
+/// preconditioner live on the device, so the hook sees their host-side
+/// summary (CurState::row_indices/col_indices/rank/rho, cur.hpp:228-242;
+/// Preconditioner::rank/target_level, SvdPreconditioner spectra,
+/// preconditioner.hpp:19-56) instead of the objects themselves.
+struct CurStateView {
+  Index rank = 0;
+  std::span<const Index> row_indices, col_indices;
+  double rho = 0.0;
+};
+struct PreconditionerView {
+  Index rank = 0;
+  PrecondVariant variant = PrecondVariant::svd;
+  double target_level = 0.0;
+  double smallest_cur_sigma = 0.0;           // svd; svd-free: target_level
+  std::span<const double> cur_spectrum;          // svd variant only
+  std::span<const double> regularized_spectrum;  // svd variant only
+};
+
+/// Diagnostic observers (solver.hpp:114-120); they must not mutate solver state.
 struct SolveHooks {
+  // after a preconditioner rebuild, before its LSQR phase
+  std::function<void(const CurStateView&, const PreconditionerView&, int phase)> on_rebuild;
+  // at the end of each phase: (phase, x so far)
   std::function<void(int phase, std::span<const double> x)> on_phase_end;
 };
 
-/// solver.hpp:162 -- adaptive CUR-preconditioned LSQR on the GPU
+namespace b200 {
+struct HookBridge {
+  const SolveHooks* hooks;
+  std::exception_ptr error;
+  static void rebuild(void* user, const apc_rebuild_info* ri) {
+    auto* self = static_cast<HookBridge*>(user);
+    if (self->error) return;
+    try {
+      CurStateView cv{ri->rank, {ri->rows, static_cast<size_t>(ri->rank)}, {ri->cols, static_cast<size_t>(ri->rank)},
+                      ri->rho};
+      PreconditionerView pv{ri->rank, static_cast<PrecondVariant>(ri->variant), ri->sigma_hat, ri->sigma_floor,
+                            {ri->sigma_cur, static_cast<size_t>(ri->sigma_cur ? ri->n_sigma : 0)},
+                            {ri->sigma_reg, static_cast<size_t>(ri->sigma_reg ? ri->n_sigma : 0)}};
+      self->hooks->on_rebuild(cv, pv, ri->phase);
+    } catch (...) {
+      self->error = std::current_exception();
+    }
+  }
+  static void phase_end(void* user, std::int32_t phase, const double* x, std::int64_t n) {
+    auto* self = static_cast<HookBridge*>(user);
+    if (self->error) return;
+    try {
+      self->hooks->on_phase_end(phase, std::span<const double>(x, static_cast<size_t>(n)));
+    } catch (...) {
+      self->error = std::current_exception();
+    }
+  }
+};
+}  // namespace b200
+
+/// solver.hpp:162 -- adaptive CUR-preconditioned LSQR on the GPU.  A hook
+/// that throws stops forwarding further callbacks; its exception is rethrown
+/// after the solve returns.
 inline SolveResult aplicur_solve(const ProblemInstance& problem, const SolverConfig& config,
                                  const SolveHooks* hooks = nullptr) {
-  if (hooks && hooks->on_phase_end)
-    throw Error(ErrorKind::not_applicable, "aplicur_solve: SolveHooks are not supported by the device solver");
-  return b200::run(problem, config, 0);
+  if (!hooks || (!hooks->on_rebuild && !hooks->on_phase_end)) return b200::run(problem, config, 0);
+  b200::HookBridge bridge{hooks, nullptr};
+  apc_hooks h{&bridge, hooks->on_rebuild ? &b200::HookBridge::rebuild : nullptr,
+              hooks->on_phase_end ? &b200::HookBridge::phase_end : nullptr};
+  SolveResult r = b200::run(problem, config, 0, &h);
+  if (bridge.error) std::rethrow_exception(bridge.error);
+  return r;
 }
 
 /// solver.hpp:396 -- unpreconditioned LSQR baseline on the GPU
@@ -409,12 +472,18 @@ inline void write_solve_report(const SolverConfig& config, const SolveResult& r,
                                const std::string& path) {
   const apc_solver_config k = b200::to_c(config);
   const auto ph = b200::to_c(r.phases);
+  std::vector<const double*> spec;
+  std::vector<std::int64_t> nspec;
+  for (const auto& p : r.phases) {
+    spec.push_back(p.precond_spectrum.data());
+    nspec.push_back(static_cast<std::int64_t>(p.precond_spectrum.size()));
+  }
   b200::check(apc_report_json_write(path.c_str(), &k, static_cast<std::int32_t>(r.status), r.final_relres, r.final_rho,
                                     r.sketch_applications, r.system_matvecs, trace_path.c_str(),
                                     r.row_indices.data(), r.col_indices.data(),
                                     static_cast<std::int64_t>(r.row_indices.size()), r.rho_history.data(),
                                     static_cast<std::int64_t>(r.rho_history.size()), ph.data(),
-                                    static_cast<std::int64_t>(ph.size())));
+                                    static_cast<std::int64_t>(ph.size()), spec.data(), nspec.data()));
 }
 
 }  // namespace aplicur

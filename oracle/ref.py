@@ -44,7 +44,7 @@ class RefOut(C.Structure):
                 ("ph_rho", _dp), ("ph_sigma_hat", _dp), ("ph_relres", _dp), ("ph_t_lsqr_ms", _dp),
                 ("ph_t_total_ms", _dp), ("n_ph", _i64), ("cap_ph", _i64),
                 ("tr_phase", C.POINTER(_i32)), ("tr_iter", _i64p), ("tr_phibar", _dp),
-                ("tr_matvecs", C.POINTER(_u64)), ("n_tr", _i64), ("cap_tr", _i64),
+                ("tr_matvecs", C.POINTER(_u64)), ("tr_relres", _dp), ("n_tr", _i64), ("cap_tr", _i64),
                 ("wall_ms", C.c_double)]
 
 
@@ -221,6 +221,7 @@ class RefResult:
     trace_iter: np.ndarray
     trace_phibar: np.ndarray
     trace_matvecs: np.ndarray
+    trace_true_relres: np.ndarray
     wall_ms: float
 
 
@@ -239,7 +240,7 @@ def solve(p: Problem, b, cfg: dict, plain=False, cap_idx=20000, cap_rho=4096, ca
         ph_rho=np.zeros(cap_ph), ph_sigma_hat=np.zeros(cap_ph), ph_relres=np.zeros(cap_ph),
         ph_t_lsqr_ms=np.zeros(cap_ph), ph_t_total_ms=np.zeros(cap_ph),
         tr_phase=np.zeros(cap_tr, np.int32), tr_iter=np.zeros(cap_tr, np.int64), tr_phibar=np.zeros(cap_tr),
-        tr_matvecs=np.zeros(cap_tr, np.uint64))
+        tr_matvecs=np.zeros(cap_tr, np.uint64), tr_relres=np.zeros(cap_tr))
     o = RefOut()
     o.x = x.ctypes.data_as(_dp)
     ftypes = dict(RefOut._fields_)
@@ -254,7 +255,7 @@ def solve(p: Problem, b, cfg: dict, plain=False, cap_idx=20000, cap_rho=4096, ca
                      bufs["ph_rho"][:nph].copy(), bufs["ph_sigma_hat"][:nph].copy(), bufs["ph_relres"][:nph].copy(),
                      bufs["ph_t_lsqr_ms"][:nph].copy(), bufs["ph_t_total_ms"][:nph].copy(),
                      bufs["tr_phase"][:ntr].copy(), bufs["tr_iter"][:ntr].copy(), bufs["tr_phibar"][:ntr].copy(),
-                     bufs["tr_matvecs"][:ntr].copy(), o.wall_ms)
+                     bufs["tr_matvecs"][:ntr].copy(), bufs["tr_relres"][:ntr].copy(), o.wall_ms)
 
 
 def cur_steps(p: Problem, block, seed, steps, xi=8, probes=10, core=0, gaussian=False):

@@ -123,6 +123,7 @@ struct RefOut {
   std::int64_t* tr_iter;
   double* tr_phibar;
   std::uint64_t* tr_matvecs;
+  double* tr_relres;  // sampled true residual (NaN where not sampled)
   std::int64_t n_tr, cap_tr;
   double wall_ms;
 };
@@ -199,6 +200,7 @@ void fill_out(const SolveResult& r, RefOut* o) {
     o->tr_iter[k] = t.iter;
     o->tr_phibar[k] = t.phibar;
     o->tr_matvecs[k] = t.matvecs;
+    o->tr_relres[k] = t.true_relres;
   }
 }
 

@@ -93,6 +93,21 @@ class _Config(C.Structure):
     ]
 
 
+class _RebuildInfo(C.Structure):  # apc_rebuild_info
+    _fields_ = [("phase", C.c_int32), ("variant", C.c_int32), ("rank", C.c_int64),
+                ("rows", C.POINTER(C.c_int64)), ("cols", C.POINTER(C.c_int64)), ("rho", C.c_double),
+                ("sigma_hat", C.c_double), ("sigma_floor", C.c_double), ("sigma_cur", C.POINTER(C.c_double)),
+                ("sigma_reg", C.POINTER(C.c_double)), ("n_sigma", C.c_int64)]
+
+
+_REBUILD_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(_RebuildInfo))
+_PHASE_END_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.c_int64)
+
+
+class _Hooks(C.Structure):  # apc_hooks
+    _fields_ = [("user", C.c_void_p), ("on_rebuild", _REBUILD_FN), ("on_phase_end", _PHASE_END_FN)]
+
+
 class _Phase(C.Structure):
     _fields_ = [
         ("phase", C.c_int32), ("reason", C.c_int32), ("rank", _i64), ("rho", C.c_double),
@@ -161,6 +176,8 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
         "apc_result_indices": (C.c_int, [vp, _i64p, _i64p]),
         "apc_result_rho_history": (C.c_int, [vp, _dp]),
         "apc_result_phases": (C.c_int, [vp, C.POINTER(_Phase)]),
+        "apc_result_phase_spectrum": (C.c_int, [vp, _i64, _dp, _i64p]),
+        "apc_solve_hooked": (C.c_int, [vp, vp, _dp, C.POINTER(_Config), C.POINTER(_Hooks), C.POINTER(vp)]),
         "apc_result_trace": (C.c_int, [vp, C.POINTER(_Trace)]),
         "apc_result_timing": (C.c_int, [vp, _dp, _dp, _dp]),
         "apc_cur_create": (C.c_int, [vp, _i64, _u64, _i64, _i64, C.c_int, C.c_int, C.POINTER(vp)]),
@@ -181,7 +198,7 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
         "apc_trace_csv_write": (C.c_int, [C.c_char_p, C.POINTER(_Trace), _i64, C.POINTER(_Phase), _i64, C.c_int32]),
         "apc_report_json_write": (C.c_int, [C.c_char_p, C.POINTER(_Config), C.c_int32, C.c_double, C.c_double,
                                             _u64, _u64, C.c_char_p, _i64p, _i64p, _i64, _dp, _i64,
-                                            C.POINTER(_Phase), _i64]),
+                                            C.POINTER(_Phase), _i64, C.POINTER(_dp), _i64p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -519,6 +536,7 @@ class PhaseReport:
     t_lsqr_ms: float
     relres_at_end: float
     t_lsqr_device_ms: float = 0.0
+    precond_spectrum: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros(0))  # svd variant only
 
 
 @dataclasses.dataclass
@@ -565,10 +583,13 @@ class SolveResult:
         ri = np.ascontiguousarray(self.row_indices, dtype=np.int64)
         ci = np.ascontiguousarray(self.col_indices, dtype=np.int64)
         rho = np.ascontiguousarray(self.rho_history, dtype=np.float64)
+        specs = [np.ascontiguousarray(p.precond_spectrum, dtype=np.float64) for p in self.phases]
+        sp = (_dp * max(1, len(specs)))(*[_dptr(a) for a in specs])
+        nsp = np.array([a.size for a in specs] or [0], dtype=np.int64)
         _check(load_library().apc_report_json_write(
             str(path).encode(), C.byref(c), int(self.status), self.final_relres, self.final_rho,
             self.sketch_applications, self.system_matvecs, str(trace_path).encode(), _iptr(ri), _iptr(ci), len(ri),
-            _dptr(rho), len(rho), self._phase_array(), len(self.phases)))
+            _dptr(rho), len(rho), self._phase_array(), len(self.phases), sp, _iptr(nsp)))
 
 
 def _collect(h) -> SolveResult:
@@ -591,16 +612,83 @@ def _collect(h) -> SolveResult:
     tt, tl, ts = C.c_double(), C.c_double(), C.c_double()
     lib.apc_result_timing(h, C.byref(tt), C.byref(tl), C.byref(ts))
     tr = np.ctypeslib.as_array(trace)[: ntr.value].copy()
+    specs = []
+    for k in range(nph.value):
+        ns = _i64()
+        lib.apc_result_phase_spectrum(h, k, None, C.byref(ns))
+        a = np.zeros(ns.value)
+        lib.apc_result_phase_spectrum(h, k, _dptr(a), C.byref(ns))
+        specs.append(a)
     ph = [PhaseReport(p.phase, p.rank, p.rho, p.sigma_hat, p.mu, p.lsqr_iters, StopReason(p.reason),
                       p.t_augment_ms, p.t_factor_ms, p.t_precond_ms, p.t_lsqr_ms, p.relres_at_end,
-                      p.t_lsqr_device_ms)
-          for p in phases[: nph.value]]
+                      p.t_lsqr_device_ms, specs[k])
+          for k, p in enumerate(phases[: nph.value])]
     return SolveResult(None, ph, tr, SolveStatus(st.value), frho.value, frel.value, sk.value, smv.value,
                        rows, cols, rho, tt.value, tl.value, ts.value, phases)
 
 
+@dataclasses.dataclass
+class CurStateView:
+    """Host summary of the device CUR state handed to on_rebuild (cur.hpp:228-242)."""
+    rank: int
+    row_indices: np.ndarray
+    col_indices: np.ndarray
+    rho: float
+
+
+@dataclasses.dataclass
+class PreconditionerView:
+    """Host summary of the device preconditioner (preconditioner.hpp:19-56)."""
+    rank: int
+    variant: PrecondVariant
+    target_level: float
+    smallest_cur_sigma: float
+    cur_spectrum: np.ndarray  # svd variant only (else empty)
+    regularized_spectrum: np.ndarray
+
+
+@dataclasses.dataclass
+class SolveHooks:
+    """SolveHooks (solver.hpp:114-120): diagnostic observers.
+
+    on_rebuild(cur: CurStateView, precond: PreconditionerView, phase) runs after
+    each preconditioner build, before its LSQR phase; on_phase_end(phase, x)
+    at the end of every phase with x so far."""
+    on_rebuild: Optional[object] = None
+    on_phase_end: Optional[object] = None
+
+
+def _hook_struct(hooks: SolveHooks, errors: list):
+    def rebuild(_user, info_p):
+        if errors:
+            return
+        try:
+            ri = info_p.contents
+            k, ns = ri.rank, ri.n_sigma
+            cv = CurStateView(k, np.ctypeslib.as_array(ri.rows, (k,)).copy() if k else np.zeros(0, np.int64),
+                              np.ctypeslib.as_array(ri.cols, (k,)).copy() if k else np.zeros(0, np.int64), ri.rho)
+            sc = np.ctypeslib.as_array(ri.sigma_cur, (ns,)).copy() if ns and ri.sigma_cur else np.zeros(0)
+            sr = np.ctypeslib.as_array(ri.sigma_reg, (ns,)).copy() if ns and ri.sigma_reg else np.zeros(0)
+            pv = PreconditionerView(k, PrecondVariant(ri.variant), ri.sigma_hat, ri.sigma_floor, sc, sr)
+            hooks.on_rebuild(cv, pv, ri.phase)
+        except BaseException as e:  # re-raised after the solve returns
+            errors.append(e)
+
+    def phase_end(_user, phase, x, n):
+        if errors:
+            return
+        try:
+            hooks.on_phase_end(int(phase), np.ctypeslib.as_array(x, (n,)).copy())
+        except BaseException as e:
+            errors.append(e)
+
+    fr = _REBUILD_FN(rebuild) if hooks.on_rebuild else _REBUILD_FN()
+    fp = _PHASE_END_FN(phase_end) if hooks.on_phase_end else _PHASE_END_FN()
+    return _Hooks(None, fr, fp), (fr, fp)
+
+
 def solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig, plain: bool = False,
-          full: Optional[DeviceMatrix] = None) -> SolveResult:
+          full: Optional[DeviceMatrix] = None, hooks: Optional[SolveHooks] = None) -> SolveResult:
     """Run aplicur_solve (plain=False) or plain_lsqr_solve on a device-resident A.
 
     With ``full`` given, ``mat`` is this rank's row block (row-partitioned
@@ -611,7 +699,12 @@ def solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig, plain: bool = 
     assert b.size == mat.m
     c = config._c()
     h = C.c_void_p()
-    if full is not None or mat.ctx.nranks > 1:
+    errors: list = []
+    if hooks is not None and not plain and (hooks.on_rebuild or hooks.on_phase_end):
+        hs, _keep = _hook_struct(hooks, errors)
+        _check(lib.apc_solve_hooked(None if full is None else full.h, mat.h, _dptr(b), C.byref(c), C.byref(hs),
+                                    C.byref(h)))
+    elif full is not None or mat.ctx.nranks > 1:
         _check(lib.apc_solve_sharded(None if full is None else full.h, mat.h, _dptr(b), C.byref(c), int(plain),
                                      C.byref(h)))
     else:
@@ -623,13 +716,15 @@ def solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig, plain: bool = 
         res.x = x
     finally:
         lib.apc_result_free(h)
+    if errors:
+        raise errors[0]
     return res
 
 
 def aplicur_solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig,
-                  full: Optional[DeviceMatrix] = None) -> SolveResult:
+                  full: Optional[DeviceMatrix] = None, hooks: Optional[SolveHooks] = None) -> SolveResult:
     """solver.hpp:162 -- adaptive CUR-preconditioned LSQR."""
-    return solve(mat, b, config, plain=False, full=full)
+    return solve(mat, b, config, plain=False, full=full, hooks=hooks)
 
 
 def plain_lsqr_solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig) -> SolveResult:

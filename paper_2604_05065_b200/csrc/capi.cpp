@@ -403,6 +403,15 @@ int apc_solve_sharded(apc_mat* full, apc_mat* shard, const double* b, const apc_
   });
 }
 
+int apc_solve_hooked(apc_mat* full, apc_mat* a, const double* b, const apc_solver_config* cfg,
+                     const apc_hooks* hooks, apc_result** out) {
+  *out = nullptr;
+  return guard(a->ctx, [&] {
+    APC_CUDA(cudaSetDevice(a->ctx->device));
+    *out = aplicur_solve_sharded(full ? *full : *a, *a, b, *cfg, hooks);
+  });
+}
+
 int apc_result_free(apc_result* r) {
   delete r;
   return APC_OK;
@@ -441,6 +450,15 @@ int apc_result_rho_history(const apc_result* r, double* rho) {
 
 int apc_result_phases(const apc_result* r, apc_phase_report* phases) {
   std::copy(r->phases.begin(), r->phases.end(), phases);
+  return APC_OK;
+}
+
+int apc_result_phase_spectrum(const apc_result* r, int64_t k, double* out, int64_t* n) {
+  if (!r || !n || k < 0 || k >= static_cast<int64_t>(r->phases.size())) return APC_INVALID_ARGUMENT;
+  static const std::vector<double> none;
+  const auto& s = k < static_cast<int64_t>(r->spectra.size()) ? r->spectra[static_cast<size_t>(k)] : none;
+  *n = static_cast<int64_t>(s.size());
+  if (out) std::copy(s.begin(), s.end(), out);
   return APC_OK;
 }
 

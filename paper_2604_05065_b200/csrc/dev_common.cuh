@@ -97,8 +97,9 @@ struct LsqrState {
   int done;                    // 1: stop (no further kernel does work)
   int reason;                  // StopReason (lsqr.hpp:17-24)
   int breakdown;               // 1: non-finite recurrence (numerical_breakdown)
-  int pad;
+  int samp_skip;               // 1: this iteration takes no true-residual sample
   unsigned long long t0_ns;
+  long long samp_last;         // iteration of the last sampling gate
 };
 
 struct TraceRow {  // LsqrTraceRow (lsqr.hpp:38-47)

@@ -277,7 +277,7 @@ int apc_report_json_write(const char* path, const apc_solver_config* cfg, int32_
                           double final_rho, uint64_t sketch_applications, uint64_t system_matvecs,
                           const char* trace_path, const int64_t* row_indices, const int64_t* col_indices,
                           int64_t rank, const double* rho_history, int64_t n_rho, const apc_phase_report* phases,
-                          int64_t n_phases) {
+                          int64_t n_phases, const double* const* spectra, const int64_t* n_spectra) {
   return capi_guard(nullptr, [&] {
     require(path && cfg, APC_INVALID_ARGUMENT, "apc_report_json_write: bad arguments");
     const auto i64s = [](int64_t v) { return std::to_string(v); };
@@ -322,6 +322,8 @@ int apc_report_json_write(const char* path, const apc_solver_config* cfg, int32_
       j += ",\"relres_at_end\":" + jnum(p.relres_at_end);
       j += ",\"wall_ms\":{\"augment\":" + jnum(p.t_augment_ms) + ",\"factor\":" + jnum(p.t_factor_ms) +
            ",\"precond\":" + jnum(p.t_precond_ms) + ",\"lsqr\":" + jnum(p.t_lsqr_ms) + "}";
+      if (spectra && n_spectra && n_spectra[k] > 0 && spectra[k])
+        j += ",\"precond_spectrum\":" + jarr(spectra[k], n_spectra[k], dbl);
       j += "}";
     }
     j += "]}\n";

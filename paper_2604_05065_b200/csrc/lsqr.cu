@@ -175,6 +175,28 @@ struct LsqrFwdEpi {  // u <- (A z) - alpha * u/beta ; ||u_top||^2 -> g[n]
   }
 };
 
+// true-residual sample: ||b - A xs||^2 over the local rows -> *out_norm2
+struct ResidSampleEpi {
+  const double* b;
+  double* part;
+  unsigned* ctr;
+  double* out_norm2;
+  __device__ void begin() {}
+  __device__ double load(long long r) { return b[r]; }
+  __device__ double row(long long, double av, double bo) {
+    const double t = av - bo;
+    return t * t;
+  }
+  __device__ void tile_done(unsigned tile, unsigned ntiles, double sq) {
+    __shared__ double sh[32];
+    if (threadIdx.x == 0) part[tile] = sq;
+    if (elect_last_block(ctr, ntiles)) {
+      double s = ordered_sum<256>(part, ntiles, sh);
+      if (threadIdx.x == 0) *out_norm2 = s;
+    }
+  }
+};
+
 // Explicit basis (dense B, n x l column-major): out = x + B s through the dense
 // forward kernel (8 rows per thread, split over the l columns) instead of a
 // thread-per-row chain over l.  mode 0: out_j = x_j + (B s)_j ; mode 1:
@@ -331,6 +353,53 @@ lsqr_update_kernel(LsqrPtrs P, cudaGraphConditionalHandle cond, int use_cond) {
 }
 
 // ---------------------------------------------------------------------------
+// true-residual sampling (the solver's observer, solver.hpp:222-236, 418-427)
+// ---------------------------------------------------------------------------
+// gate: sample iff this graph body completed iteration j >= 1 and j % stride == 0
+__global__ void samp_gate_kernel(LsqrState* st, long long stride) {
+  const long long j = st->iter;
+  const bool take = j >= 1 && j != st->samp_last && !st->breakdown && j % stride == 0;
+  st->samp_last = j;
+  st->samp_skip = take ? 0 : 1;
+}
+
+// xs = d (+ x_base) ; tail: ||mu xs||^2 -> sc[1] (last block)
+__global__ void __launch_bounds__(kVecThreads)
+samp_combine_kernel(const LsqrState* st, const double* d, const double* x_base, double* xs, long long n,
+                    double mu, double* part, unsigned* ctr, double* sc) {  // xs may alias d
+  __shared__ double sh[32];
+  if (st->samp_skip) return;
+  const long long j = static_cast<long long>(blockIdx.x) * kVecThreads + threadIdx.x;
+  double sq = 0.0;
+  if (j < n) {
+    const double v = x_base ? d[j] + x_base[j] : d[j];
+    if (x_base) xs[j] = v;
+    const double t = mu * v;
+    sq = t * t;
+  }
+  if (mu <= 0.0) return;
+  sq = block_sum<kVecThreads>(sq, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = sq;
+  if (elect_last_block(ctr, gridDim.x)) {
+    const double s = ordered_sum<kVecThreads>(part, gridDim.x, sh);
+    if (threadIdx.x == 0) sc[1] = s;
+  }
+}
+
+__global__ void samp_zero_kernel(const LsqrState* st, double* sc) {
+  if (!st->samp_skip) sc[0] = 0.0;
+}
+
+// sampled[j] = sqrt(top + tail) / bnorm (system_relres, solver.hpp:147-153)
+__global__ void samp_final_kernel(const LsqrState* st, const double* sc, double bnorm, int tail,
+                                  double* sampled, long long cap) {
+  if (st->samp_skip) return;
+  const long long j = st->iter;
+  if (j < 0 || j >= cap) return;
+  sampled[j] = bnorm > 0.0 ? sqrt(sc[0] + (tail ? sc[1] : 0.0)) / bnorm : 0.0;
+}
+
+// ---------------------------------------------------------------------------
 // preconditioner kernels:  out = x + B (K (B^T x))  or  x + R^T (G (R x))
 // ---------------------------------------------------------------------------
 // s = K t with K stored row-major (KT[i * l + k] = K(i, k)): one warp per row,
@@ -453,6 +522,7 @@ struct LsqrWork {
   DBuf<unsigned> ctr, pc_ctr, pcf_ctr;
   DBuf<LsqrState> st;
   DBuf<TraceRow> trace;
+  DBuf<double> xs, samp_part, samp_tpart, samp_sc, sampled;  // true-residual sampling
   LsqrState* hst = nullptr;  // pinned
   cudaEvent_t ev[2] = {nullptr, nullptr};
   cudaEvent_t tev[2] = {nullptr, nullptr};  // timing of the iteration loop
@@ -602,6 +672,39 @@ void enqueue_iteration(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P
   ctx->launches++;
 }
 
+// the observer's sample after iteration j (no-ops unless the gate opens)
+void enqueue_sample(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P, const SampleCfg& sc,
+                    long long cap) {
+  apc_ctx* ctx = w->ctx;
+  cudaStream_t st = ctx->stream;
+  const long long n = w->n;
+  samp_gate_kernel<<<1, 1, 0, st>>>(P.st, sc.stride);
+  ctx->launches++;
+  const int* skip = &P.st->samp_skip;
+  const double* xs = P.y;
+  if (p && p->kind != 0) {  // P^{-1} y
+    pc_project_core(w, *p, P.y, false, skip);
+    pc_expand(w, P, *p, P.y, w->xs.p, 0, skip);
+    xs = w->xs.p;
+  }
+  if (sc.x_base || P.has_tail) {  // + x ; ||mu xs||^2
+    double* out = sc.x_base ? w->xs.p : const_cast<double*>(xs);
+    samp_combine_kernel<<<nb(n), kVecThreads, 0, st>>>(P.st, xs, sc.x_base, out, n, P.has_tail ? P.mu : 0.0,
+                                                       w->samp_tpart.p, P.ctr + 5, w->samp_sc.p);
+    ctx->launches++;
+    xs = out;
+  }
+  if (w->mloc > 0) {
+    launch_fwd(a, xs, skip, ResidSampleEpi{sc.b_local, w->samp_part.p, P.ctr + 4, w->samp_sc.p}, st);
+  } else {
+    samp_zero_kernel<<<1, 1, 0, st>>>(P.st, w->samp_sc.p);
+    ctx->launches++;
+  }
+  comm_allreduce(ctx, w->samp_sc.p, 1);
+  samp_final_kernel<<<1, 1, 0, st>>>(P.st, w->samp_sc.p, sc.bnorm, P.has_tail, w->sampled.p, cap);
+  ctx->launches++;
+}
+
 }  // namespace
 
 void precond_apply(apc_ctx* ctx, PrecondDev& p, bool transpose, const double* x, double* out) {
@@ -625,7 +728,7 @@ void precond_apply(apc_ctx* ctx, PrecondDev& p, bool transpose, const double* x,
 // one phase
 // ---------------------------------------------------------------------------
 void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const double* rhs_d,
-                const StopCfg& stop, int phase, double* y_d, PhaseOut& out) {
+                const StopCfg& stop, int phase, double* y_d, PhaseOut& out, const SampleCfg* samp) {
   (void)phase;
   apc_ctx* ctx = w->ctx;
   cudaStream_t st = ctx->stream;
@@ -635,6 +738,15 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   if (p && p->kind != 0) ensure_pc_buffers(w, *p);
   const long long cap = stop.max_iters > 0 ? stop.max_iters : 4 * n;
   w->trace.ensure(cap + 1);
+  const bool sampling = samp && samp->stride > 0;
+  if (sampling) {
+    w->xs.ensure(std::max<long long>(1, n));
+    w->samp_part.ensure(w->fwd_part.n);
+    w->samp_tpart.ensure(nb(n));
+    w->samp_sc.ensure(2);
+    w->sampled.ensure(cap + 1);
+    APC_CUDA(cudaMemsetAsync(w->sampled.p, 0xFF, sizeof(double) * (cap + 1), st));  // NaN
+  }
 
   LsqrState h{};
   h.eps = stop.eps_lsqr;
@@ -702,7 +814,8 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   const char* mode_env = std::getenv("APC_LSQR_MODE");
   const std::string mode = mode_env ? mode_env : "";
   const bool eager = mode == "eager";
-  const bool persistent = (mode.empty() || mode == "persistent") && persistent_eligible(a, p, ctx);
+  const bool persistent =
+      !sampling && (mode.empty() || mode == "persistent") && persistent_eligible(a, p, ctx);
   const bool use_while = !persistent && ctx->nranks == 1 && mode != "batch" && !eager;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -784,6 +897,7 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
     APC_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeThreadLocal));
     enqueue_iteration(w, a, p, P, cond, 1);
+    if (sampling) enqueue_sample(w, a, p, P, *samp, cap + 1);
     per_iter = ctx->launches - launches_before_capture;
     APC_CUDA(cudaStreamEndCapture(st, &body));
     APC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
@@ -793,7 +907,10 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
     if (!w->hst[1].done) APC_CUDA(cudaGraphLaunch(exec, st));
   } else if (eager) {
     for (;;) {
-      for (int k = 0; k < 8; ++k) enqueue_iteration(w, a, p, P, cudaGraphConditionalHandle{}, 0);
+      for (int k = 0; k < 8; ++k) {
+        enqueue_iteration(w, a, p, P, cudaGraphConditionalHandle{}, 0);
+        if (sampling) enqueue_sample(w, a, p, P, *samp, cap + 1);
+      }
       APC_CUDA(cudaMemcpyAsync(&w->hst[1], w->st.p, sizeof(LsqrState), cudaMemcpyDeviceToHost, st));
       APC_CUDA(cudaStreamSynchronize(st));
       if (w->hst[1].done) break;
@@ -802,7 +919,10 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   } else {
     constexpr int kBatch = 8;
     APC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    for (int k = 0; k < kBatch; ++k) enqueue_iteration(w, a, p, P, cudaGraphConditionalHandle{}, 0);
+    for (int k = 0; k < kBatch; ++k) {
+      enqueue_iteration(w, a, p, P, cudaGraphConditionalHandle{}, 0);
+      if (sampling) enqueue_sample(w, a, p, P, *samp, cap + 1);
+    }
     per_iter = (ctx->launches - launches_before_capture) / kBatch;
     APC_CUDA(cudaStreamEndCapture(st, &graph));
     APC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
@@ -841,6 +961,12 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   out.rows.resize(static_cast<size_t>(nrows));
   static_assert(sizeof(TraceRowH) == sizeof(TraceRow), "trace row layout");
   copy_sync(st, out.rows.data(), w->trace.p, sizeof(TraceRow) * nrows, cudaMemcpyDeviceToHost);
+  if (sampling) {
+    out.sampled.resize(static_cast<size_t>(nrows));
+    copy_sync(st, out.sampled.data(), w->sampled.p, sizeof(double) * nrows, cudaMemcpyDeviceToHost);
+  } else {
+    out.sampled.clear();
+  }
   if (out.breakdown) fail(APC_NUMERICAL_BREAKDOWN, "lsqr_solve: non-finite recurrence");
 }
 

@@ -39,7 +39,18 @@ struct StopCfg {  // StopConfig (lsqr.hpp:54-59)
   i64 max_iters = 0;
 };
 
+// True-residual sampling of the solver's observer (solver.hpp:222-236 and
+// :418-427): at iterations j >= 1 with j % stride == 0 the phase records
+// ||A_mu (x_base + P^{-1} y_j) - [b; 0]|| / bnorm (x_base null: y_j itself).
+struct SampleCfg {
+  i64 stride = 0;                  // 0: off
+  const double* x_base = nullptr;  // device, n (the solver's x before this phase)
+  const double* b_local = nullptr; // device, local rows of b
+  double bnorm = 0.0;
+};
+
 struct PhaseOut {
+  std::vector<double> sampled;  // per iteration (NaN where not sampled); empty when sampling is off
   i64 iters = 0;
   int reason = 0;
   bool breakdown = false;
@@ -55,8 +66,11 @@ void lsqr_work_destroy(LsqrWork* w);
 // One LSQR call from y = 0 on the right-preconditioned system A_mu P^{-1}
 // (operators.hpp:75-90) for rhs (device, local rows [+ n tail rows when
 // mu > 0]); y_d (device, n) receives the solution.  Throws Status on breakdown.
+// Sampling (samp non-null with stride > 0) runs the graph path: the sample's
+// preconditioner apply and forward product are no-ops on other iterations.
 void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* p, const double* rhs_d,
-                const StopCfg& stop, int phase, double* y_d, PhaseOut& out);
+                const StopCfg& stop, int phase, double* y_d, PhaseOut& out,
+                const SampleCfg* samp = nullptr);
 
 // out = P^{-1} x (transpose: P^{-T} x); device pointers, ctx stream.
 void precond_apply(apc_ctx* ctx, PrecondDev& p, bool transpose, const double* x, double* out);

@@ -39,14 +39,15 @@ bool is_solver_error(const Status& s) { return s.code >= 1 && s.code <= 9; }
 
 }  // namespace
 
-apc_result* aplicur_solve(apc_mat& a, const double* b, const apc_solver_config& cfg_in) {
-  return aplicur_solve_sharded(a, a, b, cfg_in);
+apc_result* aplicur_solve(apc_mat& a, const double* b, const apc_solver_config& cfg_in, const apc_hooks* hooks) {
+  return aplicur_solve_sharded(a, a, b, cfg_in, hooks);
 }
 
 // `full`: the whole matrix (sketch + CUR selection, replicated on every rank);
 // `a`: this rank's block of rows (LSQR operator, residuals; NCCL allreduce
 // of the partial A^T u when the ctx has several ranks).
-apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, const apc_solver_config& cfg_in) {
+apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, const apc_solver_config& cfg_in,
+                                  const apc_hooks* hooks) {
   require(full.ctx == a.ctx && full.m == a.m && full.n == a.n, APC_INVALID_ARGUMENT,
           "aplicur_solve: full matrix and shard must describe the same A on the same context");
   auto t_start = clock_t_::now();
@@ -105,13 +106,21 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
     stop.max_iters = cfg.lsqr_cap > 0 ? cfg.lsqr_cap : 4 * n;
     stop.sigma_floor = info.sigma_floor;
     PhaseOut po;
-    lsqr_phase(work, a, mu, &P, d_rhs.p, stop, phase, d_y.p, po);
+    SampleCfg samp;  // the observer's true-residual samples (solver.hpp:222-236)
+    samp.stride = cfg.trace_sample_stride;
+    samp.x_base = d_x.p;
+    samp.b_local = d_b.p;
+    samp.bnorm = bnorm;
+    lsqr_phase(work, a, mu, &P, d_rhs.p, stop, phase, d_y.p, po, &samp);
     matvecs += po.iters > 0 ? 1 + 2 * static_cast<std::uint64_t>(po.iters) : (po.reason == 5 ? 0 : 1);
     precond_apply(ctx, P, false, d_y.p, d_dx.p);  // x += P^{-1} y (solver.hpp:238-240)
     axpy(ctx, d_x.p, d_dx.p, n);
-    for (const auto& row : po.rows)
+    for (size_t k = 0; k < po.rows.size(); ++k) {
+      const auto& row = po.rows[k];
+      const double tr = k < po.sampled.size() ? po.sampled[k] : std::numeric_limits<double>::quiet_NaN();
       res->trace.push_back(apc_trace_row{phase, 0, row.iter, row.phibar, row.cvgrate, row.cvgdiff, row.matvecs,
-                                         row.wall_ms, std::numeric_limits<double>::quiet_NaN()});
+                                         row.wall_ms, tr});
+    }
     res->last_reason = po.reason;
     rep.phase = phase;
     rep.mu = mu;
@@ -124,6 +133,11 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
     rep.t_lsqr_device_ms = po.device_ms;
     res->lsqr_ms += po.ms;
     rep.relres_at_end = bnorm > 0.0 ? std::sqrt(residual(a, vw, d_x.p, d_b.p, nullptr)) / bnorm : 0.0;
+    if (hooks && hooks->on_phase_end) {  // solver.hpp:261
+      std::vector<double> xh(static_cast<size_t>(n));
+      copy_sync(st, xh.data(), d_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost);
+      hooks->on_phase_end(hooks->user, phase, xh.data(), n);
+    }
   };
 
   for (i64 outer = 0; outer < cfg.outer_cap && !done; ++outer) {
@@ -249,9 +263,18 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
         break;
       }
       rep.t_precond_ms = ms_since(t_pre0);
+      if (hooks && hooks->on_rebuild) {  // solver.hpp:367
+        const bool svd = cfg.variant == 0;
+        const i64 ns = svd ? static_cast<i64>(std::min(info.sigma_cur.size(), info.sigma_reg.size())) : 0;
+        apc_rebuild_info ri{phase, cfg.variant, cur.rank(), cur.rows().data(), cur.cols().data(), rho,
+                            info.sigma_hat, info.sigma_floor, ns ? info.sigma_cur.data() : nullptr,
+                            ns ? info.sigma_reg.data() : nullptr, ns};
+        hooks->on_rebuild(hooks->user, &ri);
+      }
       run_phase(P, final_phase, rho, rep, info);
       if (std::isfinite(rho)) d_cur = rho - cfg.eps_cur;
       res->phases.push_back(rep);
+      res->spectra.push_back(cfg.variant == 0 ? info.sigma_reg : Vec{});  // solver.hpp:258-260
     }
   }
 
@@ -263,6 +286,7 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
     PrecondInfo info;
     run_phase(ident, true, cur.rho(), rep, info);
     res->phases.push_back(rep);
+    res->spectra.emplace_back();
   }
 
   res->x.resize(static_cast<size_t>(n));

@@ -11,6 +11,7 @@ struct apc_result {
   apc::i64 n = 0;
   std::vector<double> x;
   std::vector<apc_phase_report> phases;
+  std::vector<std::vector<double>> spectra;  // PhaseReport::precond_spectrum per phase
   std::vector<apc_trace_row> trace;
   int status = 0;  // SolveStatus
   int last_reason = 0;
@@ -27,7 +28,9 @@ namespace apc {
 apc_solver_config resolve_config(const apc_solver_config& in, i64 n);
 
 apc_result* plain_solve(apc_mat& a, const double* b, const apc_solver_config& cfg);
-apc_result* aplicur_solve(apc_mat& a, const double* b, const apc_solver_config& cfg);
-apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& shard, const double* b, const apc_solver_config& cfg);
+apc_result* aplicur_solve(apc_mat& a, const double* b, const apc_solver_config& cfg,
+                          const apc_hooks* hooks = nullptr);
+apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& shard, const double* b, const apc_solver_config& cfg,
+                                  const apc_hooks* hooks = nullptr);
 
 }  // namespace apc

@@ -55,7 +55,11 @@ apc_result* plain_solve(apc_mat& a, const double* b, const apc_solver_config& cf
   LsqrWork* w = lsqr_work_create(a, mu);
   PhaseOut po;
   try {
-    lsqr_phase(w, a, mu, nullptr, d_rhs.p, stop, 1, d_x.p, po);
+    SampleCfg samp;  // the observer of plain_lsqr_solve samples y itself (solver.hpp:418-427)
+    samp.stride = cfg.trace_sample_stride;
+    samp.b_local = d_b.p;
+    samp.bnorm = bnorm;
+    lsqr_phase(w, a, mu, nullptr, d_rhs.p, stop, 1, d_x.p, po, &samp);
   } catch (...) {
     lsqr_work_destroy(w);
     throw;
@@ -68,9 +72,12 @@ apc_result* plain_solve(apc_mat& a, const double* b, const apc_solver_config& cf
   copy_sync(st, r->x.data(), d_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost);
   VecWork vw(a, mu);
   const double rr = bnorm > 0.0 ? std::sqrt(residual(a, vw, d_x.p, d_b.p, nullptr)) / bnorm : 0.0;
-  for (const auto& row : po.rows)
+  for (size_t k = 0; k < po.rows.size(); ++k) {
+    const auto& row = po.rows[k];
+    const double tr = k < po.sampled.size() ? po.sampled[k] : std::numeric_limits<double>::quiet_NaN();
     r->trace.push_back(apc_trace_row{1, 0, row.iter, row.phibar, row.cvgrate, row.cvgdiff, row.matvecs,
-                                     row.wall_ms, std::numeric_limits<double>::quiet_NaN()});
+                                     row.wall_ms, tr});
+  }
   apc_phase_report rep{};
   rep.phase = 1;
   rep.reason = po.reason;
@@ -81,6 +88,7 @@ apc_result* plain_solve(apc_mat& a, const double* b, const apc_solver_config& cf
   rep.t_lsqr_device_ms = po.device_ms;
   rep.relres_at_end = rr;
   r->phases.push_back(rep);
+  r->spectra.emplace_back();
   r->last_reason = po.reason;
   r->final_relres = rr;
   r->final_rho = std::numeric_limits<double>::infinity();

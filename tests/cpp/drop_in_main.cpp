@@ -51,6 +51,34 @@ int main(int argc, char** argv) {
   for (const auto& ph : r.phases) it += ph.lsqr_iters;
   std::printf("], \"iters\": %lld, \"final_relres\": %.17g, \"plain_iters\": %lld, \"status\": %d, \"ax0\": %.17g}\n",
               (long long)it, r.final_relres, (long long)q.phases[0].lsqr_iters, (int)r.status, y[0]);
+  // SolveHooks (solver.hpp:114-120): observers see every rebuild and phase end
+  int rebuilds = 0, phase_ends = 0, last_phase = 0, hook_ok = 1;
+  std::vector<double> last_x;
+  SolveHooks hooks;
+  hooks.on_rebuild = [&](const CurStateView& cur, const PreconditionerView& pc, int phase) {
+    ++rebuilds;
+    if (cur.rank != pc.rank || pc.regularized_spectrum.size() != static_cast<size_t>(pc.rank)) hook_ok = 0;
+    if (phase != last_phase + 1) hook_ok = 0;
+  };
+  hooks.on_phase_end = [&](int phase, std::span<const double> x) {
+    ++phase_ends;
+    last_phase = phase;
+    last_x.assign(x.begin(), x.end());
+  };
+  SolveResult h = aplicur_solve(p, c, &hooks);
+  const bool same = h.x == r.x && last_x == r.x && h.row_indices == r.row_indices;
+  const size_t nspec = r.phases.back().precond_spectrum.size();
+  std::printf("{\"hook_rebuilds\": %d, \"hook_phase_ends\": %d, \"phases\": %zu, \"hook_ok\": %d, \"same\": %d, "
+              "\"spectrum\": %zu, \"last_rank\": %lld}\n",
+              rebuilds, phase_ends, r.phases.size(), hook_ok, same ? 1 : 0, nspec, (long long)r.phases.back().rank);
+  try {  // a throwing hook surfaces after the solve
+    SolveHooks bad;
+    bad.on_phase_end = [](int, std::span<const double>) { throw std::runtime_error("hook"); };
+    aplicur_solve(p, c, &bad);
+    return 4;
+  } catch (const std::runtime_error& e) {
+    if (std::string(e.what()) != "hook") return 5;
+  }
   try {  // error mapping: shape errors arrive as aplicur::Error
     std::vector<double> bad(3);
     p.a.matvec(bad, y);

@@ -28,7 +28,14 @@ def test_drop_in_header_compiles(tmp_path):
 def test_drop_in_solve_matches_reference(apc, ref, tmp_path):
     exe = _build(tmp_path)
     out = subprocess.run([str(exe), "2", "4000", "400"], check=True, capture_output=True, text=True).stdout
-    d = json.loads(out)
+    lines = out.splitlines()
+    d, hk = json.loads(lines[0]), json.loads(lines[1])
+    # SolveHooks: one rebuild and one phase end per phase, phases numbered
+    # 1, 2, ...; the last phase-end x is the result; the hooked run is
+    # bit-identical to the unhooked one; svd phases carry their spectrum
+    assert hk["hook_rebuilds"] == hk["phases"] == hk["hook_phase_ends"]
+    assert hk["hook_ok"] == 1 and hk["same"] == 1
+    assert hk["spectrum"] == hk["last_rank"]
     p = apc.Problem(2, 4000, 400)
     r = ref.solve(ref.Problem.from_apc(p), p.b, dict(mu=1e-3, eps_lsqr=1e-10, block=8, seed=3, max_rank=40,
                                                      trace_sample_stride=0))
