@@ -135,7 +135,7 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
         return _lib
     # APC_LIB_PATH: an alternative build of the same library (kernel-variant
     # experiments, scripts/build_variant.py); the default is the in-tree build
-    p = Path(path) if path else Path(os.environ.get("APC_LIB_PATH", LIB_PATH))
+    p = Path(path) if path else Path(os.environ.get("APC_LIB_PATH") or LIB_PATH)
     if not p.exists():
         raise ApcError(20, f"CUDA library missing: {p} (run __graft_entry__.build())")
     lib = C.CDLL(str(p), mode=C.RTLD_GLOBAL)

@@ -105,21 +105,48 @@ struct DBuf {
 // ---------------------------------------------------------------------------
 // Compressed sparse rows (int32 indices; values fp64)
 // ---------------------------------------------------------------------------
-struct Csr {
-  i64 rows = 0, cols = 0, nnz = 0;
-  DBuf<i32> ptr;  // rows+1
-  DBuf<i32> idx;  // nnz
-  DBuf<double> val;
-  // nnz-balanced work units for rows longer than a warp can take in one unit:
-  // unit u covers [ustart[u], uend[u]) of row urow[u]; rows split in several
-  // units write partial sums to upart[slot] which a fix-up pass adds in order.
-  i64 n_units = 0, n_parts = 0, max_row_nnz = 0;
+// nnz-balanced work units over the rows of a CSR (one warp per unit): unit u
+// covers [ustart[u], uend[u]) of row urow[u]; rows split in several units write
+// partial sums to upart[slot] which a fix-up pass adds in order.
+struct Units {
+  i64 n_units = 0, n_parts = 0;
   DBuf<i32> urow, ustart, uend, uslot;  // per unit (uslot < 0: whole row)
   DBuf<i32> rfirst, rcount;             // per row: first partial slot (-1: not split), count
   i64 n_split = 0;
   DBuf<i32> srows;                      // the split rows (summed into the output by op_adj_raw)
   DBuf<double> upart;                   // n_parts partial sums
+};
+
+struct Csr : Units {
+  i64 rows = 0, cols = 0, nnz = 0;
+  DBuf<i32> ptr;  // rows+1
+  DBuf<i32> idx;  // nnz
+  DBuf<double> val;
+  i64 max_row_nnz = 0;
   double avg_row_nnz = 0.0;
+};
+
+// Row-blocked A^T u for the long (Zipf-head) rows of CSR(A^T): the local rows
+// of A are cut into blocks of kHeadRows.  The head entries of block b are
+// stored contiguously at [bptr[b], bptr[b+1]), sorted by (head column, row),
+// each with a packed key (head column << 16 | row within block).  A CTA stages
+// its block of u in shared memory and streams the block's entries (warp steps
+// of 32 coalesced entries, segmented scan by column), producing one partial per
+// (head column, block) at part[k * nblocks + b]; a warp per head column adds its
+// partials in block order.  The remaining (tail) rows of A^T go through `tail`
+// work units gathering u from L2 as before.
+struct HeadAdj {
+  i64 ncols = 0, nblocks = 0, nnz = 0;
+  int parts = 1;       // CTAs (work items) per block
+  DBuf<i32> bptr;      // nblocks + 1 (multiples of 128; padding keys are -1)
+  DBuf<i32> hkey;      // nnz: k << 16 | (row - block start)
+  DBuf<double> hval;   // nnz
+  DBuf<i32> zptr, zcol;  // per block: head columns absent from it (partial = 0)
+  DBuf<i32> hcol;      // per head column: original column
+  DBuf<double> part;   // ncols x nblocks
+  DBuf<double> bnd;    // per work item: first / last piece (HeadPiece, ops.cu)
+  Units tail;
+  bool built() const { return ncols > 0; }
 };
 
 // SELL-32 copy of a CSR (built on demand for L2-resident systems): rows in
@@ -131,6 +158,21 @@ struct Sell {
   DBuf<i32> off;  // chunks + 1 (entries)
   DBuf<i32> idx;  // slots (padding never read)
   DBuf<double> val;
+};
+
+// Hot-relabelled SELL-32 copy of a large (HBM-streamed) CSR for the forward
+// product: columns renumbered by descending nnz count (hot[k] = original id of
+// relabelled column k), each row's entries sorted by the new id.  Lane l of a
+// warp walks row 32c + l, so the k-th gather of the 32 rows of a chunk hits the
+// few cache lines of x that hold the hottest columns (Zipf-headed matrices:
+// ~40% fewer L1 wavefronts than gathering by original id).  x is permuted into
+// xr (n doubles) before each product.
+struct HotSell {
+  Sell s;
+  i64 n = 0;
+  DBuf<i32> hot;    // n: relabelled -> original column
+  DBuf<double> xr;  // n: x in relabelled order (scratch of each product)
+  bool built() const { return s.chunks > 0; }
 };
 
 }  // namespace apc
@@ -186,6 +228,8 @@ struct apc_mat {
   apc::Csr a;               // CSR of the local rows (mloc x n)
   apc::Csr at;              // CSR of their transpose (n x mloc)
   apc::Sell sell;           // SELL-32 copy of `a` (persistent LSQR, built lazily)
+  apc::HotSell hot;         // hot-relabelled SELL-32 of `a` (large CSR forward, built at upload)
+  apc::HeadAdj head;        // row-blocked A^T u of the long rows of `at` (built with `hot`)
   apc::i64 nnz_global = 0;
   apc::i64 mloc() const { return r1 - r0; }
 };

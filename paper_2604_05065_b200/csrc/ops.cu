@@ -3,6 +3,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -144,6 +146,10 @@ __global__ void expand_cols_kernel(const int* colptr, long long ncols, long long
   }
   colof[k] = static_cast<int>(lo);
 }
+__global__ void fill_int_kernel(int* p, long long n, int v) {
+  long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) p[k] = v;
+}
 __global__ void iota_kernel(int* p, long long n) {
   long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k < n) p[k] = static_cast<int>(k);
@@ -171,6 +177,51 @@ __global__ void row_ptr_kernel(const int* sorted_rows, long long nnz, long long 
 
 inline unsigned nblk(long long n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
+// ---- hot-relabelled SELL-32 build (HotSell, apc_internal.hpp)
+__device__ __forceinline__ long long upper_slot(const int* ptr, long long n, long long p) {
+  long long lo = 0, hi = n;  // last k with ptr[k] <= p
+  while (hi - lo > 1) {
+    const long long mid = (lo + hi) >> 1;
+    if (ptr[mid] <= p) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+// entry p of the relabelled column order: key = its row, value = p
+__global__ void hot_keys_kernel(const int* nptr, const int* hot, const int* tptr, const int* trow, long long n,
+                                long long nnz, int* keys, int* vals) {
+  const long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= nnz) return;
+  const long long k = upper_slot(nptr, n, p);
+  keys[p] = trow[tptr[hot[k]] + (p - nptr[k])];
+  vals[p] = static_cast<int>(p);
+}
+__global__ void hot_width_kernel(const int* __restrict__ ptr, long long rows, long long chunks, int* __restrict__ width) {
+  const long long ch = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (ch > chunks) return;
+  int w = 0;
+  if (ch < chunks) {
+    const long long rend = ch * 32 + 32 < rows ? ch * 32 + 32 : rows;
+    for (long long r = ch * 32; r < rend; ++r) w = max(w, ptr[r + 1] - ptr[r]);
+  }
+  width[ch] = 32 * w;
+}
+// sorted entry q (row-major, relabelled column order within rows) -> its SELL slot
+__global__ void hot_fill_kernel(const int* sorted_vals, const int* rptr, const int* off, const int* nptr,
+                                const int* hot, const int* tptr, const double* tval, long long n, long long rows,
+                                int* sidx, double* sval) {
+  const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const long long base = off[r >> 5] + (r & 31);
+  const int b = rptr[r], e = rptr[r + 1];
+  for (int q = b; q < e; ++q) {
+    const long long p = sorted_vals[q];
+    const long long k = upper_slot(nptr, n, p);
+    sidx[base + 32LL * (q - b)] = static_cast<int>(k);
+    sval[base + 32LL * (q - b)] = tval[tptr[hot[k]] + (p - nptr[k])];
+  }
+}
+
 // sum of the partials of every split row (rows longer than one work unit),
 // block per split row, fixed order: written to out[row] so every consumer of
 // op_adj_raw (LSQR epilogue, NCCL allreduce, op_adj) reads plain values
@@ -187,9 +238,279 @@ split_fixup_kernel(const int* __restrict__ srows, const int* __restrict__ rfirst
   if (threadIdx.x == 0) out[j] = s;
 }
 
+// ---- row-blocked A^T u of the head rows (HeadAdj, apc_internal.hpp)
+// Work item = (block b, part p): a contiguous, 128-aligned range of block b's
+// head entries.  The CTA stages block b's u in shared memory; each warp walks a
+// contiguous sub-range, 128 entries per step (lane = 4 consecutive entries,
+// vector loads), and closes (head column) pieces with a lane-local segmented
+// prefix + one warp segmented scan.  Pieces interior to a warp range are
+// complete (column, block) sums and are stored directly; the first and the
+// last piece of each range are chained across the warps in order (one
+// thread), then across the parts of a block (head_bnd_kernel).  Every sum has
+// a fixed order.
+struct HeadPiece {
+  int fk, lk;  // first / last piece column (-1: none)
+  double fs, ls;
+};
+
+// chain step: piece (pk, ps) follows the open piece (k, s)
+__device__ __forceinline__ void head_chain(int& k, double& s, int pk, double ps, int& fk, double& fs, bool& first,
+                                           double* part, long long nblocks, long long blk) {
+  if (pk < 0) return;
+  if (pk == k) {
+    s += ps;
+    return;
+  }
+  if (k >= 0) {
+    if (first) {
+      fk = k;
+      fs = s;
+      first = false;
+    } else {
+      part[static_cast<long long>(k) * nblocks + blk] = s;
+    }
+  }
+  k = pk;
+  s = ps;
+}
+
+__global__ void __launch_bounds__(kHeadThreads)
+head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, const double* __restrict__ hval,
+                const double* __restrict__ u, long long mloc, long long nblocks, int parts,
+                const int* __restrict__ zptr, const int* __restrict__ zcol, double* __restrict__ part,
+                HeadPiece* __restrict__ bnd, const int* done) {
+  constexpr int NW = kHeadThreads / 32;
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ double us[];
+  __shared__ HeadPiece pc[NW];
+  if (done && *done) return;
+  const int nb = static_cast<int>(nblocks);
+  const int blk = blockIdx.x / parts;
+  const int prt = blockIdx.x % parts;
+  const long long r0 = static_cast<long long>(blk) * kHeadRows;
+  const int nr = static_cast<int>(mloc - r0 < kHeadRows ? mloc - r0 : kHeadRows);
+  for (int i = threadIdx.x; i < nr; i += kHeadThreads) us[i] = __ldcg(u + r0 + i);
+  if (prt == 0)
+    for (int z = __ldg(zptr + blk) + threadIdx.x; z < __ldg(zptr + blk + 1); z += kHeadThreads)
+      part[__ldg(zcol + z) * nb + blk] = 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int b0 = __ldg(bptr + blk), b1 = __ldg(bptr + blk + 1);  // multiples of 128
+  const int pper = (((b1 - b0) >> 7) + parts - 1) / parts * 128;
+  const int p0 = min(b1, b0 + prt * pper), p1 = min(b1, p0 + pper);
+  const int wper = (((p1 - p0) >> 7) + NW - 1) / NW * 128;
+  const int rb = min(p1, p0 + w * wper), re = min(p1, rb + wper);
+  int ck = -1, fk = -1;  // open (carried) piece, first closed piece (warp-uniform)
+  double cs = 0.0, fs = 0.0;
+  const int4* kp = reinterpret_cast<const int4*>(hkey) + lane;
+  const double2* vp = reinterpret_cast<const double2*>(hval) + 2 * lane;
+  // software pipeline: the next step's entries are in flight while this one is scanned
+  int4 nkq = make_int4(0, 0, 0, 0);
+  double2 nva = make_double2(0.0, 0.0), nvb = nva;
+  if (rb < re) {
+    nkq = __ldcs(kp + (rb >> 2));
+    nva = __ldcs(vp + (rb >> 1));
+    nvb = __ldcs(vp + (rb >> 1) + 1);
+  }
+  for (int e = rb; e < re; e += 128) {
+    const int4 kq = nkq;
+    const double2 va = nva, vb = nvb;
+    if (e + 128 < re) {
+      nkq = __ldcs(kp + ((e + 128) >> 2));
+      nva = __ldcs(vp + ((e + 128) >> 1));
+      nvb = __ldcs(vp + ((e + 128) >> 1) + 1);
+    }
+    // padding keys carry column kHeadPad and row 0 (value 0): a run that is never stored
+    const int k0 = kq.x >> 16, k1 = kq.y >> 16, k2 = kq.z >> 16, k3 = kq.w >> 16;
+    double x0 = va.x * us[kq.x & (kHeadRows - 1)];
+    const double x1 = va.y * us[kq.y & (kHeadRows - 1)];
+    const double x2 = vb.x * us[kq.z & (kHeadRows - 1)];
+    const double x3 = vb.y * us[kq.w & (kHeadRows - 1)];
+    const int kl0 = __shfl_sync(FULL, k0, 0);
+    if (ck >= 0 && kl0 != ck) {  // the carried piece ended with the previous step
+      if (fk < 0) {
+        fk = ck;
+        fs = cs;
+      } else if (lane == 0) {
+        part[ck * nb + blk] = cs;
+      }
+      ck = -1;
+    }
+    if (lane == 0 && k0 == ck) x0 = cs + x0;  // carried sum first
+    const int kprev = __shfl_up_sync(FULL, k3, 1);
+    const bool h0 = lane == 0 || k0 != kprev;
+    const bool h1 = k1 != k0, h2 = k2 != k1, h3 = k3 != k2;
+    const double q0 = x0;
+    const double q1 = h1 ? x1 : q0 + x1;
+    const double q2 = h2 ? x2 : q1 + x2;
+    const double q3 = h3 ? x3 : q2 + x3;
+    // warp segmented inclusive scan of (head seen, open-run sum) over lanes
+    bool F = h0 || h1 || h2 || h3;
+    double A = q3;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double Au = __shfl_up_sync(FULL, A, d);
+      const bool Fu = __shfl_up_sync(FULL, F ? 1 : 0, d) != 0;
+      const bool in = lane >= d;
+      A = (in && !F) ? Au + A : A;
+      F = F || (in && Fu);
+    }
+    const double E = __shfl_up_sync(FULL, A, 1);  // sum carried into this lane's first run
+    const double y0 = h0 ? q0 : E + q0;
+    const double y1 = (h0 || h1) ? q1 : E + q1;
+    const double y2 = (h0 || h1 || h2) ? q2 : E + q2;
+    const double y3 = (h0 || h1 || h2 || h3) ? q3 : E + q3;
+    const int knext = __shfl_down_sync(FULL, k0, 1);
+    bool e0 = k0 != kHeadPad && k0 != k1;
+    bool e1 = k1 != kHeadPad && k1 != k2;
+    bool e2 = k2 != kHeadPad && k2 != k3;
+    bool e3 = k3 != kHeadPad && lane < 31 && k3 != knext;  // lane 31's last entry stays open
+    const unsigned m = __ballot_sync(FULL, e0 || e1 || e2 || e3);
+    // this lane's first closed piece (used when it is the range's first piece)
+    const int jk = e0 ? k0 : e1 ? k1 : e2 ? k2 : k3;
+    const double js = e0 ? y0 : e1 ? y1 : e2 ? y2 : y3;
+    const int fl = (__ffs(m) - 1) & 31;
+    const int bk = __shfl_sync(FULL, jk, fl);
+    const double bs = __shfl_sync(FULL, js, fl);
+    if (m != 0 && fk < 0) {
+      fk = bk;
+      fs = bs;
+      if (lane == fl) {
+        if (e0) e0 = false;
+        else if (e1) e1 = false;
+        else if (e2) e2 = false;
+        else e3 = false;
+      }
+    }
+    const int pb = blk;
+    if (e0) part[k0 * nb + pb] = y0;
+    if (e1) part[k1 * nb + pb] = y1;
+    if (e2) part[k2 * nb + pb] = y2;
+    if (e3) part[k3 * nb + pb] = y3;
+    ck = __shfl_sync(FULL, k3, 31);
+    cs = __shfl_sync(FULL, y3, 31);
+    if (ck == kHeadPad) ck = -1;
+  }
+  if (lane == 0) pc[w] = fk < 0 ? HeadPiece{ck, -1, cs, 0.0} : HeadPiece{fk, ck, fs, cs};
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int k = -1, f = -1;
+    double sum = 0.0, fsum = 0.0;
+    bool first = parts > 1;  // with one part per block the CTA's pieces are all complete
+    for (int i = 0; i < NW; ++i) {
+      const HeadPiece P = pc[i];
+      head_chain(k, sum, P.fk, P.fs, f, fsum, first, part, nblocks, blk);
+      head_chain(k, sum, P.lk, P.ls, f, fsum, first, part, nblocks, blk);
+    }
+    if (parts > 1) {
+      bnd[blockIdx.x] = first ? HeadPiece{k, -1, sum, 0.0} : HeadPiece{f, k, fsum, sum};
+    } else if (k >= 0) {
+      part[static_cast<long long>(k) * nblocks + blk] = sum;
+    }
+  }
+}
+
+// pieces at the part boundaries of each block, chained in part order
+__global__ void head_bnd_kernel(const HeadPiece* __restrict__ bnd, int parts, long long nblocks,
+                                double* __restrict__ part, const int* done) {
+  if (done && *done) return;
+  const long long blk = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (blk >= nblocks) return;
+  int k = -1, f = -1;
+  double sum = 0.0, fsum = 0.0;
+  bool first = false;
+  for (int i = 0; i < parts; ++i) {
+    const HeadPiece P = bnd[blk * parts + i];
+    head_chain(k, sum, P.fk, P.fs, f, fsum, first, part, nblocks, blk);
+    head_chain(k, sum, P.lk, P.ls, f, fsum, first, part, nblocks, blk);
+  }
+  if (k >= 0) part[static_cast<long long>(k) * nblocks + blk] = sum;
+}
+
+// warp per head column: its partials in block order -> out[col]
+__global__ void __launch_bounds__(256)
+head_combine_kernel(const double* __restrict__ part, long long nblocks, const int* __restrict__ hcol,
+                    long long ncols, double* __restrict__ out, const int* done) {
+  if (done && *done) return;
+  const long long k = (static_cast<long long>(blockIdx.x) * 256 + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (k >= ncols) return;
+  const double* pk = part + k * nblocks;
+  double s = 0.0;
+  for (long long q = lane; q < nblocks; q += 32) s += pk[q];
+  s = warp_sum(s);
+  if (lane == 0) out[__ldg(hcol + k)] = s;
+}
+
 }  // namespace
 
-unsigned fwd_gs_grid(apc_ctx* ctx, const void* kfn) {
+__global__ void hot_permute_kernel(const int* __restrict__ hot, long long n, const double* __restrict__ x,
+                                   double* __restrict__ xr) {
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) xr[k] = __ldg(x + __ldg(hot + k));
+}
+
+void build_hot_sell(apc_mat& a, const std::vector<long long>& col_nnz) {
+  apc_ctx* ctx = a.ctx;
+  cudaStream_t st = ctx->stream;
+  const long long n = a.n, rows = a.a.rows, nnz = a.a.nnz;
+  HotSell& h = a.hot;
+  h.s = Sell();
+  if (rows == 0 || nnz == 0) return;
+  // relabel: descending column length, ties by original id
+  std::vector<int> hot(n), nptr(n + 1);
+  for (long long j = 0; j < n; ++j) hot[j] = static_cast<int>(j);
+  std::stable_sort(hot.begin(), hot.end(), [&](int x, int y) { return col_nnz[x] > col_nnz[y]; });
+  nptr[0] = 0;
+  for (long long k = 0; k < n; ++k) nptr[k + 1] = nptr[k] + static_cast<int>(col_nnz[hot[k]]);
+  h.n = n;
+  h.hot.alloc(n);
+  h.xr.alloc(n);
+  DBuf<int> dn(n + 1), keys(nnz), vals(nnz), kout(nnz), vout(nnz);
+  APC_CUDA(cudaMemcpyAsync(h.hot.p, hot.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  APC_CUDA(cudaMemcpyAsync(dn.p, nptr.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice, st));
+  hot_keys_kernel<<<nblk(nnz, 256), 256, 0, st>>>(dn.p, h.hot.p, a.at.ptr.p, a.at.idx.p, n, nnz, keys.p, vals.p);
+  int end_bit = 1;
+  while ((1LL << end_bit) < rows + 1 && end_bit < 31) ++end_bit;
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, kout.p, vals.p, vout.p, static_cast<int>(nnz), 0,
+                                  end_bit, st);
+  DBuf<char> tmp(static_cast<long long>(std::max<size_t>(tmp_bytes, 1)));
+  APC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, kout.p, vals.p, vout.p, static_cast<int>(nnz),
+                                           0, end_bit, st));
+  Sell& s = h.s;
+  s.rows = rows;
+  s.chunks = (rows + 31) / 32;
+  s.off.alloc(s.chunks + 1);
+  DBuf<int> width(s.chunks + 1);
+  hot_width_kernel<<<nblk(s.chunks + 1, 256), 256, 0, st>>>(a.a.ptr.p, rows, s.chunks, width.p);
+  size_t stmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, stmp, width.p, s.off.p, static_cast<int>(s.chunks + 1), st);
+  DBuf<char> sbuf(static_cast<long long>(std::max<size_t>(stmp, 1)));
+  APC_CUDA(cub::DeviceScan::ExclusiveSum(sbuf.p, stmp, width.p, s.off.p, static_cast<int>(s.chunks + 1), st));
+  int slots = 0;
+  copy_sync(st, &slots, s.off.p + s.chunks, sizeof(int), cudaMemcpyDeviceToHost);
+  s.slots = slots;
+  s.idx.alloc(std::max(1, slots));
+  s.val.alloc(std::max(1, slots));
+  if (slots > nnz) {  // padding of ragged chunks (never read: rows stop at their length)
+    APC_CUDA(cudaMemsetAsync(s.idx.p, 0, s.idx.bytes(), st));
+    APC_CUDA(cudaMemsetAsync(s.val.p, 0, s.val.bytes(), st));
+  }
+  hot_fill_kernel<<<nblk(rows, 256), 256, 0, st>>>(vout.p, a.a.ptr.p, s.off.p, dn.p, h.hot.p, a.at.ptr.p, a.at.val.p,
+                                                  n, rows, s.idx.p, s.val.p);
+  ctx->launches += 4;
+  APC_CUDA(cudaGetLastError());
+  APC_CUDA(cudaStreamSynchronize(st));
+}
+
+bool hot_sell_wanted(long long nnz) {
+  const char* e = std::getenv("APC_HOT_SELL");
+  if (e) return std::atoi(e) != 0;
+  return nnz >= (1LL << 24);
+}
+
+unsigned fwd_gs_grid(apc_ctx* ctx, const void* kfn, int threads) {
   static std::mutex mu;
   static std::map<std::pair<int, const void*>, unsigned> cache;
   std::lock_guard<std::mutex> lk(mu);
@@ -197,7 +518,7 @@ unsigned fwd_gs_grid(apc_ctx* ctx, const void* kfn) {
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int per_sm = 0;
-  APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kCsrFwdThreads, 0));
+  APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, threads, 0));
   const unsigned g = static_cast<unsigned>(ctx->num_sms * std::max(1, per_sm));
   cache[key] = g;
   return g;
@@ -289,16 +610,36 @@ void op_adj_raw(apc_mat& a, const double* u, double* out, const int* done) {
     return;
   }
   const Csr& c = a.at;
-  if (c.n_units == 0) return;
-  unsigned nb = nblk(c.n_units * 32, kCsrUnitThreads);
-  csr_units_kernel<<<nb, kCsrUnitThreads, 0, st>>>(c.ptr.p, c.idx.p, c.val.p, u, c.n_units,
-                                                   c.urow.p, c.ustart.p, c.uend.p, c.uslot.p, out,
-                                                   c.upart.p, done);
-  a.ctx->launches++;
-  if (c.n_split > 0) {
-    split_fixup_kernel<<<static_cast<unsigned>(c.n_split), 256, 0, st>>>(c.srows.p, c.rfirst.p, c.rcount.p, c.upart.p,
-                                                                         out, done);
-    a.ctx->launches++;
+  if (a.head.built()) {
+    const HeadAdj& h = a.head;
+    launch_units(a.ctx, c, h.tail, u, out, done);
+    head_adj_kernel<<<static_cast<unsigned>(h.nblocks * h.parts), kHeadThreads, sizeof(double) * kHeadRows, st>>>(
+        h.bptr.p, h.hkey.p, h.hval.p, u, a.mloc(), h.nblocks, h.parts, h.zptr.p, h.zcol.p, h.part.p,
+        reinterpret_cast<HeadPiece*>(h.bnd.p), done);
+    if (h.parts > 1) {
+      head_bnd_kernel<<<nblk(h.nblocks, 128), 128, 0, st>>>(reinterpret_cast<const HeadPiece*>(h.bnd.p), h.parts,
+                                                            h.nblocks, h.part.p, done);
+      a.ctx->launches++;
+    }
+    head_combine_kernel<<<nblk(h.ncols * 32, 256), 256, 0, st>>>(h.part.p, h.nblocks, h.hcol.p, h.ncols, out, done);
+    a.ctx->launches += 2;
+    return;
+  }
+  launch_units(a.ctx, c, c, u, out, done);
+}
+
+void launch_units(apc_ctx* ctx, const Csr& c, const Units& un, const double* u, double* out, const int* done) {
+  cudaStream_t st = ctx->stream;
+  if (un.n_units == 0) return;
+  unsigned nb = nblk(un.n_units * 32, kCsrUnitThreads);
+  csr_units_kernel<<<nb, kCsrUnitThreads, 0, st>>>(c.ptr.p, c.idx.p, c.val.p, u, un.n_units,
+                                                   un.urow.p, un.ustart.p, un.uend.p, un.uslot.p, out,
+                                                   un.upart.p, done);
+  ctx->launches++;
+  if (un.n_split > 0) {
+    split_fixup_kernel<<<static_cast<unsigned>(un.n_split), 256, 0, st>>>(un.srows.p, un.rfirst.p, un.rcount.p,
+                                                                          un.upart.p, out, done);
+    ctx->launches++;
   }
 }
 
@@ -332,23 +673,36 @@ void op_adj(apc_mat& a, double mu, bool augmented, const double* u, double* y) {
 // work units for a CSR (host-built from the row lengths)
 // ---------------------------------------------------------------------------
 void build_units(apc_ctx* ctx, Csr& c, const std::vector<long long>& row_nnz) {
-  std::vector<int> urow, ustart, uend, uslot, rfirst(c.rows, -1), rcount(c.rows, 0);
-  urow.reserve(c.rows);
-  long long off = 0, nparts = 0, maxr = 0;
+  std::vector<long long> off(c.rows + 1, 0);
+  long long maxr = 0;
   for (long long r = 0; r < c.rows; ++r) {
-    long long L = row_nnz[r];
-    maxr = std::max(maxr, L);
+    off[r + 1] = off[r] + row_nnz[r];
+    maxr = std::max(maxr, row_nnz[r]);
+  }
+  c.max_row_nnz = maxr;
+  c.avg_row_nnz = c.rows > 0 ? static_cast<double>(off[c.rows]) / static_cast<double>(c.rows) : 0.0;
+  build_units_sel(ctx, c, c.rows, off, row_nnz, nullptr);
+}
+
+void build_units_sel(apc_ctx* ctx, Units& c, long long rows, const std::vector<long long>& off,
+                     const std::vector<long long>& row_nnz, const std::vector<char>* skip) {
+  std::vector<int> urow, ustart, uend, uslot, rfirst(rows, -1), rcount(rows, 0);
+  urow.reserve(rows);
+  long long nparts = 0;
+  for (long long r = 0; r < rows; ++r) {
+    if (skip && (*skip)[r]) continue;
+    const long long L = row_nnz[r], o = off[r];
     if (L <= kCsrUnitMax) {
       urow.push_back(static_cast<int>(r));
-      ustart.push_back(static_cast<int>(off));
-      uend.push_back(static_cast<int>(off + L));
+      ustart.push_back(static_cast<int>(o));
+      uend.push_back(static_cast<int>(o + L));
       uslot.push_back(-1);
     } else {
       long long k = (L + kCsrUnitMax - 1) / kCsrUnitMax;
       rfirst[r] = static_cast<int>(nparts);
       rcount[r] = static_cast<int>(k);
       for (long long q = 0; q < k; ++q) {
-        long long b = off + q * kCsrUnitMax, e = std::min(off + L, b + kCsrUnitMax);
+        long long b = o + q * kCsrUnitMax, e = std::min(o + L, b + kCsrUnitMax);
         urow.push_back(static_cast<int>(r));
         ustart.push_back(static_cast<int>(b));
         uend.push_back(static_cast<int>(e));
@@ -356,16 +710,13 @@ void build_units(apc_ctx* ctx, Csr& c, const std::vector<long long>& row_nnz) {
       }
       nparts += k;
     }
-    off += L;
   }
   c.n_units = static_cast<long long>(urow.size());
   c.n_parts = nparts;
   std::vector<int> srows;
-  for (long long r = 0; r < c.rows; ++r)
+  for (long long r = 0; r < rows; ++r)
     if (rfirst[r] >= 0) srows.push_back(static_cast<int>(r));
   c.n_split = static_cast<long long>(srows.size());
-  c.max_row_nnz = maxr;
-  c.avg_row_nnz = c.rows > 0 ? static_cast<double>(off) / static_cast<double>(c.rows) : 0.0;
   auto up = [&](DBuf<int>& d, const std::vector<int>& h) {
     d.alloc(static_cast<long long>(h.size()));
     if (!h.empty())
@@ -380,6 +731,128 @@ void build_units(apc_ctx* ctx, Csr& c, const std::vector<long long>& row_nnz) {
   up(c.srows, srows);
   c.upart.alloc(std::max<long long>(1, nparts));
   APC_CUDA(cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
+}
+
+// Head/tail split of CSR(A^T) for the row-blocked adjoint (HeadAdj).  Host
+// inputs: CSR(A^T) row offsets and int32 local row indices (the upload's
+// staging copy) and the row lengths.  A row of A^T (column of A) is "head"
+// when it averages >= APC_HEAD_MIN (default 8) entries per block of kHeadRows.
+struct HeadSegs {  // per head column: entry offsets of its segment in each block
+  const int* tptr;
+  const int* hidx;
+  const std::vector<int>* hc;
+  long long nblocks;
+  std::vector<int>* seg;  // ncols x (nblocks + 1)
+  void operator()(long long k0, long long k1) const {
+    for (long long k = k0; k < k1; ++k) {
+      const int j = (*hc)[k];
+      int* sg = seg->data() + k * (nblocks + 1);
+      long long q = tptr[j];
+      const long long e = tptr[j + 1];
+      for (long long b = 0; b < nblocks; ++b) {
+        sg[b] = static_cast<int>(q);
+        const long long lim = (b + 1) * static_cast<long long>(kHeadRows);
+        while (q < e && hidx[q] < lim) ++q;
+      }
+      sg[nblocks] = static_cast<int>(e);
+    }
+  }
+};
+
+// copy of the head entries, block-major: warp per (head column, block) segment
+__global__ void head_pack_kernel(const int* __restrict__ seg, const int* __restrict__ dst, long long ncols,
+                                 long long nblocks, const int* __restrict__ tidx, const double* __restrict__ tval,
+                                 int* __restrict__ hkey, double* __restrict__ hval) {
+  const long long t = (static_cast<long long>(blockIdx.x) * 256 + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= ncols * nblocks) return;
+  const long long k = t / nblocks, b = t % nblocks;
+  const int s0 = seg[k * (nblocks + 1) + b], s1 = seg[k * (nblocks + 1) + b + 1];
+  const int d = dst[b * ncols + k];
+  const int rb = static_cast<int>(b * kHeadRows);
+  for (int q = s0 + lane; q < s1; q += 32) {
+    hkey[d + q - s0] = static_cast<int>(k << 16) | (tidx[q] - rb);  // k < kHeadPad
+    hval[d + q - s0] = tval[q];
+  }
+}
+
+void build_head_adj(apc_mat& a, const std::vector<int>& tptr, const int* hidx, const std::vector<long long>& tlen) {
+  apc_ctx* ctx = a.ctx;
+  cudaStream_t st = ctx->stream;
+  HeadAdj& h = a.head;
+  h = HeadAdj();
+  const long long n = a.n, mloc = a.mloc();
+  const long long nblocks = (mloc + kHeadRows - 1) / kHeadRows;
+  if (nblocks == 0 || n == 0) return;
+  const char* env = std::getenv("APC_HEAD_MIN");
+  const double per_block = env ? std::atof(env) : 8.0;
+  const long long thr = std::max<long long>(64, static_cast<long long>(per_block * static_cast<double>(nblocks)));
+  std::vector<int> hc;
+  std::vector<char> is_head(n, 0);
+  for (long long j = 0; j < n && static_cast<long long>(hc.size()) < kHeadPad; ++j)
+    if (tlen[j] >= thr) {
+      hc.push_back(static_cast<int>(j));
+      is_head[j] = 1;
+    }
+  if (hc.empty()) return;
+  const long long H = static_cast<long long>(hc.size());
+  std::vector<int> seg(static_cast<size_t>(H * (nblocks + 1)));
+  host_parallel_for(H, HeadSegs{tptr.data(), hidx, &hc, nblocks, &seg}, 1);
+  // destination of segment (k, b): block-major, columns ascending within a block
+  std::vector<int> dst(static_cast<size_t>(H * nblocks)), bptr(nblocks + 1, 0), zptr(nblocks + 1, 0), zcol;
+  long long tot = 0;
+  for (long long b = 0; b < nblocks; ++b) {
+    bptr[b] = static_cast<int>(tot);
+    for (long long k = 0; k < H; ++k) {
+      const int len = seg[k * (nblocks + 1) + b + 1] - seg[k * (nblocks + 1) + b];
+      dst[b * H + k] = static_cast<int>(tot);
+      tot += len;
+      if (len == 0) zcol.push_back(static_cast<int>(k));
+    }
+    tot = (tot + 127) / 128 * 128;  // 128-aligned blocks: padding keys are -1
+    zptr[b + 1] = static_cast<int>(zcol.size());
+  }
+  require(tot < (1LL << 31), APC_INVALID_ARGUMENT, "build_head_adj: head entries exceed int32 range");
+  bptr[nblocks] = static_cast<int>(tot);
+  const char* penv = std::getenv("APC_HEAD_PARTS");
+  h.parts = penv ? std::max(1, std::atoi(penv)) : 1;
+  h.ncols = H;
+  h.nblocks = nblocks;
+  h.nnz = tot;
+  auto up = [&](DBuf<int>& d, const std::vector<int>& v) {
+    d.alloc(std::max<long long>(1, static_cast<long long>(v.size())));
+    if (!v.empty()) APC_CUDA(cudaMemcpyAsync(d.p, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  };
+  up(h.bptr, bptr);
+  up(h.zptr, zptr);
+  up(h.zcol, zcol);
+  up(h.hcol, hc);
+  h.hkey.alloc(std::max<long long>(128, tot));
+  h.hval.alloc(std::max<long long>(128, tot));
+  fill_int_kernel<<<nblk(h.hkey.n, 256), 256, 0, st>>>(h.hkey.p, h.hkey.n, kHeadPad << 16);
+  ctx->launches++;
+  APC_CUDA(cudaMemsetAsync(h.hval.p, 0, h.hval.bytes(), st));
+  h.part.alloc(H * nblocks);
+  h.bnd.alloc(nblocks * h.parts * 3);  // HeadPiece = 24 bytes
+  {
+    DBuf<int> dseg(static_cast<long long>(seg.size())), ddst(static_cast<long long>(dst.size()));
+    APC_CUDA(cudaMemcpyAsync(dseg.p, seg.data(), seg.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    APC_CUDA(cudaMemcpyAsync(ddst.p, dst.data(), dst.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    head_pack_kernel<<<nblk(H * nblocks * 32, 256), 256, 0, st>>>(dseg.p, ddst.p, H, nblocks, a.at.idx.p, a.at.val.p,
+                                                                  h.hkey.p, h.hval.p);
+    ctx->launches++;
+    APC_CUDA(cudaGetLastError());
+    APC_CUDA(cudaStreamSynchronize(st));
+  }
+  APC_CUDA(cudaFuncSetAttribute(head_adj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sizeof(double) * kHeadRows)));
+  std::vector<long long> off(n + 1);
+  for (long long j = 0; j <= n; ++j) off[j] = tptr[j];
+  build_units_sel(ctx, h.tail, n, off, tlen, &is_head);  // synchronizes: host vectors may go
+  const char* pe = std::getenv("APC_SETUP_PROF");
+  if (pe && std::atoi(pe) != 0)
+    std::fprintf(stderr, "[apc] head adjoint: %lld head columns (>= %lld nnz), %lld blocks, %lld head nnz, %lld tail units\n",
+                 H, thr, nblocks, tot, h.tail.n_units);
 }
 
 // ---------------------------------------------------------------------------
@@ -490,6 +963,12 @@ void upload_csc(apc_mat& a, const long long* colptr, const long long* rowidx, co
   }
   c.avg_row_nnz = mloc > 0 ? static_cast<double>(nnz) / static_cast<double>(mloc) : 0.0;
   APC_CUDA(cudaGetLastError());
+  if (hot_sell_wanted(nnz)) {
+    ps.reset(new ProfScope("upload.hot_sell"));
+    build_hot_sell(a, tlen);
+    ps.reset(new ProfScope("upload.head_adj"));
+    build_head_adj(a, tptr, hidx, tlen);
+  }
 }
 
 }  // namespace apc

@@ -34,6 +34,15 @@ constexpr int kCsrFwdThreads = 256;
 constexpr int kCsrFwdRowsPerBlock = 256;
 constexpr int kCsrUnitThreads = 256;
 constexpr int kCsrUnitMax = 2048;  // max nnz per work unit of the transpose SpMV
+#ifndef APC_HEAD_ROWS
+#define APC_HEAD_ROWS 8192
+#endif
+#ifndef APC_HEAD_THREADS
+#define APC_HEAD_THREADS 512
+#endif
+constexpr int kHeadRows = APC_HEAD_ROWS;  // rows of A per block of the head adjoint (u block in shared memory)
+constexpr int kHeadThreads = APC_HEAD_THREADS;
+constexpr int kHeadPad = 0x7fff;   // column of the padding entries (head columns are below it)
 
 // ---------------------------------------------------------------------------
 // forward epilogue interface:
@@ -235,6 +244,71 @@ csr_fwd_gs_kernel(const int* __restrict__ ptr, const int* __restrict__ idx, cons
 }
 
 // ---------------------------------------------------------------------------
+// Large CSR through the hot-relabelled SELL-32 copy (HotSell): lane = row, the
+// co-resident CTAs walk 32-row chunks grid-stride (one epilogue slot per CTA).
+// idx/val of entry k of the chunk's 32 rows are one coalesced 128 B / 256 B
+// line each; each row is still summed sequentially (in relabelled column
+// order), and the row's epilogue input (u_r) is a coalesced load too.
+// ---------------------------------------------------------------------------
+#ifndef APC_HOT_KU
+#define APC_HOT_KU 16
+#endif
+#ifndef APC_HOT_MINB
+#define APC_HOT_MINB 4
+#endif
+constexpr int kHotThreads = 256;
+
+__global__ void hot_permute_kernel(const int* __restrict__ hot, long long n, const double* __restrict__ x,
+                                   double* __restrict__ xr);
+
+template <class Epi>
+__global__ void __launch_bounds__(kHotThreads, APC_HOT_MINB)
+hot_sell_fwd_kernel(const int* __restrict__ ptr, const int* __restrict__ off, const int* __restrict__ sidx,
+                    const double* __restrict__ sval, long long rows, long long chunks,
+                    const double* __restrict__ xr, const int* done, Epi epi) {
+  constexpr int KU = APC_HOT_KU;
+  __shared__ double red[32];
+  if (done && *done) return;
+  epi.begin();
+  const int lane = threadIdx.x & 31;
+  const long long wstride = static_cast<long long>(gridDim.x) * (kHotThreads / 32);
+  double sq = 0.0;
+  for (long long ch = static_cast<long long>(blockIdx.x) * (kHotThreads / 32) + (threadIdx.x >> 5); ch < chunks;
+       ch += wstride) {
+    const long long r = ch * 32 + lane;
+    const bool ok = r < rows;
+    int len = 0;
+    double pre = 0.0;
+    if (ok) {
+      const int b = __ldg(ptr + r);
+      len = __ldg(ptr + r + 1) - b;
+      pre = epi.load(r);
+    }
+    const int o = __ldg(off + ch);
+    const int w = (__ldg(off + ch + 1) - o) >> 5;
+    const int* ip = sidx + o + lane;
+    const double* vp = sval + o + lane;
+    double s = 0.0;
+    for (int k = 0; k < w; k += KU) {
+      int id[KU];
+      double v[KU];
+#pragma unroll
+      for (int q = 0; q < KU; ++q) {
+        const bool on = k + q < len;
+        id[q] = on ? __ldcs(ip + 32 * (k + q)) : 0;
+        v[q] = on ? __ldcs(vp + 32 * (k + q)) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < KU; ++q)
+        if (k + q < len) s += v[q] * __ldg(xr + id[q]);
+    }
+    if (ok) sq += epi.row(r, s, pre);
+  }
+  sq = block_sum<kHotThreads>(sq, red);
+  epi.tile_done(blockIdx.x, gridDim.x, sq);
+}
+
+// ---------------------------------------------------------------------------
 // CSR A^T u over nnz-balanced work units (one warp per unit).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kCsrUnitThreads)
@@ -276,6 +350,13 @@ void op_adj_raw(apc_mat& a, const double* u, double* out, const int* done);
 // device CSR build from host CSC (matrix upload)
 void upload_csc(apc_mat& a, const long long* colptr, const long long* rowidx, const double* val);
 void build_units(apc_ctx* ctx, apc::Csr& c, const std::vector<long long>& row_nnz);
+// units over the rows of a CSR with explicit row offsets, skipping rows with skip[r] != 0
+void build_units_sel(apc_ctx* ctx, apc::Units& u, long long rows, const std::vector<long long>& off,
+                     const std::vector<long long>& row_nnz, const std::vector<char>* skip);
+void launch_units(apc_ctx* ctx, const apc::Csr& c, const apc::Units& un, const double* u, double* out,
+                  const int* done);
+// head/tail split of CSR(A^T) for the row-blocked adjoint (called at upload)
+void build_head_adj(apc_mat& a, const std::vector<int>& tptr, const int* hidx, const std::vector<long long>& tlen);
 
 template <class Epi>
 void launch_dense_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaStream_t st) {
@@ -289,13 +370,25 @@ void launch_dense_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cud
 }
 
 // co-resident CTAs of a grid-stride forward kernel (cached occupancy)
-unsigned fwd_gs_grid(apc_ctx* ctx, const void* kfn);
+unsigned fwd_gs_grid(apc_ctx* ctx, const void* kfn, int threads = kCsrFwdThreads);
+// hot-relabelled SELL-32 copy of a large CSR (called at upload)
+void build_hot_sell(apc_mat& a, const std::vector<long long>& col_nnz);
 
 template <class Epi>
 void launch_csr_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaStream_t st) {
   const long long rows = a.a.rows;
   const unsigned nb = static_cast<unsigned>((rows + kCsrFwdRowsPerBlock - 1) / kCsrFwdRowsPerBlock);
   if (nb == 0) return;
+  if (a.hot.built()) {
+    // grid <= nb keeps the epilogue's slots within fwd_num_tiles(a)
+    const unsigned grid =
+        std::min<unsigned>(nb, fwd_gs_grid(a.ctx, reinterpret_cast<const void*>(hot_sell_fwd_kernel<Epi>), kHotThreads));
+    hot_permute_kernel<<<static_cast<unsigned>((a.n + 255) / 256), 256, 0, st>>>(a.hot.hot.p, a.n, x, a.hot.xr.p);
+    hot_sell_fwd_kernel<Epi><<<grid, kHotThreads, 0, st>>>(a.a.ptr.p, a.hot.s.off.p, a.hot.s.idx.p, a.hot.s.val.p,
+                                                           rows, a.hot.s.chunks, a.hot.xr.p, done, epi);
+    a.ctx->launches += 2;
+    return;
+  }
   const bool big = rows >= (1LL << 21);
 #define APC_FWD_CASE(GG)                                                                                      \
   case GG:                                                                                                    \
