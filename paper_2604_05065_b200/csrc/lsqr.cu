@@ -469,18 +469,48 @@ pc_expand_kernel(LsqrPtrs P, int kind, const double* __restrict__ B, long long l
                  const double* __restrict__ x, double* __restrict__ out, int mode,
                  const int* done) {
   __shared__ double sh[32];
+  // implicit basis: R^T rows longer than kExpandLong (the Zipf-head columns of
+  // a sparse A appear in most selected rows) are summed by a whole warp
+  // instead of one thread, so one column does not serialise the launch
+  constexpr int kExpandLong = 32;
+  __shared__ int defer[kVecThreads];
+  __shared__ double dacc[kVecThreads];
+  __shared__ int ndefer;
   if (done && *done) return;
   long long j = static_cast<long long>(blockIdx.x) * kVecThreads + threadIdx.x;
   const long long n = P.n;
   double beta = 0.0;
   if (mode == 1) beta = sqrt(P.g[n] + P.st->tail_norm2);
   double sq = 0.0;
+  double acc = 0.0;
+  bool deferred = false;
+  if (kind != 1) {
+    if (threadIdx.x == 0) ndefer = 0;
+    __syncthreads();
+    if (j < n) {
+      const int q0 = tptr[j], q1 = tptr[j + 1];
+      if (q1 - q0 > kExpandLong) {
+        defer[atomicAdd(&ndefer, 1)] = threadIdx.x;
+        deferred = true;
+      } else {
+        for (int q = q0; q < q1; ++q) acc += tval[q] * s[tidx[q]];
+      }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    for (int d = threadIdx.x >> 5; d < ndefer; d += kVecThreads / 32) {
+      const long long jj = static_cast<long long>(blockIdx.x) * kVecThreads + defer[d];
+      double a = 0.0;
+      for (int q = tptr[jj] + lane; q < tptr[jj + 1]; q += 32) a += tval[q] * s[tidx[q]];
+      a = warp_sum(a);
+      if (lane == 0) dacc[defer[d]] = a;
+    }
+    __syncthreads();
+    if (deferred) acc = dacc[threadIdx.x];
+  }
   if (j < n) {
-    double acc = 0.0;
     if (kind == 1) {
       for (long long t = 0; t < l; ++t) acc += B[t * n + j] * s[t];
-    } else {
-      for (int q = tptr[j]; q < tptr[j + 1]; ++q) acc += tval[q] * s[tidx[q]];
     }
     const double o = x[j] + acc;
     if (mode == 0) {

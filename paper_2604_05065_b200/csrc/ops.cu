@@ -225,17 +225,20 @@ __global__ void hot_fill_kernel(const int* sorted_vals, const int* rptr, const i
 // sum of the partials of every split row (rows longer than one work unit),
 // block per split row, fixed order: written to out[row] so every consumer of
 // op_adj_raw (LSQR epilogue, NCCL allreduce, op_adj) reads plain values
+// split rows of a units CSR: warp per row adds its partials in slot order
 __global__ void __launch_bounds__(256)
 split_fixup_kernel(const int* __restrict__ srows, const int* __restrict__ rfirst, const int* __restrict__ rcount,
-                   const double* __restrict__ upart, double* __restrict__ out, const int* done) {
-  __shared__ double red[32];
+                   long long n_split, const double* __restrict__ upart, double* __restrict__ out, const int* done) {
   if (done && *done) return;
-  const int j = srows[blockIdx.x];
+  const long long r = (static_cast<long long>(blockIdx.x) * 256 + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= n_split) return;
+  const int j = srows[r];
   const int f = rfirst[j], cnt = rcount[j];
   double s = 0.0;
-  for (int k = threadIdx.x; k < cnt; k += 256) s += upart[f + k];
-  s = block_sum<256>(s, red);
-  if (threadIdx.x == 0) out[j] = s;
+  for (int k = lane; k < cnt; k += 32) s += upart[f + k];
+  s = warp_sum(s);
+  if (lane == 0) out[j] = s;
 }
 
 // ---- row-blocked A^T u of the head rows (HeadAdj, apc_internal.hpp)
@@ -637,8 +640,8 @@ void launch_units(apc_ctx* ctx, const Csr& c, const Units& un, const double* u, 
                                                    un.upart.p, done);
   ctx->launches++;
   if (un.n_split > 0) {
-    split_fixup_kernel<<<static_cast<unsigned>(un.n_split), 256, 0, st>>>(un.srows.p, un.rfirst.p, un.rcount.p,
-                                                                          un.upart.p, out, done);
+    split_fixup_kernel<<<nblk(un.n_split * 32, 256), 256, 0, st>>>(un.srows.p, un.rfirst.p, un.rcount.p, un.n_split,
+                                                                    un.upart.p, out, done);
     ctx->launches++;
   }
 }
