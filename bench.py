@@ -152,9 +152,13 @@ def hbm_operator_pair(apc, ctx, cfg_id, reps=20):
         byts = 24 * p.nnz + 4 * (p.m + 1) + 4 * (p.n + 1) + 16 * (p.m + p.n)
     else:
         byts = 16 * p.m * p.n + 16 * (p.m + p.n)
+    kernels = ("hot_permute_kernel + hot_sell_fwd_kernel (hot-relabelled SELL-32) | csr_units_kernel (tail rows of A^T) "
+               "+ head_adj_kernel (row-blocked head rows, u in shared memory) + head_combine_kernel"
+               if p.sparse else "dense_fwd_kernel | dense_adj_kernel")
     A.free()
     del p
-    return {"fwd_us": tf * 1e6, "adj_us": ta * 1e6, "bytes": byts, "GBps": byts / (tf + ta) / 1e9}
+    return {"fwd_us": tf * 1e6, "adj_us": ta * 1e6, "bytes": byts, "GBps": byts / (tf + ta) / 1e9,
+            "kernels": kernels}
 
 
 def cpu_time_to_tol(ref, rp, p, sample_iters=1200):

@@ -510,7 +510,7 @@ void build_hot_sell(apc_mat& a, const std::vector<long long>& col_nnz) {
 bool hot_sell_wanted(long long nnz) {
   const char* e = std::getenv("APC_HOT_SELL");
   if (e) return std::atoi(e) != 0;
-  return nnz >= (1LL << 24);
+  return nnz * 12 > (96LL << 20);  // HBM-streamed (the persistent kernel takes the L2-resident ones)
 }
 
 unsigned fwd_gs_grid(apc_ctx* ctx, const void* kfn, int threads) {

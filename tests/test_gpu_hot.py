@@ -2,8 +2,8 @@
 ops.cuh `hot_sell_fwd_kernel`, A*x gathering x by columns renumbered by
 descending nnz count) and the row-blocked head adjoint (HeadAdj, ops.cu
 `head_adj_kernel`, A^T*u of the long rows of A^T with u staged in shared
-memory, the rest through work units).  Both are built at upload for
-nnz >= 2^24; APC_HOT_SELL=1 forces them on the small matrices here so their
+memory, the rest through work units).  Both are built at upload when the
+CSR is HBM-streamed (12 nnz > 96 MB); APC_HOT_SELL=1 forces them on the small matrices here so their
 results can be checked against the reference Matrix::matvec /
 matvec_transpose (matrix.hpp:151-195) with the componentwise summation bound,
 and whole solves against the default CSR path."""
