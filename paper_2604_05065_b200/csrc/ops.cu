@@ -792,7 +792,9 @@ void build_head_adj(apc_mat& a, const std::vector<int>& tptr, const int* hidx, c
   const long long thr = std::max<long long>(64, static_cast<long long>(per_block * static_cast<double>(nblocks)));
   std::vector<int> hc;
   std::vector<char> is_head(n, 0);
-  for (long long j = 0; j < n && static_cast<long long>(hc.size()) < kHeadPad; ++j)
+  // head column ids fit below kHeadPad, and the (column, block) partial index in int32
+  const long long hmax = std::min<long long>(kHeadPad, ((1LL << 31) - 1) / nblocks);
+  for (long long j = 0; j < n && static_cast<long long>(hc.size()) < hmax; ++j)
     if (tlen[j] >= thr) {
       hc.push_back(static_cast<int>(j));
       is_head[j] = 1;
