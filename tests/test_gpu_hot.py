@@ -116,3 +116,27 @@ def test_head_adjoint_blocks_and_split_tail(apc, ref, ctx, monkeypatch, parts):
     assert np.array_equal(A.apply(u, transpose=True), g)
     x = rng.standard_normal(len(lens))
     assert np.allclose(A.apply(x), ref.matvec(rp, x), rtol=1e-13, atol=1e-13)
+
+
+def test_hot_row_shard_products_and_sharded_entry(apc, ctx, monkeypatch):
+    # a row shard builds its own hot SELL / head blocks over its local rows
+    p = apc.Problem(5, 30000, 3000)
+    monkeypatch.setenv("APC_HOT_SELL", "0")
+    A = apc.DeviceMatrix.from_problem(ctx, p)
+    monkeypatch.setenv("APC_HOT_SELL", "1")
+    monkeypatch.setenv("APC_HEAD_MIN", "2")
+    r0, r1 = 4321, 21000
+    S = apc.DeviceMatrix.from_problem(ctx, p, r0, r1)
+    x = np.random.default_rng(0).standard_normal(p.n)
+    np.testing.assert_allclose(S.apply(x), A.apply(x)[r0:r1], rtol=1e-12, atol=1e-14)
+    u = np.random.default_rng(1).standard_normal(r1 - r0)
+    full_u = np.zeros(p.m)
+    full_u[r0:r1] = u
+    np.testing.assert_allclose(S.apply(u, transpose=True), A.apply(full_u, transpose=True), rtol=1e-11, atol=1e-13)
+    # single-rank sharded entry over the hot layout agrees with the default path
+    H = apc.DeviceMatrix.from_problem(ctx, p)
+    cfg = apc.SolverConfig(mu=1e-6, eps_lsqr=1e-8, block=20, max_rank=40, seed=1, trace_sample_stride=0)
+    g0 = apc.aplicur_solve(A, p.b, cfg)
+    g1 = apc.aplicur_solve(H, p.b, cfg, full=H)
+    assert np.array_equal(g0.row_indices, g1.row_indices)
+    assert abs(g1.lsqr_iters - g0.lsqr_iters) <= max(2, 0.05 * g0.lsqr_iters)
