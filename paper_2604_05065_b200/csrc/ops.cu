@@ -297,39 +297,75 @@ head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, cons
     for (int z = __ldg(zptr + blk) + threadIdx.x; z < __ldg(zptr + blk + 1); z += kHeadThreads)
       part[__ldg(zcol + z) * nb + blk] = 0.0;
   __syncthreads();
+  constexpr int KL = kHeadPerLane, STEP = 32 * KL;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int b0 = __ldg(bptr + blk), b1 = __ldg(bptr + blk + 1);  // multiples of 128
-  const int pper = (((b1 - b0) >> 7) + parts - 1) / parts * 128;
+  const int b0 = __ldg(bptr + blk), b1 = __ldg(bptr + blk + 1);  // multiples of STEP
+  const int pper = ((b1 - b0) / STEP + parts - 1) / parts * STEP;
   const int p0 = min(b1, b0 + prt * pper), p1 = min(b1, p0 + pper);
-  const int wper = (((p1 - p0) >> 7) + NW - 1) / NW * 128;
+  const int wper = ((p1 - p0) / STEP + NW - 1) / NW * STEP;
   const int rb = min(p1, p0 + w * wper), re = min(p1, rb + wper);
   int ck = -1, fk = -1;  // open (carried) piece, first closed piece (warp-uniform)
   double cs = 0.0, fs = 0.0;
-  const int4* kp = reinterpret_cast<const int4*>(hkey) + lane;
-  const double2* vp = reinterpret_cast<const double2*>(hval) + 2 * lane;
+  const int4* kp = reinterpret_cast<const int4*>(hkey) + (KL / 4) * lane;
+  const double2* vp = reinterpret_cast<const double2*>(hval) + (KL / 2) * lane;
+#if APC_HEAD_PREFETCH
   // software pipeline: the next step's entries are in flight while this one is scanned
-  int4 nkq = make_int4(0, 0, 0, 0);
-  double2 nva = make_double2(0.0, 0.0), nvb = nva;
+  int4 nkq[KL / 4];
+  double2 nvq[KL / 2];
   if (rb < re) {
-    nkq = __ldcs(kp + (rb >> 2));
-    nva = __ldcs(vp + (rb >> 1));
-    nvb = __ldcs(vp + (rb >> 1) + 1);
+#pragma unroll
+    for (int i = 0; i < KL / 4; ++i) nkq[i] = __ldcs(kp + (rb >> 2) + i);
+#pragma unroll
+    for (int i = 0; i < KL / 2; ++i) nvq[i] = __ldcs(vp + (rb >> 1) + i);
   }
-  for (int e = rb; e < re; e += 128) {
-    const int4 kq = nkq;
-    const double2 va = nva, vb = nvb;
-    if (e + 128 < re) {
-      nkq = __ldcs(kp + ((e + 128) >> 2));
-      nva = __ldcs(vp + ((e + 128) >> 1));
-      nvb = __ldcs(vp + ((e + 128) >> 1) + 1);
+#endif
+  for (int e = rb; e < re; e += STEP) {
+    int key[KL];
+    double vv[KL];
+#if APC_HEAD_PREFETCH
+#pragma unroll
+    for (int i = 0; i < KL / 4; ++i) {
+      key[4 * i] = nkq[i].x;
+      key[4 * i + 1] = nkq[i].y;
+      key[4 * i + 2] = nkq[i].z;
+      key[4 * i + 3] = nkq[i].w;
     }
+#pragma unroll
+    for (int i = 0; i < KL / 2; ++i) {
+      vv[2 * i] = nvq[i].x;
+      vv[2 * i + 1] = nvq[i].y;
+    }
+    if (e + STEP < re) {
+#pragma unroll
+      for (int i = 0; i < KL / 4; ++i) nkq[i] = __ldcs(kp + ((e + STEP) >> 2) + i);
+#pragma unroll
+      for (int i = 0; i < KL / 2; ++i) nvq[i] = __ldcs(vp + ((e + STEP) >> 1) + i);
+    }
+#else
+#pragma unroll
+    for (int i = 0; i < KL / 4; ++i) {
+      const int4 q = __ldcs(kp + (e >> 2) + i);
+      key[4 * i] = q.x;
+      key[4 * i + 1] = q.y;
+      key[4 * i + 2] = q.z;
+      key[4 * i + 3] = q.w;
+    }
+#pragma unroll
+    for (int i = 0; i < KL / 2; ++i) {
+      const double2 q = __ldcs(vp + (e >> 1) + i);
+      vv[2 * i] = q.x;
+      vv[2 * i + 1] = q.y;
+    }
+#endif
     // padding keys carry column kHeadPad and row 0 (value 0): a run that is never stored
-    const int k0 = kq.x >> 16, k1 = kq.y >> 16, k2 = kq.z >> 16, k3 = kq.w >> 16;
-    double x0 = va.x * us[kq.x & (kHeadRows - 1)];
-    const double x1 = va.y * us[kq.y & (kHeadRows - 1)];
-    const double x2 = vb.x * us[kq.z & (kHeadRows - 1)];
-    const double x3 = vb.y * us[kq.w & (kHeadRows - 1)];
-    const int kl0 = __shfl_sync(FULL, k0, 0);
+    int k[KL];
+    double x[KL];
+#pragma unroll
+    for (int i = 0; i < KL; ++i) {
+      k[i] = key[i] >> 16;
+      x[i] = vv[i] * us[key[i] & (kHeadRows - 1)];
+    }
+    const int kl0 = __shfl_sync(FULL, k[0], 0);
     if (ck >= 0 && kl0 != ck) {  // the carried piece ended with the previous step
       if (fk < 0) {
         fk = ck;
@@ -339,17 +375,21 @@ head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, cons
       }
       ck = -1;
     }
-    if (lane == 0 && k0 == ck) x0 = cs + x0;  // carried sum first
-    const int kprev = __shfl_up_sync(FULL, k3, 1);
-    const bool h0 = lane == 0 || k0 != kprev;
-    const bool h1 = k1 != k0, h2 = k2 != k1, h3 = k3 != k2;
-    const double q0 = x0;
-    const double q1 = h1 ? x1 : q0 + x1;
-    const double q2 = h2 ? x2 : q1 + x2;
-    const double q3 = h3 ? x3 : q2 + x3;
+    if (lane == 0 && k[0] == ck) x[0] = cs + x[0];  // carried sum first
+    const int kprev = __shfl_up_sync(FULL, k[KL - 1], 1);
+    bool hd[KL];  // entry i starts a run within the lane (entry 0: relative to the previous lane)
+    hd[0] = lane == 0 || k[0] != kprev;
+#pragma unroll
+    for (int i = 1; i < KL; ++i) hd[i] = k[i] != k[i - 1];
+    double q[KL];
+    q[0] = x[0];
+#pragma unroll
+    for (int i = 1; i < KL; ++i) q[i] = hd[i] ? x[i] : q[i - 1] + x[i];
     // warp segmented inclusive scan of (head seen, open-run sum) over lanes
-    bool F = h0 || h1 || h2 || h3;
-    double A = q3;
+    bool F = false;
+#pragma unroll
+    for (int i = 0; i < KL; ++i) F = F || hd[i];
+    double A = q[KL - 1];
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const double Au = __shfl_up_sync(FULL, A, d);
@@ -359,19 +399,30 @@ head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, cons
       F = F || (in && Fu);
     }
     const double E = __shfl_up_sync(FULL, A, 1);  // sum carried into this lane's first run
-    const double y0 = h0 ? q0 : E + q0;
-    const double y1 = (h0 || h1) ? q1 : E + q1;
-    const double y2 = (h0 || h1 || h2) ? q2 : E + q2;
-    const double y3 = (h0 || h1 || h2 || h3) ? q3 : E + q3;
-    const int knext = __shfl_down_sync(FULL, k0, 1);
-    bool e0 = k0 != kHeadPad && k0 != k1;
-    bool e1 = k1 != kHeadPad && k1 != k2;
-    bool e2 = k2 != kHeadPad && k2 != k3;
-    bool e3 = k3 != kHeadPad && lane < 31 && k3 != knext;  // lane 31's last entry stays open
-    const unsigned m = __ballot_sync(FULL, e0 || e1 || e2 || e3);
+    double y[KL];
+    bool seen = false;
+#pragma unroll
+    for (int i = 0; i < KL; ++i) {
+      seen = seen || hd[i];
+      y[i] = seen ? q[i] : E + q[i];
+    }
+    const int knext = __shfl_down_sync(FULL, k[0], 1);
+    bool en[KL];
+#pragma unroll
+    for (int i = 0; i < KL - 1; ++i) en[i] = k[i] != kHeadPad && k[i] != k[i + 1];
+    en[KL - 1] = k[KL - 1] != kHeadPad && lane < 31 && k[KL - 1] != knext;  // lane 31's last entry stays open
+    bool anyen = false;
+#pragma unroll
+    for (int i = 0; i < KL; ++i) anyen = anyen || en[i];
+    const unsigned m = __ballot_sync(FULL, anyen);
     // this lane's first closed piece (used when it is the range's first piece)
-    const int jk = e0 ? k0 : e1 ? k1 : e2 ? k2 : k3;
-    const double js = e0 ? y0 : e1 ? y1 : e2 ? y2 : y3;
+    int jk = k[KL - 1];
+    double js = y[KL - 1];
+#pragma unroll
+    for (int i = KL - 2; i >= 0; --i) {
+      jk = en[i] ? k[i] : jk;
+      js = en[i] ? y[i] : js;
+    }
     const int fl = (__ffs(m) - 1) & 31;
     const int bk = __shfl_sync(FULL, jk, fl);
     const double bs = __shfl_sync(FULL, js, fl);
@@ -379,19 +430,20 @@ head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, cons
       fk = bk;
       fs = bs;
       if (lane == fl) {
-        if (e0) e0 = false;
-        else if (e1) e1 = false;
-        else if (e2) e2 = false;
-        else e3 = false;
+        bool cleared = false;
+#pragma unroll
+        for (int i = 0; i < KL; ++i) {
+          const bool c = en[i] && !cleared;
+          cleared = cleared || en[i];
+          en[i] = en[i] && !c;
+        }
       }
     }
-    const int pb = blk;
-    if (e0) part[k0 * nb + pb] = y0;
-    if (e1) part[k1 * nb + pb] = y1;
-    if (e2) part[k2 * nb + pb] = y2;
-    if (e3) part[k3 * nb + pb] = y3;
-    ck = __shfl_sync(FULL, k3, 31);
-    cs = __shfl_sync(FULL, y3, 31);
+#pragma unroll
+    for (int i = 0; i < KL; ++i)
+      if (en[i]) part[k[i] * nb + blk] = y[i];
+    ck = __shfl_sync(FULL, k[KL - 1], 31);
+    cs = __shfl_sync(FULL, y[KL - 1], 31);
     if (ck == kHeadPad) ck = -1;
   }
   if (lane == 0) pc[w] = fk < 0 ? HeadPiece{ck, -1, cs, 0.0} : HeadPiece{fk, ck, fs, cs};
@@ -814,7 +866,7 @@ void build_head_adj(apc_mat& a, const std::vector<int>& tptr, const int* hidx, c
       tot += len;
       if (len == 0) zcol.push_back(static_cast<int>(k));
     }
-    tot = (tot + 127) / 128 * 128;  // 128-aligned blocks: padding keys are -1
+    tot = (tot + kHeadStep - 1) / kHeadStep * kHeadStep;  // step-aligned blocks (padding: column kHeadPad)
     zptr[b + 1] = static_cast<int>(zcol.size());
   }
   require(tot < (1LL << 31), APC_INVALID_ARGUMENT, "build_head_adj: head entries exceed int32 range");
@@ -832,8 +884,8 @@ void build_head_adj(apc_mat& a, const std::vector<int>& tptr, const int* hidx, c
   up(h.zptr, zptr);
   up(h.zcol, zcol);
   up(h.hcol, hc);
-  h.hkey.alloc(std::max<long long>(128, tot));
-  h.hval.alloc(std::max<long long>(128, tot));
+  h.hkey.alloc(std::max<long long>(kHeadStep, tot));
+  h.hval.alloc(std::max<long long>(kHeadStep, tot));
   fill_int_kernel<<<nblk(h.hkey.n, 256), 256, 0, st>>>(h.hkey.p, h.hkey.n, kHeadPad << 16);
   ctx->launches++;
   APC_CUDA(cudaMemsetAsync(h.hval.p, 0, h.hval.bytes(), st));

@@ -42,7 +42,15 @@ constexpr int kCsrUnitMax = 2048;  // max nnz per work unit of the transpose SpM
 #endif
 constexpr int kHeadRows = APC_HEAD_ROWS;  // rows of A per block of the head adjoint (u block in shared memory)
 constexpr int kHeadThreads = APC_HEAD_THREADS;
-constexpr int kHeadPad = 0x7fff;   // column of the padding entries (head columns are below it)
+constexpr int kHeadPad = 0x7fff;
+#ifndef APC_HEAD_PER_LANE
+#define APC_HEAD_PER_LANE 4
+#endif
+#ifndef APC_HEAD_PREFETCH
+#define APC_HEAD_PREFETCH 1
+#endif
+constexpr int kHeadPerLane = APC_HEAD_PER_LANE;       // consecutive entries per lane (4 or 8)
+constexpr int kHeadStep = 32 * kHeadPerLane;          // entries per warp step   // column of the padding entries (head columns are below it)
 
 // ---------------------------------------------------------------------------
 // forward epilogue interface:
