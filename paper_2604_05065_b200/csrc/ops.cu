@@ -277,7 +277,10 @@ __device__ __forceinline__ void head_chain(int& k, double& s, int pk, double ps,
   s = ps;
 }
 
-__global__ void __launch_bounds__(kHeadThreads)
+#ifndef APC_HEAD_MINB
+#define APC_HEAD_MINB 1
+#endif
+__global__ void __launch_bounds__(kHeadThreads, APC_HEAD_MINB)
 head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, const double* __restrict__ hval,
                 const double* __restrict__ u, long long mloc, long long nblocks, int parts,
                 const int* __restrict__ zptr, const int* __restrict__ zcol, double* __restrict__ part,
