@@ -587,14 +587,19 @@ unsigned fwd_gs_grid(apc_ctx* ctx, const void* kfn, int threads) {
 // ---------------------------------------------------------------------------
 DenseFwdPlan dense_fwd_plan(const apc_mat& a) { return dense_fwd_plan(a.mloc(), a.n, a.ctx->num_sms); }
 
+// columns per split at least APC_DENSE_FWD_MINCOLS: short, wide operands (the
+// explicit preconditioner basis B, n x l) need many splits to fill the GPU
+#ifndef APC_DENSE_FWD_MINCOLS
+#define APC_DENSE_FWD_MINCOLS 16
+#endif
 DenseFwdPlan dense_fwd_plan(long long mloc, long long ncols, int num_sms) {
   DenseFwdPlan p;
   p.ntiles = (mloc + kDenseFwdTile - 1) / kDenseFwdTile;
   if (p.ntiles < 1) p.ntiles = 1;
-  // aim for >= 6 CTAs per SM, but keep >= 64 columns per split
+  // aim for >= 6 CTAs per SM, but keep >= APC_DENSE_FWD_MINCOLS columns per split
   const long long want = 6LL * num_sms;
   long long ns = (want + p.ntiles - 1) / p.ntiles;
-  long long maxs = std::max<long long>(1, ncols / 64);
+  long long maxs = std::max<long long>(1, ncols / APC_DENSE_FWD_MINCOLS);
   ns = std::max<long long>(1, std::min(ns, maxs));
   p.nsplit = std::min<long long>(ns, 65535);
   p.cols_per_split = (ncols + p.nsplit - 1) / p.nsplit;
