@@ -140,3 +140,22 @@ def test_hot_row_shard_products_and_sharded_entry(apc, ctx, monkeypatch):
     g1 = apc.aplicur_solve(H, p.b, cfg, full=H)
     assert np.array_equal(g0.row_indices, g1.row_indices)
     assert abs(g1.lsqr_iters - g0.lsqr_iters) <= max(2, 0.05 * g0.lsqr_iters)
+
+
+def test_hot_solve_matches_reference(apc, ref, ctx, monkeypatch):
+    # the whole adaptive solve through the hot SELL forward and the head adjoint
+    # (forced on a C5-shaped system) against the unmodified reference solver
+    monkeypatch.setenv("APC_HOT_SELL", "1")
+    monkeypatch.setenv("APC_HEAD_MIN", "2")
+    p = apc.Problem(5, 30000, 3000)
+    knobs = dict(mu=1e-8, eps_lsqr=1e-8, block=25, seed=1, max_rank=50, eps_cur=3e-7)
+    A = apc.DeviceMatrix.from_problem(ctx, p)
+    g = apc.aplicur_solve(A, p.b, apc.SolverConfig(**knobs))
+    r = ref.solve(ref.Problem.from_apc(p), p.b, dict(knobs, trace_sample_stride=0))
+    assert np.array_equal(g.row_indices, r.row_indices)
+    assert np.array_equal(g.col_indices, r.col_indices)
+    assert np.array_equal(g.rho_history.view(np.uint64), r.rho_history.view(np.uint64))
+    assert [ph.rank for ph in g.phases] == list(r.phase_rank)
+    it_g, it_r = g.lsqr_iters, int(r.phase_iters.sum())
+    assert abs(it_g - it_r) <= max(3, 0.05 * it_r), (it_g, it_r)
+    assert abs(g.final_relres - r.final_relres) <= 1e-5 * r.final_relres

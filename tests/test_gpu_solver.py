@@ -28,6 +28,9 @@ CASES = [
     (2, 4000, 400, dict(mu=1e-3, eps_lsqr=1e-10, block=8, seed=3, max_rank=40, variant=1)),
     (1, 400, 50, dict(mu=0.05, eps_lsqr=1e-10, block=5, seed=1, variant=1)),
     (3, 3000, 300, dict(mu=1e-2, eps_lsqr=1e-8, block=10, seed=1, max_rank=60, variant=1)),
+    # C4-shaped (square, planted low rank + noise) and C5-shaped (Zipf columns) systems
+    (4, 1200, 1200, dict(mu=0.0, eps_lsqr=1e-10, block=30, seed=1, max_rank=30, lsqr_cap=40)),
+    (5, 30000, 3000, dict(mu=1e-8, eps_lsqr=1e-8, block=25, seed=1, max_rank=50, eps_cur=3e-7)),
 ]
 
 
