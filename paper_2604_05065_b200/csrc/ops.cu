@@ -515,6 +515,19 @@ void build_hot_sell(apc_mat& a, const std::vector<long long>& col_nnz) {
   HotSell& h = a.hot;
   h.s = Sell();
   if (rows == 0 || nnz == 0) return;
+  {
+    // SELL slots (chunk width = its longest row) must stay in int32: very
+    // ragged rows keep the CSR forward instead
+    std::vector<int> rp(static_cast<size_t>(rows + 1));
+    copy_sync(st, rp.data(), a.a.ptr.p, sizeof(int) * rp.size(), cudaMemcpyDeviceToHost);
+    long long slots = 0;
+    for (long long c = 0; c * 32 < rows; ++c) {
+      int w = 0;
+      for (long long r = c * 32; r < std::min(rows, c * 32 + 32); ++r) w = std::max(w, rp[r + 1] - rp[r]);
+      slots += 32LL * w;
+    }
+    if (slots >= (1LL << 31)) return;
+  }
   // relabel: descending column length, ties by original id
   std::vector<int> hot(n), nptr(n + 1);
   for (long long j = 0; j < n; ++j) hot[j] = static_cast<int>(j);
