@@ -389,17 +389,22 @@ head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, cons
 #pragma unroll
     for (int i = 1; i < KL; ++i) q[i] = hd[i] ? x[i] : q[i - 1] + x[i];
     // warp segmented inclusive scan of (head seen, open-run sum) over lanes
-    bool F = false;
+    bool F0 = false;
 #pragma unroll
-    for (int i = 0; i < KL; ++i) F = F || hd[i];
+    for (int i = 0; i < KL; ++i) F0 = F0 || hd[i];
+    // lanes holding a run start; before the step of offset d a lane's segment
+    // flag covers lanes [lane - d + 1, lane], read off this mask instead of
+    // being shuffled along with the sums (shuffles share the L1TEX pipe)
+    const unsigned Hm = __ballot_sync(FULL, F0);
+    const unsigned upto = (2u << lane) - 1u;  // bits [0, lane]
     double A = q[KL - 1];
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const double Au = __shfl_up_sync(FULL, A, d);
-      const bool Fu = __shfl_up_sync(FULL, F ? 1 : 0, d) != 0;
-      const bool in = lane >= d;
-      A = (in && !F) ? Au + A : A;
-      F = F || (in && Fu);
+      const int lo = lane - d + 1;
+      const unsigned win = lo > 0 ? upto & ~((1u << lo) - 1u) : upto;
+      const bool F = (Hm & win) != 0u;
+      A = (lane >= d && !F) ? Au + A : A;
     }
     const double E = __shfl_up_sync(FULL, A, 1);  // sum carried into this lane's first run
     double y[KL];
@@ -426,12 +431,10 @@ head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, cons
       jk = en[i] ? k[i] : jk;
       js = en[i] ? y[i] : js;
     }
-    const int fl = (__ffs(m) - 1) & 31;
-    const int bk = __shfl_sync(FULL, jk, fl);
-    const double bs = __shfl_sync(FULL, js, fl);
-    if (m != 0 && fk < 0) {
-      fk = bk;
-      fs = bs;
+    if (m != 0 && fk < 0) {  // warp-uniform; taken once per range
+      const int fl = __ffs(m) - 1;
+      fk = __shfl_sync(FULL, jk, fl);
+      fs = __shfl_sync(FULL, js, fl);
       if (lane == fl) {
         bool cleared = false;
 #pragma unroll
