@@ -815,7 +815,7 @@ void build_units_sel(apc_ctx* ctx, Units& c, long long rows, const std::vector<l
 // Head/tail split of CSR(A^T) for the row-blocked adjoint (HeadAdj).  Host
 // inputs: CSR(A^T) row offsets and int32 local row indices (the upload's
 // staging copy) and the row lengths.  A row of A^T (column of A) is "head"
-// when it averages >= APC_HEAD_MIN (default 8) entries per block of kHeadRows.
+// when it averages >= APC_HEAD_MIN (default 2) entries per block of kHeadRows.
 struct HeadSegs {  // per head column: entry offsets of its segment in each block
   const int* tptr;
   const int* hidx;
@@ -864,7 +864,7 @@ void build_head_adj(apc_mat& a, const std::vector<int>& tptr, const int* hidx, c
   const long long nblocks = (mloc + kHeadRows - 1) / kHeadRows;
   if (nblocks == 0 || n == 0) return;
   const char* env = std::getenv("APC_HEAD_MIN");
-  const double per_block = env ? std::atof(env) : 8.0;
+  const double per_block = env ? std::atof(env) : 2.0;
   const long long thr = std::max<long long>(64, static_cast<long long>(per_block * static_cast<double>(nblocks)));
   std::vector<int> hc;
   std::vector<char> is_head(n, 0);
