@@ -79,6 +79,9 @@ dense_adj_kernel(const double* __restrict__ A, long long ld, long long mloc, lon
 // ---------------------------------------------------------------------------
 // CSR over work units (transpose products)
 // ---------------------------------------------------------------------------
+#ifndef APC_UNITS_PRED
+#define APC_UNITS_PRED 1
+#endif
 __global__ void __launch_bounds__(kCsrUnitThreads)
 csr_units_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
                  const double* __restrict__ val, const double* __restrict__ u, long long n_units,
@@ -100,7 +103,28 @@ csr_units_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
     s2 += __ldcs(val + q + 64) * __ldg(u + i2);
     s3 += __ldcs(val + q + 96) * __ldg(u + i3);
   }
+#if APC_UNITS_PRED
+  // the remainder (< 128 entries) as one predicated block: its index loads, then
+  // its u gathers, all in flight together (short rows: the common case of the
+  // tail rows of a head-split A^T)
+  if (q < e) {
+    const bool o1 = q + 32 < e, o2 = q + 64 < e;
+    const int i0 = __ldcs(idx + q);
+    const int i1 = o1 ? __ldcs(idx + q + 32) : 0;
+    const int i2 = o2 ? __ldcs(idx + q + 64) : 0;
+    const double v0 = __ldcs(val + q);
+    const double v1 = o1 ? __ldcs(val + q + 32) : 0.0;
+    const double v2 = o2 ? __ldcs(val + q + 64) : 0.0;
+    const double g0 = __ldg(u + i0);
+    const double g1 = o1 ? __ldg(u + i1) : 0.0;
+    const double g2 = o2 ? __ldg(u + i2) : 0.0;
+    s0 += v0 * g0;
+    if (o1) s1 += v1 * g1;
+    if (o2) s2 += v2 * g2;
+  }
+#else
   for (; q < e; q += 32) s0 += __ldcs(val + q) * __ldg(u + __ldcs(idx + q));
+#endif
   s0 += s2;
   s1 += s3;
   double s = warp_sum(s0 + s1);
