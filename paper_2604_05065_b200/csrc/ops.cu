@@ -82,39 +82,47 @@ dense_adj_kernel(const double* __restrict__ A, long long ld, long long mloc, lon
 #ifndef APC_UNITS_PRED
 #define APC_UNITS_PRED 1
 #endif
+// lanes per work unit: units are at most kCsrUnitMax entries and most rows of
+// A^T are short, so a half warp per unit doubles the units in flight
+#ifndef APC_UNITS_G
+#define APC_UNITS_G 32
+#endif
 __global__ void __launch_bounds__(kCsrUnitThreads)
 csr_units_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
                  const double* __restrict__ val, const double* __restrict__ u, long long n_units,
                  const int* __restrict__ urow, const int* __restrict__ ustart,
                  const int* __restrict__ uend, const int* __restrict__ uslot,
                  double* __restrict__ out, double* __restrict__ upart, const int* done) {
+  constexpr int G = APC_UNITS_G;
   if (done && *done) return;
-  const long long unit = (static_cast<long long>(blockIdx.x) * kCsrUnitThreads + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (unit >= n_units) return;
-  const int b = __ldg(ustart + unit), e = __ldg(uend + unit);
+  const long long unit = (static_cast<long long>(blockIdx.x) * kCsrUnitThreads + threadIdx.x) / G;
+  const int lane = threadIdx.x % G;
+  const bool ok = unit < n_units;
+  if (G == 32 && !ok) return;
+  const int b = ok ? __ldg(ustart + unit) : 0, e = ok ? __ldg(uend + unit) : 0;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   int q = b + lane;
   // CSR(A^T) streamed with evict-first loads so the gathered u stays in L2
-  for (; q + 96 < e; q += 128) {
-    const int i0 = __ldcs(idx + q), i1 = __ldcs(idx + q + 32), i2 = __ldcs(idx + q + 64), i3 = __ldcs(idx + q + 96);
+  for (; q + 3 * G < e; q += 4 * G) {
+    const int i0 = __ldcs(idx + q), i1 = __ldcs(idx + q + G), i2 = __ldcs(idx + q + 2 * G),
+              i3 = __ldcs(idx + q + 3 * G);
     s0 += __ldcs(val + q) * __ldg(u + i0);
-    s1 += __ldcs(val + q + 32) * __ldg(u + i1);
-    s2 += __ldcs(val + q + 64) * __ldg(u + i2);
-    s3 += __ldcs(val + q + 96) * __ldg(u + i3);
+    s1 += __ldcs(val + q + G) * __ldg(u + i1);
+    s2 += __ldcs(val + q + 2 * G) * __ldg(u + i2);
+    s3 += __ldcs(val + q + 3 * G) * __ldg(u + i3);
   }
 #if APC_UNITS_PRED
-  // the remainder (< 128 entries) as one predicated block: its index loads, then
+  // the remainder (< 4 G entries) as one predicated block: its index loads, then
   // its u gathers, all in flight together (short rows: the common case of the
   // tail rows of a head-split A^T)
   if (q < e) {
-    const bool o1 = q + 32 < e, o2 = q + 64 < e;
+    const bool o1 = q + G < e, o2 = q + 2 * G < e;
     const int i0 = __ldcs(idx + q);
-    const int i1 = o1 ? __ldcs(idx + q + 32) : 0;
-    const int i2 = o2 ? __ldcs(idx + q + 64) : 0;
+    const int i1 = o1 ? __ldcs(idx + q + G) : 0;
+    const int i2 = o2 ? __ldcs(idx + q + 2 * G) : 0;
     const double v0 = __ldcs(val + q);
-    const double v1 = o1 ? __ldcs(val + q + 32) : 0.0;
-    const double v2 = o2 ? __ldcs(val + q + 64) : 0.0;
+    const double v1 = o1 ? __ldcs(val + q + G) : 0.0;
+    const double v2 = o2 ? __ldcs(val + q + 2 * G) : 0.0;
     const double g0 = __ldg(u + i0);
     const double g1 = o1 ? __ldg(u + i1) : 0.0;
     const double g2 = o2 ? __ldg(u + i2) : 0.0;
@@ -123,12 +131,14 @@ csr_units_kernel(const int* __restrict__ ptr, const int* __restrict__ idx,
     if (o2) s2 += v2 * g2;
   }
 #else
-  for (; q < e; q += 32) s0 += __ldcs(val + q) * __ldg(u + __ldcs(idx + q));
+  for (; q < e; q += G) s0 += __ldcs(val + q) * __ldg(u + __ldcs(idx + q));
 #endif
   s0 += s2;
   s1 += s3;
-  double s = warp_sum(s0 + s1);
-  if (lane == 0) {
+  double s = s0 + s1;
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (ok && lane == 0) {
     const int slot = __ldg(uslot + unit);
     if (slot < 0) out[__ldg(urow + unit)] = s;
     else upart[slot] = s;
@@ -734,7 +744,7 @@ void op_adj_raw(apc_mat& a, const double* u, double* out, const int* done) {
 void launch_units(apc_ctx* ctx, const Csr& c, const Units& un, const double* u, double* out, const int* done) {
   cudaStream_t st = ctx->stream;
   if (un.n_units == 0) return;
-  unsigned nb = nblk(un.n_units * 32, kCsrUnitThreads);
+  unsigned nb = nblk(un.n_units * APC_UNITS_G, kCsrUnitThreads);
   csr_units_kernel<<<nb, kCsrUnitThreads, 0, st>>>(c.ptr.p, c.idx.p, c.val.p, u, un.n_units,
                                                    un.urow.p, un.ustart.p, un.uend.p, un.uslot.p, out,
                                                    un.upart.p, done);
