@@ -126,6 +126,195 @@ sketch_ss_dense_kernel(const double* __restrict__ A, long long m, long long n, i
   for (int i = lane; i < s; i += 32) Y[j * s + i] = yc[i];
 }
 
+// Dense A, inverted over S: every sketch row r keeps its own list of the A
+// rows k that feed it (ascending k, packed k << 1 | sign > 0), so Y(r, j) is
+// one thread's running sum, added in exactly the reference's k order
+// (sketch.hpp:77-111: rows ascending, zero entries skipped).  A CTA takes
+// kInvCols columns; their rows are staged kInvRows at a time in shared memory
+// (coalesced, each A element read once), and each thread walks its list
+// through the chunk for all kInvCols columns at once.  A is streamed once:
+// HBM-bound instead of one dependent shared-memory update per row of A.
+constexpr int kInvCols = 8;
+constexpr int kInvRows = 256;
+__device__ __forceinline__ unsigned inv_smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void inv_bulk(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   inv_smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(inv_smem_u32(bar))
+               : "memory");
+}
+// chunk [c0, c0 + rows) of the CTA's columns and the chunk's S entries -> one
+// buffer (bulk copies completing on bar; plain loads when a copy would be
+// misaligned)
+__device__ __forceinline__ void inv_stage(const double* __restrict__ A, long long m, long long j0, int nc,
+                                          long long c0, int rows, const short* __restrict__ ent, int xi,
+                                          double* abuf, short* ebuf, unsigned long long* bar, bool tma) {
+  const unsigned abytes = static_cast<unsigned>(rows) * 8u;
+  const unsigned ebytes = static_cast<unsigned>(rows) * static_cast<unsigned>(xi) * 2u;
+  const short* esrc = ent + c0 * xi;
+  if (tma) {
+    if (threadIdx.x == 0) {
+      // the block barrier ordered the generic reads of this buffer; hand it to the async proxy
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(inv_smem_u32(bar)),
+                   "r"(abytes * static_cast<unsigned>(nc) + ebytes)
+                   : "memory");
+      for (int c = 0; c < nc; ++c) inv_bulk(abuf + c * kInvRows, A + (j0 + c) * m + c0, abytes, bar);
+      inv_bulk(ebuf, esrc, ebytes, bar);
+    }
+  } else {
+    for (int c = 0; c < nc; ++c) {
+      const double* col = A + (j0 + c) * m + c0;
+      for (int i = threadIdx.x; i < rows; i += blockDim.x) abuf[c * kInvRows + i] = __ldcs(col + i);
+    }
+    for (int i = threadIdx.x; i < rows * xi; i += blockDim.x) ebuf[i] = esrc[i];
+  }
+}
+__device__ __forceinline__ void inv_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n IWAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra IWAIT_%=;\n}" ::"r"(
+          inv_smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// Dense A, inverted over S: Y(r, j) is one thread's running sum over the A rows
+// k that feed sketch row r, added in exactly the reference's k order
+// (sketch.hpp:77-111: rows ascending, zero entries skipped).  The S entries are
+// stored chunk-major: for each chunk of kInvRows rows of A, by target row r,
+// k ascending within r, packed (k - chunk start) << 1 | sign > 0 in 16 bits,
+// with cptr[chunk * (s + 1) + r] the offset of r's run inside the chunk.  A
+// CTA takes kInvCols columns; every chunk (those columns' rows and the chunk's
+// S entries) is staged by TMA bulk copies, double-buffered, and each thread
+// walks its run in shared memory for all kInvCols columns at once.  A is read
+// from HBM exactly once.
+__global__ void __launch_bounds__(1024)
+sketch_ss_dense_inv_kernel(const double* __restrict__ A, long long m, long long n, int s, int xi,
+                           const int* __restrict__ cptr, const short* __restrict__ ent,
+                           const int* __restrict__ srow, const signed char* __restrict__ ssgn, double scale,
+                           double mu_scale, int aug, double* __restrict__ Y) {
+  // [2 x (kInvCols x kInvRows doubles)] [2 x (kInvRows x xi shorts)] [s x kInvCols doubles: mu tail]
+  extern __shared__ __align__(16) double dyn_inv[];
+  __shared__ __align__(8) unsigned long long bars[2];
+  double* abuf = dyn_inv;
+  short* ebuf = reinterpret_cast<short*>(dyn_inv + 2 * kInvCols * kInvRows);
+  const int estride = (kInvRows * xi + 7) & ~7;  // shorts per entry buffer (16-byte multiple)
+  double* ysh = reinterpret_cast<double*>(ebuf + 2 * estride);
+  const long long j0 = static_cast<long long>(blockIdx.x) * kInvCols;
+  const int nc = static_cast<int>(n - j0 < kInvCols ? n - j0 : kInvCols);
+  const int r = threadIdx.x;
+  const bool own = r < s;
+  double acc[kInvCols];
+#pragma unroll
+  for (int c = 0; c < kInvCols; ++c) acc[c] = 0.0;
+  // bulk copies need 16-byte aligned columns and copy sizes
+  const bool tma = (m % 2 == 0) && (xi % 8 == 0) && ((reinterpret_cast<unsigned long long>(A) & 15ull) == 0) &&
+                   ((reinterpret_cast<unsigned long long>(ent) & 15ull) == 0);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(inv_smem_u32(&bars[0])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(inv_smem_u32(&bars[1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const long long nchunks = (m + kInvRows - 1) / kInvRows;
+  auto rows_of = [&](long long ch) { return static_cast<int>(m - ch * kInvRows < kInvRows ? m - ch * kInvRows : kInvRows); };
+  if (nchunks > 0) inv_stage(A, m, j0, nc, 0, rows_of(0), ent, xi, abuf, ebuf, &bars[0], tma);
+  int rb = own ? __ldg(cptr + r) : 0, re = own ? __ldg(cptr + r + 1) : 0;
+  for (long long ch = 0; ch < nchunks; ++ch) {
+    const int b = static_cast<int>(ch & 1);
+    if (ch + 1 < nchunks)  // the other buffer was released by the barrier at the end of ch - 1
+      inv_stage(A, m, j0, nc, (ch + 1) * kInvRows, rows_of(ch + 1), ent, xi, abuf + (1 - b) * kInvCols * kInvRows,
+                ebuf + (1 - b) * estride, &bars[1 - b], tma);
+    // this thread's run in the next chunk (prefetched while this one is walked)
+    int nrb = 0, nre = 0;
+    if (own && ch + 1 < nchunks) {
+      nrb = __ldg(cptr + (ch + 1) * (s + 1) + r);
+      nre = __ldg(cptr + (ch + 1) * (s + 1) + r + 1);
+    }
+    if (tma) inv_wait(&bars[b], static_cast<unsigned>((ch >> 1) & 1));
+    else __syncthreads();
+    // sv = scale * A(k, j) once per element (the reference computes it once per
+    // row k and adds sv * (+-1) to each of its xi targets).  A zero A(k, j) is
+    // skipped by the reference; a nonzero one whose sv underflows to +-0 would
+    // add +-0, which cannot change a sum that starts at +0 -- so testing sv
+    // instead of A(k, j) keeps every bit.
+    double* asw = abuf + b * kInvCols * kInvRows;
+    for (int i = threadIdx.x; i < nc * kInvRows; i += blockDim.x) asw[i] = scale * asw[i];
+    __syncthreads();
+    const double* as = asw;
+    const short* es = ebuf + b * estride;
+    for (int i = rb; i < re; ++i) {
+      const int e = es[i];
+      const int kk = e >> 1;
+      const bool pos = (e & 1) != 0;
+#pragma unroll
+      for (int c = 0; c < kInvCols; ++c) {
+        const double sv = as[c * kInvRows + kk];
+        if (c < nc && sv != 0.0) acc[c] += pos ? sv : -sv;  // sv * (+-1.0), exact
+      }
+    }
+    rb = nrb;
+    re = nre;
+    __syncthreads();  // every thread is done with buffer b before it is refilled
+  }
+  if (aug) {  // mu tail: column m + j of S (sketch.hpp:152-160), added last
+#pragma unroll
+    for (int c = 0; c < kInvCols; ++c)
+      if (own && c < nc) ysh[c * s + r] = acc[c];
+    __syncthreads();
+    if (threadIdx.x < xi)
+      for (int c = 0; c < nc; ++c) {
+        const long long e = (m + j0 + c) * xi + threadIdx.x;
+        ysh[c * s + srow[e]] += mu_scale * static_cast<double>(ssgn[e]);
+      }
+    __syncthreads();
+    for (int c = 0; c < nc; ++c)
+      if (own) Y[(j0 + c) * s + r] = ysh[c * s + r];
+  } else {
+#pragma unroll
+    for (int c = 0; c < kInvCols; ++c)
+      if (own && c < nc) Y[(j0 + c) * s + r] = acc[c];
+  }
+}
+
+// chunk-major inverted index of S over its first m columns: entry e = k * xi + q
+// keyed by (chunk of k) * s + target row, sorted stably (k ascending within a
+// key); every chunk holds exactly rows * xi entries, so chunk c starts at
+// c * kInvRows * xi
+__global__ void sketch_inv_keys_kernel(const int* __restrict__ srow, long long cnt, int xi, int s,
+                                       int* __restrict__ keys, int* __restrict__ vals) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= cnt) return;
+  const long long k = e / xi;
+  keys[e] = static_cast<int>((k / kInvRows) * s + srow[e]);
+  vals[e] = static_cast<int>(e);
+}
+__global__ void sketch_inv_pack_kernel(const int* __restrict__ vals, long long cnt, int xi,
+                                       const signed char* __restrict__ ssgn, short* __restrict__ ent) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= cnt) return;
+  const int e = vals[i];
+  const int k = e / xi;
+  ent[i] = static_cast<short>(((k % kInvRows) << 1) | (ssgn[e] > 0 ? 1 : 0));
+}
+// cptr[ch * (s + 1) + r] = offset of (ch, r)'s run inside chunk ch
+__global__ void sketch_inv_ptr_kernel(const int* __restrict__ skeys, long long cnt, long long nchunks, int s, int xi,
+                                      int* __restrict__ cptr) {
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nchunks * (s + 1)) return;
+  const long long ch = t / (s + 1), r = t % (s + 1);
+  const long long key = ch * s + r;  // r == s: the next chunk's first key
+  long long lo = 0, hi = cnt;  // first entry with key >= key
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (skeys[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  cptr[t] = static_cast<int>(lo - ch * kInvRows * xi);
+}
+
 // CSC input: the device CSR(A^T) rows are the reference CSC columns
 __global__ void __launch_bounds__(kSketchWarps * 32)
 sketch_ss_csc_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
@@ -1155,10 +1344,44 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
       APC_CUDA(cudaFuncSetAttribute(sketch_ss_csc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
     const unsigned g = nb(n_, kSketchWarps);
-    if (!a.sparse)
+    const char* inv_env = std::getenv("APC_SKETCH_INV");
+    const bool inv = !a.sparse && (inv_env ? std::atoi(inv_env) != 0 : true) && s_ <= 1024 && m_ * x < (1LL << 30) &&
+                     ((m_ + kInvRows - 1) / kInvRows) * s_ < (1LL << 30);
+    if (inv) {
+      // chunk-major inverted index of S (rows of A feeding each sketch row, k ascending)
+      const long long cnt = m_ * x;
+      const long long nchunks = (m_ + kInvRows - 1) / kInvRows;
+      DBuf<int> keys(cnt), vals(cnt), skeys(cnt), svals(cnt), cptr(nchunks * (s_ + 1));
+      DBuf<short> ent(cnt + 8);
+      sketch_inv_keys_kernel<<<nb(cnt, 256), 256, 0, st>>>(d_rows.p, cnt, static_cast<int>(x), static_cast<int>(s_),
+                                                           keys.p, vals.p);
+      int end_bit = 1;
+      while ((1LL << end_bit) < nchunks * s_ + 1 && end_bit < 31) ++end_bit;
+      size_t tb = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, svals.p, static_cast<int>(cnt), 0, end_bit,
+                                      st);
+      DBuf<char> tmp(static_cast<long long>(std::max<size_t>(tb, 1)));
+      APC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, svals.p, static_cast<int>(cnt), 0,
+                                               end_bit, st));
+      sketch_inv_pack_kernel<<<nb(cnt, 256), 256, 0, st>>>(svals.p, cnt, static_cast<int>(x), d_sg.p, ent.p);
+      sketch_inv_ptr_kernel<<<nb(nchunks * (s_ + 1), 256), 256, 0, st>>>(skeys.p, cnt, nchunks, static_cast<int>(s_),
+                                                                        static_cast<int>(x), cptr.p);
+      const int threads = static_cast<int>((s_ + 31) / 32 * 32);
+      const long long estride = (kInvRows * x + 7) & ~7LL;
+      const size_t ysm = sizeof(double) * 2 * kInvCols * kInvRows + sizeof(short) * 2 * estride +
+                         (aug ? sizeof(double) * s_ * kInvCols : 0);
+      APC_CUDA(cudaFuncSetAttribute(sketch_ss_dense_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(ysm)));
+      sketch_ss_dense_inv_kernel<<<static_cast<unsigned>((n_ + kInvCols - 1) / kInvCols), threads, ysm, st>>>(
+          a.dense.p, m_, n_, static_cast<int>(s_), static_cast<int>(x), cptr.p, ent.p, d_rows.p, d_sg.p, scale,
+          mu_scale, aug, Y_.p);
+      ctx_->launches += 6;
+      APC_CUDA(cudaGetLastError());
+      APC_CUDA(cudaStreamSynchronize(st));  // temporaries go back to the pool
+    } else if (!a.sparse) {
       sketch_ss_dense_kernel<<<g, kSketchWarps * 32, smem, st>>>(a.dense.p, m_, n_, (int)s_, (int)x, d_rows.p,
                                                                 d_sg.p, scale, mu_scale, aug, Y_.p);
-    else {
+    } else {
       // columns longer than kHeavy go to the row-parallel kernel
       constexpr int kHeavy = 8192;
       std::vector<int> cp(static_cast<size_t>(n_ + 1));

@@ -117,3 +117,22 @@ def test_device_rng_stream_matches_host(apc, ctx, seed, stream, index, count):
     assert lib.apc_rng_fill_device(ctx.h, seed, stream, index, count,
                                    dev.ctypes.data_as(C.POINTER(C.c_uint64))) == 0
     assert np.array_equal(host, dev)
+
+
+@pytest.mark.parametrize("inv", ["1", "0"])
+def test_dense_sketch_zero_skip_and_ragged_chunks(apc, ref, ctx, monkeypatch, inv):
+    # dense sparse-sign sketch (inverted-index kernel and the warp-per-column
+    # kernel): exact zeros and signed zeros must be skipped as the reference
+    # skips them, m spans a partial row chunk, n a partial column group
+    monkeypatch.setenv("APC_SKETCH_INV", inv)
+    rng = np.random.default_rng(5)
+    m, n = 2500, 13
+    A = rng.standard_normal((m, n))
+    A[rng.random((m, n)) < 0.3] = 0.0
+    A[rng.random((m, n)) < 0.05] = -0.0
+    A[:, 4] = 0.0
+    D = apc.DeviceMatrix.from_numpy(ctx, A)
+    cur = apc.CurState(D, 7, seed=3)
+    Y = cur.sketch_matrix()
+    Yr = ref.cur_steps(ref.Problem.from_numpy(A), 7, 3, 0)["Y"]
+    assert np.array_equal(Y.view(np.uint64), Yr.view(np.uint64))
