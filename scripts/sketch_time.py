@@ -1,3 +1,6 @@
+"""One-time sketch timing on a BASELINE config (profiling driver):
+    python scripts/sketch_time.py CONFIG BLOCK
+prints (host embedding ms, device sketch ms) for three CurState inits."""
 import sys, time
 sys.path.insert(0, "/root/repo")
 import paper_2604_05065_b200 as apc
