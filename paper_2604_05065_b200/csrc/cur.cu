@@ -134,7 +134,10 @@ sketch_ss_dense_kernel(const double* __restrict__ A, long long m, long long n, i
 // (coalesced, each A element read once), and each thread walks its list
 // through the chunk for all kInvCols columns at once.  A is streamed once:
 // HBM-bound instead of one dependent shared-memory update per row of A.
-constexpr int kInvCols = 8;
+#ifndef APC_INV_COLS
+#define APC_INV_COLS 4
+#endif
+constexpr int kInvCols = APC_INV_COLS;  // columns of A per CTA
 constexpr int kInvRows = 256;
 __device__ __forceinline__ unsigned inv_smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
