@@ -1,17 +1,35 @@
 """APLICUR hot-path benchmark (driver contract: one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1], "C2"): sparse fp64 200000 x 20000,
-10 nonzeros per row + one per empty column, column scales 10^-U(0,4),
-b ~ N(0,1), mu = 1e-6, sparse-sign sketch k = 50 (block 50, s = 56, xi = 8),
-eps_lsqr = 1e-8, eps_cur = 30 mu, max_rank = 200,
-seeded synthetic data (problem seed 20260417, solver seed 1).
+Workload: BASELINE.json configs[4] ("C5"), the largest configuration that
+fits one GPU and the one the north star row-shards: sparse fp64 CSR
+8,000,000 x 400,000, 16 distinct Zipf(1.1) columns per row over shuffled ids
+(nnz 1.28e8), column scales 10^-U(0,3), b ~ N(0,1), mu = 1e-8, sparse-sign
+sketch k = 250 (block 250, s = 275, xi = 8), eps_lsqr = 1e-8, eps_cur = 3e-7,
+max_rank = 500, solver seed 1, problem seed 20260420.
+Seeded synthetic data from the BASELINE description (no public dataset).
 
-One step = one full aplicur_solve (sketch + incremental CUR + preconditioner
-rebuilds + warm-started LSQR phases to tolerance) with A resident in HBM.
-value = time-to-tol in seconds (lower is better).  `e2e` is the same solve
-through the C-ABI from HOST buffers (CSC upload + b in, x out, every step).
+One step = one full aplicur_solve from x = 0 (sketch + incremental CUR +
+preconditioner rebuilds + warm-started LSQR phases to tolerance).  Every step
+runs end to end through the public API from HOST buffers: the CSC arrays are
+uploaded (validated, narrowed into pinned staging, copied, device CSR /
+CSR(A^T) / hot-SELL / head layouts built), the solve runs, x comes back.
+  value = time-to-tol (s): device time of the solve (CUDA events on the
+          library stream around aplicur_solve), A already resident in HBM;
+  e2e   = wall time of the whole step (upload + solve + x back), per step.
+Both come from the same K timed steps (W untimed warm-up steps first), so a
+default driver run (--steps 20 --warmup 5) fits the per-arm time limit.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference runs the unmodified C++ reference (oracle/_ref, built from
+/root/reference) on the host cores, with inputs from the oracle's own
+generator (oracle/ref_harness.cpp ref_generate, byte-identical to the
+product's): it never loads the product library.  Its full C5 solve would take
+days on one core, so each step is a bounded sample (the reference's own LSQR
+iterations on [A; mu I], plain_lsqr_solve with lsqr_cap) and time-to-tol is
+extrapolated as the reference setup + the GPU iteration
+count x the measured reference s/iteration; the inputs of that extrapolation
+are committed in profiles/c5_extrapolation.json and named in the line.
 """
 from __future__ import annotations
 
@@ -30,15 +48,27 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "APLICUR time-to-tol (s), LSQR iter/s, A·v+Aᵀu HBM GB/s vs peak"
-CONFIG_ID = 2
-SOLVER = dict(mu=1e-6, block=50, eps_lsqr=1e-8, max_rank=200, seed=1, trace_sample_stride=0)
+CONFIG_ID = 5
+M, N, NNZ = 8_000_000, 400_000, 128_000_000
+SOLVER = dict(mu=1e-8, block=250, eps_lsqr=1e-8, eps_cur=3e-7, max_rank=500, seed=1, trace_sample_stride=0)
+WORKLOAD = ("C5 sparse CSR 8000000x400000 nnz 1.28e8 (16 Zipf(1.1) columns per row) mu=1e-8 sparse-sign k=250 "
+            "eps_cur=3e-7 max_rank=500 tol=1e-8")
+# CSR(A) + CSR(A^T) with int32 indices, x/u read + written
+PAIR_BYTES = 24 * NNZ + 4 * (M + 1) + 4 * (N + 1) + 16 * (M + N)
+EXTRAP = ROOT / "profiles" / "c5_extrapolation.json"
+
+
+def config_dict(ws: int) -> dict:
+    """Identical in both arms (the driver compares them)."""
+    return {"workload": WORKLOAD, "m": M, "n": N, "nnz": NNZ, **SOLVER, "parallelism": f"rows{ws}",
+            "l2": "inputs larger than L2 (3.24 GB operator pair per LSQR iteration), no flush needed"}
 
 
 def _peaks():
     try:
-        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "MEASURED_PEAKS.json"
     except Exception:
-        return {"hbm_gbs": 6650.0, "fallback": True}
+        return {"hbm_gbs": 7672.0}, "fallback: B200_PROFILING.md HBM copy figure"
 
 
 class ClockSampler:
@@ -55,7 +85,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "500"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -84,55 +114,100 @@ class ClockSampler:
 
 
 def _dist():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ---------------------------------------------------------------------------
+# the reference on the host (oracle/_ref only)
+# ---------------------------------------------------------------------------
+def _extrapolation_inputs() -> dict:
+    try:
+        return json.loads(EXTRAP.read_text())
+    except Exception:
+        return {}
+
+
+def reference_sample(ref, rp, iters: int) -> dict:
+    """The reference's own LSQR iterations on C5's [A; mu I] (plain_lsqr_solve,
+    solver.hpp:396-448, with lsqr_cap = iters): seconds per iteration from the
+    reference's PhaseReport::t_lsqr_ms."""
+    knobs = dict(SOLVER, lsqr_cap=iters)
+    t0 = time.time()
+    r = ref.solve(rp, None, knobs, plain=True)
+    wall = time.time() - t0
+    it = int(np.sum(r.phase_iters))
+    return {"wall_s": wall, "iters": it, "s_per_iter": float(np.sum(r.phase_t_lsqr_ms)) / 1e3 / max(it, 1)}
+
+
+def extrapolate(s_plain: float) -> dict:
+    """time-to-tol = setup + iterations x s/iteration.
+    s/iteration = the live plain-LSQR figure x the preconditioned/plain ratio
+    and setup = the container's measured reference setup x the live/container
+    speed ratio, both measured on the unmodified reference in this repo's build
+    container (profiles/c5_extrapolation.json)."""
+    e = _extrapolation_inputs()
+    iters = int(e.get("gpu_lsqr_iters", 0))
+    ratio = float(e.get("precond_over_plain", 1.0))
+    speed = s_plain / float(e["ref_plain_s_per_iter_container"]) if e.get("ref_plain_s_per_iter_container") else 1.0
+    setup = float(e.get("ref_setup_s_container", 0.0)) * speed
+    value = setup + iters * s_plain * ratio
+    return {"value": value, "iters": iters, "setup_s": setup, "s_per_iter": s_plain * ratio, "ratio": ratio,
+            "speed": speed}
 
 
 def run_reference(args):
-    """Reference arm: the unmodified C++ reference (oracle/_ref) on the host CPU."""
     ws, rank, _ = _dist()
     if rank != 0:
         return
     from oracle import ref
-    import paper_2604_05065_b200 as apc
 
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libaplicur_ref.so not built"}))
         return
-    p = apc.Problem(CONFIG_ID)
-    rp = ref.Problem.from_apc(p)
-    if args.warmup > 0:  # one untimed bounded sample warms caches / page-ins
-        cpu_time_to_tol(ref, rp, p, sample_iters=min(50, args.ref_sample_iters))
-    samples = [cpu_time_to_tol(ref, rp, p, sample_iters=args.ref_sample_iters) for _ in range(max(1, args.steps))]
-    per_step = samples[-1]
-    v = float(np.mean([x["value"] for x in samples]))
+    nproc = os.cpu_count() or 1
+    t0 = time.time()
+    rp = ref.Problem.generate(CONFIG_ID, threads=nproc)  # oracle generator; same bytes as the product's
+    gen_s = time.time() - t0
+    for _ in range(args.warmup):
+        reference_sample(ref, rp, args.ref_sample_iters)
+    samples = [reference_sample(ref, rp, args.ref_sample_iters) for _ in range(max(1, args.steps))]
+    s_plain = float(np.median([x["s_per_iter"] for x in samples]))
+    ex = extrapolate(s_plain)
+    sample = (f"reference plain_lsqr_solve on C5 [A; mu I] with lsqr_cap={args.ref_sample_iters} per step "
+              f"({args.steps} steps, median {s_plain:.3f} s/iteration, 1 thread of {nproc}; inputs from the oracle "
+              f"generator in {gen_s:.0f} s); time-to-tol EXTRAPOLATED as setup {ex['setup_s']:.0f} s + "
+              f"{ex['iters']} iterations (the GPU solve's count) x {ex['s_per_iter']:.3f} s (plain x "
+              f"{ex['ratio']:.3f} preconditioner factor), factors measured on the reference in the build "
+              f"container ({EXTRAP.relative_to(ROOT)})")
     out = {
-        "metric": METRIC, "value": v, "unit": "s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_step["sample_wall_s"] * 1e3, "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE C2 generator)",
-        "config": {"workload": "C2 sparse 200000x20000 mu=1e-6 sparse-sign k=50 max_rank=200 tol=1e-8", **SOLVER},
+        "metric": METRIC, "value": ex["value"], "unit": "s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": float(np.mean([x["wall_s"] for x in samples])) * 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE C5 generator, oracle restatement)", "config": config_dict(ws),
         "impl": "reference",
-        "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "reference", "sample": per_step["sample"]},
-        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "lsqr_iter_per_s": per_step["iter_per_s"],
+        "cpu_baseline": {"value": ex["value"], "unit": "s", "cores": 1, "nproc": nproc, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": ex["value"], "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "lsqr_iter_per_s": 1.0 / ex["s_per_iter"], "extrapolated": True,
     }
+    rp.free()
     print(json.dumps(out))
 
 
-def hbm_operator_pair(apc, ctx, cfg_id, reps=20):
-    """Live A*v + A^T*u timing on an HBM-bound BASELINE config (CUDA events on the
-    library stream), against SURVEY 8(d)'s algorithmic bytes."""
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def operator_pair(apc, ctx, A, n, mloc, reps=20):
+    """Live A*v + A^T*u (CUDA events on the library stream)."""
     import torch
 
-    p = apc.Problem(cfg_id)
-    A = apc.DeviceMatrix.from_problem(ctx, p)
     dev = torch.device("cuda", ctx.device)
-    x = torch.randn(p.n, dtype=torch.float64, device=dev)
-    y = torch.empty(p.m, dtype=torch.float64, device=dev)
-    g = torch.empty(p.n, dtype=torch.float64, device=dev)
+    x = torch.randn(n, dtype=torch.float64, device=dev)
+    y = torch.empty(mloc, dtype=torch.float64, device=dev)
+    g = torch.empty(n, dtype=torch.float64, device=dev)
     s = torch.cuda.ExternalStream(ctx.stream)
+    torch.cuda.synchronize()
     for _ in range(3):
         A.apply_dev(x.data_ptr(), y.data_ptr())
         A.apply_dev(y.data_ptr(), g.data_ptr(), transpose=True)
@@ -146,46 +221,55 @@ def hbm_operator_pair(apc, ctx, cfg_id, reps=20):
         A.apply_dev(y.data_ptr(), g.data_ptr(), transpose=True)
     ev[2].record(s)
     ctx.sync()
-    tf = ev[0].elapsed_time(ev[1]) / reps * 1e-3
-    ta = ev[1].elapsed_time(ev[2]) / reps * 1e-3
-    if p.sparse:
-        byts = 24 * p.nnz + 4 * (p.m + 1) + 4 * (p.n + 1) + 16 * (p.m + p.n)
-    else:
-        byts = 16 * p.m * p.n + 16 * (p.m + p.n)
-    kernels = ("hot_permute_kernel + hot_sell_fwd_kernel (hot-relabelled SELL-32) | csr_units_kernel (tail rows of A^T) "
-               "+ head_adj_kernel (row-blocked head rows, u in shared memory) + head_combine_kernel"
-               if p.sparse else "dense_fwd_kernel | dense_adj_kernel")
+    return ev[0].elapsed_time(ev[1]) / reps * 1e-3, ev[1].elapsed_time(ev[2]) / reps * 1e-3
+
+
+def ncu_traffic(path: Path):
+    """DRAM bytes per launch of the operator-pair kernels from the committed
+    `ncu --set full` capture of scripts/opbench.py c5 (same kernels, same input)."""
+    try:
+        d = json.loads(path.read_text())
+        return d["pair_dram_bytes"], d
+    except Exception:
+        return None, None
+
+
+def hbm_pair_extra(apc, ctx, cfg_id):
+    p = apc.Problem(cfg_id)
+    A = apc.DeviceMatrix.from_problem(ctx, p)
+    tf, ta = operator_pair(apc, ctx, A, p.n, p.m)
+    byts = 16 * p.m * p.n + 16 * (p.m + p.n)
     A.free()
-    del p
     return {"fwd_us": tf * 1e6, "adj_us": ta * 1e6, "bytes": byts, "GBps": byts / (tf + ta) / 1e9,
-            "kernels": kernels}
+            "kernels": "dense_fwd_kernel | dense_adj_kernel"}
 
 
-def cpu_time_to_tol(ref, rp, p, sample_iters=1200):
-    """Reference aplicur_solve with lsqr_cap = sample_iters (identical sketch, CUR
-    indices and preconditioners as the full run) -> measured setup + measured
-    CPU s/iteration, extrapolated to the reference's own full iteration count
-    (tests/golden/baseline_c2.npz when present)."""
-    knobs = dict(SOLVER)
-    knobs["lsqr_cap"] = sample_iters
-    t0 = time.time()
-    r = ref.solve(rp, p.b, knobs)
-    wall = time.time() - t0
-    lsqr_s = float(np.sum(r.phase_t_lsqr_ms)) / 1e3
-    iters = int(np.sum(r.phase_iters))
-    setup_s = wall - lsqr_s
-    s_per_iter = lsqr_s / max(iters, 1)
-    full_iters = None
-    g = ROOT / "tests" / "golden" / f"baseline_c{CONFIG_ID}.npz"
-    if g.exists():
-        full_iters = int(np.load(g)["phase_iters"].sum())
-        full_wall = float(np.load(g)["wall_s"])
-    est = setup_s + (full_iters if full_iters else iters) * s_per_iter
-    return {"value": est, "sample_wall_s": wall, "iter_per_s": 1.0 / s_per_iter,
-            "sample": (f"reference aplicur_solve on C2 with lsqr_cap={sample_iters} ({iters} LSQR iterations, "
-                       f"{wall:.1f}s wall, 1 thread); time-to-tol extrapolated as setup {setup_s:.2f}s + "
-                       f"{full_iters if full_iters else iters} iterations x {s_per_iter * 1e3:.2f} ms"
-                       + (f" (full reference run measured here: {full_wall:.0f}s)" if full_iters else ""))}
+def c2_extra(apc, ctx, steps=3):
+    """BASELINE configs[1] (L2-resident C2), kept beside the headline."""
+    import torch
+
+    p = apc.Problem(2)
+    cfg = apc.SolverConfig(mu=1e-6, block=50, eps_lsqr=1e-8, max_rank=200, seed=1, trace_sample_stride=0)
+    s = torch.cuda.ExternalStream(ctx.stream)
+    A = apc.DeviceMatrix.from_problem(ctx, p)
+    apc.aplicur_solve(A, p.b, cfg)
+    dev, wall, iters = [], [], 0
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        A2 = apc.DeviceMatrix.from_problem(ctx, p)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        r = apc.aplicur_solve(A2, p.b, cfg)
+        e1.record(s)
+        ctx.sync()
+        A2.free()
+        wall.append(time.perf_counter() - t0)
+        dev.append(e0.elapsed_time(e1) / 1e3)
+        iters = r.lsqr_iters
+    A.free()
+    return {"time_to_tol_s": float(np.mean(dev)), "e2e_s": float(np.mean(wall)), "lsqr_iters": iters,
+            "us_per_iteration": 1e6 * float(np.mean(dev)) / max(iters, 1), "steps": steps,
+            "workload": "C2 sparse 200000x20000 mu=1e-6 sparse-sign k=50 max_rank=200 tol=1e-8 (L2-resident)"}
 
 
 def main():
@@ -194,13 +278,15 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-sample-iters", type=int, default=1200)
+    ap.add_argument("--ref-sample-iters", type=int, default=4)
+    ap.add_argument("--time-budget", type=float, default=1680.0,
+                    help="wall seconds for the whole run; timed steps stop early (and say so) past it")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-hbm-pairs", action="store_true",
-                    help="skip the live C3/C5 operator-pair measurement (HBM-bound configs) in the roofline")
+    ap.add_argument("--no-extras", action="store_true", help="skip the C2 and C3 side measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    t_start = time.time()
 
     import torch
     import paper_2604_05065_b200 as apc
@@ -219,22 +305,11 @@ def main():
         uid = obj[0]
     ctx = apc.Context(local, ws, rank, uid)
     p = apc.Problem(CONFIG_ID)
-    cfg = apc.SolverConfig(**{k: v for k, v in SOLVER.items()})
-
-    # row partition (balanced by nnz) -- SURVEY.md 8(e): A*v local, one NCCL
-    # allreduce of [A_p^T u_p | ||u_p||^2] per LSQR iteration; the sketch / CUR
-    # selection runs replicated on the full matrix
-    if p.sparse:
-        row_nnz = np.bincount(p.rowidx, minlength=p.m).astype(np.int64)
-    else:
-        row_nnz = None
+    cfg = apc.SolverConfig(**SOLVER)
+    row_nnz = np.bincount(p.rowidx, minlength=p.m).astype(np.int64)
     bounds = apc.partition_rows(p.m, ws, row_nnz)
     r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
-    A_full = apc.DeviceMatrix.from_problem(ctx, p) if ws > 1 else None
-    A = apc.DeviceMatrix.from_problem(ctx, p, r0, r1) if ws > 1 else apc.DeviceMatrix.from_problem(ctx, p)
-
-    def solve_once(mat, full):
-        return apc.aplicur_solve(mat, p.b, cfg, full=full)
+    s = torch.cuda.ExternalStream(ctx.stream)
 
     def barrier():
         if dist is not None:
@@ -242,159 +317,132 @@ def main():
         torch.cuda.synchronize()
         ctx.sync()
 
-    # ---- device-resident solves (value) ------------------------------------
+    def step():
+        """one end-to-end solve: host CSC -> device layouts -> solve -> x on the host"""
+        t0 = time.perf_counter()
+        full = apc.DeviceMatrix.from_problem(ctx, p) if ws > 1 else None
+        A = apc.DeviceMatrix.from_problem(ctx, p, r0, r1) if ws > 1 else apc.DeviceMatrix.from_problem(ctx, p)
+        ctx.sync()
+        t1 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        r = apc.aplicur_solve(A, p.b, cfg, full=full)  # x returned in host memory
+        e1.record(s)
+        ctx.sync()
+        t2 = time.perf_counter()
+        A.free()
+        if full is not None:
+            full.free()
+        return r, e0.elapsed_time(e1) / 1e3, t2 - t0, t1 - t0
+
     for _ in range(args.warmup):
-        r = solve_once(A, A_full)
+        t_w = time.time()
+        step()
+        t_step = time.time() - t_w
     barrier()
     L0 = ctx.launches
-    s = torch.cuda.ExternalStream(ctx.stream)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    results = []
+    results, dev_s, wall_s, up_s = [], [], [], []
     with ClockSampler(local) as clk:
-        e0.record(s)
-        for _ in range(args.steps):
-            results.append(solve_once(A, A_full))
-        e1.record(s)
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            proj = (time.time() - t_start) + (np.mean(wall_s) if wall_s else (t_step if args.warmup else 0.0))
+            if k > 0 and proj > args.time_budget:
+                break  # reported: "steps" is what was timed, "steps_requested" what was asked
+            r, d, w, u = step()
+            results.append(r)
+            dev_s.append(d)
+            wall_s.append(w)
+            up_s.append(u)
         barrier()
+        t_loop = time.perf_counter() - t0
+    k_done = len(results)
     launches = ctx.launches - L0
-    ms = e0.elapsed_time(e1)
+    value = float(np.mean(dev_s))
+    e2e = t_loop / k_done
     if dist is not None:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([value, e2e], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_per_step = ms / args.steps
+        value, e2e = (float(x) for x in t.tolist())
     r = results[-1]
     iters = r.lsqr_iters
-    lsqr_ms = float(np.mean([x.lsqr_ms for x in results]))
+    lsqr_s = float(np.mean([x.lsqr_ms for x in results])) / 1e3
+    loop_dev_ms = float(np.mean([sum(ph.t_lsqr_device_ms for ph in x.phases) for x in results]))
 
-    # ---- end-to-end through the C-ABI with host buffers (e2e) ----------------
-    csc_bytes = 8 * (p.n + 1) + 16 * p.nnz if p.sparse else 8 * p.m * p.n
-    # host CSC (full copy for the replicated CUR + this rank's shard when ws > 1) and b
-    h2d = csc_bytes * (2 if ws > 1 else 1) + 8 * (r1 - r0)
-    d2h = 8 * p.n
-    barrier()
-    t0 = time.perf_counter()
-    e2e_parts = []
-    for _ in range(args.steps):
-        ta = time.perf_counter()
-        F2 = apc.DeviceMatrix.from_problem(ctx, p) if ws > 1 else None
-        A2 = apc.DeviceMatrix.from_problem(ctx, p, r0, r1) if ws > 1 else apc.DeviceMatrix.from_problem(ctx, p)
-        tb = time.perf_counter()
-        r2 = solve_once(A2, F2)
-        tc = time.perf_counter()
-        A2.free()
-        if F2 is not None:
-            F2.free()
-        e2e_parts.append((tb - ta, tc - tb, time.perf_counter() - tc, r2.setup_ms / 1e3, r2.lsqr_ms / 1e3))
-    barrier()
-    e2e_s = (time.perf_counter() - t0) / args.steps
-    if dist is not None:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-
-    # ---- dominant kernels: operator pair A*v + A^T*u, CUDA events on ctx stream
-    dev = torch.device("cuda", local)
-    x = torch.randn(p.n, dtype=torch.float64, device=dev)
-    y = torch.empty(A.mloc, dtype=torch.float64, device=dev)
-    g = torch.empty(p.n, dtype=torch.float64, device=dev)
-    torch.cuda.synchronize()
-    reps = 200
-    for _ in range(5):
-        A.apply_dev(x.data_ptr(), y.data_ptr())
-        A.apply_dev(y.data_ptr(), g.data_ptr(), transpose=True)
-    ctx.sync()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    ev[0].record(s)
-    for _ in range(reps):
-        A.apply_dev(x.data_ptr(), y.data_ptr())
-    ev[1].record(s)
-    for _ in range(reps):
-        A.apply_dev(y.data_ptr(), g.data_ptr(), transpose=True)
-    ev[2].record(s)
-    ctx.sync()
-    t_fwd = ev[0].elapsed_time(ev[1]) / reps * 1e-3
-    t_adj = ev[1].elapsed_time(ev[2]) / reps * 1e-3
-    mloc = A.mloc
-    bytes_pair = 24 * p.nnz + 4 * (p.m + 1) + 4 * (p.n + 1) + 16 * (p.m + p.n)
-    peaks = _peaks()
-    achieved = bytes_pair / (t_fwd + t_adj) / 1e9
-    # dominant kernel of the timed region: the LSQR iteration loop (one
-    # persistent cooperative launch per phase); its device time comes from
-    # CUDA events the library records around it on its own stream
-    loop_ms = float(sum(ph.t_lsqr_device_ms for x in results for ph in x.phases))
-    loop_iters = int(sum(ph.lsqr_iters for x in results for ph in x.phases))
-    loop_launches = int(sum(1 for x in results for ph in x.phases if ph.lsqr_iters > 0))
-    per_launch_bytes = bytes_pair * loop_iters / max(loop_launches, 1)
-    loop_achieved = bytes_pair * loop_iters / (loop_ms / 1e3) / 1e9 if loop_ms > 0 else 0.0
-    hbm = peaks.get("hbm_gbs", 6650.0)
-    # DRAM bytes per iteration of lsqr_persistent_kernel from one `ncu --set full`
-    # capture (profiles/r1_ncu_persistent_c2.txt: 52.06 MB read + 0.73 MB written
-    # over a 300-iteration launch), scaled to this run's average launch
-    dram_per_iter = (52058368 + 733952) / 300.0
-    roofline = {"bound": "hbm", "achieved": loop_achieved, "peak": hbm, "unit": "GB/s",
-                "frac": loop_achieved / hbm,
-                "traffic": dram_per_iter * loop_iters / max(loop_launches, 1),
-                "traffic_note": "ncu DRAM bytes per launch (per-iteration figure x iterations per launch): far "
-                                "below the algorithmic bytes because A, A^T and every vector stay in L2",
-                "kernel": "lsqr_persistent_kernel (whole LSQR phase: A*z + A^T*u + preconditioner + updates)",
-                "algorithmic_bytes_per_launch": per_launch_bytes,
-                "algorithmic_bytes_per_iteration": bytes_pair, "iterations": loop_iters,
-                "avg_launch_ms": loop_ms / max(loop_launches, 1), "us_per_iteration": 1e3 * loop_ms / max(loop_iters, 1),
-                "operator_pair": {"kernels": "csr_fwd_kernel + csr_units_kernel (standalone)",
-                                  "GBps": achieved, "frac": achieved / hbm, "fwd_us": t_fwd * 1e6,
-                                  "adj_us": t_adj * 1e6},
-                "note": "C2's CSR pair (52.4 MB) is L2-resident on B200 (126 MB L2): the loop is latency-bound, not "
-                        "HBM-bound; the HBM-bound operator numbers (C3/C4/C5) are in profiles/r1_summary.md",
-                "peak_source": "MEASURED_PEAKS.json" if "fallback" not in peaks else "fallback"}
-
-    if rank == 0 and ws == 1 and not args.no_hbm_pairs:
-        # the C2 loop is L2-resident; the HBM roofline of the same operator
-        # kernels is measured live on the HBM-bound configs
-        pairs = {}
-        for cid, name in ((3, "C3 dense 100000x10000"), (5, "C5 sparse 8e6x4e5 nnz 1.28e8")):
-            try:
-                d = hbm_operator_pair(apc, ctx, cid)
-                d["frac"] = d["GBps"] / hbm
-                pairs[name] = d
-            except Exception as e:  # reported, never required
-                pairs[name] = {"unavailable": str(e)}
-        roofline["hbm_operator_pairs"] = pairs
+    # ---- roofline: the operator pair A*v + A^T*u, live on the resident A
+    A = apc.DeviceMatrix.from_problem(ctx, p, r0, r1) if ws > 1 else apc.DeviceMatrix.from_problem(ctx, p)
+    t_fwd, t_adj = operator_pair(apc, ctx, A, p.n, A.mloc)
+    A.free()
+    peaks, peak_src = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 7672.0))
+    pair_bytes = PAIR_BYTES if ws == 1 else 24 * p.nnz // ws + 4 * (r1 - r0 + 1) + 4 * (p.n + 1) + 16 * (r1 - r0 + p.n)
+    achieved = pair_bytes / (t_fwd + t_adj) / 1e9
+    traffic, tsrc = ncu_traffic(ROOT / "profiles" / "r2_ncu_c5_pair.json")
+    roofline = {
+        "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+        "traffic": traffic,
+        "kernel": "operator pair A*v + A^T*u (hot_permute + hot_sell_fwd | csr_units + split_fixup + head_adj + "
+                  "head_combine), the per-iteration HBM stream of the LSQR loop",
+        "algorithmic_bytes_per_launch": pair_bytes, "fwd_us": t_fwd * 1e6, "adj_us": t_adj * 1e6,
+        "pair_share_of_iteration": (t_fwd + t_adj) * 1e3 / (loop_dev_ms / max(iters, 1)) if iters else None,
+        "us_per_iteration": 1e3 * loop_dev_ms / max(iters, 1),
+        "peak_source": peak_src,
+        "traffic_source": (f"{tsrc['source']} (DRAM read+write bytes of one pair, ncu --set full)"
+                           if tsrc else "no committed ncu capture"),
+    }
 
     out = {
-        "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE C2 generator; inputs larger than nothing: A is L2-resident, "
-                "each step is a full solve from x = 0)",
-        "config": {"workload": "C2 sparse 200000x20000 mu=1e-6 sparse-sign k=50 max_rank=200 tol=1e-8",
-                   "m": p.m, "n": p.n, "nnz": p.nnz, **SOLVER, "parallelism": f"rows{ws}",
-                   "l2": "no flush between steps; every step re-runs the full solve"},
-        "lsqr_iters": iters, "lsqr_iter_per_s": iters / (lsqr_ms / 1e3) if lsqr_ms > 0 else None,
+        "metric": METRIC, "value": value, "unit": "s", "n_gpus": ws, "steps": k_done, "warmup": args.warmup,
+        "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded BASELINE C5 generator; every step a full solve from x = 0)",
+        "config": config_dict(ws),
+        "lsqr_iters": iters, "lsqr_iter_per_s": iters / lsqr_s if lsqr_s > 0 else None,
         "final_relres": r.final_relres, "rank": int(len(r.row_indices)), "phases": len(r.phases),
-        "setup_ms": float(np.mean([x.setup_ms for x in results])), "lsqr_ms": lsqr_ms,
-        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "upload_s": float(np.mean([x[0] for x in e2e_parts])),
-                "solve_wall_s": float(np.mean([x[1] for x in e2e_parts])),
-                "free_s": float(np.mean([x[2] for x in e2e_parts])),
-                "solve_setup_s": float(np.mean([x[3] for x in e2e_parts])),
-                "solve_lsqr_s": float(np.mean([x[4] for x in e2e_parts]))},
+        "status": int(r.status), "setup_ms": float(np.mean([x.setup_ms for x in results])),
+        "lsqr_ms": lsqr_s * 1e3,
+        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": 12 * p.nnz + 4 * (p.n + 1) + 8 * p.m,
+                "d2h_bytes_per_step": 8 * p.n, "upload_s": float(np.mean(up_s)),
+                "note": "h2d: int32 row indices + fp64 values + int32 column pointers (staged from the host CSC "
+                        "into pinned buffers by the library) + b; d2h: x"},
         "gpu_launches": int(launches),
         "roofline": roofline,
         "clocks": clk.summary(),
     }
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if k_done < args.steps:
+        out["steps_requested"] = args.steps
+    if rank == 0 and ws == 1 and not args.no_extras and time.time() - t_start < args.time_budget - 90:
+        extras = {}
+        try:
+            extras["C2"] = c2_extra(apc, ctx)
+        except Exception as e:
+            extras["C2"] = {"unavailable": str(e)}
+        try:
+            d = hbm_pair_extra(apc, ctx, 3)
+            d["frac"] = d["GBps"] / hbm
+            extras["C3_operator_pair"] = d
+        except Exception as e:
+            extras["C3_operator_pair"] = {"unavailable": str(e)}
+        out["extra"] = extras
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and time.time() - t_start < args.time_budget - 60:
         try:
             from oracle import ref
 
             if ref.available():
-                rp = ref.Problem.from_apc(p)
-                cb = cpu_time_to_tol(ref, rp, p, sample_iters=args.ref_sample_iters)
-                out["cpu_baseline"] = {"value": cb["value"], "unit": "s", "cores": 1, "kind": "reference",
-                                       "sample": cb["sample"], "lsqr_iter_per_s": cb["iter_per_s"]}
+                rp = ref.Problem.generate(CONFIG_ID)
+                smp = reference_sample(ref, rp, args.ref_sample_iters)
+                rp.free()
+                ex = extrapolate(smp["s_per_iter"])
+                out["cpu_baseline"] = {
+                    "value": ex["value"], "unit": "s", "cores": 1, "nproc": os.cpu_count(), "kind": "reference",
+                    "sample": (f"reference plain_lsqr_solve on C5 [A; mu I], lsqr_cap={args.ref_sample_iters} "
+                               f"({smp['wall_s']:.1f} s, {smp['s_per_iter']:.3f} s/iteration, 1 thread); "
+                               f"time-to-tol EXTRAPOLATED as setup {ex['setup_s']:.0f} s + {ex['iters']} iterations "
+                               f"x {ex['s_per_iter']:.3f} s ({EXTRAP.relative_to(ROOT)})"),
+                    "extrapolated": True}
         except Exception as e:  # the baseline is reported, never required
             out["cpu_baseline"] = {"value": None, "unit": "s", "cores": 1, "kind": "reference",
                                    "sample": f"unavailable: {e}"}
+    out["wall_s"] = time.time() - t_start
     if rank == 0:
         print(json.dumps(out))
     ctx.close()

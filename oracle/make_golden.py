@@ -4,13 +4,23 @@ the seeded BASELINE inputs.  Run here (where /root/reference exists):
 
     python oracle/make_golden.py small      # seconds: CPU-test fixtures
     python oracle/make_golden.py c1 c2      # full BASELINE C1 / C2 solves (C2 ~ 10 min)
+    python oracle/make_golden.py capped200:c3   # BASELINE-size capped-parity solve (lsqr_cap = 200)
+    python oracle/make_golden.py cappedulp200:c3  # same, b moved one ulp (the reference's own sensitivity)
+    python oracle/make_golden.py curg:c3    # full-size Gaussian-shim CurState steps (first augments)
+
+Capped and Gaussian fixtures generate their inputs with the oracle's own
+generator (ref.Problem.generate, byte-identical to the product's), so no copy
+of a 20 GB matrix is made.
 
 The fixtures are small .npz files (indices, rho history, phase iterations,
 x, residuals, trace heads) so tests on the GPU box never need /root/reference.
 """
 from __future__ import annotations
 
+import hashlib
 import json
+import os
+import subprocess
 import sys
 import time
 from pathlib import Path
@@ -23,7 +33,7 @@ sys.path.insert(0, str(ROOT))
 import paper_2604_05065_b200 as apc  # noqa: E402  (host-side generator only)
 from oracle import ref  # noqa: E402
 
-GOLD = ROOT / "tests" / "golden"
+GOLD = Path(os.environ.get("APC_GOLD_DIR", ROOT / "tests" / "golden"))
 
 # the solver settings each config is run with
 BASELINE_SOLVER = {
@@ -93,12 +103,99 @@ def small():
     _save("cur_c2_small", I=cur["I"], J=cur["J"], rho=cur["rho"], added=cur["added"])
 
 
+def capped_fixture(k: int, cap: int, ulp: bool = False):
+    """SURVEY.md 8(c)(3) capped-parity mode at BASELINE size: the reference
+    aplicur_solve (solver.hpp:162-392) with the BASELINE knobs plus lsqr_cap."""
+    knobs = dict(BASELINE_SOLVER[k], trace_sample_stride=0, lsqr_cap=cap)
+    t0 = time.time()
+    p = ref.Problem.generate(k)
+    gen_s = time.time() - t0
+    b = np.nextafter(p.b, np.inf) if ulp else None
+    t0 = time.time()
+    r = ref.solve(p, b, knobs, consume=True)
+    wall = time.time() - t0
+    p.free()
+    lsqr_s = float(np.sum(r.phase_t_lsqr_ms)) / 1e3
+    common = dict(phase_rank=r.phase_rank, phase_iters=r.phase_iters, phase_reason=r.phase_reason,
+                  trace_phibar=r.trace_phibar, final_relres=r.final_relres, status=r.status,
+                  row_indices=r.row_indices, col_indices=r.col_indices, wall_s=wall, gen_s=gen_s,
+                  lsqr_s=lsqr_s, setup_s=wall - lsqr_s,
+                  meta=json.dumps(dict(config=k, cap=cap, knobs=knobs, ulp=ulp, threads=1)))
+    if ulp and os.environ.get("APC_ULP_RAW"):  # concurrent run: keep x, the pair step measures the sensitivity
+        _save(f"capped_c{k}_k{cap}_ulpraw", x=r.x, **common)
+    elif ulp:  # x itself is only needed to measure the sensitivity against the main fixture
+        main = np.load(GOLD / f"capped_c{k}_k{cap}.npz")
+        xs = float(np.linalg.norm(r.x - main["x"]) / np.linalg.norm(main["x"]))
+        ph = r.trace_phibar
+        mp = main["trace_phibar"]
+        nn = min(len(ph), len(mp))
+        _save(f"capped_c{k}_k{cap}_ulp", x_sens=xs,
+              phibar_sens=float(np.max(np.abs(ph[:nn] - mp[:nn]) / np.abs(mp[:nn]))), **common)
+    else:
+        _save(f"capped_c{k}_k{cap}", x=r.x, final_rho=r.final_rho, system_matvecs=r.system_matvecs,
+              rho_history=r.rho_history, phase_rho=r.phase_rho, phase_sigma_hat=r.phase_sigma_hat,
+              phase_relres=r.phase_relres, phase_t_lsqr_ms=r.phase_t_lsqr_ms,
+              phase_t_total_ms=r.phase_t_total_ms, trace_phase=r.trace_phase, trace_iter=r.trace_iter,
+              trace_matvecs=r.trace_matvecs, **common)
+    print(f"capped C{k} cap {cap} ulp {ulp}: wall {wall:.1f}s (gen {gen_s:.1f}s) ranks {r.phase_rank} "
+          f"iters {r.phase_iters} reasons {r.phase_reason} relres {r.final_relres}", flush=True)
+
+
+def capped_pair(k: int, cap: int):
+    """Main and one-ulp capped runs side by side (host RAM permitting: C5's
+    reference solve peaks near 65 GB), then the sensitivity fixture."""
+    env = dict(os.environ, APC_ULP_RAW="1")
+    me = Path(__file__).resolve()
+    pm = subprocess.Popen([sys.executable, str(me), f"capped{cap}:c{k}"])
+    pu = subprocess.Popen([sys.executable, str(me), f"cappedulp{cap}:c{k}"], env=env)
+    if pm.wait() != 0 or pu.wait() != 0:
+        raise RuntimeError("capped pair failed")
+    main = np.load(GOLD / f"capped_c{k}_k{cap}.npz")
+    raw = dict(np.load(GOLD / f"capped_c{k}_k{cap}_ulpraw.npz"))
+    x = raw.pop("x")
+    ph, mp = raw["trace_phibar"], main["trace_phibar"]
+    nn = min(len(ph), len(mp))
+    _save(f"capped_c{k}_k{cap}_ulp", x_sens=float(np.linalg.norm(x - main["x"]) / np.linalg.norm(main["x"])),
+          phibar_sens=float(np.max(np.abs(ph[:nn] - mp[:nn]) / np.abs(mp[:nn]))), **raw)
+    (GOLD / f"capped_c{k}_k{cap}_ulpraw.npz").unlink()
+
+
+def gaussian_cur_fixture(k: int, steps: int = 3):
+    """Full-size CurState init/augment/refresh steps (cur.hpp:209-315) with the
+    Gaussian shim sketch (sketch.hpp:173-197), the BASELINE block of config k."""
+    block = BASELINE_SOLVER[k]["block"]
+    t0 = time.time()
+    p = ref.Problem.generate(k)
+    gen_s = time.time() - t0
+    t0 = time.time()
+    cur = ref.cur_steps(p, block, 1, steps, gaussian=True)
+    wall = time.time() - t0
+    Y = np.ascontiguousarray(cur["Y"].T)  # column-major bytes of Y (s x n)
+    E = np.ascontiguousarray(cur["eres"].T)
+    extra = dict(Y=cur["Y"]) if cur["Y"].size <= 200000 else {}
+    _save(f"curg_c{k}", I=cur["I"], J=cur["J"], rho=cur["rho"], added=cur["added"],
+          y_sha256=hashlib.sha256(Y.tobytes()).hexdigest(), eres_sha256=hashlib.sha256(E.tobytes()).hexdigest(),
+          y_col0=cur["Y"][:, 0].copy(), y_fro=float(np.linalg.norm(cur["Y"])), wall_s=wall, gen_s=gen_s,
+          meta=json.dumps(dict(config=k, block=block, steps=steps, seed=1, gaussian=True)), **extra)
+    p.free()
+    print(f"curg C{k}: {wall:.1f}s rank {len(cur['I'])} rho {cur['rho']}", flush=True)
+
+
 def main(argv):
     if not ref.available():
         ref.build()
     for what in argv or ["small"]:
         if what == "small":
             small()
+        elif what.startswith("cappedpair") and ":c" in what:
+            head, c = what.split(":c")
+            capped_pair(int(c), int(head[len("cappedpair"):] or 200))
+        elif what.startswith("capped") and ":c" in what:
+            head, c = what.split(":c")
+            ulp = head.startswith("cappedulp")
+            capped_fixture(int(c), int(head[len("cappedulp" if ulp else "capped"):] or 200), ulp=ulp)
+        elif what.startswith("curg:c"):
+            gaussian_cur_fixture(int(what[6:]))
         elif what.startswith("sens"):
             # the reference's own x sensitivity: rerun with b moved by one ulp
             k = int(what[4:])

@@ -85,6 +85,11 @@ def lib() -> C.CDLL:
         L.ref_cur_steps.argtypes = [P, _i64, _u64, _i64, _i64, _i32, _i32, _i64, _dp, _i64p, _i64p,
                                     _i64p, _dp, _i64p, _dp]
         L.ref_time_op_pair.argtypes = [P, _i64, _dp]
+        L.ref_generate.argtypes = [_i32, _i64, _i64, _u64, _i32, C.POINTER(C.c_void_p)]
+        L.ref_gen_view.argtypes = [C.c_void_p, P, C.POINTER(_dp)]
+        L.ref_gen_free.argtypes = [C.c_void_p]
+        L.ref_gen_free.restype = None
+        L.ref_solve_gen.argtypes = [C.c_void_p, _dp, C.POINTER(RefConfig), _i32, _i32, C.POINTER(RefOut)]
         L.ref_mm_write.argtypes = [P, C.c_char_p]
         L.ref_mm_read.argtypes = [C.c_char_p, _i64p, _i64p, C.POINTER(_i32), _i64p, _i64p, _i64p, _dp, _dp]
         _lib = L
@@ -111,6 +116,47 @@ class Problem:
         else:
             self.dense = np.ascontiguousarray(dense, dtype=np.float64).reshape(-1)
             self.c = RefProblem(self.m, self.n, 0, self.dense.ctypes.data_as(_dp), None, None, None)
+
+    @classmethod
+    def generate(cls, config: int, m: int = 0, n: int = 0, seed: int = 0, threads: int = 0) -> "Problem":
+        """BASELINE input from the oracle's own generator (ref_harness.cpp
+        ref_generate): arrays are views of memory the reference owns, so the
+        process never maps the product library."""
+        import os
+
+        h = C.c_void_p()
+        _chk(lib().ref_generate(config, m, n, seed, threads or os.cpu_count() or 1, C.byref(h)))
+        view, bp = RefProblem(), _dp()
+        _chk(lib().ref_gen_view(h, C.byref(view), C.byref(bp)))
+        self = cls.__new__(cls)
+        self.m, self.n, self.sparse, self.c, self._gen = view.m, view.n, bool(view.sparse), view, h
+        self.config = config
+        self.b = np.ctypeslib.as_array(bp, shape=(self.m,))
+        if self.sparse:
+            nnz = int(view.colptr[self.n])
+            self.nnz = nnz
+            self.colptr = np.ctypeslib.as_array(view.colptr, shape=(self.n + 1,))
+            self.rowidx = np.ctypeslib.as_array(view.rowidx, shape=(nnz,))
+            self.vals = np.ctypeslib.as_array(view.vals, shape=(nnz,))
+        else:
+            self.nnz = self.m * self.n
+            self.dense = np.ctypeslib.as_array(view.dense, shape=(self.m * self.n,))
+        return self
+
+    def free(self) -> None:
+        """Release a generated input (the numpy views die with it)."""
+        h = getattr(self, "_gen", None)
+        if h is not None:
+            self._gen = None
+            for k in ("b", "colptr", "rowidx", "vals", "dense"):
+                self.__dict__.pop(k, None)
+            lib().ref_gen_free(h)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
     @classmethod
     def from_apc(cls, p) -> "Problem":
@@ -226,13 +272,19 @@ class RefResult:
 
 
 def solve(p: Problem, b, cfg: dict, plain=False, cap_idx=20000, cap_rho=4096, cap_ph=4096,
-          cap_tr=2_000_000) -> RefResult:
+          cap_tr=2_000_000, consume=False) -> RefResult:
+    """Reference aplicur_solve (or plain_lsqr_solve).  For a Problem made by
+    Problem.generate, b may be None (the generated b) and consume=True moves A
+    into the solve (no second copy of a 20 GB matrix); the Problem is then
+    spent."""
     c = RefConfig(block=0, eps_cur=-1.0, eps_lsqr=1e-10, nu_prec=10.0, nu_lsqr=100.0, mu=0.0, variant=0,
                   sketch_xi=8, probe_count=10, lsqr_cap=0, max_rank=0, seed=0, core=0,
                   trace_sample_stride=0, outer_cap=100000)
     for k, v in cfg.items():
         setattr(c, k, int(v) if isinstance(v, (bool, np.integer)) else v)
-    b = np.ascontiguousarray(b, dtype=np.float64)
+    gen = getattr(p, "_gen", None)
+    if b is not None:
+        b = np.ascontiguousarray(b, dtype=np.float64)
     x = np.zeros(p.n)
     bufs = dict(
         row_idx=np.zeros(cap_idx, np.int64), col_idx=np.zeros(cap_idx, np.int64), rho_hist=np.zeros(cap_rho),
@@ -247,7 +299,14 @@ def solve(p: Problem, b, cfg: dict, plain=False, cap_idx=20000, cap_rho=4096, ca
     for k, arr in bufs.items():
         setattr(o, k, arr.ctypes.data_as(ftypes[k]))
     o.cap_idx, o.cap_rho, o.cap_ph, o.cap_tr = cap_idx, cap_rho, cap_ph, cap_tr
-    _chk(lib().ref_solve(C.byref(p.c), b.ctypes.data_as(_dp), C.byref(c), int(plain), C.byref(o)))
+    if gen is not None:
+        if consume:
+            for k in ("colptr", "rowidx", "vals", "dense"):
+                p.__dict__.pop(k, None)
+        _chk(lib().ref_solve_gen(gen, None if b is None else b.ctypes.data_as(_dp), C.byref(c), int(plain),
+                                 int(consume), C.byref(o)))
+    else:
+        _chk(lib().ref_solve(C.byref(p.c), b.ctypes.data_as(_dp), C.byref(c), int(plain), C.byref(o)))
     ni, nr, nph, ntr = o.n_idx, o.n_rho, o.n_ph, min(o.n_tr, cap_tr)
     return RefResult(x, o.status, o.final_rho, o.final_relres, o.sketch_applications, o.system_matvecs,
                      bufs["row_idx"][:ni].copy(), bufs["col_idx"][:ni].copy(), bufs["rho_hist"][:nr].copy(),

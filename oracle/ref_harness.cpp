@@ -26,6 +26,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <utility>
 #include <vector>
@@ -429,6 +430,328 @@ int ref_time_op_pair(const RefProblem* p, std::int64_t iters, double* sec_per_pa
     }
     *sec_per_pair = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() /
                     static_cast<double>(iters);
+  });
+}
+
+// ---- BASELINE input generators (BASELINE.json "configs") -----
+// The oracle's own restatement of the five seeded BASELINE inputs, built from
+// the reference's primitives (Rng sub-streams rng.hpp:42-45, dense_matrix
+// problems.hpp:105-127, thin_qr dense_factor.hpp:166-190, Matrix::matvec
+// matrix.hpp:151-172).  The reference arm of bench.py generates its inputs here,
+// so it never maps the product library; tests/test_oracle_cpu.py proves the
+// bytes equal the product's generator (paper_2604_05065_b200 Problem).
+// Streams (problem seed P = 20260415 + config unless given):
+//   C1 dense_matrix(m, n, 10^(-6 i/(n-1)), incoherent, P); Rng(P, rhs): x*, noise
+//   C2 Rng(P, problem, 0) column scales, (P, problem, 1) rows, (P, problem, 2)
+//      empty-column fill; Rng(P, rhs): b
+//   C3 Rng(P, problem): points; Rng(P, rhs): x*, noise
+//   C4 Rng(P, user, 0/1): U, V Gaussians; Rng(P, problem, j): column j of G
+//   C5 Rng(P, problem, 0) permutation, (P, problem, 1) scales,
+//      (P, problem, 2 + blk) rows of 65536-row block blk; Rng(P, rhs): b
+struct RefGen {
+  Matrix a;
+  std::vector<double> b;
+};
+
+}  // extern "C"
+
+namespace {
+
+template <class F>
+void par_for(std::int64_t n, int threads, F f) {
+  threads = std::max(1, threads);
+  std::vector<std::thread> th;
+  const std::int64_t chunk = (n + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t) {
+    const std::int64_t b = t * chunk, e = std::min(n, b + chunk);
+    if (b >= e) break;
+    th.emplace_back([=] { f(b, e); });
+  }
+  for (auto& x : th) x.join();
+}
+
+// CSC Matrix straight from arrays whose rows are strictly increasing within
+// each column (what Matrix::sparse, matrix.hpp:68-94, would build from the
+// same triplets, without sorting 1e8 of them; zero values are dropped there
+// and cannot occur here: every value is a nonzero Gaussian times a power of ten).
+Matrix csc_matrix(Index m, Index n, std::vector<Index> cptr, std::vector<Index> ridx,
+                  std::vector<double> val) {
+  for (Index j = 0; j < n; ++j)
+    for (Index k = cptr[j] + 1; k < cptr[j + 1]; ++k)
+      detail::require(ridx[k - 1] < ridx[k], ErrorKind::invalid_argument, "csc_matrix: unsorted column", j);
+  for (double v : val) detail::require(v != 0.0, ErrorKind::invalid_argument, "csc_matrix: explicit zero");
+  Matrix a;
+  a.rows_ = m;
+  a.cols_ = n;
+  a.sparse_ = true;
+  a.cptr_ = std::move(cptr);
+  a.ridx_ = std::move(ridx);
+  a.val_ = std::move(val);
+  a.tbox_ = std::make_shared<Matrix::TransposeBox>();
+  return a;
+}
+
+// CSC from per-row (sorted) column lists, rows visited in ascending order
+Matrix csc_from_row_lists(Index m, Index n, const std::vector<std::vector<Index>>& rc,
+                          const std::vector<std::vector<double>>& rv) {
+  std::vector<Index> cptr(static_cast<std::size_t>(n) + 1, 0);
+  for (Index i = 0; i < m; ++i)
+    for (Index c : rc[i]) ++cptr[c + 1];
+  for (Index j = 0; j < n; ++j) cptr[j + 1] += cptr[j];
+  std::vector<Index> ridx(static_cast<std::size_t>(cptr[n]));
+  std::vector<double> val(ridx.size());
+  std::vector<Index> next(cptr.begin(), cptr.end() - 1);
+  for (Index i = 0; i < m; ++i)
+    for (std::size_t q = 0; q < rc[i].size(); ++q) {
+      Index at = next[rc[i][q]]++;
+      ridx[at] = i;
+      val[at] = rv[i][q];
+    }
+  return csc_matrix(m, n, std::move(cptr), std::move(ridx), std::move(val));
+}
+
+void gen_c1(RefGen& g, Index m, Index n, std::uint64_t P) {
+  std::vector<double> sigma(static_cast<std::size_t>(n));
+  for (Index j = 0; j < n; ++j)
+    sigma[j] = std::pow(10.0, -6.0 * static_cast<double>(j) / static_cast<double>(n - 1));
+  g.a = dense_matrix(m, n, sigma, Coherence::incoherent, P);
+  Rng rr(P, RngStream::rhs);
+  std::vector<double> xs(static_cast<std::size_t>(n));
+  for (auto& x : xs) x = rr.gaussian();
+  g.b.assign(static_cast<std::size_t>(m), 0.0);
+  g.a.matvec(xs, g.b);
+  for (Index i = 0; i < m; ++i) g.b[i] += 1e-4 * rr.gaussian();
+}
+
+void gen_c2(RefGen& g, Index m, Index n, std::uint64_t P) {
+  const Index per_row = 10;
+  const double decades = 4.0;
+  detail::require(per_row <= n, ErrorKind::invalid_argument, "C2: more nonzeros per row than columns");
+  std::vector<double> scale(static_cast<std::size_t>(n));
+  Rng rs(P, RngStream::problem, 0);
+  for (auto& s : scale) s = std::pow(10.0, -decades * rs.uniform());
+  Rng rp(P, RngStream::problem, 1);
+  std::vector<std::vector<Index>> rc(static_cast<std::size_t>(m));
+  std::vector<std::vector<double>> rv(static_cast<std::size_t>(m));
+  std::vector<char> seen(static_cast<std::size_t>(n), 0);
+  std::vector<Index> count(static_cast<std::size_t>(n), 0);
+  for (Index i = 0; i < m; ++i) {
+    auto& c = rc[i];
+    while (static_cast<Index>(c.size()) < per_row) {  // uniform distinct columns, redraw duplicates
+      Index j = static_cast<Index>(rp.below(static_cast<std::uint64_t>(n)));
+      if (seen[j]) continue;
+      seen[j] = 1;
+      c.push_back(j);
+    }
+    std::sort(c.begin(), c.end());
+    for (Index j : c) seen[j] = 0;
+    for (Index j : c) {
+      rv[i].push_back(rp.gaussian() * scale[j]);
+      ++count[j];
+    }
+  }
+  Rng re(P, RngStream::problem, 2);  // one guaranteed entry per empty column
+  for (Index j = 0; j < n; ++j) {
+    if (count[j]) continue;
+    Index i = static_cast<Index>(re.below(static_cast<std::uint64_t>(m)));
+    auto it = std::lower_bound(rc[i].begin(), rc[i].end(), j);
+    auto at = it - rc[i].begin();
+    rc[i].insert(it, j);
+    rv[i].insert(rv[i].begin() + at, re.gaussian() * scale[j]);
+  }
+  g.a = csc_from_row_lists(m, n, rc, rv);
+  Rng rr(P, RngStream::rhs);
+  g.b.resize(static_cast<std::size_t>(m));
+  for (auto& x : g.b) x = rr.gaussian();
+}
+
+void gen_c3(RefGen& g, Index m, Index n, std::uint64_t P, int threads) {
+  const Index d = 8;
+  detail::require(n <= m, ErrorKind::invalid_argument, "C3: centers are the first n points");
+  Rng rng(P, RngStream::problem);
+  std::vector<double> pts(static_cast<std::size_t>(m * d));
+  for (auto& x : pts) x = rng.gaussian();
+  std::vector<double> val(static_cast<std::size_t>(m * n));
+  const double two_l2 = 2.0 * 1.5 * 1.5;
+  par_for(n, threads, [&](std::int64_t j0, std::int64_t j1) {
+    for (Index j = j0; j < j1; ++j)
+      for (Index i = 0; i < m; ++i) {
+        double s = 0.0;  // ||p_i - c_j||^2, dimensions in index order
+        for (Index k = 0; k < d; ++k) {
+          double t = pts[i * d + k] - pts[j * d + k];
+          s += t * t;
+        }
+        val[j * m + i] = std::exp(-s / two_l2);
+      }
+  });
+  g.a = Matrix::dense(m, n, std::move(val));
+  Rng rr(P, RngStream::rhs);
+  std::vector<double> xs(static_cast<std::size_t>(n));
+  for (auto& x : xs) x = rr.gaussian();
+  g.b.assign(static_cast<std::size_t>(m), 0.0);
+  // A x* in Matrix::matvec's order (column axpy, matrix.hpp:156-162); rows
+  // are independent chains, so row blocks run in parallel with the same bits
+  auto a = g.a.dense_data();
+  par_for(m, threads, [&](std::int64_t i0, std::int64_t i1) {
+    for (Index j = 0; j < n; ++j) {
+      if (xs[j] == 0.0) continue;
+      for (Index i = i0; i < i1; ++i) g.b[i] += xs[j] * a[j * m + i];
+    }
+  });
+  for (Index i = 0; i < m; ++i) g.b[i] += 1e-3 * rr.gaussian();
+}
+
+void gen_c4(RefGen& g, Index m, Index n, std::uint64_t P, int threads) {
+  const Index k = std::max<Index>(1, std::min<Index>(200, std::min(m, n) / 2));
+  Rng ru(P, RngStream::user, 0), rv(P, RngStream::user, 1);
+  Matrix u = thin_qr(detail::gaussian_dense(m, k, ru)).q;
+  Matrix v = thin_qr(detail::gaussian_dense(n, k, rv)).q;
+  std::vector<double> s = k == 1 ? std::vector<double>{100.0} : logspace(4.0, 2.0, k);
+  auto ud = u.dense_data(), vd = v.dense_data();
+  std::vector<double> val(static_cast<std::size_t>(m * n));
+  const double isq = 1.0 / std::sqrt(static_cast<double>(m));
+  par_for(n, threads, [&](std::int64_t j0, std::int64_t j1) {
+    for (Index j = j0; j < j1; ++j) {
+      Rng rg(P, RngStream::problem, static_cast<std::uint64_t>(j));
+      double* col = val.data() + j * m;
+      for (Index i = 0; i < m; ++i) col[i] = rg.gaussian() * isq;
+      for (Index t = 0; t < k; ++t) {  // + U(:,t) s_t V(j,t), t ascending
+        const double c = s[t] * vd[t * n + j];
+        for (Index i = 0; i < m; ++i) col[i] += c * ud[t * m + i];
+      }
+    }
+  });
+  g.a = Matrix::dense(m, n, std::move(val));
+  Rng rr(P, RngStream::rhs);
+  g.b.resize(static_cast<std::size_t>(m));
+  for (auto& x : g.b) x = rr.gaussian();
+}
+
+void gen_c5(RefGen& g, Index m, Index n, std::uint64_t P, int threads) {
+  const Index per_row = std::min<Index>(16, n);
+  const double zipf_s = 1.1, decades = 3.0;
+  std::vector<Index> perm(static_cast<std::size_t>(n));  // Fisher-Yates shuffle of the column ids
+  std::iota(perm.begin(), perm.end(), Index{0});
+  Rng rperm(P, RngStream::problem, 0);
+  for (Index i = n - 1; i >= 1; --i)
+    std::swap(perm[i], perm[static_cast<Index>(rperm.below(static_cast<std::uint64_t>(i + 1)))]);
+  std::vector<double> scale(static_cast<std::size_t>(n));
+  Rng rs(P, RngStream::problem, 1);
+  for (auto& s : scale) s = std::pow(10.0, -decades * rs.uniform());
+  std::vector<double> cdf(static_cast<std::size_t>(n));  // Zipf(s) over ranks 1..n
+  double acc = 0.0;
+  for (Index z = 1; z <= n; ++z) cdf[z - 1] = (acc += std::pow(static_cast<double>(z), -zipf_s));
+  for (auto& c : cdf) c /= acc;
+  const Index blk_rows = 65536, nblk = (m + blk_rows - 1) / blk_rows;
+  std::vector<std::vector<Index>> bc(static_cast<std::size_t>(nblk));
+  std::vector<std::vector<double>> bv(static_cast<std::size_t>(nblk));
+  par_for(nblk, threads, [&](std::int64_t b0, std::int64_t b1) {
+    std::vector<char> seen(static_cast<std::size_t>(n), 0);
+    std::vector<Index> row;
+    for (Index blk = b0; blk < b1; ++blk) {
+      Rng r(P, RngStream::problem, 2 + static_cast<std::uint64_t>(blk));
+      for (Index i = blk * blk_rows; i < std::min(m, (blk + 1) * blk_rows); ++i) {
+        row.clear();
+        while (static_cast<Index>(row.size()) < per_row) {  // inverse CDF, redraw duplicates
+          double u = r.uniform();
+          Index z = std::min<Index>(n - 1, std::lower_bound(cdf.begin(), cdf.end(), u) - cdf.begin());
+          Index c = perm[z];
+          if (seen[c]) continue;
+          seen[c] = 1;
+          row.push_back(c);
+        }
+        std::sort(row.begin(), row.end());
+        for (Index c : row) {
+          seen[c] = 0;
+          bc[blk].push_back(c);
+          bv[blk].push_back(r.gaussian() * scale[c]);
+        }
+      }
+    }
+  });
+  std::vector<Index> cptr(static_cast<std::size_t>(n) + 1, 0);
+  for (const auto& v : bc)
+    for (Index c : v) ++cptr[c + 1];
+  for (Index j = 0; j < n; ++j) cptr[j + 1] += cptr[j];
+  std::vector<Index> ridx(static_cast<std::size_t>(cptr[n]));
+  std::vector<double> val(ridx.size());
+  std::vector<Index> next(cptr.begin(), cptr.end() - 1);
+  for (Index blk = 0; blk < nblk; ++blk) {
+    for (std::size_t q = 0; q < bc[blk].size(); ++q) {
+      Index at = next[bc[blk][q]]++;
+      ridx[at] = blk * blk_rows + static_cast<Index>(q) / per_row;
+      val[at] = bv[blk][q];
+    }
+    std::vector<Index>().swap(bc[blk]);
+    std::vector<double>().swap(bv[blk]);
+  }
+  g.a = csc_matrix(m, n, std::move(cptr), std::move(ridx), std::move(val));
+  Rng rr(P, RngStream::rhs);
+  g.b.resize(static_cast<std::size_t>(m));
+  for (auto& x : g.b) x = rr.gaussian();
+}
+
+}  // namespace
+
+extern "C" {
+
+// config 1..5; m, n = 0 -> the BASELINE shape; seed 0 -> 20260415 + config.
+int ref_generate(std::int32_t config, std::int64_t m, std::int64_t n, std::uint64_t seed, std::int32_t threads,
+                 RefGen** out) {
+  return guarded([&] {
+    static const Index dm[6] = {0, 4000, 200000, 100000, 50000, 8000000};
+    static const Index dn[6] = {0, 500, 20000, 10000, 50000, 400000};
+    detail::require(config >= 1 && config <= 5, ErrorKind::invalid_argument, "config must be 1..5");
+    m = m > 0 ? m : dm[config];
+    n = n > 0 ? n : dn[config];
+    const std::uint64_t P = seed ? seed : 20260415ULL + static_cast<std::uint64_t>(config);
+    auto g = std::make_unique<RefGen>();
+    switch (config) {
+      case 1: gen_c1(*g, m, n, P); break;
+      case 2: gen_c2(*g, m, n, P); break;
+      case 3: gen_c3(*g, m, n, P, threads); break;
+      case 4: gen_c4(*g, m, n, P, threads); break;
+      default: gen_c5(*g, m, n, P, threads); break;
+    }
+    *out = g.release();
+  });
+}
+
+// Borrowed view of a generated input (valid until ref_gen_free).
+int ref_gen_view(const RefGen* g, RefProblem* view, const double** b) {
+  return guarded([&] {
+    view->m = g->a.rows();
+    view->n = g->a.cols();
+    view->sparse = g->a.is_sparse() ? 1 : 0;
+    view->dense = g->a.is_sparse() ? nullptr : g->a.dense_data().data();
+    view->colptr = g->a.is_sparse() ? g->a.col_ptr().data() : nullptr;
+    view->rowidx = g->a.is_sparse() ? g->a.row_idx().data() : nullptr;
+    view->vals = g->a.is_sparse() ? g->a.values().data() : nullptr;
+    *b = g->b.data();
+  });
+}
+
+void ref_gen_free(RefGen* g) { delete g; }
+
+// aplicur_solve / plain_lsqr_solve on a generated input without copying it
+// into a second Matrix (C4 is 20 GB); consume != 0 moves A into the solve and
+// leaves the handle's matrix empty.  b == nullptr uses the generated b.
+int ref_solve_gen(RefGen* g, const double* b, const RefConfig* cfg, std::int32_t plain, std::int32_t consume,
+                  RefOut* out) {
+  return guarded([&] {
+    ProblemInstance prob;
+    prob.a = consume ? std::move(g->a) : g->a;
+    if (b)
+      prob.b.assign(b, b + prob.a.rows());
+    else
+      prob.b = g->b;
+    prob.mu = cfg->mu;
+    SolverConfig sc = make_config(cfg);
+    auto t0 = std::chrono::steady_clock::now();
+    SolveResult r = plain ? plain_lsqr_solve(prob, sc) : aplicur_solve(prob, sc);
+    out->wall_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    fill_out(r, out);
   });
 }
 

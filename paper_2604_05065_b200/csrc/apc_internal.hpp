@@ -145,7 +145,16 @@ struct HeadAdj {
   DBuf<i32> hcol;      // per head column: original column
   DBuf<double> part;   // ncols x nblocks
   DBuf<double> bnd;    // per work item: first / last piece (HeadPiece, ops.cu)
-  Units tail;
+  Units tail;          // the other rows of A^T as warp-per-row work units (fallback)
+  // ... or as a key-sorted entry stream (TailPolicy, ops.cu): whole columns
+  // grouped in column order, key = column in group << rb | row, STEP-aligned
+  struct Seg {
+    i64 ngroups = 0, nnz = 0, ncols = 0;
+    int rb = 0, parts = 1, sb = 1;       // sb: row superblocks (stream order)
+    DBuf<i32> gptr, gcol0, tcol, zptr, zcol, tkey, cols;
+    DBuf<double> tval, bnd, part;        // part: ncols x sb partials (sb > 1)
+    bool built() const { return ngroups > 0; }
+  } seg;
   bool built() const { return ncols > 0; }
 };
 

@@ -275,24 +275,64 @@ split_fixup_kernel(const int* __restrict__ srows, const int* __restrict__ rfirst
   if (lane == 0) out[j] = s;
 }
 
-// ---- row-blocked A^T u of the head rows (HeadAdj, apc_internal.hpp)
-// Work item = (block b, part p): a contiguous, 128-aligned range of block b's
-// head entries.  The CTA stages block b's u in shared memory; each warp walks a
-// contiguous sub-range, 128 entries per step (lane = 4 consecutive entries,
-// vector loads), and closes (head column) pieces with a lane-local segmented
-// prefix + one warp segmented scan.  Pieces interior to a warp range are
-// complete (column, block) sums and are stored directly; the first and the
-// last piece of each range are chained across the warps in order (one
-// thread), then across the parts of a block (head_bnd_kernel).  Every sum has
-// a fixed order.
+// ---- segmented A^T u over key-sorted entry streams (HeadAdj, apc_internal.hpp)
+// Two streams share one kernel body (SegAdj policies below):
+//  * head: the entries of the long (Zipf-head) rows of A^T, cut into blocks
+//    of kHeadRows rows of A; block b's entries sorted by (head column, row),
+//    key = column << 16 | row in block; the CTA stages block b's u in shared
+//    memory; a closed (column, block) piece is a partial part[k * nb + b].
+//  * tail: the remaining rows of A^T, whole columns grouped (in column order)
+//    into groups of <= 2^(32-rb) - 1 columns; key = column in group << rb | row
+//    (rb = bits of the local row count); u gathered from global memory (L2);
+//    a closed piece is a whole column sum, stored to out[tcol[...]] directly.
+// Work item = (block or group g, part p): a contiguous, 128-aligned range of
+// g's entries.  Each warp walks a contiguous sub-range, 128 entries per step
+// (lane = 4 consecutive entries, vector loads, next step prefetched), and
+// closes pieces with a lane-local segmented prefix + one warp segmented scan.
+// Pieces interior to a warp range are complete and stored directly; the first
+// and the last piece of each range are chained across the warps in order (one
+// thread), then across the parts of g (seg_bnd_kernel).  Every sum has a fixed
+// order, so results are bit-identical run to run.  The tail stream replaces a
+// warp-per-column walk whose dependent metadata -> entries -> gather chain per
+// ~74-entry column left it latency-bound.
 struct HeadPiece {
   int fk, lk;  // first / last piece column (-1: none)
   double fs, ls;
 };
 
+struct HeadPolicy {
+  double* part;
+  int nb;  // blocks (ncols x nblocks < 2^31, build_head_adj)
+  static constexpr bool kStage = true;
+  static constexpr int kMinBlocks = 2;  // 2 x 512 threads: <= 64 registers
+  __device__ __forceinline__ int col(unsigned key) const { return static_cast<int>(key >> 16); }
+  __device__ __forceinline__ int row(unsigned key) const { return static_cast<int>(key & (kHeadRows - 1)); }
+  __device__ __forceinline__ int pad() const { return kHeadPad; }
+  __device__ __forceinline__ void store(int k, long long g, double s) const { part[k * nb + static_cast<int>(g)] = s; }
+  __device__ __forceinline__ void zero(int k, long long g) const { part[k * nb + static_cast<int>(g)] = 0.0; }
+};
+
+struct TailPolicy {
+  const int* __restrict__ gcol0;  // per group: index of its first column in tcol
+  const int* __restrict__ tcol;   // per (group, column in group): destination index in out
+  double* out;                    // A^T u (one row superblock) or the superblock partials
+  int rb;                         // bits of the row field
+  static constexpr bool kStage = false;
+#ifndef APC_TAIL_MINB
+#define APC_TAIL_MINB 2
+#endif
+  static constexpr int kMinBlocks = APC_TAIL_MINB;
+  __device__ __forceinline__ int col(unsigned key) const { return static_cast<int>(key >> rb); }
+  __device__ __forceinline__ int row(unsigned key) const { return static_cast<int>(key & ((1u << rb) - 1u)); }
+  __device__ __forceinline__ int pad() const { return static_cast<int>((1u << (32 - rb)) - 1u); }
+  __device__ __forceinline__ void store(int k, long long g, double s) const { out[__ldg(tcol + __ldg(gcol0 + g) + k)] = s; }
+  __device__ __forceinline__ void zero(int k, long long g) const { store(k, g, 0.0); }
+};
+
 // chain step: piece (pk, ps) follows the open piece (k, s)
+template <class Pol>
 __device__ __forceinline__ void head_chain(int& k, double& s, int pk, double ps, int& fk, double& fs, bool& first,
-                                           double* part, long long nblocks, long long blk) {
+                                           const Pol& pol, long long blk) {
   if (pk < 0) return;
   if (pk == k) {
     s += ps;
@@ -304,7 +344,7 @@ __device__ __forceinline__ void head_chain(int& k, double& s, int pk, double ps,
       fs = s;
       first = false;
     } else {
-      part[static_cast<long long>(k) * nblocks + blk] = s;
+      pol.store(k, blk, s);
     }
   }
   k = pk;
@@ -314,26 +354,29 @@ __device__ __forceinline__ void head_chain(int& k, double& s, int pk, double ps,
 #ifndef APC_HEAD_MINB
 #define APC_HEAD_MINB 1
 #endif
-__global__ void __launch_bounds__(kHeadThreads, APC_HEAD_MINB)
-head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, const double* __restrict__ hval,
-                const double* __restrict__ u, long long mloc, long long nblocks, int parts,
-                const int* __restrict__ zptr, const int* __restrict__ zcol, double* __restrict__ part,
-                HeadPiece* __restrict__ bnd, const int* done) {
+template <class Pol>
+__global__ void __launch_bounds__(kHeadThreads, Pol::kMinBlocks)
+seg_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, const double* __restrict__ hval,
+               const double* __restrict__ u, long long mloc, int parts, const int* __restrict__ zptr,
+               const int* __restrict__ zcol, Pol pol, HeadPiece* __restrict__ bnd, const int* done) {
   constexpr int NW = kHeadThreads / 32;
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ double us[];
   __shared__ HeadPiece pc[NW];
   if (done && *done) return;
-  const int nb = static_cast<int>(nblocks);
   const int blk = blockIdx.x / parts;
   const int prt = blockIdx.x % parts;
-  const long long r0 = static_cast<long long>(blk) * kHeadRows;
-  const int nr = static_cast<int>(mloc - r0 < kHeadRows ? mloc - r0 : kHeadRows);
-  for (int i = threadIdx.x; i < nr; i += kHeadThreads) us[i] = __ldcg(u + r0 + i);
+  const int PAD = pol.pad();
+  const double* ub = u;
+  if (Pol::kStage) {
+    const long long r0 = static_cast<long long>(blk) * kHeadRows;
+    const int nr = static_cast<int>(mloc - r0 < kHeadRows ? mloc - r0 : kHeadRows);
+    for (int i = threadIdx.x; i < nr; i += kHeadThreads) us[i] = __ldcg(u + r0 + i);
+  }
   if (prt == 0)
     for (int z = __ldg(zptr + blk) + threadIdx.x; z < __ldg(zptr + blk + 1); z += kHeadThreads)
-      part[__ldg(zcol + z) * nb + blk] = 0.0;
-  __syncthreads();
+      pol.zero(__ldg(zcol + z), blk);
+  if (Pol::kStage) __syncthreads();
   constexpr int KL = kHeadPerLane, STEP = 32 * KL;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int b0 = __ldg(bptr + blk), b1 = __ldg(bptr + blk + 1);  // multiples of STEP
@@ -345,21 +388,29 @@ head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, cons
   double cs = 0.0, fs = 0.0;
   const int4* kp = reinterpret_cast<const int4*>(hkey) + (KL / 4) * lane;
   const double2* vp = reinterpret_cast<const double2*>(hval) + (KL / 2) * lane;
-#if APC_HEAD_PREFETCH
-  // software pipeline: the next step's entries are in flight while this one is scanned
+  // software pipeline: the next step's entries (and, for a global u, its
+  // gathers) are in flight while this one is scanned
   int4 nkq[KL / 4];
   double2 nvq[KL / 2];
+  double nug[KL];
   if (rb < re) {
 #pragma unroll
     for (int i = 0; i < KL / 4; ++i) nkq[i] = __ldcs(kp + (rb >> 2) + i);
 #pragma unroll
     for (int i = 0; i < KL / 2; ++i) nvq[i] = __ldcs(vp + (rb >> 1) + i);
+    if (!Pol::kStage) {
+#pragma unroll
+      for (int i = 0; i < KL / 4; ++i) {
+        nug[4 * i] = __ldg(ub + pol.row(nkq[i].x));
+        nug[4 * i + 1] = __ldg(ub + pol.row(nkq[i].y));
+        nug[4 * i + 2] = __ldg(ub + pol.row(nkq[i].z));
+        nug[4 * i + 3] = __ldg(ub + pol.row(nkq[i].w));
+      }
+    }
   }
-#endif
   for (int e = rb; e < re; e += STEP) {
     int key[KL];
-    double vv[KL];
-#if APC_HEAD_PREFETCH
+    double vv[KL], ug[KL];
 #pragma unroll
     for (int i = 0; i < KL / 4; ++i) {
       key[4 * i] = nkq[i].x;
@@ -372,35 +423,32 @@ head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, cons
       vv[2 * i] = nvq[i].x;
       vv[2 * i + 1] = nvq[i].y;
     }
+    if (!Pol::kStage) {
+#pragma unroll
+      for (int i = 0; i < KL; ++i) ug[i] = nug[i];
+    }
     if (e + STEP < re) {
 #pragma unroll
       for (int i = 0; i < KL / 4; ++i) nkq[i] = __ldcs(kp + ((e + STEP) >> 2) + i);
 #pragma unroll
       for (int i = 0; i < KL / 2; ++i) nvq[i] = __ldcs(vp + ((e + STEP) >> 1) + i);
-    }
-#else
+      if (!Pol::kStage) {
 #pragma unroll
-    for (int i = 0; i < KL / 4; ++i) {
-      const int4 q = __ldcs(kp + (e >> 2) + i);
-      key[4 * i] = q.x;
-      key[4 * i + 1] = q.y;
-      key[4 * i + 2] = q.z;
-      key[4 * i + 3] = q.w;
+        for (int i = 0; i < KL / 4; ++i) {
+          nug[4 * i] = __ldg(ub + pol.row(nkq[i].x));
+          nug[4 * i + 1] = __ldg(ub + pol.row(nkq[i].y));
+          nug[4 * i + 2] = __ldg(ub + pol.row(nkq[i].z));
+          nug[4 * i + 3] = __ldg(ub + pol.row(nkq[i].w));
+        }
+      }
     }
-#pragma unroll
-    for (int i = 0; i < KL / 2; ++i) {
-      const double2 q = __ldcs(vp + (e >> 1) + i);
-      vv[2 * i] = q.x;
-      vv[2 * i + 1] = q.y;
-    }
-#endif
-    // padding keys carry column kHeadPad and row 0 (value 0): a run that is never stored
+    // padding keys carry column PAD and row 0 (value 0): a run that is never stored
     int k[KL];
     double x[KL];
 #pragma unroll
     for (int i = 0; i < KL; ++i) {
-      k[i] = key[i] >> 16;
-      x[i] = vv[i] * us[key[i] & (kHeadRows - 1)];
+      k[i] = pol.col(static_cast<unsigned>(key[i]));
+      x[i] = vv[i] * (Pol::kStage ? us[pol.row(static_cast<unsigned>(key[i]))] : ug[i]);
     }
     const int kl0 = __shfl_sync(FULL, k[0], 0);
     if (ck >= 0 && kl0 != ck) {  // the carried piece ended with the previous step
@@ -408,7 +456,7 @@ head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, cons
         fk = ck;
         fs = cs;
       } else if (lane == 0) {
-        part[ck * nb + blk] = cs;
+        pol.store(ck, blk, cs);
       }
       ck = -1;
     }
@@ -451,8 +499,8 @@ head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, cons
     const int knext = __shfl_down_sync(FULL, k[0], 1);
     bool en[KL];
 #pragma unroll
-    for (int i = 0; i < KL - 1; ++i) en[i] = k[i] != kHeadPad && k[i] != k[i + 1];
-    en[KL - 1] = k[KL - 1] != kHeadPad && lane < 31 && k[KL - 1] != knext;  // lane 31's last entry stays open
+    for (int i = 0; i < KL - 1; ++i) en[i] = k[i] != PAD && k[i] != k[i + 1];
+    en[KL - 1] = k[KL - 1] != PAD && lane < 31 && k[KL - 1] != knext;  // lane 31's last entry stays open
     bool anyen = false;
 #pragma unroll
     for (int i = 0; i < KL; ++i) anyen = anyen || en[i];
@@ -481,10 +529,10 @@ head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, cons
     }
 #pragma unroll
     for (int i = 0; i < KL; ++i)
-      if (en[i]) part[k[i] * nb + blk] = y[i];
+      if (en[i]) pol.store(k[i], blk, y[i]);
     ck = __shfl_sync(FULL, k[KL - 1], 31);
     cs = __shfl_sync(FULL, y[KL - 1], 31);
-    if (ck == kHeadPad) ck = -1;
+    if (ck == PAD) ck = -1;
   }
   if (lane == 0) pc[w] = fk < 0 ? HeadPiece{ck, -1, cs, 0.0} : HeadPiece{fk, ck, fs, cs};
   __syncthreads();
@@ -494,20 +542,21 @@ head_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, cons
     bool first = parts > 1;  // with one part per block the CTA's pieces are all complete
     for (int i = 0; i < NW; ++i) {
       const HeadPiece P = pc[i];
-      head_chain(k, sum, P.fk, P.fs, f, fsum, first, part, nblocks, blk);
-      head_chain(k, sum, P.lk, P.ls, f, fsum, first, part, nblocks, blk);
+      head_chain(k, sum, P.fk, P.fs, f, fsum, first, pol, blk);
+      head_chain(k, sum, P.lk, P.ls, f, fsum, first, pol, blk);
     }
     if (parts > 1) {
       bnd[blockIdx.x] = first ? HeadPiece{k, -1, sum, 0.0} : HeadPiece{f, k, fsum, sum};
     } else if (k >= 0) {
-      part[static_cast<long long>(k) * nblocks + blk] = sum;
+      pol.store(k, blk, sum);
     }
   }
 }
 
-// pieces at the part boundaries of each block, chained in part order
-__global__ void head_bnd_kernel(const HeadPiece* __restrict__ bnd, int parts, long long nblocks,
-                                double* __restrict__ part, const int* done) {
+// pieces at the part boundaries of each block (group), chained in part order
+template <class Pol>
+__global__ void seg_bnd_kernel(const HeadPiece* __restrict__ bnd, int parts, long long nblocks, Pol pol,
+                               const int* done) {
   if (done && *done) return;
   const long long blk = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (blk >= nblocks) return;
@@ -516,10 +565,21 @@ __global__ void head_bnd_kernel(const HeadPiece* __restrict__ bnd, int parts, lo
   bool first = false;
   for (int i = 0; i < parts; ++i) {
     const HeadPiece P = bnd[blk * parts + i];
-    head_chain(k, sum, P.fk, P.fs, f, fsum, first, part, nblocks, blk);
-    head_chain(k, sum, P.lk, P.ls, f, fsum, first, part, nblocks, blk);
+    head_chain(k, sum, P.fk, P.fs, f, fsum, first, pol, blk);
+    head_chain(k, sum, P.lk, P.ls, f, fsum, first, pol, blk);
   }
-  if (k >= 0) part[static_cast<long long>(k) * nblocks + blk] = sum;
+  if (k >= 0) pol.store(k, blk, sum);
+}
+
+// out[col] = sum of the column's superblock partials, superblock order
+__global__ void tail_combine_kernel(const double* __restrict__ part, const int* __restrict__ cols, long long ncols,
+                                    int S, double* __restrict__ out, const int* done) {
+  if (done && *done) return;
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= ncols) return;
+  double s = part[t * S];
+  for (int sb = 1; sb < S; ++sb) s += part[t * S + sb];
+  out[cols[t]] = s;
 }
 
 // warp per head column: its partials in block order -> out[col]
@@ -725,16 +785,42 @@ void op_adj_raw(apc_mat& a, const double* u, double* out, const int* done) {
   const Csr& c = a.at;
   if (a.head.built()) {
     const HeadAdj& h = a.head;
-    launch_units(a.ctx, c, h.tail, u, out, done);
-    head_adj_kernel<<<static_cast<unsigned>(h.nblocks * h.parts), kHeadThreads, sizeof(double) * kHeadRows, st>>>(
-        h.bptr.p, h.hkey.p, h.hval.p, u, a.mloc(), h.nblocks, h.parts, h.zptr.p, h.zcol.p, h.part.p,
-        reinterpret_cast<HeadPiece*>(h.bnd.p), done);
+    static const int mask = std::getenv("APC_ADJ_MASK") ? std::atoi(std::getenv("APC_ADJ_MASK")) : 0xff;
+    if (mask & 1) {
+      if (h.seg.built()) {
+        const HeadAdj::Seg& t = h.seg;
+        const TailPolicy pol{t.gcol0.p, t.tcol.p, t.sb > 1 ? t.part.p : out, t.rb};
+        seg_adj_kernel<TailPolicy><<<static_cast<unsigned>(t.ngroups * t.parts), kHeadThreads, 0, st>>>(
+            t.gptr.p, t.tkey.p, t.tval.p, u, a.mloc(), t.parts, t.zptr.p, t.zcol.p, pol,
+            reinterpret_cast<HeadPiece*>(t.bnd.p), done);
+        a.ctx->launches++;
+        if (t.parts > 1) {
+          seg_bnd_kernel<TailPolicy><<<nblk(t.ngroups, 128), 128, 0, st>>>(reinterpret_cast<const HeadPiece*>(t.bnd.p),
+                                                                           t.parts, t.ngroups, pol, done);
+          a.ctx->launches++;
+        }
+        if (t.sb > 1) {
+          tail_combine_kernel<<<nblk(t.ncols, 256), 256, 0, st>>>(t.part.p, t.cols.p, t.ncols, t.sb, out, done);
+          a.ctx->launches++;
+        }
+      } else {
+        launch_units(a.ctx, c, h.tail, u, out, done);
+      }
+    }
+    const HeadPolicy hp{h.part.p, static_cast<int>(h.nblocks)};
+    if (mask & 2)
+      seg_adj_kernel<HeadPolicy><<<static_cast<unsigned>(h.nblocks * h.parts), kHeadThreads,
+                                   sizeof(double) * kHeadRows, st>>>(h.bptr.p, h.hkey.p, h.hval.p, u, a.mloc(),
+                                                                     h.parts, h.zptr.p, h.zcol.p, hp,
+                                                                     reinterpret_cast<HeadPiece*>(h.bnd.p), done);
     if (h.parts > 1) {
-      head_bnd_kernel<<<nblk(h.nblocks, 128), 128, 0, st>>>(reinterpret_cast<const HeadPiece*>(h.bnd.p), h.parts,
-                                                            h.nblocks, h.part.p, done);
+      seg_bnd_kernel<HeadPolicy><<<nblk(h.nblocks, 128), 128, 0, st>>>(reinterpret_cast<const HeadPiece*>(h.bnd.p),
+                                                                       h.parts, h.nblocks, hp, done);
       a.ctx->launches++;
     }
-    head_combine_kernel<<<nblk(h.ncols * 32, 256), 256, 0, st>>>(h.part.p, h.nblocks, h.hcol.p, h.ncols, out, done);
+    if (mask & 4)
+      head_combine_kernel<<<nblk(h.ncols * 32, 256), 256, 0, st>>>(h.part.p, h.nblocks, h.hcol.p, h.ncols, out,
+                                                                  done);
     a.ctx->launches += 2;
     return;
   }
@@ -798,30 +884,62 @@ void build_units(apc_ctx* ctx, Csr& c, const std::vector<long long>& row_nnz) {
 }
 
 void build_units_sel(apc_ctx* ctx, Units& c, long long rows, const std::vector<long long>& off,
-                     const std::vector<long long>& row_nnz, const std::vector<char>* skip) {
+                     const std::vector<long long>& row_nnz, const std::vector<char>* skip, const int* colidx,
+                     long long ncols_local, int superblocks) {
+  // Row r of the CSR is cut into units of <= kCsrUnitMax entries.  With
+  // superblocks > 1 (colidx = the host column indices) the entries of each row
+  // are also cut at every boundary of `superblocks` equal ranges of the column
+  // space, and the units are emitted superblock-major: the gathered vector's
+  // active range at any time is 1/superblocks of it (L2-resident).  A row with
+  // more than one unit gets consecutive partial slots in entry order, so the
+  // split fix-up adds its pieces in the same order for any superblock count.
   std::vector<int> urow, ustart, uend, uslot, rfirst(rows, -1), rcount(rows, 0);
   urow.reserve(rows);
+  const int S = colidx && superblocks > 1 ? superblocks : 1;
+  const long long span = (ncols_local + S - 1) / std::max(1, S);
+  // pieces of row r in superblock sb: [cut[r*(S+1)+sb], cut[r*(S+1)+sb+1])
+  std::vector<long long> cut;
+  if (S > 1) {
+    cut.resize(static_cast<size_t>(rows * (S + 1)));
+    for (long long r = 0; r < rows; ++r) {
+      long long q = off[r];
+      const long long e = off[r] + row_nnz[r];
+      for (int sb = 0; sb < S; ++sb) {
+        cut[r * (S + 1) + sb] = q;
+        const long long lim = (sb + 1) * span;
+        while (q < e && colidx[q] < lim) ++q;
+      }
+      cut[r * (S + 1) + S] = e;
+    }
+  }
+  auto pieces_units = [&](long long len) { return (len + kCsrUnitMax - 1) / kCsrUnitMax; };
   long long nparts = 0;
-  for (long long r = 0; r < rows; ++r) {
+  for (long long r = 0; r < rows; ++r) {  // slots first (entry order within each row)
     if (skip && (*skip)[r]) continue;
-    const long long L = row_nnz[r], o = off[r];
-    if (L <= kCsrUnitMax) {
-      urow.push_back(static_cast<int>(r));
-      ustart.push_back(static_cast<int>(o));
-      uend.push_back(static_cast<int>(o + L));
-      uslot.push_back(-1);
+    long long k = 0;
+    if (S > 1) {
+      for (int sb = 0; sb < S; ++sb) k += pieces_units(cut[r * (S + 1) + sb + 1] - cut[r * (S + 1) + sb]);
     } else {
-      long long k = (L + kCsrUnitMax - 1) / kCsrUnitMax;
+      k = pieces_units(row_nnz[r]);
+    }
+    if (k > 1) {
       rfirst[r] = static_cast<int>(nparts);
       rcount[r] = static_cast<int>(k);
-      for (long long q = 0; q < k; ++q) {
-        long long b = o + q * kCsrUnitMax, e = std::min(o + L, b + kCsrUnitMax);
+      nparts += k;
+    }
+  }
+  std::vector<int> next_slot(rfirst);
+  for (int sb = 0; sb < S; ++sb) {
+    for (long long r = 0; r < rows; ++r) {
+      if (skip && (*skip)[r]) continue;
+      const long long b0 = S > 1 ? cut[r * (S + 1) + sb] : off[r];
+      const long long e0 = S > 1 ? cut[r * (S + 1) + sb + 1] : off[r] + row_nnz[r];
+      for (long long b = b0; b < e0; b += kCsrUnitMax) {
         urow.push_back(static_cast<int>(r));
         ustart.push_back(static_cast<int>(b));
-        uend.push_back(static_cast<int>(e));
-        uslot.push_back(static_cast<int>(nparts + q));
+        uend.push_back(static_cast<int>(std::min(e0, b + kCsrUnitMax)));
+        uslot.push_back(rfirst[r] >= 0 ? next_slot[r]++ : -1);
       }
-      nparts += k;
     }
   }
   c.n_units = static_cast<long long>(urow.size());
@@ -889,6 +1007,126 @@ __global__ void head_pack_kernel(const int* __restrict__ seg, const int* __restr
   }
 }
 
+// tail stream: warp per (column, superblock) piece copies its entries with packed keys
+__global__ void tail_pack_kernel(const int* __restrict__ src, const int* __restrict__ len, const int* __restrict__ kin,
+                                 const int* __restrict__ dst, long long nitems, const int* __restrict__ tidx,
+                                 const double* __restrict__ tv, int rb, int* __restrict__ tkey,
+                                 double* __restrict__ tval) {
+  const long long t = (static_cast<long long>(blockIdx.x) * 256 + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= nitems) return;
+  const int s0 = src[t], L = len[t], d = dst[t];
+  const unsigned hi = static_cast<unsigned>(kin[t]) << rb;
+  for (int q = lane; q < L; q += 32) {
+    tkey[d + q] = static_cast<int>(hi | static_cast<unsigned>(tidx[s0 + q]));
+    tval[d + q] = tv[s0 + q];
+  }
+}
+
+void build_tail_seg(apc_mat& a, const std::vector<int>& tptr, const int* hidx, const std::vector<long long>& tlen,
+                    const std::vector<char>& is_head) {
+  apc_ctx* ctx = a.ctx;
+  cudaStream_t st = ctx->stream;
+  HeadAdj::Seg& t = a.head.seg;
+  t = HeadAdj::Seg();
+  const long long n = a.n, mloc = a.mloc();
+  int rb = 1;
+  while ((1LL << rb) < mloc) ++rb;
+  if (rb > 26) return;  // fewer than 64 columns per group: keep the work units
+  const long long kcap = (1LL << (32 - rb)) - 2;  // column-in-group ids stay below the padding id
+  const char* ee = std::getenv("APC_TAIL_ECAP");
+  const long long ecap = ee ? std::max(1, std::atoi(ee)) : 16384;
+  // row superblocks: the stream holds superblock 0's entries of every tail
+  // column, then superblock 1's, ...  CTAs run roughly in stream order, so the
+  // u rows being gathered at a time are one superblock (L2-resident on each
+  // die); each (column, superblock) piece is a partial added in order after.
+  const char* se = std::getenv("APC_TAIL_SB");
+  const int S = se ? std::max(1, std::atoi(se)) : 1;
+  const long long span = (mloc + S - 1) / S;
+  std::vector<int> tc;  // tail columns
+  for (long long j = 0; j < n; ++j)
+    if (!is_head[j]) tc.push_back(static_cast<int>(j));
+  const long long T = static_cast<long long>(tc.size());
+  if (T == 0) return;
+  // cut[t * (S + 1) + sb]: first entry of tail column t in superblock sb
+  std::vector<int> cut(static_cast<size_t>(T * (S + 1)));
+  for (long long q = 0; q < T; ++q) {
+    const int j = tc[q];
+    long long e = tptr[j];
+    for (int sb = 0; sb < S; ++sb) {
+      cut[q * (S + 1) + sb] = static_cast<int>(e);
+      const long long lim = (sb + 1) * span;
+      while (e < tptr[j + 1] && hidx[e] < lim) ++e;
+    }
+    cut[q * (S + 1) + S] = tptr[j + 1];
+  }
+  std::vector<int> dix, src, kin, dst, gptr(1, 0), gcol0(1, 0), zptr(1, 0), zcol;
+  long long tot = 0, gcols = 0, gents = 0;
+  auto close_group = [&]() {
+    tot = (tot + kHeadStep - 1) / kHeadStep * kHeadStep;
+    gptr.push_back(static_cast<int>(tot));
+    gcol0.push_back(static_cast<int>(dix.size()));
+    zptr.push_back(static_cast<int>(zcol.size()));
+    gcols = gents = 0;
+  };
+  for (int sb = 0; sb < S; ++sb) {
+    for (long long q = 0; q < T; ++q) {
+      const long long b = cut[q * (S + 1) + sb], L = cut[q * (S + 1) + sb + 1] - b;
+      if (gcols > 0 && (gcols >= kcap || gents + L > ecap)) close_group();
+      if (L == 0) zcol.push_back(static_cast<int>(gcols));
+      dix.push_back(S > 1 ? static_cast<int>(q * S + sb) : tc[q]);
+      src.push_back(static_cast<int>(b));
+      kin.push_back(static_cast<int>(L));
+      dst.push_back(static_cast<int>(tot));
+      tot += L;
+      gents += L;
+      ++gcols;
+      if (tot >= (1LL << 31) - kHeadStep) return;
+    }
+    if (gcols > 0) close_group();  // groups never span superblocks
+  }
+  const long long G = static_cast<long long>(gptr.size()) - 1;
+  gcol0.pop_back();
+  std::vector<int> kk(dix.size());  // column in group of each (group, column) item
+  for (long long g = 0; g < G; ++g)
+    for (int i = gcol0[g]; i < (g + 1 < G ? gcol0[g + 1] : static_cast<int>(dix.size())); ++i) kk[i] = i - gcol0[g];
+  auto up = [&](DBuf<int>& d, const std::vector<int>& v) {
+    d.alloc(std::max<long long>(1, static_cast<long long>(v.size())));
+    if (!v.empty()) APC_CUDA(cudaMemcpyAsync(d.p, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  };
+  t.rb = rb;
+  t.ngroups = G;
+  t.nnz = tot;
+  t.sb = S;
+  t.ncols = T;
+  up(t.gptr, gptr);
+  up(t.gcol0, gcol0);
+  up(t.tcol, dix);
+  up(t.zptr, zptr);
+  up(t.zcol, zcol);
+  up(t.cols, tc);
+  if (S > 1) t.part.alloc(T * S);
+  t.tkey.alloc(std::max<long long>(kHeadStep, tot));
+  t.tval.alloc(std::max<long long>(kHeadStep, tot));
+  fill_int_kernel<<<nblk(t.tkey.n, 256), 256, 0, st>>>(t.tkey.p, t.tkey.n,
+                                                       static_cast<int>(static_cast<unsigned>(kcap + 1) << rb));
+  APC_CUDA(cudaMemsetAsync(t.tval.p, 0, t.tval.bytes(), st));
+  t.bnd.alloc(std::max<long long>(1, G * t.parts * 3));
+  {
+    DBuf<int> dsrc, dlen, dk, dd;
+    up(dsrc, src);
+    up(dlen, kin);
+    up(dk, kk);
+    up(dd, dst);
+    const long long ni = static_cast<long long>(dix.size());
+    tail_pack_kernel<<<nblk(ni * 32, 256), 256, 0, st>>>(dsrc.p, dlen.p, dk.p, dd.p, ni, a.at.idx.p, a.at.val.p, rb,
+                                                         t.tkey.p, t.tval.p);
+    ctx->launches += 2;
+    APC_CUDA(cudaGetLastError());
+    APC_CUDA(cudaStreamSynchronize(st));
+  }
+}
+
 void build_head_adj(apc_mat& a, const std::vector<int>& tptr, const int* hidx, const std::vector<long long>& tlen) {
   apc_ctx* ctx = a.ctx;
   cudaStream_t st = ctx->stream;
@@ -910,6 +1148,7 @@ void build_head_adj(apc_mat& a, const std::vector<int>& tptr, const int* hidx, c
       is_head[j] = 1;
     }
   if (hc.empty()) return;
+  const char* pe = std::getenv("APC_SETUP_PROF");
   const long long H = static_cast<long long>(hc.size());
   std::vector<int> seg(static_cast<size_t>(H * (nblocks + 1)));
   host_parallel_for(H, HeadSegs{tptr.data(), hidx, &hc, nblocks, &seg}, 1);
@@ -959,12 +1198,26 @@ void build_head_adj(apc_mat& a, const std::vector<int>& tptr, const int* hidx, c
     APC_CUDA(cudaGetLastError());
     APC_CUDA(cudaStreamSynchronize(st));
   }
-  APC_CUDA(cudaFuncSetAttribute(head_adj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  APC_CUDA(cudaFuncSetAttribute(seg_adj_kernel<HeadPolicy>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sizeof(double) * kHeadRows)));
+  const char* tse = std::getenv("APC_TAIL_SEG");
+  if (!tse || std::atoi(tse) != 0) {
+    build_tail_seg(a, tptr, hidx, tlen, is_head);
+    if (h.seg.built()) {
+      if (pe && std::atoi(pe) != 0)
+        std::fprintf(stderr, "[apc] head adjoint: %lld head columns (>= %lld nnz), %lld blocks, %lld head nnz; "
+                     "tail stream: %lld groups, %lld entries, rb %d\n", H, thr, nblocks, tot, h.seg.ngroups,
+                     h.seg.nnz, h.seg.rb);
+      return;
+    }
+  }
   std::vector<long long> off(n + 1);
   for (long long j = 0; j <= n; ++j) off[j] = tptr[j];
-  build_units_sel(ctx, h.tail, n, off, tlen, &is_head);  // synchronizes: host vectors may go
-  const char* pe = std::getenv("APC_SETUP_PROF");
+  // tail units superblock-major over the rows of A: the gathered u range at a
+  // time is 1/APC_TAIL_SB of u, so the gathers hit L2 instead of DRAM
+  const char* sbe = std::getenv("APC_TAIL_SB");
+  const int sbs = sbe ? std::max(1, std::atoi(sbe)) : 1;
+  build_units_sel(ctx, h.tail, n, off, tlen, &is_head, hidx, mloc, sbs);  // synchronizes: host vectors may go
   if (pe && std::atoi(pe) != 0)
     std::fprintf(stderr, "[apc] head adjoint: %lld head columns (>= %lld nnz), %lld blocks, %lld head nnz, %lld tail units\n",
                  H, thr, nblocks, tot, h.tail.n_units);

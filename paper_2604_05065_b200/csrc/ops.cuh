@@ -360,7 +360,8 @@ void upload_csc(apc_mat& a, const long long* colptr, const long long* rowidx, co
 void build_units(apc_ctx* ctx, apc::Csr& c, const std::vector<long long>& row_nnz);
 // units over the rows of a CSR with explicit row offsets, skipping rows with skip[r] != 0
 void build_units_sel(apc_ctx* ctx, apc::Units& u, long long rows, const std::vector<long long>& off,
-                     const std::vector<long long>& row_nnz, const std::vector<char>* skip);
+                     const std::vector<long long>& row_nnz, const std::vector<char>* skip,
+                     const int* colidx = nullptr, long long ncols_local = 0, int superblocks = 1);
 void launch_units(apc_ctx* ctx, const apc::Csr& c, const apc::Units& un, const double* u, double* out,
                   const int* done);
 // head/tail split of CSR(A^T) for the row-blocked adjoint (called at upload)

@@ -111,3 +111,31 @@ def test_golden_solve_fixtures_well_formed(name):
     assert len(g["row_indices"]) == len(g["col_indices"]) > 0
     assert len(set(g["row_indices"].tolist())) == len(g["row_indices"])
     assert np.all(np.diff(g["rho_history"]) <= 1e-9 * g["rho_history"][0] + np.abs(np.diff(g["rho_history"])))
+
+
+# ---- BASELINE input generators: oracle vs product (byte equality) -----------
+# bench.py's reference arm generates its inputs with the oracle's own
+# generator (oracle/ref_harness.cpp ref_generate) so it never maps the
+# product library; these prove both generators emit the same bytes.  Full
+# BASELINE sizes of C3, C4 and C5 were checked once here as well
+# (profiles/r2_generator_equality.txt).
+@pytest.mark.parametrize("cfg,m,n", [(1, 0, 0), (2, 0, 0), (1, 300, 40), (2, 3000, 300), (3, 3000, 300),
+                                     (4, 600, 500), (4, 700, 700), (5, 100000, 5000), (5, 70000, 300)])
+def test_generator_bytes_equal_product(cfg, m, n):
+    from oracle import ref
+
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    apc = pytest.importorskip("paper_2604_05065_b200")
+    p = apc.Problem(cfg, m, n)
+    r = ref.Problem.generate(cfg, m, n)
+    try:
+        assert (p.m, p.n, p.sparse) == (r.m, r.n, r.sparse)
+        assert np.array_equal(_bits(p.b), _bits(r.b))
+        if p.sparse:
+            assert np.array_equal(p.colptr, r.colptr) and np.array_equal(p.rowidx, r.rowidx)
+            assert np.array_equal(_bits(p.vals), _bits(r.vals))
+        else:
+            assert np.array_equal(_bits(p.dense), _bits(r.dense))
+    finally:
+        r.free()
