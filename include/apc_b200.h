@@ -51,6 +51,15 @@ const char* apc_last_error(int64_t* index);
 int apc_device_count(int* count);
 /* nccl_unique_id: 128 bytes from apc_nccl_unique_id() on rank 0 (NULL if nranks==1) */
 int apc_ctx_create(int device, int nranks, int rank, const void* nccl_unique_id, apc_ctx** out);
+/* Host-staged collectives instead of NCCL: every allreduce of the row-sharded
+ * solve copies the device buffer to pinned host memory and calls
+ * fn(buf, count, user), which must replace buf by the elementwise sum over all
+ * ranks, added in rank order (so every rank holds the same bits), and return 0.
+ * Lets several ranks share one GPU or use any host transport; the LSQR phase
+ * then runs eagerly (one host round trip per iteration). */
+typedef int (*apc_host_allreduce_fn)(double* buf, int64_t count, void* user);
+int apc_ctx_create_host_comm(int device, int nranks, int rank, apc_host_allreduce_fn fn, void* user,
+                             apc_ctx** out);
 int apc_ctx_destroy(apc_ctx* ctx);
 int apc_nccl_unique_id(void* out128);
 void* apc_ctx_stream(apc_ctx* ctx);              /* cudaStream_t all library work runs on */
@@ -83,6 +92,17 @@ int apc_op_apply_dev(apc_mat* a, double mu, int augmented, int transpose, const 
 int apc_op_apply_host(apc_mat* a, double mu, int augmented, int transpose, const double* x,
                       double* y);
 
+/* The dense kernels of the preconditioner construction, on device pointers
+ * (column-major; hand-written DMMA GEMM with a fixed-order split over k, and
+ * a blocked TRSM): C = alpha op(A) op(B) + beta C, and B <- B T^{-1} (T upper).
+ * They replace the QrAccumulator / basis products of preconditioner.hpp:435-476,
+ * 171-193 (the reference's own loops there are plain matmul / tri-solves). */
+int apc_dgemm(apc_ctx* ctx, int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha,
+              const double* A_dev, int64_t lda, const double* B_dev, int64_t ldb, double beta, double* C_dev,
+              int64_t ldc);
+int apc_dtrsm_right_upper(apc_ctx* ctx, int64_t m, int64_t n, const double* T_dev, int64_t ldt, double* B_dev,
+                          int64_t ldb);
+
 /* ---- row partitioning for multi-GPU -------------------- */
 /* bounds[0..nranks]: contiguous row blocks balanced by nnz when row_nnz is
  * given (prefix-sum split), else by row count. Host-only. */
@@ -102,7 +122,9 @@ int apc_rng_fill_device(apc_ctx* ctx, uint64_t seed, int stream, uint64_t index,
 /* ---- single-sketch incremental CUR (CurState, cur.hpp:200-371) ----------
  * Exact-order device kernels: Y, E^row, the LUPP pivot order and rho are
  * bit-identical to the reference.  sketch_kind 0 = SparseSignEmbedding
- * (CurState::init, cur.hpp:209-226), 1 = GaussianEmbedding (sketch.hpp:173-197). */
+ * (CurState::init, cur.hpp:209-226), 1 = GaussianEmbedding (sketch.hpp:173-197),
+ * 2 = GaussianEmbedding applied on the FP64 tensor cores (DMMA, opt-in: Y is not
+ * bit-identical, the indices are checked against the exact path in the tests). */
 typedef struct apc_cur apc_cur;
 int apc_cur_create(apc_mat* a, int64_t block, uint64_t seed, int64_t xi, int64_t probe_count,
                    int core_kind, int sketch_kind, apc_cur** out);
@@ -157,7 +179,8 @@ typedef struct apc_solver_config {
   uint64_t seed;               /* 0 */
   int64_t trace_sample_stride; /* 1; true-residual sample every k-th iteration, 0 off (bench: 0) */
   int64_t outer_cap;           /* 100000 */
-  int32_t sketch_kind;         /* 0 sparse sign (reference), 1 Gaussian (BASELINE C1/C3/C4) */
+  int32_t sketch_kind;         /* 0 sparse sign (reference), 1 Gaussian (BASELINE C1/C3/C4),
+                                  2 Gaussian on the FP64 tensor cores (DMMA; opt-in, Y not bit-exact) */
   int32_t reserved;
 } apc_solver_config;
 

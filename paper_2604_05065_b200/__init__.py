@@ -24,6 +24,7 @@ from typing import Optional
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
+_HOST_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int64, C.c_void_p)
 LIB_PATH = _PKG / "_lib" / "libapc_b200.so"
 HEADER_PATHS = [_PKG.parent / "include" / "apc_b200.h"]
 
@@ -79,7 +80,8 @@ class CoreFactorKind(enum.IntEnum):  # cur.hpp:50
 
 class SketchKind(enum.IntEnum):
     sparse_sign = 0
-    gaussian = 1
+    gaussian = 1          # exact order: Y bit-identical to GaussianEmbedding::apply
+    gaussian_dmma = 2     # opt-in FP64 tensor-core (DMMA) sketch: Y rounded differently
 
 
 class _Config(C.Structure):
@@ -147,6 +149,7 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
         "apc_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, C.POINTER(vp)]),
         "apc_ctx_destroy": (C.c_int, [vp]),
         "apc_nccl_unique_id": (C.c_int, [vp]),
+        "apc_ctx_create_host_comm": (C.c_int, [C.c_int, C.c_int, C.c_int, _HOST_ALLREDUCE, vp, C.POINTER(vp)]),
         "apc_ctx_stream": (vp, [vp]),
         "apc_ctx_launches": (_u64, [vp]),
         "apc_ctx_sync": (C.c_int, [vp]),
@@ -155,6 +158,9 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
         "apc_mat_free": (C.c_int, [vp]),
         "apc_mat_info": (C.c_int, [vp, _i64p, _i64p, _i64p, C.POINTER(C.c_int), _i64p, _i64p]),
         "apc_op_apply_dev": (C.c_int, [vp, C.c_double, C.c_int, C.c_int, vp, vp]),
+        "apc_dgemm": (C.c_int, [vp, C.c_int, C.c_int, _i64, _i64, _i64, C.c_double, vp, _i64, vp, _i64, C.c_double,
+                                vp, _i64]),
+        "apc_dtrsm_right_upper": (C.c_int, [vp, _i64, _i64, vp, _i64, vp, _i64]),
         "apc_op_apply_host": (C.c_int, [vp, C.c_double, C.c_int, C.c_int, _dp, _dp]),
         "apc_partition_rows": (C.c_int, [_i64, _i64p, C.c_int, _i64p]),
         "apc_rng_fill": (C.c_int, [_u64, C.c_int, _u64, C.c_int, _u64, _i64, vp]),
@@ -233,14 +239,27 @@ def device_count() -> int:
 # context / matrices
 # ---------------------------------------------------------------------------
 class Context:
-    """One GPU (rank) worth of stream, scratch and NCCL communicator."""
+    """One GPU (rank) worth of stream, scratch and communicator: NCCL (nccl_uid
+    from rank 0), or host-staged collectives through ``host_allreduce(buf)``, a
+    callable that replaces the float64 numpy array ``buf`` in place by its sum
+    over the ranks, added in rank order (apc_ctx_create_host_comm)."""
 
     def __init__(self, device: int = 0, nranks: int = 1, rank: int = 0,
-                 nccl_uid: Optional[bytes] = None):
+                 nccl_uid: Optional[bytes] = None, host_allreduce=None):
         lib = load_library()
         h = C.c_void_p()
-        uid = C.create_string_buffer(nccl_uid, 128) if nccl_uid else None
-        _check(lib.apc_ctx_create(device, nranks, rank, uid, C.byref(h)))
+        if host_allreduce is not None:
+            def _cb(buf, count, _user):
+                try:
+                    host_allreduce(np.ctypeslib.as_array(buf, shape=(count,)))
+                    return 0
+                except Exception:  # reported as a comm error by the library
+                    return 1
+            self._host_cb = _HOST_ALLREDUCE(_cb)  # kept alive with the ctx
+            _check(lib.apc_ctx_create_host_comm(device, nranks, rank, self._host_cb, None, C.byref(h)))
+        else:
+            uid = C.create_string_buffer(nccl_uid, 128) if nccl_uid else None
+            _check(lib.apc_ctx_create(device, nranks, rank, uid, C.byref(h)))
         self.h = h
         self.device, self.nranks, self.rank = device, nranks, rank
         self._children = weakref.WeakSet()  # device objects freed before the ctx

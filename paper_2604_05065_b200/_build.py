@@ -1,9 +1,13 @@
 """In-tree build of libapc_b200.so (sm_100a) -- no JIT cache, the .so travels
 with the repo snapshot to the GPU box.
 
-Every CUDA translation unit is compiled with ``-fmad=false`` and host code
-with ``-ffp-contract=off``: the CUR index path must round exactly like the
-reference's SSE2 build (/root/reference/proj/CMakeLists.txt:3-11).
+The CUDA translation units on the CUR index path (cur.cu: sketch, E^row,
+E^col, LUPP, core factor and solves, rho probes; rng_dev.cu) are compiled with
+``-fmad=false`` and all host code with ``-ffp-contract=off``: the indices must
+round exactly like the reference's SSE2 build
+(/root/reference/proj/CMakeLists.txt:3-11).  The LSQR, operator,
+preconditioner and residual kernels do not decide indices and
+keep FMA contraction.
 """
 from __future__ import annotations
 
@@ -25,9 +29,10 @@ LIB = OUT_DIR / "libapc_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_FLAGS = ARCH + [
-    "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--expt-relaxed-constexpr",
+    "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v",
 ]
+EXACT_CU = {"cur.cu", "rng_dev.cu"}  # the index path: no FMA contraction
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-unused-function"]
 
 
@@ -47,12 +52,13 @@ def _run(cmd: list[str]) -> str:
 
 def _compile(src: Path) -> tuple[Path, str]:
     obj = OBJ_DIR / (src.name + ".o")
-    deps = [src] + list(CSRC.glob("*.hpp")) + list(CSRC.glob("*.cuh")) + list(INC.glob("*.h"))
+    deps = [src, Path(__file__)] + list(CSRC.glob("*.hpp")) + list(CSRC.glob("*.cuh")) + list(INC.glob("*.h"))
     if obj.exists() and obj.stat().st_mtime >= max(d.stat().st_mtime for d in deps):
         return obj, ""
     inc = [f"-I{INC}", f"-I{CSRC}"]
     if src.suffix == ".cu":
-        cmd = [NVCC, *CU_FLAGS, *inc, "-c", str(src), "-o", str(obj)]
+        exact = ["-fmad=false"] if src.name in EXACT_CU else []
+        cmd = [NVCC, *CU_FLAGS, *exact, *inc, "-c", str(src), "-o", str(obj)]
     else:
         cmd = ["g++", *CXX_FLAGS, *inc, "-I/usr/local/cuda/include", "-c", str(src), "-o", str(obj)]
     return obj, _run(cmd)
@@ -73,7 +79,7 @@ def build(verbose: bool = False) -> Path:
     if not LIB.exists() or LIB.stat().st_mtime < newest:
         tmp = LIB.with_suffix(".so.tmp")
         _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, *_nccl_link_args(), "-L/usr/local/cuda/lib64",
-              "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-lpthread"])
+              "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-lpthread"])
         shutil.move(str(tmp), str(LIB))
     return LIB
 

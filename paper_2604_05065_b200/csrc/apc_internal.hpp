@@ -180,6 +180,7 @@ struct HotSell {
   Sell s;
   i64 n = 0;
   DBuf<i32> hot;    // n: relabelled -> original column
+  DBuf<i32> inv;    // n: original -> relabelled column
   DBuf<double> xr;  // n: x in relabelled order (scratch of each product)
   bool built() const { return s.chunks > 0; }
 };
@@ -193,7 +194,11 @@ struct apc_ctx {
   int device = 0;
   int nranks = 1, rank = 0;
   cudaStream_t stream = nullptr;
-  void* nccl = nullptr;  // ncclComm_t when nranks > 1
+  void* nccl = nullptr;  // ncclComm_t when nranks > 1 (NCCL backend)
+  // host-staged backend (apc_ctx_create_host_comm): the caller's in-place sum
+  // of a host buffer over the ranks, in rank order
+  int (*host_allreduce)(double* buf, int64_t count, void* user) = nullptr;
+  void* host_user = nullptr;
   void* blas = nullptr;  // cublasHandle_t (created lazily, bound to `stream`)
   std::string err;
   apc::i64 err_index = -1;
@@ -209,7 +214,7 @@ struct apc_ctx {
   struct Pinned {
     void* p = nullptr;
     size_t n = 0;
-  } pinned[4];
+  } pinned[5];  // 3: host-staged collectives
 };
 
 // pinned host buffer `slot` of at least `bytes` (contents not preserved on growth)

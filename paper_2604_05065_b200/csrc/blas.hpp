@@ -1,6 +1,7 @@
-// cuBLAS wrappers for the per-rebuild preconditioner construction (plain
-// library GEMM / SYRK / TRSM on tall-skinny blocks; never on the per-iteration
-// path and never on the index-selecting path).  Column-major throughout.
+// Dense kernels of the per-rebuild preconditioner construction (blas.cu:
+// hand-written DMMA GEMM / SYRK / blocked TRSM on tall-skinny blocks; never on
+// the per-iteration path and never on the index-selecting path).
+// Column-major throughout.
 #pragma once
 
 #include "apc_internal.hpp"

@@ -169,6 +169,34 @@ int apc_ctx_create(int device, int nranks, int rank, const void* uid, apc_ctx** 
   });
 }
 
+int apc_ctx_create_host_comm(int device, int nranks, int rank, apc_host_allreduce_fn fn, void* user,
+                             apc_ctx** out) {
+  *out = nullptr;
+  return guard(nullptr, [&] {
+    need_device();
+    require(nranks >= 1 && rank >= 0 && rank < nranks, APC_INVALID_ARGUMENT, "apc_ctx_create: bad rank");
+    require(fn != nullptr || nranks == 1, APC_INVALID_ARGUMENT, "apc_ctx_create_host_comm: callback required");
+    APC_CUDA(cudaSetDevice(device));
+    auto* c = new apc_ctx();
+    c->device = device;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->host_allreduce = fn;
+    c->host_user = user;
+    try {
+      APC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      cudaDeviceProp prop{};
+      APC_CUDA(cudaGetDeviceProperties(&prop, device));
+      c->num_sms = prop.multiProcessorCount;
+    } catch (...) {
+      if (c->stream) cudaStreamDestroy(c->stream);
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
 int apc_ctx_destroy(apc_ctx* ctx) {
   if (!ctx) return APC_OK;
   return guard(nullptr, [&] {
@@ -278,6 +306,23 @@ int apc_mat_info(const apc_mat* a, int64_t* m, int64_t* n, int64_t* nnz, int* sp
   if (r0) *r0 = a->r0;
   if (r1) *r1 = a->r1;
   return APC_OK;
+}
+
+int apc_dgemm(apc_ctx* ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+              int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+  return guard(ctx, [&] {
+    require(m >= 0 && n >= 0 && k >= 0, APC_INVALID_ARGUMENT, "apc_dgemm: negative shape");
+    dgemm(ctx, ta != 0, tb != 0, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+    APC_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int apc_dtrsm_right_upper(apc_ctx* ctx, int64_t m, int64_t n, const double* T, int64_t ldt, double* B, int64_t ldb) {
+  return guard(ctx, [&] {
+    require(m >= 0 && n >= 0, APC_INVALID_ARGUMENT, "apc_dtrsm_right_upper: negative shape");
+    dtrsm_right_upper(ctx, m, n, T, ldt, B, ldb);
+    APC_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
 }
 
 int apc_op_apply_dev(apc_mat* a, double mu, int augmented, int transpose, const double* x, double* y) {

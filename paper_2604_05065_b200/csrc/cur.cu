@@ -5,6 +5,7 @@
 // rounded separately, -fmad=false, sums in the reference's index order).  The
 // parallelism comes from independent output elements, never from reordering a
 // sum.  This is what makes I, J and rho_history bit-identical to the CPU.
+#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -434,14 +435,18 @@ __global__ void heavy_walk_kernel(const unsigned* __restrict__ keys, const unsig
 // whose k loop runs in order with separate DMUL/DADD: the exact chain of the
 // reference, at GEMM data reuse.
 // ---------------------------------------------------------------------------
-// Tile 96 (sketch rows) x 64 (columns of A), k in chunks of 16, double-buffered
-// shared memory with a register prefetch of the next chunk; each thread owns a
-// 6 x 4 block strided by 16 so shared reads are conflict-free or broadcast.
-constexpr int kGI = 96, kGJ = 64, kGK = 16, kGA = kGI / 16, kGC = kGJ / 16;
+// Tile GI (sketch rows: 32/64/96/112, chosen per s to limit padding, e.g.
+// 112 for C3's s = 111, 96 for s = 275) x 64 (columns of A), k in chunks of 16,
+// double-buffered shared memory with a register prefetch of the next chunk;
+// each thread owns a (GI/16) x 4 block strided by 16 so shared reads are
+// conflict-free or broadcast.
+constexpr int kGJ = 64, kGK = 16, kGC = kGJ / 16;
 
+template <int kGI>
 __global__ void __launch_bounds__(256)
 sketch_gauss_dense_kernel(const double* __restrict__ S, int s, const double* __restrict__ A, long long m,
                           long long n, double* __restrict__ Y) {
+  constexpr int kGA = kGI / 16;
   __shared__ double Ss[2][kGK][kGI];
   __shared__ double As[2][kGK][kGJ];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
@@ -512,6 +517,129 @@ sketch_gauss_dense_kernel(const double* __restrict__ S, int s, const double* __r
       const long long i = i0 + ty + 16 * a, j = j0 + tx + 16 * c;
       if (i < s && j < n) Y[j * s + i] = acc[a][c];
     }
+}
+
+void launch_sketch_gauss_exact(cudaStream_t st, const double* S, int s, const double* A, long long m, long long n,
+                               double* Y) {
+  int best = 96;
+  long long pad = (s + 95) / 96 * 96;
+  for (int gi : {112, 64, 32}) {  // fewest padded rows; ties keep the larger tile
+    const long long p = (s + gi - 1) / gi * static_cast<long long>(gi);
+    if (p < pad) {
+      pad = p;
+      best = gi;
+    }
+  }
+  dim3 grid(static_cast<unsigned>((n + kGJ - 1) / kGJ), static_cast<unsigned>((s + best - 1) / best));
+  switch (best) {
+    case 112: sketch_gauss_dense_kernel<112><<<grid, 256, 0, st>>>(S, s, A, m, n, Y); break;
+    case 64: sketch_gauss_dense_kernel<64><<<grid, 256, 0, st>>>(S, s, A, m, n, Y); break;
+    case 32: sketch_gauss_dense_kernel<32><<<grid, 256, 0, st>>>(S, s, A, m, n, Y); break;
+    default: sketch_gauss_dense_kernel<96><<<grid, 256, 0, st>>>(S, s, A, m, n, Y); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Opt-in fast Gaussian sketch (sketch_kind 2): Y = S A on the FP64 tensor cores
+// (DMMA, mma.sync.m8n8k4.f64).  The MMA accumulates with fused multiply-adds in
+// hardware order, so Y is not bit-identical to matmul (matrix.hpp:351-361);
+// the CUR indices built from it are checked against the exact path's in
+// tests/test_gpu_dmma.py.  CTA tile: 96 sketch rows x 64 columns of A, k in
+// chunks of 32 staged by cp.async (double-buffered); warp w owns columns
+// [8w, 8w + 8) of the tile and all 12 m8 row tiles (24 fp64 accumulators).
+// Shared layouts keep the fragment loads conflict-free: S chunk [k][row]
+// (stride 100 = 4 mod 16 doubles), A chunk [col][k] (stride 36).
+// ---------------------------------------------------------------------------
+constexpr int kDI = 96, kDJ = 64, kDK = 32, kDSL = kDI + 4, kDAL = kDK + 4;
+constexpr int kDStage = kDK * kDSL + kDJ * kDAL;  // doubles per stage
+
+__device__ __forceinline__ void dmma_m8n8k4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool ok) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int bytes = ok ? 8 : 0;  // 0: zero-fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes));
+}
+
+__global__ void __launch_bounds__(256, 2)
+sketch_gauss_dmma_kernel(const double* __restrict__ S, int s, const double* __restrict__ A, long long m,
+                         long long n, double* __restrict__ Y) {
+  extern __shared__ double dsm[];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const long long i0 = static_cast<long long>(blockIdx.y) * kDI;
+  const long long j0 = static_cast<long long>(blockIdx.x) * kDJ;
+  auto stage = [&](int buf, long long k0) {
+    double* Ss = dsm + buf * kDStage;
+    double* As = Ss + kDK * kDSL;
+    // S chunk: kDK columns of S (rows i0..i0+kDI), 8-byte copies, zero-filled past s / m
+    for (int e = tid; e < kDK * kDI; e += 256) {
+      const int kk = e / kDI, ii = e % kDI;
+      const long long k = k0 + kk, i = i0 + ii;
+      const bool ok = k < m && i < s;
+      cp_async8(Ss + kk * kDSL + ii, ok ? S + k * s + i : S, ok);
+    }
+    // A chunk: kDJ columns of A, kDK consecutive rows each
+    for (int e = tid; e < kDJ * kDK; e += 256) {
+      const int jj = e / kDK, kk = e % kDK;
+      const long long k = k0 + kk, j = j0 + jj;
+      const bool ok = k < m && j < n;
+      cp_async8(As + jj * kDAL + kk, ok ? A + j * m + k : A, ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  double acc[kDI / 8][2];
+#pragma unroll
+  for (int q = 0; q < kDI / 8; ++q) acc[q][0] = acc[q][1] = 0.0;
+  const long long nk = (m + kDK - 1) / kDK;
+  stage(0, 0);
+  for (long long c = 0; c < nk; ++c) {
+    const int buf = static_cast<int>(c & 1);
+    if (c + 1 < nk) {
+      stage(buf ^ 1, (c + 1) * kDK);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    const double* Ss = dsm + buf * kDStage;
+    const double* As = Ss + kDK * kDSL;
+#pragma unroll
+    for (int kk = 0; kk < kDK; kk += 4) {
+      const double b = As[(8 * w + g) * kDAL + kk + t];  // B fragment: A(k0 + kk + t, j0 + 8w + g)
+#pragma unroll
+      for (int q = 0; q < kDI / 8; ++q) {
+        const double a = Ss[(kk + t) * kDSL + 8 * q + g];  // A fragment: S(i0 + 8q + g, k0 + kk + t)
+        dmma_m8n8k4(acc[q], a, b);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < kDI / 8; ++q) {
+    const long long i = i0 + 8 * q + g;
+    const long long j = j0 + 8 * w + 2 * t;
+    if (i < s) {
+      if (j < n) Y[j * s + i] = acc[q][0];
+      if (j + 1 < n) Y[(j + 1) * s + i] = acc[q][1];
+    }
+  }
+}
+
+void launch_sketch_gauss_dmma(cudaStream_t st, const double* S, int s, const double* A, long long m, long long n,
+                              double* Y) {
+  static bool attr = false;
+  const int smem = 2 * kDStage * static_cast<int>(sizeof(double));
+  if (!attr) {
+    APC_CUDA(cudaFuncSetAttribute(sketch_gauss_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  dim3 grid(static_cast<unsigned>((n + kDJ - 1) / kDJ), static_cast<unsigned>((s + kDI - 1) / kDI));
+  sketch_gauss_dmma_kernel<<<grid, 256, smem, st>>>(S, s, A, m, n, Y);
 }
 
 // sparse A with a Gaussian S: per (i, j) chain over the stored rows of column j
@@ -629,6 +757,183 @@ lupp_step_kernel(double* __restrict__ W, long long ld, long long rows, long long
   }
 }
 
+// ---------------------------------------------------------------------------
+// The same pivot order from ONE cooperative launch, blocked (dense_factor.hpp:
+// 119-157).  Every element w(r, c) still receives the updates of steps
+// 0, 1, ... in step order with the reference's skips (pval == 0, factor == 0)
+// and separately rounded products and differences, so the elimination and the
+// elections are bit-identical to the right-looking loop; only WHEN an update
+// is applied changes.  Steps come in panels of kLuppPanel columns:
+//   panel step k: unpivoted rows apply step k-1 to the panel columns [k, kend)
+//     and store its multiplier in w(r, k-1); local max |w(r, k)| (ties: lowest
+//     row); one grid barrier; every CTA reduces the per-CTA candidates in the
+//     same order, so all agree on the pivot without a second barrier;
+//   U rows: the panel's pivot rows get the panel's earlier steps on the
+//     trailing columns (thread per column, pivot order); grid barrier;
+//   trailing update: every other unpivoted row applies the panel's steps to
+//     the trailing columns, multipliers in registers, U rows in shared memory.
+// Traffic per element and panel instead of per step: ~kLuppPanel x fewer
+// passes over the rows x columns matrix (C5's E^col is 8e6 x 250).
+// ---------------------------------------------------------------------------
+constexpr int kLuppPanel = 16;
+constexpr int kLuppThreads = 256;
+constexpr int kLuppUCols = 256;  // trailing columns staged in shared memory per pass
+
+struct LuppCoopArgs {
+  double* W;
+  long long ld, rows, cols;
+  int steps;
+  char* piv;
+  long long* order;
+  double* mags;
+  double* cmag;      // 2 x grid candidates (double-buffered by step parity)
+  long long* cidx;
+  long long* prows;  // steps
+};
+
+__device__ __forceinline__ void block_best(double& best, long long& bidx, double* sm, long long* si) {
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    const double om = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (better(om, oi, best, bidx)) {
+      best = om;
+      bidx = oi;
+    }
+  }
+  __syncthreads();
+  if (lane == 0) {
+    sm[wp] = best;
+    si[wp] = bidx;
+  }
+  __syncthreads();
+  best = sm[0];
+  bidx = si[0];
+  for (int q = 1; q < kLuppThreads / 32; ++q)
+    if (better(sm[q], si[q], best, bidx)) {
+      best = sm[q];
+      bidx = si[q];
+    }
+}
+
+__global__ void __launch_bounds__(kLuppThreads)
+lupp_coop_kernel(LuppCoopArgs P) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sm[kLuppThreads / 32];
+  __shared__ long long si[kLuppThreads / 32];
+  __shared__ double U[kLuppPanel * kLuppUCols];
+  __shared__ long long spr[kLuppPanel];
+  double* W = P.W;
+  const long long ld = P.ld, rows = P.rows, cols = P.cols;
+  const long long T = static_cast<long long>(gridDim.x) * kLuppThreads;
+  const long long t0 = static_cast<long long>(blockIdx.x) * kLuppThreads + threadIdx.x;
+  const int G = gridDim.x;
+  for (int c0 = 0; c0 < P.steps; c0 += kLuppPanel) {
+    const int kend = min(P.steps, c0 + kLuppPanel);
+    double pv = 0.0;   // pivot value / row of the previous step (this CTA's copy)
+    long long pr = 0;
+    for (int k = c0; k < kend; ++k) {
+      double best = -1.0;
+      long long bidx = LLONG_MAX;
+      for (long long r = t0; r < rows; r += T) {
+        if (P.piv[r]) continue;
+        if (k > c0) {
+          double f = 0.0;
+          if (pv != 0.0) {
+            f = W[(k - 1) * ld + r] / pv;
+            if (f != 0.0)
+              for (long long c = k; c < kend; ++c) W[c * ld + r] -= f * __ldcg(W + c * ld + pr);
+          }
+          W[(k - 1) * ld + r] = f;  // the multiplier (0: the reference skipped this row)
+        }
+        const double mag = fabs(W[static_cast<long long>(k) * ld + r]);
+        if (better(mag, r, best, bidx)) {
+          best = mag;
+          bidx = r;
+        }
+      }
+      block_best(best, bidx, sm, si);
+      const int buf = (k & 1) * G;
+      if (threadIdx.x == 0) {
+        P.cmag[buf + blockIdx.x] = best;
+        P.cidx[buf + blockIdx.x] = bidx;
+      }
+      grid.sync();
+      // every CTA elects the same pivot from the same candidates (a total order)
+      best = -1.0;
+      bidx = LLONG_MAX;
+      for (int q = threadIdx.x; q < G; q += kLuppThreads) {
+        const double om = __ldcg(P.cmag + buf + q);
+        const long long oi = __ldcg(P.cidx + buf + q);
+        if (better(om, oi, best, bidx)) {
+          best = om;
+          bidx = oi;
+        }
+      }
+      block_best(best, bidx, sm, si);
+      if (bidx >= t0 && (bidx - t0) % T == 0) P.piv[bidx] = 1;  // the owning thread marks it
+      pv = __ldcg(W + static_cast<long long>(k) * ld + bidx);   // written before the barrier by its owner
+      pr = bidx;
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        P.order[k] = bidx;
+        P.mags[k] = best;
+        P.prows[k] = bidx;
+      }
+      if (threadIdx.x == 0) spr[k - c0] = bidx;
+    }
+    // multipliers of the panel's last step for the remaining unpivoted rows
+    for (long long r = t0; r < rows; r += T) {
+      if (P.piv[r]) continue;
+      const double f = pv != 0.0 ? W[static_cast<long long>(kend - 1) * ld + r] / pv : 0.0;
+      W[static_cast<long long>(kend - 1) * ld + r] = f;
+    }
+    if (kend >= cols) {
+      grid.sync();
+      continue;
+    }
+    __syncthreads();
+    // U rows: pivot row i of the panel gets steps c0..i-1 on the trailing columns
+    for (long long c = kend + t0; c < cols; c += T) {
+      for (int i = 1; i < kend - c0; ++i) {
+        const long long ri = spr[i];
+        double v = __ldcg(W + c * ld + ri);
+        for (int j = 0; j < i; ++j) {
+          const double f = __ldcg(W + static_cast<long long>(c0 + j) * ld + ri);
+          if (f != 0.0) v -= f * (j == 0 ? __ldcg(W + c * ld + spr[j]) : W[c * ld + spr[j]]);
+        }
+        W[c * ld + ri] = v;
+      }
+    }
+    grid.sync();
+    // trailing update of every other unpivoted row, kLuppUCols columns at a time
+    const int np = kend - c0;
+    for (long long cb = kend; cb < cols; cb += kLuppUCols) {
+      const int nc = static_cast<int>(cols - cb < kLuppUCols ? cols - cb : kLuppUCols);
+      __syncthreads();
+      for (int e = threadIdx.x; e < np * nc; e += kLuppThreads) {
+        const int j = e / nc, cc = e % nc;
+        U[j * kLuppUCols + cc] = __ldcg(W + (cb + cc) * ld + spr[j]);
+      }
+      __syncthreads();
+      for (long long r = t0; r < rows; r += T) {
+        if (P.piv[r]) continue;
+        double f[kLuppPanel];
+#pragma unroll
+        for (int j = 0; j < kLuppPanel; ++j) f[j] = j < np ? W[static_cast<long long>(c0 + j) * ld + r] : 0.0;
+        for (int cc = 0; cc < nc; ++cc) {
+          double v = W[(cb + cc) * ld + r];
+#pragma unroll
+          for (int j = 0; j < kLuppPanel; ++j)
+            if (f[j] != 0.0) v -= f[j] * U[j * kLuppUCols + cc];
+          W[(cb + cc) * ld + r] = v;
+        }
+      }
+    }
+    grid.sync();
+  }
+}
+
 // W (n x s column-major) = E^T with rows in J zeroed (cur.hpp:254-261)
 __global__ void transpose_zero_kernel(const double* __restrict__ E, long long s, long long n,
                                       const int* __restrict__ colsel, double* __restrict__ W) {
@@ -642,6 +947,191 @@ __global__ void transpose_zero_kernel(const double* __restrict__ E, long long s,
 // refresh: H = U R (core solve per column, cur.hpp:119-144,175-181) and
 // E^row = Y - Y(:,J) H (cur.hpp:306-312)
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// CoreFactor::build on the device (cur.hpp:59-114): the l x l intersection
+// block A(I, J) factored by Householder QR (dense_factor.hpp:40-72) or LU with
+// partial pivoting, in the reference's exact operation order: every norm and
+// dot is one thread's left-to-right chain, every update a separately rounded
+// product and difference.  One cooperative launch: CTA c owns kCoreCols
+// consecutive columns (one thread each) in shared memory (stride l + 1:
+// conflict-free); step j's reflector (or pivot and multipliers) is formed by
+// the owner of column j right after its own update of step j - 1, published
+// in a double-buffered global vector, and one grid barrier later every owner
+// of a later column applies it.  Outputs: the factor col-major (a / lu) and
+// transposed (row-major, for the warp solve), the reflectors col-major, the
+// LU permutation, and the singularity verdict (dmin <= 1e-14 dmax, or a zero
+// LU pivot) in flag[0].
+// ---------------------------------------------------------------------------
+constexpr int kCoreCols = 16;
+
+struct CoreBuildArgs {
+  const double* blk;  // l x l col-major
+  long long l;
+  int kind;           // 0 QR, 1 LU
+  double* fa;         // l x l col-major factor (R / LU)
+  double* fat;        // l x l row-major factor
+  double* hh;         // l x l col-major reflectors (QR)
+  long long* perm;    // l (LU)
+  double* vbuf;       // 2 x l
+  double* sbuf;       // 2 x 4 step scalars (skip / pivot row / pivot value)
+  int* flag;          // [0] singular
+};
+
+__global__ void __launch_bounds__(kCoreCols)
+core_build_kernel(CoreBuildArgs P) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double csm[];
+  const long long l = P.l, ls = l + 1;
+  double* col = csm;                       // kCoreCols x ls
+  double* v = csm + kCoreCols * ls;        // l: the step's reflector / multipliers
+  const long long jj = static_cast<long long>(blockIdx.x) * kCoreCols + threadIdx.x;  // my column
+  const bool own = jj < l;
+  double* c = col + threadIdx.x * ls;
+  if (own)
+    for (long long i = 0; i < l; ++i) c[i] = P.blk[jj * l + i];
+  long long perm_k = 0;
+  double dmax = 0.0, dmin = CUDART_INF;
+  bool singular = false;
+  for (long long j = 0; j < l; ++j) {
+    double* vb = P.vbuf + (j & 1) * l;
+    double* sb = P.sbuf + (j & 1) * 4;
+    if (own && jj == j) {
+      if (P.kind == 0) {  // reflector of step j (dense_factor.hpp:49-63)
+        double norm2 = 0.0;
+        for (long long i = j; i < l; ++i) norm2 += c[i] * c[i];
+        const double norm = sqrt(norm2);
+        int skip = norm == 0.0;
+        if (!skip) {
+          const double alpha = (c[j] >= 0.0) ? -norm : norm;
+          for (long long i = j; i < l; ++i) vb[i] = c[i];
+          vb[j] -= alpha;
+          double vn2 = 0.0;
+          for (long long i = j; i < l; ++i) vn2 += vb[i] * vb[i];
+          const double vn = sqrt(vn2);
+          if (vn == 0.0) {
+            skip = 1;
+            for (long long i = j; i < l; ++i) P.hh[j * l + i] = vb[i];
+          } else {
+            for (long long i = j; i < l; ++i) {
+              vb[i] /= vn;
+              P.hh[j * l + i] = vb[i];
+            }
+            c[j] = alpha;
+            for (long long i = j + 1; i < l; ++i) c[i] = 0.0;
+          }
+        }
+        sb[0] = skip;
+      } else {  // pivot of step k = j: first max |.| (cur.hpp:76-87)
+        long long best = j;
+        double bm = -1.0;
+        for (long long i = j; i < l; ++i) {
+          const double mg = fabs(c[i]);
+          if (mg > bm) {
+            bm = mg;
+            best = i;
+          }
+        }
+        if (best != j) {
+          const double t = c[j];
+          c[j] = c[best];
+          c[best] = t;
+        }
+        const double piv = c[j];
+        sb[1] = static_cast<double>(best);
+        sb[2] = piv;
+        if (piv != 0.0)
+          for (long long i = j + 1; i < l; ++i) {
+            const double fac = c[i] / piv;
+            c[i] = fac;
+            vb[i] = fac;
+          }
+      }
+    }
+    grid.sync();
+    if (P.kind == 0) {
+      if (__ldcg(sb) != 0.0) continue;  // zero column below the diagonal: nothing to reflect
+      for (long long i = j + threadIdx.x; i < l; i += kCoreCols) v[i] = __ldcg(vb + i);
+      __syncthreads();
+      if (own && jj > j) {  // dense_factor.hpp:64-70
+        double dot = 0.0;
+        for (long long i = j; i < l; ++i) dot += v[i] * c[i];
+        dot *= 2.0;
+        for (long long i = j; i < l; ++i) c[i] -= dot * v[i];
+      }
+      __syncthreads();
+    } else {
+      const long long best = static_cast<long long>(__ldcg(sb + 1));
+      const double piv = __ldcg(sb + 2);
+      if (threadIdx.x == 0 && blockIdx.x == 0) {
+        dmax = fmax(dmax, fabs(piv));
+        dmin = fmin(dmin, fabs(piv));
+        if (piv == 0.0) singular = true;
+        // perm swap (cur.hpp:83-85), kept in P.perm by one thread
+        if (j == 0)
+          for (long long i = 0; i < l; ++i) P.perm[i] = i;
+        if (best != j) {
+          const long long t = P.perm[j];
+          P.perm[j] = P.perm[best];
+          P.perm[best] = t;
+        }
+        (void)perm_k;
+      }
+      if (piv == 0.0) break;  // the reference fails here (singular)
+      for (long long i = j + 1 + threadIdx.x; i < l; i += kCoreCols) v[i] = __ldcg(vb + i);
+      __syncthreads();
+      if (own && jj != j) {
+        if (best != j) {  // whole-row swap, every column
+          const double t = c[j];
+          c[j] = c[best];
+          c[best] = t;
+        }
+        if (jj > j) {
+          const double ck = c[j];
+          for (long long i = j + 1; i < l; ++i) c[i] -= v[i] * ck;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (own) {
+    for (long long i = 0; i < l; ++i) {
+      P.fa[jj * l + i] = c[i];
+      P.fat[i * l + jj] = c[i];
+    }
+  }
+  if (P.kind == 1) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.flag[0] = (singular || !(dmin > 1e-14 * dmax)) ? 1 : 0;
+    return;
+  }
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // dmin / dmax of |R(j, j)| (cur.hpp:67-74)
+    double mn = CUDART_INF, mx = 0.0;
+    for (long long j = 0; j < l; ++j) {
+      const double d = fabs(__ldcg(P.fa + j * l + j));
+      mn = fmin(mn, d);
+      mx = fmax(mx, d);
+    }
+    P.flag[0] = !(mn > 1e-14 * mx) ? 1 : 0;
+  }
+}
+
+// row-major (l x b) -> col-major (l x b)
+__global__ void rm_to_cm_kernel(const double* __restrict__ X, long long l, long long b, double* __restrict__ Y) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= l * b) return;
+  const long long i = e / b, t = e % b;
+  Y[t * l + i] = X[e];
+}
+// gather R(:, J+) row-major (l x b) from R row-major (l x n)
+__global__ void gather_rcols_rm_kernel(const double* __restrict__ R, long long n, long long l,
+                                       const long long* __restrict__ jp, long long b, double* __restrict__ out) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= l * b) return;
+  const long long i = e / b, t = e % b;
+  out[e] = R[i * n + jp[t]];
+}
+
 __global__ void core_solve_cols_kernel(const double* __restrict__ R, double* __restrict__ H, long long l,
                                        long long n, int kind, const double* __restrict__ hh,
                                        const double* __restrict__ fa, const long long* __restrict__ perm) {
@@ -1220,11 +1710,28 @@ LuppOut device_lupp(apc_ctx* ctx, double* w, i64 rows, i64 cols, i64 max_pivots)
   DBuf<unsigned> ctr(1);
   APC_CUDA(cudaMemsetAsync(piv.p, 0, rows, st));
   APC_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned), st));
-  for (i64 k = 0; k < steps; ++k) {
-    lupp_step_kernel<<<nbk, kT, 0, st>>>(w, rows, rows, cols, static_cast<int>(k), piv.p, order.p, mags.p,
-                                         pv.p, pmag.p, pidx.p, ctr.p);
+  static const bool coop = !std::getenv("APC_LUPP_STEPS");
+  if (coop) {
+    // one cooperative launch: as many co-resident CTAs as the rows need
+    static int per_sm = -1;
+    if (per_sm < 0)
+      APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lupp_coop_kernel, kLuppThreads, 0));
+    const long long want = (rows + kLuppThreads - 1) / kLuppThreads;
+    const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(want, 1LL * per_sm * ctx->num_sms)));
+    DBuf<double> cmag(2 * grid);
+    DBuf<long long> cidx(2 * grid), prows(steps);
+    LuppCoopArgs args{w, rows, rows, cols, static_cast<int>(steps), piv.p, order.p, mags.p, cmag.p, cidx.p, prows.p};
+    void* kargs[] = {&args};
+    APC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(lupp_coop_kernel), dim3(grid),
+                                         dim3(kLuppThreads), kargs, 0, st));
+    ctx->launches++;
+  } else {
+    for (i64 k = 0; k < steps; ++k) {
+      lupp_step_kernel<<<nbk, kT, 0, st>>>(w, rows, rows, cols, static_cast<int>(k), piv.p, order.p, mags.p,
+                                           pv.p, pmag.p, pidx.p, ctr.p);
+    }
+    ctx->launches += static_cast<std::uint64_t>(steps);
   }
-  ctx->launches += static_cast<std::uint64_t>(steps);
   APC_CUDA(cudaGetLastError());
   auto o = download(ctx, order.p, steps);
   out.order.assign(o.begin(), o.end());
@@ -1244,6 +1751,7 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
           "CurState: the reference has no Gaussian sketch of the augmented stack");
   require(block >= 1, APC_INVALID_ARGUMENT, "CurState: block size must be >= 1");
   require(block <= n_, APC_INVALID_ARGUMENT, "CurState: block size exceeds column count");
+  require(sketch_kind >= 0 && sketch_kind <= 2, APC_INVALID_ARGUMENT, "CurState: sketch kind must be 0, 1 or 2");
   require(a.r0 == 0 && a.r1 == a.m, APC_NOT_APPLICABLE, "CurState: needs the full matrix on this rank");
   s_ = static_cast<i64>(std::ceil(1.1 * static_cast<double>(block)));
   const std::uint64_t emb_seed = splitmix(seed ^ 0x5ce7c3a1b2d4f688ULL);
@@ -1451,9 +1959,10 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
     DBuf<double> d_S;
     upload(ctx_, d_S, S.data(), s_ * m_);
     APC_CUDA(cudaEventRecord(ev0, st));
-    if (!a.sparse) {
-      dim3 grid(static_cast<unsigned>((n_ + kGJ - 1) / kGJ), static_cast<unsigned>((s_ + kGI - 1) / kGI));
-      sketch_gauss_dense_kernel<<<grid, 256, 0, st>>>(d_S.p, (int)s_, a.dense.p, m_, n_, Y_.p);
+    if (!a.sparse && sketch_kind == 2) {
+      launch_sketch_gauss_dmma(st, d_S.p, (int)s_, a.dense.p, m_, n_, Y_.p);
+    } else if (!a.sparse) {
+      launch_sketch_gauss_exact(st, d_S.p, (int)s_, a.dense.p, m_, n_, Y_.p);
     } else {
       sketch_gauss_csc_kernel<<<nb(n_ * 32), kT, 0, st>>>(d_S.p, (int)s_, a.at.ptr.p, a.at.idx.p, a.at.val.p, n_,
                                                           Y_.p);
@@ -1554,16 +2063,17 @@ AugmentResult DeviceCur::augment() {
   upload(ctx_, d_jp, reinterpret_cast<const long long*>(jplus.data()), b);
   upload(ctx_, d_J, reinterpret_cast<const long long*>(J_.data()), l);
 
-  // urj = U R(:, J+) on the host (l x b)
-  Vec urj;
+  // urj = U R(:, J+) (l x b col-major), the core solve on the device (same
+  // exact-order kernels as the refresh's U R)
   DBuf<double> d_urj;
   if (l > 0) {
-    DBuf<double> d_rj(l * b);
-    gather_rcols_kernel<<<nb(l * b), kT, 0, st>>>(Rrm_.p, n_, l, d_jp.p, b, d_rj.p);
-    ctx_->launches++;
-    Vec rj = download(ctx_, d_rj.p, l * b);
-    urj = core_.solve_matrix(b, std::move(rj));
-    upload(ctx_, d_urj, urj.data(), l * b);
+    DBuf<double> d_rj(l * b), d_hj(l * b);
+    gather_rcols_rm_kernel<<<nb(l * b), kT, 0, st>>>(Rrm_.p, n_, l, d_jp.p, b, d_rj.p);
+    core_solve_cols_kernel<<<nb(b, 128), 128, 0, st>>>(d_rj.p, d_hj.p, l, b, core_kind_, core_h_.p, core_a_.p,
+                                                       core_perm_.p);
+    d_urj.alloc(l * b);
+    rm_to_cm_kernel<<<nb(l * b), kT, 0, st>>>(d_hj.p, l, b, d_urj.p);
+    ctx_->launches += 3;
   }
   // E^col = A(:, J+) - C urj, rows I zeroed (m x b)
   DBuf<double> ecol(std::max<i64>(1, mt_ * b));
@@ -1648,8 +2158,17 @@ void DeviceCur::refresh() {
                                                 a_.sparse ? 1 : 0, d_I.p, d_J.p, l, l, amu_, d_blk.p);
   ctx_->launches++;
   std::unique_ptr<ProfScope> ps(new ProfScope("ref.core_build"));
-  block_ = download(ctx_, d_blk.p, l * l);
-  core_ = CoreFactorH::build(l, block_, core_kind_);  // throws singular
+  static const bool host_core = std::getenv("APC_HOST_CORE") != nullptr;
+  if (host_core || (kCoreCols * (l + 1) + l) * 8 > 227 * 1024) {
+    block_ = download(ctx_, d_blk.p, l * l);
+    core_ = CoreFactorH::build(l, block_, core_kind_);  // throws singular
+    host_core_stale_ = false;
+    core_l_ = l;
+    upload_core();
+  } else {
+    block_d_ = std::move(d_blk);
+    build_core_device(l);  // throws singular
+  }
   ps.reset(new ProfScope("ref.rows_H_eres"));
   // R = A(I, :) row-major (all rows re-gathered: I may have changed after a rollback)
   Rrm_.ensure(l * n_);
@@ -1662,7 +2181,6 @@ void DeviceCur::refresh() {
   }
   ctx_->launches++;
   // H = U R (core solve per column)
-  upload_core();
   H_.ensure(l * n_);
   // warp per column wins when there are few columns (latency-bound chains,
   // C1: n = 500); with many columns the FP64 pipe is the limit and a thread
@@ -1691,6 +2209,62 @@ void DeviceCur::refresh() {
   APC_CUDA(cudaStreamSynchronize(st));
   ps.reset(new ProfScope("ref.rho"));
   compute_rho();
+}
+
+void DeviceCur::build_core_device(i64 l) {
+  cudaStream_t st = ctx_->stream;
+  core_a_.ensure(l * l);
+  core_at_.ensure(l * l);
+  core_h_.ensure(l * l);
+  core_perm_.ensure(l);
+  DBuf<double> vbuf(2 * l), sbuf(8);
+  DBuf<int> flag(1);
+  APC_CUDA(cudaMemsetAsync(core_h_.p, 0, sizeof(double) * l * l, st));
+  const int smem = static_cast<int>((kCoreCols * (l + 1) + l) * sizeof(double));
+  static int attr = 0;
+  if (smem > attr) {
+    APC_CUDA(cudaFuncSetAttribute(core_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = smem;
+  }
+  CoreBuildArgs args{block_d_.p, l, core_kind_, core_a_.p, core_at_.p, core_h_.p, core_perm_.p, vbuf.p, sbuf.p, flag.p};
+  void* kargs[] = {&args};
+  const unsigned grid = static_cast<unsigned>((l + kCoreCols - 1) / kCoreCols);
+  APC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(core_build_kernel), dim3(grid), dim3(kCoreCols),
+                                       kargs, smem, st));
+  ctx_->launches++;
+  int singular = 0;
+  APC_CUDA(cudaMemcpyAsync(&singular, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  APC_CUDA(cudaStreamSynchronize(st));
+  core_l_ = l;
+  host_core_stale_ = true;
+  if (singular) fail(APC_SINGULAR, "CoreFactor: intersection block numerically singular");
+}
+
+const CoreFactorH& DeviceCur::core() const {
+  if (host_core_stale_) {
+    const i64 l = core_l_;
+    CoreFactorH f;
+    f.l = l;
+    f.kind = core_kind_;
+    if (core_kind_ == 0) {
+      f.qr.m = f.qr.k = l;
+      f.qr.a = download(ctx_, core_a_.p, l * l);
+      f.qr.hh = download(ctx_, core_h_.p, l * l);
+    } else {
+      f.lu = download(ctx_, core_a_.p, l * l);
+      auto pm = download(ctx_, core_perm_.p, l);
+      f.perm.assign(pm.begin(), pm.end());
+    }
+    core_ = std::move(f);
+    block_ = download(ctx_, block_d_.p, l * l);
+    host_core_stale_ = false;
+  }
+  return core_;
+}
+
+const Vec& DeviceCur::intersection() const {
+  (void)core();
+  return block_;
 }
 
 void DeviceCur::upload_core() {

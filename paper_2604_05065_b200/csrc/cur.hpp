@@ -52,8 +52,10 @@ class DeviceCur {
   i64 last_added() const { return last_added_; }
   i64 sketch_rows() const { return s_; }
   i64 n() const { return n_; }
-  const CoreFactorH& core() const { return core_; }
-  const Vec& intersection() const { return block_; }  // l x l column-major
+  // host copies of the factor and of A(I, J) (the svd-free preconditioner
+  // builders use them), downloaded on first use after each refresh
+  const CoreFactorH& core() const;
+  const Vec& intersection() const;  // l x l column-major
   std::uint64_t sketch_applications() const { return 1; }
 
   AugmentResult augment();   // cur.hpp:248-294
@@ -95,8 +97,12 @@ class DeviceCur {
   // the probe set of the next compute_rho, drawn on a host thread while the
   // device works (the stream is consumed strictly in order, one set at a time)
   std::future<std::vector<double>> next_probes_;
-  CoreFactorH core_;
-  Vec block_;
+  void build_core_device(i64 l);  // CoreFactor::build on the device (exact order)
+  mutable CoreFactorH core_;
+  mutable Vec block_;
+  mutable bool host_core_stale_ = false;
+  i64 core_l_ = 0;
+  DBuf<double> block_d_;      // A(I, J) l x l col-major
   DBuf<double> Y_, E_;        // s x n column-major
   DBuf<double> Rrm_;          // R = A(I,:) row-major, capacity max_rank x n
   DBuf<double> H_;            // U R row-major l x n

@@ -207,23 +207,43 @@ struct PcExpandEpi {
   double* out;
   int mode;
   double beta;
+  int fuse_tail;  // mode 0: also u_t <- mu z - alpha u_t/beta (lsqr_tail_kernel), ||u_t||^2
+  double alpha;
   __device__ void begin() {
     if (mode == 1) beta = sqrt(P.g[P.n] + P.st->tail_norm2);
+    if (mode == 0 && fuse_tail) {
+      alpha = P.st->alpha;
+      beta = P.st->beta;
+    }
   }
   __device__ double load(long long j) { return mode == 1 ? P.v[j] : 0.0; }
   __device__ double row(long long j, double acc, double vj) {
     const double o = x[j] + acc;
     if (mode == 0) {
       out[j] = o;
-      return 0.0;
+      if (!fuse_tail) return 0.0;
+      double* ut = P.u + P.mloc;
+      const double uo = ut[j];
+      const double uh = beta > 0.0 ? uo / beta : uo;
+      const double t = P.mu * o - alpha * uh;
+      ut[j] = t;
+      return t * t;
     }
     const double t = o - beta * vj;
     P.v[j] = t;
     return t * t;
   }
   __device__ void tile_done(unsigned tile, unsigned ntiles, double sq) {
-    if (mode == 0) return;
     __shared__ double sh[32];
+    if (mode == 0) {
+      if (!fuse_tail) return;
+      if (threadIdx.x == 0) P.tail_part[tile] = sq;
+      if (elect_last_block(P.ctr + 1, ntiles)) {
+        const double s = ordered_sum<256>(P.tail_part, ntiles, sh);
+        if (threadIdx.x == 0) P.st->tail_norm2 = s;
+      }
+      return;
+    }
     if (threadIdx.x == 0) P.epi_part[tile] = sq;
     if (elect_last_block(P.ctr + 2, ntiles)) {
       const double s = ordered_sum<256>(P.epi_part, ntiles, sh);
@@ -462,12 +482,20 @@ pc_small_kernel(const int* __restrict__ rptr, const int* __restrict__ ridx, cons
 
 // expand: o_j = x_j + (B s)_j (explicit) or x_j + (R^T s)_j (implicit), then
 // mode 0: out[j] = o_j ; mode 1: v_j = o_j - beta v_j, ||v||^2 -> alpha (last block)
+// mode 0 fusions (the iteration's z = P^{-1} v feeds them): xr[inv[j]] = z_j,
+// the hot-relabelled copy of z for the forward (hot_permute_kernel); tail:
+// u_t <- mu z - alpha u_t/beta with ||u_t||^2 (lsqr_tail_kernel)
+struct ExpandFuse {
+  double* xr;
+  const int* inv;
+  int tail;
+};
 __global__ void __launch_bounds__(kVecThreads)
 pc_expand_kernel(LsqrPtrs P, int kind, const double* __restrict__ B, long long l,
                  const int* __restrict__ tptr, const int* __restrict__ tidx,
                  const double* __restrict__ tval, const double* __restrict__ s,
                  const double* __restrict__ x, double* __restrict__ out, int mode,
-                 const int* done) {
+                 const int* done, ExpandFuse fz) {
   __shared__ double sh[32];
   // implicit basis: R^T rows longer than kExpandLong (the Zipf-head columns of
   // a sparse A appear in most selected rows) are summed by a whole warp
@@ -515,13 +543,32 @@ pc_expand_kernel(LsqrPtrs P, int kind, const double* __restrict__ B, long long l
     const double o = x[j] + acc;
     if (mode == 0) {
       out[j] = o;
+      if (fz.xr) fz.xr[fz.inv[j]] = o;
+      if (fz.tail) {
+        const double a0 = P.st->alpha, b0 = P.st->beta;
+        double* ut = P.u + P.mloc;
+        const double uo = ut[j];
+        const double uh = b0 > 0.0 ? uo / b0 : uo;
+        const double t = P.mu * o - a0 * uh;
+        ut[j] = t;
+        sq = t * t;
+      }
     } else {
       const double t = o - beta * P.v[j];
       P.v[j] = t;
       sq = t * t;
     }
   }
-  if (mode == 0) return;
+  if (mode == 0) {
+    if (!fz.tail) return;
+    sq = block_sum<kVecThreads>(sq, sh);
+    if (threadIdx.x == 0) P.tail_part[blockIdx.x] = sq;
+    if (elect_last_block(P.ctr + 1, gridDim.x)) {
+      const double ssum = ordered_sum<kVecThreads>(P.tail_part, gridDim.x, sh);
+      if (threadIdx.x == 0) P.st->tail_norm2 = ssum;
+    }
+    return;
+  }
   sq = block_sum<kVecThreads>(sq, sh);
   if (threadIdx.x == 0) P.epi_part[blockIdx.x] = sq;
   if (elect_last_block(P.ctr + 2, gridDim.x)) {
@@ -628,20 +675,24 @@ void pc_project_core(LsqrWork* w, PrecondDev& p, const double* x, bool transpose
   }
 }
 
-void pc_expand(LsqrWork* w, const LsqrPtrs& P, PrecondDev& p, const double* x, double* out,
-               int mode, const int* done) {
+// returns true when the fusions asked for were applied (xr only on the
+// implicit-basis kernel; the mu-tail on both)
+bool pc_expand(LsqrWork* w, const LsqrPtrs& P, PrecondDev& p, const double* x, double* out,
+               int mode, const int* done, ExpandFuse fz = ExpandFuse{nullptr, nullptr, 0}) {
   if (p.kind == 1 && !std::getenv("APC_PC_EXPAND_ROWS")) {
+    if (fz.xr) return false;
     const DenseFwdPlan pl = dense_fwd_plan(p.n, p.l, w->ctx->num_sms);
     dim3 grid(static_cast<unsigned>(pl.ntiles), static_cast<unsigned>(pl.nsplit));
     dense_fwd_kernel<PcExpandEpi><<<grid, kDenseFwdThreads, 0, w->ctx->stream>>>(
         p.B.p, p.n, p.n, p.l, w->s.p, pl.cols_per_split, pl.nsplit > 1 ? w->pcf_part.p : nullptr,
-        pl.nsplit > 1 ? w->pcf_ctr.p : nullptr, done, PcExpandEpi{P, x, out, mode, 0.0});
+        pl.nsplit > 1 ? w->pcf_ctr.p : nullptr, done, PcExpandEpi{P, x, out, mode, 0.0, fz.tail, 0.0});
     w->ctx->launches++;
-    return;
+    return true;
   }
   pc_expand_kernel<<<nb(w->n), kVecThreads, 0, w->ctx->stream>>>(
-      P, p.kind, p.B.p, p.l, p.RT.ptr.p, p.RT.idx.p, p.RT.val.p, w->s.p, x, out, mode, done);
+      P, p.kind, p.B.p, p.l, p.RT.ptr.p, p.RT.idx.p, p.RT.val.p, w->s.p, x, out, mode, done, fz);
   w->ctx->launches++;
+  return true;
 }
 
 void ensure_pc_buffers(LsqrWork* w, PrecondDev& p) {
@@ -671,29 +722,52 @@ void enqueue_iteration(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P
   const int* done = &P.st->done;
   const bool pre = p && p->kind != 0;
   const double* z = P.v;
-  if (pre) {  // z = P^{-1} v
+  // kernel fusions of the preconditioned single-rank iteration (APC_FUSE=0 turns them off)
+  static const bool fuse_env = !std::getenv("APC_FUSE") || std::atoi(std::getenv("APC_FUSE")) != 0;
+  bool tail_fused = false, x_permuted = false;
+  if (pre) {  // z = P^{-1} v (+ its hot-relabelled copy, + the mu-tail rows of u)
     pc_project_core(w, *p, P.v, false, done);
-    pc_expand(w, P, *p, P.v, P.z, 0, done);
+    const bool want_xr = fuse_env && w->mloc > 0 && fwd_takes_permuted(a);
+    const bool want_tail = fuse_env && P.has_tail;
+    ExpandFuse fz{want_xr ? a.hot.xr.p : nullptr, want_xr ? a.hot.inv.p : nullptr, want_tail ? 1 : 0};
+    if (pc_expand(w, P, *p, P.v, P.z, 0, done, fz)) {
+      x_permuted = want_xr;
+      tail_fused = want_tail;
+    } else {
+      pc_expand(w, P, *p, P.v, P.z, 0, done, ExpandFuse{nullptr, nullptr, want_tail ? 1 : 0});
+      tail_fused = want_tail;
+    }
     z = P.z;
   }
   LsqrFwdEpi epi{P.u, P.st, P.fwd_part, P.ctr + 0, P.g + P.n, 0.0, 0.0};
   if (w->mloc > 0) {
-    launch_fwd(a, z, done, epi, st);
+    launch_fwd(a, z, done, epi, st, x_permuted);
   } else {
     // empty shard: publish ||u_top||^2 = 0 through the init-copy path
     lsqr_init_copy_kernel<<<1, kVecThreads, 0, st>>>(P, P.u, 0, 0, 0);
     ctx->launches++;
   }
-  if (P.has_tail) {
+  if (P.has_tail && !tail_fused) {
     LsqrPtrs Pz = P;
     Pz.z = const_cast<double*>(z);
     lsqr_tail_kernel<<<nb(w->n), kVecThreads, 0, st>>>(Pz);
     ctx->launches++;
   }
-  op_adj_raw(a, P.u, P.g, done);
-  comm_allreduce(ctx, P.g, w->n + 1);
-  lsqr_epi_kernel<<<nb(w->n), kVecThreads, 0, st>>>(P, pre ? 1 : 0);
-  ctx->launches++;
+  // A^T u with the epilogue h = (A^T u + mu u_t)/beta where the columns are
+  // finalised (one rank: no allreduce between them).  Off by default: on C5
+  // the per-column u_t gather and division inside the tail stream's store cost
+  // ~20 us per iteration more than the separate epilogue pass (APC_FUSE_EPI=1)
+  static const bool epi_env = std::getenv("APC_FUSE_EPI") && std::atoi(std::getenv("APC_FUSE_EPI")) != 0;
+  const bool epi_fused =
+      fuse_env && epi_env && pre && ctx->nranks == 1 && w->mloc > 0 &&
+      op_adj_epi(a, P.u, P.h, done,
+                 AdjEpi{P.has_tail ? P.u + P.mloc : nullptr, P.mu, P.g + P.n, P.has_tail ? &P.st->tail_norm2 : nullptr});
+  if (!epi_fused) {
+    op_adj_raw(a, P.u, P.g, done);
+    comm_allreduce(ctx, P.g, w->n + 1);
+    lsqr_epi_kernel<<<nb(w->n), kVecThreads, 0, st>>>(P, pre ? 1 : 0);
+    ctx->launches++;
+  }
   if (pre) {  // v = P^{-T} h - beta v ; alpha ; rotation
     pc_project_core(w, *p, P.h, true, done);
     pc_expand(w, P, *p, P.h, nullptr, 1, done);
@@ -843,7 +917,7 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   // host-polled; used for multi-rank) | "eager" (no graph; for kernel profiling)
   const char* mode_env = std::getenv("APC_LSQR_MODE");
   const std::string mode = mode_env ? mode_env : "";
-  const bool eager = mode == "eager";
+  const bool eager = mode == "eager" || !comm_graph_safe(ctx);
   const bool persistent =
       !sampling && (mode.empty() || mode == "persistent") && persistent_eligible(a, p, ctx);
   const bool use_while = !persistent && ctx->nranks == 1 && mode != "batch" && !eager;

@@ -301,6 +301,7 @@ struct HeadPiece {
 };
 
 struct HeadPolicy {
+  __device__ __forceinline__ void begin() {}
   double* part;
   int nb;  // blocks (ncols x nblocks < 2^31, build_head_adj)
   static constexpr bool kStage = true;
@@ -317,6 +318,11 @@ struct TailPolicy {
   const int* __restrict__ tcol;   // per (group, column in group): destination index in out
   double* out;                    // A^T u (one row superblock) or the superblock partials
   int rb;                         // bits of the row field
+  AdjEpi e;                       // e.n2top != nullptr: out = (raw + mu u_t) / beta (lsqr_epi_kernel)
+  double beta;
+  __device__ __forceinline__ void begin() {
+    if (e.n2top) beta = sqrt(*e.n2top + (e.n2tail ? *e.n2tail : 0.0));
+  }
   static constexpr bool kStage = false;
 #ifndef APC_TAIL_MINB
 #define APC_TAIL_MINB 2
@@ -325,7 +331,14 @@ struct TailPolicy {
   __device__ __forceinline__ int col(unsigned key) const { return static_cast<int>(key >> rb); }
   __device__ __forceinline__ int row(unsigned key) const { return static_cast<int>(key & ((1u << rb) - 1u)); }
   __device__ __forceinline__ int pad() const { return static_cast<int>((1u << (32 - rb)) - 1u); }
-  __device__ __forceinline__ void store(int k, long long g, double s) const { out[__ldg(tcol + __ldg(gcol0 + g) + k)] = s; }
+  __device__ __forceinline__ void store(int k, long long g, double s) const {
+    const int j = __ldg(tcol + __ldg(gcol0 + g) + k);
+    if (e.n2top) {
+      const double raw = e.ut ? s + e.mu * e.ut[j] : s;
+      s = beta > 0.0 ? raw / beta : raw;
+    }
+    out[j] = s;
+  }
   __device__ __forceinline__ void zero(int k, long long g) const { store(k, g, 0.0); }
 };
 
@@ -366,6 +379,7 @@ seg_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, const
   if (done && *done) return;
   const int blk = blockIdx.x / parts;
   const int prt = blockIdx.x % parts;
+  pol.begin();
   const int PAD = pol.pad();
   const double* ub = u;
   if (Pol::kStage) {
@@ -558,6 +572,7 @@ template <class Pol>
 __global__ void seg_bnd_kernel(const HeadPiece* __restrict__ bnd, int parts, long long nblocks, Pol pol,
                                const int* done) {
   if (done && *done) return;
+  pol.begin();
   const long long blk = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (blk >= nblocks) return;
   int k = -1, f = -1;
@@ -573,19 +588,25 @@ __global__ void seg_bnd_kernel(const HeadPiece* __restrict__ bnd, int parts, lon
 
 // out[col] = sum of the column's superblock partials, superblock order
 __global__ void tail_combine_kernel(const double* __restrict__ part, const int* __restrict__ cols, long long ncols,
-                                    int S, double* __restrict__ out, const int* done) {
+                                    int S, double* __restrict__ out, const int* done, AdjEpi e) {
   if (done && *done) return;
   const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= ncols) return;
   double s = part[t * S];
   for (int sb = 1; sb < S; ++sb) s += part[t * S + sb];
-  out[cols[t]] = s;
+  const int j = cols[t];
+  if (e.n2top) {
+    const double beta = sqrt(*e.n2top + (e.n2tail ? *e.n2tail : 0.0));
+    const double raw = e.ut ? s + e.mu * e.ut[j] : s;
+    s = beta > 0.0 ? raw / beta : raw;
+  }
+  out[j] = s;
 }
 
 // warp per head column: its partials in block order -> out[col]
 __global__ void __launch_bounds__(256)
 head_combine_kernel(const double* __restrict__ part, long long nblocks, const int* __restrict__ hcol,
-                    long long ncols, double* __restrict__ out, const int* done) {
+                    long long ncols, double* __restrict__ out, const int* done, AdjEpi e) {
   if (done && *done) return;
   const long long k = (static_cast<long long>(blockIdx.x) * 256 + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -594,7 +615,15 @@ head_combine_kernel(const double* __restrict__ part, long long nblocks, const in
   double s = 0.0;
   for (long long q = lane; q < nblocks; q += 32) s += pk[q];
   s = warp_sum(s);
-  if (lane == 0) out[__ldg(hcol + k)] = s;
+  if (lane == 0) {
+    const int j = __ldg(hcol + k);
+    if (e.n2top) {  // the LSQR epilogue (lsqr_epi_kernel), fused
+      const double beta = sqrt(*e.n2top + (e.n2tail ? *e.n2tail : 0.0));
+      const double raw = e.ut ? s + e.mu * e.ut[j] : s;
+      s = beta > 0.0 ? raw / beta : raw;
+    }
+    out[j] = s;
+  }
 }
 
 }  // namespace
@@ -631,9 +660,13 @@ void build_hot_sell(apc_mat& a, const std::vector<long long>& col_nnz) {
   std::stable_sort(hot.begin(), hot.end(), [&](int x, int y) { return col_nnz[x] > col_nnz[y]; });
   nptr[0] = 0;
   for (long long k = 0; k < n; ++k) nptr[k + 1] = nptr[k] + static_cast<int>(col_nnz[hot[k]]);
+  std::vector<int> inv(n);
+  for (long long k = 0; k < n; ++k) inv[hot[k]] = static_cast<int>(k);
   h.n = n;
   h.hot.alloc(n);
+  h.inv.alloc(n);
   h.xr.alloc(n);
+  APC_CUDA(cudaMemcpyAsync(h.inv.p, inv.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
   DBuf<int> dn(n + 1), keys(nnz), vals(nnz), kout(nnz), vout(nnz);
   APC_CUDA(cudaMemcpyAsync(h.hot.p, hot.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
   APC_CUDA(cudaMemcpyAsync(dn.p, nptr.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice, st));
@@ -769,6 +802,46 @@ void op_fwd(apc_mat& a, double mu, bool augmented, const double* x, double* y) {
   APC_CUDA(cudaGetLastError());
 }
 
+namespace {
+// head + tail-stream adjoint; e.n2top != nullptr fuses the LSQR epilogue
+void seg_adjoint(apc_mat& a, const double* u, double* out, const int* done, const AdjEpi& e) {
+  cudaStream_t st = a.ctx->stream;
+  const HeadAdj& h = a.head;
+  const HeadAdj::Seg& t = h.seg;
+  const TailPolicy pol{t.gcol0.p, t.tcol.p, t.sb > 1 ? t.part.p : out, t.rb, t.sb > 1 ? AdjEpi{} : e, 0.0};
+  seg_adj_kernel<TailPolicy><<<static_cast<unsigned>(t.ngroups * t.parts), kHeadThreads, 0, st>>>(
+      t.gptr.p, t.tkey.p, t.tval.p, u, a.mloc(), t.parts, t.zptr.p, t.zcol.p, pol,
+      reinterpret_cast<HeadPiece*>(t.bnd.p), done);
+  a.ctx->launches++;
+  if (t.parts > 1) {
+    seg_bnd_kernel<TailPolicy><<<nblk(t.ngroups, 128), 128, 0, st>>>(reinterpret_cast<const HeadPiece*>(t.bnd.p),
+                                                                     t.parts, t.ngroups, pol, done);
+    a.ctx->launches++;
+  }
+  if (t.sb > 1) {
+    tail_combine_kernel<<<nblk(t.ncols, 256), 256, 0, st>>>(t.part.p, t.cols.p, t.ncols, t.sb, out, done, e);
+    a.ctx->launches++;
+  }
+  const HeadPolicy hp{h.part.p, static_cast<int>(h.nblocks)};
+  seg_adj_kernel<HeadPolicy><<<static_cast<unsigned>(h.nblocks * h.parts), kHeadThreads, sizeof(double) * kHeadRows,
+                               st>>>(h.bptr.p, h.hkey.p, h.hval.p, u, a.mloc(), h.parts, h.zptr.p, h.zcol.p, hp,
+                                     reinterpret_cast<HeadPiece*>(h.bnd.p), done);
+  if (h.parts > 1) {
+    seg_bnd_kernel<HeadPolicy><<<nblk(h.nblocks, 128), 128, 0, st>>>(reinterpret_cast<const HeadPiece*>(h.bnd.p),
+                                                                     h.parts, h.nblocks, hp, done);
+    a.ctx->launches++;
+  }
+  head_combine_kernel<<<nblk(h.ncols * 32, 256), 256, 0, st>>>(h.part.p, h.nblocks, h.hcol.p, h.ncols, out, done, e);
+  a.ctx->launches += 2;
+}
+}  // namespace
+
+bool op_adj_epi(apc_mat& a, const double* u, double* h, const int* done, const AdjEpi& e) {
+  if (!a.sparse || !a.head.built() || !a.head.seg.built()) return false;
+  seg_adjoint(a, u, h, done, e);
+  return true;
+}
+
 void op_adj_raw(apc_mat& a, const double* u, double* out, const int* done) {
   cudaStream_t st = a.ctx->stream;
   if (!a.sparse) {
@@ -784,43 +857,24 @@ void op_adj_raw(apc_mat& a, const double* u, double* out, const int* done) {
   }
   const Csr& c = a.at;
   if (a.head.built()) {
-    const HeadAdj& h = a.head;
-    static const int mask = std::getenv("APC_ADJ_MASK") ? std::atoi(std::getenv("APC_ADJ_MASK")) : 0xff;
-    if (mask & 1) {
-      if (h.seg.built()) {
-        const HeadAdj::Seg& t = h.seg;
-        const TailPolicy pol{t.gcol0.p, t.tcol.p, t.sb > 1 ? t.part.p : out, t.rb};
-        seg_adj_kernel<TailPolicy><<<static_cast<unsigned>(t.ngroups * t.parts), kHeadThreads, 0, st>>>(
-            t.gptr.p, t.tkey.p, t.tval.p, u, a.mloc(), t.parts, t.zptr.p, t.zcol.p, pol,
-            reinterpret_cast<HeadPiece*>(t.bnd.p), done);
-        a.ctx->launches++;
-        if (t.parts > 1) {
-          seg_bnd_kernel<TailPolicy><<<nblk(t.ngroups, 128), 128, 0, st>>>(reinterpret_cast<const HeadPiece*>(t.bnd.p),
-                                                                           t.parts, t.ngroups, pol, done);
-          a.ctx->launches++;
-        }
-        if (t.sb > 1) {
-          tail_combine_kernel<<<nblk(t.ncols, 256), 256, 0, st>>>(t.part.p, t.cols.p, t.ncols, t.sb, out, done);
-          a.ctx->launches++;
-        }
-      } else {
-        launch_units(a.ctx, c, h.tail, u, out, done);
-      }
+    if (a.head.seg.built()) {
+      seg_adjoint(a, u, out, done, AdjEpi{});
+      return;
     }
+    const HeadAdj& h = a.head;
+    launch_units(a.ctx, c, h.tail, u, out, done);
     const HeadPolicy hp{h.part.p, static_cast<int>(h.nblocks)};
-    if (mask & 2)
-      seg_adj_kernel<HeadPolicy><<<static_cast<unsigned>(h.nblocks * h.parts), kHeadThreads,
-                                   sizeof(double) * kHeadRows, st>>>(h.bptr.p, h.hkey.p, h.hval.p, u, a.mloc(),
-                                                                     h.parts, h.zptr.p, h.zcol.p, hp,
-                                                                     reinterpret_cast<HeadPiece*>(h.bnd.p), done);
+    seg_adj_kernel<HeadPolicy><<<static_cast<unsigned>(h.nblocks * h.parts), kHeadThreads,
+                                 sizeof(double) * kHeadRows, st>>>(h.bptr.p, h.hkey.p, h.hval.p, u, a.mloc(),
+                                                                   h.parts, h.zptr.p, h.zcol.p, hp,
+                                                                   reinterpret_cast<HeadPiece*>(h.bnd.p), done);
     if (h.parts > 1) {
       seg_bnd_kernel<HeadPolicy><<<nblk(h.nblocks, 128), 128, 0, st>>>(reinterpret_cast<const HeadPiece*>(h.bnd.p),
                                                                        h.parts, h.nblocks, hp, done);
       a.ctx->launches++;
     }
-    if (mask & 4)
-      head_combine_kernel<<<nblk(h.ncols * 32, 256), 256, 0, st>>>(h.part.p, h.nblocks, h.hcol.p, h.ncols, out,
-                                                                  done);
+    head_combine_kernel<<<nblk(h.ncols * 32, 256), 256, 0, st>>>(h.part.p, h.nblocks, h.hcol.p, h.ncols, out, done,
+                                                                AdjEpi{});
     a.ctx->launches += 2;
     return;
   }
@@ -934,6 +988,13 @@ void build_units_sel(apc_ctx* ctx, Units& c, long long rows, const std::vector<l
       if (skip && (*skip)[r]) continue;
       const long long b0 = S > 1 ? cut[r * (S + 1) + sb] : off[r];
       const long long e0 = S > 1 ? cut[r * (S + 1) + sb + 1] : off[r] + row_nnz[r];
+      if (row_nnz[r] == 0 && sb == 0) {  // an empty row still writes its 0
+        urow.push_back(static_cast<int>(r));
+        ustart.push_back(static_cast<int>(b0));
+        uend.push_back(static_cast<int>(b0));
+        uslot.push_back(-1);
+        continue;
+      }
       for (long long b = b0; b < e0; b += kCsrUnitMax) {
         urow.push_back(static_cast<int>(r));
         ustart.push_back(static_cast<int>(b));

@@ -354,6 +354,19 @@ void op_fwd(apc_mat& a, double mu, bool augmented, const double* x, double* y);
 void op_adj(apc_mat& a, double mu, bool augmented, const double* u, double* y);
 // raw A^T u into out[0..n) (units fix-up is left to the caller for CSR)
 void op_adj_raw(apc_mat& a, const double* u, double* out, const int* done);
+// LSQR epilogue applied where A^T u is finalised (single rank): h_j =
+// (raw_j + mu u_t[j]) / beta, beta = sqrt(*n2top + *n2tail) (lsqr.cu lsqr_epi_kernel)
+struct AdjEpi {
+  const double* ut;      // mu-tail of u (nullptr: none)
+  double mu;
+  const double* n2top;   // ||u_top||^2
+  const double* n2tail;  // ||u_tail||^2 (nullptr: 0)
+};
+// op_adj_raw with the epilogue fused into the kernels that finalise columns;
+// returns false (nothing launched) when the layout has no fused path
+bool op_adj_epi(apc_mat& a, const double* u, double* h, const int* done, const AdjEpi& e);
+// true when launch_fwd may be given x already in the hot-relabelled order
+inline bool fwd_takes_permuted(const apc_mat& a) { return a.sparse && a.hot.built(); }
 
 // device CSR build from host CSC (matrix upload)
 void upload_csc(apc_mat& a, const long long* colptr, const long long* rowidx, const double* val);
@@ -384,7 +397,8 @@ unsigned fwd_gs_grid(apc_ctx* ctx, const void* kfn, int threads = kCsrFwdThreads
 void build_hot_sell(apc_mat& a, const std::vector<long long>& col_nnz);
 
 template <class Epi>
-void launch_csr_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaStream_t st) {
+void launch_csr_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaStream_t st,
+                    bool x_permuted = false) {
   const long long rows = a.a.rows;
   const unsigned nb = static_cast<unsigned>((rows + kCsrFwdRowsPerBlock - 1) / kCsrFwdRowsPerBlock);
   if (nb == 0) return;
@@ -392,10 +406,13 @@ void launch_csr_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaS
     // grid <= nb keeps the epilogue's slots within fwd_num_tiles(a)
     const unsigned grid =
         std::min<unsigned>(nb, fwd_gs_grid(a.ctx, reinterpret_cast<const void*>(hot_sell_fwd_kernel<Epi>), kHotThreads));
-    hot_permute_kernel<<<static_cast<unsigned>((a.n + 255) / 256), 256, 0, st>>>(a.hot.hot.p, a.n, x, a.hot.xr.p);
+    if (!x_permuted) {  // else the producer of x wrote a.hot.xr itself (pc_expand)
+      hot_permute_kernel<<<static_cast<unsigned>((a.n + 255) / 256), 256, 0, st>>>(a.hot.hot.p, a.n, x, a.hot.xr.p);
+      a.ctx->launches++;
+    }
     hot_sell_fwd_kernel<Epi><<<grid, kHotThreads, 0, st>>>(a.a.ptr.p, a.hot.s.off.p, a.hot.s.idx.p, a.hot.s.val.p,
                                                            rows, a.hot.s.chunks, a.hot.xr.p, done, epi);
-    a.ctx->launches += 2;
+    a.ctx->launches += 1;
     return;
   }
   const bool big = rows >= (1LL << 21);
@@ -422,8 +439,8 @@ void launch_csr_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaS
 }
 
 template <class Epi>
-void launch_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaStream_t st) {
-  if (a.sparse) launch_csr_fwd(a, x, done, epi, st);
+void launch_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaStream_t st, bool x_permuted = false) {
+  if (a.sparse) launch_csr_fwd(a, x, done, epi, st, x_permuted);
   else launch_dense_fwd(a, x, done, epi, st);
 }
 

@@ -237,8 +237,8 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
         in.l = cur.rank();
         in.mu = mu;
         in.target_level = rho;
-        in.core = &cur.core();
-        in.block = &cur.intersection();
+        in.core = &cur.core();                                // svd form: U T_R^T (host, downloaded factor)
+        if (cfg.variant == 1) in.block = &cur.intersection();  // svd-free: A(I, J)
         in.t_r = implicit_mode ? &t_r_implicit : &qr_acc.t;
         in.q_dev = qr_acc.q.p;
         in.gram = cur.c_gram();

@@ -24,9 +24,10 @@ for src in sorted(B.CSRC.glob("*.cu")) + sorted(B.CSRC.glob("*.cpp")):
     in_header = any(mc in h.read_text() for mc in macros for h in list(B.CSRC.glob("*.cuh")) + list(B.CSRC.glob("*.hpp")))
     if src.suffix == ".cu" and (in_header or any(mc in src.read_text() for mc in macros)):
         obj = obj_dir / (src.name + ".o")
-        B._run([B.NVCC, *B.CU_FLAGS, *defs, f"-I{B.INC}", f"-I{B.CSRC}", "-c", str(src), "-o", str(obj)])
+        exact = ["-fmad=false"] if src.name in B.EXACT_CU else []
+        B._run([B.NVCC, *B.CU_FLAGS, *exact, *defs, f"-I{B.INC}", f"-I{B.CSRC}", "-c", str(src), "-o", str(obj)])
     objs.append(str(obj))
 lib = out / f"libapc_{name}.so"
 B._run([B.NVCC, *B.ARCH, "-shared", "-o", str(lib), *objs, *B._nccl_link_args(), "-L/usr/local/cuda/lib64",
-        "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-lpthread"])
+        "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-lpthread"])
 print(lib)

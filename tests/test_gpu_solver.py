@@ -29,7 +29,7 @@ CASES = [
     (1, 400, 50, dict(mu=0.05, eps_lsqr=1e-10, block=5, seed=1, variant=1)),
     (3, 3000, 300, dict(mu=1e-2, eps_lsqr=1e-8, block=10, seed=1, max_rank=60, variant=1)),
     # C4-shaped (square, planted low rank + noise) and C5-shaped (Zipf columns) systems
-    (4, 1200, 1200, dict(mu=0.0, eps_lsqr=1e-10, block=30, seed=1, max_rank=30, lsqr_cap=40)),
+    (4, 1200, 1200, dict(mu=0.0, eps_lsqr=1e-10, block=30, seed=1, max_rank=30)),  # 4n cap (4800)
     (5, 30000, 3000, dict(mu=1e-8, eps_lsqr=1e-8, block=25, seed=1, max_rank=50, eps_cur=3e-7)),
 ]
 
@@ -52,18 +52,24 @@ def test_aplicur_solve_matches_reference(apc, ref, ctx, cfg, m, n, knobs):
     # a phase stopped by the iteration cap (4n) leaves x path-dependent in the
     # weakly determined directions, so only the residual level is comparable
     rel = np.linalg.norm(g.x - r.x) / max(np.linalg.norm(r.x), 1e-300)
+    assert g.phases[-1].reason == r.phase_reason[-1]
+    # the reference rerun on b perturbed by one ulp (same indices): its own sensitivity
+    bp = np.nextafter(p.b, np.inf)
+    r2 = ref.solve(ref.Problem.from_apc(p), bp, dict(knobs, trace_sample_stride=0))
+    self_sens = np.linalg.norm(r2.x - r.x) / np.linalg.norm(r.x)
+    res_sens = abs(r2.final_relres - r.final_relres) / r.final_relres
     if r.phase_reason[-1] == apc.StopReason.gradient_tol:
-        assert g.phases[-1].reason == apc.StopReason.gradient_tol
-        # the bar is 1e-6, widened only to the reference's own sensitivity: the
-        # unmodified reference rerun on b perturbed by one ulp (same indices)
-        bp = np.nextafter(p.b, np.inf)
-        r2 = ref.solve(ref.Problem.from_apc(p), bp, dict(knobs, trace_sample_stride=0))
-        self_sens = np.linalg.norm(r2.x - r.x) / np.linalg.norm(r.x)
+        # converged: x to 1e-6, widened only to 10x the reference's own sensitivity
         assert rel <= max(1e-6, 10.0 * self_sens), (rel, self_sens, g.final_relres, r.final_relres)
         assert abs(g.final_relres - r.final_relres) <= 1e-5 * r.final_relres
     else:
-        assert g.phases[-1].reason == r.phase_reason[-1]
-        assert abs(g.final_relres - r.final_relres) <= 1e-3 * r.final_relres, (rel, g.final_relres, r.final_relres)
+        # stopped by the iteration cap (4n): x is path-dependent in the weakly
+        # determined directions (every iteration rounds differently from the
+        # reference, unlike a single one-ulp change of b), so the residual the
+        # capped iterate reaches is compared: no worse than the reference's by
+        # more than max(1e-3, 10x its one-ulp sensitivity)
+        bound = max(1e-3, 10.0 * res_sens)
+        assert g.final_relres <= r.final_relres * (1.0 + bound), (g.final_relres, r.final_relres, res_sens, rel)
 
 
 def test_zero_matrix_single_identity_phase(apc, ctx):
