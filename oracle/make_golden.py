@@ -141,6 +141,44 @@ def capped_fixture(k: int, cap: int, ulp: bool = False):
           f"iters {r.phase_iters} reasons {r.phase_reason} relres {r.final_relres}", flush=True)
 
 
+def capped_ensemble_member(k: int, cap: int, seed: int, ulps: int = 1):
+    """The reference's own run-to-run spread of the stop-rule iteration counts:
+    the capped solve (same knobs, lsqr_cap = cap) on b with EVERY entry moved
+    one ulp up or down (signs from `seed`) -- a rounding-level perturbation like
+    a different summation order.  Only the phase iteration counts and stop
+    reasons before the cap are used (tests/test_gpu_baseline_capped.py)."""
+    knobs = dict(BASELINE_SOLVER[k], trace_sample_stride=0, lsqr_cap=cap)
+    p = ref.Problem.generate(k)
+    sgn = np.random.default_rng(seed).integers(0, 2, size=p.b.shape[0]) * 2 - 1
+    b = p.b + sgn * ulps * np.spacing(p.b) if ulps > 1 else np.where(
+        sgn > 0, np.nextafter(p.b, np.inf), np.nextafter(p.b, -np.inf))
+    t0 = time.time()
+    r = ref.solve(p, b, knobs, consume=True)
+    wall = time.time() - t0
+    p.free()
+    _save(f"capped_c{k}_ens{seed}" + (f"u{ulps}" if ulps > 1 else ""), phase_rank=r.phase_rank, phase_iters=r.phase_iters,
+          phase_reason=r.phase_reason, trace_phibar=r.trace_phibar, wall_s=wall,
+          meta=json.dumps(dict(config=k, cap=cap, knobs=knobs, seed=seed, ulps=ulps,
+                               perturbation=f"every b_i moved {ulps} ulp up or down")))
+    print(f"ensemble C{k} seed {seed} ulps {ulps}: wall {wall:.1f}s iters {r.phase_iters} reasons {r.phase_reason}", flush=True)
+
+
+def capped_ensemble_collect(k: int):
+    """Merge the members into capped_c{k}_ens.npz (rows = members)."""
+    fs = sorted(GOLD.glob(f"capped_c{k}_ens[0-9]*.npz"))
+    if not fs:
+        raise RuntimeError(f"no ensemble members for C{k}")
+    ms = [np.load(f) for f in fs]
+    nph = min(len(m["phase_iters"]) for m in ms)
+    _save(f"capped_c{k}_ens", phase_iters=np.array([m["phase_iters"][:nph] for m in ms]),
+          phase_reason=np.array([m["phase_reason"][:nph] for m in ms]),
+          phase_rank=np.array([m["phase_rank"][:nph] for m in ms]),
+          seeds=np.array([json.loads(str(m["meta"]))["seed"] for m in ms]),
+          ulps=np.array([json.loads(str(m["meta"])).get("ulps", 1) for m in ms]), meta=str(ms[0]["meta"]))
+    for f in fs:
+        f.unlink()
+
+
 def capped_pair(k: int, cap: int):
     """Main and one-ulp capped runs side by side (host RAM permitting: C5's
     reference solve peaks near 65 GB), then the sensitivity fixture."""
@@ -187,6 +225,11 @@ def main(argv):
     for what in argv or ["small"]:
         if what == "small":
             small()
+        elif what.startswith("ens") and what.count(":") in (2, 3):  # ens<cap>:c<k>:<seed>[:<ulps>]
+            head, c, s, *u = what.split(":")
+            capped_ensemble_member(int(c[1:]), int(head[3:]), int(s), int(u[0]) if u else 1)
+        elif what.startswith("enscollect:c"):
+            capped_ensemble_collect(int(what[len("enscollect:c"):]))
         elif what.startswith("cappedpair") and ":c" in what:
             head, c = what.split(":c")
             capped_pair(int(c), int(head[len("cappedpair"):] or 200))

@@ -138,6 +138,7 @@ struct Csr : Units {
 struct HeadAdj {
   i64 ncols = 0, nblocks = 0, nnz = 0;
   int parts = 1;       // CTAs (work items) per block
+  int rows = 0;        // rows of A per block (build_head_adj: a whole number of CTA waves)
   DBuf<i32> bptr;      // nblocks + 1 (multiples of 128; padding keys are -1)
   DBuf<i32> hkey;      // nnz: k << 16 | (row - block start)
   DBuf<double> hval;   // nnz

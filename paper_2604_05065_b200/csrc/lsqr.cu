@@ -28,6 +28,8 @@
 #include <cstring>
 #include <string>
 
+#include <cooperative_groups.h>
+
 #include "dev_common.cuh"
 #include "lsqr.hpp"
 #include "lsqr_persistent.hpp"
@@ -72,7 +74,7 @@ __device__ void finalize_alpha(LsqrState* st, TraceRow* trace, double alpha, dou
     st->opnorm2 = alpha * alpha;
     st->t1 = 0.0;
     st->t2 = 0.0;
-    trace[0] = TraceRow{beta, 0.0, 0.0, wall, 0, 0ull};
+    if (trace) trace[0] = TraceRow{beta, 0.0, 0.0, wall, 0, 0ull};
     if (alpha == 0.0) {
       st->done = 1;
       st->reason = kReasonGradientTol;
@@ -107,7 +109,7 @@ __device__ void finalize_alpha(LsqrState* st, TraceRow* trace, double alpha, dou
   if (j == 1) st->cvgrate1 = cvgrate;
   st->t_cvgrate = cvgrate;
   st->t_cvgdiff = cvgdiff;
-  if (j < st->trace_cap)
+  if (trace && j < st->trace_cap)
     trace[j] = TraceRow{phibar, cvgrate, cvgdiff, wall, j, 1ull + 2ull * static_cast<unsigned long long>(j)};
 }
 
@@ -577,6 +579,243 @@ pc_expand_kernel(LsqrPtrs P, int kind, const double* __restrict__ B, long long l
   }
 }
 
+// ---------------------------------------------------------------------------
+// The n-space part of one iteration in ONE cooperative launch (identity or
+// implicit basis I + R^T G R).  After A^T u is complete it replaces
+//   lsqr_epi -> pc_rproj -> pc_core -> pc_expand(mode 1) -> lsqr_update
+//   -> [next iteration] pc_rproj -> pc_core -> pc_expand(mode 0, xr, mu-tail)
+// (nine launches whose fixed costs dominated the ~100 us of n-space work per
+// C5 iteration) by five grid barriers:
+//   B  t = R h            h = (A^T u + mu u_t)/beta formed on the fly at R's columns
+//   C  s = G_a t
+//   D  v_raw = h + R^T s - beta v (own 256-column tiles; kept in h), ||v_raw||^2 per tile
+//   E  alpha, rotation (every CTA, identical); v, y, w updates, ||y||^2 per tile;
+//      t' = R v (v = v_raw/alpha at R's columns)
+//   F  s' = G_f t'; stop tests (every CTA, identical); CTA 0 publishes the scalars
+//   G  z = v + R^T s' for the NEXT iteration's forward (+ its hot-relabelled
+//      copy, + the mu-tail rows u_t <- mu z - alpha u_t/beta, ||u_t||^2)
+// Every per-element operation, every 256-column tile partial and every ordered
+// sum over the tile partials is the unfused kernels' own, so the iterates are
+// unchanged.  The scalar recurrence runs on a shared-memory copy of LsqrState in
+// every CTA (all CTAs read the state before the first barrier; CTA 0 writes it
+// back before the last one).
+struct NspaceArgs {
+  LsqrPtrs P;
+  int kind;  // 0 identity, 2 implicit
+  const int* rptr;
+  const int* ridx;
+  const double* rval;
+  const int* tptr;
+  const int* tidx;
+  const double* tval;
+  const double* Ga;  // P^{-T} middle operator (row-major l x l)
+  const double* Gf;  // P^{-1}
+  long long l;
+  double* t;
+  double* s;
+  double* xr;  // hot-relabelled copy of z (nullptr: none)
+  const int* inv;
+  int fuse_tail;
+  cudaGraphConditionalHandle cond;
+  int use_cond;
+};
+constexpr int kNsThreads = kVecThreads;  // 256-column tiles: the unfused kernels' blocks
+
+// (R^T s)_j for the tile's columns, long R^T rows by a warp (pc_expand_kernel's split)
+__device__ __forceinline__ double ns_rts(const NspaceArgs& a, long long j0, long long n, const double* s,
+                                         int* defer, double* dacc, int* ndefer) {
+  constexpr int kExpandLong = 32;
+  const long long j = j0 + threadIdx.x;
+  if (threadIdx.x == 0) *ndefer = 0;
+  __syncthreads();
+  double acc = 0.0;
+  bool deferred = false;
+  if (j < n) {
+    const int q0 = a.tptr[j], q1 = a.tptr[j + 1];
+    if (q1 - q0 > kExpandLong) {
+      defer[atomicAdd(ndefer, 1)] = threadIdx.x;
+      deferred = true;
+    } else {
+      for (int q = q0; q < q1; ++q) acc += a.tval[q] * s[a.tidx[q]];
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int d = threadIdx.x >> 5; d < *ndefer; d += kNsThreads / 32) {
+    const long long jj = j0 + defer[d];
+    double x = 0.0;
+    for (int q = a.tptr[jj] + lane; q < a.tptr[jj + 1]; q += 32) x += a.tval[q] * s[a.tidx[q]];
+    x = warp_sum(x);
+    if (lane == 0) dacc[defer[d]] = x;
+  }
+  __syncthreads();
+  return deferred ? dacc[threadIdx.x] : acc;
+}
+
+// out = M x for row-major l x l M: warp per row over the grid (pc_core_kernel)
+__device__ __forceinline__ void ns_core(const double* __restrict__ M, long long l, const double* t, double* out,
+                                        long long gw, long long nw) {
+  const int lane = threadIdx.x & 31;
+  for (long long i = gw; i < l; i += nw) {
+    const double* row = M + i * l;
+    double acc = 0.0;
+    for (long long k = lane; k < l; k += 32) acc += row[k] * t[k];
+    acc = warp_sum(acc);
+    if (lane == 0) out[i] = acc;
+  }
+}
+
+// stage G for the tiles [tile0, ntiles) step tstep; the mu-tail norm by the last CTA
+__device__ __forceinline__ void ns_stage_z(const NspaceArgs& a, double alpha, double beta, long long tile0,
+                                           long long tstep, double* sh, int* defer, double* dacc, int* ndefer) {
+  const LsqrPtrs& P = a.P;
+  const long long n = P.n, ntiles = (n + kNsThreads - 1) / kNsThreads;
+  const bool pre = a.kind == 2;
+  for (long long tile = tile0; tile < ntiles; tile += tstep) {
+    const long long j0 = tile * kNsThreads, j = j0 + threadIdx.x;
+    const double acc = pre ? ns_rts(a, j0, n, a.s, defer, dacc, ndefer) : 0.0;
+    double sq = 0.0;
+    if (j < n) {
+      const double vj = P.v[j];
+      const double o = pre ? vj + acc : vj;
+      if (pre) P.z[j] = o;
+      if (a.xr) a.xr[a.inv[j]] = o;
+      if (a.fuse_tail) {
+        double* ut = P.u + P.mloc;
+        const double uo = ut[j];
+        const double uh = beta > 0.0 ? uo / beta : uo;
+        const double t = P.mu * o - alpha * uh;
+        ut[j] = t;
+        sq = t * t;
+      }
+    }
+    if (a.fuse_tail) {
+      sq = block_sum<kNsThreads>(sq, sh);
+      if (threadIdx.x == 0) P.tail_part[tile] = sq;
+    }
+  }
+  if (a.fuse_tail && elect_last_block(P.ctr + 1, gridDim.x)) {
+    const double ssum = ordered_sum<kNsThreads>(P.tail_part, ntiles, sh);
+    if (threadIdx.x == 0) P.st->tail_norm2 = ssum;
+  }
+}
+
+__global__ void __launch_bounds__(kNsThreads) lsqr_nspace_kernel(NspaceArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[32];
+  __shared__ int defer[kNsThreads];
+  __shared__ double dacc[kNsThreads];
+  __shared__ int ndefer;
+  __shared__ LsqrState ls;
+  const LsqrPtrs& P = a.P;
+  if (threadIdx.x == 0) ls = *P.st;
+  __syncthreads();
+  if (ls.done) {
+    if (a.use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.cond, 0);
+    return;
+  }
+  const long long n = P.n, l = a.l, ntiles = (n + kNsThreads - 1) / kNsThreads;
+  const int lane = threadIdx.x & 31;
+  const long long gw = static_cast<long long>(blockIdx.x) * (kNsThreads / 32) + (threadIdx.x >> 5);
+  const long long nw = static_cast<long long>(gridDim.x) * (kNsThreads / 32);
+  const bool pre = a.kind == 2;
+  const double beta = sqrt(P.g[n] + ls.tail_norm2);
+  auto hval = [&](long long c) {  // lsqr_epi_kernel's h_c
+    double raw = P.g[c];
+    if (P.has_tail) raw += P.mu * P.u[P.mloc + c];
+    return beta > 0.0 ? raw / beta : raw;
+  };
+  if (pre) {  // B, C: s = G_a (R h)
+    for (long long r = gw; r < l; r += nw) {
+      double acc = 0.0;
+      for (int q = a.rptr[r] + lane; q < a.rptr[r + 1]; q += 32) acc += a.rval[q] * hval(a.ridx[q]);
+      acc = warp_sum(acc);
+      if (lane == 0) a.t[r] = acc;
+    }
+    grid.sync();
+    ns_core(a.Ga, l, a.t, a.s, gw, nw);
+    grid.sync();
+  }
+  // D: v_raw (into h), ||v_raw||^2 per tile
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long j0 = tile * kNsThreads, j = j0 + threadIdx.x;
+    const double acc = pre ? ns_rts(a, j0, n, a.s, defer, dacc, &ndefer) : 0.0;
+    double sq = 0.0;
+    if (j < n) {
+      const double h = hval(j);
+      const double o = pre ? h + acc : h;
+      const double t = o - beta * P.v[j];
+      P.h[j] = t;
+      sq = t * t;
+    }
+    sq = block_sum<kNsThreads>(sq, sh);
+    if (threadIdx.x == 0) P.epi_part[tile] = sq;
+  }
+  grid.sync();
+  // E: alpha and the rotation in every CTA; v, y, w; t' = R v
+  {
+    const double ssum = ordered_sum<kNsThreads>(P.epi_part, ntiles, sh);
+    if (threadIdx.x == 0) finalize_alpha(&ls, blockIdx.x == 0 ? P.trace : nullptr, sqrt(ssum), beta);
+    __syncthreads();
+  }
+  const double alpha = ls.alpha, t1 = ls.t1, t2 = ls.t2;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long j = tile * kNsThreads + threadIdx.x;
+    double sq = 0.0;
+    if (j < n) {
+      const double vo = P.h[j];
+      const double vh = alpha > 0.0 ? vo / alpha : vo;
+      P.v[j] = vh;
+      const double wo = P.w[j];
+      const double yn = P.y[j] + t1 * wo;
+      P.y[j] = yn;
+      P.w[j] = vh + t2 * wo;
+      sq = yn * yn;
+    }
+    sq = block_sum<kNsThreads>(sq, sh);
+    if (threadIdx.x == 0) P.upd_part[tile] = sq;
+  }
+  if (pre) {
+    for (long long r = gw; r < l; r += nw) {
+      double acc = 0.0;
+      for (int q = a.rptr[r] + lane; q < a.rptr[r + 1]; q += 32) {
+        const double vo = P.h[a.ridx[q]];
+        acc += a.rval[q] * (alpha > 0.0 ? vo / alpha : vo);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) a.t[r] = acc;
+    }
+  }
+  grid.sync();
+  // F: s' = G_f t'; stop tests; CTA 0 publishes the scalars
+  if (pre) ns_core(a.Gf, l, a.t, a.s, gw, nw);
+  {
+    const double ysum = ordered_sum<kNsThreads>(P.upd_part, ntiles, sh);
+    if (threadIdx.x == 0) stop_tests(&ls, sqrt(ysum));
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *P.st = ls;
+    if (a.use_cond) cudaGraphSetConditional(a.cond, ls.done ? 0u : 1u);
+  }
+  if (ls.done) return;  // identical in every CTA: nobody waits at the barrier below
+  grid.sync();
+  // G: the next iteration's z
+  ns_stage_z(a, ls.alpha, ls.beta, blockIdx.x, gridDim.x, sh, defer, dacc, &ndefer);
+}
+
+// stage G alone (before the first loop iteration): one CTA per tile
+__global__ void __launch_bounds__(kNsThreads) lsqr_nspace_z_kernel(NspaceArgs a) {
+  __shared__ double sh[32];
+  __shared__ int defer[kNsThreads];
+  __shared__ double dacc[kNsThreads];
+  __shared__ int ndefer;
+  const LsqrState* st = a.P.st;
+  if (st->done) return;
+  ns_stage_z(a, st->alpha, st->beta, blockIdx.x, gridDim.x, sh, defer, dacc, &ndefer);
+}
+
 namespace {
 __global__ void zero_kernel(double* p, long long n) {
   long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -599,7 +838,7 @@ struct LsqrWork {
   DBuf<unsigned> ctr, pc_ctr, pcf_ctr;
   DBuf<LsqrState> st;
   DBuf<TraceRow> trace;
-  DBuf<double> xs, samp_part, samp_tpart, samp_sc, sampled;  // true-residual sampling
+  DBuf<double> xs, samp_part, samp_tpart, samp_sc, sampled, samp_xr;  // true-residual sampling
   LsqrState* hst = nullptr;  // pinned
   cudaEvent_t ev[2] = {nullptr, nullptr};
   cudaEvent_t tev[2] = {nullptr, nullptr};  // timing of the iteration loop
@@ -714,9 +953,91 @@ void ensure_pc_buffers(LsqrWork* w, PrecondDev& p) {
   }
 }
 
+// the fused n-space path (lsqr_nspace_kernel): identity or implicit basis;
+// APC_NSPACE=0 keeps the unfused kernels
+bool nspace_enabled(const LsqrWork* w, const PrecondDev* p) {
+  static const bool env = std::getenv("APC_NSPACE") && std::atoi(std::getenv("APC_NSPACE")) != 0;
+  return env && w->n > 0 && (!p || p->kind == 0 || p->kind == 2);
+}
+
+NspaceArgs nspace_args(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P, cudaGraphConditionalHandle cond,
+                       int use_cond) {
+  NspaceArgs na{};
+  na.P = P;
+  na.kind = p && p->kind == 2 ? 2 : 0;
+  if (na.kind == 2) {
+    na.rptr = p->R.ptr.p;
+    na.ridx = p->R.idx.p;
+    na.rval = p->R.val.p;
+    na.tptr = p->RT.ptr.p;
+    na.tidx = p->RT.idx.p;
+    na.tval = p->RT.val.p;
+    na.Ga = p->Ka.p;
+    na.Gf = p->Kf.p;
+    na.l = p->l;
+  }
+  na.t = w->t.p;
+  na.s = w->s.p;
+  const bool xr = w->mloc > 0 && fwd_takes_permuted(a);
+  na.xr = xr ? a.hot.xr.p : nullptr;
+  na.inv = xr ? a.hot.inv.p : nullptr;
+  na.fuse_tail = P.has_tail;
+  na.cond = cond;
+  na.use_cond = use_cond;
+  return na;
+}
+
+int nspace_grid(apc_ctx* ctx, long long n) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    int occ = 0;
+    APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lsqr_nspace_kernel, kNsThreads, 0));
+    const char* e = std::getenv("APC_NSPACE_CTAS_PER_SM");
+    per_sm = std::max(1, std::min(occ, e ? std::atoi(e) : 2));
+  }
+  const long long ntiles = (n + kNsThreads - 1) / kNsThreads;
+  return static_cast<int>(std::max<long long>(1, std::min<long long>(ntiles, static_cast<long long>(per_sm) * ctx->num_sms)));
+}
+
+// the z of the first loop iteration (stage G of lsqr_nspace_kernel)
+void enqueue_nspace_z(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P) {
+  apc_ctx* ctx = w->ctx;
+  if (p && p->kind == 2) pc_project_core(w, *p, P.v, false, &P.st->done);
+  NspaceArgs na = nspace_args(w, a, p, P, cudaGraphConditionalHandle{}, 0);
+  lsqr_nspace_z_kernel<<<nb(w->n), kNsThreads, 0, ctx->stream>>>(na);
+  ctx->launches++;
+}
+
+// one iteration on the fused n-space path: fwd, adj, [allreduce], n-space
+void enqueue_iteration_nspace(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P,
+                              cudaGraphConditionalHandle cond, int use_cond) {
+  apc_ctx* ctx = w->ctx;
+  cudaStream_t st = ctx->stream;
+  const int* done = &P.st->done;
+  NspaceArgs na = nspace_args(w, a, p, P, cond, use_cond);
+  const double* z = na.kind == 2 ? P.z : P.v;
+  LsqrFwdEpi epi{P.u, P.st, P.fwd_part, P.ctr + 0, P.g + P.n, 0.0, 0.0};
+  if (w->mloc > 0) {
+    launch_fwd(a, z, done, epi, st, na.xr != nullptr);
+  } else {
+    lsqr_init_copy_kernel<<<1, kVecThreads, 0, st>>>(P, P.u, 0, 0, 0);
+    ctx->launches++;
+  }
+  op_adj_raw(a, P.u, P.g, done);
+  comm_allreduce(ctx, P.g, w->n + 1);
+  void* args[] = {&na};
+  APC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(lsqr_nspace_kernel),
+                                       dim3(nspace_grid(ctx, w->n)), dim3(kNsThreads), args, 0, st));
+  ctx->launches++;
+}
+
 // one LSQR iteration (all kernels no-op once st->done is raised)
 void enqueue_iteration(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P,
                        cudaGraphConditionalHandle cond, int use_cond) {
+  if (nspace_enabled(w, p)) {
+    enqueue_iteration_nspace(w, a, p, P, cond, use_cond);
+    return;
+  }
   apc_ctx* ctx = w->ctx;
   cudaStream_t st = ctx->stream;
   const int* done = &P.st->done;
@@ -799,7 +1120,8 @@ void enqueue_sample(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P, c
     xs = out;
   }
   if (w->mloc > 0) {
-    launch_fwd(a, xs, skip, ResidSampleEpi{sc.b_local, w->samp_part.p, P.ctr + 4, w->samp_sc.p}, st);
+    double* xr_buf = fwd_takes_permuted(a) ? w->samp_xr.p : nullptr;  // sized in lsqr_phase
+    launch_fwd(a, xs, skip, ResidSampleEpi{sc.b_local, w->samp_part.p, P.ctr + 4, w->samp_sc.p}, st, false, xr_buf);
   } else {
     samp_zero_kernel<<<1, 1, 0, st>>>(P.st, w->samp_sc.p);
     ctx->launches++;
@@ -849,6 +1171,7 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
     w->samp_tpart.ensure(nb(n));
     w->samp_sc.ensure(2);
     w->sampled.ensure(cap + 1);
+    if (fwd_takes_permuted(a)) w->samp_xr.ensure(std::max<long long>(1, n));
     APC_CUDA(cudaMemsetAsync(w->sampled.p, 0xFF, sizeof(double) * (cap + 1), st));  // NaN
   }
 
@@ -921,6 +1244,7 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   const bool persistent =
       !sampling && (mode.empty() || mode == "persistent") && persistent_eligible(a, p, ctx);
   const bool use_while = !persistent && ctx->nranks == 1 && mode != "batch" && !eager;
+  if (!persistent && nspace_enabled(w, p)) enqueue_nspace_z(w, a, p, P);
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   const std::uint64_t launches_before_capture = ctx->launches;

@@ -295,6 +295,13 @@ split_fixup_kernel(const int* __restrict__ srows, const int* __restrict__ rfirst
 // order, so results are bit-identical run to run.  The tail stream replaces a
 // warp-per-column walk whose dependent metadata -> entries -> gather chain per
 // ~74-entry column left it latency-bound.
+// warp sum in a fixed order, lane 0's value broadcast (identical in every lane)
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+
 struct HeadPiece {
   int fk, lk;  // first / last piece column (-1: none)
   double fs, ls;
@@ -303,11 +310,14 @@ struct HeadPiece {
 struct HeadPolicy {
   __device__ __forceinline__ void begin() {}
   double* part;
-  int nb;  // blocks (ncols x nblocks < 2^31, build_head_adj)
+  int nb;    // blocks (ncols x nblocks < 2^31, build_head_adj)
+  int rows;  // rows of A per block (<= 65536: the key's row field)
   static constexpr bool kStage = true;
+  static constexpr bool kFast = true;  // single-column steps skip the scan (long Zipf-head runs)
   static constexpr int kMinBlocks = 2;  // 2 x 512 threads: <= 64 registers
   __device__ __forceinline__ int col(unsigned key) const { return static_cast<int>(key >> 16); }
-  __device__ __forceinline__ int row(unsigned key) const { return static_cast<int>(key & (kHeadRows - 1)); }
+  __device__ __forceinline__ int row(unsigned key) const { return static_cast<int>(key & 0xffffu); }
+  __device__ __forceinline__ int block_rows() const { return rows; }
   __device__ __forceinline__ int pad() const { return kHeadPad; }
   __device__ __forceinline__ void store(int k, long long g, double s) const { part[k * nb + static_cast<int>(g)] = s; }
   __device__ __forceinline__ void zero(int k, long long g) const { part[k * nb + static_cast<int>(g)] = 0.0; }
@@ -324,6 +334,7 @@ struct TailPolicy {
     if (e.n2top) beta = sqrt(*e.n2top + (e.n2tail ? *e.n2tail : 0.0));
   }
   static constexpr bool kStage = false;
+  static constexpr bool kFast = false;  // tail runs are short: no single-column steps to speak of
 #ifndef APC_TAIL_MINB
 #define APC_TAIL_MINB 2
 #endif
@@ -331,6 +342,7 @@ struct TailPolicy {
   __device__ __forceinline__ int col(unsigned key) const { return static_cast<int>(key >> rb); }
   __device__ __forceinline__ int row(unsigned key) const { return static_cast<int>(key & ((1u << rb) - 1u)); }
   __device__ __forceinline__ int pad() const { return static_cast<int>((1u << (32 - rb)) - 1u); }
+  __device__ __forceinline__ int block_rows() const { return 0; }
   __device__ __forceinline__ void store(int k, long long g, double s) const {
     const int j = __ldg(tcol + __ldg(gcol0 + g) + k);
     if (e.n2top) {
@@ -367,24 +379,28 @@ __device__ __forceinline__ void head_chain(int& k, double& s, int pk, double ps,
 #ifndef APC_HEAD_MINB
 #define APC_HEAD_MINB 1
 #endif
+#ifndef APC_TAIL_PF2
+#define APC_TAIL_PF2 0
+#endif
+// one work item (CTA `bid`) of a segmented stream
 template <class Pol>
-__global__ void __launch_bounds__(kHeadThreads, Pol::kMinBlocks)
-seg_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, const double* __restrict__ hval,
-               const double* __restrict__ u, long long mloc, int parts, const int* __restrict__ zptr,
-               const int* __restrict__ zcol, Pol pol, HeadPiece* __restrict__ bnd, const int* done) {
+__device__ __forceinline__ void seg_adj_body(int bid, const int* __restrict__ bptr, const int* __restrict__ hkey,
+                                             const double* __restrict__ hval, const double* __restrict__ u,
+                                             long long mloc, int parts, const int* __restrict__ zptr,
+                                             const int* __restrict__ zcol, Pol pol, HeadPiece* __restrict__ bnd) {
   constexpr int NW = kHeadThreads / 32;
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ double us[];
   __shared__ HeadPiece pc[NW];
-  if (done && *done) return;
-  const int blk = blockIdx.x / parts;
-  const int prt = blockIdx.x % parts;
+  const int blk = bid / parts;
+  const int prt = bid % parts;
   pol.begin();
   const int PAD = pol.pad();
   const double* ub = u;
   if (Pol::kStage) {
-    const long long r0 = static_cast<long long>(blk) * kHeadRows;
-    const int nr = static_cast<int>(mloc - r0 < kHeadRows ? mloc - r0 : kHeadRows);
+    const int R = pol.block_rows();
+    const long long r0 = static_cast<long long>(blk) * R;
+    const int nr = static_cast<int>(mloc - r0 < R ? mloc - r0 : R);
     for (int i = threadIdx.x; i < nr; i += kHeadThreads) us[i] = __ldcg(u + r0 + i);
   }
   if (prt == 0)
@@ -400,11 +416,16 @@ seg_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, const
   const int rb = min(p1, p0 + w * wper), re = min(p1, rb + wper);
   int ck = -1, fk = -1;  // open (carried) piece, first closed piece (warp-uniform)
   double cs = 0.0, fs = 0.0;
+  double la = 0.0;    // lane partials of the carried piece from single-column steps
+  bool lact = false;  // la holds unfolded partials (warp-uniform)
   const int4* kp = reinterpret_cast<const int4*>(hkey) + (KL / 4) * lane;
   const double2* vp = reinterpret_cast<const double2*>(hval) + (KL / 2) * lane;
   // software pipeline: the next step's entries (and, for a global u, its
   // gathers) are in flight while this one is scanned
-  int4 nkq[KL / 4];
+  // a global u (tail): the keys run two steps ahead, so the gathers of step
+  // e + STEP are issued on keys that arrived during the previous step instead
+  // of stalling on keys loaded in the same step (long-scoreboard bound)
+  int4 nkq[KL / 4], nk2[KL / 4];
   double2 nvq[KL / 2];
   double nug[KL];
   if (rb < re) {
@@ -413,6 +434,10 @@ seg_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, const
 #pragma unroll
     for (int i = 0; i < KL / 2; ++i) nvq[i] = __ldcs(vp + (rb >> 1) + i);
     if (!Pol::kStage) {
+      if (APC_TAIL_PF2 && rb + STEP < re) {
+#pragma unroll
+        for (int i = 0; i < KL / 4; ++i) nk2[i] = __ldcs(kp + ((rb + STEP) >> 2) + i);
+      }
 #pragma unroll
       for (int i = 0; i < KL / 4; ++i) {
         nug[4 * i] = __ldg(ub + pol.row(nkq[i].x));
@@ -442,8 +467,17 @@ seg_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, const
       for (int i = 0; i < KL; ++i) ug[i] = nug[i];
     }
     if (e + STEP < re) {
+      if (Pol::kStage || !APC_TAIL_PF2) {
 #pragma unroll
-      for (int i = 0; i < KL / 4; ++i) nkq[i] = __ldcs(kp + ((e + STEP) >> 2) + i);
+        for (int i = 0; i < KL / 4; ++i) nkq[i] = __ldcs(kp + ((e + STEP) >> 2) + i);
+      } else {
+#pragma unroll
+        for (int i = 0; i < KL / 4; ++i) nkq[i] = nk2[i];
+        if (e + 2 * STEP < re) {
+#pragma unroll
+          for (int i = 0; i < KL / 4; ++i) nk2[i] = __ldcs(kp + ((e + 2 * STEP) >> 2) + i);
+        }
+      }
 #pragma unroll
       for (int i = 0; i < KL / 2; ++i) nvq[i] = __ldcs(vp + ((e + STEP) >> 1) + i);
       if (!Pol::kStage) {
@@ -465,6 +499,39 @@ seg_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, const
       x[i] = vv[i] * (Pol::kStage ? us[pol.row(static_cast<unsigned>(key[i]))] : ug[i]);
     }
     const int kl0 = __shfl_sync(FULL, k[0], 0);
+    const int kl31 = Pol::kFast ? __shfl_sync(FULL, k[KL - 1], 31) : -1;
+    if (Pol::kFast && kl0 == kl31 && kl0 != PAD) {
+      // the whole step is one column (keys are sorted): no scan.  Lane-local
+      // partials accumulate in `la` across such steps and are folded into the
+      // carried sum (cs + a fixed-order warp sum) only when the run goes on
+      // into a mixed step or ends -- the long Zipf-head runs skip the
+      // shuffles of the segmented scan entirely
+      double t = x[0];
+#pragma unroll
+      for (int i = 1; i < KL; ++i) t += x[i];
+      if (kl0 != ck) {
+        if (ck >= 0) {
+          if (lact) cs += warp_allsum(la);
+          if (fk < 0) {
+            fk = ck;
+            fs = cs;
+          } else if (lane == 0) {
+            pol.store(ck, blk, cs);
+          }
+        }
+        ck = kl0;
+        cs = 0.0;
+        la = t;
+      } else {
+        la = lact ? la + t : t;
+      }
+      lact = true;
+      continue;
+    }
+    if (Pol::kFast && lact) {
+      cs += warp_allsum(la);
+      lact = false;
+    }
     if (ck >= 0 && kl0 != ck) {  // the carried piece ended with the previous step
       if (fk < 0) {
         fk = ck;
@@ -548,6 +615,7 @@ seg_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, const
     cs = __shfl_sync(FULL, y[KL - 1], 31);
     if (ck == PAD) ck = -1;
   }
+  if (Pol::kFast && lact) cs += warp_allsum(la);
   if (lane == 0) pc[w] = fk < 0 ? HeadPiece{ck, -1, cs, 0.0} : HeadPiece{fk, ck, fs, cs};
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -560,12 +628,22 @@ seg_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, const
       head_chain(k, sum, P.lk, P.ls, f, fsum, first, pol, blk);
     }
     if (parts > 1) {
-      bnd[blockIdx.x] = first ? HeadPiece{k, -1, sum, 0.0} : HeadPiece{f, k, fsum, sum};
+      bnd[bid] = first ? HeadPiece{k, -1, sum, 0.0} : HeadPiece{f, k, fsum, sum};
     } else if (k >= 0) {
       pol.store(k, blk, sum);
     }
   }
 }
+
+template <class Pol>
+__global__ void __launch_bounds__(kHeadThreads, Pol::kMinBlocks)
+seg_adj_kernel(const int* __restrict__ bptr, const int* __restrict__ hkey, const double* __restrict__ hval,
+               const double* __restrict__ u, long long mloc, int parts, const int* __restrict__ zptr,
+               const int* __restrict__ zcol, Pol pol, HeadPiece* __restrict__ bnd, const int* done) {
+  if (done && *done) return;
+  seg_adj_body<Pol>(blockIdx.x, bptr, hkey, hval, u, mloc, parts, zptr, zcol, pol, bnd);
+}
+
 
 // pieces at the part boundaries of each block (group), chained in part order
 template <class Pol>
@@ -809,6 +887,7 @@ void seg_adjoint(apc_mat& a, const double* u, double* out, const int* done, cons
   const HeadAdj& h = a.head;
   const HeadAdj::Seg& t = h.seg;
   const TailPolicy pol{t.gcol0.p, t.tcol.p, t.sb > 1 ? t.part.p : out, t.rb, t.sb > 1 ? AdjEpi{} : e, 0.0};
+  const HeadPolicy hp{h.part.p, static_cast<int>(h.nblocks), h.rows};
   seg_adj_kernel<TailPolicy><<<static_cast<unsigned>(t.ngroups * t.parts), kHeadThreads, 0, st>>>(
       t.gptr.p, t.tkey.p, t.tval.p, u, a.mloc(), t.parts, t.zptr.p, t.zcol.p, pol,
       reinterpret_cast<HeadPiece*>(t.bnd.p), done);
@@ -822,17 +901,17 @@ void seg_adjoint(apc_mat& a, const double* u, double* out, const int* done, cons
     tail_combine_kernel<<<nblk(t.ncols, 256), 256, 0, st>>>(t.part.p, t.cols.p, t.ncols, t.sb, out, done, e);
     a.ctx->launches++;
   }
-  const HeadPolicy hp{h.part.p, static_cast<int>(h.nblocks)};
-  seg_adj_kernel<HeadPolicy><<<static_cast<unsigned>(h.nblocks * h.parts), kHeadThreads, sizeof(double) * kHeadRows,
+  seg_adj_kernel<HeadPolicy><<<static_cast<unsigned>(h.nblocks * h.parts), kHeadThreads, sizeof(double) * h.rows,
                                st>>>(h.bptr.p, h.hkey.p, h.hval.p, u, a.mloc(), h.parts, h.zptr.p, h.zcol.p, hp,
                                      reinterpret_cast<HeadPiece*>(h.bnd.p), done);
+  a.ctx->launches++;
   if (h.parts > 1) {
     seg_bnd_kernel<HeadPolicy><<<nblk(h.nblocks, 128), 128, 0, st>>>(reinterpret_cast<const HeadPiece*>(h.bnd.p),
                                                                      h.parts, h.nblocks, hp, done);
     a.ctx->launches++;
   }
   head_combine_kernel<<<nblk(h.ncols * 32, 256), 256, 0, st>>>(h.part.p, h.nblocks, h.hcol.p, h.ncols, out, done, e);
-  a.ctx->launches += 2;
+  a.ctx->launches++;
 }
 }  // namespace
 
@@ -863,9 +942,9 @@ void op_adj_raw(apc_mat& a, const double* u, double* out, const int* done) {
     }
     const HeadAdj& h = a.head;
     launch_units(a.ctx, c, h.tail, u, out, done);
-    const HeadPolicy hp{h.part.p, static_cast<int>(h.nblocks)};
+    const HeadPolicy hp{h.part.p, static_cast<int>(h.nblocks), h.rows};
     seg_adj_kernel<HeadPolicy><<<static_cast<unsigned>(h.nblocks * h.parts), kHeadThreads,
-                                 sizeof(double) * kHeadRows, st>>>(h.bptr.p, h.hkey.p, h.hval.p, u, a.mloc(),
+                                 sizeof(double) * h.rows, st>>>(h.bptr.p, h.hkey.p, h.hval.p, u, a.mloc(),
                                                                    h.parts, h.zptr.p, h.zcol.p, hp,
                                                                    reinterpret_cast<HeadPiece*>(h.bnd.p), done);
     if (h.parts > 1) {
@@ -1033,7 +1112,7 @@ struct HeadSegs {  // per head column: entry offsets of its segment in each bloc
   const int* tptr;
   const int* hidx;
   const std::vector<int>* hc;
-  long long nblocks;
+  long long nblocks, rows;
   std::vector<int>* seg;  // ncols x (nblocks + 1)
   void operator()(long long k0, long long k1) const {
     for (long long k = k0; k < k1; ++k) {
@@ -1043,7 +1122,7 @@ struct HeadSegs {  // per head column: entry offsets of its segment in each bloc
       const long long e = tptr[j + 1];
       for (long long b = 0; b < nblocks; ++b) {
         sg[b] = static_cast<int>(q);
-        const long long lim = (b + 1) * static_cast<long long>(kHeadRows);
+        const long long lim = (b + 1) * rows;
         while (q < e && hidx[q] < lim) ++q;
       }
       sg[nblocks] = static_cast<int>(e);
@@ -1053,15 +1132,15 @@ struct HeadSegs {  // per head column: entry offsets of its segment in each bloc
 
 // copy of the head entries, block-major: warp per (head column, block) segment
 __global__ void head_pack_kernel(const int* __restrict__ seg, const int* __restrict__ dst, long long ncols,
-                                 long long nblocks, const int* __restrict__ tidx, const double* __restrict__ tval,
-                                 int* __restrict__ hkey, double* __restrict__ hval) {
+                                 long long nblocks, int rows, const int* __restrict__ tidx,
+                                 const double* __restrict__ tval, int* __restrict__ hkey, double* __restrict__ hval) {
   const long long t = (static_cast<long long>(blockIdx.x) * 256 + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= ncols * nblocks) return;
   const long long k = t / nblocks, b = t % nblocks;
   const int s0 = seg[k * (nblocks + 1) + b], s1 = seg[k * (nblocks + 1) + b + 1];
   const int d = dst[b * ncols + k];
-  const int rb = static_cast<int>(b * kHeadRows);
+  const int rb = static_cast<int>(b * rows);
   for (int q = s0 + lane; q < s1; q += 32) {
     hkey[d + q - s0] = static_cast<int>(k << 16) | (tidx[q] - rb);  // k < kHeadPad
     hval[d + q - s0] = tval[q];
@@ -1194,11 +1273,26 @@ void build_head_adj(apc_mat& a, const std::vector<int>& tptr, const int* hidx, c
   HeadAdj& h = a.head;
   h = HeadAdj();
   const long long n = a.n, mloc = a.mloc();
-  const long long nblocks = (mloc + kHeadRows - 1) / kHeadRows;
-  if (nblocks == 0 || n == 0) return;
+  if (mloc == 0 || n == 0) return;
+  // block rows: kHeadRows, or -- once there is more than a wave of blocks --
+  // the size that makes the block count a whole number of waves of the
+  // co-resident CTAs (2 per SM: 64 registers x 512 threads).  977 blocks of
+  // 8192 rows ran as 3.3 waves on 148 SMs; 888 blocks of 9010 rows run as 3
+  const long long slots = 2LL * ctx->num_sms;
+  long long rows = kHeadRows;
+  const char* re = std::getenv("APC_HEAD_BLOCK_ROWS");
+  if (re && *re) {
+    rows = std::max(256, std::min(12288, std::atoi(re)));
+  } else if (mloc > slots * kHeadRows) {
+    const long long waves = std::max<long long>(1, std::llround(static_cast<double>(mloc) / (slots * kHeadRows)));
+    rows = std::min<long long>(12288, (mloc + slots * waves - 1) / (slots * waves));
+  }
+  const long long nblocks = (mloc + rows - 1) / rows;
   const char* env = std::getenv("APC_HEAD_MIN");
   const double per_block = env ? std::atof(env) : 2.0;
-  const long long thr = std::max<long long>(64, static_cast<long long>(per_block * static_cast<double>(nblocks)));
+  // the head threshold stays tied to kHeadRows-row blocks (independent of the wave fit)
+  const long long thr = std::max<long long>(
+      64, static_cast<long long>(per_block * static_cast<double>((mloc + kHeadRows - 1) / kHeadRows)));
   std::vector<int> hc;
   std::vector<char> is_head(n, 0);
   // head column ids fit below kHeadPad, and the (column, block) partial index in int32
@@ -1212,7 +1306,7 @@ void build_head_adj(apc_mat& a, const std::vector<int>& tptr, const int* hidx, c
   const char* pe = std::getenv("APC_SETUP_PROF");
   const long long H = static_cast<long long>(hc.size());
   std::vector<int> seg(static_cast<size_t>(H * (nblocks + 1)));
-  host_parallel_for(H, HeadSegs{tptr.data(), hidx, &hc, nblocks, &seg}, 1);
+  host_parallel_for(H, HeadSegs{tptr.data(), hidx, &hc, nblocks, rows, &seg}, 1);
   // destination of segment (k, b): block-major, columns ascending within a block
   std::vector<int> dst(static_cast<size_t>(H * nblocks)), bptr(nblocks + 1, 0), zptr(nblocks + 1, 0), zcol;
   long long tot = 0;
@@ -1233,6 +1327,7 @@ void build_head_adj(apc_mat& a, const std::vector<int>& tptr, const int* hidx, c
   h.parts = penv ? std::max(1, std::atoi(penv)) : 1;
   h.ncols = H;
   h.nblocks = nblocks;
+  h.rows = static_cast<int>(rows);
   h.nnz = tot;
   auto up = [&](DBuf<int>& d, const std::vector<int>& v) {
     d.alloc(std::max<long long>(1, static_cast<long long>(v.size())));
@@ -1253,14 +1348,14 @@ void build_head_adj(apc_mat& a, const std::vector<int>& tptr, const int* hidx, c
     DBuf<int> dseg(static_cast<long long>(seg.size())), ddst(static_cast<long long>(dst.size()));
     APC_CUDA(cudaMemcpyAsync(dseg.p, seg.data(), seg.size() * sizeof(int), cudaMemcpyHostToDevice, st));
     APC_CUDA(cudaMemcpyAsync(ddst.p, dst.data(), dst.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    head_pack_kernel<<<nblk(H * nblocks * 32, 256), 256, 0, st>>>(dseg.p, ddst.p, H, nblocks, a.at.idx.p, a.at.val.p,
-                                                                  h.hkey.p, h.hval.p);
+    head_pack_kernel<<<nblk(H * nblocks * 32, 256), 256, 0, st>>>(dseg.p, ddst.p, H, nblocks, h.rows, a.at.idx.p,
+                                                                  a.at.val.p, h.hkey.p, h.hval.p);
     ctx->launches++;
     APC_CUDA(cudaGetLastError());
     APC_CUDA(cudaStreamSynchronize(st));
   }
   APC_CUDA(cudaFuncSetAttribute(seg_adj_kernel<HeadPolicy>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(sizeof(double) * kHeadRows)));
+                                static_cast<int>(sizeof(double) * rows)));
   const char* tse = std::getenv("APC_TAIL_SEG");
   if (!tse || std::atoi(tse) != 0) {
     build_tail_seg(a, tptr, hidx, tlen, is_head);

@@ -398,7 +398,7 @@ void build_hot_sell(apc_mat& a, const std::vector<long long>& col_nnz);
 
 template <class Epi>
 void launch_csr_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaStream_t st,
-                    bool x_permuted = false) {
+                    bool x_permuted = false, double* xr_buf = nullptr) {
   const long long rows = a.a.rows;
   const unsigned nb = static_cast<unsigned>((rows + kCsrFwdRowsPerBlock - 1) / kCsrFwdRowsPerBlock);
   if (nb == 0) return;
@@ -406,12 +406,15 @@ void launch_csr_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaS
     // grid <= nb keeps the epilogue's slots within fwd_num_tiles(a)
     const unsigned grid =
         std::min<unsigned>(nb, fwd_gs_grid(a.ctx, reinterpret_cast<const void*>(hot_sell_fwd_kernel<Epi>), kHotThreads));
-    if (!x_permuted) {  // else the producer of x wrote a.hot.xr itself (pc_expand)
-      hot_permute_kernel<<<static_cast<unsigned>((a.n + 255) / 256), 256, 0, st>>>(a.hot.hot.p, a.n, x, a.hot.xr.p);
+    // xr_buf: a private permuted copy (the observer's sample must not clobber
+    // the z copy the fused n-space kernel left in a.hot.xr for the next forward)
+    double* xr = xr_buf ? xr_buf : a.hot.xr.p;
+    if (!x_permuted) {  // else the producer of x wrote a.hot.xr itself (pc_expand / lsqr_nspace_kernel)
+      hot_permute_kernel<<<static_cast<unsigned>((a.n + 255) / 256), 256, 0, st>>>(a.hot.hot.p, a.n, x, xr);
       a.ctx->launches++;
     }
     hot_sell_fwd_kernel<Epi><<<grid, kHotThreads, 0, st>>>(a.a.ptr.p, a.hot.s.off.p, a.hot.s.idx.p, a.hot.s.val.p,
-                                                           rows, a.hot.s.chunks, a.hot.xr.p, done, epi);
+                                                           rows, a.hot.s.chunks, xr, done, epi);
     a.ctx->launches += 1;
     return;
   }
@@ -439,8 +442,9 @@ void launch_csr_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaS
 }
 
 template <class Epi>
-void launch_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaStream_t st, bool x_permuted = false) {
-  if (a.sparse) launch_csr_fwd(a, x, done, epi, st, x_permuted);
+void launch_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cudaStream_t st, bool x_permuted = false,
+                double* xr_buf = nullptr) {
+  if (a.sparse) launch_csr_fwd(a, x, done, epi, st, x_permuted, xr_buf);
   else launch_dense_fwd(a, x, done, epi, st);
 }
 
