@@ -618,38 +618,38 @@ struct NspaceArgs {
   int fuse_tail;
   cudaGraphConditionalHandle cond;
   int use_cond;
+  int noop;  // timing experiments only (APC_NSPACE_NOOP): skip the work
 };
 constexpr int kNsThreads = kVecThreads;  // 256-column tiles: the unfused kernels' blocks
 
-// (R^T s)_j for the tile's columns, long R^T rows by a warp (pc_expand_kernel's split)
-__device__ __forceinline__ double ns_rts(const NspaceArgs& a, long long j0, long long n, const double* s,
-                                         int* defer, double* dacc, int* ndefer) {
+// (R^T s)_j for column j = j0 + threadIdx.x: short R^T rows summed by the
+// thread, rows longer than 32 entries (Zipf-head columns of a sparse A appear
+// in most selected rows) by the whole warp -- pc_expand_kernel's split and sum
+// orders, warp-synchronous (no block barrier)
+__device__ __forceinline__ double ns_rts(const NspaceArgs& a, long long j0, long long n, const double* s) {
   constexpr int kExpandLong = 32;
   const long long j = j0 + threadIdx.x;
-  if (threadIdx.x == 0) *ndefer = 0;
-  __syncthreads();
-  double acc = 0.0;
-  bool deferred = false;
-  if (j < n) {
-    const int q0 = a.tptr[j], q1 = a.tptr[j + 1];
-    if (q1 - q0 > kExpandLong) {
-      defer[atomicAdd(ndefer, 1)] = threadIdx.x;
-      deferred = true;
-    } else {
-      for (int q = q0; q < q1; ++q) acc += a.tval[q] * s[a.tidx[q]];
-    }
-  }
-  __syncthreads();
   const int lane = threadIdx.x & 31;
-  for (int d = threadIdx.x >> 5; d < *ndefer; d += kNsThreads / 32) {
-    const long long jj = j0 + defer[d];
-    double x = 0.0;
-    for (int q = a.tptr[jj] + lane; q < a.tptr[jj + 1]; q += 32) x += a.tval[q] * s[a.tidx[q]];
-    x = warp_sum(x);
-    if (lane == 0) dacc[defer[d]] = x;
+  int q0 = 0, q1 = 0;
+  if (j < n) {
+    q0 = a.tptr[j];
+    q1 = a.tptr[j + 1];
   }
-  __syncthreads();
-  return deferred ? dacc[threadIdx.x] : acc;
+  const bool lng = q1 - q0 > kExpandLong;
+  double acc = 0.0;
+  if (!lng)
+    for (int q = q0; q < q1; ++q) acc += a.tval[q] * s[a.tidx[q]];
+  unsigned m = __ballot_sync(0xffffffffu, lng);
+  while (m) {
+    const int L = __ffs(m) - 1;
+    m &= m - 1;
+    const int b0 = __shfl_sync(0xffffffffu, q0, L), b1 = __shfl_sync(0xffffffffu, q1, L);
+    double x = 0.0;
+    for (int q = b0 + lane; q < b1; q += 32) x += a.tval[q] * s[a.tidx[q]];
+    x = warp_sum(x);
+    if (lane == L) acc = x;
+  }
+  return acc;
 }
 
 // out = M x for row-major l x l M: warp per row over the grid (pc_core_kernel)
@@ -667,13 +667,13 @@ __device__ __forceinline__ void ns_core(const double* __restrict__ M, long long 
 
 // stage G for the tiles [tile0, ntiles) step tstep; the mu-tail norm by the last CTA
 __device__ __forceinline__ void ns_stage_z(const NspaceArgs& a, double alpha, double beta, long long tile0,
-                                           long long tstep, double* sh, int* defer, double* dacc, int* ndefer) {
+                                           long long tstep, double* sh) {
   const LsqrPtrs& P = a.P;
   const long long n = P.n, ntiles = (n + kNsThreads - 1) / kNsThreads;
   const bool pre = a.kind == 2;
   for (long long tile = tile0; tile < ntiles; tile += tstep) {
     const long long j0 = tile * kNsThreads, j = j0 + threadIdx.x;
-    const double acc = pre ? ns_rts(a, j0, n, a.s, defer, dacc, ndefer) : 0.0;
+    const double acc = pre ? ns_rts(a, j0, n, a.s) : 0.0;
     double sq = 0.0;
     if (j < n) {
       const double vj = P.v[j];
@@ -700,17 +700,22 @@ __device__ __forceinline__ void ns_stage_z(const NspaceArgs& a, double alpha, do
   }
 }
 
-__global__ void __launch_bounds__(kNsThreads) lsqr_nspace_kernel(NspaceArgs a) {
+__global__ void __launch_bounds__(kNsThreads, 4) lsqr_nspace_kernel(NspaceArgs a) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[32];
-  __shared__ int defer[kNsThreads];
-  __shared__ double dacc[kNsThreads];
-  __shared__ int ndefer;
   __shared__ LsqrState ls;
   const LsqrPtrs& P = a.P;
   if (threadIdx.x == 0) ls = *P.st;
   __syncthreads();
+  if (a.noop) {  // count iterations only, stop at the cap
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const long long j = ++P.st->iter;
+      if (j >= ls.cap) P.st->done = 1;
+      if (a.use_cond) cudaGraphSetConditional(a.cond, j >= ls.cap ? 0u : 1u);
+    }
+    return;
+  }
   if (ls.done) {
     if (a.use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.cond, 0);
     return;
@@ -740,7 +745,7 @@ __global__ void __launch_bounds__(kNsThreads) lsqr_nspace_kernel(NspaceArgs a) {
   // D: v_raw (into h), ||v_raw||^2 per tile
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long long j0 = tile * kNsThreads, j = j0 + threadIdx.x;
-    const double acc = pre ? ns_rts(a, j0, n, a.s, defer, dacc, &ndefer) : 0.0;
+    const double acc = pre ? ns_rts(a, j0, n, a.s) : 0.0;
     double sq = 0.0;
     if (j < n) {
       const double h = hval(j);
@@ -802,18 +807,15 @@ __global__ void __launch_bounds__(kNsThreads) lsqr_nspace_kernel(NspaceArgs a) {
   if (ls.done) return;  // identical in every CTA: nobody waits at the barrier below
   grid.sync();
   // G: the next iteration's z
-  ns_stage_z(a, ls.alpha, ls.beta, blockIdx.x, gridDim.x, sh, defer, dacc, &ndefer);
+  ns_stage_z(a, ls.alpha, ls.beta, blockIdx.x, gridDim.x, sh);
 }
 
 // stage G alone (before the first loop iteration): one CTA per tile
 __global__ void __launch_bounds__(kNsThreads) lsqr_nspace_z_kernel(NspaceArgs a) {
   __shared__ double sh[32];
-  __shared__ int defer[kNsThreads];
-  __shared__ double dacc[kNsThreads];
-  __shared__ int ndefer;
   const LsqrState* st = a.P.st;
   if (st->done) return;
-  ns_stage_z(a, st->alpha, st->beta, blockIdx.x, gridDim.x, sh, defer, dacc, &ndefer);
+  ns_stage_z(a, st->alpha, st->beta, blockIdx.x, gridDim.x, sh);
 }
 
 namespace {
@@ -984,6 +986,7 @@ NspaceArgs nspace_args(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P
   na.fuse_tail = P.has_tail;
   na.cond = cond;
   na.use_cond = use_cond;
+  na.noop = std::getenv("APC_NSPACE_NOOP") ? 1 : 0;
   return na;
 }
 
@@ -993,7 +996,7 @@ int nspace_grid(apc_ctx* ctx, long long n) {
     int occ = 0;
     APC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lsqr_nspace_kernel, kNsThreads, 0));
     const char* e = std::getenv("APC_NSPACE_CTAS_PER_SM");
-    per_sm = std::max(1, std::min(occ, e ? std::atoi(e) : 2));
+    per_sm = std::max(1, std::min(occ, e ? std::atoi(e) : 4));
   }
   const long long ntiles = (n + kNsThreads - 1) / kNsThreads;
   return static_cast<int>(std::max<long long>(1, std::min<long long>(ntiles, static_cast<long long>(per_sm) * ctx->num_sms)));

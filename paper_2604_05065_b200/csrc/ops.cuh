@@ -262,7 +262,7 @@ csr_fwd_gs_kernel(const int* __restrict__ ptr, const int* __restrict__ idx, cons
 #define APC_HOT_KU 16
 #endif
 #ifndef APC_HOT_MINB
-#define APC_HOT_MINB 4
+#define APC_HOT_MINB 6
 #endif
 constexpr int kHotThreads = 256;
 
