@@ -154,6 +154,7 @@ struct HeadAdj {
     int rb = 0, parts = 1, sb = 1;       // sb: row superblocks (stream order)
     DBuf<i32> gptr, gcol0, tcol, zptr, zcol, tkey, cols;
     DBuf<double> tval, bnd, part;        // part: ncols x sb partials (sb > 1)
+    DBuf<double> outc;                   // sb == 1: column sums in tail order, scattered by tcol
     bool built() const { return ngroups > 0; }
   } seg;
   bool built() const { return ncols > 0; }

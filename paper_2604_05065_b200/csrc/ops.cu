@@ -309,6 +309,7 @@ struct HeadPiece {
 
 struct HeadPolicy {
   __device__ __forceinline__ void begin() {}
+  __device__ __forceinline__ void begin_item(int) {}
   double* part;
   int nb;    // blocks (ncols x nblocks < 2^31, build_head_adj)
   int rows;  // rows of A per block (<= 65536: the key's row field)
@@ -330,8 +331,16 @@ struct TailPolicy {
   int rb;                         // bits of the row field
   AdjEpi e;                       // e.n2top != nullptr: out = (raw + mu u_t) / beta (lsqr_epi_kernel)
   double beta;
+  double* outc;  // non-null: column sums in tail order (outc[gcol0[g] + k]); tail_scatter_kernel maps them
+  int gbase;
   __device__ __forceinline__ void begin() {
     if (e.n2top) beta = sqrt(*e.n2top + (e.n2tail ? *e.n2tail : 0.0));
+  }
+  // the group's first tail-order slot, once per work item: a closed piece's
+  // store then needs no dependent tcol lookup (which stalled the warp's
+  // in-order issue on every step that closed a column)
+  __device__ __forceinline__ void begin_item(int g) {
+    if (outc) gbase = __ldg(gcol0 + g);
   }
   static constexpr bool kStage = false;
   static constexpr bool kFast = false;  // tail runs are short: no single-column steps to speak of
@@ -344,6 +353,10 @@ struct TailPolicy {
   __device__ __forceinline__ int pad() const { return static_cast<int>((1u << (32 - rb)) - 1u); }
   __device__ __forceinline__ int block_rows() const { return 0; }
   __device__ __forceinline__ void store(int k, long long g, double s) const {
+    if (outc) {
+      outc[gbase + k] = s;
+      return;
+    }
     const int j = __ldg(tcol + __ldg(gcol0 + g) + k);
     if (e.n2top) {
       const double raw = e.ut ? s + e.mu * e.ut[j] : s;
@@ -395,6 +408,7 @@ __device__ __forceinline__ void seg_adj_body(int bid, const int* __restrict__ bp
   const int blk = bid / parts;
   const int prt = bid % parts;
   pol.begin();
+  pol.begin_item(blk);
   const int PAD = pol.pad();
   const double* ub = u;
   if (Pol::kStage) {
@@ -653,6 +667,7 @@ __global__ void seg_bnd_kernel(const HeadPiece* __restrict__ bnd, int parts, lon
   pol.begin();
   const long long blk = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (blk >= nblocks) return;
+  pol.begin_item(static_cast<int>(blk));
   int k = -1, f = -1;
   double sum = 0.0, fsum = 0.0;
   bool first = false;
@@ -679,6 +694,14 @@ __global__ void tail_combine_kernel(const double* __restrict__ part, const int* 
     s = beta > 0.0 ? raw / beta : raw;
   }
   out[j] = s;
+}
+
+// tail-order column sums -> out[original column]
+__global__ void tail_scatter_kernel(const double* __restrict__ outc, const int* __restrict__ tcol, long long ncols,
+                                    double* __restrict__ out, const int* done) {
+  if (done && *done) return;
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < ncols) out[__ldg(tcol + i)] = __ldg(outc + i);
 }
 
 // warp per head column: its partials in block order -> out[col]
@@ -886,7 +909,10 @@ void seg_adjoint(apc_mat& a, const double* u, double* out, const int* done, cons
   cudaStream_t st = a.ctx->stream;
   const HeadAdj& h = a.head;
   const HeadAdj::Seg& t = h.seg;
-  const TailPolicy pol{t.gcol0.p, t.tcol.p, t.sb > 1 ? t.part.p : out, t.rb, t.sb > 1 ? AdjEpi{} : e, 0.0};
+  // tail-order stores (then one scatter) unless superblock partials or the fused epilogue are in use
+  const bool compact = t.sb == 1 && !e.n2top && t.outc.p;
+  const TailPolicy pol{t.gcol0.p, t.tcol.p, t.sb > 1 ? t.part.p : out, t.rb, t.sb > 1 ? AdjEpi{} : e, 0.0,
+                       compact ? t.outc.p : nullptr, 0};
   const HeadPolicy hp{h.part.p, static_cast<int>(h.nblocks), h.rows};
   seg_adj_kernel<TailPolicy><<<static_cast<unsigned>(t.ngroups * t.parts), kHeadThreads, 0, st>>>(
       t.gptr.p, t.tkey.p, t.tval.p, u, a.mloc(), t.parts, t.zptr.p, t.zcol.p, pol,
@@ -899,6 +925,10 @@ void seg_adjoint(apc_mat& a, const double* u, double* out, const int* done, cons
   }
   if (t.sb > 1) {
     tail_combine_kernel<<<nblk(t.ncols, 256), 256, 0, st>>>(t.part.p, t.cols.p, t.ncols, t.sb, out, done, e);
+    a.ctx->launches++;
+  }
+  if (compact) {
+    tail_scatter_kernel<<<nblk(t.ncols, 256), 256, 0, st>>>(t.outc.p, t.tcol.p, t.ncols, out, done);
     a.ctx->launches++;
   }
   seg_adj_kernel<HeadPolicy><<<static_cast<unsigned>(h.nblocks * h.parts), kHeadThreads, sizeof(double) * h.rows,
@@ -1246,6 +1276,8 @@ void build_tail_seg(apc_mat& a, const std::vector<int>& tptr, const int* hidx, c
   up(t.zcol, zcol);
   up(t.cols, tc);
   if (S > 1) t.part.alloc(T * S);
+  static const bool compact_env = !std::getenv("APC_TAIL_COMPACT") || std::atoi(std::getenv("APC_TAIL_COMPACT")) != 0;
+  if (S == 1 && compact_env) t.outc.alloc(std::max<long long>(1, static_cast<long long>(dix.size())));
   t.tkey.alloc(std::max<long long>(kHeadStep, tot));
   t.tval.alloc(std::max<long long>(kHeadStep, tot));
   fill_int_kernel<<<nblk(t.tkey.n, 256), 256, 0, st>>>(t.tkey.p, t.tkey.n,
