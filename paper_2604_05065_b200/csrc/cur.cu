@@ -2182,24 +2182,7 @@ void DeviceCur::refresh() {
   ctx_->launches++;
   // H = U R (core solve per column)
   H_.ensure(l * n_);
-  // warp per column wins when there are few columns (latency-bound chains,
-  // C1: n = 500); with many columns the FP64 pipe is the limit and a thread
-  // per column issues 32x fewer predicated instructions (C2/C3: n >= 10^4)
-  if (l <= 1024 && n_ <= 4096 && !std::getenv("APC_CORE_SOLVE_THREAD")) {
-    const unsigned g = static_cast<unsigned>((n_ * 32 + 127) / 128);
-    const int li = static_cast<int>(l);
-    if (l <= 128)
-      core_solve_warp_kernel<4><<<g, 128, 0, st>>>(Rrm_.p, H_.p, li, n_, core_kind_, core_h_.p, core_at_.p, core_perm_.p);
-    else if (l <= 256)
-      core_solve_warp_kernel<8><<<g, 128, 0, st>>>(Rrm_.p, H_.p, li, n_, core_kind_, core_h_.p, core_at_.p, core_perm_.p);
-    else if (l <= 512)
-      core_solve_warp_kernel<16><<<g, 128, 0, st>>>(Rrm_.p, H_.p, li, n_, core_kind_, core_h_.p, core_at_.p, core_perm_.p);
-    else
-      core_solve_warp_kernel<32><<<g, 128, 0, st>>>(Rrm_.p, H_.p, li, n_, core_kind_, core_h_.p, core_at_.p, core_perm_.p);
-  } else {
-    core_solve_cols_kernel<<<nb(n_, 128), 128, 0, st>>>(Rrm_.p, H_.p, l, n_, core_kind_, core_h_.p, core_a_.p,
-                                                        core_perm_.p);
-  }
+  launch_core_solve(Rrm_.p, H_.p, n_);
   // E^row = Y - Y(:, J) H
   DBuf<double> d_sc(s_ * l);
   gather_sc_kernel<<<nb(s_ * l), kT, 0, st>>>(Y_.p, s_, d_J.p, l, d_sc.p);
@@ -2209,6 +2192,44 @@ void DeviceCur::refresh() {
   APC_CUDA(cudaStreamSynchronize(st));
   ps.reset(new ProfScope("ref.rho"));
   compute_rho();
+}
+
+// out = U rhs for the ncols columns of a row-major l x ncols block (CoreFactor
+// solve, cur.hpp:119-144): warp per column when there are few columns
+// (latency-bound chains, C1: n = 500); with many columns the FP64 pipe is the
+// limit and a thread per column issues 32x fewer predicated instructions
+void DeviceCur::launch_core_solve(const double* rhs_rm, double* out_rm, i64 ncols) const {
+  cudaStream_t st = ctx_->stream;
+  const i64 l = core_l_;
+  if (l <= 1024 && ncols <= 4096 && !std::getenv("APC_CORE_SOLVE_THREAD")) {
+    const unsigned g = static_cast<unsigned>((ncols * 32 + 127) / 128);
+    const int li = static_cast<int>(l);
+    if (l <= 128)
+      core_solve_warp_kernel<4><<<g, 128, 0, st>>>(rhs_rm, out_rm, li, ncols, core_kind_, core_h_.p, core_at_.p,
+                                                  core_perm_.p);
+    else if (l <= 256)
+      core_solve_warp_kernel<8><<<g, 128, 0, st>>>(rhs_rm, out_rm, li, ncols, core_kind_, core_h_.p, core_at_.p,
+                                                  core_perm_.p);
+    else if (l <= 512)
+      core_solve_warp_kernel<16><<<g, 128, 0, st>>>(rhs_rm, out_rm, li, ncols, core_kind_, core_h_.p, core_at_.p,
+                                                   core_perm_.p);
+    else
+      core_solve_warp_kernel<32><<<g, 128, 0, st>>>(rhs_rm, out_rm, li, ncols, core_kind_, core_h_.p, core_at_.p,
+                                                   core_perm_.p);
+  } else {
+    core_solve_cols_kernel<<<nb(ncols, 128), 128, 0, st>>>(rhs_rm, out_rm, l, ncols, core_kind_, core_h_.p,
+                                                           core_a_.p, core_perm_.p);
+  }
+  ctx_->launches++;
+  APC_CUDA(cudaGetLastError());
+}
+
+Vec DeviceCur::core_solve_rm(const Vec& rhs_rm, i64 ncols) const {
+  const i64 l = core_l_;
+  DBuf<double> b(std::max<i64>(1, l * ncols)), o(std::max<i64>(1, l * ncols));
+  APC_CUDA(cudaMemcpyAsync(b.p, rhs_rm.data(), sizeof(double) * l * ncols, cudaMemcpyHostToDevice, ctx_->stream));
+  launch_core_solve(b.p, o.p, ncols);
+  return download(ctx_, o.p, l * ncols);
 }
 
 void DeviceCur::build_core_device(i64 l) {

@@ -56,6 +56,9 @@ class DeviceCur {
   // builders use them), downloaded on first use after each refresh
   const CoreFactorH& core() const;
   const Vec& intersection() const;  // l x l column-major
+  // U B for the ncols columns of a host row-major l x ncols block, on the
+  // device (the svd form's U T_R^T, preconditioner.hpp:158-192); row-major out
+  Vec core_solve_rm(const Vec& rhs_rm, i64 ncols) const;
   std::uint64_t sketch_applications() const { return 1; }
 
   AugmentResult augment();   // cur.hpp:248-294
@@ -98,6 +101,7 @@ class DeviceCur {
   // device works (the stream is consumed strictly in order, one set at a time)
   std::future<std::vector<double>> next_probes_;
   void build_core_device(i64 l);  // CoreFactor::build on the device (exact order)
+  void launch_core_solve(const double* rhs_rm, double* out_rm, i64 ncols) const;
   mutable CoreFactorH core_;
   mutable Vec block_;
   mutable bool host_core_stale_ = false;

@@ -1,15 +1,20 @@
 // Preconditioner construction per rebuild (preconditioner.hpp:138-396,
 // 424-592) and its upload as the device form I + B K B^T / I + R^T G R that
-// the LSQR loop applies (lsqr.cu).  The tall products (C^T C, Q^T c, Q p,
-// Q_R V_M) run on the device through cuBLAS; the l x l algebra (Cholesky of
-// the Gram matrix, core spectrum, middle operators) runs on the host with the
-// restated reference routines.  None of it is index-affecting:
-// only the x / iteration parity bar applies.
+// the LSQR loop applies (lsqr.cu).  Everything runs on the device: the tall
+// products (C^T C, Q^T c, Q p, Q_R V_M) on the DMMA GEMM (blas.cu), the l x l
+// algebra (Cholesky of the Gram matrices, the core solve U T_R^T, the core
+// spectrum by Jacobi, the middle operators' triangular solves and products)
+// on dense_small.cu / svd.cu / the CoreFactor kernels.  The host keeps the
+// l^2 bookkeeping (transposes, diagonal scalings) and two rare fallbacks: QR
+// when a Gram matrix is not positive definite, Householder for a small
+// nearly dependent QrAccumulator block.  None of it is index-affecting
+// (SURVEY.md G8): only the x / iteration parity bar applies.
 #include <cmath>
 #include <memory>
 
 #include "blas.hpp"
 #include "cur.hpp"
+#include "dense_small.hpp"
 #include "precond.hpp"
 #include "svd.hpp"
 
@@ -39,6 +44,24 @@ Vec chol_gram_sparse(i64 m, i64 k, const std::vector<i64>& cp, const std::vector
   }
   return chol_upper(k, g, "chol_gram: non-positive pivot");
 }
+
+}  // namespace
+
+// T_R with T_R^T T_R = R R^T from the device rows of R (row-major l x n ==
+// column-major n x l): Gram by the DMMA SYRK, Cholesky on the device; a
+// non-positive pivot falls back to the host QR of the sparse rows
+Vec gram_factor_rows_dev(apc_ctx* ctx, i64 n, i64 l, const double* r_rm, const std::vector<i64>& cp,
+                         const std::vector<i64>& ri, const Vec& va) {
+  require(l >= 1, APC_INVALID_ARGUMENT, "chol_gram: empty matrix");
+  DBuf<double> G(l * l);
+  dsyrk_t(ctx, l, n, 1.0, r_rm, n, 0.0, G.p, l);
+  if (dpotrf_upper_dev(ctx, l, G.p) >= 0) return gram_factor_sparse(n, l, cp, ri, va);
+  Vec t(static_cast<size_t>(l * l));
+  copy_sync(ctx->stream, t.data(), G.p, sizeof(double) * l * l, cudaMemcpyDeviceToHost);
+  return t;
+}
+
+namespace {
 
 Vec densify_csc(i64 m, i64 k, const std::vector<i64>& cp, const std::vector<i64>& ri, const Vec& va) {
   Vec d(static_cast<size_t>(m * k), 0.0);
@@ -98,11 +121,9 @@ void upload_r(apc_ctx* ctx, i64 n, i64 l, const std::vector<i64>& cp, const std:
 }
 
 // G = T^{-1} K T^{-T} for an implicit basis Q = R^T T^{-1} (l x l, T upper)
-Vec conjugate_by_tinv(i64 l, const Vec& t, const Vec& K) {
-  Vec X = K;
-  for (i64 j = 0; j < l; ++j) tri_solve(l, t.data(), X.data() + j * l, false);
-  Vec Xt = transpose(l, l, X);
-  for (i64 j = 0; j < l; ++j) tri_solve(l, t.data(), Xt.data() + j * l, false);
+Vec conjugate_by_tinv(apc_ctx* ctx, i64 l, const Vec& t, const Vec& K) {
+  const Vec X = dtri_solve_cols(ctx, l, t, K, l, false);
+  const Vec Xt = dtri_solve_cols(ctx, l, t, transpose(l, l, X), l, false);
   return transpose(l, l, Xt);
 }
 
@@ -116,18 +137,10 @@ void symmetrize_upper(i64 n, Vec& g) {
 Vec cholqr_step(apc_ctx* ctx, i64 m, i64 b, double* e) {
   DBuf<double> G(b * b);
   dsyrk_t(ctx, b, m, 1.0, e, m, 0.0, G.p, b);
-  Vec g = download_vec(ctx, G.p, b * b);
-  symmetrize_upper(b, g);
-  Vec r;
-  try {
-    r = chol_upper(b, g, "QrAccumulator: dependent block");
-  } catch (const Status& s) {
-    fail(APC_RANK_DEFICIENT, "QrAccumulator: dependent block", s.index);
-  }
-  DBuf<double> R(b * b);
-  upload_vec(ctx, R, r);
-  dtrsm_right_upper(ctx, m, b, R.p, b, e, m);
-  APC_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int bad = dpotrf_upper_dev(ctx, b, G.p);  // G <- R (upper), on the device
+  if (bad >= 0) fail(APC_RANK_DEFICIENT, "QrAccumulator: dependent block", bad);
+  dtrsm_right_upper(ctx, m, b, G.p, b, e, m);
+  Vec r = download_vec(ctx, G.p, b * b);
   return r;
 }
 
@@ -154,10 +167,31 @@ void DevQrAcc::append(i64 m, i64 b, const double* c) {  // preconditioner.hpp:43
     dgemm(ctx, false, false, m, b, k, -1.0, q.p, m, P.p, k, 1.0, e.p, m);
     p2 = download_vec(ctx, P.p, k * b);
   }
-  // factor the block: Householder on the host when small, CholeskyQR2 on the device otherwise
+  // factor the block: CholeskyQR2 on the device; a small block whose Gram
+  // matrix is not numerically positive definite (condition number beyond
+  // ~1e8) goes to Householder on the host, which still tells a nearly
+  // dependent block (|R_jj| <= 1e-12 scale) from a merely ill-conditioned one
   Vec rb;
-  if (static_cast<double>(m) * b * b <= 2e8) {
-    Vec eh = download_vec(ctx, e.p, m * b);
+  const bool small = static_cast<double>(m) * b * b <= 2e8;
+  DBuf<double> e0;
+  if (small) {
+    e0.alloc(m * b);
+    APC_CUDA(cudaMemcpyAsync(e0.p, e.p, sizeof(double) * m * b, cudaMemcpyDeviceToDevice, st));
+  }
+  bool done = false;
+  try {
+    Vec r1 = cholqr_step(ctx, m, b, e.p);
+    Vec r2 = cholqr_step(ctx, m, b, e.p);
+    rb = dmatmul(ctx, b, b, b, r2, r1);
+    done = true;
+  } catch (const Status& s) {
+    if (!small || s.code != APC_RANK_DEFICIENT) throw;
+  }
+  if (done) {
+    for (i64 j = 0; j < b; ++j)
+      if (std::fabs(rb[j * b + j]) <= 1e-12 * scale) fail(APC_RANK_DEFICIENT, "QrAccumulator: dependent block", j);
+  } else {
+    Vec eh = download_vec(ctx, e0.p, m * b);
     Householder f = householder(m, b, std::move(eh));
     for (i64 j = 0; j < b; ++j)
       if (std::fabs(f.a[j * m + j]) <= 1e-12 * scale) fail(APC_RANK_DEFICIENT, "QrAccumulator: dependent block", j);
@@ -166,12 +200,6 @@ void DevQrAcc::append(i64 m, i64 b, const double* c) {  // preconditioner.hpp:43
     normalise_signs(m, b, qe, rb);
     APC_CUDA(cudaMemcpyAsync(e.p, qe.data(), sizeof(double) * m * b, cudaMemcpyHostToDevice, st));
     APC_CUDA(cudaStreamSynchronize(st));
-  } else {
-    Vec r1 = cholqr_step(ctx, m, b, e.p);
-    Vec r2 = cholqr_step(ctx, m, b, e.p);
-    rb = matmul(b, b, b, r2, r1);
-    for (i64 j = 0; j < b; ++j)
-      if (std::fabs(rb[j * b + j]) <= 1e-12 * scale) fail(APC_RANK_DEFICIENT, "QrAccumulator: dependent block", j);
   }
   // Q <- [Q, q_e]
   if (k + b > cap) {
@@ -218,7 +246,7 @@ void build_precond(const BuildInputs& in, PrecondDev& p, PrecondInfo& info) {
   Vec t_c;
   std::unique_ptr<ProfScope> ps(new ProfScope("pre.chol"));
   try {
-    t_c = chol_upper(l, in.gram, "chol_gram: non-positive pivot");
+    t_c = dchol_upper(ctx, l, in.gram, "chol_gram: non-positive pivot");
   } catch (const Status& s) {
     if (s.code != APC_NOT_POSITIVE) throw;
     t_c = thin_qr(in.m, l, in.c_dense()).t;
@@ -226,17 +254,15 @@ void build_precond(const BuildInputs& in, PrecondDev& p, PrecondInfo& info) {
   if (in.variant == 0) {
     // SVD form: M = T_C U T_R^T, small_svd(M) (preconditioner.hpp:158-192)
     ps.reset(new ProfScope("pre.core_matmul"));
-    Vec ut = in.core->solve_matrix(l, transpose(l, l, *in.t_r));
-    Vec mm = matmul(l, l, l, t_c, ut);
+    // U T_R^T on the device: T_R's column-major bytes are T_R^T row-major;
+    // the row-major result transposed is the column-major product
+    Vec ut = transpose(l, l, in.core_solve_rm(*in.t_r, l));
+    Vec mm = dmatmul(ctx, l, l, l, t_c, ut);
     ps.reset(new ProfScope("pre.svd"));
     require(l <= 4096, APC_INVALID_ARGUMENT, "small_svd: dimension exceeds the small-problem cap");
     SvdH s;
-    if (l > 96) {  // parallel-order Jacobi on the device; serial cyclic on the host for small cores
-      s.m = s.n = l;
-      device_jacobi_svd(ctx, l, mm, s.sigma, s.v);
-    } else {
-      s = small_svd(l, l, mm);
-    }
+    s.m = s.n = l;
+    device_jacobi_svd(ctx, l, mm, s.sigma, s.v);  // parallel-order one-sided Jacobi (svd.cu)
     ps.reset(new ProfScope("pre.G"));
     info.sigma_cur = s.sigma;
     info.sigma_reg.resize(l);
@@ -260,12 +286,11 @@ void build_precond(const BuildInputs& in, PrecondDev& p, PrecondInfo& info) {
     } else {
       // V = R^T T_R^{-1} V_M: G = W diag(d) W^T with W = T_R^{-1} V_M (symmetric)
       p.kind = 2;
-      Vec W = s.v;
-      for (i64 j = 0; j < l; ++j) tri_solve(l, in.t_r->data(), W.data() + j * l, false);
+      const Vec W = dtri_solve_cols(ctx, l, *in.t_r, s.v, l, false);
       Vec WD = W;
       for (i64 t = 0; t < l; ++t)
         for (i64 i = 0; i < l; ++i) WD[t * l + i] *= d[t];
-      Vec G = matmul(l, l, l, WD, transpose(l, l, W));
+      Vec G = dmatmul(ctx, l, l, l, WD, transpose(l, l, W));
       upload_r(ctx, n, l, in.r_ptr, in.r_idx, in.r_val, p);
       upload_vec(ctx, p.Kf, G);
       upload_vec(ctx, p.Ka, G);
@@ -275,20 +300,11 @@ void build_precond(const BuildInputs& in, PrecondDev& p, PrecondInfo& info) {
     // M^{-1} = T_R^{-T} B T_C^{-1}  (preconditioner.hpp:279-318)
     info.sigma_hat = in.target_level;
     info.sigma_floor = in.target_level;
-    Vec Minv(static_cast<size_t>(l * l), 0.0);
-    Vec e(l), bw(l);
-    for (i64 kcol = 0; kcol < l; ++kcol) {
-      std::fill(e.begin(), e.end(), 0.0);
-      e[kcol] = 1.0;
-      tri_solve(l, t_c.data(), e.data(), false);
-      for (i64 i = 0; i < l; ++i) {
-        double acc = 0.0;
-        for (i64 t = 0; t < l; ++t) acc += (*in.block)[t * l + i] * e[t];
-        bw[i] = acc;
-      }
-      tri_solve(l, in.t_r->data(), bw.data(), true);
-      for (i64 i = 0; i < l; ++i) Minv[kcol * l + i] = bw[i];
-    }
+    // M^{-1} = T_R^{-T} A(I,J) T_C^{-1}: triangular solves and the product on the device
+    Vec eye(static_cast<size_t>(l * l), 0.0);
+    for (i64 i = 0; i < l; ++i) eye[i * l + i] = 1.0;
+    const Vec tcinv = dtri_solve_cols(ctx, l, t_c, eye, l, false);
+    const Vec Minv = dtri_solve_cols(ctx, l, *in.t_r, dmatmul(ctx, l, l, l, *in.block, tcinv), l, true);
     Vec Kf(static_cast<size_t>(l * l)), Ka(static_cast<size_t>(l * l));
     for (i64 j = 0; j < l; ++j)
       for (i64 i = 0; i < l; ++i) {
@@ -305,8 +321,8 @@ void build_precond(const BuildInputs& in, PrecondDev& p, PrecondInfo& info) {
     } else {
       p.kind = 2;
       upload_r(ctx, n, l, in.r_ptr, in.r_idx, in.r_val, p);
-      upload_vec(ctx, p.Kf, transpose(l, l, conjugate_by_tinv(l, *in.t_r, Kf)));
-      upload_vec(ctx, p.Ka, transpose(l, l, conjugate_by_tinv(l, *in.t_r, Ka)));
+      upload_vec(ctx, p.Kf, transpose(l, l, conjugate_by_tinv(ctx, l, *in.t_r, Kf)));
+      upload_vec(ctx, p.Ka, transpose(l, l, conjugate_by_tinv(ctx, l, *in.t_r, Ka)));
     }
   }
   p.sigma_hat = info.sigma_hat;

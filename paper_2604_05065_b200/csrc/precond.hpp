@@ -25,6 +25,10 @@ struct DevQrAcc {
 };
 
 Vec gram_factor_sparse(i64 m, i64 k, const std::vector<i64>& cp, const std::vector<i64>& ri, const Vec& va);
+// the same factor from the device rows of R (row-major l x n); the sparse host
+// routine above is its fallback for a non-positive pivot
+Vec gram_factor_rows_dev(apc_ctx* ctx, i64 n, i64 l, const double* r_rm, const std::vector<i64>& cp,
+                         const std::vector<i64>& ri, const Vec& va);
 
 struct BuildInputs {
   apc_ctx* ctx = nullptr;
@@ -32,7 +36,7 @@ struct BuildInputs {
   bool implicit = false;
   i64 m = 0, n = 0, l = 0;  // m: target rows (C's rows)
   double mu = 0.0, target_level = 0.0;
-  const CoreFactorH* core = nullptr;
+  std::function<Vec(const Vec&, i64)> core_solve_rm;  // U B for a row-major l x ncols B (DeviceCur, on the device)
   const Vec* block = nullptr;  // intersection A(I, J), l x l
   const Vec* t_r = nullptr;    // T_R (l x l upper)
   const double* q_dev = nullptr;  // explicit Q_R on the device (n x l, ld = n)

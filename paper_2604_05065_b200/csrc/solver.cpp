@@ -219,7 +219,7 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
         std::vector<i64> rp, ri;
         Vec rv;
         cur.rt_csc(rp, ri, rv);
-        t_r_implicit = gram_factor_sparse(n, cur.rank(), rp, ri, rv);
+        t_r_implicit = gram_factor_rows_dev(ctx, n, cur.rank(), cur.r_rowmajor_dev(), rp, ri, rv);
         t_r_stale = false;
         rep.t_factor_ms += ms_since(t_f0);
       }
@@ -237,7 +237,7 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
         in.l = cur.rank();
         in.mu = mu;
         in.target_level = rho;
-        in.core = &cur.core();                                // svd form: U T_R^T (host, downloaded factor)
+        in.core_solve_rm = [&cur](const Vec& b, i64 nc) { return cur.core_solve_rm(b, nc); };  // svd form: U T_R^T
         if (cfg.variant == 1) in.block = &cur.intersection();  // svd-free: A(I, J)
         in.t_r = implicit_mode ? &t_r_implicit : &qr_acc.t;
         in.q_dev = qr_acc.q.p;
