@@ -1980,11 +1980,53 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
   }
   APC_CUDA(cudaGetLastError());
   APC_CUDA(cudaMemcpyAsync(E_.p, Y_.p, sizeof(double) * s_ * n_, cudaMemcpyDeviceToDevice, st));
-  // ztol = 1e-14 ||Y||_F (frob_norm: sequential over storage order, cur.hpp:224)
-  std::vector<double> yh = download(ctx_, Y_.p, s_ * n_);
-  double f2 = 0.0;
-  for (double v : yh) f2 += v * v;
-  ztol_ = 1e-14 * std::sqrt(f2);
+  // ztol = 1e-14 ||Y||_F (frob_norm: sequential over storage order,
+  // cur.hpp:224).  The exact sequential sum needs Y on the host; it is read in
+  // chunks on a side stream (copy engine) by a host thread while the device
+  // goes on with the first augment, and joined when ztol is first used.
+  {
+    APC_CUDA(cudaEventCreateWithFlags(&ev_sketch_, cudaEventDisableTiming));
+    APC_CUDA(cudaEventRecord(ev_sketch_, st));
+    const double* y = Y_.p;
+    const i64 total = s_ * n_;
+    cudaEvent_t ready = ev_sketch_;
+    const int dev = ctx_->device;
+    ztol_future_ = std::async(std::launch::async, [y, total, ready, dev]() {
+      APC_CUDA(cudaSetDevice(dev));
+      cudaStream_t cs;
+      APC_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      APC_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+      constexpr i64 kChunk = 1 << 22;  // 32 MB of doubles per staging buffer
+      double* stage[2] = {nullptr, nullptr};
+      const i64 cap = std::min<i64>(kChunk, std::max<i64>(1, total));
+      APC_CUDA(cudaMallocHost(&stage[0], sizeof(double) * cap));
+      APC_CUDA(cudaMallocHost(&stage[1], sizeof(double) * cap));
+      cudaEvent_t done[2];
+      APC_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+      APC_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+      double f2 = 0.0;
+      const i64 nch = (total + cap - 1) / cap;
+      auto issue = [&](i64 c) {
+        const i64 b = c * cap, len = std::min(cap, total - b);
+        APC_CUDA(cudaMemcpyAsync(stage[c & 1], y + b, sizeof(double) * len, cudaMemcpyDeviceToHost, cs));
+        APC_CUDA(cudaEventRecord(done[c & 1], cs));
+      };
+      if (nch > 0) issue(0);
+      for (i64 c = 0; c < nch; ++c) {
+        if (c + 1 < nch) issue(c + 1);  // double-buffered: the next chunk streams while this one is summed
+        APC_CUDA(cudaEventSynchronize(done[c & 1]));
+        const i64 b = c * cap, len = std::min(cap, total - b);
+        const double* h = stage[c & 1];
+        for (i64 i = 0; i < len; ++i) f2 += h[i] * h[i];
+      }
+      cudaEventDestroy(done[0]);
+      cudaEventDestroy(done[1]);
+      cudaFreeHost(stage[0]);
+      cudaFreeHost(stage[1]);
+      cudaStreamDestroy(cs);
+      return 1e-14 * std::sqrt(f2);
+    });
+  }
   rowsel_.alloc(std::max<i64>(1, mt_));
   colsel_.alloc(std::max<i64>(1, n_));
   APC_CUDA(cudaMemsetAsync(rowsel_.p, 0, rowsel_.bytes(), st));
@@ -1993,7 +2035,10 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
   SetupProf::add("init.sketch_kernel", sketch_ms_);
 }
 
-DeviceCur::~DeviceCur() = default;
+DeviceCur::~DeviceCur() {
+  if (ztol_future_.valid()) ztol_future_.wait();  // the reader thread still streams Y_
+  if (ev_sketch_) cudaEventDestroy(ev_sketch_);
+}
 
 std::vector<double> DeviceCur::draw_probes() {
   // probe p = the p-th block of n consecutive Gaussians of the probe stream
@@ -2053,7 +2098,7 @@ AugmentResult DeviceCur::augment() {
   std::unique_ptr<ProfScope> ps(new ProfScope("aug.col_lupp"));
   LuppOut col_piv = device_lupp(ctx_, work_.p, n_, s_, want);
   ps.reset(new ProfScope("aug.ecol"));
-  std::vector<i64> jplus = admissible(col_piv, want, ztol_);
+  std::vector<i64> jplus = admissible(col_piv, want, ztol());
   if (jplus.empty()) {
     if (rank() == 0) compute_rho();
     return {0, true};
@@ -2111,7 +2156,7 @@ AugmentResult DeviceCur::augment() {
   ps.reset(new ProfScope("aug.row_lupp"));
   LuppOut row_piv = device_lupp(ctx_, ecol.p, mt_, b, b);
   ps.reset();
-  std::vector<i64> iplus = admissible(row_piv, b, ztol_);
+  std::vector<i64> iplus = admissible(row_piv, b, ztol());
   if (iplus.empty()) return {0, true};
   const bool exhausted = static_cast<i64>(iplus.size()) < want;
   jplus.resize(iplus.size());

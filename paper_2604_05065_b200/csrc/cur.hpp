@@ -91,7 +91,13 @@ class DeviceCur {
   double amu_ = 0.0; // mu of the augmented target (0: plain A)
   double embed_ms_ = 0.0, sketch_ms_ = 0.0;
   int core_kind_;
-  double ztol_ = 0.0;
+  double ztol_ = -1.0;
+  std::future<double> ztol_future_;  // the host's exact sequential ||Y||_F^2 (joined on first use)
+  cudaEvent_t ev_sketch_ = nullptr;
+  double ztol() {
+    if (ztol_ < 0.0) ztol_ = ztol_future_.get();
+    return ztol_;
+  }
   double rho_;
   i64 last_added_ = 0;
   std::vector<i64> I_, J_;
