@@ -12,10 +12,14 @@ import sys
 
 rep, cubin, kname = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+fname = sys.argv[5] if len(sys.argv) > 5 else kname  # substring of the mangled name in the cubin
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(out)))
-hdr, rows = r[1], r[2:]
+# several kernels: take the first SASS section whose "Kernel Name" line matches
+start = next(i for i, x in enumerate(r) if x and x[0] == "Kernel Name" and kname in x[1]) + 1
+end = next((i for i in range(start + 1, len(r)) if r[i] and r[i][0] == "Kernel Name"), len(r))
+hdr, rows = r[start], r[start + 1:end]
 si = hdr.index("Warp Stall Sampling (All Samples)")
 dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
 # find the function section
@@ -28,7 +32,7 @@ for ln in lines:
     if m:
         fun = m.group(1)
         continue
-    if fun is None or kname not in fun:
+    if fun is None or fname not in fun:
         continue
     m = re.search(r"//## File \"([^\"]+)\", line (\d+)", ln)
     if m:
