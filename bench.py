@@ -333,7 +333,7 @@ def main():
     def step():
         """one end-to-end solve: host CSC -> device layouts -> solve -> x on the host"""
         t0 = time.perf_counter()
-        full = apc.DeviceMatrix.from_problem(ctx, p) if ws > 1 else None
+        full = apc.DeviceMatrix.from_problem(ctx, p) if ws > 1 and rank == 0 else None  # setup runs on rank 0
         A = apc.DeviceMatrix.from_problem(ctx, p, r0, r1) if ws > 1 else apc.DeviceMatrix.from_problem(ctx, p)
         ctx.sync()
         t1 = time.perf_counter()

@@ -209,10 +209,13 @@ int apc_config_default(apc_solver_config* cfg);
 int apc_solve(apc_mat* a, const double* b, const apc_solver_config* cfg, int plain,
               apc_result** out);
 /* Row-partitioned solve: `shard` holds this rank's rows
- * [r0, r1) on a ctx created with nranks > 1; `full` the whole matrix for the
- * replicated sketch / CUR selection (NULL is allowed for plain != 0).  Every
- * rank passes the full b; per LSQR iteration the ranks exchange one NCCL
- * allreduce of n + 1 doubles ([A_p^T u_p | ||u_p||^2]). */
+ * [r0, r1) on a ctx created with nranks > 1.  Rank 0 passes `full`, the whole
+ * matrix: the sketch, the CUR selection and every preconditioner build run
+ * there and are broadcast (decision, preconditioner, indices); the other
+ * ranks pass NULL (or anything: it is not used) and hold only their rows.
+ * `full` may be NULL everywhere for plain != 0.  Every rank passes the full
+ * b; per LSQR iteration the ranks exchange one allreduce of n + 1 doubles
+ * ([A_p^T u_p | ||u_p||^2]). */
 int apc_solve_sharded(apc_mat* full, apc_mat* shard, const double* b, const apc_solver_config* cfg,
                       int plain, apc_result** out);
 /* SolveHooks (solver.hpp:114-120): diagnostic observers, called on the host

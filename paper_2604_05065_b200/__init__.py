@@ -710,9 +710,11 @@ def solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig, plain: bool = 
           full: Optional[DeviceMatrix] = None, hooks: Optional[SolveHooks] = None) -> SolveResult:
     """Run aplicur_solve (plain=False) or plain_lsqr_solve on a device-resident A.
 
-    With ``full`` given, ``mat`` is this rank's row block (row-partitioned
-    multi-GPU solve: NCCL allreduce per iteration) and ``full`` the whole
-    matrix used for the replicated sketch / CUR selection."""
+    On a multi-rank context ``mat`` is this rank's row block (row-partitioned
+    multi-GPU solve: one allreduce per LSQR iteration).  Rank 0 passes
+    ``full``, the whole matrix: the sketch, the CUR selection and every
+    preconditioner build run there and are broadcast; the other ranks pass
+    ``full=None`` and hold only their rows."""
     lib = load_library()
     b = np.ascontiguousarray(b, dtype=np.float64)
     assert b.size == mat.m

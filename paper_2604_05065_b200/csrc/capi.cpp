@@ -442,8 +442,9 @@ int apc_solve_sharded(apc_mat* full, apc_mat* shard, const double* b, const apc_
     APC_CUDA(cudaSetDevice(shard->ctx->device));
     if (plain) *out = plain_solve(*shard, b, *cfg);
     else {
-      require(full != nullptr, APC_INVALID_ARGUMENT, "apc_solve_sharded: full matrix required for aplicur_solve");
-      *out = aplicur_solve_sharded(*full, *shard, b, *cfg);
+      require(full != nullptr || shard->ctx->rank != 0, APC_INVALID_ARGUMENT,
+              "apc_solve_sharded: rank 0 needs the full matrix for aplicur_solve");
+      *out = aplicur_solve_sharded(full ? *full : *shard, *shard, b, *cfg);
     }
   });
 }

@@ -59,6 +59,18 @@ void comm_allreduce(apc_ctx* ctx, double* buf, i64 count) {
              "ncclAllReduce");
 }
 
+void comm_bcast(apc_ctx* ctx, double* buf, i64 count, int root) {
+  if (ctx->nranks <= 1 || count <= 0) return;
+  if (ctx->host_allreduce) {  // a sum with zeros everywhere but the root: the root's values, exactly
+    if (ctx->rank != root) APC_CUDA(cudaMemsetAsync(buf, 0, sizeof(double) * count, ctx->stream));
+    comm_allreduce(ctx, buf, count);
+    return;
+  }
+  nccl_check(ncclBroadcast(buf, buf, static_cast<size_t>(count), ncclDouble, root, static_cast<ncclComm_t>(ctx->nccl),
+                           ctx->stream),
+             "ncclBroadcast");
+}
+
 }  // namespace apc
 
 extern "C" int apc_nccl_unique_id(void* out128) {

@@ -77,6 +77,9 @@ void precond_apply(apc_ctx* ctx, PrecondDev& p, bool transpose, const double* x,
 
 // allreduce(sum) of a device fp64 buffer over the ctx communicator (no-op at 1 rank)
 void comm_allreduce(apc_ctx* ctx, double* buf, i64 count);
+// broadcast(fp64) of a device buffer from `root` (the root-only setup of the
+// row-sharded solve); no-op at 1 rank
+void comm_bcast(apc_ctx* ctx, double* buf, i64 count, int root);
 // false when the collective cannot be captured in a CUDA graph (host-staged)
 bool comm_graph_safe(const apc_ctx* ctx);
 void comm_init(apc_ctx* ctx, const void* uid);

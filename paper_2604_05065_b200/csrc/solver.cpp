@@ -37,6 +37,112 @@ bool reprecondition_check(double d_cur, double rho, double eps_cur, double nu_pr
 
 bool is_solver_error(const Status& s) { return s.code >= 1 && s.code <= 9; }
 
+// ---- broadcasts of the root-only setup (comm_bcast: fp64; integers are
+// carried as doubles, exact below 2^53)
+void bcast_host(apc_ctx* ctx, Vec& v) {
+  if (v.empty()) return;
+  const i64 cnt = static_cast<i64>(v.size());
+  DBuf<double> d(cnt);
+  APC_CUDA(cudaMemcpyAsync(d.p, v.data(), sizeof(double) * cnt, cudaMemcpyHostToDevice, ctx->stream));
+  comm_bcast(ctx, d.p, cnt, 0);
+  copy_sync(ctx->stream, v.data(), d.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost);
+}
+
+void bcast_scalar(apc_ctx* ctx, double& x) {
+  Vec v{x};
+  bcast_host(ctx, v);
+  x = v[0];
+}
+
+void bcast_dbuf(apc_ctx* ctx, DBuf<double>& d, i64 cnt) {
+  if (ctx->rank != 0) d.alloc(std::max<i64>(1, cnt));
+  if (cnt > 0) comm_bcast(ctx, d.p, cnt, 0);
+}
+
+void bcast_ibuf(apc_ctx* ctx, DBuf<i32>& d, i64 cnt) {
+  std::vector<i32> h(static_cast<size_t>(std::max<i64>(cnt, 0)));
+  if (ctx->rank == 0 && cnt > 0) copy_sync(ctx->stream, h.data(), d.p, sizeof(i32) * cnt, cudaMemcpyDeviceToHost);
+  Vec v(h.begin(), h.end());
+  bcast_host(ctx, v);
+  if (ctx->rank != 0) {
+    d.alloc(std::max<i64>(1, cnt));
+    for (i64 i = 0; i < cnt; ++i) h[i] = static_cast<i32>(v[i]);
+    if (cnt > 0) APC_CUDA(cudaMemcpyAsync(d.p, h.data(), sizeof(i32) * cnt, cudaMemcpyHostToDevice, ctx->stream));
+    APC_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+}
+
+void bcast_csr(apc_ctx* ctx, Csr& c, i64 rows, i64 cols, i64 nnz) {
+  c.rows = rows;
+  c.cols = cols;
+  c.nnz = nnz;
+  bcast_ibuf(ctx, c.ptr, rows + 1);
+  bcast_ibuf(ctx, c.idx, nnz);
+  bcast_dbuf(ctx, c.val, nnz);
+}
+
+// one outer step: the decision, the phase report's setup timings and (when a
+// phase runs) the device preconditioner and its spectra
+void bcast_step(apc_ctx* ctx, int& action, bool& done, bool& final_phase, double& rho, apc_phase_report& rep,
+                PrecondDev& P, PrecondInfo& info) {
+  Vec h{static_cast<double>(action), done ? 1.0 : 0.0, final_phase ? 1.0 : 0.0, rho, rep.t_augment_ms,
+        rep.t_factor_ms, rep.t_precond_ms, static_cast<double>(P.kind), static_cast<double>(P.n),
+        static_cast<double>(P.l), static_cast<double>(P.R.nnz), static_cast<double>(P.B.n > 0 && P.kind == 1),
+        P.sigma_hat, P.sigma_floor, info.sigma_hat, info.sigma_floor, static_cast<double>(info.sigma_cur.size()),
+        static_cast<double>(info.sigma_reg.size())};
+  bcast_host(ctx, h);
+  action = static_cast<int>(h[0]);
+  done = h[1] != 0.0;
+  final_phase = h[2] != 0.0;
+  rho = h[3];
+  rep.t_augment_ms = h[4];
+  rep.t_factor_ms = h[5];
+  rep.t_precond_ms = h[6];
+  if (action != 1) return;
+  P.kind = static_cast<int>(h[7]);
+  P.n = static_cast<i64>(h[8]);
+  P.l = static_cast<i64>(h[9]);
+  const i64 nnz = static_cast<i64>(h[10]), n = P.n, l = P.l;
+  P.sigma_hat = h[12];
+  P.sigma_floor = h[13];
+  info.sigma_hat = h[14];
+  info.sigma_floor = h[15];
+  info.sigma_cur.resize(static_cast<size_t>(h[16]));
+  info.sigma_reg.resize(static_cast<size_t>(h[17]));
+  bcast_host(ctx, info.sigma_cur);
+  bcast_host(ctx, info.sigma_reg);
+  if (P.kind == 0) return;
+  bcast_dbuf(ctx, P.Kf, l * l);
+  bcast_dbuf(ctx, P.Ka, l * l);
+  if (P.kind == 1) {
+    bcast_dbuf(ctx, P.B, n * l);
+  } else {
+    bcast_csr(ctx, P.R, l, n, nnz);
+    bcast_csr(ctx, P.RT, n, l, nnz);
+  }
+  APC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// the CUR outcome of the solve (indices, rho history, status)
+void bcast_result(apc_ctx* ctx, apc_result& r) {
+  Vec h{static_cast<double>(r.status), r.final_rho, static_cast<double>(r.sketch_applications),
+        static_cast<double>(r.rows.size()), static_cast<double>(r.cols.size()),
+        static_cast<double>(r.rho_history.size())};
+  bcast_host(ctx, h);
+  r.status = static_cast<int>(h[0]);
+  r.final_rho = h[1];
+  r.sketch_applications = static_cast<std::uint64_t>(h[2]);
+  Vec rows(r.rows.begin(), r.rows.end()), cols(r.cols.begin(), r.cols.end());
+  rows.resize(static_cast<size_t>(h[3]));
+  cols.resize(static_cast<size_t>(h[4]));
+  r.rho_history.resize(static_cast<size_t>(h[5]));
+  bcast_host(ctx, rows);
+  bcast_host(ctx, cols);
+  bcast_host(ctx, r.rho_history);
+  r.rows.assign(rows.begin(), rows.end());
+  r.cols.assign(cols.begin(), cols.end());
+}
+
 }  // namespace
 
 apc_result* aplicur_solve(apc_mat& a, const double* b, const apc_solver_config& cfg_in, const apc_hooks* hooks) {
@@ -50,6 +156,8 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
                                   const apc_hooks* hooks) {
   require(full.ctx == a.ctx && full.m == a.m && full.n == a.n, APC_INVALID_ARGUMENT,
           "aplicur_solve: full matrix and shard must describe the same A on the same context");
+  require(a.ctx->nranks <= 1 || a.ctx->rank != 0 || (full.r0 == 0 && full.mloc() == full.m), APC_INVALID_ARGUMENT,
+          "aplicur_solve: rank 0 of a row-sharded solve needs the whole matrix");
   auto t_start = clock_t_::now();
   const i64 n = a.n, m = a.m;
   apc_solver_config cfg = resolve_config(cfg_in, n);
@@ -62,11 +170,20 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
   // CUR target: A for the svd variant; the regularised stack [A; mu I] for the
   // svd-free variant whenever mu > 0 (solver.hpp:183-186)
   const bool target_augmented = cfg.variant == 1 && mu > 0.0;
+  // Row-sharded solves (ctx->nranks > 1) run the sketch, the CUR selection and
+  // every preconditioner build on rank 0 only (it alone needs `full`); the
+  // other ranks hold just their row block and receive each phase's decision
+  // and preconditioner by broadcast.  The LSQR phases run on
+  // every rank over the row partition.
+  const bool multi = ctx->nranks > 1;
+  const bool root = !multi || ctx->rank == 0;
   std::unique_ptr<ProfScope> ps_init(new ProfScope("cur_init"));
-  DeviceCur cur(full, cfg.block, cfg.seed, cfg.sketch_xi, cfg.probe_count, cfg.core, cfg.sketch_kind,
-                cfg.max_rank, target_augmented ? mu : 0.0);
+  std::unique_ptr<DeviceCur> curp;
+  if (root)
+    curp.reset(new DeviceCur(full, cfg.block, cfg.seed, cfg.sketch_xi, cfg.probe_count, cfg.core, cfg.sketch_kind,
+                             cfg.max_rank, target_augmented ? mu : 0.0));
   ps_init.reset();
-  i64 max_rank = std::min(cur.target_rows(), n);
+  i64 max_rank = root ? std::min(curp->target_rows(), n) : n;
   if (cfg.max_rank > 0) max_rank = std::min(max_rank, cfg.max_rank);
   const double density = (m * n == 0) ? 0.0 : static_cast<double>(a.nnz_global) / static_cast<double>(m * n);
   const bool implicit_mode = a.sparse && density < 0.10;
@@ -140,137 +257,151 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
     }
   };
 
+  // one outer step's outcome, decided on rank 0 and broadcast
+  enum { kSkip = 0, kRun = 1, kStop = 2 };
   for (i64 outer = 0; outer < cfg.outer_cap && !done; ++outer) {
     apc_phase_report rep{};
     bool final_phase = false;
-    auto t_aug0 = clock_t_::now();
-    bool grew = false;
-    if (cur.rank() < max_rank) {
-      AugmentResult out;
-      {
-        ProfScope ps("augment");
-        out = cur.augment();
-      }
-      if (out.added > 0) {
-        try {
-          ProfScope ps("refresh");
-          cur.refresh();
-          grew = true;
-        } catch (const Status& e) {
-          if (e.code != APC_SINGULAR) throw;
-          cur.rollback_last_augment();
+    int action = kSkip;
+    double rho = 0.0;
+    PrecondDev P;
+    PrecondInfo info;
+    if (root) {
+      DeviceCur& cur = *curp;
+      auto t_aug0 = clock_t_::now();
+      bool grew = false;
+      if (cur.rank() < max_rank) {
+        AugmentResult out;
+        {
+          ProfScope ps("augment");
+          out = cur.augment();
+        }
+        if (out.added > 0) {
+          try {
+            ProfScope ps("refresh");
+            cur.refresh();
+            grew = true;
+          } catch (const Status& e) {
+            if (e.code != APC_SINGULAR) throw;
+            cur.rollback_last_augment();
+            res->status = 1;
+            final_phase = true;
+            done = true;
+          }
+        } else {
           res->status = 1;
           final_phase = true;
           done = true;
         }
       } else {
-        res->status = 1;
+        if (cur.rho() > cfg.eps_cur) res->status = 1;
         final_phase = true;
         done = true;
       }
-    } else {
-      if (cur.rho() > cfg.eps_cur) res->status = 1;
-      final_phase = true;
-      done = true;
-    }
-    rep.t_augment_ms = ms_since(t_aug0);
+      rep.t_augment_ms = ms_since(t_aug0);
 
-    auto t_fac0 = clock_t_::now();
-    std::unique_ptr<ProfScope> ps_fac(new ProfScope("factor"));
-    if (grew) {
-      const i64 l = cur.rank();
-      if (implicit_mode) {
-        // T_R with T_R^T T_R = R R^T (the reference maintains it with
-        // CholGramAccumulator; the from-scratch gram_factor is the same
-        // factor), computed when a preconditioner is next built
-        t_r_stale = true;
-      } else {
-        const i64 added = cur.last_added();
-        // rows of R are stored row-major on the device: added x n == column-major n x added
-        try {
-          qr_acc.append(n, added, cur.r_rows_dev(l - added));
-        } catch (const Status& e) {
-          if (!is_solver_error(e)) throw;
-          qr_acc.clear();
-          qr_acc.append(n, l, cur.r_rows_dev(0));  // full refactorisation
+      auto t_fac0 = clock_t_::now();
+      std::unique_ptr<ProfScope> ps_fac(new ProfScope("factor"));
+      if (grew) {
+        const i64 l = cur.rank();
+        if (implicit_mode) {
+          // T_R with T_R^T T_R = R R^T (the reference maintains it with
+          // CholGramAccumulator; the from-scratch gram_factor is the same
+          // factor), computed when a preconditioner is next built
+          t_r_stale = true;
+        } else {
+          const i64 added = cur.last_added();
+          // rows of R are stored row-major on the device: added x n == column-major n x added
+          try {
+            qr_acc.append(n, added, cur.r_rows_dev(l - added));
+          } catch (const Status& e) {
+            if (!is_solver_error(e)) throw;
+            qr_acc.clear();
+            qr_acc.append(n, l, cur.r_rows_dev(0));  // full refactorisation
+          }
+        }
+        if (cur.rank() >= max_rank) {
+          final_phase = true;
+          done = true;
+          if (cur.rho() > cfg.eps_cur) res->status = 1;
         }
       }
-      if (cur.rank() >= max_rank) {
+      ps_fac.reset();
+      rep.t_factor_ms = ms_since(t_fac0);
+
+      rho = cur.rho();
+      if (rho <= cfg.eps_cur) {
         final_phase = true;
         done = true;
-        if (cur.rho() > cfg.eps_cur) res->status = 1;
+        res->status = 0;
+      }
+      const bool trigger = final_phase || reprecondition_check(d_cur, rho, cfg.eps_cur, cfg.nu_prec);
+      if (trigger && cur.rank() > 0) {
+        if (!res->phases.empty() && res->phases.back().rank == cur.rank()) {
+          action = kStop;  // duplicate rank
+        } else {
+          if (implicit_mode && t_r_stale) {
+            ProfScope ps("factor");
+            auto t_f0 = clock_t_::now();
+            std::vector<i64> rp, ri;
+            Vec rv;
+            cur.rt_csc(rp, ri, rv);
+            t_r_implicit = gram_factor_rows_dev(ctx, n, cur.rank(), cur.r_rowmajor_dev(), rp, ri, rv);
+            t_r_stale = false;
+            rep.t_factor_ms += ms_since(t_f0);
+          }
+          auto t_pre0 = clock_t_::now();
+          try {
+            BuildInputs in;
+            in.ctx = ctx;
+            in.variant = cfg.variant;
+            in.implicit = implicit_mode;
+            in.m = cur.target_rows();
+            in.n = n;
+            in.l = cur.rank();
+            in.mu = mu;
+            in.target_level = rho;
+            in.core_solve_rm = [&cur](const Vec& bb, i64 nc) { return cur.core_solve_rm(bb, nc); };  // U T_R^T
+            if (cfg.variant == 1) in.block = &cur.intersection();  // svd-free: A(I, J)
+            in.t_r = implicit_mode ? &t_r_implicit : &qr_acc.t;
+            in.q_dev = qr_acc.q.p;
+            in.gram = cur.c_gram();
+            in.c_dense = [&cur, &full]() -> Vec {  // only for the QR fallback of gram_factor
+              if (!full.sparse) return cur.c_dense();
+              std::vector<i64> cp, ci;
+              Vec cv;
+              cur.c_csc(cp, ci, cv);
+              const i64 mt = cur.target_rows(), l = cur.rank();
+              Vec dd(static_cast<size_t>(mt * l), 0.0);
+              for (i64 j = 0; j < l; ++j)
+                for (i64 q = cp[j]; q < cp[j + 1]; ++q) dd[j * mt + ci[q]] = cv[q];
+              return dd;
+            };
+            ProfScope ps("precond");
+            if (implicit_mode) cur.rt_csc(in.r_ptr, in.r_idx, in.r_val);
+            build_precond(in, P, info);
+            action = kRun;
+          } catch (const Status& e) {
+            if (!is_solver_error(e)) throw;
+            res->status = 2;
+            action = kStop;
+          }
+          rep.t_precond_ms = ms_since(t_pre0);
+          if (action == kRun && hooks && hooks->on_rebuild) {  // solver.hpp:367
+            const bool svd = cfg.variant == 0;
+            const i64 ns = svd ? static_cast<i64>(std::min(info.sigma_cur.size(), info.sigma_reg.size())) : 0;
+            apc_rebuild_info ri{phase + 1, cfg.variant, cur.rank(), cur.rows().data(), cur.cols().data(), rho,
+                                info.sigma_hat, info.sigma_floor, ns ? info.sigma_cur.data() : nullptr,
+                                ns ? info.sigma_reg.data() : nullptr, ns};
+            hooks->on_rebuild(hooks->user, &ri);
+          }
+        }
       }
     }
-    ps_fac.reset();
-    rep.t_factor_ms = ms_since(t_fac0);
-
-    const double rho = cur.rho();
-    if (rho <= cfg.eps_cur) {
-      final_phase = true;
-      done = true;
-      res->status = 0;
-    }
-    const bool trigger = final_phase || reprecondition_check(d_cur, rho, cfg.eps_cur, cfg.nu_prec);
-    if (trigger && cur.rank() > 0) {
-      if (!res->phases.empty() && res->phases.back().rank == cur.rank()) break;  // duplicate rank
-      if (implicit_mode && t_r_stale) {
-        ProfScope ps("factor");
-        auto t_f0 = clock_t_::now();
-        std::vector<i64> rp, ri;
-        Vec rv;
-        cur.rt_csc(rp, ri, rv);
-        t_r_implicit = gram_factor_rows_dev(ctx, n, cur.rank(), cur.r_rowmajor_dev(), rp, ri, rv);
-        t_r_stale = false;
-        rep.t_factor_ms += ms_since(t_f0);
-      }
+    if (multi) bcast_step(ctx, action, done, final_phase, rho, rep, P, info);
+    if (action == kStop) break;
+    if (action == kRun) {
       ++phase;
-      auto t_pre0 = clock_t_::now();
-      PrecondDev P;
-      PrecondInfo info;
-      try {
-        BuildInputs in;
-        in.ctx = ctx;
-        in.variant = cfg.variant;
-        in.implicit = implicit_mode;
-        in.m = cur.target_rows();
-        in.n = n;
-        in.l = cur.rank();
-        in.mu = mu;
-        in.target_level = rho;
-        in.core_solve_rm = [&cur](const Vec& b, i64 nc) { return cur.core_solve_rm(b, nc); };  // svd form: U T_R^T
-        if (cfg.variant == 1) in.block = &cur.intersection();  // svd-free: A(I, J)
-        in.t_r = implicit_mode ? &t_r_implicit : &qr_acc.t;
-        in.q_dev = qr_acc.q.p;
-        in.gram = cur.c_gram();
-        in.c_dense = [&cur, &full]() -> Vec {  // only for the QR fallback of gram_factor
-          if (!full.sparse) return cur.c_dense();
-          std::vector<i64> cp, ci;
-          Vec cv;
-          cur.c_csc(cp, ci, cv);
-          const i64 mt = cur.target_rows(), l = cur.rank();
-          Vec d(static_cast<size_t>(mt * l), 0.0);
-          for (i64 j = 0; j < l; ++j)
-            for (i64 q = cp[j]; q < cp[j + 1]; ++q) d[j * mt + ci[q]] = cv[q];
-          return d;
-        };
-        ProfScope ps("precond");
-        if (implicit_mode) cur.rt_csc(in.r_ptr, in.r_idx, in.r_val);
-        build_precond(in, P, info);
-      } catch (const Status& e) {
-        if (!is_solver_error(e)) throw;
-        res->status = 2;
-        --phase;
-        break;
-      }
-      rep.t_precond_ms = ms_since(t_pre0);
-      if (hooks && hooks->on_rebuild) {  // solver.hpp:367
-        const bool svd = cfg.variant == 0;
-        const i64 ns = svd ? static_cast<i64>(std::min(info.sigma_cur.size(), info.sigma_reg.size())) : 0;
-        apc_rebuild_info ri{phase, cfg.variant, cur.rank(), cur.rows().data(), cur.cols().data(), rho,
-                            info.sigma_hat, info.sigma_floor, ns ? info.sigma_cur.data() : nullptr,
-                            ns ? info.sigma_reg.data() : nullptr, ns};
-        hooks->on_rebuild(hooks->user, &ri);
-      }
       run_phase(P, final_phase, rho, rep, info);
       if (std::isfinite(rho)) d_cur = rho - cfg.eps_cur;
       res->phases.push_back(rep);
@@ -284,20 +415,25 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
     PrecondDev ident;
     ident.n = n;
     PrecondInfo info;
-    run_phase(ident, true, cur.rho(), rep, info);
+    double rho0 = root ? curp->rho() : 0.0;
+    if (multi) bcast_scalar(ctx, rho0);
+    run_phase(ident, true, rho0, rep, info);
     res->phases.push_back(rep);
     res->spectra.emplace_back();
   }
 
   res->x.resize(static_cast<size_t>(n));
   copy_sync(st, res->x.data(), d_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost);
-  res->final_rho = cur.rho();
+  if (root) {
+    res->final_rho = curp->rho();
+    res->sketch_applications = curp->sketch_applications();
+    res->rows.assign(curp->rows().begin(), curp->rows().end());
+    res->cols.assign(curp->cols().begin(), curp->cols().end());
+    res->rho_history = curp->rho_history();
+  }
+  if (multi) bcast_result(ctx, *res);
   res->final_relres = bnorm > 0.0 ? std::sqrt(residual(a, vw, d_x.p, d_b.p, nullptr)) / bnorm : 0.0;
-  res->sketch_applications = cur.sketch_applications();
   res->system_matvecs = matvecs;
-  res->rows.assign(cur.rows().begin(), cur.rows().end());
-  res->cols.assign(cur.cols().begin(), cur.cols().end());
-  res->rho_history = cur.rho_history();
   res->total_ms = ms_since(t_start);
   res->setup_ms = res->total_ms - res->lsqr_ms;
   SetupProf::add("lsqr_phases(total)", res->lsqr_ms);

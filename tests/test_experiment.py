@@ -68,7 +68,7 @@ def test_run_experiment_files_problem(apc, ctx, tmp_path):
         assert m["median_final_relres"] == sorted(r["final_relres"] for r in recs)[1]
         assert m["median_system_matvecs"] == sorted(float(r["system_matvecs"]) for r in recs)[1]
         for r in recs:
-            assert (out / r["trace_file"]).exists()
+            assert (out / r["trace"]).exists()  # report_io.hpp:101
             assert r["optimal_relres"] == 0.0 and r["final_relres_plain"] > 0.0
             assert {"method", "trial", "seed", "wall_ms", "status", "phases", "config"} <= set(r)
     # the same solve through the API: the cell's record holds its numbers

@@ -1,7 +1,9 @@
 """Row-sharded aplicur_solve with world size 2 through the library's own
 sharded entry (apc_solve_sharded) and kernels: two processes share the one
 B200, each owning half of A's rows (balanced by nnz, apc_partition_rows) for
-the LSQR operator, with the host-staged collective backend
+the LSQR operator; rank 0 alone holds the whole matrix and runs the sketch,
+the CUR selection and the preconditioner builds, which reach rank 1 by
+broadcast; with the host-staged collective backend
 (apc_ctx_create_host_comm) summing [A_p^T u_p | ||u_p||^2] and the residual
 norms over gloo in rank order (solver.hpp:204-262,
 matrix.hpp:175-195).  Against the single-rank solve: CUR indices bit-exact,
@@ -55,7 +57,9 @@ def _rank_main(rank, world, port, case, out_path):
     p = apc.Problem(cfg_id, m, n)
     row_nnz = np.bincount(p.rowidx, minlength=p.m).astype(np.int64) if p.sparse else None
     bounds = apc.partition_rows(p.m, world, row_nnz)
-    full = apc.DeviceMatrix.from_problem(ctx, p)
+    # rank 0 alone holds the whole matrix (sketch, CUR, preconditioner builds);
+    # rank 1 holds only its rows and receives each phase's preconditioner
+    full = apc.DeviceMatrix.from_problem(ctx, p) if rank == 0 else None
     shard = apc.DeviceMatrix.from_problem(ctx, p, int(bounds[rank]), int(bounds[rank + 1]))
     r = apc.aplicur_solve(shard, p.b, apc.SolverConfig(**knobs), full=full)
     res = dict(x=r.x, I=r.row_indices, J=r.col_indices, rho=r.rho_history, iters=[ph.lsqr_iters for ph in r.phases],
@@ -64,7 +68,8 @@ def _rank_main(rank, world, port, case, out_path):
     with open(f"{out_path}.{rank}", "wb") as f:
         pickle.dump(res, f)
     shard.free()
-    full.free()
+    if full is not None:
+        full.free()
     ctx.close()
     dist.destroy_process_group()
 
