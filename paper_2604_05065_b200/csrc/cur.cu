@@ -1996,7 +1996,9 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
       cudaStream_t cs;
       APC_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
       APC_CUDA(cudaStreamWaitEvent(cs, ready, 0));
-      constexpr i64 kChunk = 1 << 22;  // 32 MB of doubles per staging buffer
+      // small chunks: the main thread's short synchronous copies share the
+      // copy engine and must not queue behind a long one
+      static const i64 kChunk = std::getenv("APC_ZTOL_CHUNK") ? std::atoll(std::getenv("APC_ZTOL_CHUNK")) : (1 << 17);
       double* stage[2] = {nullptr, nullptr};
       const i64 cap = std::min<i64>(kChunk, std::max<i64>(1, total));
       APC_CUDA(cudaMallocHost(&stage[0], sizeof(double) * cap));
@@ -2246,7 +2248,8 @@ void DeviceCur::refresh() {
 void DeviceCur::launch_core_solve(const double* rhs_rm, double* out_rm, i64 ncols) const {
   cudaStream_t st = ctx_->stream;
   const i64 l = core_l_;
-  if (l <= 1024 && ncols <= 4096 && !std::getenv("APC_CORE_SOLVE_THREAD")) {
+  static const bool force_warp = std::getenv("APC_CORE_SOLVE_WARP") != nullptr;
+  if (l <= 1024 && (ncols <= 4096 || force_warp) && !std::getenv("APC_CORE_SOLVE_THREAD")) {
     const unsigned g = static_cast<unsigned>((ncols * 32 + 127) / 128);
     const int li = static_cast<int>(l);
     if (l <= 128)
