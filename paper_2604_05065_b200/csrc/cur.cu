@@ -550,8 +550,14 @@ void launch_sketch_gauss_exact(cudaStream_t st, const double* S, int s, const do
 // Shared layouts keep the fragment loads conflict-free: S chunk [k][row]
 // (stride 100 = 4 mod 16 doubles), A chunk [col][k] (stride 36).
 // ---------------------------------------------------------------------------
-constexpr int kDI = 96, kDJ = 64, kDK = 32, kDSL = kDI + 4, kDAL = kDK + 4;
-constexpr int kDStage = kDK * kDSL + kDJ * kDAL;  // doubles per stage
+// sketch-row tile DI: 112 rows cover s <= 112 in one tile (C3's s = 111 ran
+// as 96 + a 15-live-row tile: 42% of its MMAs on padding), 96 otherwise
+constexpr int kDJ = 64, kDK = 32, kDAL = kDK + 4;
+template <int DI>
+struct DmmaTile {
+  static constexpr int SL = DI + 4;                  // S chunk stride (doubles): 4 mod 16 keeps fragments conflict-free
+  static constexpr int Stage = kDK * SL + kDJ * kDAL;  // doubles per stage
+};
 
 __device__ __forceinline__ void dmma_m8n8k4(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
@@ -565,14 +571,21 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes));
 }
 
+template <int kDI>
 __global__ void __launch_bounds__(256, 2)
 sketch_gauss_dmma_kernel(const double* __restrict__ S, int s, const double* __restrict__ A, long long m,
                          long long n, double* __restrict__ Y) {
+  constexpr int kDSL = DmmaTile<kDI>::SL, kDStage = DmmaTile<kDI>::Stage;
   extern __shared__ double dsm[];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const long long i0 = static_cast<long long>(blockIdx.y) * kDI;
   const long long j0 = static_cast<long long>(blockIdx.x) * kDJ;
+  // split over k (grid.z): this CTA's chunk range; partial Y per split
+  const long long nkall = (m + kDK - 1) / kDK;
+  const long long kper = (nkall + gridDim.z - 1) / gridDim.z;
+  const long long kc0 = blockIdx.z * kper, kc1 = kc0 + kper < nkall ? kc0 + kper : nkall;
+  Y += static_cast<long long>(blockIdx.z) * s * n;
   auto stage = [&](int buf, long long k0) {
     double* Ss = dsm + buf * kDStage;
     double* As = Ss + kDK * kDSL;
@@ -595,12 +608,12 @@ sketch_gauss_dmma_kernel(const double* __restrict__ S, int s, const double* __re
   double acc[kDI / 8][2];
 #pragma unroll
   for (int q = 0; q < kDI / 8; ++q) acc[q][0] = acc[q][1] = 0.0;
-  const long long nk = (m + kDK - 1) / kDK;
-  stage(0, 0);
+  const long long nk = kc1 > kc0 ? kc1 - kc0 : 0;
+  if (nk > 0) stage(0, kc0 * kDK);
   for (long long c = 0; c < nk; ++c) {
     const int buf = static_cast<int>(c & 1);
     if (c + 1 < nk) {
-      stage(buf ^ 1, (c + 1) * kDK);
+      stage(buf ^ 1, (kc0 + c + 1) * kDK);
       asm volatile("cp.async.wait_group 1;\n" ::);
     } else {
       asm volatile("cp.async.wait_group 0;\n" ::);
@@ -630,16 +643,49 @@ sketch_gauss_dmma_kernel(const double* __restrict__ S, int s, const double* __re
   }
 }
 
-void launch_sketch_gauss_dmma(cudaStream_t st, const double* S, int s, const double* A, long long m, long long n,
-                              double* Y) {
+// Y = sum of the k-split partials, split order
+__global__ void dmma_split_sum_kernel(const double* __restrict__ part, int splits, long long cnt,
+                                      double* __restrict__ Y) {
+  const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= cnt) return;
+  double v = part[q];
+  for (int z = 1; z < splits; ++z) v += part[z * cnt + q];
+  Y[q] = v;
+}
+
+template <int DI>
+void launch_sketch_gauss_dmma_t(apc_ctx* ctx, const double* S, int s, const double* A, long long m, long long n,
+                                double* Y) {
+  cudaStream_t st = ctx->stream;
   static bool attr = false;
-  const int smem = 2 * kDStage * static_cast<int>(sizeof(double));
+  const int smem = 2 * DmmaTile<DI>::Stage * static_cast<int>(sizeof(double));
   if (!attr) {
-    APC_CUDA(cudaFuncSetAttribute(sketch_gauss_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    APC_CUDA(cudaFuncSetAttribute(sketch_gauss_dmma_kernel<DI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  dim3 grid(static_cast<unsigned>((n + kDJ - 1) / kDJ), static_cast<unsigned>((s + kDI - 1) / kDI));
-  sketch_gauss_dmma_kernel<<<grid, 256, smem, st>>>(S, s, A, m, n, Y);
+  // k splits until the grid fills the co-resident slots (2 CTAs per SM)
+  const long long tiles = ((n + kDJ - 1) / kDJ) * ((s + DI - 1) / DI);
+  const long long slots = 2LL * ctx->num_sms;
+  const long long nkall = (m + kDK - 1) / kDK;
+  const int splits = static_cast<int>(std::max<long long>(1, std::min<long long>((slots + tiles - 1) / std::max<long long>(1, tiles),
+                                                                                   nkall / 8)));
+  dim3 grid(static_cast<unsigned>((n + kDJ - 1) / kDJ), static_cast<unsigned>((s + DI - 1) / DI),
+            static_cast<unsigned>(splits));
+  if (splits == 1) {
+    sketch_gauss_dmma_kernel<DI><<<grid, 256, smem, st>>>(S, s, A, m, n, Y);
+    return;
+  }
+  DBuf<double> part(static_cast<long long>(splits) * s * n);
+  sketch_gauss_dmma_kernel<DI><<<grid, 256, smem, st>>>(S, s, A, m, n, part.p);
+  const long long cnt = static_cast<long long>(s) * n;
+  dmma_split_sum_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, st>>>(part.p, splits, cnt, Y);
+  APC_CUDA(cudaStreamSynchronize(st));  // part goes out of scope
+}
+
+void launch_sketch_gauss_dmma(apc_ctx* ctx, const double* S, int s, const double* A, long long m, long long n,
+                              double* Y) {
+  if (s <= 112) launch_sketch_gauss_dmma_t<112>(ctx, S, s, A, m, n, Y);
+  else launch_sketch_gauss_dmma_t<96>(ctx, S, s, A, m, n, Y);
 }
 
 // sparse A with a Gaussian S: per (i, j) chain over the stored rows of column j
@@ -1960,7 +2006,7 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
     upload(ctx_, d_S, S.data(), s_ * m_);
     APC_CUDA(cudaEventRecord(ev0, st));
     if (!a.sparse && sketch_kind == 2) {
-      launch_sketch_gauss_dmma(st, d_S.p, (int)s_, a.dense.p, m_, n_, Y_.p);
+      launch_sketch_gauss_dmma(ctx_, d_S.p, (int)s_, a.dense.p, m_, n_, Y_.p);
     } else if (!a.sparse) {
       launch_sketch_gauss_exact(st, d_S.p, (int)s_, a.dense.p, m_, n_, Y_.p);
     } else {
