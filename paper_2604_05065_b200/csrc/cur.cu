@@ -2162,11 +2162,12 @@ AugmentResult DeviceCur::augment() {
   if (l > 0) {
     DBuf<double> d_rj(l * b), d_hj(l * b);
     gather_rcols_rm_kernel<<<nb(l * b), kT, 0, st>>>(Rrm_.p, n_, l, d_jp.p, b, d_rj.p);
-    core_solve_cols_kernel<<<nb(b, 128), 128, 0, st>>>(d_rj.p, d_hj.p, l, b, core_kind_, core_h_.p, core_a_.p,
-                                                       core_perm_.p);
+    // b columns only: warp per column (a thread per column left b threads
+    // running l^2-long chains: ~5 ms per augment at C1's l = 500)
+    launch_core_solve(d_rj.p, d_hj.p, b);
     d_urj.alloc(l * b);
     rm_to_cm_kernel<<<nb(l * b), kT, 0, st>>>(d_hj.p, l, b, d_urj.p);
-    ctx_->launches += 3;
+    ctx_->launches += 2;
   }
   // E^col = A(:, J+) - C urj, rows I zeroed (m x b)
   DBuf<double> ecol(std::max<i64>(1, mt_ * b));
