@@ -102,6 +102,14 @@ int apc_dgemm(apc_ctx* ctx, int transa, int transb, int64_t m, int64_t n, int64_
               int64_t ldc);
 int apc_dtrsm_right_upper(apc_ctx* ctx, int64_t m, int64_t n, const double* T_dev, int64_t ldt, double* B_dev,
                           int64_t ldb);
+/* The l x l algebra of every rebuild (dense_small.cu): in-place upper
+ * Cholesky of a column-major k x k matrix (chol_upper, dense_factor.hpp:229-244;
+ * lower part zeroed), *bad = -1 or the first column with a non-positive pivot
+ * (the caller's APC_NOT_POSITIVE); and X <- T^{-1} X or T^{-T} X for a
+ * row-major k x ncols X and upper column-major T (tri_solve on every column,
+ * dense_factor.hpp:406-424; APC_SINGULAR on a zero diagonal). */
+int apc_dpotrf_upper(apc_ctx* ctx, int64_t k, double* A_dev, int64_t* bad);
+int apc_dtrsm_rows(apc_ctx* ctx, int64_t k, const double* T_dev, double* X_dev, int64_t ncols, int transpose);
 
 /* ---- row partitioning for multi-GPU -------------------- */
 /* bounds[0..nranks]: contiguous row blocks balanced by nnz when row_nnz is

@@ -161,6 +161,8 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
         "apc_dgemm": (C.c_int, [vp, C.c_int, C.c_int, _i64, _i64, _i64, C.c_double, vp, _i64, vp, _i64, C.c_double,
                                 vp, _i64]),
         "apc_dtrsm_right_upper": (C.c_int, [vp, _i64, _i64, vp, _i64, vp, _i64]),
+        "apc_dpotrf_upper": (C.c_int, [vp, _i64, vp, _i64p]),
+        "apc_dtrsm_rows": (C.c_int, [vp, _i64, vp, vp, _i64, C.c_int]),
         "apc_op_apply_host": (C.c_int, [vp, C.c_double, C.c_int, C.c_int, _dp, _dp]),
         "apc_partition_rows": (C.c_int, [_i64, _i64p, C.c_int, _i64p]),
         "apc_rng_fill": (C.c_int, [_u64, C.c_int, _u64, C.c_int, _u64, _i64, vp]),

@@ -12,6 +12,7 @@
 
 #include "apc_internal.hpp"
 #include "blas.hpp"
+#include "dense_small.hpp"
 #include "host_rng.hpp"
 #include "rng_dev.hpp"
 #include "lsqr.hpp"
@@ -321,6 +322,22 @@ int apc_dtrsm_right_upper(apc_ctx* ctx, int64_t m, int64_t n, const double* T, i
   return guard(ctx, [&] {
     require(m >= 0 && n >= 0, APC_INVALID_ARGUMENT, "apc_dtrsm_right_upper: negative shape");
     dtrsm_right_upper(ctx, m, n, T, ldt, B, ldb);
+    APC_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int apc_dpotrf_upper(apc_ctx* ctx, int64_t k, double* A, int64_t* bad) {
+  return guard(ctx, [&] {
+    require(k >= 0, APC_INVALID_ARGUMENT, "apc_dpotrf_upper: negative shape");
+    const int b = k > 0 ? dpotrf_upper_dev(ctx, k, A) : -1;
+    if (bad) *bad = b;
+  });
+}
+
+int apc_dtrsm_rows(apc_ctx* ctx, int64_t k, const double* T, double* X, int64_t ncols, int transpose) {
+  return guard(ctx, [&] {
+    require(k >= 0 && ncols >= 0, APC_INVALID_ARGUMENT, "apc_dtrsm_rows: negative shape");
+    dtrsm_rows_dev(ctx, k, T, X, ncols, transpose != 0);
     APC_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }

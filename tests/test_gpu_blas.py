@@ -54,3 +54,53 @@ def test_dtrsm_right_upper(apc, ctx, m, n):
                                                      C.c_void_p(dB.data_ptr()), m) == 0
     X = dB.cpu().numpy().reshape(n, m).T
     assert np.allclose(X @ T, B, rtol=0, atol=1e-11 * np.abs(B).max())
+
+
+@pytest.mark.parametrize("k", [1, 7, 64, 65, 250, 1000])
+def test_dpotrf_upper_matches_numpy(apc, ctx, k):
+    """Blocked device Cholesky (dense_small.cu) vs numpy: T upper, T^T T = G,
+    lower part zeroed; a non-positive pivot is reported with its column."""
+    import ctypes as C
+
+    rng = np.random.default_rng(k)
+    X = rng.standard_normal((2 * k + 3, k))
+    G = X.T @ X
+    d = _dev(G)
+    bad = C.c_int64(7)
+    lib = apc.load_library()
+    assert lib.apc_dpotrf_upper(ctx.h, k, C.c_void_p(d.data_ptr()), C.byref(bad)) == 0
+    assert bad.value == -1
+    T = d.cpu().numpy().reshape(k, k).T
+    assert np.all(np.tril(T, -1) == 0.0) and np.all(np.diag(T) > 0)
+    want = np.linalg.cholesky(G).T
+    assert np.max(np.abs(T - want)) <= 1e-10 * np.max(np.abs(want))
+    if k >= 3:  # make column 2 dependent on columns 0, 1: pivot 2 is (numerically) not positive
+        X[:, 2] = X[:, 0] - X[:, 1]
+        G2 = X.T @ X
+        G2[2, 2] -= 1e-3 * abs(G2[2, 2])
+        d2 = _dev(G2)
+        assert lib.apc_dpotrf_upper(ctx.h, k, C.c_void_p(d2.data_ptr()), C.byref(bad)) == 0
+        assert bad.value == 2
+
+
+@pytest.mark.parametrize("transpose", [False, True])
+@pytest.mark.parametrize("k,ncols", [(1, 3), (50, 50), (500, 37), (1000, 1000)])
+def test_dtrsm_rows_matches_numpy(apc, ctx, k, ncols, transpose):
+    """X <- T^{-1} X / T^{-T} X for every column (tri_solve, dense_factor.hpp:406-424)."""
+    import ctypes as C
+
+    rng = np.random.default_rng(k + ncols)
+    T = np.triu(rng.standard_normal((k, k))) + 4.0 * np.eye(k)
+    X = rng.standard_normal((k, ncols))
+    dT = _dev(T)
+    dX = torch.from_numpy(np.ascontiguousarray(X).reshape(-1).copy()).cuda()  # row-major k x ncols
+    lib = apc.load_library()
+    assert lib.apc_dtrsm_rows(ctx.h, k, C.c_void_p(dT.data_ptr()), C.c_void_p(dX.data_ptr()), ncols,
+                              int(transpose)) == 0
+    got = dX.cpu().numpy().reshape(k, ncols)
+    M = T.T if transpose else T
+    assert np.max(np.abs(M @ got - X)) <= 1e-10 * (np.abs(M) @ np.abs(got) + np.abs(X)).max()
+    T[k // 2, k // 2] = 0.0
+    dT = _dev(T)
+    assert lib.apc_dtrsm_rows(ctx.h, k, C.c_void_p(dT.data_ptr()), C.c_void_p(dX.data_ptr()), ncols,
+                              int(transpose)) == 4  # APC_SINGULAR
