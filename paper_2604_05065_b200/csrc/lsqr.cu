@@ -924,10 +924,16 @@ bool pc_expand(LsqrWork* w, const LsqrPtrs& P, PrecondDev& p, const double* x, d
     if (fz.xr) return false;
     const DenseFwdPlan pl = dense_fwd_plan(p.n, p.l, w->ctx->num_sms);
     dim3 grid(static_cast<unsigned>(pl.ntiles), static_cast<unsigned>(pl.nsplit));
+    const PcExpandEpi epi{P, x, out, mode, 0.0, fz.tail, 0.0};
     dense_fwd_kernel<PcExpandEpi><<<grid, kDenseFwdThreads, 0, w->ctx->stream>>>(
         p.B.p, p.n, p.n, p.l, w->s.p, pl.cols_per_split, pl.nsplit > 1 ? w->pcf_part.p : nullptr,
-        pl.nsplit > 1 ? w->pcf_ctr.p : nullptr, done, PcExpandEpi{P, x, out, mode, 0.0, fz.tail, 0.0});
+        pl.nsplit > 1 ? w->pcf_ctr.p : nullptr, done, epi);
     w->ctx->launches++;
+    if (pl.nsplit > 1) {
+      dense_split_epi_kernel<PcExpandEpi><<<static_cast<unsigned>((p.n + 255) / 256), 256, 0, w->ctx->stream>>>(
+          w->pcf_part.p, static_cast<int>(pl.nsplit), p.n, done, epi);
+      w->ctx->launches++;
+    }
     return true;
   }
   pc_expand_kernel<<<nb(w->n), kVecThreads, 0, w->ctx->stream>>>(

@@ -124,28 +124,15 @@ dense_fwd_kernel(const double* __restrict__ A, long long ld, long long mloc, lon
         if (ok[k]) acc[k] += __ldg(ab + c * ld + k * kDenseFwdThreads) * xc;
     }
   }
-  double pre[R];  // epilogue inputs (loaded only by the CTA that finishes the tile; in flight
-                 // while the split partials are summed)
-  if (nsplit > 1) {
+  if (nsplit > 1) {  // partials only: dense_split_epi_kernel sums them and runs the epilogue
 #pragma unroll
     for (int k = 0; k < R; ++k)
       if (ok[k]) part[blockIdx.y * mloc + r[k]] = acc[k];
-    if (!elect_last_block(tile_ctr + tile, nsplit)) return;
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-      pre[k] = ok[k] ? epi.load(r[k]) : 0.0;
-      acc[k] = 0.0;
-    }
-    for (int sp = 0; sp < nsplit; ++sp) {
-#pragma unroll
-      for (int k = 0; k < R; ++k)
-        if (ok[k]) acc[k] += ((volatile double*)part)[sp * mloc + r[k]];
-    }
+    return;
   }
-  else {
+  double pre[R];
 #pragma unroll
-    for (int k = 0; k < R; ++k) pre[k] = ok[k] ? epi.load(r[k]) : 0.0;
-  }
+  for (int k = 0; k < R; ++k) pre[k] = ok[k] ? epi.load(r[k]) : 0.0;
   epi.begin();
   double sq = 0.0;
 #pragma unroll
@@ -153,6 +140,28 @@ dense_fwd_kernel(const double* __restrict__ A, long long ld, long long mloc, lon
     if (ok[k]) sq += epi.row(r[k], acc[k], pre[k]);
   sq = block_sum<kDenseFwdThreads>(sq, red);
   epi.tile_done(static_cast<unsigned>(tile), gridDim.x, sq);
+}
+
+// the split partials of dense_fwd_kernel summed in split order, thread per
+// row (the loads of one row are independent and in flight together), then the
+// epilogue; one norm partial per CTA.  A separate launch: the last CTA of a
+// tile used to sum every split of its 2048 rows with one dependent load after
+// another (~60 us for the 62 splits of an explicit basis B, n x l = 1e4 x 1000)
+template <class Epi>
+__global__ void __launch_bounds__(256)
+dense_split_epi_kernel(const double* __restrict__ part, int nsplit, long long mloc, const int* done, Epi epi) {
+  __shared__ double red[32];
+  if (done && *done) return;
+  const long long r = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x;
+  double pre = 0.0, acc = 0.0;
+  if (r < mloc) {
+    pre = epi.load(r);
+    for (int sp = 0; sp < nsplit; ++sp) acc += __ldcg(part + sp * mloc + r);
+  }
+  epi.begin();
+  double sq = r < mloc ? epi.row(r, acc, pre) : 0.0;
+  sq = block_sum<256>(sq, red);
+  epi.tile_done(blockIdx.x, gridDim.x, sq);
 }
 
 // ---------------------------------------------------------------------------
@@ -389,6 +398,11 @@ void launch_dense_fwd(apc_mat& a, const double* x, const int* done, Epi epi, cud
   dense_fwd_kernel<Epi><<<grid, kDenseFwdThreads, 0, st>>>(a.dense.p, a.mloc(), a.mloc(), a.n, x,
                                                              p.cols_per_split, part, ctr, done, epi);
   a.ctx->launches++;
+  if (p.nsplit > 1) {
+    dense_split_epi_kernel<Epi><<<static_cast<unsigned>((a.mloc() + 255) / 256), 256, 0, st>>>(
+        part, static_cast<int>(p.nsplit), a.mloc(), done, epi);
+    a.ctx->launches++;
+  }
 }
 
 // co-resident CTAs of a grid-stride forward kernel (cached occupancy)
