@@ -440,13 +440,13 @@ __global__ void heavy_walk_kernel(const unsigned* __restrict__ keys, const unsig
 // double-buffered shared memory with a register prefetch of the next chunk;
 // each thread owns a (GI/16) x 4 block strided by 16 so shared reads are
 // conflict-free or broadcast.
-constexpr int kGJ = 64, kGK = 16, kGC = kGJ / 16;
+constexpr int kGK = 16;
 
-template <int kGI>
+template <int kGI, int kGJ>
 __global__ void __launch_bounds__(256)
 sketch_gauss_dense_kernel(const double* __restrict__ S, int s, const double* __restrict__ A, long long m,
                           long long n, double* __restrict__ Y) {
-  constexpr int kGA = kGI / 16;
+  constexpr int kGA = kGI / 16, kGC = kGJ / 16;
   __shared__ double Ss[2][kGK][kGI];
   __shared__ double As[2][kGK][kGJ];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
@@ -519,8 +519,18 @@ sketch_gauss_dense_kernel(const double* __restrict__ S, int s, const double* __r
     }
 }
 
-void launch_sketch_gauss_exact(cudaStream_t st, const double* S, int s, const double* A, long long m, long long n,
-                               double* Y) {
+template <int GI>
+void launch_gauss_exact_gi(cudaStream_t st, int gj, dim3 grid, const double* S, int s, const double* A, long long m,
+                           long long n, double* Y) {
+  switch (gj) {
+    case 16: sketch_gauss_dense_kernel<GI, 16><<<grid, 256, 0, st>>>(S, s, A, m, n, Y); break;
+    case 32: sketch_gauss_dense_kernel<GI, 32><<<grid, 256, 0, st>>>(S, s, A, m, n, Y); break;
+    default: sketch_gauss_dense_kernel<GI, 64><<<grid, 256, 0, st>>>(S, s, A, m, n, Y); break;
+  }
+}
+
+void launch_sketch_gauss_exact(cudaStream_t st, int num_sms, const double* S, int s, const double* A, long long m,
+                               long long n, double* Y) {
   int best = 96;
   long long pad = (s + 95) / 96 * 96;
   for (int gi : {112, 64, 32}) {  // fewest padded rows; ties keep the larger tile
@@ -530,12 +540,18 @@ void launch_sketch_gauss_exact(cudaStream_t st, const double* S, int s, const do
       best = gi;
     }
   }
-  dim3 grid(static_cast<unsigned>((n + kGJ - 1) / kGJ), static_cast<unsigned>((s + best - 1) / best));
+  // column tile: the widest that still gives >= 4 CTAs per SM (the k chains
+  // cannot be split, so a narrow output -- C3: s = 111, n = 1e4 -- needs
+  // narrow tiles to fill the GPU: 157 CTAs of 64 columns left half of it idle)
+  const long long rt = (s + best - 1) / best;
+  int gj = 64;
+  while (gj > 16 && ((n + gj - 1) / gj) * rt < 4LL * num_sms) gj /= 2;
+  dim3 grid(static_cast<unsigned>((n + gj - 1) / gj), static_cast<unsigned>(rt));
   switch (best) {
-    case 112: sketch_gauss_dense_kernel<112><<<grid, 256, 0, st>>>(S, s, A, m, n, Y); break;
-    case 64: sketch_gauss_dense_kernel<64><<<grid, 256, 0, st>>>(S, s, A, m, n, Y); break;
-    case 32: sketch_gauss_dense_kernel<32><<<grid, 256, 0, st>>>(S, s, A, m, n, Y); break;
-    default: sketch_gauss_dense_kernel<96><<<grid, 256, 0, st>>>(S, s, A, m, n, Y); break;
+    case 112: launch_gauss_exact_gi<112>(st, gj, grid, S, s, A, m, n, Y); break;
+    case 64: launch_gauss_exact_gi<64>(st, gj, grid, S, s, A, m, n, Y); break;
+    case 32: launch_gauss_exact_gi<32>(st, gj, grid, S, s, A, m, n, Y); break;
+    default: launch_gauss_exact_gi<96>(st, gj, grid, S, s, A, m, n, Y); break;
   }
 }
 
@@ -2008,7 +2024,7 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
     if (!a.sparse && sketch_kind == 2) {
       launch_sketch_gauss_dmma(ctx_, d_S.p, (int)s_, a.dense.p, m_, n_, Y_.p);
     } else if (!a.sparse) {
-      launch_sketch_gauss_exact(st, d_S.p, (int)s_, a.dense.p, m_, n_, Y_.p);
+      launch_sketch_gauss_exact(st, ctx_->num_sms, d_S.p, (int)s_, a.dense.p, m_, n_, Y_.p);
     } else {
       sketch_gauss_csc_kernel<<<nb(n_ * 32), kT, 0, st>>>(d_S.p, (int)s_, a.at.ptr.p, a.at.idx.p, a.at.val.p, n_,
                                                           Y_.p);
