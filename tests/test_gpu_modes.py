@@ -144,3 +144,34 @@ def test_split_transpose_rows_all_modes(apc, ctx):
         s, e = p.colptr[j], p.colptr[j + 1]
         ref[j] = np.dot(p.vals[s:e], u[p.rowidx[s:e]])
     np.testing.assert_allclose(A.apply(u, transpose=True), ref, rtol=1e-11, atol=1e-12 * np.abs(ref).max())
+
+
+def test_fused_nspace_kernel_bit_identical(tmp_path):
+    """The opt-in one-launch n-space kernel (lsqr.cu lsqr_nspace_kernel,
+    APC_NSPACE=1) reproduces the unfused kernels' iterates bit for bit, for the
+    implicit preconditioner and for plain LSQR (the env switch is read once per
+    process, so each variant runs in its own interpreter)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    script = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2604_05065_b200 as apc\n"
+        "ctx = apc.Context(0); p = apc.Problem(5, 60000, 4000)\n"
+        "A = apc.DeviceMatrix.from_problem(ctx, p)\n"
+        "r = apc.aplicur_solve(A, p.b, apc.SolverConfig(mu=1e-8, block=25, max_rank=50, eps_cur=3e-7, seed=1,"
+        " eps_lsqr=1e-8, lsqr_cap=300, trace_sample_stride=0))\n"
+        "q = apc.plain_lsqr_solve(A, p.b, apc.SolverConfig(mu=1e-8, eps_lsqr=1e-8, lsqr_cap=200,"
+        " trace_sample_stride=0))\n"
+        "np.savez(sys.argv[1], x=r.x, ph=np.asarray(r.trace['phibar']), xp=q.x)\n" % str(root))
+    out = {}
+    for v in ("0", "1"):
+        f = tmp_path / f"ns{v}.npz"
+        env = dict(os.environ, APC_NSPACE=v, APC_LSQR_MODE="while", APC_HOT_SELL="1")  # graph path, hot layouts
+        subprocess.run([sys.executable, "-c", script, str(f)], check=True, env=env, timeout=600)
+        out[v] = np.load(f)
+    for k in ("x", "ph", "xp"):
+        assert np.array_equal(out["0"][k], out["1"][k]), k
