@@ -217,10 +217,18 @@ int apc_config_default(apc_solver_config* cfg);
 int apc_solve(apc_mat* a, const double* b, const apc_solver_config* cfg, int plain,
               apc_result** out);
 /* Row-partitioned solve: `shard` holds this rank's rows
- * [r0, r1) on a ctx created with nranks > 1.  Rank 0 passes `full`, the whole
- * matrix: the sketch, the CUR selection and every preconditioner build run
- * there and are broadcast (decision, preconditioner, indices); the other
- * ranks pass NULL (or anything: it is not used) and hold only their rows.
+ * [r0, r1) on a ctx created with nranks > 1 (contiguous blocks in rank order
+ * for the sharded setup).  Two setups:
+ *  - rank 0 passes `full`, the whole matrix: the sketch, the CUR selection
+ *    and every preconditioner build run there and are broadcast (decision,
+ *    preconditioner, indices); the other ranks' `full` is not used;
+ *  - `full` NULL on rank 0 (sharded setup): no rank holds the whole matrix.
+ *    The sketch is one running sum carried from rank to rank in row order,
+ *    E^col stays on the row blocks, the row pivots come from one candidate
+ *    allgather per pivot, R's rows are broadcast by their owners; I, J and
+ *    rho are bit-identical to one rank's.  Rank 0 builds the preconditioner
+ *    (C^T C summed over the ranks) and broadcasts it.  Not for the svd-free
+ *    variant with mu > 0 (its [A; mu I] target): APC_NOT_APPLICABLE.
  * `full` may be NULL everywhere for plain != 0.  Every rank passes the full
  * b; per LSQR iteration the ranks exchange one allreduce of n + 1 doubles
  * ([A_p^T u_p | ||u_p||^2]). */

@@ -130,6 +130,24 @@ class _Trace(C.Structure):
 _lib = None
 
 
+def _preload_nccl() -> None:
+    """One NCCL per process: the library links libnccl.so.2 by soname.  When
+    torch is in the same process it needs its bundled NCCL (newer symbols), so
+    that copy is loaded first when present; whichever is loaded first then
+    satisfies both."""
+    import importlib.util
+
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        cand = Path(base) / "nccl" / "lib" / "libnccl.so.2"
+        if cand.exists():
+            try:
+                C.CDLL(str(cand), mode=C.RTLD_GLOBAL)
+            except OSError:
+                pass
+            return
+
+
 def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
     """Load libapc_b200.so (in-tree build).  Raises if it is missing."""
     global _lib
@@ -140,6 +158,7 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
     p = Path(path) if path else Path(os.environ.get("APC_LIB_PATH") or LIB_PATH)
     if not p.exists():
         raise ApcError(20, f"CUDA library missing: {p} (run __graft_entry__.build())")
+    _preload_nccl()
     lib = C.CDLL(str(p), mode=C.RTLD_GLOBAL)
     vp = C.c_void_p
     sig = {
@@ -713,10 +732,12 @@ def solve(mat: DeviceMatrix, b: np.ndarray, config: SolverConfig, plain: bool = 
     """Run aplicur_solve (plain=False) or plain_lsqr_solve on a device-resident A.
 
     On a multi-rank context ``mat`` is this rank's row block (row-partitioned
-    multi-GPU solve: one allreduce per LSQR iteration).  Rank 0 passes
-    ``full``, the whole matrix: the sketch, the CUR selection and every
-    preconditioner build run there and are broadcast; the other ranks pass
-    ``full=None`` and hold only their rows."""
+    multi-GPU solve: one allreduce per LSQR iteration).  Root-only setup:
+    rank 0 passes ``full``, the whole matrix, and the sketch, the CUR
+    selection and every preconditioner build run there and are broadcast.
+    Sharded setup: every rank passes ``full=None`` and no rank holds the whole
+    matrix (carried sketch, row pivots over the shards, R rows from their
+    owners; the same indices as one rank)."""
     lib = load_library()
     b = np.ascontiguousarray(b, dtype=np.float64)
     assert b.size == mat.m

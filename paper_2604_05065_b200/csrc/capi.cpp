@@ -459,9 +459,8 @@ int apc_solve_sharded(apc_mat* full, apc_mat* shard, const double* b, const apc_
     APC_CUDA(cudaSetDevice(shard->ctx->device));
     if (plain) *out = plain_solve(*shard, b, *cfg);
     else {
-      require(full != nullptr || shard->ctx->rank != 0, APC_INVALID_ARGUMENT,
-              "apc_solve_sharded: rank 0 needs the full matrix for aplicur_solve");
-      *out = aplicur_solve_sharded(full ? *full : *shard, *shard, b, *cfg);
+      // rank 0 with `full`: root-only setup; NULL on rank 0: the sharded setup
+      *out = aplicur_solve_sharded(full && shard->ctx->rank == 0 ? *full : *shard, *shard, b, *cfg);
     }
   });
 }

@@ -20,6 +20,7 @@
 
 #include "blas.hpp"
 #include "cur.hpp"
+#include "lsqr.hpp"
 #include "rng_dev.hpp"
 #include "dev_common.cuh"
 #include "ops.cuh"
@@ -95,14 +96,15 @@ __device__ __forceinline__ SketchSmem sketch_smem(double* base, int s, int xi, i
 __global__ void __launch_bounds__(kSketchWarps * 32)
 sketch_ss_dense_kernel(const double* __restrict__ A, long long m, long long n, int s, int xi,
                        const int* __restrict__ srow, const signed char* __restrict__ ssgn,
-                       double scale, double mu_scale, int aug, double* __restrict__ Y) {
+                       double scale, double mu_scale, int aug, int carry, double* __restrict__ Y) {
   extern __shared__ double ysh[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long j = static_cast<long long>(blockIdx.x) * kSketchWarps + w;
   if (j >= n) return;
   SketchSmem sm = sketch_smem(ysh, s, xi, w);
   double* yc = sm.y;
-  for (int i = lane; i < s; i += 32) yc[i] = 0.0;
+  // carry: the running sums continue from the previous row block's (sharded setup)
+  for (int i = lane; i < s; i += 32) yc[i] = carry ? Y[j * s + i] : 0.0;
   __syncwarp();
   const double* col = A + j * m;
   for (long long k0 = 0; k0 < m; k0 += 32) {
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(1024)
 sketch_ss_dense_inv_kernel(const double* __restrict__ A, long long m, long long n, int s, int xi,
                            const int* __restrict__ cptr, const short* __restrict__ ent,
                            const int* __restrict__ srow, const signed char* __restrict__ ssgn, double scale,
-                           double mu_scale, int aug, double* __restrict__ Y) {
+                           double mu_scale, int aug, int carry, double* __restrict__ Y) {
   // [2 x (kInvCols x kInvRows doubles)] [2 x (kInvRows x xi shorts)] [s x kInvCols doubles: mu tail]
   extern __shared__ __align__(16) double dyn_inv[];
   __shared__ __align__(8) unsigned long long bars[2];
@@ -212,7 +214,7 @@ sketch_ss_dense_inv_kernel(const double* __restrict__ A, long long m, long long 
   const bool own = r < s;
   double acc[kInvCols];
 #pragma unroll
-  for (int c = 0; c < kInvCols; ++c) acc[c] = 0.0;
+  for (int c = 0; c < kInvCols; ++c) acc[c] = (carry && own && c < nc) ? Y[(j0 + c) * s + r] : 0.0;
   // bulk copies need 16-byte aligned columns and copy sizes
   const bool tma = (m % 2 == 0) && (xi % 8 == 0) && ((reinterpret_cast<unsigned long long>(A) & 15ull) == 0) &&
                    ((reinterpret_cast<unsigned long long>(ent) & 15ull) == 0);
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(kSketchWarps * 32)
 sketch_ss_csc_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
                      const double* __restrict__ cval, long long m, long long n, int s, int xi,
                      const int* __restrict__ srow, const signed char* __restrict__ ssgn,
-                     double scale, double mu_scale, int aug, int heavy, double* __restrict__ Y) {
+                     double scale, double mu_scale, int aug, int heavy, int carry, double* __restrict__ Y) {
   extern __shared__ double ysh[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long j = static_cast<long long>(blockIdx.x) * kSketchWarps + w;
@@ -333,7 +335,7 @@ sketch_ss_csc_kernel(const int* __restrict__ cptr, const int* __restrict__ ridx,
   double* yc = sm.y;
   const int b = cptr[j], e = cptr[j + 1];
   if (e - b > heavy) return;  // long columns: the inverted-index kernels below
-  for (int i = lane; i < s; i += 32) yc[i] = 0.0;
+  for (int i = lane; i < s; i += 32) yc[i] = carry ? Y[j * s + i] : 0.0;
   __syncwarp();
   for (int p0 = b; p0 < e; p0 += 32) {
     const int p = p0 + lane;
@@ -387,7 +389,8 @@ __global__ void heavy_walk_kernel(const unsigned* __restrict__ keys, const unsig
                                   long long npairs, const int* __restrict__ bcols, int nb, int s, int xi,
                                   const int* __restrict__ ridx, const double* __restrict__ cval,
                                   const signed char* __restrict__ ssgn, const int* __restrict__ srow,
-                                  double scale, double mu_scale, int aug, long long m, double* __restrict__ Y) {
+                                  double scale, double mu_scale, int aug, long long m, int carry,
+                                  double* __restrict__ Y) {
   const long long key = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (key >= static_cast<long long>(nb) * s) return;
   // segment [lower_bound(key), lower_bound(key + 1)) of the sorted keys
@@ -403,7 +406,7 @@ __global__ void heavy_walk_kernel(const unsigned* __restrict__ keys, const unsig
   const long long b = lower(static_cast<unsigned>(key)), e = lower(static_cast<unsigned>(key + 1));
   const int i = static_cast<int>(key % s);
   const long long j = bcols[key / s];
-  double acc = 0.0;
+  double acc = carry ? Y[j * s + i] : 0.0;
   long long q = b;
   for (; q + 4 <= e; q += 4) {  // loads ahead of the (ordered) add chain
     double sv[4], sg[4];
@@ -445,7 +448,7 @@ constexpr int kGK = 16;
 template <int kGI, int kGJ>
 __global__ void __launch_bounds__(256)
 sketch_gauss_dense_kernel(const double* __restrict__ S, int s, const double* __restrict__ A, long long m,
-                          long long n, double* __restrict__ Y) {
+                          long long n, int carry, double* __restrict__ Y) {
   constexpr int kGA = kGI / 16, kGC = kGJ / 16;
   __shared__ double Ss[2][kGK][kGI];
   __shared__ double As[2][kGK][kGJ];
@@ -484,7 +487,10 @@ sketch_gauss_dense_kernel(const double* __restrict__ S, int s, const double* __r
 #pragma unroll
   for (int a = 0; a < kGA; ++a)
 #pragma unroll
-    for (int c = 0; c < kGC; ++c) acc[a][c] = 0.0;
+    for (int c = 0; c < kGC; ++c) {
+      const long long i = i0 + ty + 16 * a, j = j0 + tx + 16 * c;
+      acc[a][c] = (carry && i < s && j < n) ? Y[j * s + i] : 0.0;  // sharded setup: continue the k chain
+    }
   fetch(0);
   stash(0);
   __syncthreads();
@@ -521,16 +527,16 @@ sketch_gauss_dense_kernel(const double* __restrict__ S, int s, const double* __r
 
 template <int GI>
 void launch_gauss_exact_gi(cudaStream_t st, int gj, dim3 grid, const double* S, int s, const double* A, long long m,
-                           long long n, double* Y) {
+                           long long n, int carry, double* Y) {
   switch (gj) {
-    case 16: sketch_gauss_dense_kernel<GI, 16><<<grid, 256, 0, st>>>(S, s, A, m, n, Y); break;
-    case 32: sketch_gauss_dense_kernel<GI, 32><<<grid, 256, 0, st>>>(S, s, A, m, n, Y); break;
-    default: sketch_gauss_dense_kernel<GI, 64><<<grid, 256, 0, st>>>(S, s, A, m, n, Y); break;
+    case 16: sketch_gauss_dense_kernel<GI, 16><<<grid, 256, 0, st>>>(S, s, A, m, n, carry, Y); break;
+    case 32: sketch_gauss_dense_kernel<GI, 32><<<grid, 256, 0, st>>>(S, s, A, m, n, carry, Y); break;
+    default: sketch_gauss_dense_kernel<GI, 64><<<grid, 256, 0, st>>>(S, s, A, m, n, carry, Y); break;
   }
 }
 
 void launch_sketch_gauss_exact(cudaStream_t st, int num_sms, const double* S, int s, const double* A, long long m,
-                               long long n, double* Y) {
+                               long long n, double* Y, int carry = 0) {
   int best = 96;
   long long pad = (s + 95) / 96 * 96;
   for (int gi : {112, 64, 32}) {  // fewest padded rows; ties keep the larger tile
@@ -548,10 +554,10 @@ void launch_sketch_gauss_exact(cudaStream_t st, int num_sms, const double* S, in
   while (gj > 16 && ((n + gj - 1) / gj) * rt < 4LL * num_sms) gj /= 2;
   dim3 grid(static_cast<unsigned>((n + gj - 1) / gj), static_cast<unsigned>(rt));
   switch (best) {
-    case 112: launch_gauss_exact_gi<112>(st, gj, grid, S, s, A, m, n, Y); break;
-    case 64: launch_gauss_exact_gi<64>(st, gj, grid, S, s, A, m, n, Y); break;
-    case 32: launch_gauss_exact_gi<32>(st, gj, grid, S, s, A, m, n, Y); break;
-    default: launch_gauss_exact_gi<96>(st, gj, grid, S, s, A, m, n, Y); break;
+    case 112: launch_gauss_exact_gi<112>(st, gj, grid, S, s, A, m, n, carry, Y); break;
+    case 64: launch_gauss_exact_gi<64>(st, gj, grid, S, s, A, m, n, carry, Y); break;
+    case 32: launch_gauss_exact_gi<32>(st, gj, grid, S, s, A, m, n, carry, Y); break;
+    default: launch_gauss_exact_gi<96>(st, gj, grid, S, s, A, m, n, carry, Y); break;
   }
 }
 
@@ -707,12 +713,12 @@ void launch_sketch_gauss_dmma(apc_ctx* ctx, const double* S, int s, const double
 // sparse A with a Gaussian S: per (i, j) chain over the stored rows of column j
 __global__ void sketch_gauss_csc_kernel(const double* __restrict__ S, int s, const int* __restrict__ cptr,
                                         const int* __restrict__ ridx, const double* __restrict__ cval,
-                                        long long n, double* __restrict__ Y) {
+                                        long long n, int carry, double* __restrict__ Y) {
   const int lane = threadIdx.x & 31;
   const long long j = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (j >= n) return;
   for (int i = lane; i < s; i += 32) {
-    double acc = 0.0;
+    double acc = carry ? Y[j * s + i] : 0.0;
     for (int p = cptr[j]; p < cptr[j + 1]; ++p) acc += cval[p] * S[static_cast<long long>(ridx[p]) * s + i];
     Y[j * s + i] = acc;
   }
@@ -994,6 +1000,117 @@ lupp_coop_kernel(LuppCoopArgs P) {
     }
     grid.sync();
   }
+}
+
+// ---------------------------------------------------------------------------
+// Row-sharded LUPP: the row pivots of the sharded setup, where every rank
+// holds its block of the rows of E^col (dense_factor.hpp:119-157).  Step k:
+//   lupp_dist_local_kernel: the local unpivoted rows apply step k-1 (the
+//     pivot row's values from the replicated `pr`), then the local best
+//     |w(r, k)| is elected (ties: the lowest GLOBAL row); the last CTA writes
+//     the candidate [mag, global row, that row's w(0..cols-1)];
+//   comm_allgather of the candidates (bit-exact);
+//   lupp_dist_elect_kernel: every rank elects the same winner from the same
+//     gathered candidates (a total order), records it, marks it pivoted on
+//     its owner and copies its row into `pr` for step k+1.
+// The per-row elimination (separately rounded quotient, products and
+// differences; skips on a zero pivot or factor) and the election are
+// lupp_step_kernel's, so the order and magnitudes equal one rank's.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kT)
+lupp_dist_local_kernel(double* __restrict__ W, long long ld, long long rows, long long cols, int k, long long row0,
+                       char* __restrict__ piv, const double* __restrict__ pr, double* __restrict__ pmag,
+                       long long* __restrict__ pidx, unsigned* __restrict__ ctr, double* __restrict__ cand) {
+  __shared__ double sm[kT / 32];
+  __shared__ long long si[kT / 32];
+  const long long r = static_cast<long long>(blockIdx.x) * kT + threadIdx.x;
+  double best = -1.0;
+  long long bidx = LLONG_MAX;
+  if (r < rows && !piv[r]) {
+    if (k > 0) {
+      const double pval = pr[k - 1];
+      if (pval != 0.0) {
+        const double f = W[(k - 1) * ld + r] / pval;
+        if (f != 0.0)
+          for (long long c = k; c < cols; ++c) W[c * ld + r] -= f * pr[c];
+      }
+    }
+    best = fabs(W[static_cast<long long>(k) * ld + r]);
+    bidx = row0 + r;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double om = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (better(om, oi, best, bidx)) {
+      best = om;
+      bidx = oi;
+    }
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sm[w] = best;
+    si[w] = bidx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < kT / 32; ++q)
+      if (better(sm[q], si[q], best, bidx)) {
+        best = sm[q];
+        bidx = si[q];
+      }
+    pmag[blockIdx.x] = best;
+    pidx[blockIdx.x] = bidx;
+  }
+  if (!elect_last_block(ctr, gridDim.x)) return;
+  __shared__ double wbest;
+  __shared__ long long widx;
+  if (threadIdx.x == 0) {
+    best = -1.0;
+    bidx = LLONG_MAX;
+    for (unsigned q = 0; q < gridDim.x; ++q) {
+      const double om = ((volatile double*)pmag)[q];
+      const long long oi = ((volatile long long*)pidx)[q];
+      if (better(om, oi, best, bidx)) {
+        best = om;
+        bidx = oi;
+      }
+    }
+    wbest = best;
+    widx = bidx;
+    cand[0] = best;  // -1: no unpivoted row on this rank
+    cand[1] = best < 0.0 ? -1.0 : static_cast<double>(bidx);
+  }
+  __syncthreads();
+  if (wbest >= 0.0)
+    for (long long c = threadIdx.x; c < cols; c += kT) cand[2 + c] = __ldcg(W + c * ld + (widx - row0));
+}
+
+__global__ void lupp_dist_elect_kernel(const double* __restrict__ gath, int nranks, long long stride, int k,
+                                       long long cols, long long row0, long long rows, char* __restrict__ piv,
+                                       double* __restrict__ pr, long long* __restrict__ order,
+                                       double* __restrict__ mags) {
+  __shared__ int win;
+  if (threadIdx.x == 0) {
+    double best = -1.0;
+    long long bidx = LLONG_MAX;
+    int wp = 0;
+    for (int p = 0; p < nranks; ++p) {
+      const double mg = gath[p * stride];
+      if (mg < 0.0) continue;
+      const long long i = static_cast<long long>(gath[p * stride + 1]);
+      if (better(mg, i, best, bidx)) {
+        best = mg;
+        bidx = i;
+        wp = p;
+      }
+    }
+    order[k] = bidx;
+    mags[k] = best;
+    if (bidx >= row0 && bidx < row0 + rows) piv[bidx - row0] = 1;
+    win = wp;
+  }
+  __syncthreads();
+  for (long long c = threadIdx.x; c < cols; c += blockDim.x) pr[c] = gath[win * stride + 2 + c];
 }
 
 // W (n x s column-major) = E^T with rows in J zeroed (cur.hpp:254-261)
@@ -1564,6 +1681,15 @@ __global__ void gather_sc_kernel(const double* Y, long long s, const long long* 
   SC[e] = Y[J[t] * s + i];
 }
 
+// R(q[t], :) = packed row t (the sharded setup's R rows from their owner)
+__global__ void place_rows_kernel(const double* __restrict__ pk, const long long* __restrict__ q, long long cnt,
+                                  long long n, double* __restrict__ R) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= cnt * n) return;
+  const long long t = e / n, c = e % n;
+  R[q[t] * n + c] = pk[e];
+}
+
 // R(:, J+) from the row-major R (l x b, column-major)
 __global__ void gather_rcols_kernel(const double* R, long long n, long long l, const long long* Jp, long long b,
                                     double* out) {
@@ -1801,11 +1927,44 @@ LuppOut device_lupp(apc_ctx* ctx, double* w, i64 rows, i64 cols, i64 max_pivots)
   return out;
 }
 
+// Pivot order of LUPP over a row-sharded column-major matrix: this rank's
+// rows [row0, row0 + rows) of a rows_global x cols matrix (w destroyed).  Every
+// rank returns the same order (global rows) and magnitudes, equal to
+// device_lupp over the whole matrix.  One step = two launches and one allgather.
+LuppOut device_lupp_dist(apc_ctx* ctx, double* w, i64 rows, i64 row0, i64 rows_global, i64 cols, i64 max_pivots) {
+  LuppOut out;
+  i64 steps = std::min(rows_global, cols);
+  if (max_pivots >= 0) steps = std::min(steps, max_pivots);
+  if (steps <= 0) return out;
+  cudaStream_t st = ctx->stream;
+  const unsigned nbk = std::max(1u, nb(rows));
+  const i64 stride = cols + 2;
+  DBuf<char> piv(std::max<i64>(1, rows));
+  DBuf<long long> order(steps), pidx(nbk);
+  DBuf<double> mags(steps), pmag(nbk), pr(cols), cand(stride), gath(stride * ctx->nranks);
+  DBuf<unsigned> ctr(1);
+  APC_CUDA(cudaMemsetAsync(piv.p, 0, piv.bytes(), st));
+  APC_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned), st));
+  for (i64 k = 0; k < steps; ++k) {
+    lupp_dist_local_kernel<<<nbk, kT, 0, st>>>(w, std::max<i64>(1, rows), rows, cols, static_cast<int>(k), row0,
+                                               piv.p, pr.p, pmag.p, pidx.p, ctr.p, cand.p);
+    comm_allgather(ctx, cand.p, stride, gath.p);
+    lupp_dist_elect_kernel<<<1, 128, 0, st>>>(gath.p, ctx->nranks, stride, static_cast<int>(k), cols, row0, rows,
+                                              piv.p, pr.p, order.p, mags.p);
+  }
+  ctx->launches += 2 * static_cast<std::uint64_t>(steps);
+  APC_CUDA(cudaGetLastError());
+  auto o = download(ctx, order.p, steps);
+  out.order.assign(o.begin(), o.end());
+  out.mags = download(ctx, mags.p, steps);
+  return out;
+}
+
 // ---------------------------------------------------------------------------
 // DeviceCur
 // ---------------------------------------------------------------------------
 DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 probes, int core_kind,
-                     int sketch_kind, i64 max_rank, double aug_mu)
+                     int sketch_kind, i64 max_rank, double aug_mu, bool distributed)
     : a_(a), ctx_(a.ctx), m_(a.m), n_(a.n), block_size_(block), probes_(probes), max_rank_(max_rank),
       mt_(a.m + (aug_mu > 0.0 ? a.n : 0)), amu_(aug_mu > 0.0 ? aug_mu : 0.0), core_kind_(core_kind),
       rho_(std::numeric_limits<double>::infinity()), probe_rng_(seed, Stream::probes) {
@@ -1814,12 +1973,51 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
   require(block >= 1, APC_INVALID_ARGUMENT, "CurState: block size must be >= 1");
   require(block <= n_, APC_INVALID_ARGUMENT, "CurState: block size exceeds column count");
   require(sketch_kind >= 0 && sketch_kind <= 2, APC_INVALID_ARGUMENT, "CurState: sketch kind must be 0, 1 or 2");
-  require(a.r0 == 0 && a.r1 == a.m, APC_NOT_APPLICABLE, "CurState: needs the full matrix on this rank");
+  dist_ = distributed && ctx_->nranks > 1;
+  row0_ = dist_ ? a.r0 : 0;
+  mloc_ = dist_ ? a.mloc() : m_;
+  if (!dist_) {
+    require(a.r0 == 0 && a.r1 == a.m, APC_NOT_APPLICABLE, "CurState: needs the full matrix on this rank");
+  } else {
+    require(amu_ == 0.0, APC_NOT_APPLICABLE,
+            "CurState: the sharded setup has no augmented target [A; mu I] (pass the whole matrix on rank 0)");
+    // every rank's row block: contiguous, in rank order, covering [0, m)
+    const int P = ctx_->nranks;
+    DBuf<double> mine(2), all(2 * P);
+    const double mr[2] = {static_cast<double>(a.r0), static_cast<double>(a.r1)};
+    APC_CUDA(cudaMemcpyAsync(mine.p, mr, sizeof(mr), cudaMemcpyHostToDevice, ctx_->stream));
+    comm_allgather(ctx_, mine.p, 2, all.p);
+    std::vector<double> h = download(ctx_, all.p, 2 * P);
+    bounds_.resize(static_cast<size_t>(P + 1));
+    for (int p = 0; p < P; ++p) {
+      require(h[2 * p] == (p == 0 ? 0.0 : h[2 * p - 1]) && h[2 * p] <= h[2 * p + 1], APC_INVALID_ARGUMENT,
+              "CurState: the sharded setup needs contiguous row blocks in rank order");
+      bounds_[p] = static_cast<i64>(h[2 * p]);
+    }
+    require(h[2 * P - 1] == static_cast<double>(m_), APC_INVALID_ARGUMENT,
+            "CurState: the row blocks of the sharded setup must cover every row");
+    bounds_[P] = m_;
+  }
   s_ = static_cast<i64>(std::ceil(1.1 * static_cast<double>(block)));
   const std::uint64_t emb_seed = splitmix(seed ^ 0x5ce7c3a1b2d4f688ULL);
   cudaStream_t st = ctx_->stream;
   Y_.alloc(std::max<i64>(1, s_ * n_));
   E_.alloc(std::max<i64>(1, s_ * n_));
+  // Y = S A over this rank's rows.  Sharded: ONE running sum per entry of Y in
+  // row order, carried from rank to rank -- rank p continues the sums rank p-1
+  // broadcast, the last rank's Y reaches everyone -- so every chain is the
+  // reference's and Y is bit-identical to one rank's.
+  auto run_carried = [&](const std::function<void(int)>& f) {
+    if (!dist_) {
+      f(0);
+      return;
+    }
+    APC_CUDA(cudaMemsetAsync(Y_.p, 0, Y_.bytes(), st));
+    for (int p = 0; p < ctx_->nranks; ++p) {
+      if (p == ctx_->rank) f(p > 0 ? 1 : 0);
+      comm_bcast(ctx_, Y_.p, s_ * n_, p);
+    }
+  };
   cudaEvent_t ev0, ev1;
   APC_CUDA(cudaEventCreate(&ev0));
   APC_CUDA(cudaEventCreate(&ev1));
@@ -1916,98 +2114,105 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
       APC_CUDA(cudaFuncSetAttribute(sketch_ss_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       APC_CUDA(cudaFuncSetAttribute(sketch_ss_csc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
-    const unsigned g = nb(n_, kSketchWarps);
-    const char* inv_env = std::getenv("APC_SKETCH_INV");
-    const bool inv = !a.sparse && (inv_env ? std::atoi(inv_env) != 0 : true) && s_ <= 1024 && m_ * x < (1LL << 30) &&
-                     ((m_ + kInvRows - 1) / kInvRows) * s_ < (1LL << 30);
-    if (inv) {
-      // chunk-major inverted index of S (rows of A feeding each sketch row, k ascending)
-      const long long cnt = m_ * x;
-      const long long nchunks = (m_ + kInvRows - 1) / kInvRows;
-      DBuf<int> keys(cnt), vals(cnt), skeys(cnt), svals(cnt), cptr(nchunks * (s_ + 1));
-      DBuf<short> ent(cnt + 8);
-      sketch_inv_keys_kernel<<<nb(cnt, 256), 256, 0, st>>>(d_rows.p, cnt, static_cast<int>(x), static_cast<int>(s_),
-                                                           keys.p, vals.p);
-      int end_bit = 1;
-      while ((1LL << end_bit) < nchunks * s_ + 1 && end_bit < 31) ++end_bit;
-      size_t tb = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, svals.p, static_cast<int>(cnt), 0, end_bit,
-                                      st);
-      DBuf<char> tmp(static_cast<long long>(std::max<size_t>(tb, 1)));
-      APC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, svals.p, static_cast<int>(cnt), 0,
-                                               end_bit, st));
-      sketch_inv_pack_kernel<<<nb(cnt, 256), 256, 0, st>>>(svals.p, cnt, static_cast<int>(x), d_sg.p, ent.p);
-      sketch_inv_ptr_kernel<<<nb(nchunks * (s_ + 1), 256), 256, 0, st>>>(skeys.p, cnt, nchunks, static_cast<int>(s_),
-                                                                        static_cast<int>(x), cptr.p);
-      const int threads = static_cast<int>((s_ + 31) / 32 * 32);
-      const long long estride = (kInvRows * x + 7) & ~7LL;
-      const size_t ysm = sizeof(double) * 2 * kInvCols * kInvRows + sizeof(short) * 2 * estride +
-                         (aug ? sizeof(double) * s_ * kInvCols : 0);
-      APC_CUDA(cudaFuncSetAttribute(sketch_ss_dense_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(ysm)));
-      sketch_ss_dense_inv_kernel<<<static_cast<unsigned>((n_ + kInvCols - 1) / kInvCols), threads, ysm, st>>>(
-          a.dense.p, m_, n_, static_cast<int>(s_), static_cast<int>(x), cptr.p, ent.p, d_rows.p, d_sg.p, scale,
-          mu_scale, aug, Y_.p);
-      ctx_->launches += 6;
-      APC_CUDA(cudaGetLastError());
-      APC_CUDA(cudaStreamSynchronize(st));  // temporaries go back to the pool
-    } else if (!a.sparse) {
-      sketch_ss_dense_kernel<<<g, kSketchWarps * 32, smem, st>>>(a.dense.p, m_, n_, (int)s_, (int)x, d_rows.p,
-                                                                d_sg.p, scale, mu_scale, aug, Y_.p);
-    } else {
-      // columns longer than kHeavy go to the row-parallel kernel
-      constexpr int kHeavy = 8192;
-      std::vector<int> cp(static_cast<size_t>(n_ + 1));
-      copy_sync(st, cp.data(), a.at.ptr.p, sizeof(int) * (n_ + 1), cudaMemcpyDeviceToHost);
-      std::vector<int> heavy;
-      for (i64 j = 0; j < n_; ++j)
-        if (cp[j + 1] - cp[j] > kHeavy) heavy.push_back(static_cast<int>(j));
-      sketch_ss_csc_kernel<<<g, kSketchWarps * 32, smem, st>>>(a.at.ptr.p, a.at.idx.p, a.at.val.p, m_, n_, (int)s_,
-                                                              (int)x, d_rows.p, d_sg.p, scale, mu_scale, aug,
-                                                              kHeavy, Y_.p);
-      if (!heavy.empty()) {
-        // inverted-index pass over the long columns, in batches of <= 2^28 pairs
-        require(static_cast<double>(a.at.nnz) * x < 4.0e9, APC_INVALID_ARGUMENT,
-                "sketch: nnz * xi exceeds the 32-bit pair encoding");
-        constexpr long long kMaxPairs = 1LL << 28;
-        size_t h0 = 0;
-        while (h0 < heavy.size()) {
-          std::vector<int> bcols;
-          std::vector<long long> boff;
-          long long tot = 0;
+    const i64 ml = mloc_;  // this rank's rows (all of A unless distributed)
+    const int* srow = d_rows.p + row0_ * x;  // S columns of those rows
+    const signed char* ssg = d_sg.p + row0_ * x;
+    auto sketch_rows = [&](int carry) {
+      if (ml == 0) return;
+      const unsigned g = nb(n_, kSketchWarps);
+      const char* inv_env = std::getenv("APC_SKETCH_INV");
+      const bool inv = !a.sparse && (inv_env ? std::atoi(inv_env) != 0 : true) && s_ <= 1024 && ml * x < (1LL << 30) &&
+                       ((ml + kInvRows - 1) / kInvRows) * s_ < (1LL << 30);
+      if (inv) {
+        // chunk-major inverted index of S (rows of A feeding each sketch row, k ascending)
+        const long long cnt = ml * x;
+        const long long nchunks = (ml + kInvRows - 1) / kInvRows;
+        DBuf<int> keys(cnt), vals(cnt), skeys(cnt), svals(cnt), cptr(nchunks * (s_ + 1));
+        DBuf<short> ent(cnt + 8);
+        sketch_inv_keys_kernel<<<nb(cnt, 256), 256, 0, st>>>(srow, cnt, static_cast<int>(x), static_cast<int>(s_),
+                                                             keys.p, vals.p);
+        int end_bit = 1;
+        while ((1LL << end_bit) < nchunks * s_ + 1 && end_bit < 31) ++end_bit;
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, svals.p, static_cast<int>(cnt), 0, end_bit,
+                                        st);
+        DBuf<char> tmp(static_cast<long long>(std::max<size_t>(tb, 1)));
+        APC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, svals.p, static_cast<int>(cnt), 0,
+                                                 end_bit, st));
+        sketch_inv_pack_kernel<<<nb(cnt, 256), 256, 0, st>>>(svals.p, cnt, static_cast<int>(x), ssg, ent.p);
+        sketch_inv_ptr_kernel<<<nb(nchunks * (s_ + 1), 256), 256, 0, st>>>(skeys.p, cnt, nchunks, static_cast<int>(s_),
+                                                                          static_cast<int>(x), cptr.p);
+        const int threads = static_cast<int>((s_ + 31) / 32 * 32);
+        const long long estride = (kInvRows * x + 7) & ~7LL;
+        const size_t ysm = sizeof(double) * 2 * kInvCols * kInvRows + sizeof(short) * 2 * estride +
+                           (aug ? sizeof(double) * s_ * kInvCols : 0);
+        APC_CUDA(cudaFuncSetAttribute(sketch_ss_dense_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(ysm)));
+        sketch_ss_dense_inv_kernel<<<static_cast<unsigned>((n_ + kInvCols - 1) / kInvCols), threads, ysm, st>>>(
+            a.dense.p, ml, n_, static_cast<int>(s_), static_cast<int>(x), cptr.p, ent.p, srow, ssg, scale,
+            mu_scale, aug, carry, Y_.p);
+        ctx_->launches += 6;
+        APC_CUDA(cudaGetLastError());
+        APC_CUDA(cudaStreamSynchronize(st));  // temporaries go back to the pool
+      } else if (!a.sparse) {
+        sketch_ss_dense_kernel<<<g, kSketchWarps * 32, smem, st>>>(a.dense.p, ml, n_, (int)s_, (int)x, srow, ssg,
+                                                                  scale, mu_scale, aug, carry, Y_.p);
+      } else {
+        // columns longer than kHeavy go to the row-parallel kernel
+        constexpr int kHeavy = 8192;
+        std::vector<int> cp(static_cast<size_t>(n_ + 1));
+        copy_sync(st, cp.data(), a.at.ptr.p, sizeof(int) * (n_ + 1), cudaMemcpyDeviceToHost);
+        std::vector<int> heavy;
+        for (i64 j = 0; j < n_; ++j)
+          if (cp[j + 1] - cp[j] > kHeavy) heavy.push_back(static_cast<int>(j));
+        sketch_ss_csc_kernel<<<g, kSketchWarps * 32, smem, st>>>(a.at.ptr.p, a.at.idx.p, a.at.val.p, ml, n_, (int)s_,
+                                                                (int)x, srow, ssg, scale, mu_scale, aug, kHeavy,
+                                                                carry, Y_.p);
+        if (!heavy.empty()) {
+          // inverted-index pass over the long columns, in batches of <= 2^28 pairs
+          require(static_cast<double>(a.at.nnz) * x < 4.0e9, APC_INVALID_ARGUMENT,
+                  "sketch: nnz * xi exceeds the 32-bit pair encoding");
+          constexpr long long kMaxPairs = 1LL << 28;
+          size_t h0 = 0;
           while (h0 < heavy.size()) {
-            const long long len = cp[heavy[h0] + 1] - cp[heavy[h0]];
-            if (!bcols.empty() && (tot + len) * x > kMaxPairs) break;
-            bcols.push_back(heavy[h0]);
-            boff.push_back(tot);
-            tot += len;
-            ++h0;
+            std::vector<int> bcols;
+            std::vector<long long> boff;
+            long long tot = 0;
+            while (h0 < heavy.size()) {
+              const long long len = cp[heavy[h0] + 1] - cp[heavy[h0]];
+              if (!bcols.empty() && (tot + len) * x > kMaxPairs) break;
+              bcols.push_back(heavy[h0]);
+              boff.push_back(tot);
+              tot += len;
+              ++h0;
+            }
+            const long long npairs = tot * x;
+            const int nbc = static_cast<int>(bcols.size());
+            DBuf<int> d_bcols;
+            DBuf<long long> d_boff;
+            upload(ctx_, d_bcols, bcols.data(), nbc);
+            upload(ctx_, d_boff, boff.data(), nbc);
+            DBuf<unsigned> kin(npairs), kout(npairs), vin(npairs), vout(npairs);
+            heavy_pairs_kernel<<<nb(tot), kT, 0, st>>>(a.at.ptr.p, a.at.idx.p, d_bcols.p, d_boff.p, nbc, tot,
+                                                       (int)s_, (int)x, srow, kin.p, vin.p);
+            int end_bit = 1;
+            while ((1LL << end_bit) < static_cast<long long>(nbc) * s_ && end_bit < 32) ++end_bit;
+            size_t tmp_bytes = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kin.p, kout.p, vin.p, vout.p,
+                                            static_cast<std::int64_t>(npairs), 0, end_bit, st);
+            DBuf<char> tmp(static_cast<i64>(tmp_bytes));
+            APC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, kin.p, kout.p, vin.p, vout.p,
+                                                     static_cast<std::int64_t>(npairs), 0, end_bit, st));
+            heavy_walk_kernel<<<nb(static_cast<long long>(nbc) * s_), kT, 0, st>>>(
+                kout.p, vout.p, npairs, d_bcols.p, nbc, (int)s_, (int)x, a.at.idx.p, a.at.val.p, ssg, srow,
+                scale, mu_scale, aug, ml, carry, Y_.p);
+            ctx_->launches += 3;
+            APC_CUDA(cudaStreamSynchronize(st));
           }
-          const long long npairs = tot * x;
-          const int nbc = static_cast<int>(bcols.size());
-          DBuf<int> d_bcols;
-          DBuf<long long> d_boff;
-          upload(ctx_, d_bcols, bcols.data(), nbc);
-          upload(ctx_, d_boff, boff.data(), nbc);
-          DBuf<unsigned> kin(npairs), kout(npairs), vin(npairs), vout(npairs);
-          heavy_pairs_kernel<<<nb(tot), kT, 0, st>>>(a.at.ptr.p, a.at.idx.p, d_bcols.p, d_boff.p, nbc, tot,
-                                                     (int)s_, (int)x, d_rows.p, kin.p, vin.p);
-          int end_bit = 1;
-          while ((1LL << end_bit) < static_cast<long long>(nbc) * s_ && end_bit < 32) ++end_bit;
-          size_t tmp_bytes = 0;
-          cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kin.p, kout.p, vin.p, vout.p,
-                                          static_cast<std::int64_t>(npairs), 0, end_bit, st);
-          DBuf<char> tmp(static_cast<i64>(tmp_bytes));
-          APC_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, kin.p, kout.p, vin.p, vout.p,
-                                                   static_cast<std::int64_t>(npairs), 0, end_bit, st));
-          heavy_walk_kernel<<<nb(static_cast<long long>(nbc) * s_), kT, 0, st>>>(
-              kout.p, vout.p, npairs, d_bcols.p, nbc, (int)s_, (int)x, a.at.idx.p, a.at.val.p, d_sg.p, d_rows.p,
-              scale, mu_scale, aug, m_, Y_.p);
-          ctx_->launches += 3;
-          APC_CUDA(cudaStreamSynchronize(st));
         }
       }
-    }
+    };
+    run_carried(sketch_rows);
     ctx_->launches++;
     APC_CUDA(cudaEventRecord(ev1, st));
     APC_CUDA(cudaStreamSynchronize(st));
@@ -2019,17 +2224,21 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
     fill_gaussians(rng, S.data(), s_ * m_, scale, true);  // scale * gaussian() in storage order
     embed_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
     DBuf<double> d_S;
-    upload(ctx_, d_S, S.data(), s_ * m_);
+    const i64 ml = mloc_;
+    upload(ctx_, d_S, S.data() + row0_ * s_, s_ * ml);  // S(:, this rank's rows)
     APC_CUDA(cudaEventRecord(ev0, st));
-    if (!a.sparse && sketch_kind == 2) {
-      launch_sketch_gauss_dmma(ctx_, d_S.p, (int)s_, a.dense.p, m_, n_, Y_.p);
-    } else if (!a.sparse) {
-      launch_sketch_gauss_exact(st, ctx_->num_sms, d_S.p, (int)s_, a.dense.p, m_, n_, Y_.p);
-    } else {
-      sketch_gauss_csc_kernel<<<nb(n_ * 32), kT, 0, st>>>(d_S.p, (int)s_, a.at.ptr.p, a.at.idx.p, a.at.val.p, n_,
-                                                          Y_.p);
-    }
-    ctx_->launches++;
+    run_carried([&](int carry) {
+      if (ml == 0) return;
+      if (!a.sparse && sketch_kind == 2 && !dist_) {  // DMMA: not a carried chain (sharded: the exact kernel)
+        launch_sketch_gauss_dmma(ctx_, d_S.p, (int)s_, a.dense.p, ml, n_, Y_.p);
+      } else if (!a.sparse) {
+        launch_sketch_gauss_exact(st, ctx_->num_sms, d_S.p, (int)s_, a.dense.p, ml, n_, Y_.p, carry);
+      } else {
+        sketch_gauss_csc_kernel<<<nb(n_ * 32), kT, 0, st>>>(d_S.p, (int)s_, a.at.ptr.p, a.at.idx.p, a.at.val.p, n_,
+                                                            carry, Y_.p);
+      }
+      ctx_->launches++;
+    });
     APC_CUDA(cudaEventRecord(ev1, st));
     APC_CUDA(cudaStreamSynchronize(st));
   }
@@ -2091,7 +2300,7 @@ DeviceCur::DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 prob
       return 1e-14 * std::sqrt(f2);
     });
   }
-  rowsel_.alloc(std::max<i64>(1, mt_));
+  rowsel_.alloc(std::max<i64>(1, rowsel_len()));
   colsel_.alloc(std::max<i64>(1, n_));
   APC_CUDA(cudaMemsetAsync(rowsel_.p, 0, rowsel_.bytes(), st));
   APC_CUDA(cudaMemsetAsync(colsel_.p, 0, colsel_.bytes(), st));
@@ -2185,41 +2394,44 @@ AugmentResult DeviceCur::augment() {
     rm_to_cm_kernel<<<nb(l * b), kT, 0, st>>>(d_hj.p, l, b, d_urj.p);
     ctx_->launches += 2;
   }
-  // E^col = A(:, J+) - C urj, rows I zeroed (m x b)
-  DBuf<double> ecol(std::max<i64>(1, mt_ * b));
+  // E^col = A(:, J+) - C urj, rows I zeroed (m x b; sharded: this rank's rows)
+  const i64 ml = mloc_, eld = rowsel_len();
+  DBuf<double> ecol(std::max<i64>(1, eld * b));
   DBuf<int> colpos(n_);
   APC_CUDA(cudaMemsetAsync(colpos.p, 0xff, colpos.bytes(), st));
   if (l > 0) set_colpos_kernel<<<nb(l), kT, 0, st>>>(colpos.p, d_J.p, l);
   if (amu_ > 0.0) {  // rows m..m+n-1 of the augmented stack
-    ecol_tail_kernel<<<nb(n_), kT, 0, st>>>(m_, n_, mt_, colpos.p, l, d_jp.p, b, d_urj.p, rowsel_.p, amu_, ecol.p);
+    ecol_tail_kernel<<<nb(n_), kT, 0, st>>>(m_, n_, eld, colpos.p, l, d_jp.p, b, d_urj.p, rowsel_.p, amu_, ecol.p);
     ctx_->launches++;
   }
-  if (!a_.sparse) {
-    dim3 grid(nb(m_), static_cast<unsigned>((b + kEcolTile - 1) / kEcolTile));
-    ecol_dense_kernel<<<grid, kT, 0, st>>>(a_.dense.p, m_, mt_, d_J.p, l, d_jp.p, b, d_urj.p, rowsel_.p, ecol.p);
+  if (ml == 0) {
+    // an empty row block: no local rows of E^col
+  } else if (!a_.sparse) {
+    dim3 grid(nb(ml), static_cast<unsigned>((b + kEcolTile - 1) / kEcolTile));
+    ecol_dense_kernel<<<grid, kT, 0, st>>>(a_.dense.p, ml, eld, d_J.p, l, d_jp.p, b, d_urj.p, rowsel_.p, ecol.p);
     ctx_->launches++;
   } else {
-    DBuf<int> ccnt(m_ + 1), cptr(m_ + 1);
-    crow_count_kernel<<<nb(m_), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, m_, colpos.p, ccnt.p);
-    APC_CUDA(cudaMemsetAsync(ccnt.p + m_, 0, sizeof(int), st));
+    DBuf<int> ccnt(ml + 1), cptr(ml + 1);
+    crow_count_kernel<<<nb(ml), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, ml, colpos.p, ccnt.p);
+    APC_CUDA(cudaMemsetAsync(ccnt.p + ml, 0, sizeof(int), st));
     size_t tmp = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp, ccnt.p, cptr.p, static_cast<int>(m_ + 1), st);
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, ccnt.p, cptr.p, static_cast<int>(ml + 1), st);
     DBuf<char> tbuf(static_cast<i64>(tmp));
-    APC_CUDA(cub::DeviceScan::ExclusiveSum(tbuf.p, tmp, ccnt.p, cptr.p, static_cast<int>(m_ + 1), st));
+    APC_CUDA(cub::DeviceScan::ExclusiveSum(tbuf.p, tmp, ccnt.p, cptr.p, static_cast<int>(ml + 1), st));
     int total = 0;
-    APC_CUDA(cudaMemcpyAsync(&total, cptr.p + m_, sizeof(int), cudaMemcpyDeviceToHost, st));
+    APC_CUDA(cudaMemcpyAsync(&total, cptr.p + ml, sizeof(int), cudaMemcpyDeviceToHost, st));
     APC_CUDA(cudaStreamSynchronize(st));
     DBuf<int> ct(std::max(1, total));
     DBuf<double> cv(std::max(1, total));
-    crow_fill_kernel<<<nb(m_), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p, m_, colpos.p, cptr.p, ct.p, cv.p);
-    ecol_sparse_kernel<<<nb(m_), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p, m_, mt_, cptr.p, ct.p, cv.p, l,
+    crow_fill_kernel<<<nb(ml), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p, ml, colpos.p, cptr.p, ct.p, cv.p);
+    ecol_sparse_kernel<<<nb(ml), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p, ml, eld, cptr.p, ct.p, cv.p, l,
                                               d_jp.p, b, d_urj.p, rowsel_.p, ecol.p);
     ctx_->launches += 4;
     APC_CUDA(cudaStreamSynchronize(st));
   }
   APC_CUDA(cudaGetLastError());
   ps.reset(new ProfScope("aug.row_lupp"));
-  LuppOut row_piv = device_lupp(ctx_, ecol.p, mt_, b, b);
+  LuppOut row_piv = dist_ ? device_lupp_dist(ctx_, ecol.p, ml, row0_, m_, b, b) : device_lupp(ctx_, ecol.p, mt_, b, b);
   ps.reset();
   std::vector<i64> iplus = admissible(row_piv, b, ztol());
   if (iplus.empty()) return {0, true};
@@ -2228,14 +2440,69 @@ AugmentResult DeviceCur::augment() {
   I_.insert(I_.end(), iplus.begin(), iplus.end());
   J_.insert(J_.end(), jplus.begin(), jplus.end());
   last_added_ = static_cast<i64>(iplus.size());
-  DBuf<long long> d_ip;
-  upload(ctx_, d_ip, reinterpret_cast<const long long*>(iplus.data()), last_added_);
   upload(ctx_, d_jp, reinterpret_cast<const long long*>(jplus.data()), last_added_);
-  set_flags_kernel<<<nb(last_added_), kT, 0, st>>>(rowsel_.p, d_ip.p, last_added_, 1);
+  set_row_flags(iplus, 1);
   set_flags_kernel<<<nb(last_added_), kT, 0, st>>>(colsel_.p, d_jp.p, last_added_, 1);
-  ctx_->launches += 2;
+  ctx_->launches++;
   APC_CUDA(cudaStreamSynchronize(st));
   return {last_added_, exhausted};
+}
+
+// rows of the target flagged in rowsel_ (sharded: only this rank's rows, local ids)
+void DeviceCur::set_row_flags(const std::vector<i64>& rows, int value) {
+  std::vector<long long> loc;
+  for (i64 i : rows)
+    if (i >= row0_ && i - row0_ < rowsel_len()) loc.push_back(i - row0_);
+  if (loc.empty()) return;
+  DBuf<long long> d;
+  upload(ctx_, d, loc.data(), static_cast<i64>(loc.size()));
+  set_flags_kernel<<<nb(static_cast<i64>(loc.size())), kT, 0, ctx_->stream>>>(rowsel_.p, d.p,
+                                                                            static_cast<i64>(loc.size()), value);
+  ctx_->launches++;
+  APC_CUDA(cudaStreamSynchronize(ctx_->stream));
+}
+
+// Sharded setup: rows I[first..l) of R = A(I, :) from their owners.  Rank p
+// packs the new rows it owns (row-major) and broadcasts them; every rank
+// places them in Rrm_.  Exact copies, so R is one rank's R bit for bit.
+void DeviceCur::gather_r_rows_dist(i64 first) {
+  cudaStream_t st = ctx_->stream;
+  const i64 l = rank();
+  if (Rrm_.n < l * n_) {  // grow (contents discarded): room for max_rank rows, all rows gathered again
+    const i64 cap = std::max(l, std::min(max_rank_ > 0 ? max_rank_ : l, std::min(m_, n_)));
+    Rrm_.alloc(std::max<i64>(1, cap * n_));
+    first = 0;
+  }
+  for (int p = 0; p < ctx_->nranks; ++p) {
+    std::vector<long long> q, loc;  // slots in R and (on the owner) local rows
+    for (i64 t = first; t < l; ++t)
+      if (I_[t] >= bounds_[p] && I_[t] < bounds_[p + 1]) {
+        q.push_back(t);
+        loc.push_back(I_[t] - bounds_[p]);
+      }
+    const i64 cnt = static_cast<i64>(q.size());
+    if (cnt == 0) continue;
+    DBuf<double> pk(cnt * n_);
+    if (p == ctx_->rank) {
+      DBuf<long long> d_loc;
+      upload(ctx_, d_loc, loc.data(), cnt);
+      if (!a_.sparse) {
+        gather_rows_dense_kernel<<<nb(cnt * n_), kT, 0, st>>>(a_.dense.p, mloc_, n_, d_loc.p, cnt, 0.0, pk.p);
+      } else {
+        APC_CUDA(cudaMemsetAsync(pk.p, 0, pk.bytes(), st));
+        scatter_rows_csr_kernel<<<static_cast<unsigned>(cnt), 128, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p,
+                                                                           mloc_, n_, d_loc.p, cnt, 0.0, pk.p);
+      }
+      ctx_->launches++;
+    }
+    comm_bcast(ctx_, pk.p, cnt * n_, p);
+    DBuf<long long> d_q;
+    upload(ctx_, d_q, q.data(), cnt);
+    place_rows_kernel<<<nb(cnt * n_), kT, 0, st>>>(pk.p, d_q.p, cnt, n_, Rrm_.p);
+    ctx_->launches++;
+    APC_CUDA(cudaStreamSynchronize(st));  // pk and the index buffers go back to the pool
+  }
+  rvalid_ = l;
 }
 
 void DeviceCur::rollback_last_augment() {
@@ -2243,15 +2510,15 @@ void DeviceCur::rollback_last_augment() {
           "CurState::rollback_last_augment: nothing to roll back");
   cudaStream_t st = ctx_->stream;
   std::vector<i64> di(I_.end() - last_added_, I_.end()), dj(J_.end() - last_added_, J_.end());
-  DBuf<long long> d_i, d_j;
-  upload(ctx_, d_i, reinterpret_cast<const long long*>(di.data()), last_added_);
+  DBuf<long long> d_j;
   upload(ctx_, d_j, reinterpret_cast<const long long*>(dj.data()), last_added_);
-  set_flags_kernel<<<nb(last_added_), kT, 0, st>>>(rowsel_.p, d_i.p, last_added_, 0);
+  set_row_flags(di, 0);
   set_flags_kernel<<<nb(last_added_), kT, 0, st>>>(colsel_.p, d_j.p, last_added_, 0);
-  ctx_->launches += 2;
+  ctx_->launches++;
   APC_CUDA(cudaStreamSynchronize(st));
   I_.resize(I_.size() - last_added_);
   J_.resize(J_.size() - last_added_);
+  rvalid_ = std::min(rvalid_, rank());
   last_added_ = 0;
 }
 
@@ -2262,10 +2529,16 @@ void DeviceCur::refresh() {
   DBuf<long long> d_I, d_J;
   upload(ctx_, d_I, reinterpret_cast<const long long*>(I_.data()), l);
   upload(ctx_, d_J, reinterpret_cast<const long long*>(J_.data()), l);
-  // intersection block A(I, J) -> host factor
+  // intersection block A(I, J) -> host factor (sharded: R's columns J, after
+  // the new rows of R arrived from their owners)
   DBuf<double> d_blk(l * l);
-  gather_block_kernel<<<nb(l * l), kT, 0, st>>>(a_.dense.p, m_, a_.a.ptr.p, a_.a.idx.p, a_.a.val.p,
-                                                a_.sparse ? 1 : 0, d_I.p, d_J.p, l, l, amu_, d_blk.p);
+  if (dist_) {
+    gather_r_rows_dist(rvalid_);
+    gather_rcols_kernel<<<nb(l * l), kT, 0, st>>>(Rrm_.p, n_, l, d_J.p, l, d_blk.p);
+  } else {
+    gather_block_kernel<<<nb(l * l), kT, 0, st>>>(a_.dense.p, m_, a_.a.ptr.p, a_.a.idx.p, a_.a.val.p,
+                                                  a_.sparse ? 1 : 0, d_I.p, d_J.p, l, l, amu_, d_blk.p);
+  }
   ctx_->launches++;
   std::unique_ptr<ProfScope> ps(new ProfScope("ref.core_build"));
   static const bool host_core = std::getenv("APC_HOST_CORE") != nullptr;
@@ -2282,7 +2555,9 @@ void DeviceCur::refresh() {
   ps.reset(new ProfScope("ref.rows_H_eres"));
   // R = A(I, :) row-major (all rows re-gathered: I may have changed after a rollback)
   Rrm_.ensure(l * n_);
-  if (!a_.sparse) {
+  if (dist_) {
+    // gathered above
+  } else if (!a_.sparse) {
     gather_rows_dense_kernel<<<nb(l * n_), kT, 0, st>>>(a_.dense.p, m_, n_, d_I.p, l, amu_, Rrm_.p);
   } else {
     APC_CUDA(cudaMemsetAsync(Rrm_.p, 0, sizeof(double) * l * n_, st));
@@ -2422,27 +2697,34 @@ Vec DeviceCur::c_gram() const {
   DBuf<long long> d_J;
   upload(ctx_, d_J, reinterpret_cast<const long long*>(J_.data()), l);
   DBuf<double> G(l * l);
-  if (!a_.sparse) {
-    DBuf<double> C(m_ * l);
-    gather_cols_kernel<<<nb(m_ * l), kT, 0, st>>>(a_.dense.p, m_, d_J.p, l, C.p);
+  const i64 ml = mloc_;  // sharded: this rank's rows, then a sum over the ranks
+  APC_CUDA(cudaMemsetAsync(G.p, 0, G.bytes(), st));
+  if (ml == 0) {
+    // no local rows: a zero partial
+  } else if (!a_.sparse) {
+    DBuf<double> C(ml * l);
+    gather_cols_kernel<<<nb(ml * l), kT, 0, st>>>(a_.dense.p, ml, d_J.p, l, C.p);
     // exact chol_gram order: T_C then equals the reference's factor bit for bit
     dim3 grid(static_cast<unsigned>((l + 63) / 64), static_cast<unsigned>((l + 63) / 64));
-    gram_exact_kernel<<<grid, 256, 0, st>>>(C.p, m_, l, G.p);
+    gram_exact_kernel<<<grid, 256, 0, st>>>(C.p, ml, l, G.p);
     ctx_->launches += 2;
   } else {
     DBuf<int> colpos(n_);
     APC_CUDA(cudaMemsetAsync(colpos.p, 0xff, colpos.bytes(), st));
     set_colpos_kernel<<<nb(l), kT, 0, st>>>(colpos.p, d_J.p, l);
-    const i64 rb = std::min<i64>(m_, std::max<i64>(1, (1LL << 28) / std::max<i64>(1, l)));  // <= 2 GB blocks
+    const i64 rb = std::min<i64>(ml, std::max<i64>(1, (1LL << 28) / std::max<i64>(1, l)));  // <= 2 GB blocks
     DBuf<double> D(rb * l);
-    for (i64 r0 = 0; r0 < m_; r0 += rb) {
-      const i64 cnt = std::min(rb, m_ - r0);
+    for (i64 r0 = 0; r0 < ml; r0 += rb) {
+      const i64 cnt = std::min(rb, ml - r0);
       APC_CUDA(cudaMemsetAsync(D.p, 0, sizeof(double) * cnt * l, st));
       densify_rows_kernel<<<nb(cnt), kT, 0, st>>>(a_.a.ptr.p, a_.a.idx.p, a_.a.val.p, r0, cnt, colpos.p, D.p);
       dsyrk_t(ctx_, l, cnt, 1.0, D.p, cnt, r0 == 0 ? 0.0 : 1.0, G.p, l);
       ctx_->launches++;
     }
   }
+  // sharded: the ranks' partial Grams summed (identical on every rank; the
+  // single-rank chol_gram sum order is not kept across the row blocks)
+  if (dist_) comm_allreduce(ctx_, G.p, l * l);
   Vec g = download(ctx_, G.p, l * l);
   for (i64 j = 0; j < l; ++j)
     for (i64 i = j + 1; i < l; ++i) g[j * l + i] = g[i * l + j];  // mirror the upper triangle
@@ -2457,6 +2739,7 @@ Vec DeviceCur::r_dense_rows(i64 first, i64 count) const {
 
 Vec DeviceCur::c_dense() const {
   require(!a_.sparse, APC_INVALID_ARGUMENT, "c_dense: dense A only");
+  require(!dist_, APC_NOT_APPLICABLE, "c_dense: the sharded setup holds no whole column of A");
   const i64 l = rank();
   Vec out(static_cast<size_t>(mt_ * l), 0.0);
   for (i64 t = 0; t < l; ++t)
@@ -2468,7 +2751,61 @@ Vec DeviceCur::c_dense() const {
   return out;
 }
 
+// warp per row: nonzeros of each row of a row-major l x n matrix
+__global__ void row_nnz_kernel(const double* __restrict__ R, long long l, long long n, int* __restrict__ cnt) {
+  const long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= l) return;
+  int c = 0;
+  for (long long j = lane; j < n; j += 32) c += R[i * n + j] != 0.0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) cnt[i] = c;
+}
+// warp per row: (column, value) of the nonzeros in column order from ptr[i]
+__global__ void row_compact_kernel(const double* __restrict__ R, long long l, long long n,
+                                   const long long* __restrict__ ptr, int* __restrict__ idx,
+                                   double* __restrict__ val) {
+  const long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= l) return;
+  long long q = ptr[i];
+  for (long long j0 = 0; j0 < n; j0 += 32) {
+    const long long j = j0 + lane;
+    const double v = j < n ? R[i * n + j] : 0.0;
+    const unsigned mask = __ballot_sync(0xffffffffu, v != 0.0);
+    if (v != 0.0) {
+      const long long at = q + __popc(mask & ((1u << lane) - 1u));
+      idx[at] = static_cast<int>(j);
+      val[at] = v;
+    }
+    q += __popc(mask);
+  }
+}
+
 namespace {
+// nonzeros of the rows of a device row-major l x n matrix as a host CSC-like
+// triple (column t = row t)
+void dense_rows_to_host_csr(apc_ctx* ctx, const double* R, i64 l, i64 n, std::vector<i64>& ptr,
+                            std::vector<i64>& idx, Vec& val) {
+  cudaStream_t st = ctx->stream;
+  DBuf<int> cnt(std::max<i64>(1, l));
+  row_nnz_kernel<<<nb(l * 32), kT, 0, st>>>(R, l, n, cnt.p);
+  std::vector<int> hc = download(ctx, cnt.p, l);
+  std::vector<long long> hp(static_cast<size_t>(l + 1), 0);
+  for (i64 i = 0; i < l; ++i) hp[i + 1] = hp[i] + hc[i];
+  const i64 nnz = hp[l];
+  DBuf<long long> d_ptr;
+  upload(ctx, d_ptr, hp.data(), l + 1);
+  DBuf<int> d_idx(std::max<i64>(1, nnz));
+  DBuf<double> d_val(std::max<i64>(1, nnz));
+  row_compact_kernel<<<nb(l * 32), kT, 0, st>>>(R, l, n, d_ptr.p, d_idx.p, d_val.p);
+  ctx->launches += 2;
+  std::vector<int> hi = download(ctx, d_idx.p, nnz);
+  val = download(ctx, d_val.p, nnz);
+  ptr.assign(hp.begin(), hp.end());
+  idx.assign(hi.begin(), hi.end());
+}
+
 // rows `which` of a device CSR as a host CSC-like triple (columns = which order)
 void csr_rows_to_host(apc_ctx* ctx, const Csr& c, const std::vector<i64>& which, std::vector<i64>& ptr,
                       std::vector<i64>& idx, Vec& val) {
@@ -2496,6 +2833,7 @@ void csr_rows_to_host(apc_ctx* ctx, const Csr& c, const std::vector<i64>& which,
 }  // namespace
 
 void DeviceCur::c_csc(std::vector<i64>& ptr, std::vector<i64>& idx, Vec& val) const {
+  require(!dist_, APC_NOT_APPLICABLE, "c_csc: the sharded setup holds no whole column of A");
   csr_rows_to_host(ctx_, a_.at, J_, ptr, idx, val);  // CSR(A^T) row j == column j of A
   if (amu_ > 0.0) {  // + amu at row m + J[t] of column t (matrix.hpp:439-446)
     std::vector<i64> p2(1, 0), i2;
@@ -2516,6 +2854,10 @@ void DeviceCur::c_csc(std::vector<i64>& ptr, std::vector<i64>& idx, Vec& val) co
 }
 
 void DeviceCur::rt_csc(std::vector<i64>& ptr, std::vector<i64>& idx, Vec& val) const {
+  if (dist_) {  // from the replicated dense rows of R: their nonzeros, compacted on the device
+    dense_rows_to_host_csr(ctx_, Rrm_.p, rank(), n_, ptr, idx, val);
+    return;
+  }
   // row i of the target == column of R^T; augmented rows are amu e_{i-m}
   std::vector<i64> base;
   for (i64 i : I_)

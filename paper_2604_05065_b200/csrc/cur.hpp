@@ -26,6 +26,9 @@ struct LuppOut {
 // Pivot order of partial-pivoting elimination on a column-major rows x cols
 // device matrix (destroyed), lu_partial_pivot semantics (dense_factor.hpp:119-157).
 LuppOut device_lupp(apc_ctx* ctx, double* w, i64 rows, i64 cols, i64 max_pivots);
+// The same order over a row-sharded matrix: this rank holds rows
+// [row0, row0 + rows) of rows_global; collective over the ctx ranks.
+LuppOut device_lupp_dist(apc_ctx* ctx, double* w, i64 rows, i64 row0, i64 rows_global, i64 cols, i64 max_pivots);
 
 struct AugmentResult {
   i64 added = 0;
@@ -36,8 +39,17 @@ class DeviceCur {
  public:
   // target = A (aug_mu == 0: the svd variant, or svd-free with mu == 0), or the
   // stacked [A; aug_mu I] (svd-free with mu > 0, CurTarget(aug), cur.hpp:21-47)
+  //
+  // distributed: the sharded setup.  `a` is this rank's row
+  // block and every rank of the ctx constructs the state (collective calls):
+  // Y = sum_p S_p A_p as one running sum carried from rank to rank in row
+  // order, E^col on the local rows, the row LUPP over the shards with one
+  // candidate allgather per pivot, R = A(I, :) broadcast by the owners of the
+  // new rows.  Every rank then holds the same Y, E^row, R, factor, I, J and rho
+  // (bit-identical to one rank's); no rank needs the whole matrix.
   DeviceCur(apc_mat& a, i64 block, std::uint64_t seed, i64 xi, i64 probes, int core_kind,
-            int sketch_kind, i64 max_rank, double aug_mu = 0.0);
+            int sketch_kind, i64 max_rank, double aug_mu = 0.0, bool distributed = false);
+  bool distributed() const { return dist_; }
   i64 target_rows() const { return mt_; }
   double embedding_ms() const { return embed_ms_; }
   double sketch_ms() const { return sketch_ms_; }
@@ -121,7 +133,15 @@ class DeviceCur {
   Vec core_at_host_;              // its host staging copy (alive until the async upload completes)
   DBuf<long long> core_perm_;
   DBuf<double> work_;         // generic scratch
-  DBuf<int> rowsel_, colsel_;  // flags (rows in I, cols in J)
+  DBuf<int> rowsel_, colsel_;  // flags (rows in I, cols in J); rows: local rows when distributed
+  // sharded setup
+  bool dist_ = false;
+  i64 row0_ = 0, mloc_ = 0;     // this rank's rows [row0_, row0_ + mloc_)
+  std::vector<i64> bounds_;     // every rank's first row, then m
+  i64 rvalid_ = 0;              // rows of Rrm_ already gathered (I[0..rvalid_))
+  i64 rowsel_len() const { return dist_ ? mloc_ : mt_; }
+  void set_row_flags(const std::vector<i64>& rows, int value);
+  void gather_r_rows_dist(i64 first);
 };
 
 }  // namespace apc

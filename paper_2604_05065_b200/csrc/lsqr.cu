@@ -424,6 +424,68 @@ __global__ void samp_final_kernel(const LsqrState* st, const double* sc, double 
 // ---------------------------------------------------------------------------
 // preconditioner kernels:  out = x + B (K (B^T x))  or  x + R^T (G (R x))
 // ---------------------------------------------------------------------------
+// Sparse and dense dot products of the preconditioner applies.  Each running
+// sum adds its terms in index order (one chain per lane or thread); the loops
+// are unrolled by hand so the loads of four terms are issued before the first
+// add waits on them (the chains were latency bound: one index load and one
+// dependent gather per term).  The add order, hence every bit, is the plain
+// loops' own (APC_NO_GATHER_UNROLL builds the plain loops for A/B runs).
+// lane-strided: sum over q = b0 + lane, b0 + lane + 32, ... < b1
+__device__ __forceinline__ double gather_dot_lanes(const int* __restrict__ idx, const double* __restrict__ val,
+                                                   const double* __restrict__ s, int b0, int b1, int lane) {
+  double x = 0.0;
+  int q = b0 + lane;
+#ifndef APC_NO_GATHER_UNROLL
+  for (; q + 96 < b1; q += 128) {
+    const int i0 = idx[q], i1 = idx[q + 32], i2 = idx[q + 64], i3 = idx[q + 96];
+    const double v0 = val[q], v1 = val[q + 32], v2 = val[q + 64], v3 = val[q + 96];
+    const double s0 = s[i0], s1 = s[i1], s2 = s[i2], s3 = s[i3];
+    x += v0 * s0;
+    x += v1 * s1;
+    x += v2 * s2;
+    x += v3 * s3;
+  }
+#endif
+  for (; q < b1; q += 32) x += val[q] * s[idx[q]];
+  return x;
+}
+// one thread: sum over q = q0 .. q1-1 (acc carried in)
+__device__ __forceinline__ double gather_dot_seq(const int* __restrict__ idx, const double* __restrict__ val,
+                                                 const double* __restrict__ s, int q0, int q1, double acc) {
+  int q = q0;
+#ifndef APC_NO_GATHER_UNROLL
+  for (; q + 3 < q1; q += 4) {
+    const int i0 = idx[q], i1 = idx[q + 1], i2 = idx[q + 2], i3 = idx[q + 3];
+    const double v0 = val[q], v1 = val[q + 1], v2 = val[q + 2], v3 = val[q + 3];
+    const double s0 = s[i0], s1 = s[i1], s2 = s[i2], s3 = s[i3];
+    acc += v0 * s0;
+    acc += v1 * s1;
+    acc += v2 * s2;
+    acc += v3 * s3;
+  }
+#endif
+  for (; q < q1; ++q) acc += val[q] * s[idx[q]];
+  return acc;
+}
+// lane-strided dense row: sum over k = lane, lane + 32, ... < l of row[k] t[k]
+__device__ __forceinline__ double row_dot_lanes(const double* __restrict__ row, const double* __restrict__ t,
+                                                long long l, int lane) {
+  double acc = 0.0;
+  long long k = lane;
+#ifndef APC_NO_GATHER_UNROLL
+  for (; k + 96 < l; k += 128) {
+    const double r0 = row[k], r1 = row[k + 32], r2 = row[k + 64], r3 = row[k + 96];
+    const double t0 = t[k], t1 = t[k + 32], t2 = t[k + 64], t3 = t[k + 96];
+    acc += r0 * t0;
+    acc += r1 * t1;
+    acc += r2 * t2;
+    acc += r3 * t3;
+  }
+#endif
+  for (; k < l; k += 32) acc += row[k] * t[k];
+  return acc;
+}
+
 // s = K t with K stored row-major (KT[i * l + k] = K(i, k)): one warp per row,
 // lanes stride k (coalesced), fixed shuffle tree
 __global__ void pc_core_kernel(const double* __restrict__ KT, long long l,
@@ -433,9 +495,7 @@ __global__ void pc_core_kernel(const double* __restrict__ KT, long long l,
   const long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= l) return;
-  const double* row = KT + i * l;
-  double acc = 0.0;
-  for (long long k = lane; k < l; k += 32) acc += row[k] * t[k];
+  double acc = row_dot_lanes(KT + i * l, t, l, lane);
   acc = warp_sum(acc);
   if (lane == 0) s[i] = acc;
 }
@@ -448,8 +508,7 @@ __global__ void pc_rproj_kernel(const int* __restrict__ rptr, const int* __restr
   const long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= l) return;
-  double acc = 0.0;
-  for (int q = rptr[i] + lane; q < rptr[i + 1]; q += 32) acc += rval[q] * x[ridx[q]];
+  double acc = gather_dot_lanes(ridx, rval, x, rptr[i], rptr[i + 1], lane);
   acc = warp_sum(acc);
   if (lane == 0) t[i] = acc;
 }
@@ -523,15 +582,14 @@ pc_expand_kernel(LsqrPtrs P, int kind, const double* __restrict__ B, long long l
         defer[atomicAdd(&ndefer, 1)] = threadIdx.x;
         deferred = true;
       } else {
-        for (int q = q0; q < q1; ++q) acc += tval[q] * s[tidx[q]];
+        acc = gather_dot_seq(tidx, tval, s, q0, q1, acc);
       }
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
     for (int d = threadIdx.x >> 5; d < ndefer; d += kVecThreads / 32) {
       const long long jj = static_cast<long long>(blockIdx.x) * kVecThreads + defer[d];
-      double a = 0.0;
-      for (int q = tptr[jj] + lane; q < tptr[jj + 1]; q += 32) a += tval[q] * s[tidx[q]];
+      double a = gather_dot_lanes(tidx, tval, s, tptr[jj], tptr[jj + 1], lane);
       a = warp_sum(a);
       if (lane == 0) dacc[defer[d]] = a;
     }
@@ -637,15 +695,13 @@ __device__ __forceinline__ double ns_rts(const NspaceArgs& a, long long j0, long
   }
   const bool lng = q1 - q0 > kExpandLong;
   double acc = 0.0;
-  if (!lng)
-    for (int q = q0; q < q1; ++q) acc += a.tval[q] * s[a.tidx[q]];
+  if (!lng) acc = gather_dot_seq(a.tidx, a.tval, s, q0, q1, acc);
   unsigned m = __ballot_sync(0xffffffffu, lng);
   while (m) {
     const int L = __ffs(m) - 1;
     m &= m - 1;
     const int b0 = __shfl_sync(0xffffffffu, q0, L), b1 = __shfl_sync(0xffffffffu, q1, L);
-    double x = 0.0;
-    for (int q = b0 + lane; q < b1; q += 32) x += a.tval[q] * s[a.tidx[q]];
+    double x = gather_dot_lanes(a.tidx, a.tval, s, b0, b1, lane);
     x = warp_sum(x);
     if (lane == L) acc = x;
   }
@@ -657,9 +713,7 @@ __device__ __forceinline__ void ns_core(const double* __restrict__ M, long long 
                                         long long gw, long long nw) {
   const int lane = threadIdx.x & 31;
   for (long long i = gw; i < l; i += nw) {
-    const double* row = M + i * l;
-    double acc = 0.0;
-    for (long long k = lane; k < l; k += 32) acc += row[k] * t[k];
+    double acc = row_dot_lanes(M + i * l, t, l, lane);
     acc = warp_sum(acc);
     if (lane == 0) out[i] = acc;
   }

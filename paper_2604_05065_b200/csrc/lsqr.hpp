@@ -80,6 +80,9 @@ void comm_allreduce(apc_ctx* ctx, double* buf, i64 count);
 // broadcast(fp64) of a device buffer from `root` (the root-only setup of the
 // row-sharded solve); no-op at 1 rank
 void comm_bcast(apc_ctx* ctx, double* buf, i64 count, int root);
+// allgather(fp64): recv (nranks x count, rank-major) = every rank's send;
+// bit-exact on both backends (the sharded CUR's pivot candidates)
+void comm_allgather(apc_ctx* ctx, const double* send, i64 count, double* recv);
 // false when the collective cannot be captured in a CUDA graph (host-staged)
 bool comm_graph_safe(const apc_ctx* ctx);
 void comm_init(apc_ctx* ctx, const void* uid);

@@ -156,8 +156,8 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
                                   const apc_hooks* hooks) {
   require(full.ctx == a.ctx && full.m == a.m && full.n == a.n, APC_INVALID_ARGUMENT,
           "aplicur_solve: full matrix and shard must describe the same A on the same context");
-  require(a.ctx->nranks <= 1 || a.ctx->rank != 0 || (full.r0 == 0 && full.mloc() == full.m), APC_INVALID_ARGUMENT,
-          "aplicur_solve: rank 0 of a row-sharded solve needs the whole matrix");
+  require(&full == &a || (full.r0 == 0 && full.mloc() == full.m), APC_INVALID_ARGUMENT,
+          "aplicur_solve: `full` must hold the whole matrix");
   auto t_start = clock_t_::now();
   const i64 n = a.n, m = a.m;
   apc_solver_config cfg = resolve_config(cfg_in, n);
@@ -170,20 +170,33 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
   // CUR target: A for the svd variant; the regularised stack [A; mu I] for the
   // svd-free variant whenever mu > 0 (solver.hpp:183-186)
   const bool target_augmented = cfg.variant == 1 && mu > 0.0;
-  // Row-sharded solves (ctx->nranks > 1) run the sketch, the CUR selection and
-  // every preconditioner build on rank 0 only (it alone needs `full`); the
-  // other ranks hold just their row block and receive each phase's decision
-  // and preconditioner by broadcast.  The LSQR phases run on
-  // every rank over the row partition.
+  // Row-sharded solves (ctx->nranks > 1), two setups:
+  //  * root-only (rank 0 passed the whole matrix as `full`): rank 0 runs the
+  //    sketch, the CUR selection and every preconditioner build;
+  //  * sharded (no rank holds the whole matrix): every rank runs the CUR state
+  //    over its row block (DeviceCur distributed: carried sketch, local E^col,
+  //    row LUPP over the shards, R rows from their owners), identical on all
+  //    ranks; rank 0 builds the preconditioner (the Gram C^T C summed over the
+  //    ranks).
+  // Either way the other ranks receive each phase's decision and
+  // preconditioner by broadcast, and the LSQR phases run on every rank over
+  // the row partition.
   const bool multi = ctx->nranks > 1;
   const bool root = !multi || ctx->rank == 0;
+  bool dist = false;
+  if (multi) {
+    double rootfull = (ctx->rank == 0 && &full != &a) ? 1.0 : 0.0;
+    bcast_scalar(ctx, rootfull);
+    dist = rootfull == 0.0;
+  }
+  const bool has_cur = root || dist;  // this rank holds a CUR state
   std::unique_ptr<ProfScope> ps_init(new ProfScope("cur_init"));
   std::unique_ptr<DeviceCur> curp;
-  if (root)
-    curp.reset(new DeviceCur(full, cfg.block, cfg.seed, cfg.sketch_xi, cfg.probe_count, cfg.core, cfg.sketch_kind,
-                             cfg.max_rank, target_augmented ? mu : 0.0));
+  if (has_cur)
+    curp.reset(new DeviceCur(dist ? a : full, cfg.block, cfg.seed, cfg.sketch_xi, cfg.probe_count, cfg.core,
+                             cfg.sketch_kind, cfg.max_rank, target_augmented ? mu : 0.0, dist));
   ps_init.reset();
-  i64 max_rank = root ? std::min(curp->target_rows(), n) : n;
+  i64 max_rank = has_cur ? std::min(curp->target_rows(), n) : n;
   if (cfg.max_rank > 0) max_rank = std::min(max_rank, cfg.max_rank);
   const double density = (m * n == 0) ? 0.0 : static_cast<double>(a.nnz_global) / static_cast<double>(m * n);
   const bool implicit_mode = a.sparse && density < 0.10;
@@ -266,7 +279,7 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
     double rho = 0.0;
     PrecondDev P;
     PrecondInfo info;
-    if (root) {
+    if (has_cur) {
       DeviceCur& cur = *curp;
       auto t_aug0 = clock_t_::now();
       bool grew = false;
@@ -304,7 +317,9 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
       std::unique_ptr<ProfScope> ps_fac(new ProfScope("factor"));
       if (grew) {
         const i64 l = cur.rank();
-        if (implicit_mode) {
+        if (!root) {
+          // sharded setup, rank > 0: rank 0 alone builds the preconditioner
+        } else if (implicit_mode) {
           // T_R with T_R^T T_R = R R^T (the reference maintains it with
           // CholGramAccumulator; the from-scratch gram_factor is the same
           // factor), computed when a preconditioner is next built
@@ -339,6 +354,9 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
       if (trigger && cur.rank() > 0) {
         if (!res->phases.empty() && res->phases.back().rank == cur.rank()) {
           action = kStop;  // duplicate rank
+        } else if (!root) {
+          (void)cur.c_gram();  // rank 0's Gram is a sum over every rank's rows (collective)
+          action = kRun;
         } else {
           if (implicit_mode && t_r_stale) {
             ProfScope ps("factor");
@@ -365,7 +383,7 @@ apc_result* aplicur_solve_sharded(apc_mat& full, apc_mat& a, const double* b, co
             if (cfg.variant == 1) in.block = &cur.intersection();  // svd-free: A(I, J)
             in.t_r = implicit_mode ? &t_r_implicit : &qr_acc.t;
             in.q_dev = qr_acc.q.p;
-            in.gram = cur.c_gram();
+            in.gram = cur.c_gram();  // collective in the sharded setup
             in.c_dense = [&cur, &full]() -> Vec {  // only for the QR fallback of gram_factor
               if (!full.sparse) return cur.c_dense();
               std::vector<i64> cp, ci;
