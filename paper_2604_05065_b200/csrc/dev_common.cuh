@@ -65,8 +65,20 @@ __device__ __forceinline__ double ordered_sum(const volatile double* partials, l
   // thread order: fixed association for fixed (n, NT)
   long long per = (n + NT - 1) / NT;
   long long b = per * threadIdx.x, e = b + per < n ? b + per : n;
+  // the stripe's loads are issued 8 at a time before the (in-order) adds: a
+  // volatile load per add made the last block's sum a chain of L2 round trips
+  // (~5 us at the LSQR kernels' 1563 tiles).  L2 loads (__ldcg): the partials
+  // come from other SMs, ordered by elect_last_block's fences.
+  const double* p = const_cast<const double*>(partials);
   double s = 0.0;
-  for (long long i = b; i < e; ++i) s += partials[i];
+  for (long long i = b; i < e; i += 8) {
+    double t[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t[k] = i + k < e ? __ldcg(p + i + k) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (i + k < e) s += t[k];
+  }
   return block_sum<NT>(s, sh);
 }
 

@@ -1387,9 +1387,14 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     APC_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeThreadLocal));
-    enqueue_iteration(w, a, p, P, cond, 1);
-    if (sampling) enqueue_sample(w, a, p, P, *samp, cap + 1);
-    per_iter = ctx->launches - launches_before_capture;
+    // APC_WHILE_UNROLL iterations per pass of the body (kernels after the stop
+    // exit on `done`): fewer body relaunches per iteration
+    static const int unroll = std::max(1, std::getenv("APC_WHILE_UNROLL") ? std::atoi(std::getenv("APC_WHILE_UNROLL")) : 1);
+    for (int k = 0; k < unroll; ++k) {
+      enqueue_iteration(w, a, p, P, cond, 1);
+      if (sampling) enqueue_sample(w, a, p, P, *samp, cap + 1);
+    }
+    per_iter = (ctx->launches - launches_before_capture) / unroll;
     APC_CUDA(cudaStreamEndCapture(st, &body));
     APC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     // skip the loop entirely if initialisation already stopped
