@@ -177,6 +177,7 @@ def load_library(path: Optional[os.PathLike] = None) -> C.CDLL:
         "apc_mat_free": (C.c_int, [vp]),
         "apc_mat_info": (C.c_int, [vp, _i64p, _i64p, _i64p, C.POINTER(C.c_int), _i64p, _i64p]),
         "apc_op_apply_dev": (C.c_int, [vp, C.c_double, C.c_int, C.c_int, vp, vp]),
+        "apc_op_pair_dev": (C.c_int, [vp, vp, vp, vp, C.POINTER(C.c_int)]),
         "apc_dgemm": (C.c_int, [vp, C.c_int, C.c_int, _i64, _i64, _i64, C.c_double, vp, _i64, vp, _i64, C.c_double,
                                 vp, _i64]),
         "apc_dtrsm_right_upper": (C.c_int, [vp, _i64, _i64, vp, _i64, vp, _i64]),
@@ -375,6 +376,14 @@ class DeviceMatrix:
                   transpose: bool = False) -> None:
         _check(load_library().apc_op_apply_dev(self.h, mu, int(augmented), int(transpose),
                                                C.c_void_p(x_ptr), C.c_void_p(y_ptr)))
+
+    def pair_dev(self, x_ptr: int, y_ptr: int, g_ptr: int) -> bool:
+        """y = A x, g[0:n] = A^T y, g[n] = ||y||^2 on device pointers (the LSQR
+        operator pair); True when the fused read-A-once kernel ran."""
+        fused = C.c_int(0)
+        _check(load_library().apc_op_pair_dev(self.h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), C.c_void_p(g_ptr),
+                                              C.byref(fused)))
+        return bool(fused.value)
 
     def free(self) -> None:
         if getattr(self, "h", None):

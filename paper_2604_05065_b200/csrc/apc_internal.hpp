@@ -187,6 +187,25 @@ struct HotSell {
   bool built() const { return s.chunks > 0; }
 };
 
+// Panel copy of a dense A for the fused operator pair (dense_pair.cu): rows
+// cut into panels of rb rows, panel p stored column-major on its own
+// (ap[(p * n + c) * rb + r] = A(p * rb + r, c), rows past mloc zero), so the
+// rb x W slice of one CTA (W consecutive columns) is ONE contiguous run: a
+// single bulk (TMA) copy per tile whatever rb is.  The CTAs form ng groups of
+// g; a group shares its panels (every CTA a column slice) and exchanges the
+// rb partial row sums of each panel through `part` / `cnt`.
+struct DensePanels {
+  i64 mloc = 0, n = 0, npanels = 0;
+  int rb = 0, W = 0, g = 0, ng = 0, stages = 0, nslot = 0;
+  size_t smem = 0;
+  int state = 0;        // 0: not tried, 1: built, -1: unsupported / disabled
+  DBuf<double> ap;      // npanels * n * rb
+  DBuf<double> part;    // ng * nslot * g * rb partial row sums (ring)
+  DBuf<double> gpart;   // ng * n column sums of the groups
+  DBuf<double> nrmp;    // ng * g norm partials
+  DBuf<unsigned> cnt;   // npanels arrival counters + 2 finish counters (zero between launches)
+};
+
 }  // namespace apc
 
 // ---------------------------------------------------------------------------
@@ -246,6 +265,7 @@ struct apc_mat {
   apc::Sell sell;           // SELL-32 copy of `a` (persistent LSQR, built lazily)
   apc::HotSell hot;         // hot-relabelled SELL-32 of `a` (large CSR forward, built at upload)
   apc::HeadAdj head;        // row-blocked A^T u of the long rows of `at` (built with `hot`)
+  apc::DensePanels panels;  // panel copy of `dense` for the fused pair (built lazily by the LSQR phase)
   apc::i64 nnz_global = 0;
   apc::i64 mloc() const { return r1 - r0; }
 };

@@ -12,6 +12,7 @@
 
 #include "apc_internal.hpp"
 #include "blas.hpp"
+#include "dense_pair.hpp"
 #include "dense_small.hpp"
 #include "host_rng.hpp"
 #include "rng_dev.hpp"
@@ -347,6 +348,20 @@ int apc_op_apply_dev(apc_mat* a, double mu, int augmented, int transpose, const 
     require(!augmented || mu >= 0.0, APC_INVALID_ARGUMENT, "AugmentedOperator: mu < 0");
     if (!transpose) op_fwd(*a, mu, augmented != 0, x, y);
     else op_adj(*a, mu, augmented != 0, x, y);
+  });
+}
+
+int apc_op_pair_dev(apc_mat* a, const double* x, double* y, double* g, int* fused) {
+  return guard(a->ctx, [&] {
+    const bool f = dense_pair_ready(*a);
+    if (fused) *fused = f ? 1 : 0;
+    if (f) {
+      launch_dense_pair(*a, x, y, nullptr, g, nullptr);
+    } else {
+      op_fwd(*a, 0.0, false, x, y);
+      op_adj(*a, 0.0, false, y, g);
+      pair_norm2(a->ctx, y, a->mloc(), g + a->n);
+    }
   });
 }
 

@@ -32,6 +32,7 @@
 
 #include "dev_common.cuh"
 #include "lsqr.hpp"
+#include "dense_pair.hpp"
 #include "lsqr_persistent.hpp"
 #include "ops.cuh"
 
@@ -1124,7 +1125,11 @@ void enqueue_iteration(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P
     z = P.z;
   }
   LsqrFwdEpi epi{P.u, P.st, P.fwd_part, P.ctr + 0, P.g + P.n, 0.0, 0.0};
-  if (w->mloc > 0) {
+  // dense A beyond L2: u, ||u||^2 and A^T u in one kernel that reads A once
+  const bool pair_fused = w->mloc > 0 && !a.sparse && dense_pair_ready(a);
+  if (pair_fused) {
+    launch_dense_pair(a, z, P.u, P.st, P.g, done);
+  } else if (w->mloc > 0) {
     launch_fwd(a, z, done, epi, st, x_permuted);
   } else {
     // empty shard: publish ||u_top||^2 = 0 through the init-copy path
@@ -1147,7 +1152,7 @@ void enqueue_iteration(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P
       op_adj_epi(a, P.u, P.h, done,
                  AdjEpi{P.has_tail ? P.u + P.mloc : nullptr, P.mu, P.g + P.n, P.has_tail ? &P.st->tail_norm2 : nullptr});
   if (!epi_fused) {
-    op_adj_raw(a, P.u, P.g, done);
+    if (!pair_fused) op_adj_raw(a, P.u, P.g, done);
     comm_allreduce(ctx, P.g, w->n + 1);
     lsqr_epi_kernel<<<nb(w->n), kVecThreads, 0, st>>>(P, pre ? 1 : 0);
     ctx->launches++;
@@ -1225,6 +1230,8 @@ void lsqr_phase(LsqrWork* w, apc_mat& a, double mu, const PrecondDev* pc, const 
   const long long n = w->n;
   require(mu == w->mu, APC_INVALID_ARGUMENT, "lsqr_phase: workspace built for another mu");
   if (p && p->kind != 0) ensure_pc_buffers(w, *p);
+  // the panel copy of a large dense A is built here, outside any graph capture
+  if (!a.sparse && w->mloc > 0) dense_pair_ready(a);
   const long long cap = stop.max_iters > 0 ? stop.max_iters : 4 * n;
   w->trace.ensure(cap + 1);
   const bool sampling = samp && samp->stride > 0;
