@@ -226,6 +226,31 @@ def operator_pair(apc, ctx, A, n, mloc, reps=20):
     return ev[0].elapsed_time(ev[1]) / reps * 1e-3, ev[1].elapsed_time(ev[2]) / reps * 1e-3
 
 
+def operator_pair_fused(apc, ctx, A, n, mloc, reps=20):
+    """Live fused pair (dense_pair_kernel: y = A x, ||y||^2, g = A^T y, A read once);
+    None when the matrix takes the two-pass kernels."""
+    import torch
+
+    dev = torch.device("cuda", ctx.device)
+    x = torch.randn(n, dtype=torch.float64, device=dev)
+    y = torch.empty(mloc, dtype=torch.float64, device=dev)
+    g = torch.empty(n + 1, dtype=torch.float64, device=dev)
+    s = torch.cuda.ExternalStream(ctx.stream)
+    torch.cuda.synchronize()
+    if not A.pair_dev(x.data_ptr(), y.data_ptr(), g.data_ptr()):
+        return None
+    for _ in range(2):
+        A.pair_dev(x.data_ptr(), y.data_ptr(), g.data_ptr())
+    ctx.sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(reps):
+        A.pair_dev(x.data_ptr(), y.data_ptr(), g.data_ptr())
+    e1.record(s)
+    ctx.sync()
+    return e0.elapsed_time(e1) / reps * 1e-3
+
+
 def ncu_traffic(path: Path):
     """DRAM bytes per launch of the operator-pair kernels from the committed
     `ncu --set full` capture of scripts/opbench.py c5 (same kernels, same input)."""
@@ -243,6 +268,14 @@ def hbm_pair_extra(apc, ctx, cfg_id, block=100, fp64_peak_tflops=37.0):
     A = apc.DeviceMatrix.from_problem(ctx, p)
     tf, ta = operator_pair(apc, ctx, A, p.n, p.m)
     byts = 16 * p.m * p.n + 16 * (p.m + p.n)
+    tp = operator_pair_fused(apc, ctx, A, p.n, p.m)
+    hbm = float(_peaks()[0].get("hbm_gbs", 7672.0))
+    fused = None if tp is None else {
+        "pair_us": tp * 1e6, "GBps_algorithmic": byts / tp / 1e9, "frac_algorithmic": byts / tp / 1e9 / hbm,
+        "read_once_bytes": 8 * p.m * p.n + 16 * (p.m + p.n),
+        "GBps_read_once": (8 * p.m * p.n + 16 * (p.m + p.n)) / tp / 1e9,
+        "frac_read_once": (8 * p.m * p.n + 16 * (p.m + p.n)) / tp / 1e9 / hbm,
+        "kernel": "dense_pair_kernel (A read from HBM once; the LSQR loop's pair on dense A beyond L2)"}
     s = int(np.ceil(1.1 * block))
     flops = 2.0 * s * p.m * p.n
     sk = {}
@@ -252,7 +285,7 @@ def hbm_pair_extra(apc, ctx, cfg_id, block=100, fp64_peak_tflops=37.0):
                          "frac_fp64_peak": flops / (ms * 1e-3) / 1e12 / fp64_peak_tflops}
     A.free()
     return {"fwd_us": tf * 1e6, "adj_us": ta * 1e6, "bytes": byts, "GBps": byts / (tf + ta) / 1e9,
-            "kernels": "dense_fwd_kernel | dense_adj_kernel",
+            "kernels": "dense_fwd_kernel | dense_adj_kernel", "fused_pair": fused,
             "gaussian_sketch_s111": dict(sk, flops=flops, fp64_peak_tflops=fp64_peak_tflops,
                                          peak_source="B200 FP64 (DMMA = FMA) nominal, B200_PROFILING.md")}
 

@@ -196,14 +196,14 @@ struct HotSell {
 // rb partial row sums of each panel through `part` / `cnt`.
 struct DensePanels {
   i64 mloc = 0, n = 0, npanels = 0;
-  int rb = 0, W = 0, g = 0, ng = 0, stages = 0, nslot = 0;
+  int rb = 0, W = 0, g = 0, gact = 0, ng = 0, stages = 0, nslot = 0;
   size_t smem = 0;
   int state = 0;        // 0: not tried, 1: built, -1: unsupported / disabled
   DBuf<double> ap;      // npanels * n * rb
-  DBuf<double> part;    // ng * nslot * g * rb partial row sums (ring)
+  DBuf<double> part;    // ng * nslot * g * rb partial row sums (ring), two flagged 8-byte words each
   DBuf<double> gpart;   // ng * n column sums of the groups
   DBuf<double> nrmp;    // ng * g norm partials
-  DBuf<unsigned> cnt;   // npanels arrival counters + 2 finish counters (zero between launches)
+  DBuf<unsigned> cnt;   // 2 finish counters (zero between launches) + the launch epoch of the exchange tags
 };
 
 }  // namespace apc

@@ -48,6 +48,7 @@ namespace {
 
 constexpr int kDpRoleThreads = 256;  // P1 and P2: 8 warps each
 constexpr int kDpNX = 8;             // exchange warps
+constexpr int kDpBatch = 10;         // partials polled together by one lane
 constexpr int kDpThreads = 32 + kDpNX * 32 + 2 * kDpRoleThreads;
 constexpr int kDpKmax = 22;          // tile elements per P1/P2 thread
 constexpr int kDpTileMax = kDpKmax * kDpRoleThreads;  // 5632 doubles = 44 KB
@@ -57,7 +58,7 @@ constexpr size_t kDpSmemMax = 227 * 1024;
 struct DpArgs {
   const double* ap;
   long long mloc, n, npanels;
-  int rb, W, g, ng, stages, nslot;
+  int rb, W, g, gact, ng, stages, nslot;  // gact: CTAs of a group that own columns
   const double* z;
   double* u;
   const LsqrState* st;
@@ -94,6 +95,12 @@ __device__ __forceinline__ void dp_bulk(void* dst, const void* src, unsigned byt
                "l"(src), "r"(bytes), "r"(dp_smem(bar))
                : "memory");
 }
+__device__ __forceinline__ void dp_st_ll(ulonglong2* p, unsigned long long w0, unsigned long long w1) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+}
+__device__ __forceinline__ void dp_ld_ll(const ulonglong2* p, unsigned long long& w0, unsigned long long& w1) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+}
 __device__ __forceinline__ unsigned dp_ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -106,11 +113,12 @@ __global__ void __launch_bounds__(kDpThreads, 1) dense_pair_kernel(DpArgs a) {
   const int S = a.stages, rb = a.rb;
   const int q = blockIdx.x / a.g, jg = blockIdx.x % a.g;   // group, CTA within the group
   const long long c0 = static_cast<long long>(jg) * a.W;   // first column of the slice
-  const int Wj = static_cast<int>(a.n - c0 < a.W ? a.n - c0 : a.W);
+  const bool active = jg < a.gact;
+  const int Wj = active ? static_cast<int>(a.n - c0 < a.W ? a.n - c0 : a.W) : 0;
   const int elems = Wj * rb;                                // doubles per tile
   const int tile_stride = a.W * rb;                         // doubles between stages (16-byte multiple)
   // the group's panels: p = q + ng * i
-  const long long ni = a.npanels > q ? (a.npanels - q + a.ng - 1) / a.ng : 0;
+  const long long ni = active && a.npanels > q ? (a.npanels - q + a.ng - 1) / a.ng : 0;
 
   double* tiles = reinterpret_cast<double*>(dp_raw);
   double* sred = tiles + static_cast<size_t>(S) * tile_stride;  // S x 8 warps x 32
@@ -163,6 +171,7 @@ __global__ void __launch_bounds__(kDpThreads, 1) dense_pair_kernel(DpArgs a) {
       beta = a.st->beta;
     }
     const int r = lane % rb, qq = lane / rb, nq = 32 / rb;
+    const unsigned epoch = a.cnt[2];  // launches so far (bumped by the last CTA of each launch)
     double nrm = 0.0;
     // at most S exchange warps take part: a warp's first panel must belong to
     // round 0 of its stage (a parity wait on a fresh mbarrier for round 1
@@ -172,11 +181,19 @@ __global__ void __launch_bounds__(kDpThreads, 1) dense_pair_kernel(DpArgs a) {
       const int s = static_cast<int>(i % S);
       const unsigned ph = static_cast<unsigned>((i / S) & 1);
       const long long p = q + static_cast<long long>(a.ng) * i;
-      const bool mine = static_cast<int>(i % a.g) == jg;  // this CTA finalises the panel's u
+      const bool mine = static_cast<int>(i % a.gact) == jg;  // this CTA finalises the panel's u
       const long long row = p * rb + lane;
       double uo = 0.0;
       if (mine && a.st && lane < rb && row < a.mloc) uo = a.u[row];
-      double* slot = a.part + ((static_cast<long long>(q) * a.nslot + (i % a.nslot)) * a.g) * rb;
+      // flag-in-word exchange (no fence, no counter): every partial travels as
+      // two 8-byte words {32 data bits | 32-bit flag}; a word is written and
+      // read whole, so a word whose flag is this launch's (epoch, panel) tag
+      // carries this panel's bits.  The slot held (epoch, i - nslot) or an
+      // (epoch - 1, .) tag before.
+      ulonglong2* slot = reinterpret_cast<ulonglong2*>(a.part) +
+                         ((static_cast<long long>(q) * a.nslot + (i % a.nslot)) * a.g) * rb;
+      const unsigned long long flag =
+          static_cast<unsigned long long>(((epoch & 0x7FFu) << 21) | (static_cast<unsigned>(i + 1) & 0x1FFFFFu)) << 32;
       dp_bar_wait(p1b + s, ph);
       if (lane < rb) {
         const double* sr = sred + (static_cast<size_t>(s) * 8) * 32 + lane;
@@ -184,27 +201,32 @@ __global__ void __launch_bounds__(kDpThreads, 1) dense_pair_kernel(DpArgs a) {
 #pragma unroll
         for (int w = 0; w < 8; ++w) pv += sr[w * 32];
         if (mine && a.st) pv -= alpha * (beta > 0.0 ? uo / beta : uo);
-        __stcg(slot + static_cast<long long>(jg) * rb + lane, pv);
+        const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(pv));
+        dp_st_ll(slot + static_cast<long long>(jg) * rb + lane, (bits & 0xFFFFFFFFull) | flag, (bits >> 32) | flag);
       }
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence();
-        atomicAdd(a.cnt + p, 1u);
-        while (dp_ld_acquire(a.cnt + p) < static_cast<unsigned>(a.g)) {
-        }
-      }
-      __syncwarp();
       // the g partials of row r, CTA order; nq lanes share a row
       double sum = 0.0;
-      for (int j0 = qq; j0 < a.g; j0 += 8 * nq) {
-        double t[8];
+      for (int j0 = qq; j0 < a.gact; j0 += kDpBatch * nq) {
+        unsigned long long lo[kDpBatch], hi[kDpBatch];
+        bool ok;
+        do {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+          for (int k = 0; k < kDpBatch; ++k) {
+            const int jj = j0 + k * nq;
+            if (jj < a.gact) dp_ld_ll(slot + static_cast<long long>(jj) * rb + r, lo[k], hi[k]);
+            else lo[k] = hi[k] = flag;
+          }
+          ok = true;
+#pragma unroll
+          for (int k = 0; k < kDpBatch; ++k)
+            ok = ok && (lo[k] & 0xFFFFFFFF00000000ull) == flag && (hi[k] & 0xFFFFFFFF00000000ull) == flag;
+        } while (!ok);
+#pragma unroll
+        for (int k = 0; k < kDpBatch; ++k) {
           const int jj = j0 + k * nq;
-          t[k] = jj < a.g ? __ldcg(slot + static_cast<long long>(jj) * rb + r) : 0.0;
+          if (jj < a.gact)
+            sum += __longlong_as_double(static_cast<long long>((lo[k] & 0xFFFFFFFFull) | (hi[k] << 32)));
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) sum += t[k];
       }
       for (int o = rb; o < 32; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
       if (lane < rb) us[s * 32 + lane] = sum;
@@ -272,7 +294,7 @@ __global__ void __launch_bounds__(kDpThreads, 1) dense_pair_kernel(DpArgs a) {
 
   // ---------------- finish: the groups' column sums and the norm ----------------
   const unsigned G = gridDim.x;
-  unsigned* fin = a.cnt + a.npanels;
+  unsigned* fin = a.cnt;
   __syncthreads();
   if (threadIdx.x == 0) {
     double sn = 0.0;
@@ -301,8 +323,10 @@ __global__ void __launch_bounds__(kDpThreads, 1) dense_pair_kernel(DpArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) last_flag = atomicAdd(fin + 1, 1u) == G - 1 ? 1 : 0;
   __syncthreads();
-  if (last_flag) {
-    for (long long k = threadIdx.x; k < a.npanels + 2; k += kDpThreads) a.cnt[k] = 0u;
+  if (last_flag && threadIdx.x == 0) {
+    a.cnt[0] = 0u;
+    a.cnt[1] = 0u;
+    a.cnt[2] = a.cnt[2] + 1u;
   }
 }
 
@@ -327,12 +351,9 @@ __global__ void __launch_bounds__(1024) pair_norm2_kernel(const double* __restri
   if (threadIdx.x == 0) *out = s;
 }
 
-int dp_env() {
-  static const int v = [] {
-    const char* e = std::getenv("APC_DENSE_PAIR");
-    return e ? std::atoi(e) : -1;
-  }();
-  return v;
+int dp_env() {  // read per matrix (the tests force the path on small shapes)
+  const char* e = std::getenv("APC_DENSE_PAIR");
+  return e ? std::atoi(e) : -1;
 }
 int dp_env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
@@ -350,9 +371,8 @@ bool dp_plan(apc_mat& a, DensePanels& d) {
   int ng = dp_env_int("APC_DP_GROUPS", G % 4 == 0 ? 4 : (G % 2 == 0 ? 2 : 1));
   if (ng < 1 || G % ng != 0) return false;
   const int g = G / ng;
-  int W = static_cast<int>((n + g - 1) / g);
-  W += W & 1;
-  if (static_cast<i64>(g - 1) * W >= n) return false;  // every CTA of a group needs columns
+  const int W = static_cast<int>((n + g - 1) / g);
+  const int gact = static_cast<int>((n + W - 1) / W);  // CTAs of a group that own columns (the others idle)
   int rb = 32;
   while (rb >= 2 && static_cast<i64>(rb) * W > kDpTileMax) rb >>= 1;
   const int rb_env = dp_env_int("APC_DP_RB", 0);
@@ -369,10 +389,12 @@ bool dp_plan(apc_mat& a, DensePanels& d) {
   d.rb = rb;
   d.W = W;
   d.g = g;
+  d.gact = gact;
   d.ng = ng;
   d.stages = S;
   d.nslot = 2 * S + 2;
   d.npanels = (mloc + rb - 1) / rb;
+  if (d.npanels / ng + 2 >= (i64{1} << 21)) return false;  // the panel tag of the exchange has 21 bits
   d.smem = dp_smem_bytes(S, tile_stride);
   return true;
 }
@@ -405,10 +427,11 @@ bool dense_pair_ready(apc_mat& a) {
   cudaStream_t st = a.ctx->stream;
   const i64 total = d.npanels * d.n * d.rb;
   d.ap.alloc(total);
-  d.part.alloc(static_cast<i64>(d.ng) * d.nslot * d.g * d.rb);
+  d.part.alloc(2 * static_cast<i64>(d.ng) * d.nslot * d.g * d.rb);  // two 8-byte words per partial
+  APC_CUDA(cudaMemsetAsync(d.part.p, 0, d.part.bytes(), st));
   d.gpart.alloc(static_cast<i64>(d.ng) * d.n);
   d.nrmp.alloc(static_cast<i64>(d.ng) * d.g);
-  d.cnt.alloc(d.npanels + 2);
+  d.cnt.alloc(4);  // finish counters (zero between launches) and the launch epoch
   APC_CUDA(cudaMemsetAsync(d.cnt.p, 0, d.cnt.bytes(), st));
   dense_panel_pack_kernel<<<a.ctx->num_sms * 16, 256, 0, st>>>(a.dense.p, a.mloc(), a.mloc(), a.n, d.rb, total,
                                                                d.ap.p);
@@ -425,7 +448,7 @@ void pair_norm2(apc_ctx* ctx, const double* y, long long m, double* out) {
 
 void launch_dense_pair(apc_mat& a, const double* z, double* u, const LsqrState* st, double* g, const int* done) {
   DensePanels& d = a.panels;
-  DpArgs args{d.ap.p, d.mloc, d.n, d.npanels, d.rb, d.W, d.g, d.ng, d.stages, d.nslot,
+  DpArgs args{d.ap.p, d.mloc, d.n, d.npanels, d.rb, d.W, d.g, d.gact, d.ng, d.stages, d.nslot,
               z, u, st, d.part.p, d.gpart.p, d.nrmp.p, d.cnt.p, g, done};
   void* kargs[] = {&args};
   APC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(dense_pair_kernel), dim3(d.ng * d.g),

@@ -81,6 +81,20 @@ def main():
         del Ad
         run(apc, ctx, A, m, n, f"rand{m}x{n}")
         A.free()
+    elif args[0] == "sweep":
+        p = apc.Problem(int(args[1][1:]))
+        combos = [dict()] + [dict(APC_DP_GROUPS=str(g), APC_DP_RB=str(rb)) for g in (1, 2, 4) for rb in (2, 4, 8, 16, 32)]
+        combos += [dict(APC_DP_STAGES=str(s)) for s in (3, 4, 5)]
+        for c in combos:
+            for k in ("APC_DP_GROUPS", "APC_DP_RB", "APC_DP_STAGES"):
+                os.environ.pop(k, None)
+            os.environ.update(c)
+            A = apc.DeviceMatrix.from_problem(ctx, p)
+            try:
+                run(apc, ctx, A, p.m, p.n, args[1])
+            except Exception as e:
+                print("failed", c, e, flush=True)
+            A.free()
     else:
         for w in args:
             p = apc.Problem(int(w[1:]))
