@@ -47,8 +47,14 @@ namespace apc {
 namespace {
 
 constexpr int kDpRoleThreads = 256;  // P1 and P2: 8 warps each
-constexpr int kDpNX = 8;             // exchange warps
-constexpr int kDpBatch = 10;         // partials polled together by one lane
+#ifndef APC_DP_NX
+#define APC_DP_NX 7
+#endif
+#ifndef APC_DP_BATCH
+#define APC_DP_BATCH 5
+#endif
+constexpr int kDpNX = APC_DP_NX;     // exchange warps
+constexpr int kDpBatch = APC_DP_BATCH;         // partials polled together by one lane
 constexpr int kDpThreads = 32 + kDpNX * 32 + 2 * kDpRoleThreads;
 constexpr int kDpKmax = 22;          // tile elements per P1/P2 thread
 constexpr int kDpTileMax = kDpKmax * kDpRoleThreads;  // 5632 doubles = 44 KB
@@ -68,6 +74,7 @@ struct DpArgs {
   unsigned* cnt;
   double* gout;
   const int* done;
+  int debug;  // APC_DP_DEBUG (experiments only; results are wrong when set)
 };
 
 __device__ __forceinline__ unsigned dp_smem(const void* p) {
@@ -118,7 +125,7 @@ __global__ void __launch_bounds__(kDpThreads, 1) dense_pair_kernel(DpArgs a) {
   const int elems = Wj * rb;                                // doubles per tile
   const int tile_stride = a.W * rb;                         // doubles between stages (16-byte multiple)
   // the group's panels: p = q + ng * i
-  const long long ni = active && a.npanels > q ? (a.npanels - q + a.ng - 1) / a.ng : 0;
+  const int ni = static_cast<int>(active && a.npanels > q ? (a.npanels - q + a.ng - 1) / a.ng : 0);  // < 2^21 (dp_plan)
 
   double* tiles = reinterpret_cast<double*>(dp_raw);
   double* sred = tiles + static_cast<size_t>(S) * tile_stride;  // S x 8 warps x 32
@@ -147,13 +154,18 @@ __global__ void __launch_bounds__(kDpThreads, 1) dense_pair_kernel(DpArgs a) {
     // ---------------- producer ----------------
     if (lane == 0) {
       const unsigned bytes = static_cast<unsigned>(elems) * 8u;
-      for (long long i = 0; i < ni; ++i) {
-        const int s = static_cast<int>(i % S);
-        const unsigned ph = static_cast<unsigned>((i / S) & 1);
+      // stage / round parity by counting: no 64-bit divisions in the per-panel loops
+      int s = 0;
+      unsigned ph = 0;
+      for (int i = 0; i < ni; ++i, s = s + 1 == S ? 0 : s + 1, ph ^= s == 0 ? 1u : 0u) {
         dp_bar_wait(empty + s, ph ^ 1u);
         const long long p = q + static_cast<long long>(a.ng) * i;
         const double* src = a.ap + (p * a.n + c0) * rb;
         double* dst = tiles + static_cast<size_t>(s) * tile_stride;
+        if (a.debug & 8) {
+          dp_bar_arrive(full + s);
+          continue;
+        }
         dp_bar_expect(full + s, bytes);
         for (unsigned off = 0; off < bytes; off += 16384u) {
           const unsigned len = bytes - off < 16384u ? bytes - off : 16384u;
@@ -177,11 +189,11 @@ __global__ void __launch_bounds__(kDpThreads, 1) dense_pair_kernel(DpArgs a) {
     // round 0 of its stage (a parity wait on a fresh mbarrier for round 1
     // passes at once), and its later ones then follow completed rounds
     const int nxw = S < kDpNX ? S : kDpNX;
-    for (long long i = xw < nxw ? xw : ni; i < ni; i += nxw) {
-      const int s = static_cast<int>(i % S);
+    for (int i = xw < nxw ? xw : ni; i < ni; i += nxw) {
+      const int s = i % S;
       const unsigned ph = static_cast<unsigned>((i / S) & 1);
       const long long p = q + static_cast<long long>(a.ng) * i;
-      const bool mine = static_cast<int>(i % a.gact) == jg;  // this CTA finalises the panel's u
+      const bool mine = i % a.gact == jg;  // this CTA finalises the panel's u
       const long long row = p * rb + lane;
       double uo = 0.0;
       if (mine && a.st && lane < rb && row < a.mloc) uo = a.u[row];
@@ -191,7 +203,7 @@ __global__ void __launch_bounds__(kDpThreads, 1) dense_pair_kernel(DpArgs a) {
       // carries this panel's bits.  The slot held (epoch, i - nslot) or an
       // (epoch - 1, .) tag before.
       ulonglong2* slot = reinterpret_cast<ulonglong2*>(a.part) +
-                         ((static_cast<long long>(q) * a.nslot + (i % a.nslot)) * a.g) * rb;
+                         ((static_cast<long long>(q) * a.nslot + i % a.nslot) * a.g) * rb;
       const unsigned long long flag =
           static_cast<unsigned long long>(((epoch & 0x7FFu) << 21) | (static_cast<unsigned>(i + 1) & 0x1FFFFFu)) << 32;
       dp_bar_wait(p1b + s, ph);
@@ -206,7 +218,7 @@ __global__ void __launch_bounds__(kDpThreads, 1) dense_pair_kernel(DpArgs a) {
       }
       // the g partials of row r, CTA order; nq lanes share a row
       double sum = 0.0;
-      for (int j0 = qq; j0 < a.gact; j0 += kDpBatch * nq) {
+      for (int j0 = (a.debug & 1) ? a.gact : qq; j0 < a.gact; j0 += kDpBatch * nq) {
         unsigned long long lo[kDpBatch], hi[kDpBatch];
         bool ok;
         do {
@@ -449,7 +461,7 @@ void pair_norm2(apc_ctx* ctx, const double* y, long long m, double* out) {
 void launch_dense_pair(apc_mat& a, const double* z, double* u, const LsqrState* st, double* g, const int* done) {
   DensePanels& d = a.panels;
   DpArgs args{d.ap.p, d.mloc, d.n, d.npanels, d.rb, d.W, d.g, d.gact, d.ng, d.stages, d.nslot,
-              z, u, st, d.part.p, d.gpart.p, d.nrmp.p, d.cnt.p, g, done};
+              z, u, st, d.part.p, d.gpart.p, d.nrmp.p, d.cnt.p, g, done, dp_env_int("APC_DP_DEBUG", 0)};
   void* kargs[] = {&args};
   APC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(dense_pair_kernel), dim3(d.ng * d.g),
                                        dim3(kDpThreads), kargs, d.smem, a.ctx->stream));

