@@ -325,7 +325,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-sample-iters", type=int, default=4)
-    ap.add_argument("--time-budget", type=float, default=1560.0,
+    ap.add_argument("--time-budget", type=float, default=1660.0,
                     help="wall seconds for the whole run; timed steps stop early (and say so) past it")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the C2 and C3 side measurements")

@@ -1143,10 +1143,10 @@ void enqueue_iteration(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P
     ctx->launches++;
   }
   // A^T u with the epilogue h = (A^T u + mu u_t)/beta where the columns are
-  // finalised (one rank: no allreduce between them).  Off by default: on C5
-  // the per-column u_t gather and division inside the tail stream's store cost
-  // ~20 us per iteration more than the separate epilogue pass (APC_FUSE_EPI=1)
-  static const bool epi_env = std::getenv("APC_FUSE_EPI") && std::atoi(std::getenv("APC_FUSE_EPI")) != 0;
+  // finalised (one rank: no allreduce between them): the tail scatter and the
+  // head combine apply it, so the separate lsqr_epi_kernel pass over n goes
+  // away (same operations per column: same bits; APC_FUSE_EPI=0 restores it)
+  const bool epi_env = !std::getenv("APC_FUSE_EPI") || std::atoi(std::getenv("APC_FUSE_EPI")) != 0;  // per enqueue: the tests toggle it
   const bool epi_fused =
       fuse_env && epi_env && pre && ctx->nranks == 1 && w->mloc > 0 &&
       op_adj_epi(a, P.u, P.h, done,

@@ -698,10 +698,18 @@ __global__ void tail_combine_kernel(const double* __restrict__ part, const int* 
 
 // tail-order column sums -> out[original column]
 __global__ void tail_scatter_kernel(const double* __restrict__ outc, const int* __restrict__ tcol, long long ncols,
-                                    double* __restrict__ out, const int* done) {
+                                    double* __restrict__ out, const int* done, AdjEpi e) {
   if (done && *done) return;
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < ncols) out[__ldg(tcol + i)] = __ldg(outc + i);
+  if (i >= ncols) return;
+  const int j = __ldg(tcol + i);
+  double s = __ldg(outc + i);
+  if (e.n2top) {  // the LSQR epilogue (lsqr_epi_kernel), fused: same operations, same bits
+    const double beta = sqrt(*e.n2top + (e.n2tail ? *e.n2tail : 0.0));
+    const double raw = e.ut ? s + e.mu * e.ut[j] : s;
+    s = beta > 0.0 ? raw / beta : raw;
+  }
+  out[j] = s;
 }
 
 // warp per head column: its partials in block order -> out[col]
@@ -909,9 +917,11 @@ void seg_adjoint(apc_mat& a, const double* u, double* out, const int* done, cons
   cudaStream_t st = a.ctx->stream;
   const HeadAdj& h = a.head;
   const HeadAdj::Seg& t = h.seg;
-  // tail-order stores (then one scatter) unless superblock partials or the fused epilogue are in use
-  const bool compact = t.sb == 1 && !e.n2top && t.outc.p;
-  const TailPolicy pol{t.gcol0.p, t.tcol.p, t.sb > 1 ? t.part.p : out, t.rb, t.sb > 1 ? AdjEpi{} : e, 0.0,
+  // tail-order stores (then one scatter) unless superblock partials are in use; a fused
+  // epilogue rides on the scatter (inside the stream's stores its u_t gather and division
+  // cost ~20 us per C5 iteration)
+  const bool compact = t.sb == 1 && t.outc.p;
+  const TailPolicy pol{t.gcol0.p, t.tcol.p, t.sb > 1 ? t.part.p : out, t.rb, t.sb > 1 || compact ? AdjEpi{} : e, 0.0,
                        compact ? t.outc.p : nullptr, 0};
   const HeadPolicy hp{h.part.p, static_cast<int>(h.nblocks), h.rows};
   seg_adj_kernel<TailPolicy><<<static_cast<unsigned>(t.ngroups * t.parts), kHeadThreads, 0, st>>>(
@@ -928,7 +938,7 @@ void seg_adjoint(apc_mat& a, const double* u, double* out, const int* done, cons
     a.ctx->launches++;
   }
   if (compact) {
-    tail_scatter_kernel<<<nblk(t.ncols, 256), 256, 0, st>>>(t.outc.p, t.tcol.p, t.ncols, out, done);
+    tail_scatter_kernel<<<nblk(t.ncols, 256), 256, 0, st>>>(t.outc.p, t.tcol.p, t.ncols, out, done, e);
     a.ctx->launches++;
   }
   seg_adj_kernel<HeadPolicy><<<static_cast<unsigned>(h.nblocks * h.parts), kHeadThreads, sizeof(double) * h.rows,

@@ -159,3 +159,25 @@ def test_hot_solve_matches_reference(apc, ref, ctx, monkeypatch):
     it_g, it_r = g.lsqr_iters, int(r.phase_iters.sum())
     assert abs(it_g - it_r) <= max(3, 0.05 * it_r), (it_g, it_r)
     assert abs(g.final_relres - r.final_relres) <= 1e-5 * r.final_relres
+
+
+def test_fused_adjoint_epilogue_is_bit_identical(apc, ctx, monkeypatch):
+    """The LSQR epilogue h = (A^T u + mu u_t)/beta applied by the tail scatter and
+    the head combine (default) against the separate lsqr_epi_kernel pass
+    (APC_FUSE_EPI=0): the same operations per column, so x and the phibar
+    trace are bit-identical (lsqr.hpp:139-150)."""
+    p = apc.Problem(5, 60000, 6000)
+    A = _upload(apc, ctx, p, monkeypatch, True)
+    cfg = apc.SolverConfig(mu=1e-8, eps_lsqr=1e-8, block=25, seed=1, max_rank=50, eps_cur=3e-7, lsqr_cap=300)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("APC_FUSE_EPI", mode)
+        L0 = ctx.launches
+        out[mode] = (apc.aplicur_solve(A, p.b, cfg), ctx.launches - L0)
+    g1, g0 = out["1"][0], out["0"][0]
+    assert np.array_equal(g1.x, g0.x)
+    assert np.array_equal(g1.trace["phibar"], g0.trace["phibar"])
+    assert g1.lsqr_iters == g0.lsqr_iters > 0
+    # the fused path launches one kernel less per preconditioned iteration
+    assert out["1"][1] < out["0"][1]
+    A.free()
