@@ -1144,9 +1144,11 @@ void enqueue_iteration(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P
   }
   // A^T u with the epilogue h = (A^T u + mu u_t)/beta where the columns are
   // finalised (one rank: no allreduce between them): the tail scatter and the
-  // head combine apply it, so the separate lsqr_epi_kernel pass over n goes
-  // away (same operations per column: same bits; APC_FUSE_EPI=0 restores it)
-  const bool epi_env = !std::getenv("APC_FUSE_EPI") || std::atoi(std::getenv("APC_FUSE_EPI")) != 0;  // per enqueue: the tests toggle it
+  // head combine apply it and the separate lsqr_epi_kernel pass over n goes
+  // away (same operations per column: same bits).  Opt-in (APC_FUSE_EPI=1):
+  // on C5 the random u_t gather and the division in the scatter cost what the
+  // coalesced pass did (791 vs 787 us per iteration, profiles/r2e_dense_pair.md)
+  const bool epi_env = std::getenv("APC_FUSE_EPI") && std::atoi(std::getenv("APC_FUSE_EPI")) != 0;  // per enqueue: the tests toggle it
   const bool epi_fused =
       fuse_env && epi_env && pre && ctx->nranks == 1 && w->mloc > 0 &&
       op_adj_epi(a, P.u, P.h, done,

@@ -163,8 +163,8 @@ def test_hot_solve_matches_reference(apc, ref, ctx, monkeypatch):
 
 def test_fused_adjoint_epilogue_is_bit_identical(apc, ctx, monkeypatch):
     """The LSQR epilogue h = (A^T u + mu u_t)/beta applied by the tail scatter and
-    the head combine (default) against the separate lsqr_epi_kernel pass
-    (APC_FUSE_EPI=0): the same operations per column, so x and the phibar
+    the head combine (APC_FUSE_EPI=1) against the separate lsqr_epi_kernel pass
+    (the default): the same operations per column, so x and the phibar
     trace are bit-identical (lsqr.hpp:139-150)."""
     p = apc.Problem(5, 60000, 6000)
     A = _upload(apc, ctx, p, monkeypatch, True)
