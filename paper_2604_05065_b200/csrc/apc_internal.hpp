@@ -215,6 +215,8 @@ struct apc_ctx {
   int device = 0;
   int nranks = 1, rank = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // fork / join branch of the library stream (created on first use)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* nccl = nullptr;  // ncclComm_t when nranks > 1 (NCCL backend)
   // host-staged backend (apc_ctx_create_host_comm): the caller's in-place sum
   // of a host buffer over the ranks, in rank order

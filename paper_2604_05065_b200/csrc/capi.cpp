@@ -210,6 +210,11 @@ int apc_ctx_destroy(apc_ctx* ctx) {
       if (b.p) cudaFreeHost(b.p);
     ctx->scratch_d.release();
     ctx->counters.release();
+    if (ctx->side) {
+      cudaStreamDestroy(ctx->side);
+      cudaEventDestroy(ctx->ev_fork);
+      cudaEventDestroy(ctx->ev_join);
+    }
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     pool_trim();

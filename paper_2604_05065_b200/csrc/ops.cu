@@ -924,34 +924,60 @@ void seg_adjoint(apc_mat& a, const double* u, double* out, const int* done, cons
   const TailPolicy pol{t.gcol0.p, t.tcol.p, t.sb > 1 ? t.part.p : out, t.rb, t.sb > 1 || compact ? AdjEpi{} : e, 0.0,
                        compact ? t.outc.p : nullptr, 0};
   const HeadPolicy hp{h.part.p, static_cast<int>(h.nblocks), h.rows};
-  seg_adj_kernel<TailPolicy><<<static_cast<unsigned>(t.ngroups * t.parts), kHeadThreads, 0, st>>>(
+  // APC_ADJ_OVERLAP=1: the tail stream (latency-bound on its u gathers) on a
+  // side stream beside the head stream (HBM-bound, 2 CTAs per SM by its shared
+  // memory): fork / join by events, also inside graph capture.  The two write
+  // disjoint columns of `out`.
+  static const int overlap_mode = std::getenv("APC_ADJ_OVERLAP") ? std::atoi(std::getenv("APC_ADJ_OVERLAP")) : 0;
+  const bool overlap_env = overlap_mode != 0;  // 1: head launched first, 2: tail first
+  cudaStream_t ts = st;
+  if (overlap_env) {
+    apc_ctx* c = a.ctx;
+    if (!c->side) {
+      APC_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+      APC_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      APC_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
+    ts = c->side;
+    APC_CUDA(cudaEventRecord(c->ev_fork, st));
+    APC_CUDA(cudaStreamWaitEvent(ts, c->ev_fork, 0));
+  }
+  auto head = [&] {
+    seg_adj_kernel<HeadPolicy><<<static_cast<unsigned>(h.nblocks * h.parts), kHeadThreads, sizeof(double) * h.rows,
+                                 st>>>(h.bptr.p, h.hkey.p, h.hval.p, u, a.mloc(), h.parts, h.zptr.p, h.zcol.p, hp,
+                                       reinterpret_cast<HeadPiece*>(h.bnd.p), done);
+    a.ctx->launches++;
+    if (h.parts > 1) {
+      seg_bnd_kernel<HeadPolicy><<<nblk(h.nblocks, 128), 128, 0, st>>>(reinterpret_cast<const HeadPiece*>(h.bnd.p),
+                                                                       h.parts, h.nblocks, hp, done);
+      a.ctx->launches++;
+    }
+    head_combine_kernel<<<nblk(h.ncols * 32, 256), 256, 0, st>>>(h.part.p, h.nblocks, h.hcol.p, h.ncols, out, done, e);
+    a.ctx->launches++;
+  };
+  if (overlap_mode == 1) head();  // first: its CTAs take their 2 slots per SM, the tail fills the rest
+  seg_adj_kernel<TailPolicy><<<static_cast<unsigned>(t.ngroups * t.parts), kHeadThreads, 0, ts>>>(
       t.gptr.p, t.tkey.p, t.tval.p, u, a.mloc(), t.parts, t.zptr.p, t.zcol.p, pol,
       reinterpret_cast<HeadPiece*>(t.bnd.p), done);
   a.ctx->launches++;
   if (t.parts > 1) {
-    seg_bnd_kernel<TailPolicy><<<nblk(t.ngroups, 128), 128, 0, st>>>(reinterpret_cast<const HeadPiece*>(t.bnd.p),
+    seg_bnd_kernel<TailPolicy><<<nblk(t.ngroups, 128), 128, 0, ts>>>(reinterpret_cast<const HeadPiece*>(t.bnd.p),
                                                                      t.parts, t.ngroups, pol, done);
     a.ctx->launches++;
   }
   if (t.sb > 1) {
-    tail_combine_kernel<<<nblk(t.ncols, 256), 256, 0, st>>>(t.part.p, t.cols.p, t.ncols, t.sb, out, done, e);
+    tail_combine_kernel<<<nblk(t.ncols, 256), 256, 0, ts>>>(t.part.p, t.cols.p, t.ncols, t.sb, out, done, e);
     a.ctx->launches++;
   }
   if (compact) {
-    tail_scatter_kernel<<<nblk(t.ncols, 256), 256, 0, st>>>(t.outc.p, t.tcol.p, t.ncols, out, done, e);
+    tail_scatter_kernel<<<nblk(t.ncols, 256), 256, 0, ts>>>(t.outc.p, t.tcol.p, t.ncols, out, done, e);
     a.ctx->launches++;
   }
-  seg_adj_kernel<HeadPolicy><<<static_cast<unsigned>(h.nblocks * h.parts), kHeadThreads, sizeof(double) * h.rows,
-                               st>>>(h.bptr.p, h.hkey.p, h.hval.p, u, a.mloc(), h.parts, h.zptr.p, h.zcol.p, hp,
-                                     reinterpret_cast<HeadPiece*>(h.bnd.p), done);
-  a.ctx->launches++;
-  if (h.parts > 1) {
-    seg_bnd_kernel<HeadPolicy><<<nblk(h.nblocks, 128), 128, 0, st>>>(reinterpret_cast<const HeadPiece*>(h.bnd.p),
-                                                                     h.parts, h.nblocks, hp, done);
-    a.ctx->launches++;
+  if (overlap_mode != 1) head();
+  if (overlap_env) {
+    APC_CUDA(cudaEventRecord(a.ctx->ev_join, ts));
+    APC_CUDA(cudaStreamWaitEvent(st, a.ctx->ev_join, 0));
   }
-  head_combine_kernel<<<nblk(h.ncols * 32, 256), 256, 0, st>>>(h.part.p, h.nblocks, h.hcol.p, h.ncols, out, done, e);
-  a.ctx->launches++;
 }
 }  // namespace
 
