@@ -50,6 +50,9 @@ constexpr int kDpRoleThreads = 256;  // P1 and P2: 8 warps each
 #ifndef APC_DP_NX
 #define APC_DP_NX 7
 #endif
+#ifndef APC_DP_EVICT
+#define APC_DP_EVICT 1
+#endif
 #ifndef APC_DP_BATCH
 #define APC_DP_BATCH 5
 #endif
@@ -96,11 +99,29 @@ __device__ __forceinline__ void dp_bar_wait(unsigned long long* b, unsigned pari
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void dp_bulk(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+// A is streamed once per launch and is far larger than L2: its lines are
+// marked evict-first so the explicit basis B, K and the n-space vectors of the
+// LSQR iteration (~100 MB) stay L2-resident from one iteration to the next
+__device__ __forceinline__ unsigned long long dp_evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void dp_bulk(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                        unsigned long long pol) {
+#if APC_DP_EVICT
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          dp_smem(dst)),
+      "l"(src), "r"(bytes), "r"(dp_smem(bar)), "l"(pol)
+      : "memory");
+#else
+  (void)pol;
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    dp_smem(dst)),
                "l"(src), "r"(bytes), "r"(dp_smem(bar))
                : "memory");
+#endif
 }
 __device__ __forceinline__ void dp_st_ll(ulonglong2* p, unsigned long long w0, unsigned long long w1) {
   asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
@@ -154,6 +175,7 @@ __global__ void __launch_bounds__(kDpThreads, 1) dense_pair_kernel(DpArgs a) {
     // ---------------- producer ----------------
     if (lane == 0) {
       const unsigned bytes = static_cast<unsigned>(elems) * 8u;
+      const unsigned long long pol = dp_evict_first_policy();
       // stage / round parity by counting: no 64-bit divisions in the per-panel loops
       int s = 0;
       unsigned ph = 0;
@@ -170,7 +192,7 @@ __global__ void __launch_bounds__(kDpThreads, 1) dense_pair_kernel(DpArgs a) {
         for (unsigned off = 0; off < bytes; off += 16384u) {
           const unsigned len = bytes - off < 16384u ? bytes - off : 16384u;
           dp_bulk(reinterpret_cast<unsigned char*>(dst) + off, reinterpret_cast<const unsigned char*>(src) + off, len,
-                  full + s);
+                  full + s, pol);
         }
       }
     }

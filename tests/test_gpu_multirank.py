@@ -127,3 +127,13 @@ def test_row_sharded_matches_single_rank(apc, ctx, tmp_path, run):
         assert rel <= 1e-6 or abs(rs[0]["relres"] - g.final_relres) <= 1e-6 * g.final_relres, rel
     else:
         assert abs(rs[0]["relres"] - g.final_relres) <= 1e-3 * g.final_relres
+
+
+def test_row_sharded_dense_on_the_fused_pair(apc, ctx, tmp_path, monkeypatch):
+    """The same contract with every rank's LSQR products on the fused
+    read-A-once kernel (dense_pair.cu, forced on this small shape): each rank
+    runs it on its row block, the partial A_p^T u_p and ||u_p||^2 it leaves in
+    g meet in the allreduce as before."""
+    monkeypatch.setenv("APC_DENSE_PAIR", "1")
+    test_row_sharded_matches_single_rank(apc, ctx, tmp_path, (1, 2, "sharded"))
+    test_row_sharded_matches_single_rank(apc, ctx, tmp_path, (1, 2, "root"))
