@@ -93,7 +93,7 @@ int apc_op_apply_host(apc_mat* a, double mu, int augmented, int transpose, const
                       double* y);
 /* The operator pair of one LSQR iteration (lsqr.hpp:139-150 calls matvec and
  * matvec_transpose back to back): y = A x (len local m), g[0:n] = A^T y and
- * g[n] = ||y||^2, device pointers, ctx stream.  A dense A that does not fit L2
+ * g[n] = ||y||^2, device pointers, ctx stream.  A dense A of 64 MB or more
  * goes through the fused kernel that reads A from HBM once (a panel of rows
  * stays in shared memory between the two products); everything else runs the
  * two products one after the other.  *fused (may be NULL) reports which. */

@@ -442,8 +442,10 @@ bool dense_pair_ready(apc_mat& a) {
   const int env = dp_env();
   if (env == 0 || a.sparse || a.mloc() <= 0 || a.n <= 0) return false;
   const double bytes = 8.0 * static_cast<double>(a.mloc()) * static_cast<double>(a.n);
-  // below ~1 GB the two-pass kernels run out of L2 or close to it
-  if (env < 0 && bytes < 1e9) return false;
+  // measured down to 60 MB (L2-resident) the single pass still wins (3000 x 2500: 1.34x,
+  // 10007 x 4001: 1.65x, profiles/r2e_dense_pair.md); below that the launch is
+  // latency-bound either way and the panel copy is not worth its bytes
+  if (env < 0 && bytes < 64e6) return false;
   if (!dp_plan(a, d)) return false;
   size_t free_b = 0, total_b = 0;
   APC_CUDA(cudaMemGetInfo(&free_b, &total_b));

@@ -2,7 +2,7 @@
 //   u <- A z - alpha * u/beta,  ||u||^2,  g = A^T u
 // with A read from HBM ONCE.  Replaces dense_fwd_kernel + dense_adj_kernel
 // (Matrix::matvec + Matrix::matvec_transpose, matrix.hpp:151-195, as lsqr_solve
-// calls them back to back, lsqr.hpp:139-150) for matrices that do not fit L2.
+// calls them back to back, lsqr.hpp:139-150) for matrices of 64 MB or more.
 #pragma once
 
 #include "apc_internal.hpp"

@@ -1125,7 +1125,7 @@ void enqueue_iteration(LsqrWork* w, apc_mat& a, PrecondDev* p, const LsqrPtrs& P
     z = P.z;
   }
   LsqrFwdEpi epi{P.u, P.st, P.fwd_part, P.ctr + 0, P.g + P.n, 0.0, 0.0};
-  // dense A beyond L2: u, ||u||^2 and A^T u in one kernel that reads A once
+  // dense A of 64 MB or more: u, ||u||^2 and A^T u in one kernel that reads A once
   const bool pair_fused = w->mloc > 0 && !a.sparse && dense_pair_ready(a);
   if (pair_fused) {
     launch_dense_pair(a, z, P.u, P.st, P.g, done);

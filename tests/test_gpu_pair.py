@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture
 def forced_pair():
     """APC_DENSE_PAIR=1: the fused path on every shape the kernel supports
-    (by default only matrices beyond L2 take it); read once per matrix."""
+    (by default only matrices of 64 MB or more take it); read once per matrix."""
     old = {k: os.environ.get(k) for k in ("APC_DENSE_PAIR", "APC_DP_RB", "APC_DP_GROUPS", "APC_DP_STAGES")}
     os.environ["APC_DENSE_PAIR"] = "1"
     yield os.environ
