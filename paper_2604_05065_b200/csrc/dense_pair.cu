@@ -447,6 +447,10 @@ bool dense_pair_ready(apc_mat& a) {
   // latency-bound either way and the panel copy is not worth its bytes
   if (env < 0 && bytes < 64e6) return false;
   if (!dp_plan(a, d)) return false;
+  // narrow matrices: a panel costs ~0.8 us of pipeline latency whatever its
+  // size, so tiles under 16 KB (n < ~2500) lose to the two streaming passes
+  // (20000 x 1000: 0.126 ms against 0.083 ms)
+  if (env < 0 && static_cast<i64>(d.rb) * d.W * 8 < 16384) return false;
   size_t free_b = 0, total_b = 0;
   APC_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const size_t need = static_cast<size_t>(d.npanels) * d.n * d.rb * 8;
