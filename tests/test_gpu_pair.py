@@ -77,6 +77,24 @@ def test_small_matrices_keep_the_two_pass_kernels(apc, ctx):
     A.free()
 
 
+def test_auto_rule_by_size_and_width(apc, ctx):
+    """Without APC_DENSE_PAIR: 64 MB or more AND tiles of 16 KB or more take the
+    fused kernel (10000 x 3000), a narrow matrix of the same bytes does not
+    (30000 x 1000: its 7 KB tiles lose to the two streaming passes)."""
+    assert "APC_DENSE_PAIR" not in os.environ
+    rng = np.random.default_rng(11)
+    for (m, n, want) in [(10000, 3000, True), (30000, 1000, False)]:
+        Ah = rng.standard_normal((m, n))
+        x = rng.standard_normal(n)
+        A = apc.DeviceMatrix.from_numpy(ctx, Ah)
+        fused, y, g = _pair(ctx, A, x, m, n)
+        assert fused == want, (m, n, fused)
+        yr = Ah @ x
+        assert np.allclose(y, yr, rtol=0, atol=1e-11 * np.abs(yr).max())
+        assert np.allclose(g[:n], Ah.T @ yr, rtol=0, atol=1e-11 * np.abs(Ah.T @ yr).max())
+        A.free()
+
+
 def test_sparse_matrix_runs_the_two_products(apc, ctx):
     p = apc.Problem(2, 4000, 400)
     A = apc.DeviceMatrix.from_problem(ctx, p)
