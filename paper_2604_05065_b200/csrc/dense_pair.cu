@@ -23,9 +23,14 @@
 //     panel hides behind the tiles of the next ones (S stages of ~40 KB):
 //       producer (1 thread)  empty[s] -> bulk copy -> full[s]
 //       P1 (8 warps)         full[s]  -> partial rows of A z (own columns) -> p1[s]
-//       X  (8 warps, one panel each in turn)
-//                            p1[s] -> publish the CTA's rb partials, count the
-//                            group's arrivals, sum the g partials in CTA order
+//       X  (7 warps, one panel each in turn; with the producer and the 16
+//          compute warps that is 24 warps: 25 would round to 28 in the
+//          register file and cap the kernel at 72 registers with spills)
+//                            p1[s] -> publish the CTA's rb partials as flagged
+//                            words (two 8-byte words {32 data bits | (launch
+//                            epoch, panel) tag}: a matching tag proves the data,
+//                            no fence / counter / flag poll), gather the group's
+//                            g partials the same way and add them in CTA order
 //                            (every CTA gets the same bits) -> u of the panel in
 //                            shared memory -> ub[s]; the panel's designated CTA
 //                            folds -alpha*u_old/beta into its partial, stores u
